@@ -1,0 +1,367 @@
+"""ORACLE (test infrastructure only) — transport operators H, S, F.
+
+Follows PAPER.md §3.2 and eq. Discretized_kNTE with
+the readings of SURVEY.md §8(c).3 (listed in DESIGN.md):
+  Z1  F = fission, S = scattering (labels at P:990-991 swapped)
+  Z3  Intg^b = C_b 1_L w^T (full-L reading of P:1254)
+  Z4  S energy factor = full transfer matrix sigma_s[g <- g']
+  Z5  F energy factor = chi nu_sigma_f^T
+  Z6  boundary rows follow the displayed matrices
+  Z7  row -> cell association is octant dependent
+  Z12 nv vertices per axis, nv-1 cells, Delta = extent / (nv-1)
+  Z28 core order (x, y, z, angle, group), first index fastest
+  Z34 heterogeneous cross sections by painted boxes, octant-shifted cells
+
+Two independent constructions are provided and pinned against each other:
+  * `dense_operators`: Kronecker sums of the per-octant factor matrices;
+  * `eq4_apply`: the row equations of eq. Discretized_kNTE evaluated with
+    explicit index loops (interior rows), generalised per octant (Z7).
+"""
+from __future__ import annotations
+
+import math
+import numpy as np
+
+from . import tt as ott
+
+# ----------------------------------------------------------- factors ---
+
+
+def D_plus(n, h):
+    """D^+_x: (1/h) lower bidiagonal, diag 1, sub-diagonal -1."""
+    M = np.eye(n) - np.eye(n, k=-1)
+    return M / h
+
+
+def D_minus(n, h):
+    """D^-_x: (1/h) upper bidiagonal, diag -1, super-diagonal 1."""
+    M = -np.eye(n) + np.eye(n, k=1)
+    return M / h
+
+
+def Ip_minus(n):
+    """Ip^-_x: 1/2 upper bidiagonal (1, 1), last row (0 .. 0 1)."""
+    return 0.5 * (np.eye(n) + np.eye(n, k=1))
+
+
+def Ip_plus(n):
+    """Ip^+_x: 1/2 lower bidiagonal (1, 1), first row (1 0 .. 0)."""
+    return 0.5 * (np.eye(n) + np.eye(n, k=-1))
+
+
+def Ip_minus_noBC(n):
+    """Ip^-_{x,noBC}: Ip^- with the last row zeroed."""
+    M = Ip_minus(n)
+    M[-1, :] = 0.0
+    return M
+
+
+def Ip_plus_noBC(n):
+    """Ip^+_{x,noBC}: Ip^+ with the first row zeroed."""
+    M = Ip_plus(n)
+    M[0, :] = 0.0
+    return M
+
+
+def D_s(s, n, h):
+    return D_plus(n, h) if s > 0 else D_minus(n, h)
+
+
+def Ip_s(s, n):
+    return Ip_plus(n) if s > 0 else Ip_minus(n)
+
+
+def IpN_s(s, n):
+    return Ip_plus_noBC(n) if s > 0 else Ip_minus_noBC(n)
+
+
+def octant_of(quad):
+    """Octant index b (0-based) of every ordinate, from the signs of (mu, eta, xi)."""
+    mu, eta, xi = quad["mu"], quad["eta"], quad["xi"]
+    return ((mu > 0).astype(int) + 2 * (eta > 0).astype(int) + 4 * (xi > 0).astype(int))
+
+
+def C_b(quad, b):
+    """C_b: L x L selector of octant block b."""
+    return np.diag((octant_of(quad) == b).astype(float))
+
+
+def cell_of_row(s, n):
+    """Z7: in an octant with sign s on this axis, row (vertex) i stores the cell
+    equation of cell i - [s > 0]; inflow-face rows are clamped into range."""
+    c = np.arange(n) - (1 if s > 0 else 0)
+    return np.clip(c, 0, n - 2)
+
+
+def material_map(prob):
+    """Material index of every cell (ncell^3 array indexed [cz, cy, cx])."""
+    nc = prob["nv"] - 1
+    mat = np.zeros((nc, nc, nc), dtype=int)
+    for (lo, hi, m) in prob["boxes"]:
+        mat[lo[2]:hi[2], lo[1]:hi[1], lo[0]:hi[0]] = m
+    return mat
+
+
+def box_terms(prob):
+    """Decompose the painted material field into a background plus separable
+    box indicators: field = m0 + sum_t 1_box_t (m_t - parent_t) (Z34).
+    Requires each box's footprint to be uniform before it is painted
+    (nested or disjoint boxes)."""
+    nc = prob["nv"] - 1
+    mat = np.zeros((nc, nc, nc), dtype=int)
+    terms = []
+    for (lo, hi, m) in prob["boxes"]:
+        foot = mat[lo[2]:hi[2], lo[1]:hi[1], lo[0]:hi[0]]
+        parent = int(foot.flat[0])
+        if not np.all(foot == parent):
+            raise ValueError("boxes must be nested or disjoint")
+        terms.append((lo, hi, m, parent))
+        mat[lo[2]:hi[2], lo[1]:hi[1], lo[0]:hi[0]] = m
+    return terms
+
+
+# ---------------------------------------------------- rank-1 term lists ---
+# A term is (coefficient-free) list of 5 factor matrices in core order
+# [F_x, F_y, F_z, F_angle, F_group]; the operator is the sum of their Kronecker
+# products  F_group (x) F_angle (x) F_z (x) F_y (x) F_x  (paper order).
+
+
+def _axis_indicator(s, n, lo, hi):
+    c = cell_of_row(s, n)
+    return np.diag(((c >= lo) & (c < hi)).astype(float))
+
+
+def operator_terms(prob):
+    """Rank-1 terms of H = H_x + H_y + H_z + H_sigma,
+    S and F, each summed over the 8 octants (bci)."""
+    n = prob["nv"]
+    h = prob["extent"] / (n - 1)
+    quad = prob["quad"]
+    G = prob["G"]
+    mats = prob["materials"]
+    chi = prob["chi"]
+    L = len(quad["w"])
+    w = quad["w"]
+    I_G = np.eye(G)
+    terms = box_terms(prob)
+    H, S, F = [], [], []
+    for b in range(8):
+        sx, sy, sz = (1 if b & 1 else -1, 1 if b & 2 else -1, 1 if b & 4 else -1)
+        Cb = C_b(quad, b)
+        Qmu = Cb @ np.diag(quad["mu"])
+        Qeta = Cb @ np.diag(quad["eta"])
+        Qxi = Cb @ np.diag(quad["xi"])
+        Intg = Cb @ np.outer(np.ones(L), w)                       # Z3 full-L
+        Dx, Dy, Dz = D_s(sx, n, h), D_s(sy, n, h), D_s(sz, n, h)
+        Ix, Iy, Iz = Ip_s(sx, n), Ip_s(sy, n), Ip_s(sz, n)
+        Nx, Ny, Nz = IpN_s(sx, n), IpN_s(sy, n), IpN_s(sz, n)
+        H.append([Dx, Iy, Iz, Qmu, I_G])                            # H_x^{TT,b}
+        H.append([Ix, Dy, Iz, Qeta, I_G])                           # H_y^{TT,b}
+        H.append([Ix, Iy, Dz, Qxi, I_G])                            # H_z^{TT,b}
+        # H_sigma^{TT,b} = diag(sigma) o C_b o Ip o Ip o Ip, with box terms (Z34)
+        m0 = mats[0]
+        H.append([Ix, Iy, Iz, Cb, np.diag(m0["sigma_t"])])
+        S.append([Nx, Ny, Nz, Intg, m0["sigma_s"]])
+        F.append([Nx, Ny, Nz, Intg, np.outer(chi, m0["nu_sigma_f"])])
+        for (lo, hi, m, parent) in terms:
+            Ex = _axis_indicator(sx, n, lo[0], hi[0])
+            Ey = _axis_indicator(sy, n, lo[1], hi[1])
+            Ez = _axis_indicator(sz, n, lo[2], hi[2])
+            dst = mats[m]["sigma_t"] - mats[parent]["sigma_t"]
+            dss = mats[m]["sigma_s"] - mats[parent]["sigma_s"]
+            dnf = mats[m]["nu_sigma_f"] - mats[parent]["nu_sigma_f"]
+            H.append([Ex @ Ix, Ey @ Iy, Ez @ Iz, Cb, np.diag(dst)])
+            if np.any(dss != 0):
+                S.append([Ex @ Nx, Ey @ Ny, Ez @ Nz, Intg, dss])
+            if np.any(dnf != 0):
+                F.append([Ex @ Nx, Ey @ Ny, Ez @ Nz, Intg, np.outer(chi, dnf)])
+    return {"H": H, "S": S, "F": F}
+
+
+def kron_term(term):
+    Fx, Fy, Fz, Fa, Fg = term
+    return np.kron(Fg, np.kron(Fa, np.kron(Fz, np.kron(Fy, Fx))))
+
+
+def dense_operators(prob):
+    """Dense H, S, F as sums of Kronecker products."""
+    T = operator_terms(prob)
+    out = {}
+    for key in ("H", "S", "F"):
+        out[key] = sum(kron_term(t) for t in T[key])
+    if prob.get("boundary", "vacuum") == "reflective":
+        out = _reflective(prob, out)
+    return out
+
+
+# ----------------------------------------------------- Eq.-4 index loop ---
+
+
+def eq4_apply(prob, psi, k_eff=1.0):
+    """Evaluate the row equations of eq. Discretized_kNTE with explicit
+    index loops, generalised per octant (Z7): the cell of row (i,j,k) in an octant
+    with signs s is (i - [s_x>0], j - [s_y>0], k - [s_z>0]).  Returns
+    (Hpsi, Spsi, Fpsi, interior_mask) for the interior (cell-equation) rows; the
+    values at inflow-face rows are left as NaN.  psi is the dense vector
+    (linearised x fastest, then y, z, angle, group)."""
+    n = prob["nv"]
+    h = prob["extent"] / (n - 1)
+    quad = prob["quad"]
+    G = prob["G"]
+    L = len(quad["w"])
+    mats = prob["materials"]
+    chi = prob["chi"]
+    mat = material_map(prob)
+    P = psi.reshape(G, L, n, n, n)                 # [g, l, z, y, x]
+    N = G * L * n ** 3
+    Hv = np.full(N, np.nan); Sv = np.full(N, np.nan); Fv = np.full(N, np.nan)
+    mask = np.zeros(N, dtype=bool)
+    # angular integral sum_l' w_l' psi_{g', l'} per vertex (used by both S and F)
+    phi = np.einsum("l,glzyx->gzyx", quad["w"], P)
+    for g in range(G):
+        for l in range(L):
+            mu, eta, xi = quad["mu"][l], quad["eta"][l], quad["xi"][l]
+            for k in range(n):
+                for j in range(n):
+                    for i in range(n):
+                        # vertex pair (lo, hi) along each axis for this octant
+                        i0, i1 = (i - 1, i) if mu > 0 else (i, i + 1)
+                        j0, j1 = (j - 1, j) if eta > 0 else (j, j + 1)
+                        k0, k1 = (k - 1, k) if xi > 0 else (k, k + 1)
+                        if min(i0, j0, k0) < 0 or max(i1, j1, k1) > n - 1:
+                            continue                      # inflow-face (BC) row
+                        row = i + n * (j + n * (k + n * (l + L * g)))
+                        c = mat[k0, j0, i0]
+                        st = mats[c]["sigma_t"][g]
+                        sx = sum(P[g, l, kk, jj, i1] - P[g, l, kk, jj, i0]
+                                 for kk in (k0, k1) for jj in (j0, j1))
+                        sy = sum(P[g, l, kk, j1, ii] - P[g, l, kk, j0, ii]
+                                 for kk in (k0, k1) for ii in (i0, i1))
+                        sz = sum(P[g, l, k1, jj, ii] - P[g, l, k0, jj, ii]
+                                 for jj in (j0, j1) for ii in (i0, i1))
+                        s8 = sum(P[g, l, kk, jj, ii] for kk in (k0, k1)
+                                 for jj in (j0, j1) for ii in (i0, i1))
+                        Hv[row] = mu / (4 * h) * sx + eta / (4 * h) * sy + xi / (4 * h) * sz + st / 8 * s8
+                        scat = 0.0
+                        fis = 0.0
+                        for gp in range(G):
+                            p8 = sum(phi[gp, kk, jj, ii] for kk in (k0, k1)
+                                     for jj in (j0, j1) for ii in (i0, i1))
+                            scat += mats[c]["sigma_s"][g, gp] * p8 / 8
+                            fis += chi[g] * mats[c]["nu_sigma_f"][gp] * p8 / 8
+                        Sv[row] = scat
+                        Fv[row] = fis
+                        mask[row] = True
+    return Hv, Sv, Fv, mask
+
+
+# --------------------------------------------------------- reflective ---
+
+
+def _reflective(prob, ops):
+    """Reading Z15 (not in the paper): each inflow-face row of ordinate l is
+    replaced by psi_l(face) - psi_refl(l)(face) = 0; S and F rows there are zero.
+    refl flips the cosine normal to the first inflow axis (x, y, z order)."""
+    n = prob["nv"]
+    quad = prob["quad"]
+    G = prob["G"]
+    L = len(quad["w"])
+    H = ops["H"].copy(); S = ops["S"].copy(); F = ops["F"].copy()
+    cos = np.stack([quad["mu"], quad["eta"], quad["xi"]], axis=1)
+    for g in range(G):
+        for l in range(L):
+            for k in range(n):
+                for j in range(n):
+                    for i in range(n):
+                        idx = (i, j, k)
+                        axis = None
+                        for a in range(3):
+                            inflow = 0 if cos[l, a] > 0 else n - 1
+                            if idx[a] == inflow:
+                                axis = a
+                                break
+                        if axis is None:
+                            continue
+                        target = cos[l].copy(); target[axis] = -target[axis]
+                        lr = int(np.argmin(np.sum((cos - target) ** 2, axis=1)))
+                        row = i + n * (j + n * (k + n * (l + L * g)))
+                        col = i + n * (j + n * (k + n * (lr + L * g)))
+                        H[row, :] = 0.0; S[row, :] = 0.0; F[row, :] = 0.0
+                        H[row, row] = 1.0
+                        H[row, col] -= 1.0
+    return {"H": H, "S": S, "F": F}
+
+
+# ------------------------------------------------------ TT / QTT forms ---
+
+
+def term_tt(term):
+    """Rank-1 TT-matrix of one term (eqn:TT_matrices P:726-729), plain TT cores."""
+    return ott.rank1_ttm(term)
+
+
+def qtt_matrix(Fm, eps=1e-14):
+    """Algorithm 1 for one factor: reshape the 2^l x 2^l matrix to
+    2x..x2, permute (i_1..i_l, j_1..j_l) -> (i_1, j_1, .., i_l, j_l) (bits LSB first,
+    Z28), TT-SVD with modes 4 (row bit fastest), cores [r, 2, 2, r']."""
+    n = Fm.shape[0]
+    l = int(round(math.log2(n)))
+    if 2 ** l != n or l == 0:
+        raise ValueError("Alg. 1 needs a power-of-two mode >= 2")
+    T = Fm.reshape([2] * l + [2] * l, order="F")          # (i_0..i_{l-1}, j_0..j_{l-1})
+    perm = []
+    for t in range(l):
+        perm += [t, l + t]
+    T = np.transpose(T, perm)                             # (i_0, j_0, i_1, j_1, ...)
+    cores = ott.tt_svd(T.reshape(-1, order="F"), [4] * l, eps)
+    return [c.reshape(c.shape[0], 2, 2, c.shape[2], order="F") for c in cores]
+
+
+def term_qtt(term):
+    """QTT form of one term: spatial factors via Alg. 1, angle and group kept as
+    plain TT cores (mixed TT/QTT)."""
+    cores = []
+    for F in term[:3]:
+        cores += qtt_matrix(F)
+    Fa, Fg = term[3], term[4]
+    cores.append(Fa.reshape(1, Fa.shape[0], Fa.shape[1], 1))
+    cores.append(Fg.reshape(1, Fg.shape[0], Fg.shape[1], 1))
+    return cores
+
+
+def ttm_sum_round(term_list, eps=1e-13, rmax=10**9):
+    """Sum rank-1 TT-matrices (ranks add) then round them as TT-vectors
+    with mode m_k n_k ('a rank reduction step could be necessary')."""
+    rows = [c.shape[1] for c in term_list[0]]
+    cols = [c.shape[2] for c in term_list[0]]
+    acc = None
+    for T in term_list:
+        V = ott.ttm_as_tt(T)
+        acc = V if acc is None else ott.tt_add(acc, V)
+    rounded, _ = ott.tt_round(acc, eps, rmax)
+    return ott.tt_as_ttm(rounded, rows, cols)
+
+
+def tt_operators(prob, eps=1e-13, qtt=None):
+    """H, S, F as TT-matrices (QTT spatial cores when prob['qtt'])."""
+    if qtt is None:
+        qtt = prob.get("qtt", False)
+    T = operator_terms(prob)
+    make = term_qtt if qtt else term_tt
+    return {key: ttm_sum_round([make(t) for t in T[key]], eps) for key in ("H", "S", "F")}
+
+
+def ones_tt(mode_sizes):
+    return [np.ones((1, n, 1)) for n in mode_sizes]
+
+
+def qtt_modes(prob):
+    n = prob["nv"]
+    l = int(round(math.log2(n)))
+    L = len(prob["quad"]["w"])
+    return [2] * (3 * l) + [L, prob["G"]]
+
+
+def tt_modes(prob):
+    n = prob["nv"]
+    return [n, n, n, len(prob["quad"]["w"]), prob["G"]]
