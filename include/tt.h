@@ -1,0 +1,253 @@
+/*
+ * tt.h — C ABI of libtt, the B200 (sm_100a) hot path of arXiv 2309.03347:
+ * "Tensor Networks for Solving Realistic Time-independent Boltzmann Neutron
+ * Transport Equation".  Passages are cited as P:<lines> of PAPER.md and the
+ * readings Z<n> of SURVEY.md §8(c).3 (restated in DESIGN.md).
+ *
+ * Conventions
+ *   - Everything is fp64.  All `double *` arguments are DEVICE pointers; shape
+ *     arrays (`n`, `m`, `rcap`, `off`) are HOST pointers; `*_dev` are device.
+ *   - TT-vector core k (0-based) is [r_k, n_k, r_{k+1}] column-major (first index
+ *     fastest) stored compactly at data + off[k]; its slot holds
+ *     rcap[k] * n_k * rcap[k+1] doubles, so ranks may change on the device
+ *     without reallocation.  r_dev[0] = r_dev[d] = 1.
+ *   - TT-matrix core k is [R_k, m_k, n_k, R_{k+1}] column-major; (i, j) =
+ *     (row/output, column/input) index (Z27).  A TT-matrix viewed as
+ *     a TT-vector has mode m_k n_k with the row index fastest.
+ *   - Full-tensor linearisation: first core fastest (Z28).
+ *   - Ranks live on the device (int32).  The library never allocates device
+ *     memory and never frees; scratch is the caller's `ws` of `wsb` bytes,
+ *     sized by the tt_*_workspace functions.  Every call is asynchronous and
+ *     stream-ordered on `s`; buffers must outlive stream completion.
+ *   - The returned tt_status covers host-detectable errors (argument, shape,
+ *     capacity at the declared capacities, launch failures).  Conditions found
+ *     on the device (non-convergence, NaN, no fission) are written to the
+ *     caller's status word (keff_report.status_dev) and are readable after a
+ *     stream synchronisation.  tt_last_error() describes the last host error
+ *     of the calling thread.  There is no CPU fallback: an unavailable path
+ *     returns TT_ERR_NOT_IMPLEMENTED.
+ *   - Reentrant for distinct `ws` buffers and streams.
+ */
+#ifndef TT_B200_H
+#define TT_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  TT_OK = 0,
+  TT_ERR_ARG = 1,        /* invalid argument (NULL, d < 1, r_0 != 1, bad option)       */
+  TT_ERR_SHAPE = 2,      /* mode sizes disagree ("shape mismatch")                  */
+  TT_ERR_CAPACITY = 3,   /* an output rank capacity or the workspace is too small         */
+  TT_ERR_NOCONV = 4,     /* (device status) iteration budget exhausted; history written   */
+  TT_ERR_NOFISSION = 5,  /* (device status) <F^T 1, Psi> = 0                               */
+  TT_ERR_NUMERIC = 6,    /* (device status) NaN/Inf or singular local system              */
+  TT_ERR_CUDA = 7,       /* a CUDA launch failed                                          */
+  TT_ERR_NOT_IMPLEMENTED = 8
+} tt_status;
+
+typedef void *tt_stream; /* cudaStream_t; NULL = legacy default stream */
+
+#define TT_MAX_D 64      /* maximum number of cores */
+
+/* TT-vector (eqn:TT_def_element P:492-497, eqn:TT-vector P:504-512). */
+typedef struct {
+  int32_t d;               /* number of cores, 1 <= d <= TT_MAX_D                       */
+  const int32_t *n;        /* [d] host: mode sizes                                       */
+  int32_t *r_dev;          /* [d+1] device: current ranks                                */
+  const int32_t *rcap;     /* [d+1] host: rank capacities (slot sizes), rcap[0]=rcap[d]=1 */
+  double *data;            /* device: core storage                                       */
+  const int64_t *off;      /* [d] host: element offset of core k's slot                  */
+} tt_vec;
+
+/* TT-matrix (eqn:TT-matrix-componentwise P:670-680, eqn:TT-matrix-compact P:686-691). */
+typedef struct {
+  int32_t d;
+  const int32_t *m;        /* [d] host: row (output) mode sizes                          */
+  const int32_t *n;        /* [d] host: column (input) mode sizes                        */
+  int32_t *R_dev;          /* [d+1] device: current ranks                                */
+  const int32_t *Rcap;     /* [d+1] host: rank capacities                                */
+  double *data;
+  const int64_t *off;
+} tt_mat;
+
+const char *tt_last_error(void);
+const char *tt_version(void);
+
+/* ---------------------------------------------------------------- a1 ---
+ * tt_matvec: exact TT-matrix x TT-vector product ("explicit and
+ * exact algorithm").  For every core, independently,
+ *   Y_k[rho, i, rho'] = sum_j A_k[a, i, j, a'] X_k[b, j, b'],
+ *   rho = a + R_k b, rho' = a' + R_{k+1} b'  (operator rank fastest).
+ * Output ranks R_k r_k are written to y->r_dev.  Requires A->n == x->n,
+ * y->n == A->m, y->rcap[k] >= Rcap[k] * x->rcap[k] (else TT_ERR_CAPACITY).
+ * No workspace.  y must not alias A or x. */
+tt_status tt_matvec(const tt_mat *A, const tt_vec *x, tt_vec *y, tt_stream s);
+
+/* Batched form: B independent products (A[b], x[b]) -> y[b], one launch. */
+tt_status tt_matvec_batched(int32_t B, const tt_mat *A, const tt_vec *x, tt_vec *y, tt_stream s);
+
+/* ---------------------------------------------------------------- a2 ---
+ * tt_add: z = alpha x + beta y by block-diagonal core concatenation (sum of
+ * TT tensors is a TT tensor): first core [alpha X_1, beta Y_1], last
+ * core [X_d; Y_d], middle diag(X_k, Y_k); ranks add.  alpha_dev / beta_dev are
+ * device scalars (NULL = 1.0), so k^{-1} of the fixed point never leaves the
+ * device.  d = 1: z = alpha x + beta y elementwise.  z must not alias x or y. */
+tt_status tt_add(const tt_vec *x, const double *alpha_dev, const tt_vec *y,
+                 const double *beta_dev, tt_vec *z, tt_stream s);
+
+/* tt_scale: x <- alpha x (scales the first core), alpha read on the device. */
+tt_status tt_scale(tt_vec *x, const double *alpha_dev, tt_stream s);
+
+/* tt_copy: y <- x (ranks and cores); y capacities must hold x's ranks. */
+tt_status tt_copy(const tt_vec *x, tt_vec *y, tt_stream s);
+
+/* ---------------------------------------------------------------- a8 ---
+ * tt_dot: <x, y> by a left-to-right chain contraction (the "sum F Psi"
+ * reductions of eqn:TT_k_eff_fixed_points P:1409 are <F^T 1, Psi>, Z18).
+ * Result written to out_dev.  Workspace: tt_dot_workspace(x, y). */
+size_t tt_dot_workspace(const tt_vec *x, const tt_vec *y);
+tt_status tt_dot(const tt_vec *x, const tt_vec *y, double *out_dev, void *ws, size_t wsb,
+                 tt_stream s);
+
+/* ---------------------------------------------------------------- a3 ---
+ * tt_orthogonalize (rounding internals unstated in the
+ * paper, reading Z21).  dir = -1: right-to-left, for k = d-1..1:
+ * Householder QR of the transposed right unfolding (n_k r_{k+1}) x r_k,
+ * core k <- Q^T, core k-1 <- core k-1 x_3 R^T, r_k <- min(r_k, n_k r_{k+1}).
+ * dir = +1: the left-to-right mirror (QR of the left unfoldings).  In place.
+ * norm_dev (may be NULL) receives ||x||_F = ||orthogonality centre||_F.
+ * Workspace: tt_orthogonalize_workspace(x). */
+size_t tt_orthogonalize_workspace(const tt_vec *x);
+tt_status tt_orthogonalize(tt_vec *x, int32_t dir, double *norm_dev, void *ws, size_t wsb,
+                           tt_stream s);
+
+/* ---------------------------------------------------------------- a4 ---
+ * tt_round: TT rounding ("rank reduction step"), in place:
+ * right-to-left orthogonalisation, delta = eps ||x||_F / sqrt(d-1), then for
+ * k = 0..d-2 the SVD of the left unfolding (r_k n_k) x r_{k+1} (Householder QR +
+ * one-sided Jacobi on the triangular factor), new rank
+ *   r' = min(rmax, smallest r >= 1 with sum_{i>r} sigma_i^2 <= delta^2)   (Z21),
+ * core k <- U[:, :r'], core k+1 <- (Sigma V^T)[:r'] x_1 core k+1.
+ * discarded_sq_dev (may be NULL) receives the d-1 discarded tail energies;
+ * sv_dev (may be NULL) receives, per bond, the singular values (stride
+ * sv_stride doubles, zero padded).  Workspace: tt_round_workspace(x). */
+size_t tt_round_workspace(const tt_vec *x);
+tt_status tt_round(tt_vec *x, double eps, int32_t rmax, double *discarded_sq_dev,
+                   double *sv_dev, int32_t sv_stride, void *ws, size_t wsb, tt_stream s);
+
+/* ------------------------------------------------------------ a5, a6 ---
+ * Interfaces and local operator of ALS/AMEn ("fix all but one TT
+ * core").  Orientation: Phi[alpha, gamma, beta] with
+ * alpha = test rank, gamma = operator rank, beta = trial rank (alpha fastest).
+ *
+ * als_local_apply:
+ *   y[a, i, a'] = sum Phi[a, g, b] A_k[g, i, j, g'] Psi[a', g', b'] x[b, j, b']
+ * Phi [rA, R, rB], Ak [R, m, n, Rp], Psi [rAp, Rp, rBp], x [rB, n, rBp] -> y [rA, m, rAp].
+ * Evaluated as three FP64 tensor-core (DMMA) GEMMs: x.Psi^T, A_k.(.), Phi.(.).
+ * Workspace: als_workspace(...). */
+size_t als_workspace(int32_t rA, int32_t R, int32_t rB, int32_t m, int32_t n, int32_t rAp,
+                     int32_t Rp, int32_t rBp);
+tt_status als_local_apply(int32_t rA, int32_t R, int32_t rB, int32_t m, int32_t n, int32_t rAp,
+                          int32_t Rp, int32_t rBp, const double *Phi, const double *Ak,
+                          const double *Psi, const double *x, double *y, void *ws, size_t wsb,
+                          tt_stream s);
+
+/* als_update_interfaces:
+ *   dir = +1 (left):  Phi_k[a', g', b'] = sum Phi_{k-1}[a, g, b] Y_k[a, i, a'] A_k[g, i, j, g'] X_k[b, j, b']
+ *   dir = -1 (right): Psi_k[a, g, b]    = sum Psi_{k+1}[a', g', b'] Y_k[a, i, a'] A_k[g, i, j, g'] X_k[b, j, b']
+ * Y_k [rY, m, rYp], X_k [rX, n, rXp], A_k [R, m, n, Rp].  With Ak == NULL the
+ * vector interface (R = Rp = 1, B_k passed as X_k with n = m):
+ *   phi_k[a', b'] = sum phi_{k-1}[a, b] Y_k[a, i, a'] X_k[b, i, b'].
+ * Iprev: [rY, R, rX] (left) or [rYp, Rp, rXp] (right); Inext the other.
+ * Workspace: als_workspace(rY, R, rX, m, n, rYp, Rp, rXp). */
+tt_status als_update_interfaces(int32_t dir, int32_t rY, int32_t R, int32_t rX, int32_t m,
+                                int32_t n, int32_t rYp, int32_t Rp, int32_t rXp,
+                                const double *Iprev, const double *Yk, const double *Ak,
+                                const double *Xk, double *Inext, void *ws, size_t wsb,
+                                tt_stream s);
+
+/* ---------------------------------------------------------------- a7 ---
+ * amen_solve: x ~ A^{-1} b in TT ("amen_solve";
+ * reading Z20): alternating-direction sweeps, Galerkin local systems solved by
+ * device GMRES(restart) built on als_local_apply, SVD truncation with
+ * delta = eps ||x_k|| / sqrt(d-1) capped at rmax, residual TT z (ranks = its
+ * initial ranks = kickrank) and enrichment of the solution core with the
+ * residual projected on (x frames | z frames).  Stops after a sweep whose
+ * maximum local residual (measured before each local solve) is <= eps.
+ * x: in initial guess, out solution (capacities >= rmax + kickrank).
+ * z: in initial residual TT (random draws are inputs), workspace afterwards.
+ * sweeps_dev / res_dev (may be NULL): sweeps used and final max residual.
+ * Workspace: amen_workspace(A, b, x, z). */
+typedef struct {
+  double eps;              /* stopping tolerance on the local residual            */
+  double local_tol;        /* GMRES relative tolerance (<= 0: 0.1 eps)             */
+  int32_t max_sweeps;
+  int32_t rmax;
+  int32_t gmres_restart;   /* Krylov basis size m                                  */
+  int32_t gmres_max_restarts;
+} amen_opts;
+size_t amen_workspace(const tt_mat *A, const tt_vec *b, const tt_vec *x, const tt_vec *z,
+                      const amen_opts *o);
+tt_status amen_solve(const tt_mat *A, const tt_vec *b, tt_vec *x, tt_vec *z, const amen_opts *o,
+                     int32_t *sweeps_dev, double *res_dev, void *ws, size_t wsb, tt_stream s);
+
+/* ---------------------------------------------------------------- a9 ---
+ * keff_fixed_point: eqn:TT_k_eff_fixed_points, readings
+ * Z16-Z19:
+ *   B = round(round(S Psi) + k^{-1} round(F Psi));  H Psi' = B (amen_solve,
+ *   warm start Psi);  k' = k <f, Psi'> / <f, Psi>, f = F^T 1;  Psi <- Psi'/||Psi'||;
+ *   stop when |k' - k| <= tol_k or after max_outer iterations.
+ * k, ||Psi||, <f, Psi> and every rank stay on the device; the host only
+ * polls the convergence flag once per outer iteration.  psi: in Psi_0, out
+ * normalised eigenvector (capacities >= rmax + kickrank).  z: AMEn residual
+ * TT (random initial cores are an input).  Report arrays are device memory.
+ * Workspace: keff_workspace(...). */
+typedef struct {
+  double tol_k;            /* |k' - k| stopping tolerance                          */
+  double eps_round;        /* rounding tolerance of S Psi, F Psi, B                */
+  double eps_solve;        /* AMEn tolerance                                       */
+  int32_t max_outer;
+  int32_t rmax;
+  int32_t max_sweeps;
+  int32_t gmres_restart;
+  int32_t gmres_max_restarts;
+} keff_opts;
+typedef struct {
+  double *k_dev;           /* [1] final k                                          */
+  int32_t *iters_dev;      /* [1] outer iterations performed                       */
+  double *k_hist_dev;      /* [hist_cap] k after each outer iteration              */
+  int32_t *sweeps_hist_dev;/* [hist_cap] AMEn sweeps per outer iteration           */
+  int32_t hist_cap;
+  int32_t *status_dev;     /* [1] TT_OK / TT_ERR_NOCONV / TT_ERR_NOFISSION / ...   */
+} keff_report;
+size_t keff_workspace(const tt_mat *H, const tt_mat *S, const tt_mat *F, const tt_vec *psi,
+                      const tt_vec *z, const keff_opts *o);
+tt_status keff_fixed_point(const tt_mat *H, const tt_mat *S, const tt_mat *F, tt_vec *psi,
+                           tt_vec *z, double k0, const keff_opts *o, keff_report *rep, void *ws,
+                           size_t wsb, tt_stream s);
+
+/* ------------------------------------------------ operator assembly ---
+ * Host-side construction of the factor matrices of the rank-1 per-octant
+ * terms of H, S, F (readings Z3-Z7, Z34), written as plain
+ * column-major host arrays; the caller uploads them and sums/rounds on the
+ * device with tt_add / tt_round.  This is one-off setup, not a hot-path step.
+ * prob_* describe the problem; op = 0 (H),
+ * 1 (S), 2 (F).  Returns the number of terms; with out == NULL only counts.
+ * Each term writes 5 factors in core order (x, y, z, angle, group):
+ * nv*nv*3 + L*L + G*G doubles, consecutively. */
+int32_t tt_transport_terms(int32_t op, int32_t nv, double extent, int32_t G, int32_t L,
+                           const double *mu, const double *eta, const double *xi,
+                           const double *w, int32_t nmat, const double *sigma_t,
+                           const double *sigma_s, const double *nu_sigma_f, const double *chi,
+                           int32_t nbox, const int32_t *box_lo, const int32_t *box_hi,
+                           const int32_t *box_mat, double *out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TT_B200_H */

@@ -263,32 +263,48 @@ def tt_svd(T, dims, eps, rmax=10**9):
 
 
 def left_update(Phi, Yk, Ak, Xk):
-    """Phi_k[a',g',b'] = sum Phi_{k-1}[a,g,b] Y_k[a,i,a'] A_k[g,i,j,g'] X_k[b,j,b']."""
-    return np.einsum("agb,aic,gijh,bjd->chd", Phi, Yk, Ak, Xk, optimize=True)
+    """Phi_k[a',g',b'] = sum Phi_{k-1}[a,g,b] Y_k[a,i,a'] A_k[g,i,j,g'] X_k[b,j,b'],
+    as three pairwise contractions (library tensordot), in this order:
+    over a, then over (g, i), then over (b, j)."""
+    T1 = np.tensordot(Phi, Yk, axes=([0], [0]))              # [g, b, i, a']
+    T2 = np.tensordot(T1, Ak, axes=([0, 2], [0, 1]))         # [b, a', j, g']
+    return np.tensordot(T2, Xk, axes=([0, 2], [0, 1]))       # [a', g', b']
 
 
 def right_update(Psi, Yk, Ak, Xk):
-    """Psi_k[a,g,b] = sum Psi_{k+1}[a',g',b'] Y_k[a,i,a'] A_k[g,i,j,g'] X_k[b,j,b']."""
-    return np.einsum("chd,aic,gijh,bjd->agb", Psi, Yk, Ak, Xk, optimize=True)
+    """Psi_k[a,g,b] = sum Psi_{k+1}[a',g',b'] Y_k[a,i,a'] A_k[g,i,j,g'] X_k[b,j,b'];
+    contractions over b', then (j, g'), then (i, a')."""
+    T1 = np.tensordot(Xk, Psi, axes=([2], [2]))              # [b, j, a', g']
+    T2 = np.tensordot(T1, Ak, axes=([1, 3], [2, 3]))         # [b, a', g, i]
+    out = np.tensordot(Yk, T2, axes=([1, 2], [3, 1]))        # [a, b, g]
+    return np.transpose(out, (0, 2, 1))
 
 
 def left_update_vec(phi, Yk, Bk):
     """phi_k[a',b'] = sum phi_{k-1}[a,b] Y_k[a,i,a'] B_k[b,i,b'] (vector interface)."""
-    return np.einsum("ab,aic,bid->cd", phi, Yk, Bk, optimize=True)
+    T1 = np.tensordot(phi, Yk, axes=([0], [0]))              # [b, i, a']
+    return np.tensordot(T1, Bk, axes=([0, 1], [0, 1]))       # [a', b']
 
 
 def right_update_vec(psi, Yk, Bk):
-    return np.einsum("cd,aic,bid->ab", psi, Yk, Bk, optimize=True)
+    """psi_k[a,b] = sum psi_{k+1}[a',b'] Y_k[a,i,a'] B_k[b,i,b']."""
+    T1 = np.tensordot(Bk, psi, axes=([2], [1]))              # [b, i, a']
+    return np.tensordot(Yk, T1, axes=([1, 2], [1, 2]))       # [a, b]
 
 
 def local_apply(Phi, Ak, Psi, x):
-    """y[a,i,a'] = sum Phi[a,g,b] A[g,i,j,g'] Psi[a',g',b'] x[b,j,b']."""
-    return np.einsum("agb,gijh,chd,bjd->aic", Phi, Ak, Psi, x, optimize=True)
+    """y[a,i,a'] = sum Phi[a,g,b] A[g,i,j,g'] Psi[a',g',b'] x[b,j,b']:
+    (1) x x Psi over b'; (2) x A over (j, g'); (3) x Phi over (b, g)."""
+    T1 = np.tensordot(x, Psi, axes=([2], [2]))               # [b, j, a', g']
+    T2 = np.tensordot(T1, Ak, axes=([1, 3], [2, 3]))         # [b, a', g, i]
+    y = np.tensordot(Phi, T2, axes=([1, 2], [2, 0]))         # [a, a', i]
+    return np.transpose(y, (0, 2, 1))
 
 
 def local_rhs(phi, Bk, psi):
     """rhs[a,i,a'] = sum phi[a,b] B[b,i,b'] psi[a',b']."""
-    return np.einsum("ab,bic,dc->aid", phi, Bk, psi, optimize=True)
+    T1 = np.tensordot(Bk, psi, axes=([2], [1]))              # [b, i, a']
+    return np.tensordot(phi, T1, axes=([1], [0]))            # [a, i, a']
 
 
 def local_matrix(Phi, Ak, Psi):
@@ -296,7 +312,9 @@ def local_matrix(Phi, Ak, Psi):
     ra, R0, rb = Phi.shape
     rap, R1, rbp = Psi.shape
     _, m, n, _ = Ak.shape
-    T = np.einsum("agb,gijh,chd->aicbjd", Phi, Ak, Psi, optimize=True)
+    T = np.tensordot(Phi, Ak, axes=([1], [0]))               # [a, b, i, j, g']
+    T = np.tensordot(T, Psi, axes=([4], [1]))                # [a, b, i, j, a', b']
+    T = np.transpose(T, (0, 2, 4, 1, 3, 5))                  # [a, i, a', b, j, b']
     return T.reshape(ra * m * rap, rb * n * rbp, order="F")
 
 

@@ -1,0 +1,15 @@
+"""B200-native (sm_100a, fp64) hot path of arXiv 2309.03347: TT/QTT k-eigenvalue
+neutron transport — exact TT matvec, TT rounding, ALS/AMEn local apply and
+interfaces, k-eff fixed point — behind the C ABI of include/tt.h.
+
+Importing the package loads libtt.so and fails loudly if it is missing."""
+from . import _lib
+from ._lib import TTError
+
+_lib.lib()  # raise now if the CUDA library is absent (no CPU fallback)
+
+from .tt import (TTMat, TTVec, als_local_apply, als_update_interfaces, matvec_out,  # noqa: E402
+                 tt_add, tt_copy, tt_dot, tt_matvec, tt_orthogonalize, tt_round, tt_scale)
+
+__all__ = ["TTError", "TTMat", "TTVec", "tt_matvec", "matvec_out", "tt_add", "tt_scale", "tt_copy", "tt_dot",
+           "tt_orthogonalize", "tt_round", "als_local_apply", "als_update_interfaces"]

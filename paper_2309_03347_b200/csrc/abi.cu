@@ -1,0 +1,114 @@
+// extern "C" entry points of libtt (include/tt.h): argument checks, meta
+// marshalling, workspace planning.  All compute is in the kernels.
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "tt_common.cuh"
+
+using namespace tt;
+
+extern "C" const char *tt_version(void) { return "libtt-b200 0.1 (sm_100a, fp64 DMMA)"; }
+
+// tt_last_error is defined next to the error state.
+namespace tt {
+const char *last_error_cstr();
+}
+extern "C" const char *tt_last_error(void) { return tt::last_error_cstr(); }
+
+extern "C" tt_status tt_matvec(const tt_mat *A, const tt_vec *x, tt_vec *y, tt_stream s) {
+  MatMeta a;
+  VecMeta xm, ym;
+  TT_TRY(make_mat_meta(A, a));
+  TT_TRY(make_vec_meta(x, xm));
+  TT_TRY(make_vec_meta(y, ym));
+  return matvec_meta(a, xm, ym, (cudaStream_t)s);
+}
+
+extern "C" tt_status tt_matvec_batched(int32_t B, const tt_mat *A, const tt_vec *x, tt_vec *y, tt_stream s) {
+  if (B < 0 || (B > 0 && (!A || !x || !y))) return fail(TT_ERR_ARG, "tt_matvec_batched: bad batch");
+  for (int b = 0; b < B; ++b) TT_TRY(tt_matvec(A + b, x + b, y + b, s));
+  return TT_OK;
+}
+
+extern "C" tt_status tt_add(const tt_vec *x, const double *alpha_dev, const tt_vec *y, const double *beta_dev,
+                            tt_vec *z, tt_stream s) {
+  VecMeta xm, ym, zm;
+  TT_TRY(make_vec_meta(x, xm));
+  TT_TRY(make_vec_meta(y, ym));
+  TT_TRY(make_vec_meta(z, zm));
+  return add_meta(xm, alpha_dev, ym, beta_dev, zm, (cudaStream_t)s);
+}
+
+extern "C" tt_status tt_scale(tt_vec *x, const double *alpha_dev, tt_stream s) {
+  VecMeta xm;
+  TT_TRY(make_vec_meta(x, xm));
+  if (!alpha_dev) return fail(TT_ERR_ARG, "tt_scale: alpha_dev is NULL");
+  return scale_meta(xm, alpha_dev, 1.0, 0, (cudaStream_t)s);
+}
+
+extern "C" tt_status tt_copy(const tt_vec *x, tt_vec *y, tt_stream s) {
+  VecMeta xm, ym;
+  TT_TRY(make_vec_meta(x, xm));
+  TT_TRY(make_vec_meta(y, ym));
+  return copy_meta(xm, ym, (cudaStream_t)s);
+}
+
+extern "C" size_t tt_dot_workspace(const tt_vec *x, const tt_vec *y) {
+  VecMeta xm, ym;
+  if (make_vec_meta(x, xm) != TT_OK || make_vec_meta(y, ym) != TT_OK) return 0;
+  Arena ar;
+  if (dot_meta(xm, ym, nullptr, ar, nullptr) != TT_OK) return 0;
+  return ar.used;
+}
+
+extern "C" tt_status tt_dot(const tt_vec *x, const tt_vec *y, double *out_dev, void *ws, size_t wsb, tt_stream s) {
+  VecMeta xm, ym;
+  TT_TRY(make_vec_meta(x, xm));
+  TT_TRY(make_vec_meta(y, ym));
+  if (!out_dev || !ws) return fail(TT_ERR_ARG, "tt_dot: NULL pointer");
+  Arena ar;
+  ar.base = (char *)ws;
+  ar.cap = wsb;
+  return dot_meta(xm, ym, out_dev, ar, (cudaStream_t)s);
+}
+
+extern "C" size_t tt_orthogonalize_workspace(const tt_vec *x) {
+  VecMeta xm;
+  if (make_vec_meta(x, xm) != TT_OK) return 0;
+  Arena ar;
+  orth_meta(xm, -1, nullptr, ar, nullptr);
+  return ar.used;
+}
+
+extern "C" tt_status tt_orthogonalize(tt_vec *x, int32_t dir, double *norm_dev, void *ws, size_t wsb,
+                                      tt_stream s) {
+  VecMeta xm;
+  TT_TRY(make_vec_meta(x, xm));
+  if (dir != 1 && dir != -1) return fail(TT_ERR_ARG, "tt_orthogonalize: dir must be +1 or -1");
+  if (!ws) return fail(TT_ERR_ARG, "tt_orthogonalize: NULL workspace");
+  Arena ar;
+  ar.base = (char *)ws;
+  ar.cap = wsb;
+  return orth_meta(xm, dir, norm_dev, ar, (cudaStream_t)s);
+}
+
+extern "C" size_t tt_round_workspace(const tt_vec *x) {
+  VecMeta xm;
+  if (make_vec_meta(x, xm) != TT_OK) return 0;
+  Arena ar;
+  round_meta(xm, 0.0, 1, nullptr, nullptr, 0, ar, nullptr);
+  return ar.used;
+}
+
+extern "C" tt_status tt_round(tt_vec *x, double eps, int32_t rmax, double *discarded_sq_dev, double *sv_dev,
+                              int32_t sv_stride, void *ws, size_t wsb, tt_stream s) {
+  VecMeta xm;
+  TT_TRY(make_vec_meta(x, xm));
+  if (!ws) return fail(TT_ERR_ARG, "tt_round: NULL workspace");
+  if (sv_dev && sv_stride < 1) return fail(TT_ERR_ARG, "tt_round: sv_stride must be >= 1");
+  Arena ar;
+  ar.base = (char *)ws;
+  ar.cap = wsb;
+  return round_meta(xm, eps, rmax, discarded_sq_dev, sv_dev, sv_stride, ar, (cudaStream_t)s);
+}

@@ -1,0 +1,149 @@
+// FP64 tensor-core GEMM for sm_100a: mma.sync.m8n8k4.f64 (SASS DMMA.8x8x4).
+// tcgen05 has no f64 kind, so FP64 tensor work on Blackwell is warp-level
+// DMMA.  64x64x16 CTA tile, 4 warps of 32x32, operands staged
+// through double-buffered shared memory with cp.async (zero-filled edges),
+// descriptor read from device memory so sizes can follow device ranks.
+#include "tt_common.cuh"
+
+namespace tt {
+
+namespace {
+
+constexpr int BM = 64, BN = 64, BK = 16, PAD = 4;
+
+__device__ __forceinline__ void cp_async8(void *smem, const void *gmem, bool pred) {
+  unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  int sz = pred ? 8 : 0;
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(sz));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::); }
+
+__device__ __forceinline__ void dmma(double &c0, double &c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+struct Tile {
+  double a[2][BK][BM + PAD];
+  double b[2][BK][BN + PAD];
+};
+
+__device__ __forceinline__ void load_tile(Tile &t, int buf, const GemmDesc &g, int m0, int n0, int k0,
+                                          int tid) {
+  const double *A = g.A, *B = g.B;
+  // A tile: BM x BK of op(A)
+  if (!g.transA) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      int m = tid & 63, k = (tid >> 6) + 2 * i;
+      int gm = m0 + m, gk = k0 + k;
+      bool p = gm < g.M && gk < g.K;
+      const double *src = p ? A + gm + (long long)gk * g.lda : A;
+      cp_async8(&t.a[buf][k][m], src, p);
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      int k = tid & 15, m = (tid >> 4) + 8 * i;
+      int gm = m0 + m, gk = k0 + k;
+      bool p = gm < g.M && gk < g.K;
+      const double *src = p ? A + gk + (long long)gm * g.lda : A;
+      cp_async8(&t.a[buf][k][m], src, p);
+    }
+  }
+  if (!g.transB) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      int k = tid & 15, n = (tid >> 4) + 8 * i;
+      int gn = n0 + n, gk = k0 + k;
+      bool p = gn < g.N && gk < g.K;
+      const double *src = p ? B + gk + (long long)gn * g.ldb : B;
+      cp_async8(&t.b[buf][k][n], src, p);
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      int n = tid & 63, k = (tid >> 6) + 2 * i;
+      int gn = n0 + n, gk = k0 + k;
+      bool p = gn < g.N && gk < g.K;
+      const double *src = p ? B + gn + (long long)gk * g.ldb : B;
+      cp_async8(&t.b[buf][k][n], src, p);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(128) gemm_dmma_kernel(const GemmDesc *__restrict__ descs) {
+  __shared__ __align__(16) Tile t;
+  const GemmDesc g = descs[blockIdx.z];
+  const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN;
+  if (m0 >= g.M || n0 >= g.N) return;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = (warp & 1) * 32, wn = (warp >> 1) * 32;
+  double acc[4][4][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+  const int nk = (g.K + BK - 1) / BK;
+  if (nk > 0) {
+    load_tile(t, 0, g, m0, n0, 0, tid);
+    cp_async_commit();
+  }
+  for (int kt = 0; kt < nk; ++kt) {
+    const int buf = kt & 1;
+    cp_async_wait_all();
+    __syncthreads();
+    if (kt + 1 < nk) {
+      load_tile(t, buf ^ 1, g, m0, n0, (kt + 1) * BK, tid);
+      cp_async_commit();
+    }
+#pragma unroll
+    for (int kk = 0; kk < BK; kk += 4) {
+      double af[4], bf[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) af[i] = t.a[buf][kk + (lane & 3)][wm + i * 8 + (lane >> 2)];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) bf[j] = t.b[buf][kk + (lane & 3)][wn + j * 8 + (lane >> 2)];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dmma(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+    }
+    __syncthreads();
+  }
+  double alpha = g.alpha;
+  if (g.alpha_dev) alpha *= *g.alpha_dev;
+  const double beta = g.beta;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int r = m0 + wm + i * 8 + (lane >> 2);
+    if (r >= g.M) continue;
+    const long long roff = (long long)(r % g.dr) * g.s_r0 + (long long)(r / g.dr) * g.s_r1;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int c = n0 + wn + j * 8 + (lane & 3) * 2 + h;
+        if (c >= g.N) continue;
+        const long long addr = roff + (long long)(c % g.dc) * g.s_c0 + (long long)(c / g.dc) * g.s_c1;
+        double v = alpha * acc[i][j][h];
+        if (beta != 0.0) v += beta * g.C[addr];
+        g.C[addr] = v;
+      }
+    }
+  }
+}
+
+}  // namespace
+
+tt_status launch_gemm(const GemmDesc *descs_dev, int count, int Mcap, int Ncap, cudaStream_t s) {
+  if (count <= 0 || Mcap <= 0 || Ncap <= 0) return TT_OK;
+  dim3 grid((Mcap + BM - 1) / BM, (Ncap + BN - 1) / BN, count);
+  gemm_dmma_kernel<<<grid, 128, 0, s>>>(descs_dev);
+  return check_launch("gemm_dmma");
+}
+
+}  // namespace tt

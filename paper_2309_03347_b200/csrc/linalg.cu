@@ -1,0 +1,419 @@
+// Batched small dense linear algebra for TT rounding / AMEn on sm_100a (fp64):
+//   * blocked Householder QR (LAPACK geqrf/larft/larfb/orgqr structure) with an
+//     explicit Q — rank-deficient safe (tau = 0 for a zero column);
+//   * one-sided Hestenes Jacobi SVD, parallel round-robin ordering, one warp
+//     per column pair, data in shared memory when it fits.
+// One CTA per problem; problems are batched over the grid.  Sizes come from
+// descriptors in device memory (they follow device-resident TT ranks).
+#include <cfloat>
+
+#include "tt_common.cuh"
+
+namespace tt {
+
+namespace {
+
+constexpr int QR_THREADS = 256;
+constexpr int NB = 32;
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__device__ double block_sum(double v, double *red) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  v = warp_sum(v);
+  __syncthreads();
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  double t = 0.0;
+  for (int i = 0; i < nw; ++i) t += red[i];
+  return t;
+}
+
+// Block reflector application on a target matrix X (rows r0.., element (r,c)
+// at X[r*rs + c*cs]):  X[r0:m, cols] -= V * (op(T) * (V^T X[r0:m, cols]))
+// where V = unit lower trapezoidal panel stored in A[:, j0:j0+jb] (lda) with its
+// implicit unit diagonal at row j0+l, and op(T) = T^T (transT = 1) or T.
+__device__ void apply_block_reflector(int m, int j0, int jb, const double *A, long long lda,
+                                      const double (*sT)[NB + 1], int transT, double *X, long long rs,
+                                      long long cs, int c_begin, int c_end, double (*sV)[NB + 1],
+                                      double (*sX)[NB + 1], double (*sW)[NB + 1]) {
+  const int tid = threadIdx.x;
+  for (int cb = c_begin; cb < c_end; cb += NB) {
+    const int cw = min(NB, c_end - cb);
+    // W = V^T X  (jb x cw), accumulated over 32-row chunks
+    double acc[4] = {0, 0, 0, 0};
+    for (int rb = j0; rb < m; rb += NB) {
+      const int rh = min(NB, m - rb);
+      for (int e = tid; e < NB * NB; e += QR_THREADS) {
+        const int rr = e % NB, l = e / NB;
+        const int r = rb + rr;
+        double v = 0.0;
+        if (rr < rh && l < jb) {
+          const int dg = j0 + l;
+          v = (r > dg) ? A[r + (long long)(j0 + l) * lda] : (r == dg ? 1.0 : 0.0);
+        }
+        sV[rr][l] = v;
+        const int c = cb + l;
+        sX[rr][l] = (rr < rh && l < cw) ? X[(long long)r * rs + (long long)c * cs] : 0.0;
+      }
+      __syncthreads();
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int e = tid + q * QR_THREADS;  // 1024 entries (l, c)
+        const int l = e % NB, c = e / NB;
+        double s = acc[q];
+        for (int rr = 0; rr < NB; ++rr) s = fma(sV[rr][l], sX[rr][c], s);
+        acc[q] = s;
+      }
+      __syncthreads();
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int e = tid + q * QR_THREADS;
+      sW[e % NB][e / NB] = acc[q];
+    }
+    __syncthreads();
+    // W' = op(T) W
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int e = tid + q * QR_THREADS;
+      const int l = e % NB, c = e / NB;
+      double s = 0.0;
+      if (l < jb) {
+        if (transT) {
+          for (int p = 0; p <= l; ++p) s = fma(sT[p][l], sW[p][c], s);
+        } else {
+          for (int p = l; p < jb; ++p) s = fma(sT[l][p], sW[p][c], s);
+        }
+      }
+      acc[q] = s;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int e = tid + q * QR_THREADS;
+      sW[e % NB][e / NB] = acc[q];
+    }
+    __syncthreads();
+    // X -= V W'
+    for (int rb = j0; rb < m; rb += NB) {
+      const int rh = min(NB, m - rb);
+      for (int e = tid; e < NB * NB; e += QR_THREADS) {
+        const int rr = e % NB, l = e / NB;
+        const int r = rb + rr;
+        double v = 0.0;
+        if (rr < rh && l < jb) {
+          const int dg = j0 + l;
+          v = (r > dg) ? A[r + (long long)(j0 + l) * lda] : (r == dg ? 1.0 : 0.0);
+        }
+        sV[rr][l] = v;
+      }
+      __syncthreads();
+      for (int e = tid; e < NB * NB; e += QR_THREADS) {
+        const int rr = e % NB, c = e / NB;
+        if (rr < rh && c < cw) {
+          double s = 0.0;
+          for (int l = 0; l < jb; ++l) s = fma(sV[rr][l], sW[l][c], s);
+          X[(long long)(rb + rr) * rs + (long long)(cb + c) * cs] -= s;
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
+__global__ void __launch_bounds__(QR_THREADS) qr_kernel(const QRDesc *__restrict__ descs) {
+  const QRDesc g = descs[blockIdx.x];
+  const int m = g.m, n = g.n, kmin = min(m, n);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int NW = QR_THREADS / 32;
+  __shared__ double red[32];
+  __shared__ double sT[NB][NB + 1];
+  __shared__ double sG[NB][NB + 1];
+  __shared__ double sV[NB][NB + 1], sX[NB][NB + 1], sW[NB][NB + 1];
+  __shared__ double s_tau, s_scal, s_beta;
+  double *A = g.A;
+  const long long lda = g.lda;
+  // copy input into the working matrix
+  for (long long e = tid; e < (long long)m * n; e += QR_THREADS) {
+    const int r = (int)(e % m), c = (int)(e / m);
+    A[r + c * lda] = g.src[r * g.src_rs + c * g.src_cs];
+  }
+  __syncthreads();
+
+  for (int j0 = 0; j0 < kmin; j0 += NB) {
+    const int jb = min(NB, kmin - j0);
+    // ---- panel factorisation (unblocked, Householder per column)
+    for (int jj = 0; jj < jb; ++jj) {
+      const int j = j0 + jj;
+      double *col = A + (long long)j * lda;
+      double part = 0.0;
+      for (int i = j + 1 + tid; i < m; i += QR_THREADS) part = fma(col[i], col[i], part);
+      const double sigma = block_sum(part, red);
+      if (tid == 0) {
+        const double alpha = col[j];
+        double tau = 0.0, scal = 0.0, beta = alpha;
+        if (sigma > 0.0) {
+          const double nrm = sqrt(fma(alpha, alpha, sigma));
+          beta = alpha >= 0.0 ? -nrm : nrm;
+          tau = (beta - alpha) / beta;
+          scal = 1.0 / (alpha - beta);
+        }
+        s_tau = tau;
+        s_scal = scal;
+        s_beta = beta;
+        g.tau[j] = tau;
+      }
+      __syncthreads();
+      const double tau = s_tau;
+      if (tau != 0.0) {
+        const double scal = s_scal;
+        for (int i = j + 1 + tid; i < m; i += QR_THREADS) col[i] *= scal;
+      }
+      __syncthreads();
+      if (tid == 0) col[j] = s_beta;
+      if (tau != 0.0) {
+        for (int c = j + 1 + warp; c < j0 + jb; c += NW) {
+          double *cc = A + (long long)c * lda;
+          double w = 0.0;
+          for (int i = j + lane; i < m; i += 32) w = fma(i == j ? 1.0 : col[i], cc[i], w);
+          w = warp_sum(w) * tau;
+          for (int i = j + lane; i < m; i += 32) cc[i] -= w * (i == j ? 1.0 : col[i]);
+        }
+      }
+      __syncthreads();
+    }
+    // ---- T factor (larft, forward, columnwise): T upper triangular jb x jb
+    //      G[l][i] = v_l^T v_i for l < i
+    for (int pidx = warp; pidx < jb * jb; pidx += NW) {
+      const int l = pidx % jb, i = pidx / jb;
+      if (l < i) {
+        const double *vl = A + (long long)(j0 + l) * lda;
+        const double *vi = A + (long long)(j0 + i) * lda;
+        double s = 0.0;
+        for (int r = j0 + i + 1 + lane; r < m; r += 32) s = fma(vl[r], vi[r], s);
+        s = warp_sum(s);
+        if (lane == 0) sG[l][i] = s + vl[j0 + i];
+      }
+    }
+    for (int e = tid; e < NB * (NB + 1); e += QR_THREADS) (&sT[0][0])[e] = 0.0;
+    __syncthreads();
+    if (warp == 0) {
+      for (int i = 0; i < jb; ++i) {
+        const double ti = g.tau[j0 + i];
+        // T[c][i] = -tau_i * sum_{l=c}^{i-1} T[c][l] G[l][i]
+        double v = 0.0;
+        if (lane < i) {
+          for (int l = lane; l < i; ++l) v = fma(sT[lane][l], sG[l][i], v);
+          v = -ti * v;
+        }
+        __syncwarp();
+        if (lane < i) sT[lane][i] = v;
+        if (lane == 0) sT[i][i] = ti;
+        __syncwarp();
+      }
+    }
+    __syncthreads();
+    // keep T for the Q formation
+    double *Tg = g.T + (long long)(j0 / NB) * NB * NB;
+    for (int e = tid; e < NB * NB; e += QR_THREADS) Tg[e] = sT[e % NB][e / NB];
+    __syncthreads();
+    // ---- trailing update: A[:, j0+jb:n] <- (I - V T V^T)^T A = A - V T^T (V^T A)
+    if (j0 + jb < n)
+      apply_block_reflector(m, j0, jb, A, lda, sT, 1, A, 1, lda, j0 + jb, n, sV, sX, sW);
+    __syncthreads();
+  }
+  // ---- R
+  if (g.R) {
+    for (long long e = tid; e < (long long)kmin * n; e += QR_THREADS) {
+      const int r = (int)(e % kmin), c = (int)(e / kmin);
+      g.R[r + c * g.ldr] = (c >= r) ? A[r + c * lda] : 0.0;
+    }
+  }
+  // ---- explicit Q = H_1 ... H_k [I; 0]  (orgqr, backward over panels)
+  if (g.Q) {
+    for (long long e = tid; e < (long long)m * kmin; e += QR_THREADS) {
+      const int r = (int)(e % m), c = (int)(e / m);
+      g.Q[r * g.q_rs + c * g.q_cs] = (r == c) ? 1.0 : 0.0;
+    }
+    __syncthreads();
+    const int npan = (kmin + NB - 1) / NB;
+    for (int pnl = npan - 1; pnl >= 0; --pnl) {
+      const int j0 = pnl * NB, jb = min(NB, kmin - j0);
+      const double *Tg = g.T + (long long)pnl * NB * NB;
+      for (int e = tid; e < NB * NB; e += QR_THREADS) sT[e % NB][e / NB] = Tg[e];
+      __syncthreads();
+      apply_block_reflector(m, j0, jb, A, lda, sT, 0, g.Q, g.q_rs, g.q_cs, j0, kmin, sV, sX, sW);
+      __syncthreads();
+    }
+  }
+}
+
+// ------------------------------------------------------------ Jacobi SVD ---
+constexpr int SVD_THREADS = 256;
+
+__device__ void jacobi_core(int m, int p, double *W, long long ldw, double *V, long long ldv, double *s_sig,
+                            int *s_pos, int *flag, int *sweeps_out) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int NW = SVD_THREADS / 32;
+  const int P2 = p + (p & 1);  // even number of players (a phantom player is skipped)
+  const double tol = 4.0 * DBL_EPSILON;
+  int sweep = 0;
+  for (; sweep < 60; ++sweep) {
+    if (tid == 0) *flag = 0;
+    __syncthreads();
+    for (int rnd = 0; rnd < P2 - 1; ++rnd) {
+      for (int pr = warp; pr < P2 / 2; pr += NW) {
+        int a, b;
+        if (pr == 0) {
+          a = P2 - 1;
+          b = rnd;
+        } else {
+          a = (rnd + pr) % (P2 - 1);
+          b = (rnd - pr + (P2 - 1)) % (P2 - 1);
+        }
+        if (a >= p || b >= p) continue;
+        if (a > b) { int t = a; a = b; b = t; }
+        double *wa = W + (long long)a * ldw, *wb = W + (long long)b * ldw;
+        double al = 0.0, be = 0.0, ga = 0.0;
+        for (int r = lane; r < m; r += 32) {
+          const double x = wa[r], y = wb[r];
+          al = fma(x, x, al);
+          be = fma(y, y, be);
+          ga = fma(x, y, ga);
+        }
+        al = warp_sum(al);
+        be = warp_sum(be);
+        ga = warp_sum(ga);
+        if (ga == 0.0 || al == 0.0 || be == 0.0) continue;
+        if (fabs(ga) <= tol * sqrt(al) * sqrt(be)) continue;
+        const double zeta = (be - al) / (2.0 * ga);
+        const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(fma(zeta, zeta, 1.0)));
+        const double c = 1.0 / sqrt(fma(t, t, 1.0)), s = c * t;
+        for (int r = lane; r < m; r += 32) {
+          const double x = wa[r], y = wb[r];
+          wa[r] = c * x - s * y;
+          wb[r] = s * x + c * y;
+        }
+        double *va = V + (long long)a * ldv, *vb = V + (long long)b * ldv;
+        for (int r = lane; r < p; r += 32) {
+          const double x = va[r], y = vb[r];
+          va[r] = c * x - s * y;
+          vb[r] = s * x + c * y;
+        }
+        if (lane == 0) *flag = 1;
+      }
+      __syncthreads();
+    }
+    if (*flag == 0) break;
+    __syncthreads();
+  }
+  if (tid == 0 && sweeps_out) *sweeps_out = sweep + 1;
+  // singular values = column norms
+  for (int c = warp; c < p; c += NW) {
+    const double *w = W + (long long)c * ldw;
+    double s = 0.0;
+    for (int r = lane; r < m; r += 32) s = fma(w[r], w[r], s);
+    s = warp_sum(s);
+    if (lane == 0) s_sig[c] = sqrt(s);
+  }
+  __syncthreads();
+  // rank sort: position of column i in decreasing order (ties by index)
+  for (int i = tid; i < p; i += SVD_THREADS) {
+    const double si = s_sig[i];
+    int pos = 0;
+    for (int j = 0; j < p; ++j) {
+      const double sj = s_sig[j];
+      pos += (sj > si) || (sj == si && j < i);
+    }
+    s_pos[i] = pos;
+  }
+  __syncthreads();
+}
+
+template <bool SMEM>
+__global__ void __launch_bounds__(SVD_THREADS) jacobi_kernel(const SVDDesc *__restrict__ descs) {
+  extern __shared__ __align__(16) double dsm[];
+  __shared__ int s_flag;
+  const SVDDesc g = descs[blockIdx.x];
+  const int m = g.m, p = g.p, tid = threadIdx.x;
+  double *W, *V;
+  long long ldw, ldv;
+  double *s_sig;
+  int *s_pos;
+  if (SMEM) {
+    W = dsm;
+    ldw = m;
+    V = dsm + (long long)m * p;
+    ldv = p;
+    s_sig = V + (long long)p * p;
+    s_pos = reinterpret_cast<int *>(s_sig + p);
+  } else {
+    W = g.work;
+    ldw = m;
+    V = g.work + (long long)m * p;
+    ldv = p;
+    s_sig = dsm;
+    s_pos = reinterpret_cast<int *>(dsm + p);
+  }
+  for (long long e = tid; e < (long long)m * p; e += SVD_THREADS) {
+    const int r = (int)(e % m), c = (int)(e / m);
+    W[r + c * ldw] = g.W[r + c * g.ldw];
+  }
+  for (long long e = tid; e < (long long)p * p; e += SVD_THREADS) {
+    const int r = (int)(e % p), c = (int)(e / p);
+    V[r + c * ldv] = (r == c) ? 1.0 : 0.0;
+  }
+  __syncthreads();
+  jacobi_core(m, p, W, ldw, V, ldv, s_sig, s_pos, &s_flag, g.sweeps_out);
+  // sorted outputs
+  for (long long e = tid; e < (long long)m * p; e += SVD_THREADS) {
+    const int r = (int)(e % m), c = (int)(e / m);
+    const double sc = s_sig[c];
+    g.U[r + (long long)s_pos[c] * g.ldu] = sc > 0.0 ? W[r + c * ldw] / sc : 0.0;
+  }
+  for (long long e = tid; e < (long long)p * p; e += SVD_THREADS) {
+    const int r = (int)(e % p), c = (int)(e / p);
+    g.V[r + (long long)s_pos[c] * g.ldv] = V[r + c * ldv];
+  }
+  for (int c = tid; c < p; c += SVD_THREADS) g.sigma[s_pos[c]] = s_sig[c];
+}
+
+}  // namespace
+
+tt_status launch_qr(const QRDesc *descs_dev, int count, cudaStream_t s) {
+  if (count <= 0) return TT_OK;
+  qr_kernel<<<count, QR_THREADS, 0, s>>>(descs_dev);
+  return check_launch("qr");
+}
+
+static size_t svd_smem_bytes(int mcap, int pcap) {
+  return ((size_t)mcap * pcap + (size_t)pcap * pcap + pcap) * sizeof(double) + (size_t)pcap * sizeof(int) + 16;
+}
+
+tt_status launch_jacobi(const SVDDesc *descs_dev, int count, int mcap, int pcap, cudaStream_t s) {
+  if (count <= 0) return TT_OK;
+  const size_t smem = svd_smem_bytes(mcap, pcap);
+  const size_t limit = 220 * 1024;
+  if (smem <= limit) {
+    static bool attr_set = false;
+    if (!attr_set) {
+      cudaFuncSetAttribute(jacobi_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)limit);
+      attr_set = true;
+    }
+    jacobi_kernel<true><<<count, SVD_THREADS, smem, s>>>(descs_dev);
+  } else {
+    const size_t sm2 = (size_t)pcap * (sizeof(double) + sizeof(int)) + 16;
+    if (sm2 > 48 * 1024) {
+      cudaFuncSetAttribute(jacobi_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)limit);
+    }
+    jacobi_kernel<false><<<count, SVD_THREADS, sm2, s>>>(descs_dev);
+  }
+  return check_launch("jacobi");
+}
+
+}  // namespace tt

@@ -1,0 +1,156 @@
+// Internal definitions shared by the libtt translation units (sm_100a, fp64).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stddef.h>
+#include <string>
+
+#include "tt.h"
+
+namespace tt {
+
+// Host-side shape of a TT-vector / TT-matrix, passed to kernels BY VALUE (it
+// is captured into CUDA graphs with the launch).  Ranks stay on the device.
+struct VecMeta {
+  int d;
+  int n[TT_MAX_D];
+  int rcap[TT_MAX_D + 1];
+  long long off[TT_MAX_D];
+  double *data;
+  int *r;  // device ranks [d+1]
+};
+
+struct MatMeta {
+  int d;
+  int m[TT_MAX_D];
+  int n[TT_MAX_D];
+  int Rcap[TT_MAX_D + 1];
+  long long off[TT_MAX_D];
+  double *data;
+  int *R;  // device ranks [d+1]
+};
+
+// ---------------------------------------------------------------- errors ---
+void set_error(const std::string &msg);
+tt_status fail(tt_status st, const std::string &msg);
+tt_status check_launch(const char *what);
+
+#define TT_TRY(expr)                    \
+  do {                                  \
+    tt_status _st = (expr);             \
+    if (_st != TT_OK) return _st;       \
+  } while (0)
+
+// ----------------------------------------------------------- workspace ---
+// Bump allocator over the caller's workspace.  With base == nullptr it only
+// counts (used by the *_workspace size queries, which run the same plan).
+struct Arena {
+  char *base = nullptr;
+  size_t cap = 0;
+  size_t used = 0;
+  template <class T>
+  T *take(size_t count) {
+    size_t bytes = ((count * sizeof(T)) + 255) & ~size_t(255);
+    T *p = base ? reinterpret_cast<T *>(base + used) : nullptr;
+    used += bytes;
+    return p;
+  }
+  bool ok() const { return base == nullptr || used <= cap; }
+};
+
+// ----------------------------------------------------------------- GEMM ---
+// C[M x N] = alpha op(A)[M x K] op(B)[K x N] + beta C, fp64, column-major A, B.
+// C is written through a two-level scatter: row r = r0 + dr r1 (r0 < dr),
+// col c = c0 + dc c1, address = r0 s_r0 + r1 s_r1 + c0 s_c0 + c1 s_c1 — this
+// lets every tensor-contraction stage write its output directly in the layout
+// the next stage reads as a plain matrix.  The descriptor lives in device
+// memory so that sizes can follow device-resident ranks.
+struct GemmDesc {
+  int M, N, K;
+  int transA, transB;
+  long long lda, ldb;
+  const double *A;
+  const double *B;
+  double *C;
+  int dr, dc;
+  long long s_r0, s_r1, s_c0, s_c1;
+  double alpha, beta;
+  const double *alpha_dev;  // if non-null, alpha *= *alpha_dev
+};
+
+__host__ __device__ inline void gemm_plain_c(GemmDesc &g, double *C, long long ldc) {
+  g.C = C;
+  g.dr = 1 << 30;
+  g.s_r0 = 1;
+  g.s_r1 = 0;
+  g.dc = 1 << 30;
+  g.s_c0 = ldc;
+  g.s_c1 = 0;
+}
+
+// Launch `count` GEMMs described at descs_dev[0..count) with a grid sized for
+// Mcap x Ncap (tiles beyond the device-side M, N exit immediately).
+tt_status launch_gemm(const GemmDesc *descs_dev, int count, int Mcap, int Ncap, cudaStream_t s);
+
+// ------------------------------------------------------------- linalg ---
+// Householder QR of an m x n column-major matrix (one CTA per problem,
+// blocked with panel width 32, compact-WY trailing updates, explicit Q).
+struct QRDesc {
+  int m, n;              // device-side sizes (written by a plan kernel)
+  const double *src;     // input element (r, c) = src[r*src_rs + c*src_cs]
+  long long src_rs, src_cs;
+  double *A;             // workspace copy (lda >= m): R above, V below the diagonal
+  long long lda;
+  double *Q;             // out: explicit Q, m x min(m,n); element (r,c) at Q[r*q_rs + c*q_cs]
+  long long q_rs, q_cs;
+  double *R;             // out: R, min(m,n) x n, column-major (ldr); may be nullptr
+  long long ldr;
+  double *tau;           // workspace >= min(m,n)
+  double *T;             // workspace >= 32*32 * ceil(min(m,n)/32)
+};
+tt_status launch_qr(const QRDesc *descs_dev, int count, cudaStream_t s);
+
+// One-sided (Hestenes) Jacobi SVD of an m x p matrix W (m >= p), one CTA.
+// Outputs sorted by decreasing sigma: U (m x p, unit columns; zero columns for
+// sigma = 0), V (p x p), sigma (p).  W is read only.  work >= (m + p) p doubles
+// (used only when the problem does not fit in shared memory).
+struct SVDDesc {
+  int m, p;
+  const double *W; long long ldw;
+  double *U; long long ldu;
+  double *V; long long ldv;
+  double *sigma;
+  double *work;
+  int *sweeps_out;
+};
+tt_status launch_jacobi(const SVDDesc *descs_dev, int count, int mcap, int pcap, cudaStream_t s);
+
+// Strided 2-D copy with device-side sizes and strides.
+struct CopyDesc {
+  int rows, cols;
+  const double *src; long long ss_r, ss_c;
+  double *dst; long long ds_r, ds_c;
+};
+tt_status launch_copy(const CopyDesc *descs_dev, int count, long long cap_elems, cudaStream_t s);
+
+// ----------------------------------------------------------- TT helpers ---
+tt_status make_vec_meta(const tt_vec *x, VecMeta &m);
+tt_status make_mat_meta(const tt_mat *A, MatMeta &m);
+VecMeta mat_as_vec(const MatMeta &A);
+
+// Internal operations on metas (used by the drivers; the ABI wraps them).
+tt_status matvec_meta(const MatMeta &A, const VecMeta &x, const VecMeta &y, cudaStream_t s);
+tt_status add_meta(const VecMeta &x, const double *alpha, const VecMeta &y, const double *beta,
+                   const VecMeta &z, cudaStream_t s);
+tt_status scale_meta(const VecMeta &x, const double *alpha_dev, double alpha_host, int invert,
+                     cudaStream_t s);
+tt_status copy_meta(const VecMeta &x, const VecMeta &y, cudaStream_t s);
+tt_status dot_meta(const VecMeta &x, const VecMeta &y, double *out, Arena &ar, cudaStream_t s);
+tt_status orth_meta(const VecMeta &x, int dir, double *norm_dev, Arena &ar, cudaStream_t s);
+tt_status round_meta(const VecMeta &x, double eps, int rmax, double *disc, double *sv, int sv_stride,
+                     Arena &ar, cudaStream_t s);
+
+int max_slot(const VecMeta &x);      // max_k rcap[k] n_k rcap[k+1]
+int max_rank(const VecMeta &x);
+
+}  // namespace tt

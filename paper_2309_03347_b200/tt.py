@@ -1,0 +1,249 @@
+"""Thin Python binding over libtt (include/tt.h): device containers on torch
+tensors and functions with the C-ABI names.  Argument marshalling only —
+every step of the hot path runs in the CUDA kernels of libtt.so.
+
+TT-vector cores are column-major [r_k, n_k, r_{k+1}] stored compactly at the
+start of rank-capacity slots; ranks are device int32 (include/tt.h)."""
+from __future__ import annotations
+
+import ctypes as C
+from typing import List, Optional, Sequence
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import TTError, check, lib
+
+F64 = torch.float64
+
+
+def _stream(stream=None) -> int:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+def _ptr(t: Optional[torch.Tensor]):
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+class _Workspace:
+    """Grow-only device scratch buffer (uint8 tensor) shared by calls."""
+
+    def __init__(self):
+        self.buf = None
+
+    def get(self, nbytes: int, device) -> torch.Tensor:
+        nbytes = max(int(nbytes), 256)
+        if self.buf is None or self.buf.numel() < nbytes or self.buf.device != device:
+            self.buf = torch.empty(nbytes, dtype=torch.uint8, device=device)
+        return self.buf
+
+
+_WS = _Workspace()
+
+
+def workspace(nbytes: int, device="cuda") -> torch.Tensor:
+    return _WS.get(nbytes, torch.device(device))
+
+
+class TTVec:
+    """TT-vector in device memory with rank-capacity slots."""
+
+    def __init__(self, n: Sequence[int], rcap: Sequence[int], device="cuda"):
+        self.d = len(n)
+        self.n = [int(v) for v in n]
+        self.rcap = [int(v) for v in rcap]
+        assert len(self.rcap) == self.d + 1 and self.rcap[0] == 1 and self.rcap[-1] == 1
+        sizes = [self.rcap[k] * self.n[k] * self.rcap[k + 1] for k in range(self.d)]
+        self.off = [int(v) for v in np.concatenate([[0], np.cumsum(sizes)[:-1]])]
+        self.device = torch.device(device)
+        self.data = torch.zeros(int(sum(sizes)), dtype=F64, device=self.device)
+        self.r_dev = torch.ones(self.d + 1, dtype=torch.int32, device=self.device)
+        self._n = (C.c_int32 * self.d)(*self.n)
+        self._rcap = (C.c_int32 * (self.d + 1))(*self.rcap)
+        self._off = (C.c_int64 * self.d)(*self.off)
+        self._c = _lib.tt_vec(self.d, self._n, self.r_dev.data_ptr(), self._rcap, self.data.data_ptr(), self._off)
+
+    @property
+    def c(self):
+        return C.byref(self._c)
+
+    @classmethod
+    def from_cores(cls, cores: List[np.ndarray], rcap: Optional[Sequence[int]] = None, device="cuda"):
+        n = [c.shape[1] for c in cores]
+        r = [c.shape[0] for c in cores] + [cores[-1].shape[2]]
+        if rcap is None:
+            rcap = r
+        rcap = [max(int(a), int(b)) for a, b in zip(rcap, r)]
+        v = cls(n, rcap, device)
+        v.set_cores(cores)
+        return v
+
+    def set_cores(self, cores: List[np.ndarray]):
+        r = [c.shape[0] for c in cores] + [cores[-1].shape[2]]
+        host = torch.zeros(self.data.numel(), dtype=F64)
+        for k, c in enumerate(cores):
+            assert c.shape[1] == self.n[k] and c.shape[0] <= self.rcap[k] and c.shape[2] <= self.rcap[k + 1]
+            flat = torch.from_numpy(np.ascontiguousarray(np.asarray(c, dtype=np.float64).reshape(-1, order="F")))
+            host[self.off[k]:self.off[k] + flat.numel()] = flat
+        self.data.copy_(host)
+        self.r_dev.copy_(torch.tensor(r, dtype=torch.int32))
+
+    def ranks(self) -> List[int]:
+        return [int(v) for v in self.r_dev.cpu()]
+
+    def cores(self) -> List[np.ndarray]:
+        r = self.ranks()
+        host = self.data.cpu().numpy()
+        out = []
+        for k in range(self.d):
+            size = r[k] * self.n[k] * r[k + 1]
+            out.append(host[self.off[k]:self.off[k] + size].reshape(r[k], self.n[k], r[k + 1], order="F").copy())
+        return out
+
+
+class TTMat:
+    """TT-matrix in device memory; cores [R_k, m_k, n_k, R_{k+1}] column-major."""
+
+    def __init__(self, m: Sequence[int], n: Sequence[int], Rcap: Sequence[int], device="cuda"):
+        self.d = len(m)
+        self.m = [int(v) for v in m]
+        self.n = [int(v) for v in n]
+        self.Rcap = [int(v) for v in Rcap]
+        sizes = [self.Rcap[k] * self.m[k] * self.n[k] * self.Rcap[k + 1] for k in range(self.d)]
+        self.off = [int(v) for v in np.concatenate([[0], np.cumsum(sizes)[:-1]])]
+        self.device = torch.device(device)
+        self.data = torch.zeros(int(sum(sizes)), dtype=F64, device=self.device)
+        self.R_dev = torch.ones(self.d + 1, dtype=torch.int32, device=self.device)
+        self._m = (C.c_int32 * self.d)(*self.m)
+        self._n = (C.c_int32 * self.d)(*self.n)
+        self._Rcap = (C.c_int32 * (self.d + 1))(*self.Rcap)
+        self._off = (C.c_int64 * self.d)(*self.off)
+        self._c = _lib.tt_mat(self.d, self._m, self._n, self.R_dev.data_ptr(), self._Rcap,
+                              self.data.data_ptr(), self._off)
+        # the same storage viewed as a TT-vector with mode m_k n_k (row index fastest)
+        self._mn = (C.c_int32 * self.d)(*[a * b for a, b in zip(self.m, self.n)])
+        self._vc = _lib.tt_vec(self.d, self._mn, self.R_dev.data_ptr(), self._Rcap, self.data.data_ptr(), self._off)
+
+    @property
+    def c(self):
+        return C.byref(self._c)
+
+    @property
+    def as_vec_c(self):
+        return C.byref(self._vc)
+
+    @classmethod
+    def from_cores(cls, cores: List[np.ndarray], Rcap=None, device="cuda"):
+        m = [c.shape[1] for c in cores]
+        n = [c.shape[2] for c in cores]
+        R = [c.shape[0] for c in cores] + [cores[-1].shape[3]]
+        Rcap = R if Rcap is None else [max(int(a), int(b)) for a, b in zip(Rcap, R)]
+        A = cls(m, n, Rcap, device)
+        A.set_cores(cores)
+        return A
+
+    def set_cores(self, cores):
+        R = [c.shape[0] for c in cores] + [cores[-1].shape[3]]
+        host = torch.zeros(self.data.numel(), dtype=F64)
+        for k, c in enumerate(cores):
+            flat = torch.from_numpy(np.ascontiguousarray(np.asarray(c, dtype=np.float64).reshape(-1, order="F")))
+            host[self.off[k]:self.off[k] + flat.numel()] = flat
+        self.data.copy_(host)
+        self.R_dev.copy_(torch.tensor(R, dtype=torch.int32))
+
+    def ranks(self):
+        return [int(v) for v in self.R_dev.cpu()]
+
+    def cores(self):
+        R = self.ranks()
+        host = self.data.cpu().numpy()
+        out = []
+        for k in range(self.d):
+            size = R[k] * self.m[k] * self.n[k] * R[k + 1]
+            out.append(host[self.off[k]:self.off[k] + size].reshape(R[k], self.m[k], self.n[k], R[k + 1],
+                                                                     order="F").copy())
+        return out
+
+
+# ------------------------------------------------------------ operations ---
+
+def tt_matvec(A: TTMat, x: TTVec, y: TTVec, stream=None):
+    check(lib().tt_matvec(A.c, x.c, y.c, C.c_void_p(_stream(stream))))
+    return y
+
+
+def matvec_out(A: TTMat, x: TTVec) -> TTVec:
+    """Allocate y with capacities R*r and compute y = A x."""
+    y = TTVec(A.m, [a * b for a, b in zip(A.Rcap, x.rcap)], A.device)
+    return tt_matvec(A, x, y)
+
+
+def tt_add(x: TTVec, y: TTVec, z: TTVec, alpha: Optional[torch.Tensor] = None,
+           beta: Optional[torch.Tensor] = None, stream=None):
+    check(lib().tt_add(x.c, _ptr(alpha), y.c, _ptr(beta), z.c, C.c_void_p(_stream(stream))))
+    return z
+
+
+def tt_scale(x: TTVec, alpha: torch.Tensor, stream=None):
+    check(lib().tt_scale(x.c, _ptr(alpha), C.c_void_p(_stream(stream))))
+    return x
+
+
+def tt_copy(x: TTVec, y: TTVec, stream=None):
+    check(lib().tt_copy(x.c, y.c, C.c_void_p(_stream(stream))))
+    return y
+
+
+def tt_dot(x: TTVec, y: TTVec, out: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+    if out is None:
+        out = torch.zeros(1, dtype=F64, device=x.device)
+    nb = lib().tt_dot_workspace(x.c, y.c)
+    ws = workspace(nb, x.device)
+    check(lib().tt_dot(x.c, y.c, _ptr(out), _ptr(ws), ws.numel(), C.c_void_p(_stream(stream))))
+    return out
+
+
+def tt_orthogonalize(x: TTVec, direction: int = -1, norm: Optional[torch.Tensor] = None, stream=None):
+    if norm is None:
+        norm = torch.zeros(1, dtype=F64, device=x.device)
+    nb = lib().tt_orthogonalize_workspace(x.c)
+    ws = workspace(nb, x.device)
+    check(lib().tt_orthogonalize(x.c, int(direction), _ptr(norm), _ptr(ws), ws.numel(),
+                                 C.c_void_p(_stream(stream))))
+    return norm
+
+
+def tt_round(x: TTVec, eps: float, rmax: int = 1 << 30, want_info: bool = False, stream=None):
+    disc = sv = None
+    stride = 0
+    if want_info:
+        disc = torch.zeros(max(x.d - 1, 1), dtype=F64, device=x.device)
+        stride = max(x.rcap)
+        sv = torch.zeros(max(x.d - 1, 1) * stride, dtype=F64, device=x.device)
+    nb = lib().tt_round_workspace(x.c)
+    ws = workspace(nb, x.device)
+    check(lib().tt_round(x.c, float(eps), int(min(rmax, 2**31 - 1)), _ptr(disc), _ptr(sv), int(stride),
+                         _ptr(ws), ws.numel(), C.c_void_p(_stream(stream))))
+    if want_info:
+        return x, disc, sv.view(max(x.d - 1, 1), stride)
+    return x
+
+
+def als_local_apply(dims, Phi, Ak, Psi, x, y, stream=None):
+    """dims = (rA, R, rB, m, n, rAp, Rp, rBp); arrays are flat device tensors."""
+    nb = lib().als_workspace(*dims)
+    ws = workspace(nb, x.device)
+    check(lib().als_local_apply(*[int(v) for v in dims], _ptr(Phi), _ptr(Ak), _ptr(Psi), _ptr(x), _ptr(y),
+                                _ptr(ws), ws.numel(), C.c_void_p(_stream(stream))))
+    return y
+
+
+def als_update_interfaces(direction, dims, Iprev, Yk, Ak, Xk, Inext, stream=None):
+    """dims = (rY, R, rX, m, n, rYp, Rp, rXp); Ak = None for the vector interface."""
+    nb = lib().als_workspace(*dims)
+    ws = workspace(nb, Yk.device)
+    check(lib().als_update_interfaces(int(direction), *[int(v) for v in dims], _ptr(Iprev), _ptr(Yk), _ptr(Ak),
+                                      _ptr(Xk), _ptr(Inext), _ptr(ws), ws.numel(), C.c_void_p(_stream(stream))))
+    return Inext

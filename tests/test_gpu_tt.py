@@ -1,0 +1,255 @@
+"""GPU parity of the TT kernels (libtt via the C ABI) against the fp64 oracle.
+Tolerances follow BASELINE.json north_star / SURVEY.md §8(c).5."""
+import math
+
+import numpy as np
+import pytest
+
+import inputs
+from oracle import tt as ott
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a GPU", allow_module_level=True)
+
+import paper_2309_03347_b200 as tb  # noqa: E402
+
+
+def rel(a, b):
+    return np.linalg.norm(np.asarray(a) - np.asarray(b)) / max(np.linalg.norm(np.asarray(b)), 1e-300)
+
+
+def tt_diff_norm(X, Y):
+    """||X - Y||_F through the oracle (QR orthogonalisation of the concatenation,
+    no <a,a> - 2<a,b> + <b,b> cancellation)."""
+    D = ott.tt_add(X, ott.tt_scale(Y, -1.0))
+    _, nrm = ott.tt_orthogonalize_rl(D)
+    return nrm
+
+
+# ------------------------------------------------------------------ a1 ---
+
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_matvec_c2_core_exact(seed):
+    inst = inputs.c2_instance(seed)
+    A = tb.TTMat.from_cores(inst["A"])
+    X = tb.TTVec.from_cores(inst["X"])
+    Y = tb.matvec_out(A, X)
+    torch.cuda.synchronize()
+    ref = ott.tt_matvec_fast(inst["A"], inst["X"])
+    got = Y.cores()
+    assert Y.ranks() == ott.ranks(ref)                          # ranks multiply
+    for g, r in zip(got, ref):
+        assert g.shape == r.shape
+        assert np.max(np.abs(g - r)) <= 1e-14 * max(np.max(np.abs(r)), 1e-300)
+
+
+def test_matvec_d10_dense():
+    inst = inputs.c2_slice(100)
+    A = tb.TTMat.from_cores(inst["A"])
+    X = tb.TTVec.from_cores(inst["X"])
+    Y = tb.matvec_out(A, X)
+    dense = ott.ttm_full(inst["A"]) @ ott.tt_full(inst["X"])
+    assert rel(ott.tt_full(Y.cores()), dense) <= 1e-12
+
+
+def test_matvec_edge_shapes():
+    g = inputs.rng(40)
+    # d = 1, rectangular modes, big modes (80 angles, 7 groups), rank-1 pieces
+    cases = [([3], [5], [1, 1], [1, 1]),
+             ([2, 7, 3], [3, 7, 2], [1, 2, 3, 1], [1, 1, 4, 1]),
+             ([2, 80, 7], [2, 80, 7], [1, 3, 2, 1], [1, 5, 3, 1])]
+    for rows, cols, R, r in cases:
+        A = inputs.random_ttm(g, rows, cols, R)
+        X = inputs.random_tt(g, cols, r)
+        Y = tb.matvec_out(tb.TTMat.from_cores(A), tb.TTVec.from_cores(X))
+        ref = ott.tt_matvec(A, X)
+        for a, b in zip(Y.cores(), ref):
+            assert np.max(np.abs(a - b)) <= 1e-13 * max(np.abs(b).max(), 1e-300)
+    # shape mismatch is a host-detected error
+    A = tb.TTMat.from_cores(inputs.random_ttm(g, [2, 2], [2, 3], [1, 2, 1]))
+    X = tb.TTVec.from_cores(inputs.random_tt(g, [2, 2], [1, 2, 1]))
+    with pytest.raises(tb.TTError) as e:
+        tb.matvec_out(A, X)
+    assert e.value.status == 2
+
+
+# ------------------------------------------------------------- a2, a8 ---
+
+def test_add_scale_dot_copy():
+    g = inputs.rng(41)
+    dims = [2, 3, 4, 2, 5]
+    X = inputs.random_tt(g, dims, [1, 2, 3, 2, 4, 1])
+    Y = inputs.random_tt(g, dims, [1, 3, 1, 4, 2, 1])
+    gx, gy = tb.TTVec.from_cores(X), tb.TTVec.from_cores(Y)
+    z = tb.TTVec(dims, [1, 5, 4, 6, 6, 1])
+    al = torch.tensor([0.5], dtype=torch.float64, device="cuda")
+    be = torch.tensor([-3.0], dtype=torch.float64, device="cuda")
+    tb.tt_add(gx, gy, z, al, be)
+    assert z.ranks() == [1, 5, 4, 6, 6, 1]
+    assert rel(ott.tt_full(z.cores()), 0.5 * ott.tt_full(X) - 3.0 * ott.tt_full(Y)) <= 1e-14
+    d = tb.tt_dot(gx, gy)
+    assert abs(d.item() - ott.tt_dot(X, Y)) <= 1e-13 * abs(ott.tt_dot(X, Y)) + 1e-14
+    tb.tt_scale(gx, be)
+    assert rel(ott.tt_full(gx.cores()), -3.0 * ott.tt_full(X)) <= 1e-15
+    c = tb.TTVec(dims, [1, 5, 5, 5, 5, 1])
+    tb.tt_copy(gy, c)
+    assert c.ranks() == ott.ranks(Y)
+    for a, b in zip(c.cores(), Y):
+        assert np.array_equal(a, b)
+    # d = 1
+    a1 = [g.standard_normal((1, 7, 1))]
+    b1 = [g.standard_normal((1, 7, 1))]
+    z1 = tb.TTVec([7], [1, 1])
+    tb.tt_add(tb.TTVec.from_cores(a1), tb.TTVec.from_cores(b1), z1, al, be)
+    assert np.allclose(z1.cores()[0], 0.5 * a1[0] - 3.0 * b1[0], atol=1e-15)
+
+
+# ------------------------------------------------------------------ a3 ---
+
+@pytest.mark.parametrize("direction", [-1, 1])
+def test_orthogonalize(direction):
+    inst = inputs.c2_slice(101)
+    Yc = ott.tt_matvec_fast(inst["A"], inst["X"])
+    G = tb.TTVec.from_cores(Yc)
+    nrm = tb.tt_orthogonalize(G, direction)
+    torch.cuda.synchronize()
+    O = G.cores()
+    full = ott.tt_full(Yc)
+    assert rel(ott.tt_full(O), full) <= 1e-13
+    assert abs(nrm.item() - np.linalg.norm(full)) <= 1e-13 * np.linalg.norm(full)
+    ref, _ = ott.tt_orthogonalize_rl(Yc) if direction < 0 else ott.tt_orthogonalize_lr(Yc)
+    assert G.ranks() == ott.ranks(ref)
+    rng_k = range(1, len(O)) if direction < 0 else range(len(O) - 1)
+    for k in rng_k:
+        r0, n, r1 = O[k].shape
+        if direction < 0:
+            M = O[k].reshape(r0, n * r1, order="F"); Gm = M @ M.T
+        else:
+            M = O[k].reshape(r0 * n, r1, order="F"); Gm = M.T @ M
+        assert np.max(np.abs(Gm - np.eye(Gm.shape[0]))) <= 1e-13      # Z23
+
+
+def test_orthogonalize_rank_deficient():
+    """A TT whose interior ranks exceed the attainable ranks (Z24) and a zero core."""
+    g = inputs.rng(42)
+    X = inputs.random_tt(g, [2, 2, 2, 2], [1, 6, 9, 6, 1])
+    G = tb.TTVec.from_cores(X)
+    tb.tt_orthogonalize(G, -1)
+    assert G.ranks() == ott.ranks(ott.tt_orthogonalize_rl(X)[0]) == [1, 6, 4, 2, 1]
+    assert rel(ott.tt_full(G.cores()), ott.tt_full(X)) <= 1e-13
+    Z = [np.zeros((1, 3, 2)), np.zeros((2, 3, 2)), np.zeros((2, 3, 1))]
+    G = tb.TTVec.from_cores(Z)
+    nrm = tb.tt_orthogonalize(G, -1)
+    assert nrm.item() == 0.0
+    for k in (1, 2):
+        c = G.cores()[k]
+        M = c.reshape(c.shape[0], -1, order="F")
+        assert np.max(np.abs(M @ M.T - np.eye(M.shape[0]))) <= 1e-13
+
+
+# ------------------------------------------------------------------ a4 ---
+
+@pytest.mark.parametrize("eps", [1e-1, 1e-3, 1e-8])
+def test_round_d10_vs_oracle(eps):
+    inst = inputs.c2_slice(102)
+    Yc = ott.tt_matvec_fast(inst["A"], inst["X"])
+    full = ott.tt_full(Yc)
+    G = tb.TTVec.from_cores(Yc)
+    _, disc, sv = tb.tt_round(G, eps, want_info=True)
+    torch.cuda.synchronize()
+    ref, info = ott.tt_round(Yc, eps)
+    got = G.cores()
+    assert G.ranks() == ott.ranks(ref)
+    s1 = max(s[0] for s in info["sv"])
+    for k, s in enumerate(info["sv"]):
+        assert np.max(np.abs(sv[k, :len(s)].cpu().numpy() - s)) <= 1e-12 * s1
+    nX = np.linalg.norm(full)
+    err = np.linalg.norm(ott.tt_full(got) - full)
+    assert err <= eps * nX * (1 + 1e-12) + 1e-12 * nX                        # eps bound (rmax not binding)
+    assert abs(err ** 2 - disc.sum().item()) <= 1e-10 * nX ** 2              # error identity
+    assert rel(ott.tt_full(got), ott.tt_full(ref)) <= 1e-12                  # same truncation as the oracle
+
+
+@pytest.mark.parametrize("seed", [0, 1])
+def test_round_c2_d30_rmax128(seed):
+    """BASELINE.json configs[1]: apply then round(eps=1e-8, rmax=128); compare bond
+    singular values (gauge invariant) and the rounded tensors via a TT difference."""
+    inst = inputs.c2_instance(seed)
+    A = tb.TTMat.from_cores(inst["A"])
+    X = tb.TTVec.from_cores(inst["X"])
+    Y = tb.matvec_out(A, X)
+    _, disc, sv = tb.tt_round(Y, 1e-8, 128, want_info=True)
+    torch.cuda.synchronize()
+    Yc = ott.tt_matvec_fast(inst["A"], inst["X"])
+    ref, info = ott.tt_round(Yc, 1e-8, 128)
+    assert Y.ranks() == ott.ranks(ref)
+    s1 = max(s[0] for s in info["sv"])
+    for k, s in enumerate(info["sv"]):
+        assert np.max(np.abs(sv[k, :len(s)].cpu().numpy() - s)) <= 1e-12 * s1
+    nrm = info["norm"]
+    # near-ties at the cut make the truncated subspace ill-determined: skip those bonds
+    ties = any(r < len(s) and abs(s[r - 1] - s[r]) <= 1e-10 * s1
+               for r, s in zip(ott.ranks(ref)[1:-1], info["sv"]))
+    if not ties:
+        assert tt_diff_norm(Y.cores(), ref) <= 1e-12 * nrm + math.sqrt(sum(info["discarded_sq"])) * 1e-6
+    assert max(Y.ranks()) <= 128
+
+
+def test_round_special_cases():
+    g = inputs.rng(43)
+    dims = [3, 4, 3, 2]
+    X = inputs.random_tt(g, dims, [1, 3, 4, 2, 1])
+    G = tb.TTVec.from_cores(X)
+    tb.tt_round(G, 0.0)
+    assert G.ranks() == ott.ranks(X)
+    XX = ott.tt_add(X, X)
+    G = tb.TTVec.from_cores(XX)
+    tb.tt_round(G, 1e-12)
+    assert G.ranks() == ott.ranks(X)
+    assert rel(ott.tt_full(G.cores()), 2 * ott.tt_full(X)) <= 1e-12
+
+
+# ------------------------------------------------------------- a5, a6 ---
+
+def _rand(g, *shape):
+    return g.standard_normal(shape)
+
+
+def _dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a.reshape(-1, order="F"))).cuda()
+
+
+@pytest.mark.parametrize("dims", [(3, 2, 4, 2, 3, 5, 3, 2), (16, 5, 16, 4, 4, 16, 6, 16), (64, 8, 64, 16, 16, 64, 7, 64),
+                                  (70, 5, 33, 2, 8, 65, 3, 31)])
+def test_local_apply_and_interfaces(dims):
+    rA, R, rB, m, n, rAp, Rp, rBp = dims
+    g = inputs.rng(44)
+    Phi = _rand(g, rA, R, rB); Ak = _rand(g, R, m, n, Rp); Psi = _rand(g, rAp, Rp, rBp); x = _rand(g, rB, n, rBp)
+    y = torch.zeros(rA * m * rAp, dtype=torch.float64, device="cuda")
+    tb.als_local_apply(dims, _dev(Phi), _dev(Ak), _dev(Psi), _dev(x), y)
+    ref = ott.local_apply(Phi, Ak, Psi, x)
+    assert rel(y.cpu().numpy(), ref.reshape(-1, order="F")) <= 1e-13
+    # left interface: Phi_k from (Phi, Y, A, X) with Y [rA, m, rAp], X [rB, n, rBp]
+    Y = _rand(g, rA, m, rAp)
+    out = torch.zeros(rAp * Rp * rBp, dtype=torch.float64, device="cuda")
+    tb.als_update_interfaces(+1, (rA, R, rB, m, n, rAp, Rp, rBp), _dev(Phi), _dev(Y), _dev(Ak), _dev(x), out)
+    ref = ott.left_update(Phi, Y, Ak, x)
+    assert rel(out.cpu().numpy(), ref.reshape(-1, order="F")) <= 1e-13
+    # right interface: Psi_k from (Psi_{k+1}, Y, A, X)
+    out = torch.zeros(rA * R * rB, dtype=torch.float64, device="cuda")
+    tb.als_update_interfaces(-1, (rA, R, rB, m, n, rAp, Rp, rBp), _dev(Psi), _dev(Y), _dev(Ak), _dev(x), out)
+    ref = ott.right_update(Psi, Y, Ak, x)
+    assert rel(out.cpu().numpy(), ref.reshape(-1, order="F")) <= 1e-13
+    # vector interfaces (A = None, R = Rp = 1, m = n)
+    B = _rand(g, rB, m, rBp)
+    phi = _rand(g, rA, rB)
+    out = torch.zeros(rAp * rBp, dtype=torch.float64, device="cuda")
+    tb.als_update_interfaces(+1, (rA, 1, rB, m, m, rAp, 1, rBp), _dev(phi), _dev(Y), None, _dev(B), out)
+    assert rel(out.cpu().numpy(), ott.left_update_vec(phi, Y, B).reshape(-1, order="F")) <= 1e-13
+    psi = _rand(g, rAp, rBp)
+    out = torch.zeros(rA * rB, dtype=torch.float64, device="cuda")
+    tb.als_update_interfaces(-1, (rA, 1, rB, m, m, rAp, 1, rBp), _dev(psi), _dev(Y), None, _dev(B), out)
+    assert rel(out.cpu().numpy(), ott.right_update_vec(psi, Y, B).reshape(-1, order="F")) <= 1e-13
