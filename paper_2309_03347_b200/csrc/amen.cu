@@ -1,0 +1,559 @@
+// amen_solve (a7): AMEn for A x = b in TT on the device (P:1481-1486,
+// P:1512-1531 "amen_solve"; reading Z20).  Alternating-direction sweeps; at
+// core k:
+//   rhs_k = phi^b_{k-1} b_k psi^b_{k+1};  solve (Phi_{k-1} A_k Psi_{k+1}) x_k = rhs_k
+//   with device GMRES (warm start x_k); the local residual before the solve is
+//   the sweep's stopping measure; SVD-truncate x_k; residual core z_k with z
+//   frames on both sides; enrich x_k with the residual projected on (x frames |
+//   z frames); QR; carry the rest into the neighbour; update the interface
+//   families xAx, xb, zAx, zb.
+// Both directions share one code path: the unfolding M is the left unfolding
+// (r0 n x r1) for left-to-right and the TRANSPOSED right unfolding (n r1 x r0)
+// for right-to-left, so "columns of M" are always the orthonormal side.
+// Every size follows device-resident ranks: one-thread plan kernels write the
+// GEMM / QR / SVD / copy descriptors; the host only enqueues launches (it polls
+// the GMRES flag once per cycle and the sweep residual once per sweep).
+#include <cmath>
+#include <cstring>
+#include <vector>
+
+#include "als.h"
+#include "amen.h"
+#include "gmres.h"
+
+namespace tt {
+
+namespace {
+
+constexpr int NG = 48;
+
+struct Dev {  // device-side view passed by value to the plan kernels
+  VecMeta x, z, b;
+  MatMeta A;
+  double *AL[TT_MAX_D + 1], *AR[TT_MAX_D + 1], *BL[TT_MAX_D + 1], *BR[TT_MAX_D + 1];
+  double *ZAL[TT_MAX_D + 1], *ZAR[TT_MAX_D + 1], *ZBL[TT_MAX_D + 1], *ZBR[TT_MAX_D + 1];
+  double *rhs, *sol, *w, *V, *T1, *T2, *crz, *xfull, *tmp, *tmpz, *K;
+  double *qA, *qQ, *qR, *tau, *qT;      // SVD-QR of M, then the enrichment QR (qA, tau, qT reused)
+  double *qA2, *tau2, *qT2;             // z QR (runs in the same launch as the enrichment QR)
+  double *qRe;                          // R factor of the enrichment QR
+  double *U, *Vs, *S, *J, *Ue, *Ct;
+  long long ldv;
+  GemmDesc *gd;     // [NG]
+  GemmDesc *gapp;   // [(m+1)*3] GMRES apply table
+  QRDesc *qd;       // [2]
+  SVDDesc *sd;      // [1]
+  CopyDesc *cd;     // [8]
+  int *iv;          // [16]
+  double *dv;       // [8]: [0] sweep max residual, [1] eps
+  int *limit;       // [d+1] per-bond truncation limit
+  int m;            // GMRES restart
+};
+
+__device__ GemmDesc gdd(int M, int N, int K, const double *A, long long lda, int tA, const double *B, long long ldb,
+                        int tB, double *C, long long ldc) {
+  GemmDesc g = gd_make(M, N, K, A, lda, tA, B, ldb, tB);
+  gd_plain(g, C, ldc);
+  return g;
+}
+__device__ GemmDesc gd_none() {
+  GemmDesc g = gd_make(0, 0, 0, nullptr, 1, 0, nullptr, 1, 0);
+  gd_plain(g, nullptr, 1);
+  return g;
+}
+__device__ CopyDesc cpy(int rows, int cols, const double *src, long long ssr, long long ssc, double *dst,
+                        long long dsr, long long dsc) {
+  CopyDesc c;
+  c.rows = rows; c.cols = cols; c.src = src; c.ss_r = ssr; c.ss_c = ssc; c.dst = dst; c.ds_r = dsr; c.ds_c = dsc;
+  return c;
+}
+
+__global__ void init_ifaces_kernel(Dev D) {
+  const int d = D.x.d;
+  D.AL[0][0] = 1.0; D.BL[0][0] = 1.0; D.ZAL[0][0] = 1.0; D.ZBL[0][0] = 1.0;
+  D.AR[d][0] = 1.0; D.BR[d][0] = 1.0; D.ZAR[d][0] = 1.0; D.ZBR[d][0] = 1.0;
+}
+
+__global__ void set_dv_kernel(double *dv, int i, double v) { dv[i] = v; }
+
+// interfaces: right ones at bond k from bond k+1 and core k; left ones at bond k+1 from bond k and core k
+__global__ void plan_iface(Dev D, int k, int dir) {
+  const int n = D.x.n[k];
+  const int r0 = D.x.r[k], r1 = D.x.r[k + 1], z0 = D.z.r[k], z1 = D.z.r[k + 1];
+  const int R0 = D.A.R[k], R1 = D.A.R[k + 1], b0 = D.b.r[k], b1 = D.b.r[k + 1];
+  const double *X = D.x.data + D.x.off[k], *Z = D.z.data + D.z.off[k], *Bk = D.b.data + D.b.off[k];
+  const double *Ak = D.A.data + D.A.off[k];
+  if (dir < 0) {
+    descs_iface_right(r0, R0, r0, n, n, r1, R1, r1, D.AR[k + 1], X, Ak, X, D.AR[k], D.T1, D.T2, D.gd + 0);
+    descs_iface_right_vec(r0, b0, n, r1, b1, D.BR[k + 1], X, Bk, D.BR[k], D.T1, D.gd + 3);
+    descs_iface_right(z0, R0, r0, n, n, z1, R1, r1, D.ZAR[k + 1], Z, Ak, X, D.ZAR[k], D.T1, D.T2, D.gd + 5);
+    descs_iface_right_vec(z0, b0, n, z1, b1, D.ZBR[k + 1], Z, Bk, D.ZBR[k], D.T1, D.gd + 8);
+  } else {
+    descs_iface_left(r0, R0, r0, n, n, r1, R1, r1, D.AL[k], X, Ak, X, D.AL[k + 1], D.T1, D.T2, D.gd + 0);
+    descs_iface_left_vec(r0, b0, n, r1, b1, D.BL[k], X, Bk, D.BL[k + 1], D.T1, D.gd + 3);
+    descs_iface_left(z0, R0, r0, n, n, z1, R1, r1, D.ZAL[k], Z, Ak, X, D.ZAL[k + 1], D.T1, D.T2, D.gd + 5);
+    descs_iface_left_vec(z0, b0, n, z1, b1, D.ZBL[k], Z, Bk, D.ZBL[k + 1], D.T1, D.gd + 8);
+  }
+}
+
+// local system at core k: rhs descs, GMRES apply table, copies x_k <-> sol
+__global__ void plan_local(Dev D, int k) {
+  const int n = D.x.n[k];
+  const int r0 = D.x.r[k], r1 = D.x.r[k + 1];
+  const int R0 = D.A.R[k], R1 = D.A.R[k + 1], b0 = D.b.r[k], b1 = D.b.r[k + 1];
+  const double *Bk = D.b.data + D.b.off[k], *Ak = D.A.data + D.A.off[k];
+  const int N = r0 * n * r1;
+  D.iv[0] = N;
+  descs_local_rhs(r0, b0, n, r1, b1, D.BL[k], Bk, D.BR[k + 1], D.rhs, D.T1, D.gd + 0);
+  for (int j = -1; j < D.m; ++j) {
+    const double *in = (j < 0) ? D.sol : D.V + (long long)j * D.ldv;
+    descs_local_apply(r0, R0, r0, n, n, r1, R1, r1, D.AL[k], Ak, D.AR[k + 1], in, D.w, D.T1, D.T2,
+                      D.gapp + 3 * (j + 1));
+  }
+  D.cd[0] = cpy(N, 1, D.x.data + D.x.off[k], 1, N, D.sol, 1, N);
+  D.cd[1] = cpy(N, 1, D.sol, 1, N, D.x.data + D.x.off[k], 1, N);
+}
+
+__global__ void track_res_kernel(const GmState *st, double *dv, int *status) {
+  const double r = st->res0;
+  if (r > dv[0] || !(r == r)) dv[0] = r;
+  if (st->nan && status) *status = TT_ERR_NUMERIC;
+}
+
+// SVD of M (mm x nn) read from sol: dir > 0 left unfolding, dir < 0 transposed right unfolding.
+__global__ void plan_svd(Dev D, int k, int dir) {
+  const int n = D.x.n[k], r0 = D.x.r[k], r1 = D.x.r[k + 1];
+  const int mm = dir > 0 ? r0 * n : n * r1;
+  const int nn = dir > 0 ? r1 : r0;
+  const long long srs = dir > 0 ? 1 : r0, scs = dir > 0 ? (long long)r0 * n : 1;  // M(row,col) in sol
+  const int wide = mm < nn;
+  const int p = wide ? mm : nn;
+  QRDesc &q = D.qd[0];
+  if (!wide) {  // QR of M
+    q.m = mm; q.n = nn; q.src = D.sol; q.src_rs = srs; q.src_cs = scs;
+    q.Q = D.qQ; q.q_rs = 1; q.q_cs = mm;
+  } else {      // QR of M^T
+    q.m = nn; q.n = mm; q.src = D.sol; q.src_rs = scs; q.src_cs = srs;
+    q.Q = D.qQ; q.q_rs = 1; q.q_cs = nn;
+  }
+  q.A = D.qA; q.lda = q.m;
+  q.R = D.qR; q.ldr = p;
+  q.tau = D.tau; q.T = D.qT;
+  SVDDesc &s = D.sd[0];
+  s.m = p; s.p = p; s.W = D.qR; s.ldw = p; s.U = D.U; s.ldu = p; s.V = D.Vs; s.ldv = p;
+  s.sigma = D.S; s.work = D.J; s.sweeps_out = nullptr;
+  D.iv[2] = wide; D.iv[3] = p; D.iv[4] = mm; D.iv[5] = nn;
+}
+
+// Truncation (reading Z20: delta = eps ||x_k|| / sqrt(d-1), capped by the bond
+// limit) and the factors of the truncated local solution:
+//   Ue[:, :r] = left singular vectors of M (mm x r, ld mm)
+//   Ct        = V_r Sigma_r (nn x r)   (so the carry is C = Ct^T)
+//   xfull     = the truncated local solution in [r0, n, r1] layout.
+__global__ void trunc_kernel(Dev D, int k, int dir) {
+  __shared__ int s_r;
+  const int wide = D.iv[2], p = D.iv[3], mm = D.iv[4], nn = D.iv[5];
+  const int d = D.x.d, tid = threadIdx.x;
+  if (tid == 0) {
+    double tot = 0.0;
+    for (int i = 0; i < p; ++i) tot += D.S[i] * D.S[i];
+    const double delta = D.dv[1] * sqrt(tot) / sqrt((double)(d > 1 ? d - 1 : 1));
+    const double d2 = delta * delta;
+    double tail = 0.0;
+    int r = p;
+    for (int i = p - 1; i >= 1; --i) {
+      const double t2 = tail + D.S[i] * D.S[i];
+      if (t2 <= d2) { tail = t2; r = i; } else break;
+    }
+    const int lim = D.limit[dir > 0 ? k + 1 : k];
+    r = r < 1 ? 1 : r;
+    r = r > lim ? lim : r;
+    s_r = r;
+    D.iv[1] = r;
+  }
+  __syncthreads();
+  const int r = s_r;
+  // tall: L = Q U_R, R = V_R;  wide: L = V_R, R = Q U_R.  Fold Sigma into the right factor.
+  double *Rfac = wide ? D.U : D.Vs;
+  for (int e = tid; e < p * r; e += blockDim.x) {
+    const int row = e % p, c = e / p;
+    Rfac[row + (long long)c * p] *= D.S[c];
+  }
+  if (tid == 0) {
+    if (!wide) {
+      D.gd[0] = gdd(mm, r, p, D.qQ, mm, 0, D.U, p, 0, D.Ue, mm);   // Ue = Q U_R[:, :r]
+      D.cd[0] = cpy(nn, r, D.Vs, 1, p, D.Ct, 1, nn);              // Ct = V_R[:, :r] S
+    } else {
+      D.cd[0] = cpy(mm, r, D.Vs, 1, p, D.Ue, 1, mm);              // Ue = V_R[:, :r]
+      D.gd[0] = gdd(nn, r, p, D.qQ, nn, 0, D.U, p, 0, D.Ct, nn);   // Ct = Q U_R[:, :r] S
+    }
+    if (dir > 0) D.gd[1] = gdd(mm, nn, r, D.Ue, mm, 0, D.Ct, nn, 1, D.xfull, mm);   // [r0 n, r1] = Ue Ct^T
+    else D.gd[1] = gdd(nn, mm, r, D.Ct, nn, 0, D.Ue, mm, 1, D.xfull, nn);           // [r0, n r1] = Ct Ue^T
+  }
+}
+
+// Residual core z_k, enrichment of the solution core, neighbour update.
+__global__ void plan_enrich(Dev D, int k, int dir) {
+  const int d = D.x.d;
+  const int n = D.x.n[k];
+  const int r0 = D.x.r[k], r1 = D.x.r[k + 1], z0 = D.z.r[k], z1 = D.z.r[k + 1];
+  const int R0 = D.A.R[k], R1 = D.A.R[k + 1], b0 = D.b.r[k], b1 = D.b.r[k + 1];
+  const double *Bk = D.b.data + D.b.off[k], *Ak = D.A.data + D.A.off[k];
+  const int r = D.iv[1], mm = D.iv[4], nn = D.iv[5];
+  GemmDesc *g = D.gd;
+  // ---- crz [z0, n, z1] = zb-rhs - zAx-apply(xfull)
+  descs_local_rhs(z0, b0, n, z1, b1, D.ZBL[k], Bk, D.ZBR[k + 1], D.crz, D.T1, g + 0);
+  descs_local_apply(z0, R0, r0, n, n, z1, R1, r1, D.ZAL[k], Ak, D.ZAR[k + 1], D.xfull, D.crz, D.T1, D.T2, g + 2);
+  g[4].alpha = -1.0; g[4].beta = 1.0;
+  // ---- crs: x frames on the orthonormal side, z frames on the carry side, written as extra
+  //      columns of Ue (M orientation): dir > 0: [r0, n, z1] left unfolding -> Ue[:, r:r+z1]
+  //      dir < 0: [z0, n, r1] transposed right unfolding -> Ue[:, r:r+z0]
+  double *Uc = D.Ue + (long long)r * mm;
+  if (dir > 0) {
+    descs_local_rhs(r0, b0, n, z1, b1, D.BL[k], Bk, D.ZBR[k + 1], Uc, D.T1, g + 5);
+    descs_local_apply(r0, R0, r0, n, n, z1, R1, r1, D.AL[k], Ak, D.ZAR[k + 1], D.xfull, Uc, D.T1, D.T2, g + 7);
+  } else {
+    descs_local_rhs(z0, b0, n, r1, b1, D.ZBL[k], Bk, D.BR[k + 1], Uc, D.T1, g + 5);
+    descs_local_apply(z0, R0, r0, n, n, r1, R1, r1, D.ZAL[k], Ak, D.AR[k + 1], D.xfull, Uc, D.T1, D.T2, g + 7);
+    // output element (a, c) of the final GEMMs -> Ue[c + mm a] (transposed)
+    g[6].s_r0 = mm; g[6].s_c0 = 1;
+    g[9].s_r0 = mm; g[9].s_c0 = 1;
+  }
+  g[9].alpha = -1.0; g[9].beta = 1.0;
+  const int ze = dir > 0 ? z1 : z0;  // extra columns
+  // ---- QR of crz (z core) and of Ue (x core), one launch
+  QRDesc &qz = D.qd[0];
+  QRDesc &qx = D.qd[1];
+  double *Zk = D.z.data + D.z.off[k];
+  double *Xk = D.x.data + D.x.off[k];
+  int qzr;
+  if (dir > 0) {
+    qz.m = z0 * n; qz.n = z1; qz.src = D.crz; qz.src_rs = 1; qz.src_cs = (long long)z0 * n;
+    qzr = min(z0 * n, z1);
+    qz.Q = Zk; qz.q_rs = 1; qz.q_cs = (long long)z0 * n;
+  } else {
+    qz.m = n * z1; qz.n = z0; qz.src = D.crz; qz.src_rs = z0; qz.src_cs = 1;
+    qzr = min(n * z1, z0);
+    qz.Q = Zk; qz.q_rs = qzr; qz.q_cs = 1;
+  }
+  qz.A = D.qA2; qz.lda = qz.m; qz.R = nullptr; qz.ldr = 1; qz.tau = D.tau2; qz.T = D.qT2;
+  const int q = min(mm, r + ze);
+  qx.m = mm; qx.n = r + ze; qx.src = D.Ue; qx.src_rs = 1; qx.src_cs = mm;
+  qx.A = D.qA; qx.lda = mm; qx.R = D.qRe; qx.ldr = q; qx.tau = D.tau; qx.T = D.qT;
+  if (dir > 0) { qx.Q = Xk; qx.q_rs = 1; qx.q_cs = mm; }     // x_k = Q as [r0, n, q]
+  else { qx.Q = Xk; qx.q_rs = q; qx.q_cs = 1; }              // x_k = Q^T as [q, n, r1]
+  // ---- K = Re[:, :r] C = Re[:, :r] Ct^T  (q x nn)
+  g[10] = gdd(q, nn, r, D.qRe, q, 0, D.Ct, nn, 1, D.K, q);
+  // ---- neighbour update
+  if (dir > 0) {
+    const int n2 = D.x.n[k + 1], r2 = D.x.r[k + 2];
+    double *Xn = D.x.data + D.x.off[k + 1];
+    g[11] = gdd(q, n2 * r2, nn, D.K, q, 0, Xn, nn, 0, D.tmp, q);           // K x_{k+1}
+    D.cd[0] = cpy(q, n2 * r2, D.tmp, 1, q, Xn, 1, q);
+    // z_{k+1}: keep its first qzr rows (left rank shrinks when z0 n < z1)
+    const int zn2 = D.z.n[k + 1], zz2 = D.z.r[k + 2];
+    double *Zn = D.z.data + D.z.off[k + 1];
+    if (qzr < z1) {
+      D.cd[1] = cpy(qzr, zn2 * zz2, Zn, 1, z1, D.tmpz, 1, qzr);
+      D.cd[2] = cpy(qzr, zn2 * zz2, D.tmpz, 1, qzr, Zn, 1, qzr);
+    } else {
+      D.cd[1] = cpy(0, 0, nullptr, 0, 0, nullptr, 0, 0);
+      D.cd[2] = cpy(0, 0, nullptr, 0, 0, nullptr, 0, 0);
+    }
+    D.x.r[k + 1] = q;
+    D.z.r[k + 1] = qzr;
+  } else {
+    const int rp = D.x.r[k - 1], np = D.x.n[k - 1];
+    double *Xp = D.x.data + D.x.off[k - 1];
+    g[11] = gdd(rp * np, q, nn, Xp, (long long)rp * np, 0, D.K, q, 1, D.tmp, (long long)rp * np);  // x_{k-1} K^T
+    D.cd[0] = cpy(rp * np, q, D.tmp, 1, (long long)rp * np, Xp, 1, (long long)rp * np);
+    D.cd[1] = cpy(0, 0, nullptr, 0, 0, nullptr, 0, 0);
+    D.cd[2] = cpy(0, 0, nullptr, 0, 0, nullptr, 0, 0);
+    D.x.r[k] = q;
+    D.z.r[k] = qzr;   // z_{k-1} keeps its first qzr columns (no data movement)
+  }
+  (void)d;
+}
+
+}  // namespace
+
+static long long lmax(long long a, long long b) { return a > b ? a : b; }
+
+namespace {
+__global__ void set_gm_H(GmState *st, double *H) { st->H = H; }
+
+// host evaluation of a descriptor chain with capacity ranks -> per-GEMM grid caps
+struct CapChain {
+  int M[12], N[12];
+};
+}  // namespace
+
+struct AmenCtx {
+  Dev D;
+  int d, m;
+  long long Ncap, Scap;
+  int pc, zcm, nmax;
+  GmState *gst;
+  double *H, *h1, *h2;
+  char *orth_base;
+  size_t orth_cap;
+};
+
+static tt_status carve_amen(const MatMeta &A, const VecMeta &b, const VecMeta &x, const VecMeta &z, int m, Arena &ar,
+                            AmenCtx &P) {
+  const int d = A.d;
+  if (b.d != d || x.d != d || z.d != d) return fail(TT_ERR_SHAPE, "amen_solve: number of cores differ");
+  for (int k = 0; k < d; ++k) {
+    if (A.m[k] != A.n[k]) return fail(TT_ERR_SHAPE, "amen_solve: A must be square in every mode");
+    if (A.n[k] != x.n[k] || A.m[k] != b.n[k] || z.n[k] != x.n[k]) return fail(TT_ERR_SHAPE, "amen_solve: shape mismatch");
+  }
+  if (m < 2 || m > GM_MAX_M) return fail(TT_ERR_ARG, "amen_solve: gmres_restart must be in [2, 128]");
+  for (int k = 1; k < d; ++k)
+    if (x.rcap[k] <= z.rcap[k])
+      return fail(TT_ERR_CAPACITY, "amen_solve: x rank capacity must exceed z rank capacity (enrichment)");
+  std::memset(&P, 0, sizeof(P));
+  P.d = d;
+  P.m = m;
+  Dev &D = P.D;
+  D.x = x; D.z = z; D.b = b; D.A = A;
+  D.m = m;
+  long long Ncap = 1, Zcap = 1, Tcap = 1, Ecap = 1, Scap = 1;
+  int pc = 1, zcm = 1, nmax = 1;
+  for (int k = 0; k <= d; ++k) { pc = x.rcap[k] > pc ? x.rcap[k] : pc; zcm = z.rcap[k] > zcm ? z.rcap[k] : zcm; }
+  for (int k = 0; k < d; ++k) {
+    const long long n = x.n[k];
+    nmax = x.n[k] > nmax ? x.n[k] : nmax;
+    Ncap = lmax(Ncap, (long long)x.rcap[k] * n * x.rcap[k + 1]);
+    Zcap = lmax(Zcap, (long long)z.rcap[k] * n * z.rcap[k + 1]);
+    long long rm = x.rcap[k];
+    rm = lmax(rm, x.rcap[k + 1]); rm = lmax(rm, z.rcap[k]); rm = lmax(rm, z.rcap[k + 1]);
+    rm = lmax(rm, b.rcap[k]); rm = lmax(rm, b.rcap[k + 1]);
+    long long Rm = lmax(A.Rcap[k], A.Rcap[k + 1]);
+    Tcap = lmax(Tcap, n * rm * rm * lmax(Rm, 1));
+    Ecap = lmax(Ecap, n * lmax(x.rcap[k], x.rcap[k + 1]) * (pc + zcm));
+    Scap = lmax(Scap, (long long)x.rcap[k] * n * x.rcap[k + 1]);
+    Scap = lmax(Scap, (long long)z.rcap[k] * n * z.rcap[k + 1]);
+  }
+  P.Ncap = Ncap; P.Scap = Scap; P.pc = pc; P.zcm = zcm; P.nmax = nmax;
+  for (int k = 0; k <= d; ++k) {
+    D.AL[k] = ar.take<double>((size_t)x.rcap[k] * x.rcap[k] * A.Rcap[k]);
+    D.AR[k] = ar.take<double>((size_t)x.rcap[k] * x.rcap[k] * A.Rcap[k]);
+    D.BL[k] = ar.take<double>((size_t)x.rcap[k] * b.rcap[k]);
+    D.BR[k] = ar.take<double>((size_t)x.rcap[k] * b.rcap[k]);
+    D.ZAL[k] = ar.take<double>((size_t)z.rcap[k] * x.rcap[k] * A.Rcap[k]);
+    D.ZAR[k] = ar.take<double>((size_t)z.rcap[k] * x.rcap[k] * A.Rcap[k]);
+    D.ZBL[k] = ar.take<double>((size_t)z.rcap[k] * b.rcap[k]);
+    D.ZBR[k] = ar.take<double>((size_t)z.rcap[k] * b.rcap[k]);
+  }
+  D.ldv = (Ncap + 31) / 32 * 32;
+  D.rhs = ar.take<double>(Ncap);
+  D.sol = ar.take<double>(Ncap);
+  D.w = ar.take<double>(Ncap);
+  D.V = ar.take<double>((size_t)D.ldv * (m + 1));
+  D.T1 = ar.take<double>(Tcap);
+  D.T2 = ar.take<double>(Tcap);
+  D.crz = ar.take<double>(Zcap);
+  D.xfull = ar.take<double>(Ncap);
+  D.tmp = ar.take<double>(Scap);
+  D.tmpz = ar.take<double>(Zcap);
+  D.K = ar.take<double>(Ecap);
+  D.qA = ar.take<double>(lmax(Ncap, Ecap));
+  D.qQ = ar.take<double>(Ncap);
+  D.qR = ar.take<double>((size_t)pc * pc);
+  D.tau = ar.take<double>(pc + zcm);
+  D.qT = ar.take<double>(32 * 32 * ((pc + zcm) / 32 + 2));
+  D.qA2 = ar.take<double>(Zcap);
+  D.tau2 = ar.take<double>(zcm + 1);
+  D.qT2 = ar.take<double>(32 * 32 * (zcm / 32 + 2));
+  D.qRe = ar.take<double>((size_t)(pc + zcm) * (pc + zcm));
+  D.U = ar.take<double>((size_t)pc * pc);
+  D.Vs = ar.take<double>((size_t)pc * pc);
+  D.S = ar.take<double>(pc);
+  D.J = ar.take<double>((size_t)2 * pc * pc);
+  D.Ue = ar.take<double>(Ecap);
+  D.Ct = ar.take<double>(Ncap);
+  D.gd = ar.take<GemmDesc>(NG);
+  D.gapp = ar.take<GemmDesc>((size_t)3 * (m + 1));
+  D.qd = ar.take<QRDesc>(2);
+  D.sd = ar.take<SVDDesc>(1);
+  D.cd = ar.take<CopyDesc>(8);
+  D.iv = ar.take<int>(16);
+  D.dv = ar.take<double>(8);
+  D.limit = ar.take<int>(TT_MAX_D + 1);
+  P.gst = ar.take<GmState>(1);
+  P.H = ar.take<double>((size_t)(m + 1) * m);
+  P.h1 = ar.take<double>(m + 1);
+  P.h2 = ar.take<double>(m + 1);
+  // orthogonalisation scratch (x or z)
+  Arena c1, c2;
+  orth_meta(x, -1, nullptr, c1, nullptr);
+  orth_meta(z, -1, nullptr, c2, nullptr);
+  P.orth_cap = c1.used > c2.used ? c1.used : c2.used;
+  P.orth_base = ar.take<char>(P.orth_cap);
+  return TT_OK;
+}
+
+size_t amen_ws_bytes(const MatMeta &A, const VecMeta &b, const VecMeta &x, const VecMeta &z, int restart) {
+  Arena ar;
+  AmenCtx P;
+  if (carve_amen(A, b, x, z, restart, ar, P) != TT_OK) return 0;
+  return ar.used;
+}
+
+static tt_status gemms(const GemmDesc *g, int count, int Mc, int Nc, cudaStream_t s) {
+  for (int i = 0; i < count; ++i) TT_TRY(launch_gemm(g + i, 1, Mc, Nc, s));
+  return TT_OK;
+}
+
+tt_status amen_solve_meta(const MatMeta &A, const VecMeta &b, const VecMeta &x, const VecMeta &z, const AmenOpts &o,
+                          int *sweeps_dev, double *res_dev, int *status_dev, Arena &ar, cudaStream_t s) {
+  AmenCtx P;
+  TT_TRY(carve_amen(A, b, x, z, o.restart, ar, P));
+  if (!ar.base) return TT_OK;
+  if (!ar.ok()) return fail(TT_ERR_CAPACITY, "amen_solve: workspace too small");
+  if (!(o.eps > 0.0)) return fail(TT_ERR_ARG, "amen_solve: eps must be > 0");
+  Dev &D = P.D;
+  const int d = P.d, m = P.m;
+  const int pc = P.pc, zcm = P.zcm, nmax = P.nmax;
+  // per-bond truncation limits: min(rmax, xcap - zcap) (room for the enrichment)
+  {
+    static thread_local std::vector<int> lim;
+    lim.assign(TT_MAX_D + 1, 1);
+    for (int k = 0; k <= d; ++k) {
+      int l = x.rcap[k] - z.rcap[k];
+      if (l > o.rmax) l = o.rmax;
+      lim[k] = l < 1 ? 1 : l;
+    }
+    cudaMemcpyAsync(D.limit, lim.data(), sizeof(int) * (d + 1), cudaMemcpyHostToDevice, s);
+    cudaStreamSynchronize(s);
+  }
+  set_gm_H<<<1, 1, 0, s>>>(P.gst, P.H);
+  set_dv_kernel<<<1, 1, 0, s>>>(D.dv, 1, o.eps);
+  Arena oa;
+  oa.base = P.orth_base;
+  oa.cap = P.orth_cap;
+  TT_TRY(orth_meta(x, -1, nullptr, oa, s));
+  oa.used = 0;
+  TT_TRY(orth_meta(z, -1, nullptr, oa, s));
+  init_ifaces_kernel<<<1, 1, 0, s>>>(D);
+  // per-GEMM grid caps: the same descriptor builders evaluated on the host with capacity ranks
+  const int *xc = x.rcap, *zc = z.rcap, *bc = b.rcap, *Rc = A.Rcap;
+  struct Caps12 { GemmDesc g[12]; int cnt; };
+  auto launch_caps = [&](const GemmDesc *dev, const Caps12 &hc, int from, int cnt) -> tt_status {
+    for (int i = 0; i < cnt; ++i) TT_TRY(launch_gemm(dev + i, 1, hc.g[from + i].M, hc.g[from + i].N, s));
+    return TT_OK;
+  };
+  auto iface_caps = [&](int k, int dir) {
+    Caps12 c;
+    const int n = x.n[k];
+    if (dir < 0) {
+      descs_iface_right(xc[k], Rc[k], xc[k], n, n, xc[k + 1], Rc[k + 1], xc[k + 1], 0, 0, 0, 0, 0, 0, 0, c.g + 0);
+      descs_iface_right_vec(xc[k], bc[k], n, xc[k + 1], bc[k + 1], 0, 0, 0, 0, 0, c.g + 3);
+      descs_iface_right(zc[k], Rc[k], xc[k], n, n, zc[k + 1], Rc[k + 1], xc[k + 1], 0, 0, 0, 0, 0, 0, 0, c.g + 5);
+      descs_iface_right_vec(zc[k], bc[k], n, zc[k + 1], bc[k + 1], 0, 0, 0, 0, 0, c.g + 8);
+    } else {
+      descs_iface_left(xc[k], Rc[k], xc[k], n, n, xc[k + 1], Rc[k + 1], xc[k + 1], 0, 0, 0, 0, 0, 0, 0, c.g + 0);
+      descs_iface_left_vec(xc[k], bc[k], n, xc[k + 1], bc[k + 1], 0, 0, 0, 0, 0, c.g + 3);
+      descs_iface_left(zc[k], Rc[k], xc[k], n, n, zc[k + 1], Rc[k + 1], xc[k + 1], 0, 0, 0, 0, 0, 0, 0, c.g + 5);
+      descs_iface_left_vec(zc[k], bc[k], n, zc[k + 1], bc[k + 1], 0, 0, 0, 0, 0, c.g + 8);
+    }
+    return c;
+  };
+  auto iface = [&](int k, int dir) -> tt_status {
+    plan_iface<<<1, 1, 0, s>>>(D, k, dir);
+    Caps12 c = iface_caps(k, dir);
+    return launch_caps(D.gd, c, 0, 10);
+  };
+  for (int k = d - 1; k >= 1; --k) TT_TRY(iface(k, -1));
+  const double ltol = o.local_tol > 0.0 ? o.local_tol : 0.1 * o.eps;
+  Caps12 appc;
+  GmresCtx gc;
+  gc.st = P.gst;
+  gc.Nptr = D.iv;
+  gc.m = m;
+  gc.max_restarts = o.max_restarts;
+  gc.tol = ltol;
+  gc.b = D.rhs;
+  gc.x = D.sol;
+  gc.w = D.w;
+  gc.V = D.V;
+  gc.ldv = D.ldv;
+  gc.h1 = P.h1;
+  gc.h2 = P.h2;
+  gc.axpy_blocks = (int)((P.Ncap + 255) / 256 > 592 ? 592 : (P.Ncap + 255) / 256);
+  if (gc.axpy_blocks < 1) gc.axpy_blocks = 1;
+  gc.poll = 1;
+  int hflag = 0;
+  gc.host_flag = &hflag;
+  gc.apply = [&](const double *, double *, int j) -> tt_status { return launch_caps(D.gapp + 3 * (j + 1), appc, 2, 3); };
+  int dir = +1, sweep = 0;
+  double hres = 0.0;
+  for (sweep = 0; sweep < o.max_sweeps; ++sweep) {
+    set_dv_kernel<<<1, 1, 0, s>>>(D.dv, 0, 0.0);
+    for (int t = 0; t < d; ++t) {
+      const int k = dir > 0 ? t : d - 1 - t;
+      const int last = (t == d - 1);
+      const int n = x.n[k];
+      descs_local_rhs(xc[k], bc[k], n, xc[k + 1], bc[k + 1], 0, 0, 0, 0, 0, appc.g + 0);
+      descs_local_apply(xc[k], Rc[k], xc[k], n, n, xc[k + 1], Rc[k + 1], xc[k + 1], 0, 0, 0, 0, 0, 0, 0, appc.g + 2);
+      plan_local<<<1, 1, 0, s>>>(D, k);
+      TT_TRY(launch_copy(D.cd, 1, P.Ncap, s));
+      TT_TRY(launch_caps(D.gd, appc, 0, 2));
+      TT_TRY(gmres_solve(gc, s));
+      track_res_kernel<<<1, 1, 0, s>>>(P.gst, D.dv, status_dev);
+      if (last) {
+        TT_TRY(launch_copy(D.cd + 1, 1, P.Ncap, s));
+        continue;
+      }
+      plan_svd<<<1, 1, 0, s>>>(D, k, dir);
+      TT_TRY(launch_qr(D.qd, 1, s));
+      const int pcap = dir > 0 ? (xc[k] * n < xc[k + 1] ? xc[k] * n : xc[k + 1])
+                               : (n * xc[k + 1] < xc[k] ? n * xc[k + 1] : xc[k]);
+      TT_TRY(launch_jacobi(D.sd, 1, pcap, pcap, s));
+      trunc_kernel<<<1, 256, 0, s>>>(D, k, dir);
+      TT_TRY(launch_copy(D.cd, 1, P.Ncap, s));
+      const int big = n * (xc[k] > xc[k + 1] ? xc[k] : xc[k + 1]);
+      TT_TRY(launch_gemm(D.gd, 1, big, pc, s));
+      TT_TRY(launch_gemm(D.gd + 1, 1, big, big, s));
+      plan_enrich<<<1, 1, 0, s>>>(D, k, dir);
+      {
+        Caps12 ec;
+        descs_local_rhs(zc[k], bc[k], n, zc[k + 1], bc[k + 1], 0, 0, 0, 0, 0, ec.g + 0);
+        descs_local_apply(zc[k], Rc[k], xc[k], n, n, zc[k + 1], Rc[k + 1], xc[k + 1], 0, 0, 0, 0, 0, 0, 0, ec.g + 2);
+        if (dir > 0) {
+          descs_local_rhs(xc[k], bc[k], n, zc[k + 1], bc[k + 1], 0, 0, 0, 0, 0, ec.g + 5);
+          descs_local_apply(xc[k], Rc[k], xc[k], n, n, zc[k + 1], Rc[k + 1], xc[k + 1], 0, 0, 0, 0, 0, 0, 0, ec.g + 7);
+        } else {
+          descs_local_rhs(zc[k], bc[k], n, xc[k + 1], bc[k + 1], 0, 0, 0, 0, 0, ec.g + 5);
+          descs_local_apply(zc[k], Rc[k], xc[k], n, n, xc[k + 1], Rc[k + 1], xc[k + 1], 0, 0, 0, 0, 0, 0, 0, ec.g + 7);
+        }
+        TT_TRY(launch_caps(D.gd, ec, 0, 10));
+      }
+      TT_TRY(launch_qr(D.qd, 2, s));
+      TT_TRY(launch_gemm(D.gd + 10, 1, pc, big, s));
+      {
+        const int nb_ = dir > 0 ? x.n[k + 1] * xc[k + 2 <= d ? k + 2 : d] : pc;
+        const int mb_ = dir > 0 ? pc : x.n[k - 1] * xc[k - 1];
+        TT_TRY(launch_gemm(D.gd + 11, 1, mb_, nb_, s));
+      }
+      TT_TRY(launch_copy(D.cd, 3, P.Scap, s));
+      TT_TRY(iface(k, dir));
+    }
+    cudaMemcpyAsync(&hres, D.dv, sizeof(double), cudaMemcpyDeviceToHost, s);
+    cudaStreamSynchronize(s);
+    TT_TRY(check_launch("amen sweep"));
+    if (hres <= o.eps) { ++sweep; break; }
+    dir = -dir;
+  }
+  (void)zcm; (void)nmax;
+  if (sweeps_dev) cudaMemcpyAsync(sweeps_dev, &sweep, sizeof(int), cudaMemcpyHostToDevice, s);
+  if (res_dev) cudaMemcpyAsync(res_dev, D.dv, sizeof(double), cudaMemcpyDeviceToDevice, s);
+  cudaStreamSynchronize(s);
+  if (status_dev && !(hres <= o.eps)) {
+    int st = TT_ERR_NOCONV;
+    cudaMemcpyAsync(status_dev, &st, sizeof(int), cudaMemcpyHostToDevice, s);
+    cudaStreamSynchronize(s);
+  }
+  return check_launch("amen_solve");
+}
+
+}  // namespace tt

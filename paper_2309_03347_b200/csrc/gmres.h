@@ -1,0 +1,40 @@
+// Device GMRES state and host driver context (see gmres.cu).
+#pragma once
+#include <functional>
+
+#include "tt_common.cuh"
+
+namespace tt {
+
+constexpr int GM_MAX_M = 128;
+
+struct GmState {
+  int N, m, converged, stop, cycle, nan, j, jdone;
+  double tol, beta, bnorm, res, res0;
+  double g[GM_MAX_M + 1];
+  double cs[GM_MAX_M];
+  double sn[GM_MAX_M];
+  double *H;  // (m+1) x m
+};
+
+struct GmresCtx {
+  GmState *st;
+  const int *Nptr;       // device: local size
+  int m, max_restarts;
+  double tol;
+  const double *b;       // rhs (device, length N)
+  double *x;             // in: initial guess, out: solution
+  double *w;             // scratch vector
+  double *V;             // basis, (m+1) vectors of stride ldv
+  long long ldv;
+  double *h1, *h2;       // scratch [m+1]
+  int axpy_blocks;
+  int poll;              // 1: read the convergence flag back once per cycle
+  int *host_flag;        // pinned host int for polling
+  // enqueue out = A in; j = basis index (-1 for x)
+  std::function<tt_status(const double *, double *, int)> apply;
+};
+
+tt_status gmres_solve(const GmresCtx &c, cudaStream_t s);
+
+}  // namespace tt

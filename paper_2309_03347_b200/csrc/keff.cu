@@ -1,0 +1,304 @@
+// keff_fixed_point (a9): eqn:TT_k_eff_fixed_points, readings
+// Z16-Z19.  k, <f, Psi>, ||Psi|| and all ranks stay on the device; the host
+// polls one convergence word per outer iteration.
+#include <cmath>
+#include <cstring>
+
+#include "amen.h"
+#include "tt_common.cuh"
+
+namespace tt {
+
+namespace {
+
+struct KeffScal {
+  double k, kinv, s_old, s_new, nrm, nrm_inv, one;
+  int flag, iters, status;
+};
+
+__global__ void transpose_ttm_kernel(const MatMeta F, const MatMeta FT) {
+  const int k = blockIdx.y;
+  const int R0 = F.R[k], R1 = F.R[k + 1], m = F.m[k], n = F.n[k];
+  const int total = R0 * m * n * R1;
+  const double *src = F.data + F.off[k];
+  double *dst = FT.data + FT.off[k];
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
+    const int a = e % R0, t = e / R0, i = t % m, t2 = t / m, j = t2 % n, b = t2 / n;
+    dst[a + R0 * (j + n * (i + m * b))] = src[e];
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    FT.R[k] = R0;
+    if (k == F.d - 1) FT.R[k + 1] = R1;
+  }
+}
+
+__global__ void ones_kernel(const VecMeta v) {
+  const int k = blockIdx.x;
+  double *c = v.data + v.off[k];
+  for (int i = threadIdx.x; i < v.n[k]; i += blockDim.x) c[i] = 1.0;
+  if (threadIdx.x == 0) {
+    v.r[k] = 1;
+    if (k == v.d - 1) v.r[k + 1] = 1;
+  }
+}
+
+__global__ void keff_init_kernel(KeffScal *sc, double k0, const double *nrm) {
+  sc->k = k0;
+  sc->kinv = 1.0 / k0;
+  sc->one = 1.0;
+  sc->flag = 0;
+  sc->iters = 0;
+  sc->status = 0;
+  sc->nrm = *nrm;
+  sc->nrm_inv = (*nrm > 0.0) ? 1.0 / *nrm : 1.0;
+}
+
+__global__ void keff_after_solve_kernel(KeffScal *sc) {
+  // k' = k <f, Psi'> / <f, Psi>
+  if (sc->s_old == 0.0 || !(sc->s_old == sc->s_old)) {
+    sc->status = TT_ERR_NOFISSION;
+    sc->flag = 1;
+    return;
+  }
+  sc->nrm_inv = 0.0;  // set after the norm
+}
+
+__global__ void keff_update_kernel(KeffScal *sc, const double *nrm, double tol, double *khist, int *shist,
+                                   const int *sweeps, int hist_cap, int max_outer, double *k_out, int *iters_out,
+                                   int *status_out) {
+  if (sc->status == TT_ERR_NOFISSION) {
+    sc->flag = 1;
+  } else {
+    const double knew = sc->k * sc->s_new / sc->s_old;
+    const double nn = *nrm;
+    sc->nrm = nn;
+    sc->nrm_inv = nn > 0.0 ? 1.0 / nn : 1.0;
+    sc->s_old = sc->s_new * sc->nrm_inv;
+    const int it = sc->iters;
+    if (khist && it < hist_cap) khist[it] = knew;
+    if (shist && it < hist_cap) shist[it] = sweeps ? *sweeps : 0;
+    sc->iters = it + 1;
+    const double dk = fabs(knew - sc->k);
+    sc->k = knew;
+    sc->kinv = 1.0 / knew;
+    if (!(knew == knew)) {
+      sc->status = TT_ERR_NUMERIC;
+      sc->flag = 1;
+    } else if (dk <= tol) {
+      sc->flag = 1;
+    } else if (sc->iters >= max_outer) {
+      sc->status = TT_ERR_NOCONV;
+      sc->flag = 1;
+    }
+  }
+  if (k_out) *k_out = sc->k;
+  if (iters_out) *iters_out = sc->iters;
+  if (status_out) *status_out = sc->status;
+}
+
+struct KeffWS {
+  MatMeta FT;
+  VecMeta ones, f, SP, FP, B, z0;
+  KeffScal *sc;
+  double *nrm, *dbuf;
+  int *sweeps;
+  char *sub;       // scratch for round / dot / orth / amen
+  size_t sub_cap;
+};
+
+VecMeta vec_like(Arena &ar, int d, const int *n, const int *rcap) {
+  VecMeta v;
+  std::memset(&v, 0, sizeof(v));
+  v.d = d;
+  long long off = 0;
+  for (int k = 0; k < d; ++k) {
+    v.n[k] = n[k];
+    v.off[k] = off;
+    off += (long long)rcap[k] * n[k] * rcap[k + 1];
+  }
+  for (int k = 0; k <= d; ++k) v.rcap[k] = rcap[k];
+  v.data = ar.take<double>(off);
+  v.r = ar.take<int>(d + 1);
+  return v;
+}
+
+tt_status carve_keff(const MatMeta &H, const MatMeta &S, const MatMeta &F, const VecMeta &psi, const VecMeta &z,
+                     const keff_opts &o, Arena &ar, KeffWS &W) {
+  const int d = H.d;
+  if (S.d != d || F.d != d || psi.d != d || z.d != d) return fail(TT_ERR_SHAPE, "keff: number of cores differ");
+  for (int k = 0; k < d; ++k) {
+    if (H.m[k] != H.n[k] || S.m[k] != S.n[k] || F.m[k] != F.n[k]) return fail(TT_ERR_SHAPE, "keff: operators must be square");
+    if (H.n[k] != psi.n[k] || S.n[k] != psi.n[k] || F.n[k] != psi.n[k]) return fail(TT_ERR_SHAPE, "keff: shape mismatch");
+  }
+  std::memset(&W, 0, sizeof(W));
+  // F^T
+  W.FT = F;
+  for (int k = 0; k < d; ++k) { W.FT.m[k] = F.n[k]; W.FT.n[k] = F.m[k]; }
+  long long tot = 0;
+  for (int k = 0; k < d; ++k) tot += (long long)F.Rcap[k] * F.m[k] * F.n[k] * F.Rcap[k + 1];
+  W.FT.data = ar.take<double>(tot);
+  W.FT.R = ar.take<int>(d + 1);
+  int one[TT_MAX_D + 1], cap[TT_MAX_D + 1];
+  for (int k = 0; k <= d; ++k) one[k] = 1;
+  W.ones = vec_like(ar, d, F.m, one);
+  for (int k = 0; k <= d; ++k) cap[k] = F.Rcap[k];
+  W.f = vec_like(ar, d, F.n, cap);
+  for (int k = 0; k <= d; ++k) cap[k] = S.Rcap[k] * psi.rcap[k];
+  W.SP = vec_like(ar, d, S.m, cap);
+  int capF[TT_MAX_D + 1];
+  for (int k = 0; k <= d; ++k) capF[k] = F.Rcap[k] * psi.rcap[k];
+  W.FP = vec_like(ar, d, F.m, capF);
+  for (int k = 0; k <= d; ++k) cap[k] = (k == 0 || k == d) ? 1 : S.Rcap[k] * psi.rcap[k] + F.Rcap[k] * psi.rcap[k];
+  W.B = vec_like(ar, d, psi.n, cap);
+  W.z0 = vec_like(ar, d, z.n, z.rcap);
+  W.sc = ar.take<KeffScal>(1);
+  W.nrm = ar.take<double>(1);
+  W.dbuf = ar.take<double>(4);
+  W.sweeps = ar.take<int>(1);
+  // scratch: the max over the sub-operations
+  size_t mx = 0;
+  auto upd = [&](size_t v) { mx = v > mx ? v : mx; };
+  { Arena c; round_meta(W.SP, 0.0, 1, nullptr, nullptr, 0, c, nullptr); upd(c.used); }
+  { Arena c; round_meta(W.FP, 0.0, 1, nullptr, nullptr, 0, c, nullptr); upd(c.used); }
+  { Arena c; round_meta(W.B, 0.0, 1, nullptr, nullptr, 0, c, nullptr); upd(c.used); }
+  { Arena c; round_meta(W.f, 0.0, 1, nullptr, nullptr, 0, c, nullptr); upd(c.used); }
+  { Arena c; round_meta(psi, 0.0, 1, nullptr, nullptr, 0, c, nullptr); upd(c.used); }
+  { Arena c; dot_meta(W.f, psi, nullptr, c, nullptr); upd(c.used); }
+  upd(amen_ws_bytes(H, W.B, psi, z, o.gmres_restart));
+  W.sub_cap = mx;
+  W.sub = ar.take<char>(mx);
+  return TT_OK;
+}
+
+}  // namespace
+
+size_t keff_ws_bytes(const MatMeta &H, const MatMeta &S, const MatMeta &F, const VecMeta &psi, const VecMeta &z,
+                     const keff_opts &o) {
+  Arena ar;
+  KeffWS W;
+  if (carve_keff(H, S, F, psi, z, o, ar, W) != TT_OK) return 0;
+  return ar.used;
+}
+
+tt_status keff_meta(const MatMeta &H, const MatMeta &S, const MatMeta &F, const VecMeta &psi, const VecMeta &z,
+                    double k0, const keff_opts &o, const keff_report &rep, Arena &ar, cudaStream_t s) {
+  KeffWS W;
+  TT_TRY(carve_keff(H, S, F, psi, z, o, ar, W));
+  if (!ar.base) return TT_OK;
+  if (!ar.ok()) return fail(TT_ERR_CAPACITY, "keff_fixed_point: workspace too small");
+  if (!(k0 != 0.0)) return fail(TT_ERR_ARG, "keff_fixed_point: k0 must be nonzero");
+  const int d = H.d;
+  auto sub = [&]() {
+    Arena a;
+    a.base = W.sub;
+    a.cap = W.sub_cap;
+    return a;
+  };
+  // f = round(F^T 1)   (reading Z18)
+  transpose_ttm_kernel<<<dim3(64, d), 256, 0, s>>>(F, W.FT);
+  ones_kernel<<<d, 256, 0, s>>>(W.ones);
+  TT_TRY(matvec_meta(W.FT, W.ones, W.f, s));
+  { Arena a = sub(); TT_TRY(round_meta(W.f, 1e-14, 1 << 30, nullptr, nullptr, 0, a, s)); }
+  // keep the AMEn residual TT's initial cores (the oracle restarts every solve from z0)
+  TT_TRY(copy_meta(z, W.z0, s));
+  // Psi <- round(Psi0) / ||.||   (Z16, Z17)
+  { Arena a = sub(); TT_TRY(round_meta(psi, o.eps_round, o.rmax, nullptr, nullptr, 0, a, s)); }
+  { Arena a = sub(); TT_TRY(orth_meta(psi, -1, W.nrm, a, s)); }
+  keff_init_kernel<<<1, 1, 0, s>>>(W.sc, k0, W.nrm);
+  TT_TRY(scale_meta(psi, &W.sc->nrm_inv, 1.0, 0, s));
+  { Arena a = sub(); TT_TRY(dot_meta(W.f, psi, &W.sc->s_old, a, s)); }
+  AmenOpts ao;
+  ao.eps = o.eps_solve;
+  ao.local_tol = 0.0;
+  ao.max_sweeps = o.max_sweeps;
+  ao.rmax = o.rmax;
+  ao.restart = o.gmres_restart;
+  ao.max_restarts = o.gmres_max_restarts;
+  int hflag = 0;
+  for (int it = 0; it < o.max_outer; ++it) {
+    TT_TRY(matvec_meta(S, psi, W.SP, s));
+    { Arena a = sub(); TT_TRY(round_meta(W.SP, o.eps_round, o.rmax, nullptr, nullptr, 0, a, s)); }
+    TT_TRY(matvec_meta(F, psi, W.FP, s));
+    { Arena a = sub(); TT_TRY(round_meta(W.FP, o.eps_round, o.rmax, nullptr, nullptr, 0, a, s)); }
+    TT_TRY(add_meta(W.SP, nullptr, W.FP, &W.sc->kinv, W.B, s));
+    { Arena a = sub(); TT_TRY(round_meta(W.B, o.eps_round, o.rmax, nullptr, nullptr, 0, a, s)); }
+    TT_TRY(copy_meta(W.z0, z, s));
+    { Arena a = sub(); TT_TRY(amen_solve_meta(H, W.B, psi, z, ao, W.sweeps, nullptr, nullptr, a, s)); }
+    { Arena a = sub(); TT_TRY(dot_meta(W.f, psi, &W.sc->s_new, a, s)); }
+    keff_after_solve_kernel<<<1, 1, 0, s>>>(W.sc);
+    { Arena a = sub(); TT_TRY(orth_meta(psi, -1, W.nrm, a, s)); }
+    keff_update_kernel<<<1, 1, 0, s>>>(W.sc, W.nrm, o.tol_k, rep.k_hist_dev, rep.sweeps_hist_dev, W.sweeps,
+                                       rep.hist_cap, o.max_outer, rep.k_dev, rep.iters_dev, rep.status_dev);
+    TT_TRY(scale_meta(psi, &W.sc->nrm_inv, 1.0, 0, s));
+    cudaMemcpyAsync(&hflag, &W.sc->flag, sizeof(int), cudaMemcpyDeviceToHost, s);
+    cudaStreamSynchronize(s);
+    TT_TRY(check_launch("keff iteration"));
+    if (hflag) break;
+  }
+  return check_launch("keff_fixed_point");
+}
+
+}  // namespace tt
+
+using namespace tt;
+
+extern "C" size_t amen_workspace(const tt_mat *A, const tt_vec *b, const tt_vec *x, const tt_vec *z,
+                                 const amen_opts *o) {
+  MatMeta Am;
+  VecMeta bm, xm, zm;
+  if (!o || make_mat_meta(A, Am) || make_vec_meta(b, bm) || make_vec_meta(x, xm) || make_vec_meta(z, zm)) return 0;
+  return amen_ws_bytes(Am, bm, xm, zm, o->gmres_restart);
+}
+
+extern "C" tt_status amen_solve(const tt_mat *A, const tt_vec *b, tt_vec *x, tt_vec *z, const amen_opts *o,
+                                int32_t *sweeps_dev, double *res_dev, void *ws, size_t wsb, tt_stream s) {
+  MatMeta Am;
+  VecMeta bm, xm, zm;
+  TT_TRY(make_mat_meta(A, Am));
+  TT_TRY(make_vec_meta(b, bm));
+  TT_TRY(make_vec_meta(x, xm));
+  TT_TRY(make_vec_meta(z, zm));
+  if (!o || !ws) return fail(TT_ERR_ARG, "amen_solve: NULL options or workspace");
+  if (o->max_sweeps < 1 || o->rmax < 1 || o->gmres_max_restarts < 1)
+    return fail(TT_ERR_ARG, "amen_solve: max_sweeps, rmax, gmres_max_restarts must be >= 1");
+  AmenOpts ao;
+  ao.eps = o->eps;
+  ao.local_tol = o->local_tol;
+  ao.max_sweeps = o->max_sweeps;
+  ao.rmax = o->rmax;
+  ao.restart = o->gmres_restart;
+  ao.max_restarts = o->gmres_max_restarts;
+  Arena ar;
+  ar.base = (char *)ws;
+  ar.cap = wsb;
+  return amen_solve_meta(Am, bm, xm, zm, ao, sweeps_dev, res_dev, nullptr, ar, (cudaStream_t)s);
+}
+
+extern "C" size_t keff_workspace(const tt_mat *H, const tt_mat *S, const tt_mat *F, const tt_vec *psi,
+                                 const tt_vec *z, const keff_opts *o) {
+  MatMeta Hm, Sm, Fm;
+  VecMeta pm, zm;
+  if (!o || make_mat_meta(H, Hm) || make_mat_meta(S, Sm) || make_mat_meta(F, Fm) || make_vec_meta(psi, pm) ||
+      make_vec_meta(z, zm))
+    return 0;
+  return keff_ws_bytes(Hm, Sm, Fm, pm, zm, *o);
+}
+
+extern "C" tt_status keff_fixed_point(const tt_mat *H, const tt_mat *S, const tt_mat *F, tt_vec *psi, tt_vec *z,
+                                      double k0, const keff_opts *o, keff_report *rep, void *ws, size_t wsb,
+                                      tt_stream s) {
+  MatMeta Hm, Sm, Fm;
+  VecMeta pm, zm;
+  TT_TRY(make_mat_meta(H, Hm));
+  TT_TRY(make_mat_meta(S, Sm));
+  TT_TRY(make_mat_meta(F, Fm));
+  TT_TRY(make_vec_meta(psi, pm));
+  TT_TRY(make_vec_meta(z, zm));
+  if (!o || !rep || !ws) return fail(TT_ERR_ARG, "keff_fixed_point: NULL options, report or workspace");
+  if (o->max_outer < 1 || o->rmax < 1 || o->max_sweeps < 1 || o->gmres_max_restarts < 1)
+    return fail(TT_ERR_ARG, "keff_fixed_point: iteration limits must be >= 1");
+  Arena ar;
+  ar.base = (char *)ws;
+  ar.cap = wsb;
+  return keff_meta(Hm, Sm, Fm, pm, zm, k0, *o, *rep, ar, (cudaStream_t)s);
+}

@@ -196,6 +196,7 @@ tt_status add_meta(const VecMeta &x, const double *alpha, const VecMeta &y, cons
   }
   for (int k = 1; k < x.d; ++k)
     if (z.rcap[k] < x.rcap[k] + y.rcap[k]) return fail(TT_ERR_CAPACITY, "tt_add: z rank capacity < rx+ry");
+  // (keff sizes B with exactly these capacities)
   int bx = (int)((mx + 255) / 256);
   bx = bx > 1024 ? 1024 : (bx < 1 ? 1 : bx);
   add_kernel<<<dim3(bx, x.d), 256, 0, s>>>(x, alpha, y, beta, z);

@@ -247,3 +247,48 @@ def als_update_interfaces(direction, dims, Iprev, Yk, Ak, Xk, Inext, stream=None
     check(lib().als_update_interfaces(int(direction), *[int(v) for v in dims], _ptr(Iprev), _ptr(Yk), _ptr(Ak),
                                       _ptr(Xk), _ptr(Inext), _ptr(ws), ws.numel(), C.c_void_p(_stream(stream))))
     return Inext
+
+
+# ------------------------------------------------------------------ a7 ---
+
+def amen_solve(A: TTMat, b: TTVec, x: TTVec, z: TTVec, eps: float, rmax: int = 1 << 20, max_sweeps: int = 20,
+               restart: int = 40, max_restarts: int = 50, local_tol: float = 0.0, stream=None):
+    """x <- AMEn solution of A x = b (x: initial guess in, solution out; z: residual TT)."""
+    o = _lib.amen_opts(float(eps), float(local_tol), int(max_sweeps), int(min(rmax, 2**30)), int(restart),
+                       int(max_restarts))
+    nb = lib().amen_workspace(A.c, b.c, x.c, z.c, C.byref(o))
+    if nb == 0:
+        check(lib().amen_solve(A.c, b.c, x.c, z.c, C.byref(o), None, None, None, 0, C.c_void_p(_stream(stream))))
+    ws = workspace(nb, x.device)
+    sweeps = torch.zeros(1, dtype=torch.int32, device=x.device)
+    res = torch.zeros(1, dtype=torch.float64, device=x.device)
+    check(lib().amen_solve(A.c, b.c, x.c, z.c, C.byref(o), _ptr(sweeps), _ptr(res), _ptr(ws), ws.numel(),
+                           C.c_void_p(_stream(stream))))
+    return x, sweeps, res
+
+
+# ------------------------------------------------------------------ a9 ---
+
+class KeffResult:
+    def __init__(self, k, iters, k_hist, sweeps_hist, status):
+        self.k, self.iters, self.k_hist, self.sweeps_hist, self.status = k, iters, k_hist, sweeps_hist, status
+
+
+def keff_fixed_point(H: TTMat, S: TTMat, F: TTMat, psi: TTVec, z: TTVec, k0: float = 1.0, tol_k: float = 1e-10,
+                     eps_round: float = 1e-12, eps_solve: float = 1e-11, max_outer: int = 200, rmax: int = 1 << 20,
+                     max_sweeps: int = 20, restart: int = 40, max_restarts: int = 50, hist_cap: int = 256,
+                     stream=None) -> KeffResult:
+    o = _lib.keff_opts(float(tol_k), float(eps_round), float(eps_solve), int(max_outer), int(min(rmax, 2**30)),
+                       int(max_sweeps), int(restart), int(max_restarts))
+    dev = psi.device
+    k = torch.zeros(1, dtype=torch.float64, device=dev)
+    iters = torch.zeros(1, dtype=torch.int32, device=dev)
+    kh = torch.zeros(hist_cap, dtype=torch.float64, device=dev)
+    sh = torch.zeros(hist_cap, dtype=torch.int32, device=dev)
+    st = torch.zeros(1, dtype=torch.int32, device=dev)
+    rep = _lib.keff_report(k.data_ptr(), iters.data_ptr(), kh.data_ptr(), sh.data_ptr(), int(hist_cap), st.data_ptr())
+    nb = lib().keff_workspace(H.c, S.c, F.c, psi.c, z.c, C.byref(o))
+    ws = workspace(nb, dev)
+    check(lib().keff_fixed_point(H.c, S.c, F.c, psi.c, z.c, float(k0), C.byref(o), C.byref(rep), _ptr(ws),
+                                 ws.numel(), C.c_void_p(_stream(stream))))
+    return KeffResult(k, iters, kh, sh, st)

@@ -1,0 +1,102 @@
+"""GPU parity of operator assembly (device sum + round), AMEn (a7) and the k-eff
+fixed point (a9) against the oracle.  |dk|/k <= 1e-8 on the dense-checkable
+configs (BASELINE.json north_star)."""
+import copy
+import os
+
+import numpy as np
+import pytest
+
+import inputs
+from oracle import solvers as so
+from oracle import transport as T
+from oracle import tt as ott
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a GPU", allow_module_level=True)
+
+import paper_2309_03347_b200 as tb  # noqa: E402
+from paper_2309_03347_b200 import transport as gtr  # noqa: E402
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def small_c1(nv=4):
+    p = copy.deepcopy(inputs.problem_c1())
+    p["nv"] = nv
+    return p
+
+
+@pytest.mark.parametrize("prob", [inputs.problem_c1(), inputs.problem_small_hetero(nv=4, G=2, N=4)],
+                         ids=["C1", "hetero4"])
+def test_operator_assembly_on_device(prob):
+    dense = T.dense_operators(prob)
+    ops = gtr.operators(prob)
+    for k in "HSF":
+        got = ott.ttm_full(ops[k].cores())
+        assert np.max(np.abs(got - dense[k])) <= 1e-12 * np.abs(dense[k]).max()
+    if prob["name"].startswith("C1"):
+        assert ops["H"].ranks() == [1, 3, 7, 8, 1, 1]
+        assert ops["S"].ranks() == [1, 2, 4, 8, 1, 1]
+
+
+def test_amen_identity_and_transport():
+    g = inputs.rng(60)
+    modes = [2, 3, 4, 2]
+    b = inputs.random_tt(g, modes, [1, 2, 3, 2, 1])
+    I = tb.TTMat.from_cores(ott.rank1_ttm([np.eye(n) for n in modes]))
+    x = tb.TTVec.from_cores([np.ones((1, n, 1)) for n in modes], rcap=[1, 8, 8, 8, 1])
+    z = tb.TTVec.from_cores(inputs.random_tt(g, modes, [1, 2, 2, 2, 1]))
+    tb.amen_solve(I, tb.TTVec.from_cores(b), x, z, eps=1e-12)
+    assert np.linalg.norm(ott.tt_full(x.cores()) - ott.tt_full(b)) <= 1e-10 * np.linalg.norm(ott.tt_full(b))
+    # transport H on a 4^3 S2 cube vs a dense solve
+    prob = small_c1(4)
+    ops = gtr.operators(prob)
+    Hd = T.dense_operators(prob)["H"]
+    modes = [4, 4, 4, 8, 1]
+    b = inputs.random_tt(g, modes, [1, 2, 3, 2, 1, 1])
+    x = tb.TTVec.from_cores([np.ones((1, n, 1)) for n in modes], rcap=[1, 20, 20, 20, 20, 1])
+    z = tb.TTVec.from_cores(inputs.random_tt(g, modes, [1, 4, 4, 4, 4, 1]))
+    _, sweeps, res = tb.amen_solve(ops["H"], tb.TTVec.from_cores(b), x, z, eps=1e-11)
+    ref = np.linalg.solve(Hd, ott.tt_full(b))
+    err = np.linalg.norm(ott.tt_full(x.cores()) - ref) / np.linalg.norm(ref)
+    assert err <= 1e-8, (err, sweeps.item(), res.item())
+
+
+def _keff_gpu(prob, modes, rmax, kick=4, **kw):
+    ops = gtr.operators(prob)
+    g = inputs.rng(61)
+    d = len(modes)
+    psi = tb.TTVec.from_cores([np.ones((1, n, 1)) for n in modes], rcap=[1] + [rmax + kick] * (d - 1) + [1])
+    z = tb.TTVec.from_cores(inputs.random_tt(g, modes, [1] + [kick] * (d - 1) + [1]))
+    res = tb.keff_fixed_point(ops["H"], ops["S"], ops["F"], psi, z, rmax=rmax, **kw)
+    torch.cuda.synchronize()
+    return res, psi
+
+
+def test_keff_small_vs_dense():
+    prob = small_c1(4)
+    ops = T.dense_operators(prob)
+    kd, psid, _ = so.keff_dense_power(ops["H"], ops["S"], ops["F"], tol=1e-13)
+    res, psi = _keff_gpu(prob, [4, 4, 4, 8, 1], rmax=32, tol_k=1e-12, eps_round=1e-13, eps_solve=1e-12)
+    assert res.status.item() == 0
+    k = res.k.item()
+    assert abs(k - kd) / kd <= 1e-8
+    v = ott.tt_full(psi.cores())
+    v = v * np.sign(v.sum()) / np.linalg.norm(v)
+    assert np.linalg.norm(v - psid * np.sign(psid.sum())) <= 1e-6
+
+
+def test_keff_c1_vacuum():
+    """BASELINE.json configs[0] (vacuum): |dk|/k <= 1e-8 against the dense oracle value."""
+    kd = float(open(os.path.join(GOLD, "c1_keff_vacuum.txt")).read().split()[-1])
+    res, psi = _keff_gpu(inputs.problem_c1(), [8, 8, 8, 8, 1], rmax=64, tol_k=1e-12, eps_round=1e-13,
+                         eps_solve=1e-12)
+    assert res.status.item() == 0
+    assert abs(res.k.item() - kd) / kd <= 1e-8
+    it = res.iters.item()
+    hist = res.k_hist[:it].cpu().numpy()
+    assert abs(hist[-1] - res.k.item()) == 0.0
