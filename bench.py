@@ -1,0 +1,367 @@
+"""Benchmark of the B200 hot path of arXiv 2309.03347 (TT/QTT k-eigenvalue).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c1|c2|c5]
+                    [--impl ours|reference]
+
+A step is one pass of the whole hot path over one
+synthetic problem: one complete k-eff fixed-point solve (eqn:TT_k_eff_fixed_
+points) from psi_0 = 1, k_0 = 1 to |dk| < tol: every iteration
+runs exact matvec + rounding of S psi and F psi, the sum, the AMEn solve of
+H psi' = B (local apply, interfaces, GMRES, enrichment) and the k update.
+`value` = k-eff fixed-point iterations per second over all ranks (replicas,
+weak scaling: every rank solves its own copy, no data-path collective —
+DESIGN.md "Multi-GPU").  The contraction GFLOP/s (% of the measured FP64 DMMA
+peak) is reported beside it, and `roofline` gives the dominant kernel.
+The c2 / c5 workloads are the matvec+round and ALS sweep microbenchmarks.
+
+--impl reference times the fp64 CPU oracle (oracle/, the only other place
+bench.py executes it) on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "TT contraction FP64 GFLOP/s (% DMMA peak); k-eff fixed-point iterations/sec"
+DMMA_FALLBACK = 37.1e3   # GFLOP/s, tools/peaks_fp64 on this pool (profiles/peaks_fp64_r01.json)
+
+
+def peaks():
+    p = {"hbm_gbs": 6539.9, "hbm_src": "MEASURED_PEAKS.json", "dmma_gflops": DMMA_FALLBACK,
+         "dmma_src": "profiles/peaks_fp64_r01.json"}
+    try:
+        mp = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+        p["hbm_gbs"] = float(mp["hbm_gbs"])
+    except Exception:
+        p["hbm_gbs"], p["hbm_src"] = 6650.0, "fallback B200_PROFILING.md"
+    try:
+        pf = json.load(open(os.path.join(ROOT, "profiles", "peaks_fp64_r01.json")))
+        p["dmma_gflops"] = 1e3 * float(pf["dmma_tflops_sustained"])
+    except Exception:
+        pass
+    return p
+
+
+# ------------------------------------------------------------ clocks ---
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index, self.rows, self.stop = index, [], threading.Event()
+        self.t = threading.Thread(target=self.run, daemon=True)
+
+    def run(self):
+        while not self.stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([v.strip() for v in out.split(",")])
+            except Exception:
+                pass
+            self.stop.wait(0.2)
+
+    def __enter__(self):
+        self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self.stop.set()
+        self.t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4)
+                          if len(r) > 4 + i and r[4 + i].strip().lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": float(self.rows[0][1]) if self.rows[0][1].replace(".", "").isdigit() else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# --------------------------------------------------------- workloads ---
+def c1_setup(device):
+    import inputs
+    import paper_2309_03347_b200 as tb
+    from paper_2309_03347_b200 import transport as gtr
+    prob = inputs.problem_c1()
+    ops = gtr.operators(prob, device=device)
+    modes = [8, 8, 8, 8, 1]
+    g = inputs.rng(61)
+    z0 = inputs.random_tt(g, modes, [1, 4, 4, 4, 4, 1])
+    psi0 = [np.ones((1, n, 1)) for n in modes]
+    return {"prob": prob, "ops": ops, "modes": modes, "z0": z0, "psi0": psi0, "rmax": 64, "kick": 4,
+            "opts": dict(tol_k=1e-12, eps_round=1e-13, eps_solve=1e-12, rmax=64)}
+
+
+def c1_step(st, device, host_inputs=None):
+    import paper_2309_03347_b200 as tb
+    d = len(st["modes"])
+    cap = [1] + [st["rmax"] + st["kick"]] * (d - 1) + [1]
+    psi = tb.TTVec.from_cores(st["psi0"], rcap=cap, device=device)
+    z = tb.TTVec.from_cores(st["z0"], device=device)
+    ops = st["ops"]
+    res = tb.keff_fixed_point(ops["H"], ops["S"], ops["F"], psi, z, **st["opts"])
+    return res
+
+
+def c1_step_device(st):
+    """Device-resident step: psi / z reset by device copies, then the solve."""
+    import paper_2309_03347_b200 as tb
+    ops = st["ops"]
+    tb.tt_copy(st["psi_init"], st["psi"])
+    tb.tt_copy(st["z_init"], st["z"])
+    return tb.keff_fixed_point(ops["H"], ops["S"], ops["F"], st["psi"], st["z"], **st["opts"])
+
+
+def ops_bytes(ops):
+    return sum(int(o.data.numel()) * 8 for o in ops.values())
+
+
+# ------------------------------------------------------- oracle side ---
+def oracle_c1_sample(iters=3):
+    """Bounded sample of the same workload on the CPU oracle: `iters` fixed-point
+    iterations of the TT k-eff loop on C1 (oracle/solvers.keff_tt)."""
+    import inputs
+    from oracle import solvers as so
+    from oracle import transport as T
+    prob = inputs.problem_c1()
+    tops = T.tt_operators(prob)
+    modes = [8, 8, 8, 8, 1]
+    g = inputs.rng(61)
+    z0 = inputs.random_tt(g, modes, [1, 4, 4, 4, 4, 1])
+    psi0 = [np.ones((1, n, 1)) for n in modes]
+    t = time.perf_counter()
+    so.keff_tt(tops["H"], tops["S"], tops["F"], psi0, z0, tol_k=0.0, eps_round=1e-13, eps_solve=1e-12,
+               max_outer=iters, dense_max=0)
+    dt = time.perf_counter() - t
+    return iters / dt, dt
+
+
+def cpu_cores():
+    try:
+        import threadpoolctl
+        info = threadpoolctl.threadpool_info()
+        return max([i.get("num_threads", 1) for i in info] + [1])
+    except Exception:
+        return os.cpu_count()
+
+
+# --------------------------------------------------------------- main ---
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--workload", default="c1", choices=["c1"])
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        v, dt = oracle_c1_sample(iters=max(1, min(args.steps, 5)))
+        vals = [v]
+        for _ in range(max(0, min(args.steps, 3) - 1)):
+            vals.append(oracle_c1_sample(iters=2)[0])
+        val = statistics.median(vals)
+        line = {"impl": "reference", "metric": METRIC, "value": val, "unit": "iter/s", "n_gpus": args.gpus,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 / val,
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic", "config": {"workload": "C1 (configs[0]) TT k-eff fixed point, 8^3 S2 G=1"},
+                "cpu_baseline": {"value": val, "unit": "iter/s", "cores": cpu_cores(), "kind": "oracle",
+                                 "sample": "fixed-point iterations of oracle keff_tt on C1 (GMRES local solves)"},
+                "e2e": {"value": val, "unit": "iter/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(line))
+        return
+
+    import torch
+    torch.cuda.set_device(local)
+    device = torch.device("cuda", local)
+    dist = None
+    if world > 1:
+        import torch.distributed as tdist
+        tdist.init_process_group("nccl", device_id=device)
+        dist = tdist
+    import paper_2309_03347_b200 as tb
+    from paper_2309_03347_b200 import _lib
+    import ctypes as C
+
+    st = c1_setup(device)
+    d = len(st["modes"])
+    cap = [1] + [st["rmax"] + st["kick"]] * (d - 1) + [1]
+    st["psi_init"] = tb.TTVec.from_cores(st["psi0"], rcap=cap, device=device)
+    st["psi"] = tb.TTVec.from_cores(st["psi0"], rcap=cap, device=device)
+    st["z_init"] = tb.TTVec.from_cores(st["z0"], device=device)
+    st["z"] = tb.TTVec.from_cores(st["z0"], device=device)
+    flush = torch.empty(256 * 1024 * 1024 // 8, dtype=torch.float64, device=device)   # > 126 MB L2
+
+    for _ in range(args.warmup):
+        c1_step_device(st)
+    torch.cuda.synchronize()
+
+    cnt = (C.c_uint64 * 5)()
+    lib = _lib.lib()
+    lib.tt_counters(cnt, 1)
+    stream = torch.cuda.current_stream()
+    step_ms, iters_total = [], 0
+    with ClockSampler(local) as clk:
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            flush.fill_(1.0)                          # evict L2 between timed steps (untimed)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            res = c1_step_device(st)
+            e1.record(stream)
+            e1.synchronize()
+            step_ms.append(e0.elapsed_time(e1))
+            iters_total += int(res.iters.item())
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        wall = time.perf_counter() - t0
+    lib.tt_counters(cnt, 1)
+    dev_ms = sum(step_ms)
+    if dist:
+        t = torch.tensor([dev_ms, float(iters_total)], dtype=torch.float64, device=device)
+        mx = t.clone()
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        sm = t.clone()
+        dist.all_reduce(sm, op=dist.ReduceOp.SUM)
+        dev_ms_max, iters_all = float(mx[0]), float(sm[1])
+    else:
+        dev_ms_max, iters_all = dev_ms, float(iters_total)
+    value = iters_all / (dev_ms_max * 1e-3)
+    gemm_flops, mv_flops, qr_flops, svd_flops, ngemm = [int(v) for v in cnt]
+    contraction = (gemm_flops + mv_flops) / args.steps
+    pk = peaks()
+    contr_gflops = contraction / (dev_ms / args.steps * 1e-3) / 1e9
+
+    # ---- roofline of the dominant kernel: the DMMA contraction GEMM, timed live on
+    #      its own stream at the C1 AMEn local-apply shape (r=64, R=8, n=8)
+    roof = dominant_gemm_roofline(tb, device, pk)
+
+    # ---- end to end: host buffers (pinned) -> device, solve, result -> host
+    e2e = e2e_c1(tb, st, device, args.steps)
+
+    line = {"metric": METRIC, "value": value, "unit": "iter/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": dev_ms_max / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "C1 (configs[0]): TT k-eff fixed point to |dk|<1e-12, 8^3 vertices, S2, G=1, "
+                                   "modes (8,8,8,8,1), rmax 64",
+                       "l2": "256 MB flush between timed steps", "parallelism": f"replicas x{world}"},
+            "iters_per_step": iters_total / args.steps,
+            "contraction_gflops": contr_gflops,
+            "contraction_pct_dmma_peak": 100.0 * contr_gflops / pk["dmma_gflops"],
+            "flops_per_step": {"gemm": gemm_flops / args.steps, "matvec": mv_flops / args.steps,
+                               "qr": qr_flops / args.steps, "jacobi": svd_flops / args.steps,
+                               "gemm_calls": ngemm / args.steps},
+            "roofline": roof, "e2e": e2e, "clocks": clk.summary(),
+            "gpu_launches": None, "wall_s": wall}
+    line["gpu_launches"] = count_launches_estimate(ngemm / args.steps, iters_total / args.steps)
+    if rank == 0 and not args.no_cpu_baseline:
+        v, dt = oracle_c1_sample(iters=3)
+        line["cpu_baseline"] = {"value": v, "unit": "iter/s", "cores": cpu_cores(), "kind": "oracle",
+                                "sample": f"3 fixed-point iterations of oracle keff_tt on C1 ({dt:.1f} s)"}
+    if rank == 0:
+        print(json.dumps(line))
+    if dist:
+        dist.destroy_process_group()
+
+
+def count_launches_estimate(gemm_calls, iters):
+    """GEMM calls are counted on the device; the non-GEMM launches are roughly one
+    per GEMM chain (plan, QR, SVD, GMRES vector kernels).  Reported as counted
+    GEMM calls + estimate; the ncu launch list in profiles/ is the evidence."""
+    return int(gemm_calls * 2)
+
+
+def dominant_gemm_roofline(tb, device, pk):
+    import torch
+    rA = rB = rAp = rBp = 64
+    R = Rp = 8
+    m = n = 8
+    g = torch.Generator(device="cpu").manual_seed(5)
+    mk = lambda *s: torch.randn(*s, generator=g, dtype=torch.float64).reshape(-1).to(device)
+    Phi, Ak, Psi, x = mk(rA * R * rB), mk(R * m * n * Rp), mk(rAp * Rp * rBp), mk(rB * n * rBp)
+    y = torch.zeros(rA * m * rAp, dtype=torch.float64, device=device)
+    dims = (rA, R, rB, m, n, rAp, Rp, rBp)
+    for _ in range(5):
+        tb.als_local_apply(dims, Phi, Ak, Psi, x, y)
+    s = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    reps = 50
+    torch.cuda.synchronize()
+    e0.record(s)
+    for _ in range(reps):
+        tb.als_local_apply(dims, Phi, Ak, Psi, x, y)
+    e1.record(s)
+    e1.synchronize()
+    ms = e0.elapsed_time(e1) / reps
+    flops = 2.0 * (n * rB * rBp * rAp * Rp + m * n * rB * rAp * R * Rp + m * rA * rAp * rB * R)
+    achieved = flops / (ms * 1e-3) / 1e12
+    peak = pk["dmma_gflops"] / 1e3
+    return {"kernel": "gemm_dmma_kernel (als_local_apply chain, C1 local shape r=64 R=8 n=8)",
+            "bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+            "peak_src": "measured FP64 DMMA sustained (tools/peaks_fp64)", "traffic": None,
+            "flops_per_launch": flops, "ms_per_launch": ms}
+
+
+def e2e_c1(tb, st, device, steps):
+    """Same metric through the public API with HOST buffers: operator cores and
+    psi_0 / z_0 copied from pinned host memory every step, k and psi read back."""
+    import torch
+    ops = st["ops"]
+    host = {k: v.data.cpu().pin_memory() for k, v in ops.items()}
+    hpsi = st["psi_init"].data.cpu().pin_memory()
+    hz = st["z_init"].data.cpu().pin_memory()
+    out_psi = torch.empty_like(hpsi).pin_memory()
+    out_k = torch.empty(1, dtype=torch.float64).pin_memory()
+    s = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    iters = 0
+    torch.cuda.synchronize()
+    e0.record(s)
+    for _ in range(steps):
+        for k, v in ops.items():
+            v.data.copy_(host[k], non_blocking=True)
+        st["psi_init"].data.copy_(hpsi, non_blocking=True)
+        st["z_init"].data.copy_(hz, non_blocking=True)
+        res = c1_step_device(st)
+        out_psi.copy_(st["psi"].data, non_blocking=True)
+        out_k.copy_(res.k, non_blocking=True)
+        iters += int(res.iters.item())
+    e1.record(s)
+    e1.synchronize()
+    ms = e0.elapsed_time(e1)
+    h2d = sum(int(v.numel()) * 8 for v in host.values()) + int(hpsi.numel() + hz.numel()) * 8
+    return {"value": iters / (ms * 1e-3), "unit": "iter/s", "h2d_bytes_per_step": h2d,
+            "d2h_bytes_per_step": int(out_psi.numel()) * 8 + 8}
+
+
+if __name__ == "__main__":
+    main()

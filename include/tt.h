@@ -78,6 +78,13 @@ typedef struct {
 const char *tt_last_error(void);
 const char *tt_version(void);
 
+/* Device-side algorithmic counters (for measurement; synchronises the device):
+ * out[0] flops of the contraction GEMMs (2 M N K per call), out[1] flops of the
+ * exact matvec (2 n per output entry), out[2] nominal Householder QR flops
+ * (geqrf + orgqr), out[3] Jacobi SVD flops (column dots + rotations),
+ * out[4] number of GEMM calls.  reset != 0 zeroes them after reading. */
+void tt_counters(uint64_t *out /* [5] */, int32_t reset);
+
 /* ---------------------------------------------------------------- a1 ---
  * tt_matvec: exact TT-matrix x TT-vector product ("explicit and
  * exact algorithm").  For every core, independently,

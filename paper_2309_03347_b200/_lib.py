@@ -53,6 +53,7 @@ I32 = C.c_int32
 SIG = {
     "tt_last_error": (C.c_char_p, []),
     "tt_version": (C.c_char_p, []),
+    "tt_counters": (None, [C.POINTER(C.c_uint64), I32]),
     "tt_matvec": (I32, [C.POINTER(tt_mat), C.POINTER(tt_vec), C.POINTER(tt_vec), P]),
     "tt_matvec_batched": (I32, [I32, C.POINTER(tt_mat), C.POINTER(tt_vec), C.POINTER(tt_vec), P]),
     "tt_add": (I32, [C.POINTER(tt_vec), P, C.POINTER(tt_vec), P, C.POINTER(tt_vec), P]),

@@ -112,3 +112,24 @@ extern "C" tt_status tt_round(tt_vec *x, double eps, int32_t rmax, double *disca
   ar.cap = wsb;
   return round_meta(xm, eps, rmax, discarded_sq_dev, sv_dev, sv_stride, ar, (cudaStream_t)s);
 }
+
+namespace tt {
+void gemm_counters(unsigned long long *out, int reset);
+void matvec_counters(unsigned long long *out, int reset);
+void linalg_counters(unsigned long long *out, int reset);
+}
+
+extern "C" void tt_counters(uint64_t *out, int32_t reset) {
+  unsigned long long g[2] = {0, 0}, mv = 0, la[2] = {0, 0};
+  cudaDeviceSynchronize();
+  tt::gemm_counters(g, reset);
+  tt::matvec_counters(&mv, reset);
+  tt::linalg_counters(la, reset);
+  if (out) {
+    out[0] = g[0];
+    out[1] = mv;
+    out[2] = la[0];
+    out[3] = la[1];
+    out[4] = g[1];
+  }
+}

@@ -7,6 +7,9 @@
 
 namespace tt {
 
+// algorithmic flop counter of the contraction GEMMs (2 M N K per call) and launch count
+__device__ unsigned long long g_gemm_counters[2];
+
 namespace {
 
 constexpr int BM = 64, BN = 64, BK = 16, PAD = 4;
@@ -78,6 +81,10 @@ __global__ void __launch_bounds__(128) gemm_dmma_kernel(const GemmDesc *__restri
   __shared__ __align__(16) Tile t;
   const GemmDesc g = descs[blockIdx.z];
   const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN;
+  if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0 && g.M > 0 && g.N > 0) {
+    atomicAdd(&g_gemm_counters[0], 2ull * (unsigned long long)g.M * g.N * (g.K > 0 ? g.K : 0));
+    atomicAdd(&g_gemm_counters[1], 1ull);
+  }
   if (m0 >= g.M || n0 >= g.N) return;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wm = (warp & 1) * 32, wn = (warp >> 1) * 32;
@@ -144,6 +151,14 @@ tt_status launch_gemm(const GemmDesc *descs_dev, int count, int Mcap, int Ncap, 
   dim3 grid((Mcap + BM - 1) / BM, (Ncap + BN - 1) / BN, count);
   gemm_dmma_kernel<<<grid, 128, 0, s>>>(descs_dev);
   return check_launch("gemm_dmma");
+}
+
+void gemm_counters(unsigned long long *out, int reset) {
+  cudaMemcpyFromSymbol(out, g_gemm_counters, sizeof(g_gemm_counters));
+  if (reset) {
+    unsigned long long z[2] = {0, 0};
+    cudaMemcpyToSymbol(g_gemm_counters, z, sizeof(z));
+  }
 }
 
 }  // namespace tt

@@ -11,6 +11,9 @@
 
 namespace tt {
 
+// nominal flops: [0] Householder QR (geqrf + orgqr), [1] Jacobi rotations + column dots
+__device__ unsigned long long g_linalg_flops[2];
+
 namespace {
 
 constexpr int QR_THREADS = 256;
@@ -129,6 +132,13 @@ __device__ void apply_block_reflector(int m, int j0, int jb, const double *A, lo
 __global__ void __launch_bounds__(QR_THREADS) qr_kernel(const QRDesc *__restrict__ descs) {
   const QRDesc g = descs[blockIdx.x];
   const int m = g.m, n = g.n, kmin = min(m, n);
+  if (threadIdx.x == 0) {
+    // geqrf: 2 m n k - (m + n) k^2 + 2/3 k^3 ; orgqr (explicit Q, m x k): 4 m k^2 - 4/3 k^3 (LAPACK counts)
+    const double M = m, N = n, K = kmin;
+    double f = 2.0 * M * N * K - (M + N) * K * K + 2.0 / 3.0 * K * K * K;
+    if (g.Q) f += 4.0 * M * K * K - 4.0 / 3.0 * K * K * K;
+    atomicAdd(&g_linalg_flops[0], (unsigned long long)(f > 0 ? f : 0));
+  }
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   constexpr int NW = QR_THREADS / 32;
   __shared__ double red[32];
@@ -290,7 +300,9 @@ __device__ void jacobi_core(int m, int p, double *W, long long ldw, double *V, l
         be = warp_sum(be);
         ga = warp_sum(ga);
         if (ga == 0.0 || al == 0.0 || be == 0.0) continue;
+        if (lane == 0) atomicAdd(&g_linalg_flops[1], 6ull * m);
         if (fabs(ga) <= tol * sqrt(al) * sqrt(be)) continue;
+        if (lane == 0) atomicAdd(&g_linalg_flops[1], 6ull * (m + p));
         const double zeta = (be - al) / (2.0 * ga);
         const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(fma(zeta, zeta, 1.0)));
         const double c = 1.0 / sqrt(fma(t, t, 1.0)), s = c * t;
@@ -384,6 +396,14 @@ __global__ void __launch_bounds__(SVD_THREADS) jacobi_kernel(const SVDDesc *__re
 }
 
 }  // namespace
+
+void linalg_counters(unsigned long long *out, int reset) {
+  cudaMemcpyFromSymbol(out, g_linalg_flops, sizeof(g_linalg_flops));
+  if (reset) {
+    unsigned long long z[2] = {0, 0};
+    cudaMemcpyToSymbol(g_linalg_flops, z, sizeof(z));
+  }
+}
 
 tt_status launch_qr(const QRDesc *descs_dev, int count, cudaStream_t s) {
   if (count <= 0) return TT_OK;

@@ -92,6 +92,16 @@ int max_rank(const VecMeta &x) {
   return mx;
 }
 
+// algorithmic flops of the exact matvec (2 n per output entry)
+__device__ unsigned long long g_matvec_flops;
+void matvec_counters(unsigned long long *out, int reset) {
+  cudaMemcpyFromSymbol(out, g_matvec_flops, sizeof(unsigned long long));
+  if (reset) {
+    unsigned long long z = 0;
+    cudaMemcpyToSymbol(g_matvec_flops, &z, sizeof(z));
+  }
+}
+
 // -------------------------------------------------------------- matvec ---
 // Y_k[rho, i, rho'] = sum_j A_k[a, i, j, a'] X_k[b, j, b'], rho = a + R b.
 // One launch over all cores: blockIdx.y = core, grid-stride over output entries
@@ -122,6 +132,7 @@ __global__ void matvec_kernel(const MatMeta A, const VecMeta x, const VecMeta y)
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     y.r[k] = P;
     if (k == A.d - 1) y.r[k + 1] = P1;
+    atomicAdd(&g_matvec_flops, 2ull * (unsigned long long)total * n);
   }
 }
 
