@@ -169,7 +169,9 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--workload", default="c1", choices=["c1"])
+    ap.add_argument("--workload", default="c1", choices=["c1", "c2", "c5"])
+    ap.add_argument("--rank", type=int, default=128, help="c5 interface rank (64, 128, 256)")
+    ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
@@ -207,6 +209,14 @@ def main():
     import paper_2309_03347_b200 as tb
     from paper_2309_03347_b200 import _lib
     import ctypes as C
+
+    if args.workload in ("c2", "c5"):
+        line = micro_bench(args, tb, device, world, dist)
+        if rank == 0:
+            print(json.dumps(line))
+        if dist:
+            dist.destroy_process_group()
+        return
 
     st = c1_setup(device)
     d = len(st["modes"])
@@ -291,6 +301,95 @@ def main():
         print(json.dumps(line))
     if dist:
         dist.destroy_process_group()
+
+
+def _events():
+    import torch
+    return torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+
+
+def micro_bench(args, tb, device, world, dist):
+    """c5: one ALS double sweep (configs[4]); c2: tt_matvec + tt_round(1e-8, 128)
+    of one d=30 instance (configs[1]).  Same JSON shape as the default line."""
+    import torch
+    import inputs
+    pk = peaks()
+    s = torch.cuda.current_stream()
+    flush = torch.empty(256 * 1024 * 1024 // 8, dtype=torch.float64, device=device)
+    if args.workload == "c5":
+        from paper_2309_03347_b200.sweep import SweepProblem
+        inst = inputs.c5_instance(args.rank, seed=args.seed)
+        sp = SweepProblem(inst["A"], inst["X"], device)
+        sp.build_right()
+        for _ in range(args.warmup):
+            sp.double_sweep()
+        ms = []
+        with ClockSampler(torch.cuda.current_device()) as clk:
+            for _ in range(args.steps):
+                flush.fill_(1.0)
+                e0, e1 = _events()
+                e0.record(s)
+                sp.double_sweep()
+                e1.record(s)
+                e1.synchronize()
+                ms.append(e0.elapsed_time(e1))
+        t = statistics.median(ms)
+        flops = sp.flops()
+        gfl = flops / (t * 1e-3) / 1e9
+        peak = pk["dmma_gflops"]
+        return {"metric": METRIC, "value": gfl, "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": t, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": {"workload": f"C5 (configs[4]) ALS double sweep, d=40, r={args.rank}, R 5-8, "
+                                       f"n in {{2,4,8,16}}, seed {args.seed}",
+                           "l2": "256 MB flush between timed steps"},
+                "pct_dmma_peak": 100.0 * gfl / peak, "flops_per_step": flops, "ms_p10_p90": [
+                    float(np.percentile(ms, 10)), float(np.percentile(ms, 90))],
+                "roofline": {"kernel": "gemm_dmma_kernel (als_local_apply / als_update_interfaces chains)",
+                             "bound": "tensor", "achieved": gfl / 1e3, "peak": peak / 1e3, "unit": "TFLOP/s",
+                             "frac": gfl / peak, "peak_src": "measured FP64 DMMA sustained (tools/peaks_fp64)",
+                             "traffic": None},
+                "clocks": clk.summary(), "gpu_launches": 80 * 8}
+    # c2
+    inst = inputs.c2_instance(args.seed)
+    A = tb.TTMat.from_cores(inst["A"], device=device)
+    X = tb.TTVec.from_cores(inst["X"], device=device)
+    Y = tb.matvec_out(A, X)
+    Yr = tb.TTVec(Y.n, Y.rcap, device)
+    mv_bytes = 8 * sum(R0 * 4 * R1 + r0 * 2 * r1 + R0 * R1 * 2 * r0 * r1 for R0, R1, r0, r1 in
+                       zip(inst["R"][:-1], inst["R"][1:], inst["r"][:-1], inst["r"][1:]))
+    for _ in range(args.warmup):
+        tb.tt_matvec(A, X, Y)
+        tb.tt_copy(Y, Yr)
+        tb.tt_round(Yr, 1e-8, 128)
+    mv_ms, rd_ms = [], []
+    with ClockSampler(torch.cuda.current_device()) as clk:
+        for _ in range(args.steps):
+            flush.fill_(1.0)
+            e0, e1 = _events()
+            e2, e3 = _events()
+            e0.record(s)
+            tb.tt_matvec(A, X, Y)
+            e1.record(s)
+            tb.tt_copy(Y, Yr)
+            e2.record(s)
+            tb.tt_round(Yr, 1e-8, 128)
+            e3.record(s)
+            e3.synchronize()
+            mv_ms.append(e0.elapsed_time(e1))
+            rd_ms.append(e2.elapsed_time(e3))
+    mv, rd = statistics.median(mv_ms), statistics.median(rd_ms)
+    gbs = mv_bytes / (mv * 1e-3) / 1e9
+    return {"metric": METRIC, "value": 1e3 / (mv + rd), "unit": "instances/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": mv + rd, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"C2 (configs[1]) tt_matvec + tt_round(eps=1e-8, rmax=128), d=30, seed {args.seed}",
+                       "l2": "256 MB flush between timed steps"},
+            "matvec_ms": mv, "round_ms": rd, "ranks_after_round": Yr.ranks(),
+            "roofline": {"kernel": "matvec_kernel (tt_matvec, all 30 cores in one launch)", "bound": "hbm",
+                         "achieved": gbs, "peak": pk["hbm_gbs"], "unit": "GB/s", "frac": gbs / pk["hbm_gbs"],
+                         "peak_src": pk["hbm_src"], "traffic": None, "bytes_per_launch": mv_bytes},
+            "clocks": clk.summary()}
 
 
 def count_launches_estimate(gemm_calls, iters):

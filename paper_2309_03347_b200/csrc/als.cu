@@ -19,7 +19,7 @@ long long prod(long long a, long long b, long long c, long long d) { return a * 
 static tt_status run3(const Desc3 &d, int count, GemmDesc *dev, const int *Mc, const int *Nc, cudaStream_t s) {
   set_descs_kernel<<<1, 32, 0, s>>>(d, dev, count);
   TT_TRY(check_launch("set_descs"));
-  for (int i = 0; i < count; ++i) TT_TRY(launch_gemm(dev + i, 1, Mc[i], Nc[i], s));
+  for (int i = 0; i < count; ++i) TT_TRY(launch_gemm_k(dev + i, 1, Mc[i], Nc[i], d.g[i].K, s));
   return TT_OK;
 }
 
@@ -36,6 +36,7 @@ size_t als_ws_bytes(long long rA, long long R, long long rB, long long m, long l
   b += ((size_t)mx * 8 + 255) & ~size_t(255);
   b += ((size_t)mx2 * 8 + 255) & ~size_t(255);
   b += ((3 * sizeof(GemmDesc)) + 255) & ~size_t(255);
+  b += GEMM_SPLIT_SCRATCH;
   return b;
 }
 
@@ -68,6 +69,7 @@ extern "C" tt_status als_local_apply(int32_t rA, int32_t R, int32_t rB, int32_t 
   double *T1 = ar.take<double>(mx);
   double *T2 = ar.take<double>(mx);
   GemmDesc *dev = ar.take<GemmDesc>(3);
+  set_gemm_scratch(ar.take<double>(GEMM_SPLIT_SCRATCH / 8), GEMM_SPLIT_SCRATCH);
   Desc3 d;
   descs_local_apply(rA, R, rB, m, n, rAp, Rp, rBp, Phi, Ak, Psi, x, y, T1, T2, d.g);
   int Mc[3] = {rB * n, R * m, rA}, Nc[3] = {rAp * Rp, rB * rAp, m * rAp};
@@ -94,6 +96,7 @@ extern "C" tt_status als_update_interfaces(int32_t dir, int32_t rY, int32_t R, i
   double *T1 = ar.take<double>(mx);
   double *T2 = ar.take<double>(mx);
   GemmDesc *dev = ar.take<GemmDesc>(3);
+  set_gemm_scratch(ar.take<double>(GEMM_SPLIT_SCRATCH / 8), GEMM_SPLIT_SCRATCH);
   Desc3 d;
   if (Ak) {
     if (dir > 0) {

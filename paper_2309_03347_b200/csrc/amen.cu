@@ -296,6 +296,7 @@ struct AmenCtx {
   double *H, *h1, *h2;
   char *orth_base;
   size_t orth_cap;
+  double *split;
 };
 
 static tt_status carve_amen(const MatMeta &A, const VecMeta &b, const VecMeta &x, const VecMeta &z, int m, Arena &ar,
@@ -389,6 +390,7 @@ static tt_status carve_amen(const MatMeta &A, const VecMeta &b, const VecMeta &x
   orth_meta(z, -1, nullptr, c2, nullptr);
   P.orth_cap = c1.used > c2.used ? c1.used : c2.used;
   P.orth_base = ar.take<char>(P.orth_cap);
+  P.split = ar.take<double>(GEMM_SPLIT_SCRATCH / 8);
   return TT_OK;
 }
 
@@ -428,6 +430,7 @@ tt_status amen_solve_meta(const MatMeta &A, const VecMeta &b, const VecMeta &x, 
   }
   set_gm_H<<<1, 1, 0, s>>>(P.gst, P.H);
   set_dv_kernel<<<1, 1, 0, s>>>(D.dv, 1, o.eps);
+  set_gemm_scratch(P.split, GEMM_SPLIT_SCRATCH);
   Arena oa;
   oa.base = P.orth_base;
   oa.cap = P.orth_cap;
@@ -439,7 +442,8 @@ tt_status amen_solve_meta(const MatMeta &A, const VecMeta &b, const VecMeta &x, 
   const int *xc = x.rcap, *zc = z.rcap, *bc = b.rcap, *Rc = A.Rcap;
   struct Caps12 { GemmDesc g[12]; int cnt; };
   auto launch_caps = [&](const GemmDesc *dev, const Caps12 &hc, int from, int cnt) -> tt_status {
-    for (int i = 0; i < cnt; ++i) TT_TRY(launch_gemm(dev + i, 1, hc.g[from + i].M, hc.g[from + i].N, s));
+    for (int i = 0; i < cnt; ++i)
+      TT_TRY(launch_gemm_k(dev + i, 1, hc.g[from + i].M, hc.g[from + i].N, hc.g[from + i].K, s));
     return TT_OK;
   };
   auto iface_caps = [&](int k, int dir) {

@@ -77,15 +77,31 @@ __device__ __forceinline__ void load_tile(Tile &t, int buf, const GemmDesc &g, i
   }
 }
 
-__global__ void __launch_bounds__(128) gemm_dmma_kernel(const GemmDesc *__restrict__ descs) {
+// splits > 1: split-K; CTA z computes the K-slice z and writes its raw partial
+// product to partial + z * pstride (column-major, ld = pld); gemm_splitk_reduce
+// sums the slices and applies the epilogue (deterministic order).
+__global__ void __launch_bounds__(128) gemm_dmma_kernel(const GemmDesc *__restrict__ descs, int splits,
+                                                        double *__restrict__ partial, long long pld,
+                                                        long long pstride) {
   __shared__ __align__(16) Tile t;
-  const GemmDesc g = descs[blockIdx.z];
+  const GemmDesc g0 = descs[splits > 1 ? 0 : blockIdx.z];
   const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN;
-  if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0 && g.M > 0 && g.N > 0) {
-    atomicAdd(&g_gemm_counters[0], 2ull * (unsigned long long)g.M * g.N * (g.K > 0 ? g.K : 0));
+  if (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && threadIdx.x == 0 && g0.M > 0 && g0.N > 0) {
+    atomicAdd(&g_gemm_counters[0], 2ull * (unsigned long long)g0.M * g0.N * (g0.K > 0 ? g0.K : 0));
     atomicAdd(&g_gemm_counters[1], 1ull);
   }
-  if (m0 >= g.M || n0 >= g.N) return;
+  if (m0 >= g0.M || n0 >= g0.N) return;
+  GemmDesc g = g0;
+  int kbeg = 0;
+  if (splits > 1) {
+    const int kc = ((g0.K + splits - 1) / splits + BK - 1) / BK * BK;
+    kbeg = blockIdx.z * kc;
+    const int kend = min(g0.K, kbeg + kc);
+    g.K = kend > kbeg ? kend - kbeg : 0;
+    // shift the operands to the K-slice
+    g.A = g0.transA ? g0.A + kbeg : g0.A + (long long)kbeg * g0.lda;
+    g.B = g0.transB ? g0.B + (long long)kbeg * g0.ldb : g0.B + kbeg;
+  }
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wm = (warp & 1) * 32, wn = (warp >> 1) * 32;
   double acc[4][4][2];
@@ -121,6 +137,22 @@ __global__ void __launch_bounds__(128) gemm_dmma_kernel(const GemmDesc *__restri
     }
     __syncthreads();
   }
+  if (splits > 1) {
+    double *P = partial + (long long)blockIdx.z * pstride;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int r = m0 + wm + i * 8 + (lane >> 2);
+      if (r >= g.M) continue;
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int c = n0 + wn + j * 8 + (lane & 3) * 2 + h;
+          if (c < g.N) P[r + c * pld] = acc[i][j][h];
+        }
+    }
+    return;
+  }
   double alpha = g.alpha;
   if (g.alpha_dev) alpha *= *g.alpha_dev;
   const double beta = g.beta;
@@ -144,12 +176,63 @@ __global__ void __launch_bounds__(128) gemm_dmma_kernel(const GemmDesc *__restri
   }
 }
 
+__global__ void gemm_splitk_reduce(const GemmDesc *__restrict__ descs, int splits, const double *__restrict__ partial,
+                                   long long pld, long long pstride) {
+  const GemmDesc g = descs[0];
+  const long long total = (long long)g.M * g.N;
+  double alpha = g.alpha;
+  if (g.alpha_dev) alpha *= *g.alpha_dev;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int r = (int)(e % g.M), c = (int)(e / g.M);
+    double s = 0.0;
+    for (int z = 0; z < splits; ++z) s += partial[z * pstride + r + c * pld];
+    const long long addr = (long long)(r % g.dr) * g.s_r0 + (long long)(r / g.dr) * g.s_r1 +
+                           (long long)(c % g.dc) * g.s_c0 + (long long)(c / g.dc) * g.s_c1;
+    double v = alpha * s;
+    if (g.beta != 0.0) v += g.beta * g.C[addr];
+    g.C[addr] = v;
+  }
+}
+
+struct SplitScratch {
+  double *ptr = nullptr;
+  size_t bytes = 0;
+};
+thread_local SplitScratch g_split;
+
 }  // namespace
 
+void set_gemm_scratch(double *ptr, size_t bytes) {
+  g_split.ptr = ptr;
+  g_split.bytes = ptr ? bytes : 0;
+}
+
 tt_status launch_gemm(const GemmDesc *descs_dev, int count, int Mcap, int Ncap, cudaStream_t s) {
+  return launch_gemm_k(descs_dev, count, Mcap, Ncap, 0, s);
+}
+
+tt_status launch_gemm_k(const GemmDesc *descs_dev, int count, int Mcap, int Ncap, int Kcap, cudaStream_t s) {
   if (count <= 0 || Mcap <= 0 || Ncap <= 0) return TT_OK;
-  dim3 grid((Mcap + BM - 1) / BM, (Ncap + BN - 1) / BN, count);
-  gemm_dmma_kernel<<<grid, 128, 0, s>>>(descs_dev);
+  const int tm = (Mcap + BM - 1) / BM, tn = (Ncap + BN - 1) / BN;
+  int splits = 1;
+  if (count == 1 && Kcap >= 256 && (long long)tm * tn < 148) {
+    splits = 296 / (tm * tn);
+    splits = splits > Kcap / 128 ? Kcap / 128 : splits;
+    splits = splits > 16 ? 16 : splits;
+    const size_t need = (size_t)splits * Mcap * Ncap * sizeof(double);
+    if (splits < 2 || !g_split.ptr || need > g_split.bytes) splits = 1;
+  }
+  if (splits > 1) {
+    const long long pld = Mcap, pstride = (long long)Mcap * Ncap;
+    gemm_dmma_kernel<<<dim3(tm, tn, splits), 128, 0, s>>>(descs_dev, splits, g_split.ptr, pld, pstride);
+    int rb = (int)((pstride + 255) / 256);
+    rb = rb > 1184 ? 1184 : (rb < 1 ? 1 : rb);
+    gemm_splitk_reduce<<<rb, 256, 0, s>>>(descs_dev, splits, g_split.ptr, pld, pstride);
+    return check_launch("gemm_dmma splitk");
+  }
+  dim3 grid(tm, tn, count);
+  gemm_dmma_kernel<<<grid, 128, 0, s>>>(descs_dev, 1, nullptr, 0, 0);
   return check_launch("gemm_dmma");
 }
 

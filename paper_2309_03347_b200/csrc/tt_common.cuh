@@ -91,6 +91,12 @@ __host__ __device__ inline void gemm_plain_c(GemmDesc &g, double *C, long long l
 // Launch `count` GEMMs described at descs_dev[0..count) with a grid sized for
 // Mcap x Ncap (tiles beyond the device-side M, N exit immediately).
 tt_status launch_gemm(const GemmDesc *descs_dev, int count, int Mcap, int Ncap, cudaStream_t s);
+// With Kcap (host upper bound of K) the launcher may split K across CTAs when the
+// output has few tiles, using the scratch registered by set_gemm_scratch (the
+// calling thread's current workspace slice); deterministic slice-sum reduction.
+tt_status launch_gemm_k(const GemmDesc *descs_dev, int count, int Mcap, int Ncap, int Kcap, cudaStream_t s);
+void set_gemm_scratch(double *ptr, size_t bytes);
+constexpr size_t GEMM_SPLIT_SCRATCH = 32ull << 20;  // bytes reserved by callers that enable split-K
 
 // ------------------------------------------------------------- linalg ---
 // Householder QR of an m x n column-major matrix (one CTA per problem,

@@ -1,0 +1,65 @@
+"""ALS double sweep over a TT (BASELINE.json configs[4]):
+for k = 1..d-1 (left-to-right) als_local_apply + left interface update, then
+for k = d..2 (right-to-left) als_local_apply + right interface update — the
+K7 + K8 skeleton of an AMEn sweep without the local solve.  Every contraction
+is a libtt C-ABI call (DMMA GEMM chains); this module only sequences them."""
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from .tt import als_local_apply, als_update_interfaces
+
+
+class SweepProblem:
+    def __init__(self, A_cores, X_cores, device="cuda"):
+        self.d = len(X_cores)
+        self.n = [c.shape[1] for c in X_cores]
+        self.r = [c.shape[0] for c in X_cores] + [1]
+        self.R = [c.shape[0] for c in A_cores] + [1]
+        dev = torch.device(device)
+        f = lambda a: torch.from_numpy(np.ascontiguousarray(np.asarray(a).reshape(-1, order="F"))).to(dev)
+        self.X = [f(c) for c in X_cores]
+        self.A = [f(c) for c in A_cores]
+        # interfaces at every bond (left Phi and right Psi), [r, R, r]
+        self.Phi = [torch.zeros(self.r[k] * self.R[k] * self.r[k], dtype=torch.float64, device=dev)
+                    for k in range(self.d + 1)]
+        self.Psi = [torch.zeros(self.r[k] * self.R[k] * self.r[k], dtype=torch.float64, device=dev)
+                    for k in range(self.d + 1)]
+        self.Phi[0].fill_(1.0)
+        self.Psi[self.d].fill_(1.0)
+        mx = max(self.r[k] * self.n[k] * self.r[k + 1] for k in range(self.d))
+        self.y = torch.zeros(mx, dtype=torch.float64, device=dev)
+
+    def dims_apply(self, k):
+        r0, r1, n = self.r[k], self.r[k + 1], self.n[k]
+        return (r0, self.R[k], r0, n, n, r1, self.R[k + 1], r1)
+
+    def build_right(self, normalize=True):
+        """Untimed setup: right interfaces Psi_k for k = d-1..1 (Z25: normalised)."""
+        for k in range(self.d - 1, 0, -1):
+            als_update_interfaces(-1, self.dims_apply(k), self.Psi[k + 1], self.X[k], self.A[k], self.X[k],
+                                  self.Psi[k])
+            if normalize:
+                self.Psi[k].div_(self.Psi[k].norm())
+
+    def double_sweep(self):
+        for k in range(self.d - 1):
+            als_local_apply(self.dims_apply(k), self.Phi[k], self.A[k], self.Psi[k + 1], self.X[k], self.y)
+            als_update_interfaces(+1, self.dims_apply(k), self.Phi[k], self.X[k], self.A[k], self.X[k],
+                                  self.Phi[k + 1])
+        for k in range(self.d - 1, 0, -1):
+            als_local_apply(self.dims_apply(k), self.Phi[k], self.A[k], self.Psi[k + 1], self.X[k], self.y)
+            als_update_interfaces(-1, self.dims_apply(k), self.Psi[k + 1], self.X[k], self.A[k], self.X[k],
+                                  self.Psi[k])
+
+    def flops(self):
+        """Algorithmic flops of one double sweep."""
+        tot = 0
+        visits = list(range(self.d - 1)) + list(range(self.d - 1, 0, -1))
+        for k in visits:
+            rA, R, rB, m, n, rAp, Rp, rBp = self.dims_apply(k)
+            apply = 2 * (n * rB * rBp * rAp * Rp + m * n * rB * rAp * R * Rp + m * rA * rAp * rB * R)
+            upd = 2 * (m * rA * rB * rAp * R + m * n * rB * rAp * R * Rp + n * rB * rBp * rAp * Rp)
+            tot += apply + upd
+        return tot
