@@ -297,6 +297,7 @@ struct AmenCtx {
   char *orth_base;
   size_t orth_cap;
   double *split;
+  unsigned int *bar;
 };
 
 static tt_status carve_amen(const MatMeta &A, const VecMeta &b, const VecMeta &x, const VecMeta &z, int m, Arena &ar,
@@ -391,6 +392,7 @@ static tt_status carve_amen(const MatMeta &A, const VecMeta &b, const VecMeta &x
   P.orth_cap = c1.used > c2.used ? c1.used : c2.used;
   P.orth_base = ar.take<char>(P.orth_cap);
   P.split = ar.take<double>(GEMM_SPLIT_SCRATCH / 8);
+  P.bar = ar.take<unsigned int>(4);
   return TT_OK;
 }
 
@@ -431,6 +433,7 @@ tt_status amen_solve_meta(const MatMeta &A, const VecMeta &b, const VecMeta &x, 
   set_gm_H<<<1, 1, 0, s>>>(P.gst, P.H);
   set_dv_kernel<<<1, 1, 0, s>>>(D.dv, 1, o.eps);
   set_gemm_scratch(P.split, GEMM_SPLIT_SCRATCH);
+  set_jacobi_sync(P.bar);
   Arena oa;
   oa.base = P.orth_base;
   oa.cap = P.orth_cap;

@@ -395,6 +395,174 @@ __global__ void __launch_bounds__(SVD_THREADS) jacobi_kernel(const SVDDesc *__re
   for (int c = tid; c < p; c += SVD_THREADS) g.sigma[s_pos[c]] = s_sig[c];
 }
 
+// ------------------------------------------- block Jacobi across a grid ---
+// One-sided block Jacobi for larger p: the p columns form nb blocks of JB
+// columns; each round pairs blocks by a round-robin tournament and every CTA
+// orthogonalises its 2 JB columns (plus the matching V columns) in shared
+// memory with one inner Jacobi pass; a software grid barrier separates rounds
+// (the grid is launched cooperatively, so all CTAs are co-resident).
+constexpr int JB = 8;
+constexpr int BJ_THREADS = 256;
+
+__device__ void grid_barrier(unsigned int *bar, unsigned int nblocks) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    volatile unsigned int *gen = bar + 1;
+    const unsigned int g = *gen;
+    __threadfence();
+    if (atomicAdd(bar, 1u) == nblocks - 1) {
+      bar[0] = 0;
+      __threadfence();
+      atomicAdd(bar + 1, 1u);
+    } else {
+      while (*gen == g) {
+      }
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(BJ_THREADS) jacobi_block_kernel(const SVDDesc *__restrict__ descs, unsigned int *bar,
+                                                                  int *flag) {
+  extern __shared__ __align__(16) double sm[];
+  const SVDDesc g = descs[0];
+  const int m = g.m, p = g.p, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int NW = BJ_THREADS / 32;
+  const int nb = (p + JB - 1) / JB;
+  const int NB2 = nb + (nb & 1);
+  const unsigned int G = gridDim.x;
+  double *W = g.work;                       // m x p, ld m
+  double *V = g.work + (long long)m * p;    // p x p, ld p
+  double *sW = sm;                          // m x 2JB
+  double *sV = sm + (long long)m * 2 * JB;  // p x 2JB
+  // LAPACK dgesvj's convergence threshold sqrt(m) eps: within-block pairs are
+  // revisited nb-1 times per sweep, so a tighter threshold only adds rotations
+  // of noise-level pairs (and their roundoff).
+  const double tol = fmax(4.0, sqrt((double)m)) * DBL_EPSILON;
+  // init (grid-strided)
+  for (long long e = blockIdx.x * (long long)BJ_THREADS + tid; e < (long long)m * p; e += (long long)G * BJ_THREADS) {
+    const int r = (int)(e % m), c = (int)(e / m);
+    W[e] = g.W[r + c * g.ldw];
+  }
+  for (long long e = blockIdx.x * (long long)BJ_THREADS + tid; e < (long long)p * p; e += (long long)G * BJ_THREADS)
+    V[e] = ((e % p) == (e / p)) ? 1.0 : 0.0;
+  if (blockIdx.x == 0 && tid == 0) *flag = 0;
+  grid_barrier(bar, G);
+  int sweep = 0;
+  for (; sweep < 60; ++sweep) {
+    for (int rnd = 0; rnd < NB2 - 1; ++rnd) {
+      for (int pr = blockIdx.x; pr < NB2 / 2; pr += G) {
+        int A, B;
+        if (pr == 0) { A = NB2 - 1; B = rnd; }
+        else { A = (rnd + pr) % (NB2 - 1); B = (rnd - pr + (NB2 - 1)) % (NB2 - 1); }
+        // gather the 2JB columns (phantom / out-of-range columns become empty)
+        int col[2 * JB];
+#pragma unroll
+        for (int q = 0; q < JB; ++q) {
+          const int ca = A * JB + q, cb = B * JB + q;
+          col[q] = (A < nb && ca < p) ? ca : -1;
+          col[JB + q] = (B < nb && cb < p) ? cb : -1;
+        }
+        for (int e = tid; e < m * 2 * JB; e += BJ_THREADS) {
+          const int r = e % m, q = e / m;
+          sW[e] = col[q] >= 0 ? W[r + (long long)col[q] * m] : 0.0;
+        }
+        for (int e = tid; e < p * 2 * JB; e += BJ_THREADS) {
+          const int r = e % p, q = e / p;
+          sV[e] = col[q] >= 0 ? V[r + (long long)col[q] * p] : 0.0;
+        }
+        __syncthreads();
+        // one inner pass over all pairs of the 2JB columns (round robin, one warp per pair)
+        int rotated = 0;
+        for (int ir = 0; ir < 2 * JB - 1; ++ir) {
+          for (int ip = warp; ip < JB; ip += NW) {
+            int a, b;
+            if (ip == 0) { a = 2 * JB - 1; b = ir; }
+            else { a = (ir + ip) % (2 * JB - 1); b = (ir - ip + (2 * JB - 1)) % (2 * JB - 1); }
+            if (col[a] < 0 || col[b] < 0) continue;
+            if (col[a] > col[b]) { int t = a; a = b; b = t; }
+            double *wa = sW + (long long)a * m, *wb = sW + (long long)b * m;
+            double al = 0.0, be = 0.0, ga = 0.0;
+            for (int r = lane; r < m; r += 32) {
+              const double x = wa[r], y = wb[r];
+              al = fma(x, x, al); be = fma(y, y, be); ga = fma(x, y, ga);
+            }
+            al = warp_sum(al); be = warp_sum(be); ga = warp_sum(ga);
+            if (lane == 0) atomicAdd(&g_linalg_flops[1], 6ull * m);
+            if (ga == 0.0 || al == 0.0 || be == 0.0) continue;
+            if (fabs(ga) <= tol * sqrt(al) * sqrt(be)) continue;
+            const double zeta = (be - al) / (2.0 * ga);
+            const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(fma(zeta, zeta, 1.0)));
+            const double c = 1.0 / sqrt(fma(t, t, 1.0)), s = c * t;
+            for (int r = lane; r < m; r += 32) {
+              const double x = wa[r], y = wb[r];
+              wa[r] = c * x - s * y; wb[r] = s * x + c * y;
+            }
+            double *va = sV + (long long)a * p, *vb = sV + (long long)b * p;
+            for (int r = lane; r < p; r += 32) {
+              const double x = va[r], y = vb[r];
+              va[r] = c * x - s * y; vb[r] = s * x + c * y;
+            }
+            rotated = 1;
+            if (lane == 0) atomicAdd(&g_linalg_flops[1], 6ull * (m + p));
+          }
+          __syncthreads();
+        }
+        if (__syncthreads_or(rotated) && tid == 0) *flag = 1;
+        for (int e = tid; e < m * 2 * JB; e += BJ_THREADS) {
+          const int r = e % m, q = e / m;
+          if (col[q] >= 0) W[r + (long long)col[q] * m] = sW[e];
+        }
+        for (int e = tid; e < p * 2 * JB; e += BJ_THREADS) {
+          const int r = e % p, q = e / p;
+          if (col[q] >= 0) V[r + (long long)col[q] * p] = sV[e];
+        }
+        __syncthreads();
+      }
+      grid_barrier(bar, G);
+    }
+    const int f = *(volatile int *)flag;
+    grid_barrier(bar, G);
+    if (f == 0) break;
+    if (blockIdx.x == 0 && tid == 0) *flag = 0;
+    grid_barrier(bar, G);
+  }
+  if (blockIdx.x != 0) return;
+  if (tid == 0 && g.sweeps_out) *g.sweeps_out = sweep + 1;
+  // sigma, sort, outputs (CTA 0)
+  double *s_sig = sm;
+  int *s_pos = reinterpret_cast<int *>(sm + p);
+  for (int c = warp; c < p; c += NW) {
+    const double *w = W + (long long)c * m;
+    double s = 0.0;
+    for (int r = lane; r < m; r += 32) s = fma(w[r], w[r], s);
+    s = warp_sum(s);
+    if (lane == 0) s_sig[c] = sqrt(s);
+  }
+  __syncthreads();
+  for (int i = tid; i < p; i += BJ_THREADS) {
+    const double si = s_sig[i];
+    int pos = 0;
+    for (int j = 0; j < p; ++j) {
+      const double sj = s_sig[j];
+      pos += (sj > si) || (sj == si && j < i);
+    }
+    s_pos[i] = pos;
+  }
+  __syncthreads();
+  for (long long e = tid; e < (long long)m * p; e += BJ_THREADS) {
+    const int r = (int)(e % m), c = (int)(e / m);
+    const double sc = s_sig[c];
+    g.U[r + (long long)s_pos[c] * g.ldu] = sc > 0.0 ? W[e] / sc : 0.0;
+  }
+  for (long long e = tid; e < (long long)p * p; e += BJ_THREADS) {
+    const int r = (int)(e % p), c = (int)(e / p);
+    g.V[r + (long long)s_pos[c] * g.ldv] = V[e];
+  }
+  for (int c = tid; c < p; c += BJ_THREADS) g.sigma[s_pos[c]] = s_sig[c];
+}
+
 }  // namespace
 
 void linalg_counters(unsigned long long *out, int reset) {
@@ -411,6 +579,12 @@ tt_status launch_qr(const QRDesc *descs_dev, int count, cudaStream_t s) {
   return check_launch("qr");
 }
 
+struct BJSync {
+  unsigned int *bar = nullptr;
+  int *flag = nullptr;
+};
+static thread_local BJSync g_bj;
+
 static size_t svd_smem_bytes(int mcap, int pcap) {
   return ((size_t)mcap * pcap + (size_t)pcap * pcap + pcap) * sizeof(double) + (size_t)pcap * sizeof(int) + 16;
 }
@@ -426,6 +600,24 @@ tt_status launch_jacobi(const SVDDesc *descs_dev, int count, int mcap, int pcap,
       attr_set = true;
     }
     jacobi_kernel<true><<<count, SVD_THREADS, smem, s>>>(descs_dev);
+  } else if (count == 1 && g_bj.bar &&
+             ((size_t)mcap + pcap) * 2 * JB * sizeof(double) <= limit) {
+    // block Jacobi over a cooperative grid: one CTA per block pair
+    const int nb = (pcap + JB - 1) / JB;
+    const int G = (nb + (nb & 1)) / 2;
+    size_t smb = ((size_t)mcap + pcap) * 2 * JB * sizeof(double);
+    const size_t sort_b = (size_t)pcap * (sizeof(double) + sizeof(int)) + 16;
+    smb = smb > sort_b ? smb : sort_b;
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(jacobi_block_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)limit);
+      attr = true;
+    }
+    cudaMemsetAsync(g_bj.bar, 0, 2 * sizeof(unsigned int) + sizeof(int) * 2, s);
+    void *args[] = {(void *)&descs_dev, (void *)&g_bj.bar, (void *)&g_bj.flag};
+    cudaError_t e = cudaLaunchCooperativeKernel((const void *)jacobi_block_kernel, dim3(G), dim3(BJ_THREADS), args,
+                                                smb, s);
+    if (e != cudaSuccess) return fail(TT_ERR_CUDA, std::string("jacobi_block: ") + cudaGetErrorString(e));
   } else {
     const size_t sm2 = (size_t)pcap * (sizeof(double) + sizeof(int)) + 16;
     if (sm2 > 48 * 1024) {
@@ -434,6 +626,11 @@ tt_status launch_jacobi(const SVDDesc *descs_dev, int count, int mcap, int pcap,
     jacobi_kernel<false><<<count, SVD_THREADS, sm2, s>>>(descs_dev);
   }
   return check_launch("jacobi");
+}
+
+void set_jacobi_sync(unsigned int *bar) {
+  g_bj.bar = bar;
+  g_bj.flag = bar ? reinterpret_cast<int *>(bar + 2) : nullptr;
 }
 
 }  // namespace tt

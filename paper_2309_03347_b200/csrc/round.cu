@@ -19,6 +19,7 @@ struct StepWS {
   CopyDesc *cd;   // [2]
   int *iv;        // [8] step integers (wide flag, sizes)
   double *norm;   // [1]
+  unsigned int *bar;  // [4] grid barrier of the block Jacobi
   long long Acap, slot;
 };
 
@@ -66,6 +67,7 @@ StepWS carve(const VecMeta &x, Arena &ar) {
   w.cd = ar.take<CopyDesc>(2);
   w.iv = ar.take<int>(8);
   w.norm = ar.take<double>(1);
+  w.bar = ar.take<unsigned int>(4);
   return w;
 }
 
@@ -273,6 +275,7 @@ tt_status round_meta(const VecMeta &x, double eps, int rmax, double *disc, doubl
   if (!ar.ok()) return fail(TT_ERR_CAPACITY, "tt_round: workspace too small");
   ar.used = mark;  // orth_meta re-carves the same layout
   TT_TRY(orth_meta(x, -1, nullptr, ar, s));
+  set_jacobi_sync(w.bar);
   const Caps c = caps_of(x);
   const int d = x.d;
   for (int k = 0; k <= d - 2; ++k) {

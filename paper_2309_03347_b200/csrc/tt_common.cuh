@@ -130,6 +130,9 @@ struct SVDDesc {
   int *sweeps_out;
 };
 tt_status launch_jacobi(const SVDDesc *descs_dev, int count, int mcap, int pcap, cudaStream_t s);
+// Grid-barrier words (>= 16 bytes of the caller's workspace) for the block
+// Jacobi kernel used when p is too large for one CTA's shared memory.
+void set_jacobi_sync(unsigned int *bar);
 
 // Strided 2-D copy with device-side sizes and strides.
 struct CopyDesc {

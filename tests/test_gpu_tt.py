@@ -187,8 +187,13 @@ def test_round_c2_d30_rmax128(seed):
     ref, info = ott.tt_round(Yc, 1e-8, 128)
     assert Y.ranks() == ott.ranks(ref)
     s1 = max(s[0] for s in info["sv"])
+    # Z22: rmax binds on most bonds here, so each bond's singular values inherit the
+    # roundoff of every earlier truncated subspace (~20 chained cuts): 2e-12 sigma_1
+    binds = 0
     for k, s in enumerate(info["sv"]):
-        assert np.max(np.abs(sv[k, :len(s)].cpu().numpy() - s)) <= 1e-12 * s1
+        tol = (1e-12 if binds == 0 else 2e-12) * s1
+        assert np.max(np.abs(sv[k, :len(s)].cpu().numpy() - s)) <= tol
+        binds += int(ott.ranks(ref)[k + 1] < len(s))
     nrm = info["norm"]
     # near-ties at the cut make the truncated subspace ill-determined: skip those bonds
     ties = any(r < len(s) and abs(s[r - 1] - s[r]) <= 1e-10 * s1
@@ -196,6 +201,23 @@ def test_round_c2_d30_rmax128(seed):
     if not ties:
         assert tt_diff_norm(Y.cores(), ref) <= 1e-12 * nrm + math.sqrt(sum(info["discarded_sq"])) * 1e-6
     assert max(Y.ranks()) <= 128
+
+
+@pytest.mark.parametrize("p", [100, 200, 256])
+def test_round_large_bond_svd(p):
+    """d=2 TT with a p x p bond: the truncation SVD runs the shared-memory Jacobi
+    (p <= 112) or the grid block Jacobi (p > 112); singular values vs LAPACK."""
+    g = inputs.rng(45 + p)
+    M = g.standard_normal((p, p)) @ np.diag(np.logspace(0, -10, p)) @ g.standard_normal((p, p))
+    X = [M.reshape(1, p, p), np.eye(p).reshape(p, p, 1)]
+    G = tb.TTVec.from_cores(X)
+    _, disc, sv = tb.tt_round(G, 0.0, want_info=True)
+    s_ref = np.linalg.svd(M, compute_uv=False)
+    s_got = sv[0, :p].cpu().numpy()
+    err = np.max(np.abs(s_got - s_ref)) / s_ref[0]
+    assert err <= 5e-13, err        # ~ sqrt(p) x sweeps x eps for one kappa = 1e10 SVD
+    # M has condition 1e10 by construction: the reconstruction carries ~cond * eps in the small directions
+    assert rel(ott.tt_full(G.cores()), M.reshape(-1, order="F")) <= 1e-12
 
 
 def test_round_special_cases():
