@@ -172,6 +172,7 @@ def main():
     ap.add_argument("--workload", default="c1", choices=["c1", "c2", "c5"])
     ap.add_argument("--rank", type=int, default=128, help="c5 interface rank (64, 128, 256)")
     ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--no-graph", action="store_true", help="c5: launch the sweep without a CUDA graph")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
@@ -321,15 +322,18 @@ def micro_bench(args, tb, device, world, dist):
         inst = inputs.c5_instance(args.rank, seed=args.seed)
         sp = SweepProblem(inst["A"], inst["X"], device)
         sp.build_right()
+        run = sp.double_sweep
+        if not args.no_graph:
+            run = sp.capture().replay
         for _ in range(args.warmup):
-            sp.double_sweep()
+            run()
         ms = []
         with ClockSampler(torch.cuda.current_device()) as clk:
             for _ in range(args.steps):
                 flush.fill_(1.0)
                 e0, e1 = _events()
                 e0.record(s)
-                sp.double_sweep()
+                run()
                 e1.record(s)
                 e1.synchronize()
                 ms.append(e0.elapsed_time(e1))
@@ -342,6 +346,7 @@ def micro_bench(args, tb, device, world, dist):
                 "vs_baseline": None, "dtype": "f64", "data": "synthetic",
                 "config": {"workload": f"C5 (configs[4]) ALS double sweep, d=40, r={args.rank}, R 5-8, "
                                        f"n in {{2,4,8,16}}, seed {args.seed}",
+                           "launch": "CUDA graph of the 80 core visits" if not args.no_graph else "stream",
                            "l2": "256 MB flush between timed steps"},
                 "pct_dmma_peak": 100.0 * gfl / peak, "flops_per_step": flops, "ms_p10_p90": [
                     float(np.percentile(ms, 10)), float(np.percentile(ms, 90))],

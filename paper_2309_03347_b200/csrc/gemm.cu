@@ -1,8 +1,13 @@
 // FP64 tensor-core GEMM for sm_100a: mma.sync.m8n8k4.f64 (SASS DMMA.8x8x4).
 // tcgen05 has no f64 kind, so FP64 tensor work on Blackwell is warp-level
-// DMMA.  64x64x16 CTA tile, 4 warps of 32x32, operands staged
-// through double-buffered shared memory with cp.async (zero-filled edges),
-// descriptor read from device memory so sizes can follow device ranks.
+// DMMA.  Templated CTA tile (BM x BN x BK) of WARPS_M x
+// WARPS_N warps, each computing a (BM/WARPS_M) x (BN/WARPS_N) block of 8x8
+// DMMA tiles; operands staged through multi-stage cp.async shared-memory
+// buffers (zero-filled edges); the descriptor is read from device memory so
+// sizes can follow device-resident ranks; optional split-K with a
+// deterministic slice reduction.
+#include <cstdlib>
+
 #include "tt_common.cuh"
 
 namespace tt {
@@ -12,7 +17,7 @@ __device__ unsigned long long g_gemm_counters[2];
 
 namespace {
 
-constexpr int BM = 64, BN = 64, BK = 16, PAD = 4;
+constexpr int PAD = 4;
 
 __device__ __forceinline__ void cp_async8(void *smem, const void *gmem, bool pred) {
   unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
@@ -20,7 +25,8 @@ __device__ __forceinline__ void cp_async8(void *smem, const void *gmem, bool pre
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(sz));
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
 __device__ __forceinline__ void dmma(double &c0, double &c1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
@@ -28,51 +34,54 @@ __device__ __forceinline__ void dmma(double &c0, double &c1, double a, double b)
                : "d"(a), "d"(b));
 }
 
-struct Tile {
-  double a[2][BK][BM + PAD];
-  double b[2][BK][BN + PAD];
+template <int BM, int BN, int BK, int WM_, int WN_, int STAGES>
+struct Cfg {
+  static constexpr int WARPS = WM_ * WN_;
+  static constexpr int THREADS = 32 * WARPS;
+  static constexpr int TM = BM / WM_ / 8;  // 8x8 tiles per warp along M
+  static constexpr int TN = BN / WN_ / 8;
+  static constexpr int A_ELEMS = BK * (BM + PAD);
+  static constexpr int B_ELEMS = BK * (BN + PAD);
+  static constexpr size_t SMEM = (size_t)STAGES * (A_ELEMS + B_ELEMS) * sizeof(double);
 };
 
-__device__ __forceinline__ void load_tile(Tile &t, int buf, const GemmDesc &g, int m0, int n0, int k0,
+template <class C, int BM, int BN, int BK>
+__device__ __forceinline__ void load_tile(double *sa, double *sb, const GemmDesc &g, int m0, int n0, int k0,
                                           int tid) {
+  constexpr int T = C::THREADS;
   const double *A = g.A, *B = g.B;
-  // A tile: BM x BK of op(A)
-  if (!g.transA) {
+  if (!g.transA) {  // A(m,k) = A[m + k lda]: consecutive threads along m
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      int m = tid & 63, k = (tid >> 6) + 2 * i;
-      int gm = m0 + m, gk = k0 + k;
-      bool p = gm < g.M && gk < g.K;
-      const double *src = p ? A + gm + (long long)gk * g.lda : A;
-      cp_async8(&t.a[buf][k][m], src, p);
+    for (int e = tid; e < BM * BK; e += T) {
+      const int m = e % BM, k = e / BM;
+      const int gm = m0 + m, gk = k0 + k;
+      const bool p = gm < g.M && gk < g.K;
+      cp_async8(sa + k * (BM + PAD) + m, p ? A + gm + (long long)gk * g.lda : A, p);
     }
-  } else {
+  } else {  // A(m,k) = A[k + m lda]: consecutive threads along k
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      int k = tid & 15, m = (tid >> 4) + 8 * i;
-      int gm = m0 + m, gk = k0 + k;
-      bool p = gm < g.M && gk < g.K;
-      const double *src = p ? A + gk + (long long)gm * g.lda : A;
-      cp_async8(&t.a[buf][k][m], src, p);
+    for (int e = tid; e < BM * BK; e += T) {
+      const int k = e % BK, m = e / BK;
+      const int gm = m0 + m, gk = k0 + k;
+      const bool p = gm < g.M && gk < g.K;
+      cp_async8(sa + k * (BM + PAD) + m, p ? A + gk + (long long)gm * g.lda : A, p);
     }
   }
-  if (!g.transB) {
+  if (!g.transB) {  // B(k,n) = B[k + n ldb]
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      int k = tid & 15, n = (tid >> 4) + 8 * i;
-      int gn = n0 + n, gk = k0 + k;
-      bool p = gn < g.N && gk < g.K;
-      const double *src = p ? B + gk + (long long)gn * g.ldb : B;
-      cp_async8(&t.b[buf][k][n], src, p);
+    for (int e = tid; e < BN * BK; e += T) {
+      const int k = e % BK, n = e / BK;
+      const int gn = n0 + n, gk = k0 + k;
+      const bool p = gn < g.N && gk < g.K;
+      cp_async8(sb + k * (BN + PAD) + n, p ? B + gk + (long long)gn * g.ldb : B, p);
     }
-  } else {
+  } else {  // B(k,n) = B[n + k ldb]
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      int n = tid & 63, k = (tid >> 6) + 2 * i;
-      int gn = n0 + n, gk = k0 + k;
-      bool p = gn < g.N && gk < g.K;
-      const double *src = p ? B + gn + (long long)gk * g.ldb : B;
-      cp_async8(&t.b[buf][k][n], src, p);
+    for (int e = tid; e < BN * BK; e += T) {
+      const int n = e % BN, k = e / BN;
+      const int gn = n0 + n, gk = k0 + k;
+      const bool p = gn < g.N && gk < g.K;
+      cp_async8(sb + k * (BN + PAD) + n, p ? B + gn + (long long)gk * g.ldb : B, p);
     }
   }
 }
@@ -80,10 +89,14 @@ __device__ __forceinline__ void load_tile(Tile &t, int buf, const GemmDesc &g, i
 // splits > 1: split-K; CTA z computes the K-slice z and writes its raw partial
 // product to partial + z * pstride (column-major, ld = pld); gemm_splitk_reduce
 // sums the slices and applies the epilogue (deterministic order).
-__global__ void __launch_bounds__(128) gemm_dmma_kernel(const GemmDesc *__restrict__ descs, int splits,
-                                                        double *__restrict__ partial, long long pld,
-                                                        long long pstride) {
-  __shared__ __align__(16) Tile t;
+template <int BM, int BN, int BK, int WM_, int WN_, int STAGES>
+__global__ void __launch_bounds__(32 * WM_ * WN_) gemm_dmma_kernel(const GemmDesc *__restrict__ descs, int splits,
+                                                                   double *__restrict__ partial, long long pld,
+                                                                   long long pstride) {
+  using C = Cfg<BM, BN, BK, WM_, WN_, STAGES>;
+  extern __shared__ __align__(16) double smem[];
+  double *sA = smem;
+  double *sB = smem + STAGES * C::A_ELEMS;
   const GemmDesc g0 = descs[splits > 1 ? 0 : blockIdx.z];
   const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN;
   if (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && threadIdx.x == 0 && g0.M > 0 && g0.N > 0) {
@@ -92,59 +105,65 @@ __global__ void __launch_bounds__(128) gemm_dmma_kernel(const GemmDesc *__restri
   }
   if (m0 >= g0.M || n0 >= g0.N) return;
   GemmDesc g = g0;
-  int kbeg = 0;
   if (splits > 1) {
     const int kc = ((g0.K + splits - 1) / splits + BK - 1) / BK * BK;
-    kbeg = blockIdx.z * kc;
+    const int kbeg = blockIdx.z * kc;
     const int kend = min(g0.K, kbeg + kc);
     g.K = kend > kbeg ? kend - kbeg : 0;
-    // shift the operands to the K-slice
     g.A = g0.transA ? g0.A + kbeg : g0.A + (long long)kbeg * g0.lda;
     g.B = g0.transB ? g0.B + (long long)kbeg * g0.ldb : g0.B + kbeg;
   }
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int wm = (warp & 1) * 32, wn = (warp >> 1) * 32;
-  double acc[4][4][2];
+  const int wm = (warp % WM_) * (BM / WM_), wn = (warp / WM_) * (BN / WN_);
+  double acc[C::TM][C::TN][2];
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
+  for (int i = 0; i < C::TM; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    for (int j = 0; j < C::TN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
   const int nk = (g.K + BK - 1) / BK;
-  if (nk > 0) {
-    load_tile(t, 0, g, m0, n0, 0, tid);
+  // prologue: STAGES-1 tiles in flight
+#pragma unroll
+  for (int st = 0; st < STAGES - 1; ++st) {
+    if (st < nk) load_tile<C, BM, BN, BK>(sA + st * C::A_ELEMS, sB + st * C::B_ELEMS, g, m0, n0, st * BK, tid);
     cp_async_commit();
   }
   for (int kt = 0; kt < nk; ++kt) {
-    const int buf = kt & 1;
-    cp_async_wait_all();
+    cp_async_wait<STAGES - 2>();
     __syncthreads();
-    if (kt + 1 < nk) {
-      load_tile(t, buf ^ 1, g, m0, n0, (kt + 1) * BK, tid);
+    {  // issue the load of tile kt + STAGES - 1 into the slot freed at kt - 1
+      const int nt = kt + STAGES - 1;
+      if (nt < nk) {
+        const int sl = nt % STAGES;
+        load_tile<C, BM, BN, BK>(sA + sl * C::A_ELEMS, sB + sl * C::B_ELEMS, g, m0, n0, nt * BK, tid);
+      }
       cp_async_commit();
     }
+    const double *a = sA + (kt % STAGES) * C::A_ELEMS;
+    const double *b = sB + (kt % STAGES) * C::B_ELEMS;
 #pragma unroll
     for (int kk = 0; kk < BK; kk += 4) {
-      double af[4], bf[4];
+      double af[C::TM], bf[C::TN];
+      const int kr = kk + (lane & 3);
 #pragma unroll
-      for (int i = 0; i < 4; ++i) af[i] = t.a[buf][kk + (lane & 3)][wm + i * 8 + (lane >> 2)];
+      for (int i = 0; i < C::TM; ++i) af[i] = a[kr * (BM + PAD) + wm + i * 8 + (lane >> 2)];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) bf[j] = t.b[buf][kk + (lane & 3)][wn + j * 8 + (lane >> 2)];
+      for (int j = 0; j < C::TN; ++j) bf[j] = b[kr * (BN + PAD) + wn + j * 8 + (lane >> 2)];
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
+      for (int i = 0; i < C::TM; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) dmma(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+        for (int j = 0; j < C::TN; ++j) dmma(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
     }
-    __syncthreads();
   }
+  cp_async_wait<0>();
   if (splits > 1) {
     double *P = partial + (long long)blockIdx.z * pstride;
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
+    for (int i = 0; i < C::TM; ++i) {
       const int r = m0 + wm + i * 8 + (lane >> 2);
       if (r >= g.M) continue;
 #pragma unroll
-      for (int j = 0; j < 4; ++j)
+      for (int j = 0; j < C::TN; ++j)
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           const int c = n0 + wn + j * 8 + (lane & 3) * 2 + h;
@@ -156,18 +175,26 @@ __global__ void __launch_bounds__(128) gemm_dmma_kernel(const GemmDesc *__restri
   double alpha = g.alpha;
   if (g.alpha_dev) alpha *= *g.alpha_dev;
   const double beta = g.beta;
+  // scatter offsets: one div/mod per owned row and column (not per element)
+  long long coff[C::TN][2];
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
+  for (int j = 0; j < C::TN; ++j)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int c = n0 + wn + j * 8 + (lane & 3) * 2 + h;
+      coff[j][h] = (c < g.N) ? (long long)(c % g.dc) * g.s_c0 + (long long)(c / g.dc) * g.s_c1 : -1;
+    }
+#pragma unroll
+  for (int i = 0; i < C::TM; ++i) {
     const int r = m0 + wm + i * 8 + (lane >> 2);
     if (r >= g.M) continue;
     const long long roff = (long long)(r % g.dr) * g.s_r0 + (long long)(r / g.dr) * g.s_r1;
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
+    for (int j = 0; j < C::TN; ++j) {
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
-        const int c = n0 + wn + j * 8 + (lane & 3) * 2 + h;
-        if (c >= g.N) continue;
-        const long long addr = roff + (long long)(c % g.dc) * g.s_c0 + (long long)(c / g.dc) * g.s_c1;
+        if (coff[j][h] < 0) continue;
+        const long long addr = roff + coff[j][h];
         double v = alpha * acc[i][j][h];
         if (beta != 0.0) v += beta * g.C[addr];
         g.C[addr] = v;
@@ -201,6 +228,62 @@ struct SplitScratch {
 };
 thread_local SplitScratch g_split;
 
+// ---- variants: (BM, BN, BK, warps M, warps N, stages)
+template <int BM, int BN, int BK, int WM_, int WN_, int ST>
+struct Variant {
+  using C = Cfg<BM, BN, BK, WM_, WN_, ST>;
+  static constexpr int bm = BM, bn = BN;
+  static void prepare() {
+    static bool done = false;
+    if (!done) {
+      cudaFuncSetAttribute(gemm_dmma_kernel<BM, BN, BK, WM_, WN_, ST>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)C::SMEM);
+      done = true;
+    }
+  }
+  static void launch(dim3 grid, const GemmDesc *d, int splits, double *p, long long pld, long long ps, cudaStream_t s) {
+    prepare();
+    gemm_dmma_kernel<BM, BN, BK, WM_, WN_, ST><<<grid, C::THREADS, C::SMEM, s>>>(d, splits, p, pld, ps);
+  }
+};
+
+using V64 = Variant<64, 64, 16, 2, 2, 2>;     // round-1 baseline
+using V64K = Variant<64, 64, 32, 2, 2, 3>;    // deeper K, 3 stages
+using V128 = Variant<128, 64, 16, 4, 2, 3>;   // 8 warps
+using V128S = Variant<128, 128, 16, 4, 2, 2>; // 8 warps, 32x64 warp tiles
+
+int variant_id() {
+  static int v = -1;
+  if (v < 0) {
+    const char *e = std::getenv("TT_GEMM_VARIANT");
+    v = e ? std::atoi(e) : 0;
+  }
+  return v;
+}
+
+template <class Vt>
+tt_status launch_variant(const GemmDesc *descs_dev, int count, int Mcap, int Ncap, int Kcap, cudaStream_t s) {
+  const int tm = (Mcap + Vt::bm - 1) / Vt::bm, tn = (Ncap + Vt::bn - 1) / Vt::bn;
+  int splits = 1;
+  if (count == 1 && Kcap >= 256 && (long long)tm * tn < 148) {
+    splits = 296 / (tm * tn);
+    splits = splits > Kcap / 128 ? Kcap / 128 : splits;
+    splits = splits > 16 ? 16 : splits;
+    const size_t need = (size_t)splits * Mcap * Ncap * sizeof(double);
+    if (splits < 2 || !g_split.ptr || need > g_split.bytes) splits = 1;
+  }
+  if (splits > 1) {
+    const long long pld = Mcap, pstride = (long long)Mcap * Ncap;
+    Vt::launch(dim3(tm, tn, splits), descs_dev, splits, g_split.ptr, pld, pstride, s);
+    int rb = (int)((pstride + 255) / 256);
+    rb = rb > 1184 ? 1184 : (rb < 1 ? 1 : rb);
+    gemm_splitk_reduce<<<rb, 256, 0, s>>>(descs_dev, splits, g_split.ptr, pld, pstride);
+    return check_launch("gemm_dmma splitk");
+  }
+  Vt::launch(dim3(tm, tn, count), descs_dev, 1, nullptr, 0, 0, s);
+  return check_launch("gemm_dmma");
+}
+
 }  // namespace
 
 void set_gemm_scratch(double *ptr, size_t bytes) {
@@ -214,26 +297,12 @@ tt_status launch_gemm(const GemmDesc *descs_dev, int count, int Mcap, int Ncap, 
 
 tt_status launch_gemm_k(const GemmDesc *descs_dev, int count, int Mcap, int Ncap, int Kcap, cudaStream_t s) {
   if (count <= 0 || Mcap <= 0 || Ncap <= 0) return TT_OK;
-  const int tm = (Mcap + BM - 1) / BM, tn = (Ncap + BN - 1) / BN;
-  int splits = 1;
-  if (count == 1 && Kcap >= 256 && (long long)tm * tn < 148) {
-    splits = 296 / (tm * tn);
-    splits = splits > Kcap / 128 ? Kcap / 128 : splits;
-    splits = splits > 16 ? 16 : splits;
-    const size_t need = (size_t)splits * Mcap * Ncap * sizeof(double);
-    if (splits < 2 || !g_split.ptr || need > g_split.bytes) splits = 1;
+  switch (variant_id()) {
+    case 0: return launch_variant<V64>(descs_dev, count, Mcap, Ncap, Kcap, s);
+    case 2: return launch_variant<V128>(descs_dev, count, Mcap, Ncap, Kcap, s);
+    case 3: return launch_variant<V128S>(descs_dev, count, Mcap, Ncap, Kcap, s);
+    default: return launch_variant<V64K>(descs_dev, count, Mcap, Ncap, Kcap, s);
   }
-  if (splits > 1) {
-    const long long pld = Mcap, pstride = (long long)Mcap * Ncap;
-    gemm_dmma_kernel<<<dim3(tm, tn, splits), 128, 0, s>>>(descs_dev, splits, g_split.ptr, pld, pstride);
-    int rb = (int)((pstride + 255) / 256);
-    rb = rb > 1184 ? 1184 : (rb < 1 ? 1 : rb);
-    gemm_splitk_reduce<<<rb, 256, 0, s>>>(descs_dev, splits, g_split.ptr, pld, pstride);
-    return check_launch("gemm_dmma splitk");
-  }
-  dim3 grid(tm, tn, count);
-  gemm_dmma_kernel<<<grid, 128, 0, s>>>(descs_dev, 1, nullptr, 0, 0);
-  return check_launch("gemm_dmma");
 }
 
 void gemm_counters(unsigned long long *out, int reset) {

@@ -269,7 +269,7 @@ constexpr int SVD_THREADS = 256;
 __device__ void jacobi_core(int m, int p, double *W, long long ldw, double *V, long long ldv, double *s_sig,
                             int *s_pos, int *flag, int *sweeps_out) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  constexpr int NW = SVD_THREADS / 32;
+  const int NW = blockDim.x >> 5;
   const int P2 = p + (p & 1);  // even number of players (a phantom player is skipped)
   const double tol = 4.0 * DBL_EPSILON;
   int sweep = 0;
@@ -335,7 +335,7 @@ __device__ void jacobi_core(int m, int p, double *W, long long ldw, double *V, l
   }
   __syncthreads();
   // rank sort: position of column i in decreasing order (ties by index)
-  for (int i = tid; i < p; i += SVD_THREADS) {
+  for (int i = tid; i < p; i += blockDim.x) {
     const double si = s_sig[i];
     int pos = 0;
     for (int j = 0; j < p; ++j) {
@@ -348,7 +348,7 @@ __device__ void jacobi_core(int m, int p, double *W, long long ldw, double *V, l
 }
 
 template <bool SMEM>
-__global__ void __launch_bounds__(SVD_THREADS) jacobi_kernel(const SVDDesc *__restrict__ descs) {
+__global__ void __launch_bounds__(1024) jacobi_kernel(const SVDDesc *__restrict__ descs) {
   extern __shared__ __align__(16) double dsm[];
   __shared__ int s_flag;
   const SVDDesc g = descs[blockIdx.x];
@@ -372,27 +372,27 @@ __global__ void __launch_bounds__(SVD_THREADS) jacobi_kernel(const SVDDesc *__re
     s_sig = dsm;
     s_pos = reinterpret_cast<int *>(dsm + p);
   }
-  for (long long e = tid; e < (long long)m * p; e += SVD_THREADS) {
+  for (long long e = tid; e < (long long)m * p; e += blockDim.x) {
     const int r = (int)(e % m), c = (int)(e / m);
     W[r + c * ldw] = g.W[r + c * g.ldw];
   }
-  for (long long e = tid; e < (long long)p * p; e += SVD_THREADS) {
+  for (long long e = tid; e < (long long)p * p; e += blockDim.x) {
     const int r = (int)(e % p), c = (int)(e / p);
     V[r + c * ldv] = (r == c) ? 1.0 : 0.0;
   }
   __syncthreads();
   jacobi_core(m, p, W, ldw, V, ldv, s_sig, s_pos, &s_flag, g.sweeps_out);
   // sorted outputs
-  for (long long e = tid; e < (long long)m * p; e += SVD_THREADS) {
+  for (long long e = tid; e < (long long)m * p; e += blockDim.x) {
     const int r = (int)(e % m), c = (int)(e / m);
     const double sc = s_sig[c];
     g.U[r + (long long)s_pos[c] * g.ldu] = sc > 0.0 ? W[r + c * ldw] / sc : 0.0;
   }
-  for (long long e = tid; e < (long long)p * p; e += SVD_THREADS) {
+  for (long long e = tid; e < (long long)p * p; e += blockDim.x) {
     const int r = (int)(e % p), c = (int)(e / p);
     g.V[r + (long long)s_pos[c] * g.ldv] = V[r + c * ldv];
   }
-  for (int c = tid; c < p; c += SVD_THREADS) g.sigma[s_pos[c]] = s_sig[c];
+  for (int c = tid; c < p; c += blockDim.x) g.sigma[s_pos[c]] = s_sig[c];
 }
 
 // ------------------------------------------- block Jacobi across a grid ---
@@ -579,6 +579,13 @@ tt_status launch_qr(const QRDesc *descs_dev, int count, cudaStream_t s) {
   return check_launch("qr");
 }
 
+// one warp per column pair of a round: p/2 pairs -> up to 32 warps
+static int svd_threads(int pcap) {
+  int w = (pcap + 1) / 2;
+  w = w < 2 ? 2 : (w > 32 ? 32 : w);
+  return 32 * w;
+}
+
 struct BJSync {
   unsigned int *bar = nullptr;
   int *flag = nullptr;
@@ -599,7 +606,7 @@ tt_status launch_jacobi(const SVDDesc *descs_dev, int count, int mcap, int pcap,
       cudaFuncSetAttribute(jacobi_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)limit);
       attr_set = true;
     }
-    jacobi_kernel<true><<<count, SVD_THREADS, smem, s>>>(descs_dev);
+    jacobi_kernel<true><<<count, svd_threads(pcap), smem, s>>>(descs_dev);
   } else if (count == 1 && g_bj.bar &&
              ((size_t)mcap + pcap) * 2 * JB * sizeof(double) <= limit) {
     // block Jacobi over a cooperative grid: one CTA per block pair
@@ -623,7 +630,7 @@ tt_status launch_jacobi(const SVDDesc *descs_dev, int count, int mcap, int pcap,
     if (sm2 > 48 * 1024) {
       cudaFuncSetAttribute(jacobi_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)limit);
     }
-    jacobi_kernel<false><<<count, SVD_THREADS, sm2, s>>>(descs_dev);
+    jacobi_kernel<false><<<count, svd_threads(pcap), sm2, s>>>(descs_dev);
   }
   return check_launch("jacobi");
 }

@@ -53,6 +53,24 @@ class SweepProblem:
             als_update_interfaces(-1, self.dims_apply(k), self.Psi[k + 1], self.X[k], self.A[k], self.X[k],
                                   self.Psi[k])
 
+    def capture(self):
+        """Record one double sweep into a CUDA graph (the sequence of libtt launches
+        is fixed for fixed shapes); replay with self.graph.replay()."""
+        from .tt import workspace
+        from . import _lib
+        need = max(_lib.lib().als_workspace(*self.dims_apply(k)) for k in range(self.d))
+        workspace(need, self.X[0].device)          # allocate before capture
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            self.double_sweep()                    # warm (cudaFuncSetAttribute etc.)
+        torch.cuda.current_stream().wait_stream(s)
+        torch.cuda.synchronize()
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph):
+            self.double_sweep()
+        return self.graph
+
     def flops(self):
         """Algorithmic flops of one double sweep."""
         tot = 0
