@@ -254,6 +254,23 @@ int32_t tt_transport_terms(int32_t op, int32_t nv, double extent, int32_t G, int
                            int32_t nbox, const int32_t *box_lo, const int32_t *box_hi,
                            const int32_t *box_mat, double *out);
 
+/* 1-D slab variant: the same construction restricted to the x
+ * factor, two half-range blocks (mu < 0 then mu > 0); homogeneous material.
+ * Each term writes 3 factors (x, angle, group): nv*nv + L*L + G*G doubles. */
+int32_t tt_transport_terms_1d(int32_t op, int32_t nv, double extent, int32_t G, int32_t L,
+                              const double *mu, const double *w, const double *sigma_t,
+                              const double *sigma_s, const double *nu_sigma_f, const double *chi,
+                              double *out);
+
+/* Algorithm 1 for one factor, host side: a 2^l x 2^l column-major
+ * matrix G is reshaped to 2 x..x 2, its row/column bits paired (i_t, j_t) LSB
+ * first (Z28), and TT-SVD'd with modes 4 (row bit fastest) and the tail rule
+ * delta = eps ||G||_F / sqrt(l-1).  Cores [r_t, 2, 2, r_{t+1}] are written
+ * consecutively to cores_out (host, capacity cap doubles; NULL = size query),
+ * ranks (l+1 ints) to ranks_out.  Returns the number of doubles, -1 on error. */
+int64_t tt_qtt_matrix(int32_t n, const double *G, double eps, int32_t *ranks_out, double *cores_out,
+                      int64_t cap);
+
 #ifdef __cplusplus
 }
 #endif

@@ -23,7 +23,7 @@ import numpy as np
 __all__ = [
     "rng", "draw_core", "random_tt", "random_ttm", "c2_instance", "c2_slice",
     "c5_instance", "octant_signs", "quadrature_s2", "quadrature_ls_style",
-    "problem_c1", "problem_c3", "problem_c4", "problem_small_hetero",
+    "problem_c1", "problem_c3", "problem_c4", "problem_small_hetero", "quadrature_gl_1d", "problem_slab",
 ]
 
 
@@ -192,6 +192,30 @@ def problem_c4(seed: int = 4):
         "boundary": "vacuum", "qtt": True, "materials": [refl, blanket, core], "chi": chi,
         "boxes": [((32, 32, 32), (224, 224, 224), 1), ((64, 64, 64), (192, 192, 192), 2)],
         "seed": seed,
+    }
+
+
+def quadrature_gl_1d(L: int):
+    """1-D slab S_L set: Gauss-Legendre nodes on [-1, 1] with weights normalised to
+    sum 1; ordered as the two half-range blocks [mu_-; mu_+]
+    (P:1819-1822), each ascending.  (Reading: the paper does not name its 1-D set.)"""
+    x, w = np.polynomial.legendre.leggauss(L)
+    order = np.argsort(x)
+    x, w = x[order], w[order] / np.sum(w)
+    return {"mu": x, "w": w, "per_octant": L // 2, "name": f"GL-S{L}"}
+
+
+def problem_slab(L: int = 8, nv: int = 1024, qtt: bool = True):
+    """PAPER.md §3.5.1, Table 1: one-group Pu-239
+    slab of width 3.707444 cm, nu = 3.24, sigma_f = 0.0816, sigma_s = 0.225216,
+    sigma_t = 0.3264 cm^-1, vacuum boundaries, exactly critical (k = 1);
+    1024 spatial points (vertices, reading Z12), L ordinates."""
+    return {
+        "name": f"slab-L{L}", "dim": 1, "nv": nv, "extent": 3.707444, "G": 1,
+        "quad": quadrature_gl_1d(L), "boundary": "vacuum", "qtt": qtt,
+        "materials": [{"sigma_t": np.array([0.3264]), "sigma_s": np.array([[0.225216]]),
+                       "nu_sigma_f": np.array([3.24 * 0.0816])}],
+        "chi": np.array([1.0]), "boxes": [],
     }
 
 

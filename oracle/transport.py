@@ -134,6 +134,8 @@ def _axis_indicator(s, n, lo, hi):
 def operator_terms(prob):
     """Rank-1 terms of H = H_x + H_y + H_z + H_sigma,
     S and F, each summed over the 8 octants (bci)."""
+    if prob.get("dim", 3) == 1:
+        return operator_terms_1d(prob)
     n = prob["nv"]
     h = prob["extent"] / (n - 1)
     quad = prob["quad"]
@@ -178,9 +180,114 @@ def operator_terms(prob):
     return {"H": H, "S": S, "F": F}
 
 
+def operator_terms_1d(prob):
+    """1-D slab: the construction of P:1219-1293 restricted to the x
+    factor; the two half-range blocks b = 0 (mu < 0), 1 (mu > 0) play the octants.
+    Terms in core order [F_x, F_angle, F_group]."""
+    n = prob["nv"]
+    h = prob["extent"] / (n - 1)
+    quad = prob["quad"]
+    mu, w = quad["mu"], quad["w"]
+    L = len(w)
+    G = prob["G"]
+    m0 = prob["materials"][0]
+    chi = prob["chi"]
+    H, S, F = [], [], []
+    for b, sx in ((0, -1), (1, 1)):
+        Cb = np.diag(((mu > 0) == (sx > 0)).astype(float))
+        H.append([D_s(sx, n, h), Cb @ np.diag(mu), np.eye(G)])
+        H.append([Ip_s(sx, n), Cb, np.diag(m0["sigma_t"])])
+        Intg = Cb @ np.outer(np.ones(L), w)
+        S.append([IpN_s(sx, n), Intg, m0["sigma_s"]])
+        F.append([IpN_s(sx, n), Intg, np.outer(chi, m0["nu_sigma_f"])])
+    return {"H": H, "S": S, "F": F}
+
+
 def kron_term(term):
+    if len(term) == 3:
+        Fx, Fa, Fg = term
+        return np.kron(Fg, np.kron(Fa, Fx))
     Fx, Fy, Fz, Fa, Fg = term
     return np.kron(Fg, np.kron(Fa, np.kron(Fz, np.kron(Fy, Fx))))
+
+
+def slab_eq_apply(prob, psi):
+    """Row equations of the 1-D diamond-difference slab (the 1-D form of eq.
+    Discretized_kNTE) by explicit loops: for ordinate l with mu > 0
+    the row of vertex i >= 1 is the balance of cell (i-1, i); for mu < 0 the row
+    of vertex i <= n-2 is the balance of cell (i, i+1).  Returns (H psi, S psi,
+    F psi, interior mask); inflow rows are NaN."""
+    n = prob["nv"]
+    h = prob["extent"] / (n - 1)
+    mu, w = prob["quad"]["mu"], prob["quad"]["w"]
+    L = len(w)
+    m0 = prob["materials"][0]
+    st, ss, nf = m0["sigma_t"][0], m0["sigma_s"][0, 0], m0["nu_sigma_f"][0]
+    P = psi.reshape(L, n)
+    phi = w @ P
+    Hv = np.full(L * n, np.nan); Sv = np.full(L * n, np.nan); Fv = np.full(L * n, np.nan)
+    mask = np.zeros(L * n, dtype=bool)
+    for l in range(L):
+        for i in range(n):
+            lo, hi = (i - 1, i) if mu[l] > 0 else (i, i + 1)
+            if lo < 0 or hi > n - 1:
+                continue
+            row = i + n * l
+            Hv[row] = mu[l] / h * (P[l, hi] - P[l, lo]) + st / 2 * (P[l, lo] + P[l, hi])
+            Sv[row] = ss / 2 * (phi[lo] + phi[hi])
+            Fv[row] = nf / 2 * (phi[lo] + phi[hi])
+            mask[row] = True
+    return Hv, Sv, Fv, mask
+
+
+def slab_keff_sweep(prob, tol=1e-12, max_it=100000):
+    """Matrix-free Eq. 8 for the 1-D slab: H^{-1} is a transport sweep
+    (per ordinate, forward substitution from the inflow face); S and F act
+    through the scalar flux phi = sum_l w_l psi_l.  Returns (k, psi, iterations)."""
+    n = prob["nv"]
+    h = prob["extent"] / (n - 1)
+    mu, w = prob["quad"]["mu"], prob["quad"]["w"]
+    L = len(w)
+    m0 = prob["materials"][0]
+    st, ss, nf = m0["sigma_t"][0], m0["sigma_s"][0, 0], m0["nu_sigma_f"][0]
+
+    def rhs(psi, k):
+        phi = w @ psi
+        q = np.zeros((L, n))
+        cell = (ss + nf / k) / 2 * (phi[:-1] + phi[1:])       # per cell (i, i+1)
+        for l in range(L):
+            if mu[l] > 0:
+                q[l, 1:] = cell
+            else:
+                q[l, :-1] = cell
+        return q
+
+    def sweep(q):
+        psi = np.zeros((L, n))
+        for l in range(L):
+            a = abs(mu[l]) / h
+            if mu[l] > 0:                       # inflow at i = 0: psi_0 = 0
+                for i in range(1, n):
+                    psi[l, i] = (q[l, i] - (-a + st / 2) * psi[l, i - 1]) / (a + st / 2)
+            else:                               # inflow at i = n-1
+                for i in range(n - 2, -1, -1):
+                    psi[l, i] = (q[l, i] - (-a + st / 2) * psi[l, i + 1]) / (a + st / 2)
+        return psi
+
+    def fsum(psi):
+        phi = w @ psi
+        return nf / 2 * np.sum(phi[:-1] + phi[1:])   # sum of F psi up to the factor L (cancels in k)
+
+    psi = np.ones((L, n))
+    k = 1.0
+    for it in range(1, max_it + 1):
+        new = sweep(rhs(psi, k))
+        knew = k * fsum(new) / fsum(psi)
+        psi = new / np.linalg.norm(new)
+        if abs(knew - k) < tol:
+            return knew, psi.reshape(-1), it
+        k = knew
+    return k, psi.reshape(-1), max_it
 
 
 def dense_operators(prob):
@@ -321,9 +428,9 @@ def term_qtt(term):
     """QTT form of one term: spatial factors via Alg. 1, angle and group kept as
     plain TT cores (mixed TT/QTT)."""
     cores = []
-    for F in term[:3]:
+    for F in term[:-2]:
         cores += qtt_matrix(F)
-    Fa, Fg = term[3], term[4]
+    Fa, Fg = term[-2], term[-1]
     cores.append(Fa.reshape(1, Fa.shape[0], Fa.shape[1], 1))
     cores.append(Fg.reshape(1, Fg.shape[0], Fg.shape[1], 1))
     return cores
@@ -359,9 +466,9 @@ def qtt_modes(prob):
     n = prob["nv"]
     l = int(round(math.log2(n)))
     L = len(prob["quad"]["w"])
-    return [2] * (3 * l) + [L, prob["G"]]
+    return [2] * (prob.get("dim", 3) * l) + [L, prob["G"]]
 
 
 def tt_modes(prob):
     n = prob["nv"]
-    return [n, n, n, len(prob["quad"]["w"]), prob["G"]]
+    return [n] * prob.get("dim", 3) + [len(prob["quad"]["w"]), prob["G"]]

@@ -4,6 +4,7 @@
 // with tt_add and tt_round.  Readings: Z3 full-L integral, Z4 full
 // scattering matrix, Z5 chi nu_sigma_f^T, Z6 boundary rows as displayed, Z7
 // octant-shifted row->cell map, Z12 vertices, Z34 painted boxes.
+#include <algorithm>
 #include <cmath>
 #include <cstring>
 #include <vector>
@@ -76,6 +77,199 @@ struct Term {
 };
 
 }  // namespace
+
+// ------------------------------------------------ Alg. 1 ---
+// Host one-sided Jacobi SVD of an m x n column-major matrix (m >= n):
+// W <- U diag(s), V accumulated; returns s sorted descending with U, V permuted.
+static void host_svd(int m, int n, std::vector<double> &W, std::vector<double> &s, std::vector<double> &V) {
+  V.assign((size_t)n * n, 0.0);
+  for (int i = 0; i < n; ++i) V[(size_t)i * n + i] = 1.0;
+  for (int sweep = 0; sweep < 80; ++sweep) {
+    bool rot = false;
+    for (int a = 0; a < n - 1; ++a)
+      for (int b = a + 1; b < n; ++b) {
+        double al = 0, be = 0, ga = 0;
+        for (int r = 0; r < m; ++r) {
+          const double x = W[(size_t)a * m + r], y = W[(size_t)b * m + r];
+          al += x * x; be += y * y; ga += x * y;
+        }
+        if (ga == 0.0 || al == 0.0 || be == 0.0 || std::fabs(ga) <= 1e-15 * std::sqrt(al) * std::sqrt(be)) continue;
+        const double zeta = (be - al) / (2.0 * ga);
+        const double t = (zeta >= 0 ? 1.0 : -1.0) / (std::fabs(zeta) + std::sqrt(1.0 + zeta * zeta));
+        const double c = 1.0 / std::sqrt(1.0 + t * t), sn = c * t;
+        for (int r = 0; r < m; ++r) {
+          const double x = W[(size_t)a * m + r], y = W[(size_t)b * m + r];
+          W[(size_t)a * m + r] = c * x - sn * y;
+          W[(size_t)b * m + r] = sn * x + c * y;
+        }
+        for (int r = 0; r < n; ++r) {
+          const double x = V[(size_t)a * n + r], y = V[(size_t)b * n + r];
+          V[(size_t)a * n + r] = c * x - sn * y;
+          V[(size_t)b * n + r] = sn * x + c * y;
+        }
+        rot = true;
+      }
+    if (!rot) break;
+  }
+  s.assign(n, 0.0);
+  for (int c = 0; c < n; ++c) {
+    double t = 0;
+    for (int r = 0; r < m; ++r) t += W[(size_t)c * m + r] * W[(size_t)c * m + r];
+    s[c] = std::sqrt(t);
+  }
+  std::vector<int> idx(n);
+  for (int i = 0; i < n; ++i) idx[i] = i;
+  std::sort(idx.begin(), idx.end(), [&](int x, int y) { return s[x] > s[y]; });
+  std::vector<double> W2((size_t)m * n), V2((size_t)n * n), s2(n);
+  for (int i = 0; i < n; ++i) {
+    const int c = idx[i];
+    s2[i] = s[c];
+    for (int r = 0; r < m; ++r) W2[(size_t)i * m + r] = s[c] > 0 ? W[(size_t)c * m + r] / s[c] : 0.0;
+    for (int r = 0; r < n; ++r) V2[(size_t)i * n + r] = V[(size_t)c * n + r];
+  }
+  W.swap(W2); V.swap(V2); s.swap(s2);
+}
+
+// QTT-matrix of a 2^l x 2^l matrix G (column-major): reshape to 2 x..x 2, pair
+// the row/column bits (i_t, j_t) LSB first (Z28), TT-SVD with modes 4 (row bit
+// fastest) and tail rule delta = eps ||G|| / sqrt(l-1).  Writes the cores
+// [r_t, 2, 2, r_{t+1}] consecutively into cores_out (capacity cap doubles) and
+// the ranks (l+1) into ranks_out.  Returns the number of doubles written, or -1.
+extern "C" int64_t tt_qtt_matrix(int32_t n, const double *G, double eps, int32_t *ranks_out, double *cores_out,
+                                 int64_t cap) {
+  int l = 0;
+  while ((1 << l) < n) ++l;
+  if (n < 2 || (1 << l) != n || !G || !ranks_out) {
+    tt::set_error("tt_qtt_matrix: n must be a power of two >= 2");
+    return -1;
+  }
+  const size_t N = (size_t)n * n;
+  std::vector<double> T(N);
+  double nrm2 = 0;
+  for (int j = 0; j < n; ++j)
+    for (int i = 0; i < n; ++i) {
+      size_t lin = 0, mul = 1;
+      for (int t = 0; t < l; ++t) {
+        lin += mul * (((i >> t) & 1) + 2 * ((j >> t) & 1));
+        mul *= 4;
+      }
+      T[lin] = G[(size_t)i + (size_t)n * j];
+      nrm2 += T[lin] * T[lin];
+    }
+  const double delta = l > 1 ? eps * std::sqrt(nrm2) / std::sqrt((double)(l - 1)) : 0.0;
+  std::vector<double> C = T;  // current remainder, r x rest (column-major)
+  int r = 1;
+  size_t rest = N;
+  int64_t used = 0;
+  ranks_out[0] = 1;
+  std::vector<std::vector<double>> cores;
+  for (int t = 0; t < l - 1; ++t) {
+    const int rows = r * 4;
+    rest /= 4;
+    const int cols = (int)rest;
+    // SVD of the (rows x cols) unfolding; Jacobi on the orientation with fewer columns
+    std::vector<double> U, S, Vt;
+    int rk;
+    if (rows >= cols) {
+      std::vector<double> W = C, V;
+      host_svd(rows, cols, W, S, V);
+      rk = cols;
+      U = W;                       // rows x cols
+      Vt.assign((size_t)cols * cols, 0.0);
+      for (int i = 0; i < cols; ++i)
+        for (int c = 0; c < cols; ++c) Vt[(size_t)i + (size_t)cols * c] = V[(size_t)i * cols + c];  // (V^T)[i][c]
+    } else {
+      std::vector<double> W((size_t)cols * rows);  // transpose
+      for (int i = 0; i < rows; ++i)
+        for (int c = 0; c < cols; ++c) W[(size_t)i * cols + c] = C[(size_t)i + (size_t)rows * c];
+      std::vector<double> V;
+      host_svd(cols, rows, W, S, V);  // C^T = W S V^T -> C = V S W^T
+      rk = rows;
+      U.assign((size_t)rows * rows, 0.0);
+      for (int i = 0; i < rows; ++i)
+        for (int c = 0; c < rows; ++c) U[(size_t)c * rows + i] = V[(size_t)c * rows + i];
+      Vt.assign((size_t)rows * cols, 0.0);
+      for (int i = 0; i < rows; ++i)
+        for (int c = 0; c < cols; ++c) Vt[(size_t)i + (size_t)rows * c] = W[(size_t)i * cols + c];
+    }
+    // tail rule
+    double tail = 0;
+    int rn = rk;
+    for (int i = rk - 1; i >= 1; --i) {
+      if (tail + S[i] * S[i] <= delta * delta) { tail += S[i] * S[i]; rn = i; } else break;
+    }
+    std::vector<double> core((size_t)rows * rn);
+    for (int c = 0; c < rn; ++c)
+      for (int i = 0; i < rows; ++i) core[(size_t)i + (size_t)rows * c] = U[(size_t)c * rows + i];
+    cores.push_back(core);
+    ranks_out[t + 1] = rn;
+    std::vector<double> Cn((size_t)rn * cols);
+    for (int c = 0; c < cols; ++c)
+      for (int i = 0; i < rn; ++i) Cn[(size_t)i + (size_t)rn * c] = S[i] * Vt[(size_t)i + (size_t)rk * c];
+    C.swap(Cn);
+    r = rn;
+  }
+  cores.push_back(C);  // r x 4 (last core [r, 2, 2, 1])
+  ranks_out[l] = 1;
+  for (auto &c : cores) {
+    if (cores_out) {
+      if (used + (int64_t)c.size() > cap) {
+        tt::set_error("tt_qtt_matrix: output capacity too small");
+        return -1;
+      }
+      std::memcpy(cores_out + used, c.data(), c.size() * sizeof(double));
+    }
+    used += (int64_t)c.size();
+  }
+  return used;
+}
+
+// 1-D slab: the 3-D construction restricted to the x factor, the
+// two half-range blocks (mu < 0, mu > 0) playing the octants.  Homogeneous
+// material; each term writes [F_x (nv^2), F_angle (L^2), F_group (G^2)].
+extern "C" int32_t tt_transport_terms_1d(int32_t op, int32_t nv, double extent, int32_t G, int32_t L,
+                                         const double *mu, const double *w, const double *sigma_t,
+                                         const double *sigma_s, const double *nu_sigma_f, const double *chi,
+                                         double *out) {
+  if (op < 0 || op > 2 || nv < 2 || G < 1 || L < 1 || !mu || !w || !sigma_t || !sigma_s || !nu_sigma_f || !chi) {
+    tt::set_error("tt_transport_terms_1d: invalid argument");
+    return -1;
+  }
+  const double h = extent / (nv - 1);
+  std::vector<Mat> fac;
+  int nt = 0;
+  for (int sx : {-1, 1}) {
+    Mat Cb(L), Q(L), Intg(L);
+    for (int l = 0; l < L; ++l) {
+      if ((mu[l] > 0) != (sx > 0)) continue;
+      Cb.at(l, l) = 1.0;
+      Q.at(l, l) = mu[l];
+      for (int lp = 0; lp < L; ++lp) Intg.at(l, lp) = w[lp];
+    }
+    Mat E(G);
+    if (op == 0) {
+      Mat IG(G);
+      for (int g = 0; g < G; ++g) { IG.at(g, g) = 1.0; E.at(g, g) = sigma_t[g]; }
+      fac.push_back(diff(sx, nv, h)); fac.push_back(Q); fac.push_back(IG);
+      fac.push_back(interp(sx, nv, false)); fac.push_back(Cb); fac.push_back(E);
+      nt += 2;
+    } else {
+      for (int g = 0; g < G; ++g)
+        for (int gp = 0; gp < G; ++gp)
+          E.at(g, gp) = (op == 1) ? sigma_s[g + (size_t)G * gp] : chi[g] * nu_sigma_f[gp];
+      fac.push_back(interp(sx, nv, true)); fac.push_back(Intg); fac.push_back(E);
+      nt += 1;
+    }
+  }
+  if (out) {
+    double *p = out;
+    for (const Mat &M : fac) {
+      std::memcpy(p, M.a.data(), M.a.size() * sizeof(double));
+      p += M.a.size();
+    }
+  }
+  return nt;
+}
 
 extern "C" int32_t tt_transport_terms(int32_t op, int32_t nv, double extent, int32_t G, int32_t L, const double *mu,
                                       const double *eta, const double *xi, const double *w, int32_t nmat,

@@ -1,7 +1,9 @@
 """Transport operators H, S, F on the device (§3.2-3.3).
 
 The per-octant rank-1 factor matrices come from libtt's host-side C++
-constructor (tt_transport_terms); the sum over octants / parts (ranks add,
+constructor (tt_transport_terms); power-of-two spatial factors are converted to
+QTT by libtt's host implementation of Algorithm 1 (tt_qtt_matrix)
+when the problem asks for QTT; the sum over octants / parts (ranks add,
 P:1290-1293) and the rank reduction run on the GPU with
 tt_add and tt_round.  One-off setup, not a hot-path step."""
 from __future__ import annotations
@@ -9,7 +11,6 @@ from __future__ import annotations
 import ctypes as C
 
 import numpy as np
-import torch
 
 from . import _lib
 from .tt import TTMat, TTVec, tt_add, tt_round
@@ -21,7 +22,35 @@ def _dp(a):
     return a.ctypes.data_as(C.c_void_p)
 
 
+def factor_terms_1d(prob, op: str):
+    q = prob["quad"]
+    nv, G = int(prob["nv"]), int(prob["G"])
+    L = len(q["w"])
+    m = prob["materials"][0]
+    arr = [np.ascontiguousarray(a, dtype=np.float64) for a in
+           (q["mu"], q["w"], m["sigma_t"], m["sigma_s"].reshape(-1, order="F"), m["nu_sigma_f"], prob["chi"])]
+    args = [OPS[op], nv, float(prob["extent"]), G, L, *[_dp(a) for a in arr]]
+    lib = _lib.lib()
+    nt = lib.tt_transport_terms_1d(*args, None)
+    if nt < 0:
+        raise _lib.TTError(1, lib.tt_last_error().decode())
+    per = nv * nv + L * L + G * G
+    out = np.zeros(nt * per, dtype=np.float64)
+    lib.tt_transport_terms_1d(*args, _dp(out))
+    terms = []
+    for t in range(nt):
+        p = out[t * per:(t + 1) * per]
+        o, fac = 0, []
+        for n in (nv, L, G):
+            fac.append(p[o:o + n * n].reshape(n, n, order="F"))
+            o += n * n
+        terms.append(fac)
+    return terms
+
+
 def factor_terms(prob, op: str):
+    if prob.get("dim", 3) == 1:
+        return factor_terms_1d(prob, op)
     q = prob["quad"]
     nv, G = int(prob["nv"]), int(prob["G"])
     L = len(q["w"])
@@ -56,30 +85,78 @@ def factor_terms(prob, op: str):
     return terms
 
 
-def operator(prob, op: str, eps: float = 1e-13, device="cuda") -> TTMat:
-    """Sum of the rank-1 terms (device tt_add), then device tt_round; plain TT
-    cores (x, y, z, angle, group)."""
-    terms = factor_terms(prob, op)
-    rows = [f.shape[0] for f in terms[0]]
+def qtt_matrix(M: np.ndarray, eps: float = 1e-14):
+    """QTT cores [r, 2, 2, r'] of a 2^l x 2^l matrix via libtt's Alg. 1."""
+    n = M.shape[0]
+    l = int(round(np.log2(n)))
+    Mf = np.ascontiguousarray(M.reshape(-1, order="F"), dtype=np.float64)
+    ranks = np.zeros(l + 1, dtype=np.int32)
+    lib = _lib.lib()
+    size = lib.tt_qtt_matrix(n, _dp(Mf), float(eps), _dp(ranks), None, 0)
+    if size < 0:
+        raise _lib.TTError(1, lib.tt_last_error().decode())
+    out = np.zeros(size, dtype=np.float64)
+    lib.tt_qtt_matrix(n, _dp(Mf), float(eps), _dp(ranks), _dp(out), size)
+    cores, o = [], 0
+    for t in range(l):
+        c = ranks[t] * 4 * ranks[t + 1]
+        cores.append(out[o:o + c].reshape(ranks[t], 2, 2, ranks[t + 1], order="F"))
+        o += c
+    return cores
+
+
+def term_cores(fac, qtt: bool):
+    """Cores of one rank-1 term in core order (x, y, z, angle, group)."""
+    if not qtt:
+        return [f.reshape(1, f.shape[0], f.shape[1], 1, order="F") for f in fac]
+    cores = []
+    for f in fac[:-2]:
+        cores += qtt_matrix(f)
+    for f in fac[-2:]:
+        cores.append(f.reshape(1, f.shape[0], f.shape[1], 1, order="F"))
+    return cores
+
+
+def _sum_round(term_list, eps, device) -> TTMat:
+    rows = [c.shape[1] for c in term_list[0]]
     d = len(rows)
     acc = None
-    for t, fac in enumerate(terms):
-        term = TTVec([n * n for n in rows], [1] * (d + 1), device)
-        term.set_cores([f.reshape(1, -1, 1, order="F") for f in fac])
+    for cores in term_list:
+        r = [c.shape[0] for c in cores] + [1]
+        term = TTVec([m * m for m in rows], r, device)
+        term.set_cores([c.reshape(c.shape[0], -1, c.shape[3], order="F") for c in cores])
         if acc is None:
             acc = term
             continue
-        nxt = TTVec(acc.n, [1] + [t + 1] * (d - 1) + [1], device)
+        cap = [1] + [a + b for a, b in zip(acc.rcap[1:-1], term.rcap[1:-1])] + [1]
+        nxt = TTVec(acc.n, cap, device)
         tt_add(acc, term, nxt)
         acc = nxt
     tt_round(acc, eps)
     R = acc.ranks()
     A = TTMat(rows, rows, R, device)
-    # copy the rounded cores into the matrix container (same column-major layout)
-    cores = acc.cores()
-    A.set_cores([c.reshape(c.shape[0], m, m, c.shape[2], order="F") for c, m in zip(cores, rows)])
+    A.set_cores([c.reshape(c.shape[0], m, m, c.shape[2], order="F") for c, m in zip(acc.cores(), rows)])
     return A
 
 
-def operators(prob, eps: float = 1e-13, device="cuda"):
-    return {k: operator(prob, k, eps, device) for k in ("H", "S", "F")}
+def operator(prob, op: str, eps: float = 1e-13, device="cuda", qtt=None) -> TTMat:
+    """Sum of the rank-1 terms (device tt_add), then device tt_round."""
+    if qtt is None:
+        qtt = bool(prob.get("qtt", False))
+    terms = factor_terms(prob, op)
+    return _sum_round([term_cores(f, qtt) for f in terms], eps, device)
+
+
+def operators(prob, eps: float = 1e-13, device="cuda", qtt=None):
+    return {k: operator(prob, k, eps, device, qtt) for k in ("H", "S", "F")}
+
+
+def modes(prob, qtt=None):
+    if qtt is None:
+        qtt = bool(prob.get("qtt", False))
+    nv, L, G = int(prob["nv"]), len(prob["quad"]["w"]), int(prob["G"])
+    dim = int(prob.get("dim", 3))
+    if not qtt:
+        return [nv] * dim + [L, G]
+    l = int(round(np.log2(nv)))
+    return [2] * (dim * l) + [L, G]

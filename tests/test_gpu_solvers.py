@@ -90,6 +90,29 @@ def test_keff_small_vs_dense():
     assert np.linalg.norm(v - psid * np.sign(psid.sum())) <= 1e-6
 
 
+def test_slab_qtt_operators_on_device():
+    """QTT operators of the 1-D slab (host Alg. 1 + device sum/round) vs dense."""
+    p = inputs.problem_slab(4)
+    dense = T.dense_operators(p)
+    ops = gtr.operators(p, eps=1e-12)
+    for k in "HSF":
+        got = ott.ttm_full(ops[k].cores())
+        assert np.max(np.abs(got - dense[k])) <= 1e-11 * np.abs(dense[k]).max()
+
+
+@pytest.mark.parametrize("L", [4, 32])
+def test_keff_slab_qtt(L):
+    """NEXT-3: 1-D Pu-239 slab, 1024 points, QTT in x; GPU TT k vs
+    the oracle's matrix-free full-grid iteration; k -> 1 (exactly critical)."""
+    p = inputs.problem_slab(L)
+    ks, _, _ = T.slab_keff_sweep(p, tol=1e-13)
+    res, psi = _keff_gpu(p, gtr.modes(p), rmax=40, kick=3, tol_k=1e-11, eps_round=1e-11, eps_solve=1e-11)
+    assert res.status.item() == 0
+    assert abs(res.k.item() - ks) <= 1e-8
+    if L == 32:
+        assert 1.0 - res.k.item() < 5e-4
+
+
 def test_keff_c1_vacuum():
     """BASELINE.json configs[0] (vacuum): |dk|/k <= 1e-8 against the dense oracle value."""
     kd = float(open(os.path.join(GOLD, "c1_keff_vacuum.txt")).read().split()[-1])

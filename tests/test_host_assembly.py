@@ -1,0 +1,42 @@
+"""CPU checks of libtt's host-side setup logic (operator factor construction and
+Algorithm 1), compared with the oracle's independent constructions.  These
+call host code only (no device work)."""
+import numpy as np
+import pytest
+
+import inputs
+from oracle import transport as T
+from oracle import tt as ott
+
+
+@pytest.fixture(scope="module")
+def gtr():
+    from paper_2309_03347_b200 import build
+    build.build()
+    from paper_2309_03347_b200 import transport
+    return transport
+
+
+@pytest.mark.parametrize("prob", [inputs.problem_c1(), inputs.problem_small_hetero(nv=4, G=2, N=4),
+                                  inputs.problem_slab(4, nv=16)], ids=["C1", "hetero4", "slab16"])
+def test_factor_terms_match_oracle(gtr, prob):
+    ref = T.operator_terms(prob)
+    for op in "HSF":
+        got = gtr.factor_terms(prob, op)
+        assert len(got) == len(ref[op])
+        for ta, tb in zip(got, ref[op]):
+            for a, b in zip(ta, tb):
+                assert np.array_equal(a, b)
+
+
+def test_qtt_alg1_host(gtr):
+    """Host Alg. 1 reproduces the displayed factors exactly in QTT."""
+    for M in (T.D_plus(8, 0.25), T.D_minus(64, 0.1), T.Ip_plus_noBC(16), T.Ip_minus(32), np.eye(4)):
+        cores = gtr.qtt_matrix(M)
+        assert np.max(np.abs(ott.ttm_full(cores) - M)) <= 1e-13 * np.abs(M).max()
+        assert max(ott.ranks(cores)) <= 3
+    g = inputs.rng(71)
+    R = g.standard_normal((8, 8))                 # generic matrix: full QTT ranks
+    cores = gtr.qtt_matrix(R)
+    assert np.max(np.abs(ott.ttm_full(cores) - R)) <= 1e-13 * np.abs(R).max()
+    assert ott.ranks(cores) == [1, 4, 4, 1]
