@@ -185,7 +185,9 @@ tt_status als_update_interfaces(int32_t dir, int32_t rY, int32_t R, int32_t rX, 
  * delta = eps ||x_k|| / sqrt(d-1) capped at rmax, residual TT z (ranks = its
  * initial ranks = kickrank) and enrichment of the solution core with the
  * residual projected on (x frames | z frames).  Stops after a sweep whose
- * maximum local residual (measured before each local solve) is <= eps.
+ * maximum local residual (measured before each local solve) is <= eps, or
+ * whose maximum relative change of a local solution ||x_k^new - x_k^old|| /
+ * ||x_k^new|| is <= eps (the solution-change exit of TT-Toolbox amen_solve).
  * x: in initial guess, out solution (capacities >= rmax + kickrank).
  * z: in initial residual TT (random draws are inputs), workspace afterwards.
  * sweeps_dev / res_dev (may be NULL): sweeps used and final max residual.

@@ -140,7 +140,9 @@ def amen_solve(A, b, x0, z0, eps=1e-8, max_sweeps=20, rmax=10**9, dense_max=2000
         solution core with the residual projected onto (x frames | z frames),
         re-orthogonalise with QR and move the centre.
       * stop after a sweep whose max local residual (measured before each local
-        solve) is <= eps.
+        solve) is <= eps, or whose max relative change of the local solution
+        ||x_k^new - x_k^old|| / ||x_k^new|| is <= eps (the solution-change exit of
+        TT-Toolbox amen_solve; reading Z20).
     Returns (x, info)."""
     d = len(A)
     x, _ = ott.tt_orthogonalize_rl(x0)
@@ -159,11 +161,13 @@ def amen_solve(A, b, x0, z0, eps=1e-8, max_sweeps=20, rmax=10**9, dense_max=2000
         PhZA[k] = ott.right_update(PhZA[k + 1], z[k - 1], A[k - 1], x[k - 1])
         PhZb[k] = ott.right_update_vec(PhZb[k + 1], z[k - 1], b[k - 1])
     hist = []
+    dx_hist = []
     direction = +1
     sweeps = 0
     for sweep in range(max_sweeps):
         sweeps += 1
         maxres = 0.0
+        maxdx = 0.0
         order = range(1, d + 1) if direction > 0 else range(d, 0, -1)
         for k in order:
             Ak, bk = A[k - 1], b[k - 1]
@@ -173,6 +177,8 @@ def amen_solve(A, b, x0, z0, eps=1e-8, max_sweeps=20, rmax=10**9, dense_max=2000
             res = np.linalg.norm(Ax - rhs) / nrhs if nrhs > 0 else 0.0
             maxres = max(maxres, res)
             sol = _local_solve(PhiA[k - 1], Ak, PhiA[k + 1], rhs, x[k - 1], ltol, dense_max, restart)
+            nsol = np.linalg.norm(sol)
+            maxdx = max(maxdx, np.linalg.norm(sol - x[k - 1]) / nsol if nsol > 0 else 0.0)
             r0, n, r1 = sol.shape
             last = (k == d) if direction > 0 else (k == 1)
             if last:
@@ -239,12 +245,13 @@ def amen_solve(A, b, x0, z0, eps=1e-8, max_sweeps=20, rmax=10**9, dense_max=2000
                 PhZA[k] = ott.right_update(PhZA[k + 1], z[k - 1], Ak, x[k - 1])
                 PhZb[k] = ott.right_update_vec(PhZb[k + 1], z[k - 1], bk)
         hist.append(maxres)
+        dx_hist.append(maxdx)
         if verbose:
             print(f"amen sweep {sweep} dir {direction} maxres {maxres:.3e} ranks {ott.ranks(x)}")
-        if maxres <= eps:
+        if maxres <= eps or maxdx <= eps:
             break
         direction = -direction
-    return x, {"res_hist": hist, "sweeps": sweeps}
+    return x, {"res_hist": hist, "dx_hist": dx_hist, "sweeps": sweeps}
 
 
 # ------------------------------------------------------------ k-eff ---

@@ -32,7 +32,7 @@ struct Dev {  // device-side view passed by value to the plan kernels
   MatMeta A;
   double *AL[TT_MAX_D + 1], *AR[TT_MAX_D + 1], *BL[TT_MAX_D + 1], *BR[TT_MAX_D + 1];
   double *ZAL[TT_MAX_D + 1], *ZAR[TT_MAX_D + 1], *ZBL[TT_MAX_D + 1], *ZBR[TT_MAX_D + 1];
-  double *rhs, *sol, *w, *V, *T1, *T2, *crz, *xfull, *tmp, *tmpz, *K;
+  double *rhs, *sol, *w, *V, *T1, *T2, *crz, *xfull, *tmp, *tmpz, *K, *xold;
   double *qA, *qQ, *qR, *tau, *qT;      // SVD-QR of M, then the enrichment QR (qA, tau, qT reused)
   double *qA2, *tau2, *qT2;             // z QR (runs in the same launch as the enrichment QR)
   double *qRe;                          // R factor of the enrichment QR
@@ -111,6 +111,31 @@ __global__ void plan_local(Dev D, int k) {
   }
   D.cd[0] = cpy(N, 1, D.x.data + D.x.off[k], 1, N, D.sol, 1, N);
   D.cd[1] = cpy(N, 1, D.sol, 1, N, D.x.data + D.x.off[k], 1, N);
+  D.cd[2] = cpy(N, 1, D.x.data + D.x.off[k], 1, N, D.xold, 1, N);
+}
+
+// relative change of the local solution (solution-change exit, reading Z20)
+__global__ void track_dx_kernel(const int *Nptr, const double *sol, const double *xold, double *dv) {
+  __shared__ double r1[32], r2[32];
+  const int N = *Nptr;
+  double a = 0.0, b = 0.0;
+  for (int i = threadIdx.x; i < N; i += blockDim.x) {
+    const double d = sol[i] - xold[i];
+    a = fma(d, d, a);
+    b = fma(sol[i], sol[i], b);
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    a += __shfl_xor_sync(0xffffffffu, a, o);
+    b += __shfl_xor_sync(0xffffffffu, b, o);
+  }
+  if ((threadIdx.x & 31) == 0) { r1[threadIdx.x >> 5] = a; r2[threadIdx.x >> 5] = b; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double ta = 0.0, tb = 0.0;
+    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) { ta += r1[i]; tb += r2[i]; }
+    const double dx = tb > 0.0 ? sqrt(ta / tb) : 0.0;
+    if (dx > dv[2] || !(dx == dx)) dv[2] = dx;
+  }
 }
 
 __global__ void track_res_kernel(const GmState *st, double *dv, int *status) {
@@ -349,6 +374,7 @@ static tt_status carve_amen(const MatMeta &A, const VecMeta &b, const VecMeta &x
   D.ldv = (Ncap + 31) / 32 * 32;
   D.rhs = ar.take<double>(Ncap);
   D.sol = ar.take<double>(Ncap);
+  D.xold = ar.take<double>(Ncap);
   D.w = ar.take<double>(Ncap);
   D.V = ar.take<double>((size_t)D.ldv * (m + 1));
   D.T1 = ar.take<double>(Tcap);
@@ -496,6 +522,7 @@ tt_status amen_solve_meta(const MatMeta &A, const VecMeta &b, const VecMeta &x, 
   double hres = 0.0;
   for (sweep = 0; sweep < o.max_sweeps; ++sweep) {
     set_dv_kernel<<<1, 1, 0, s>>>(D.dv, 0, 0.0);
+    set_dv_kernel<<<1, 1, 0, s>>>(D.dv, 2, 0.0);
     for (int t = 0; t < d; ++t) {
       const int k = dir > 0 ? t : d - 1 - t;
       const int last = (t == d - 1);
@@ -504,9 +531,11 @@ tt_status amen_solve_meta(const MatMeta &A, const VecMeta &b, const VecMeta &x, 
       descs_local_apply(xc[k], Rc[k], xc[k], n, n, xc[k + 1], Rc[k + 1], xc[k + 1], 0, 0, 0, 0, 0, 0, 0, appc.g + 2);
       plan_local<<<1, 1, 0, s>>>(D, k);
       TT_TRY(launch_copy(D.cd, 1, P.Ncap, s));
+      TT_TRY(launch_copy(D.cd + 2, 1, P.Ncap, s));
       TT_TRY(launch_caps(D.gd, appc, 0, 2));
       TT_TRY(gmres_solve(gc, s));
       track_res_kernel<<<1, 1, 0, s>>>(P.gst, D.dv, status_dev);
+      track_dx_kernel<<<1, 256, 0, s>>>(D.iv, D.sol, D.xold, D.dv);
       if (last) {
         TT_TRY(launch_copy(D.cd + 1, 1, P.Ncap, s));
         continue;
@@ -545,10 +574,12 @@ tt_status amen_solve_meta(const MatMeta &A, const VecMeta &b, const VecMeta &x, 
       TT_TRY(launch_copy(D.cd, 3, P.Scap, s));
       TT_TRY(iface(k, dir));
     }
-    cudaMemcpyAsync(&hres, D.dv, sizeof(double), cudaMemcpyDeviceToHost, s);
+    double hv[3] = {0.0, 0.0, 0.0};
+    cudaMemcpyAsync(hv, D.dv, 3 * sizeof(double), cudaMemcpyDeviceToHost, s);
     cudaStreamSynchronize(s);
     TT_TRY(check_launch("amen sweep"));
-    if (hres <= o.eps) { ++sweep; break; }
+    hres = hv[0];
+    if (hv[0] <= o.eps || hv[2] <= o.eps) { ++sweep; hres = 0.0; break; }
     dir = -dir;
   }
   (void)zcm; (void)nmax;
