@@ -95,8 +95,12 @@ void tt_counters(uint64_t *out /* [5] */, int32_t reset);
  * No workspace.  y must not alias A or x. */
 tt_status tt_matvec(const tt_mat *A, const tt_vec *x, tt_vec *y, tt_stream s);
 
-/* Batched form: B independent products (A[b], x[b]) -> y[b], one launch. */
-tt_status tt_matvec_batched(int32_t B, const tt_mat *A, const tt_vec *x, tt_vec *y, tt_stream s);
+/* Batched form: B independent products (A[b], x[b]) -> y[b] (same d), one
+ * launch over (core, instance); a (core, instance) descriptor table is staged
+ * into ws (tt_matvec_batched_workspace bytes). */
+size_t tt_matvec_batched_workspace(int32_t B, const tt_mat *A);
+tt_status tt_matvec_batched(int32_t B, const tt_mat *A, const tt_vec *x, tt_vec *y, void *ws, size_t wsb,
+                            tt_stream s);
 
 /* ---------------------------------------------------------------- a2 ---
  * tt_add: z = alpha x + beta y by block-diagonal core concatenation (sum of

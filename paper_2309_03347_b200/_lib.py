@@ -55,7 +55,8 @@ SIG = {
     "tt_version": (C.c_char_p, []),
     "tt_counters": (None, [C.POINTER(C.c_uint64), I32]),
     "tt_matvec": (I32, [C.POINTER(tt_mat), C.POINTER(tt_vec), C.POINTER(tt_vec), P]),
-    "tt_matvec_batched": (I32, [I32, C.POINTER(tt_mat), C.POINTER(tt_vec), C.POINTER(tt_vec), P]),
+    "tt_matvec_batched_workspace": (C.c_size_t, [I32, C.POINTER(tt_mat)]),
+    "tt_matvec_batched": (I32, [I32, C.POINTER(tt_mat), C.POINTER(tt_vec), C.POINTER(tt_vec), P, C.c_size_t, P]),
     "tt_add": (I32, [C.POINTER(tt_vec), P, C.POINTER(tt_vec), P, C.POINTER(tt_vec), P]),
     "tt_scale": (I32, [C.POINTER(tt_vec), P, P]),
     "tt_copy": (I32, [C.POINTER(tt_vec), C.POINTER(tt_vec), P]),

@@ -25,10 +25,29 @@ extern "C" tt_status tt_matvec(const tt_mat *A, const tt_vec *x, tt_vec *y, tt_s
   return matvec_meta(a, xm, ym, (cudaStream_t)s);
 }
 
-extern "C" tt_status tt_matvec_batched(int32_t B, const tt_mat *A, const tt_vec *x, tt_vec *y, tt_stream s) {
+namespace tt {
+size_t matvec_batched_ws(int B, int d);
+tt_status matvec_batched_meta(int B, const MatMeta *A, const VecMeta *x, const VecMeta *y, void *ws, size_t wsb,
+                              cudaStream_t s);
+}
+
+extern "C" size_t tt_matvec_batched_workspace(int32_t B, const tt_mat *A) {
+  if (B <= 0 || !A) return 0;
+  return matvec_batched_ws(B, A->d);
+}
+
+extern "C" tt_status tt_matvec_batched(int32_t B, const tt_mat *A, const tt_vec *x, tt_vec *y, void *ws, size_t wsb,
+                                       tt_stream s) {
   if (B < 0 || (B > 0 && (!A || !x || !y))) return fail(TT_ERR_ARG, "tt_matvec_batched: bad batch");
-  for (int b = 0; b < B; ++b) TT_TRY(tt_matvec(A + b, x + b, y + b, s));
-  return TT_OK;
+  if (B == 0) return TT_OK;
+  std::vector<MatMeta> am(B);
+  std::vector<VecMeta> xm(B), ym(B);
+  for (int b = 0; b < B; ++b) {
+    TT_TRY(make_mat_meta(A + b, am[b]));
+    TT_TRY(make_vec_meta(x + b, xm[b]));
+    TT_TRY(make_vec_meta(y + b, ym[b]));
+  }
+  return matvec_batched_meta(B, am.data(), xm.data(), ym.data(), ws, wsb, (cudaStream_t)s);
 }
 
 extern "C" tt_status tt_add(const tt_vec *x, const double *alpha_dev, const tt_vec *y, const double *beta_dev,

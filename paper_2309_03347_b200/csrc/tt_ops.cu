@@ -1,8 +1,10 @@
 // Elementwise / structural TT operations: exact matvec (a1), add / scale (a2),
 // copy, dot (a8), plus the meta plumbing and error state of the C ABI.
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
+#include <vector>
 
 #include "tt_common.cuh"
 
@@ -107,32 +109,20 @@ void matvec_counters(unsigned long long *out, int reset) {
 // One launch over all cores: blockIdx.y = core, grid-stride over output entries
 // (consecutive threads write consecutive rho: coalesced stores, which are the
 // HBM traffic that bounds this kernel for QTT 2x2 cores).
-__global__ void matvec_kernel(const MatMeta A, const VecMeta x, const VecMeta y) {
+__device__ void matvec_core_cols(const double *__restrict__ A, const double *__restrict__ X,
+                                 double *__restrict__ Y, int R0, int R1, int r0, int r1, int m, int n, double *sm,
+                                 int smcap);
+
+__global__ void __launch_bounds__(256) matvec_kernel(const MatMeta A, const VecMeta x, const VecMeta y, int smcap) {
+  extern __shared__ double dsm_mv[];
   const int k = blockIdx.y;
   const int R0 = A.R[k], R1 = A.R[k + 1], r0 = x.r[k], r1 = x.r[k + 1];
   const int m = A.m[k], n = A.n[k];
-  const int P = R0 * r0, P1 = R1 * r1;
-  const int total = P * m * P1;
-  const double *__restrict__ Ak = A.data + A.off[k];
-  const double *__restrict__ Xk = x.data + x.off[k];
-  double *__restrict__ Yk = y.data + y.off[k];
-  const int jsA = R0 * m;
-  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
-    const int rho = e % P;
-    const int t = e / P;
-    const int i = t % m;
-    const int rho1 = t / m;
-    const int a = rho % R0, b = rho / R0, a1 = rho1 % R1, b1 = rho1 / R1;
-    const double *Ap = Ak + a + R0 * i + (long long)jsA * n * a1;
-    const double *Xp = Xk + b + (long long)r0 * n * b1;
-    double s = 0.0;
-    for (int j = 0; j < n; ++j) s = fma(Ap[(long long)j * jsA], Xp[(long long)j * r0], s);
-    Yk[e] = s;
-  }
+  matvec_core_cols(A.data + A.off[k], x.data + x.off[k], y.data + y.off[k], R0, R1, r0, r1, m, n, dsm_mv, smcap);
   if (blockIdx.x == 0 && threadIdx.x == 0) {
-    y.r[k] = P;
-    if (k == A.d - 1) y.r[k + 1] = P1;
-    atomicAdd(&g_matvec_flops, 2ull * (unsigned long long)total * n);
+    y.r[k] = R0 * r0;
+    if (k == A.d - 1) y.r[k + 1] = R1 * r1;
+    atomicAdd(&g_matvec_flops, 2ull * (unsigned long long)R0 * r0 * m * R1 * r1 * n);
   }
 }
 
@@ -149,11 +139,141 @@ tt_status matvec_meta(const MatMeta &A, const VecMeta &x, const VecMeta &y, cuda
   for (int k = 0; k <= A.d; ++k)
     if ((long long)y.rcap[k] < (long long)A.Rcap[k] * x.rcap[k])
       return fail(TT_ERR_CAPACITY, "tt_matvec: y rank capacity < R*r");
-  int bx = (int)((mx + 255) / 256);
-  if (bx > 2048) bx = 2048;
-  if (bx < 1) bx = 1;
-  matvec_kernel<<<dim3(bx, A.d), 256, 0, s>>>(A, x, y);
+  int bx = 2368 / A.d;  // columns of each core spread over bx CTAs (~16 CTAs per SM in total)
+  bx = bx < 1 ? 1 : (bx > 512 ? 512 : bx);
+  (void)mx;
+  long long acap = 1;  // operator core staged in shared memory (host-known capacity)
+  for (int k = 0; k < A.d; ++k) {
+    const long long c = (long long)A.Rcap[k] * A.m[k] * A.n[k] * A.Rcap[k + 1];
+    acap = c > acap ? c : acap;
+  }
+  const int smcap = acap <= 6144 ? (int)acap : 0;
+  matvec_kernel<<<dim3(bx, A.d), 256, (size_t)smcap * sizeof(double), s>>>(A, x, y, smcap);
   return check_launch("tt_matvec");
+}
+
+// ------------------------------------------------------- batched matvec ---
+// One launch over (core, instance): blockIdx.y = core, blockIdx.z = instance,
+// per-pair pointers and sizes from a descriptor table in the workspace.
+struct MvPair {
+  const double *A;
+  const double *X;
+  double *Y;
+  const int *R;   // operator ranks (device), index k, k+1
+  const int *r;   // vector ranks (device)
+  int *ry;        // output ranks (device)
+  int m, n, k, last;
+};
+
+// One CTA per output column rho' = a' + R1 b' (grid-strided): the slices
+// A[:, :, :, a'] (R0 m n) and X[:, :, b'] (r0 n) are staged in shared memory and
+// the contiguous column Y[:, :, rho'] (P m entries) is streamed out with
+// coalesced stores — one small division per entry, no per-entry index algebra.
+constexpr int MV_SMEM = 6144;  // doubles of staging (48 KB)
+
+__device__ __forceinline__ void matvec_core_cols(const double *__restrict__ A, const double *__restrict__ X,
+                                                 double *__restrict__ Y, int R0, int R1, int r0, int r1, int m,
+                                                 int n, double *sm, int smcap) {
+  const int P = R0 * r0, P1 = R1 * r1;
+  const int na = R0 * m * n * R1;                         // the whole operator core
+  const double *As = A;
+  if (na <= smcap) {
+    for (int e = threadIdx.x; e < na; e += blockDim.x) sm[e] = A[e];
+    __syncthreads();
+    As = sm;
+  }
+  // one thread per (rho, b'): its X[b, :, b'] values are loaded once and reused
+  // for every a' in [0, R1) and i in [0, m) (R1 m independent outputs per item)
+  const int items = P * r1;
+  const int per_col = P * m;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < items; e += gridDim.x * blockDim.x) {
+    const int b1 = e / P, rho = e - b1 * P;
+    const int b = rho / R0, a = rho - b * R0;
+    const double *Xr = X + b + (long long)r0 * n * b1;
+    double *Yr = Y + rho + (long long)per_col * R1 * b1;
+    const double *Ar = As + a;
+    if (n == 2) {
+      const double x0 = Xr[0], x1 = Xr[r0];
+      for (int a1 = 0; a1 < R1; ++a1) {
+        const double *Aa = Ar + R0 * m * 2 * a1;
+        double *Ya = Yr + (long long)per_col * a1;
+        for (int i = 0; i < m; ++i) Ya[P * i] = fma(Aa[R0 * i], x0, Aa[R0 * (i + m)] * x1);
+      }
+    } else {
+      for (int a1 = 0; a1 < R1; ++a1) {
+        const double *Aa = Ar + (long long)R0 * m * n * a1;
+        double *Ya = Yr + (long long)per_col * a1;
+        for (int i = 0; i < m; ++i) {
+          double s = 0.0;
+          for (int j = 0; j < n; ++j) s = fma(Aa[R0 * (i + m * j)], Xr[(long long)r0 * j], s);
+          Ya[P * i] = s;
+        }
+      }
+    }
+  }
+  (void)P1;
+}
+
+__global__ void __launch_bounds__(256) matvec_batched_kernel(const MvPair *__restrict__ pairs, int d, int smcap) {
+  extern __shared__ double sm[];
+  const MvPair p = pairs[blockIdx.z * d + blockIdx.y];
+  const int k = p.k;
+  const int R0 = p.R[k], R1 = p.R[k + 1], r0 = p.r[k], r1 = p.r[k + 1];
+  matvec_core_cols(p.A, p.X, p.Y, R0, R1, r0, r1, p.m, p.n, sm, smcap);
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    p.ry[k] = R0 * r0;
+    if (p.last) p.ry[k + 1] = R1 * r1;
+    atomicAdd(&g_matvec_flops, 2ull * (unsigned long long)R0 * r0 * p.m * R1 * r1 * p.n);
+  }
+}
+
+size_t matvec_batched_ws(int B, int d) { return (size_t)B * d * sizeof(MvPair); }
+
+tt_status matvec_batched_meta(int B, const MatMeta *A, const VecMeta *x, const VecMeta *y, void *ws, size_t wsb,
+                              cudaStream_t s) {
+  if (B <= 0) return TT_OK;
+  const int d = A[0].d;
+  const size_t need = (size_t)B * d * sizeof(MvPair);
+  if (!ws || wsb < need) return fail(TT_ERR_CAPACITY, "tt_matvec_batched: workspace too small");
+  // pageable staging: cudaMemcpyAsync returns once the source has been consumed
+  std::vector<MvPair> host((size_t)B * d);
+  long long mx = 0;
+  for (int b = 0; b < B; ++b) {
+    if (A[b].d != d || x[b].d != d || y[b].d != d) return fail(TT_ERR_SHAPE, "tt_matvec_batched: d differs");
+    for (int k = 0; k < d; ++k) {
+      if (A[b].n[k] != x[b].n[k] || A[b].m[k] != y[b].n[k]) return fail(TT_ERR_SHAPE, "tt_matvec_batched: shape mismatch");
+      if ((long long)y[b].rcap[k] < (long long)A[b].Rcap[k] * x[b].rcap[k])
+        return fail(TT_ERR_CAPACITY, "tt_matvec_batched: y rank capacity < R*r");
+      long long c = (long long)A[b].Rcap[k] * x[b].rcap[k] * A[b].m[k] * A[b].Rcap[k + 1] * x[b].rcap[k + 1];
+      mx = c > mx ? c : mx;
+      MvPair &p = host[(size_t)b * d + k];
+      p.A = A[b].data + A[b].off[k];
+      p.X = x[b].data + x[b].off[k];
+      p.Y = y[b].data + y[b].off[k];
+      p.R = A[b].R;
+      p.r = x[b].r;
+      p.ry = y[b].r;
+      p.m = A[b].m[k];
+      p.n = A[b].n[k];
+      p.k = k;
+      p.last = (k == d - 1);
+    }
+  }
+  cudaMemcpyAsync(ws, host.data(), need, cudaMemcpyHostToDevice, s);
+  // columns per core are distributed over bx CTAs; aim for ~16 CTAs per SM in total
+  const char *ev = getenv("TT_MV_BX");
+  int bx = ev ? atoi(ev) : (4736 / (d * B) > 4 ? 4736 / (d * B) : 4);
+  bx = bx < 1 ? 1 : (bx > 256 ? 256 : bx);
+  (void)mx;
+  long long acap = 1;
+  for (int b = 0; b < B; ++b)
+    for (int k = 0; k < d; ++k) {
+      const long long c = (long long)A[b].Rcap[k] * A[b].m[k] * A[b].n[k] * A[b].Rcap[k + 1];
+      acap = c > acap ? c : acap;
+    }
+  const int smcap = acap <= 6144 ? (int)acap : 0;
+  matvec_batched_kernel<<<dim3(bx, d, B), 256, (size_t)smcap * sizeof(double), s>>>((const MvPair *)ws, d, smcap);
+  return check_launch("tt_matvec_batched");
 }
 
 // ----------------------------------------------------------------- add ---

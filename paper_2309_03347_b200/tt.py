@@ -174,6 +174,18 @@ def tt_matvec(A: TTMat, x: TTVec, y: TTVec, stream=None):
     return y
 
 
+def tt_matvec_batched(As, xs, ys, stream=None):
+    """B independent products in one launch (C ABI tt_matvec_batched)."""
+    B = len(As)
+    Ac = (_lib.tt_mat * B)(*[a._c for a in As])
+    xc = (_lib.tt_vec * B)(*[v._c for v in xs])
+    yc = (_lib.tt_vec * B)(*[v._c for v in ys])
+    nb = lib().tt_matvec_batched_workspace(B, Ac)
+    ws = workspace(nb, xs[0].device)
+    check(lib().tt_matvec_batched(B, Ac, xc, yc, _ptr(ws), ws.numel(), C.c_void_p(_stream(stream))))
+    return ys
+
+
 def matvec_out(A: TTMat, x: TTVec) -> TTVec:
     """Allocate y with capacities R*r and compute y = A x."""
     y = TTVec(A.m, [a * b for a, b in zip(A.Rcap, x.rcap)], A.device)

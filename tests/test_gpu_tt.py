@@ -46,6 +46,19 @@ def test_matvec_c2_core_exact(seed):
         assert np.max(np.abs(g - r)) <= 1e-14 * max(np.max(np.abs(r)), 1e-300)
 
 
+def test_matvec_batched_core_exact():
+    insts = [inputs.c2_instance(s, d=12) for s in range(5)]
+    As = [tb.TTMat.from_cores(i["A"]) for i in insts]
+    Xs = [tb.TTVec.from_cores(i["X"]) for i in insts]
+    Ys = [tb.TTVec(a.m, [p * q for p, q in zip(a.Rcap, x.rcap)]) for a, x in zip(As, Xs)]
+    tb.tt_matvec_batched(As, Xs, Ys)
+    for inst, Y in zip(insts, Ys):
+        ref = ott.tt_matvec_fast(inst["A"], inst["X"])
+        assert Y.ranks() == ott.ranks(ref)
+        for g, r in zip(Y.cores(), ref):
+            assert np.max(np.abs(g - r)) <= 1e-14 * max(np.max(np.abs(r)), 1e-300)
+
+
 def test_matvec_d10_dense():
     inst = inputs.c2_slice(100)
     A = tb.TTMat.from_cores(inst["A"])
