@@ -257,15 +257,7 @@ def main():
         wall = time.perf_counter() - t0
     lib.tt_counters(cnt, 1)
     dev_ms = sum(step_ms)
-    if dist:
-        t = torch.tensor([dev_ms, float(iters_total)], dtype=torch.float64, device=device)
-        mx = t.clone()
-        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
-        sm = t.clone()
-        dist.all_reduce(sm, op=dist.ReduceOp.SUM)
-        dev_ms_max, iters_all = float(mx[0]), float(sm[1])
-    else:
-        dev_ms_max, iters_all = dev_ms, float(iters_total)
+    dev_ms_max, iters_all = aggregate_ranks(dev_ms, iters_total, dist, device)
     value = iters_all / (dev_ms_max * 1e-3)
     gemm_flops, mv_flops, qr_flops, svd_flops, ngemm = [int(v) for v in cnt]
     contraction = (gemm_flops + mv_flops) / args.steps
@@ -302,6 +294,20 @@ def main():
         print(json.dumps(line))
     if dist:
         dist.destroy_process_group()
+
+
+def aggregate_ranks(dev_ms, units, dist=None, device="cpu"):
+    """Whole-job aggregation over replicas: the device time is the MAX over ranks
+    and the work (units processed) the SUM; value = units / max time."""
+    if not dist:
+        return float(dev_ms), float(units)
+    import torch
+    t = torch.tensor([float(dev_ms), float(units)], dtype=torch.float64, device=device)
+    mx = t.clone()
+    dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+    sm = t.clone()
+    dist.all_reduce(sm, op=dist.ReduceOp.SUM)
+    return float(mx[0]), float(sm[1])
 
 
 def _events():

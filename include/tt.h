@@ -260,6 +260,17 @@ int32_t tt_transport_terms(int32_t op, int32_t nv, double extent, int32_t G, int
                            int32_t nbox, const int32_t *box_lo, const int32_t *box_hi,
                            const int32_t *box_mat, double *out);
 
+/* Reflective variant of configs[0] (reading Z15, not in the paper): H terms
+ * restricted to each octant's interior rows plus, per octant and first inflow
+ * axis a, the face equations psi_l - psi_{refl_a(l)} = 0 as rank-1 terms
+ * E_x (x) E_y (x) E_z (x) (C_b - R_{a,b}) (x) I_G; S and F as for vacuum. */
+int32_t tt_transport_terms_reflective(int32_t op, int32_t nv, double extent, int32_t G, int32_t L,
+                                      const double *mu, const double *eta, const double *xi,
+                                      const double *w, int32_t nmat, const double *sigma_t,
+                                      const double *sigma_s, const double *nu_sigma_f,
+                                      const double *chi, int32_t nbox, const int32_t *box_lo,
+                                      const int32_t *box_hi, const int32_t *box_mat, double *out);
+
 /* 1-D slab variant: the same construction restricted to the x
  * factor, two half-range blocks (mu < 0 then mu > 0); homogeneous material.
  * Each term writes 3 factors (x, angle, group): nv*nv + L*L + G*G doubles. */

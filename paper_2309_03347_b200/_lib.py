@@ -79,6 +79,8 @@ SIG = {
                                C.POINTER(tt_vec), C.c_double, C.POINTER(keff_opts), C.POINTER(keff_report),
                                P, C.c_size_t, P]),
     "tt_transport_terms": (I32, [I32, I32, C.c_double, I32, I32, P, P, P, P, I32, P, P, P, P, I32, P, P, P, P]),
+    "tt_transport_terms_reflective": (I32, [I32, I32, C.c_double, I32, I32, P, P, P, P, I32, P, P, P, P, I32, P, P,
+                                            P, P]),
     "tt_qtt_matrix": (C.c_int64, [I32, P, C.c_double, P, P, C.c_int64]),
     "tt_transport_terms_1d": (I32, [I32, I32, C.c_double, I32, I32, P, P, P, P, P, P, P]),
 }

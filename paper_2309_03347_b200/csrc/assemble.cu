@@ -271,11 +271,42 @@ extern "C" int32_t tt_transport_terms_1d(int32_t op, int32_t nv, double extent, 
   return nt;
 }
 
+static int32_t transport_terms_impl(int32_t op, int32_t nv, double extent, int32_t G, int32_t L, const double *mu,
+                                    const double *eta, const double *xi, const double *w, int32_t nmat,
+                                    const double *sigma_t, const double *sigma_s, const double *nu_sigma_f,
+                                    const double *chi, int32_t nbox, const int32_t *box_lo, const int32_t *box_hi,
+                                    const int32_t *box_mat, int32_t reflective, double *out);
+
 extern "C" int32_t tt_transport_terms(int32_t op, int32_t nv, double extent, int32_t G, int32_t L, const double *mu,
                                       const double *eta, const double *xi, const double *w, int32_t nmat,
                                       const double *sigma_t, const double *sigma_s, const double *nu_sigma_f,
                                       const double *chi, int32_t nbox, const int32_t *box_lo, const int32_t *box_hi,
                                       const int32_t *box_mat, double *out) {
+  return transport_terms_impl(op, nv, extent, G, L, mu, eta, xi, w, nmat, sigma_t, sigma_s, nu_sigma_f, chi, nbox,
+                              box_lo, box_hi, box_mat, 0, out);
+}
+
+// Reflective variant of configs[0] (reading Z15; not in the paper): the H
+// terms of octant b are restricted to its interior rows (no axis on an inflow
+// face); every inflow-face row carries psi_l - psi_refl(l) = 0, where refl
+// negates the cosine of the first inflow axis in (x, y, z) order:
+//   sum_b sum_a E^a_x (x) E^a_y (x) E^a_z (x) (C_b - R_{a,b}) (x) I_G.
+// S and F are unchanged (their inflow-face rows are already zero).
+extern "C" int32_t tt_transport_terms_reflective(int32_t op, int32_t nv, double extent, int32_t G, int32_t L,
+                                                 const double *mu, const double *eta, const double *xi,
+                                                 const double *w, int32_t nmat, const double *sigma_t,
+                                                 const double *sigma_s, const double *nu_sigma_f, const double *chi,
+                                                 int32_t nbox, const int32_t *box_lo, const int32_t *box_hi,
+                                                 const int32_t *box_mat, double *out) {
+  return transport_terms_impl(op, nv, extent, G, L, mu, eta, xi, w, nmat, sigma_t, sigma_s, nu_sigma_f, chi, nbox,
+                              box_lo, box_hi, box_mat, 1, out);
+}
+
+static int32_t transport_terms_impl(int32_t op, int32_t nv, double extent, int32_t G, int32_t L, const double *mu,
+                                    const double *eta, const double *xi, const double *w, int32_t nmat,
+                                    const double *sigma_t, const double *sigma_s, const double *nu_sigma_f,
+                                    const double *chi, int32_t nbox, const int32_t *box_lo, const int32_t *box_hi,
+                                    const int32_t *box_mat, int32_t reflective, double *out) {
   if (op < 0 || op > 2 || nv < 2 || G < 1 || L < 1 || nmat < 1 || nbox < 0 || !mu || !eta || !xi || !w || !sigma_t ||
       !sigma_s || !nu_sigma_f || !chi || (nbox > 0 && (!box_lo || !box_hi || !box_mat))) {
     tt::set_error("tt_transport_terms: invalid argument");
@@ -339,6 +370,7 @@ extern "C" int32_t tt_transport_terms(int32_t op, int32_t nv, double extent, int
     if (op == 0) {
       Mat IG(G);
       for (int g = 0; g < G; ++g) IG.at(g, g) = 1.0;
+      const size_t first = terms.size();
       push(Dx, Iy, Iz, Qmu, IG);                  // H_x^{TT,b}
       push(Ix, Dy, Iz, Qeta, IG);                 // H_y^{TT,b}
       push(Ix, Iy, Dz, Qxi, IG);                  // H_z^{TT,b}
@@ -349,6 +381,45 @@ extern "C" int32_t tt_transport_terms(int32_t op, int32_t nv, double extent, int
         push(mul(row_indicator(sx, nv, box_lo[3 * t], box_hi[3 * t]), Ix),
              mul(row_indicator(sy, nv, box_lo[3 * t + 1], box_hi[3 * t + 1]), Iy),
              mul(row_indicator(sz, nv, box_lo[3 * t + 2], box_hi[3 * t + 2]), Iz), Cb, E);
+      }
+      if (reflective) {
+        // interior-row masks of this octant (vertex not on its inflow face)
+        Mat Px(nv), Py(nv), Pz(nv), Ox(nv), Oy(nv), Oz(nv), Id(nv);
+        for (int i = 0; i < nv; ++i) {
+          Id.at(i, i) = 1.0;
+          Px.at(i, i) = (i != (sx > 0 ? 0 : nv - 1)) ? 1.0 : 0.0;
+          Py.at(i, i) = (i != (sy > 0 ? 0 : nv - 1)) ? 1.0 : 0.0;
+          Pz.at(i, i) = (i != (sz > 0 ? 0 : nv - 1)) ? 1.0 : 0.0;
+          Ox.at(i, i) = 1.0 - Px.at(i, i);
+          Oy.at(i, i) = 1.0 - Py.at(i, i);
+          Oz.at(i, i) = 1.0 - Pz.at(i, i);
+        }
+        for (size_t t = first; t < terms.size(); ++t) {
+          terms[t].fx = mul(Px, terms[t].fx);
+          terms[t].fy = mul(Py, terms[t].fy);
+          terms[t].fz = mul(Pz, terms[t].fz);
+        }
+        // face rows, by first inflow axis a: psi_l - psi_{refl_a(l)} = 0
+        for (int a = 0; a < 3; ++a) {
+          Mat Ang(L);
+          for (int l = 0; l < L; ++l) {
+            if (!in_oct(l)) continue;
+            double t3[3] = {mu[l], eta[l], xi[l]};
+            t3[a] = -t3[a];
+            int best = 0;
+            double bd = 1e300;
+            for (int lp = 0; lp < L; ++lp) {
+              const double d0 = mu[lp] - t3[0], d1 = eta[lp] - t3[1], d2 = xi[lp] - t3[2];
+              const double dd = d0 * d0 + d1 * d1 + d2 * d2;
+              if (dd < bd) { bd = dd; best = lp; }
+            }
+            Ang.at(l, l) += 1.0;
+            Ang.at(l, best) -= 1.0;
+          }
+          if (a == 0) push(Ox, Id, Id, Ang, IG);
+          else if (a == 1) push(Px, Oy, Id, Ang, IG);
+          else push(Px, Py, Oz, Ang, IG);
+        }
       }
     } else {
       const int kind = op == 1 ? 1 : 2;          // S (Z4) / F (Z5)

@@ -67,12 +67,13 @@ def factor_terms(prob, op: str):
     args = [OPS[op], nv, float(prob["extent"]), G, L, *[_dp(a) for a in arr], len(mats), _dp(st), _dp(ss),
             _dp(nf), _dp(chi), len(boxes), _dp(lo), _dp(hi), _dp(bm)]
     lib = _lib.lib()
-    nt = lib.tt_transport_terms(*args, None)
+    fn = lib.tt_transport_terms_reflective if prob.get("boundary", "vacuum") == "reflective" else lib.tt_transport_terms
+    nt = fn(*args, None)
     if nt < 0:
         raise _lib.TTError(1, lib.tt_last_error().decode())
     per = 3 * nv * nv + L * L + G * G
     out = np.zeros(nt * per, dtype=np.float64)
-    lib.tt_transport_terms(*args, _dp(out))
+    fn(*args, _dp(out))
     terms = []
     for t in range(nt):
         p = out[t * per:(t + 1) * per]

@@ -123,3 +123,22 @@ def test_keff_c1_vacuum():
     it = res.iters.item()
     hist = res.k_hist[:it].cpu().numpy()
     assert abs(hist[-1] - res.k.item()) == 0.0
+
+
+def test_keff_c1_reflective():
+    """configs[0] reflective variant (reading Z15): the device-assembled operator
+    equals the dense one, k -> k_inf = nuSf / (St - Ss) = 1.2 and, from psi0 = 1,
+    k0 = 1, the iterates follow k_tau = 1.2 - 0.2 * 0.5^tau (closed form)."""
+    prob = inputs.problem_c1("reflective")
+    dense = T.dense_operators(prob)
+    ops = gtr.operators(prob)
+    for k in "HSF":
+        got = ott.ttm_full(ops[k].cores())
+        assert np.max(np.abs(got - dense[k])) <= 1e-12 * np.abs(dense[k]).max()
+    res, psi = _keff_gpu(prob, [8, 8, 8, 8, 1], rmax=64, tol_k=1e-10, eps_round=1e-13, eps_solve=1e-12,
+                         max_outer=60)
+    it = res.iters.item()
+    hist = res.k_hist[:it].cpu().numpy()
+    assert abs(res.k.item() - 1.2) <= 1e-8
+    for tau, kt in enumerate(hist[:10], start=1):
+        assert abs(kt - (1.2 - 0.2 * 0.5 ** tau)) <= 1e-8

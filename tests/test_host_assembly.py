@@ -40,3 +40,15 @@ def test_qtt_alg1_host(gtr):
     cores = gtr.qtt_matrix(R)
     assert np.max(np.abs(ott.ttm_full(cores) - R)) <= 1e-13 * np.abs(R).max()
     assert ott.ranks(cores) == [1, 4, 4, 1]
+
+
+def test_reflective_terms_sum_to_dense(gtr):
+    """Reading Z15: the rank-1 reflective terms of the host builder sum to the
+    oracle's dense reflective operators (row-replacement construction)."""
+    import copy
+    p = copy.deepcopy(inputs.problem_c1("reflective"))
+    p["nv"] = 4
+    dense = T.dense_operators(p)
+    for op in "HSF":
+        M = sum(T.kron_term(t) for t in gtr.factor_terms(p, op))
+        assert np.array_equal(M, dense[op])
