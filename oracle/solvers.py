@@ -254,6 +254,107 @@ def amen_solve(A, b, x0, z0, eps=1e-8, max_sweeps=20, rmax=10**9, dense_max=2000
     return x, {"res_hist": hist, "dx_hist": dx_hist, "sweeps": sweeps}
 
 
+# ------------------------------------------------------------ amen_mv ---
+
+
+def amen_mv(A, b, y0, z0, eps=1e-8, max_sweeps=20, rmax=10**9):
+    """Fit-based matvec y ~ A b (P:1489-1494 eqn:mv_obj, P:1501-1506 'amen_mv';
+    NEXT-1): minimise ||A b - y|| one core at a time without forming the rank R r
+    product.  With orthonormal frames of y the local minimiser is the projection
+      y_k = Phi^{yAb}_{k-1} A_k Psi^{yAb}_{k+1} b_k
+    (Phi^{yAb} = interfaces with test y, operator A, trial b).  Then, as in
+    amen_solve: SVD truncation (delta = eps ||y_k|| / sqrt(d-1), rmax), residual
+    core z_k = proj_z (A b - y) with z frames on both sides, enrichment of y_k by
+    the residual projected on (y frames | z frames), QR, carry.  Sweeps alternate;
+    stop when the max relative change of a local core is <= eps.
+    Returns (y, info)."""
+    d = len(A)
+    y, _ = ott.tt_orthogonalize_rl(y0)
+    z, _ = ott.tt_orthogonalize_rl(z0)
+    one3 = np.ones((1, 1, 1)); one2 = np.ones((1, 1))
+    YA = [None] * (d + 2); ZA = [None] * (d + 2); ZY = [None] * (d + 2)
+    YA[0] = YA[d + 1] = one3; ZA[0] = ZA[d + 1] = one3; ZY[0] = ZY[d + 1] = one2
+    for k in range(d, 1, -1):
+        YA[k] = ott.right_update(YA[k + 1], y[k - 1], A[k - 1], b[k - 1])
+        ZA[k] = ott.right_update(ZA[k + 1], z[k - 1], A[k - 1], b[k - 1])
+        ZY[k] = ott.right_update_vec(ZY[k + 1], z[k - 1], y[k - 1])
+    direction = +1
+    dx_hist = []
+    sweeps = 0
+    for sweep in range(max_sweeps):
+        sweeps += 1
+        maxdx = 0.0
+        order = range(1, d + 1) if direction > 0 else range(d, 0, -1)
+        for k in order:
+            Ak, bk = A[k - 1], b[k - 1]
+            sol = ott.local_apply(YA[k - 1], Ak, YA[k + 1], bk)          # projection of A b
+            nsol = np.linalg.norm(sol)
+            old = y[k - 1]
+            if old.shape == sol.shape:
+                maxdx = max(maxdx, np.linalg.norm(sol - old) / nsol if nsol > 0 else 0.0)
+            else:
+                maxdx = max(maxdx, 1.0)
+            r0, n, r1 = sol.shape
+            last = (k == d) if direction > 0 else (k == 1)
+            if last:
+                y[k - 1] = sol
+                continue
+            if direction > 0:
+                M = sol.reshape(r0 * n, r1, order="F")
+                U, s, Vt = np.linalg.svd(M, full_matrices=False)
+                rr = ott.trunc_rank(s, eps * np.linalg.norm(s) / math.sqrt(d - 1), rmax)
+                U = U[:, :rr]; SV = s[:rr, None] * Vt[:rr]
+                yfull = (U @ SV).reshape(r0, n, r1, order="F")
+                crz = ott.local_apply(ZA[k - 1], Ak, ZA[k + 1], bk) - ott.local_rhs(ZY[k - 1], yfull, ZY[k + 1])
+                z0_, zn, z1_ = crz.shape
+                Qz, _ = np.linalg.qr(crz.reshape(z0_ * zn, z1_, order="F"))
+                z[k - 1] = Qz.reshape(z0_, zn, Qz.shape[1], order="F")
+                if z[k].shape[0] != Qz.shape[1]:
+                    zk1 = np.zeros((Qz.shape[1],) + z[k].shape[1:])
+                    mm = min(Qz.shape[1], z[k].shape[0])
+                    zk1[:mm] = z[k][:mm]
+                    z[k] = zk1
+                # enrichment: (y frames | z frames) projection of A b - y
+                crs = ott.local_apply(YA[k - 1], Ak, ZA[k + 1], bk) - \
+                    np.einsum("aib,cb->aic", yfull, ZY[k + 1])
+                Ue = np.concatenate([U, crs.reshape(r0 * n, -1, order="F")], axis=1)
+                Q, R = np.linalg.qr(Ue)
+                y[k - 1] = Q.reshape(r0, n, Q.shape[1], order="F")
+                y[k] = np.einsum("cb,bjd->cjd", R[:, :rr] @ SV, y[k])
+                YA[k] = ott.left_update(YA[k - 1], y[k - 1], Ak, bk)
+                ZA[k] = ott.left_update(ZA[k - 1], z[k - 1], Ak, bk)
+                ZY[k] = ott.left_update_vec(ZY[k - 1], z[k - 1], y[k - 1])
+            else:
+                M = sol.reshape(r0, n * r1, order="F")
+                U, s, Vt = np.linalg.svd(M, full_matrices=False)
+                rr = ott.trunc_rank(s, eps * np.linalg.norm(s) / math.sqrt(d - 1), rmax)
+                US = U[:, :rr] * s[:rr]; Vt = Vt[:rr]
+                yfull = (US @ Vt).reshape(r0, n, r1, order="F")
+                crz = ott.local_apply(ZA[k - 1], Ak, ZA[k + 1], bk) - ott.local_rhs(ZY[k - 1], yfull, ZY[k + 1])
+                z0_, zn, z1_ = crz.shape
+                Qz, _ = np.linalg.qr(crz.reshape(z0_, zn * z1_, order="F").T)
+                z[k - 1] = Qz.T.reshape(Qz.shape[1], zn, z1_, order="F")
+                if z[k - 2].shape[2] != Qz.shape[1]:
+                    zk1 = np.zeros(z[k - 2].shape[:2] + (Qz.shape[1],))
+                    mm = min(Qz.shape[1], z[k - 2].shape[2])
+                    zk1[:, :, :mm] = z[k - 2][:, :, :mm]
+                    z[k - 2] = zk1
+                crs = ott.local_apply(ZA[k - 1], Ak, YA[k + 1], bk) - \
+                    np.einsum("ab,bic->aic", ZY[k - 1], yfull)
+                Ve = np.concatenate([Vt, crs.reshape(crs.shape[0], n * r1, order="F")], axis=0)
+                Q, R = np.linalg.qr(Ve.T)
+                y[k - 1] = Q.T.reshape(Q.shape[1], n, r1, order="F")
+                y[k - 2] = np.einsum("aib,bc->aic", y[k - 2], US @ R[:, :rr].T)
+                YA[k] = ott.right_update(YA[k + 1], y[k - 1], Ak, bk)
+                ZA[k] = ott.right_update(ZA[k + 1], z[k - 1], Ak, bk)
+                ZY[k] = ott.right_update_vec(ZY[k + 1], z[k - 1], y[k - 1])
+        dx_hist.append(maxdx)
+        if maxdx <= eps:
+            break
+        direction = -direction
+    return y, {"dx_hist": dx_hist, "sweeps": sweeps}
+
+
 # ------------------------------------------------------------ k-eff ---
 
 

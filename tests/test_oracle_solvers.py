@@ -87,3 +87,39 @@ def test_keff_tt_matches_dense_small():
     v = ott.tt_full(psi)
     v = v * np.sign(v.sum()) / np.linalg.norm(v)
     assert np.linalg.norm(v - psid * np.sign(psid.sum())) < 1e-6
+
+
+def test_amen_mv_pins():
+    """NEXT-1 fit-based matvec: identity, rank-1 exactness, dense
+    product on a d=10 C2 slice, and a truncated transport apply vs exact+round."""
+    g = inputs.rng(80)
+    modes = [2, 3, 4, 2]
+    b = inputs.random_tt(g, modes, [1, 2, 3, 2, 1])
+    I = ott.rank1_ttm([np.eye(n) for n in modes])
+    y0 = inputs.random_tt(g, modes, [1, 1, 1, 1, 1])
+    z0 = inputs.random_tt(g, modes, [1, 2, 2, 2, 1])
+    y, _ = so.amen_mv(I, b, y0, z0, eps=1e-12)
+    assert np.linalg.norm(ott.tt_full(y) - ott.tt_full(b)) <= 1e-12 * np.linalg.norm(ott.tt_full(b))
+    Fs = [g.standard_normal((n, n)) for n in modes]
+    vs = [g.standard_normal(n).reshape(1, n, 1) for n in modes]
+    y, _ = so.amen_mv(ott.rank1_ttm(Fs), vs, y0, z0, eps=1e-12)
+    ref = ott.tt_full(ott.tt_matvec(ott.rank1_ttm(Fs), vs))
+    assert np.linalg.norm(ott.tt_full(y) - ref) <= 1e-12 * np.linalg.norm(ref)
+    inst = inputs.c2_slice(110)
+    d = 10
+    y0 = inputs.random_tt(g, [2] * d, [1] + [2] * (d - 1) + [1])
+    z0 = inputs.random_tt(g, [2] * d, [1] + [4] * (d - 1) + [1])
+    y, _ = so.amen_mv(inst["A"], inst["X"], y0, z0, eps=1e-10, max_sweeps=40)
+    ref = ott.ttm_full(inst["A"]) @ ott.tt_full(inst["X"])
+    assert np.linalg.norm(ott.tt_full(y) - ref) <= 1e-12 * np.linalg.norm(ref)
+    # QTT slab transport operator applied to a smooth rank-2 function, truncated
+    p = inputs.problem_slab(4, nv=256)
+    H = T.tt_operators(p, eps=1e-12)["H"]
+    modes = T.qtt_modes(p)
+    d = len(modes)
+    x = inputs.random_tt(g, modes, [1] + [2] * (d - 1) + [1])
+    y0 = inputs.random_tt(g, modes, [1] + [2] * (d - 1) + [1])
+    z0 = inputs.random_tt(g, modes, [1] + [3] * (d - 1) + [1])
+    y, info = so.amen_mv(H, x, y0, z0, eps=1e-8, max_sweeps=40)
+    ref = ott.tt_full(ott.tt_matvec_fast(H, x))
+    assert np.linalg.norm(ott.tt_full(y) - ref) <= 1e-7 * np.linalg.norm(ref)
