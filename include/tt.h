@@ -209,6 +209,22 @@ size_t amen_workspace(const tt_mat *A, const tt_vec *b, const tt_vec *x, const t
 tt_status amen_solve(const tt_mat *A, const tt_vec *b, tt_vec *x, tt_vec *z, const amen_opts *o,
                      int32_t *sweeps_dev, double *res_dev, void *ws, size_t wsb, tt_stream s);
 
+/* ------------------------------------------------------------ NEXT-1 ---
+ * amen_mv: y ~ A b in TT without forming the rank-R r product (P:1489-1494,
+ * P:1505-1506 "amen_mv"; reading Z37): the same alternating sweeps as
+ * amen_solve with the local projection y_k = (y|A|b)_{k-1} A_k (y|A|b)_{k+1} b_k
+ * in place of the local solve, SVD truncation at delta = eps ||y_k|| / sqrt(d-1)
+ * capped at rmax, and enrichment by the projected residual A b - y carried
+ * by the residual TT z.  Stops after a sweep whose maximum relative change of
+ * a local core is <= eps, or after max_sweeps.  A may be rectangular
+ * (A.m = y modes, A.n = b modes).  y: in initial guess (its ranks are kept as
+ * the starting frames), out the product (capacities >= rmax + z capacities).
+ * z: in initial residual TT (random draws are inputs), workspace afterwards.
+ * sweeps_dev (may be NULL): sweeps used.  Workspace: amen_mv_workspace. */
+size_t amen_mv_workspace(const tt_mat *A, const tt_vec *b, const tt_vec *y, const tt_vec *z);
+tt_status amen_mv(const tt_mat *A, const tt_vec *b, tt_vec *y, tt_vec *z, double eps, int32_t max_sweeps,
+                  int32_t rmax, int32_t *sweeps_dev, void *ws, size_t wsb, tt_stream s);
+
 /* ---------------------------------------------------------------- a9 ---
  * keff_fixed_point: eqn:TT_k_eff_fixed_points, readings
  * Z16-Z19:

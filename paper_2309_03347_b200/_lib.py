@@ -73,6 +73,10 @@ SIG = {
                                     C.POINTER(tt_vec), C.POINTER(amen_opts)]),
     "amen_solve": (I32, [C.POINTER(tt_mat), C.POINTER(tt_vec), C.POINTER(tt_vec), C.POINTER(tt_vec),
                          C.POINTER(amen_opts), P, P, P, C.c_size_t, P]),
+    "amen_mv_workspace": (C.c_size_t, [C.POINTER(tt_mat), C.POINTER(tt_vec), C.POINTER(tt_vec),
+                                       C.POINTER(tt_vec)]),
+    "amen_mv": (I32, [C.POINTER(tt_mat), C.POINTER(tt_vec), C.POINTER(tt_vec), C.POINTER(tt_vec), C.c_double,
+                      I32, I32, P, P, C.c_size_t, P]),
     "keff_workspace": (C.c_size_t, [C.POINTER(tt_mat), C.POINTER(tt_mat), C.POINTER(tt_mat),
                                     C.POINTER(tt_vec), C.POINTER(tt_vec), C.POINTER(keff_opts)]),
     "keff_fixed_point": (I32, [C.POINTER(tt_mat), C.POINTER(tt_mat), C.POINTER(tt_mat), C.POINTER(tt_vec),

@@ -216,36 +216,10 @@ __global__ void trunc_kernel(Dev D, int k, int dir) {
   }
 }
 
-// Residual core z_k, enrichment of the solution core, neighbour update.
-__global__ void plan_enrich(Dev D, int k, int dir) {
-  const int d = D.x.d;
-  const int n = D.x.n[k];
-  const int r0 = D.x.r[k], r1 = D.x.r[k + 1], z0 = D.z.r[k], z1 = D.z.r[k + 1];
-  const int R0 = D.A.R[k], R1 = D.A.R[k + 1], b0 = D.b.r[k], b1 = D.b.r[k + 1];
-  const double *Bk = D.b.data + D.b.off[k], *Ak = D.A.data + D.A.off[k];
-  const int r = D.iv[1], mm = D.iv[4], nn = D.iv[5];
-  GemmDesc *g = D.gd;
-  // ---- crz [z0, n, z1] = zb-rhs - zAx-apply(xfull)
-  descs_local_rhs(z0, b0, n, z1, b1, D.ZBL[k], Bk, D.ZBR[k + 1], D.crz, D.T1, g + 0);
-  descs_local_apply(z0, R0, r0, n, n, z1, R1, r1, D.ZAL[k], Ak, D.ZAR[k + 1], D.xfull, D.crz, D.T1, D.T2, g + 2);
-  g[4].alpha = -1.0; g[4].beta = 1.0;
-  // ---- crs: x frames on the orthonormal side, z frames on the carry side, written as extra
-  //      columns of Ue (M orientation): dir > 0: [r0, n, z1] left unfolding -> Ue[:, r:r+z1]
-  //      dir < 0: [z0, n, r1] transposed right unfolding -> Ue[:, r:r+z0]
-  double *Uc = D.Ue + (long long)r * mm;
-  if (dir > 0) {
-    descs_local_rhs(r0, b0, n, z1, b1, D.BL[k], Bk, D.ZBR[k + 1], Uc, D.T1, g + 5);
-    descs_local_apply(r0, R0, r0, n, n, z1, R1, r1, D.AL[k], Ak, D.ZAR[k + 1], D.xfull, Uc, D.T1, D.T2, g + 7);
-  } else {
-    descs_local_rhs(z0, b0, n, r1, b1, D.ZBL[k], Bk, D.BR[k + 1], Uc, D.T1, g + 5);
-    descs_local_apply(z0, R0, r0, n, n, r1, R1, r1, D.ZAL[k], Ak, D.AR[k + 1], D.xfull, Uc, D.T1, D.T2, g + 7);
-    // output element (a, c) of the final GEMMs -> Ue[c + mm a] (transposed)
-    g[6].s_r0 = mm; g[6].s_c0 = 1;
-    g[9].s_r0 = mm; g[9].s_c0 = 1;
-  }
-  g[9].alpha = -1.0; g[9].beta = 1.0;
-  const int ze = dir > 0 ? z1 : z0;  // extra columns
-  // ---- QR of crz (z core) and of Ue (x core), one launch
+// QR of crz (z core) and of Ue (x core) in one launch, K = Re[:, :r] Ct^T, and
+// the carry into the neighbour core (shared by amen_solve and amen_mv).
+__device__ void enrich_tail(const Dev &D, int k, int dir, int n, int r, int mm, int nn, int ze, int z0, int z1,
+                            GemmDesc *g) {
   QRDesc &qz = D.qd[0];
   QRDesc &qx = D.qd[1];
   double *Zk = D.z.data + D.z.off[k];
@@ -296,6 +270,38 @@ __global__ void plan_enrich(Dev D, int k, int dir) {
     D.x.r[k] = q;
     D.z.r[k] = qzr;   // z_{k-1} keeps its first qzr columns (no data movement)
   }
+}
+
+// Residual core z_k, enrichment of the solution core, neighbour update.
+__global__ void plan_enrich(Dev D, int k, int dir) {
+  const int d = D.x.d;
+  const int n = D.x.n[k];
+  const int r0 = D.x.r[k], r1 = D.x.r[k + 1], z0 = D.z.r[k], z1 = D.z.r[k + 1];
+  const int R0 = D.A.R[k], R1 = D.A.R[k + 1], b0 = D.b.r[k], b1 = D.b.r[k + 1];
+  const double *Bk = D.b.data + D.b.off[k], *Ak = D.A.data + D.A.off[k];
+  const int r = D.iv[1], mm = D.iv[4], nn = D.iv[5];
+  GemmDesc *g = D.gd;
+  // ---- crz [z0, n, z1] = zb-rhs - zAx-apply(xfull)
+  descs_local_rhs(z0, b0, n, z1, b1, D.ZBL[k], Bk, D.ZBR[k + 1], D.crz, D.T1, g + 0);
+  descs_local_apply(z0, R0, r0, n, n, z1, R1, r1, D.ZAL[k], Ak, D.ZAR[k + 1], D.xfull, D.crz, D.T1, D.T2, g + 2);
+  g[4].alpha = -1.0; g[4].beta = 1.0;
+  // ---- crs: x frames on the orthonormal side, z frames on the carry side, written as extra
+  //      columns of Ue (M orientation): dir > 0: [r0, n, z1] left unfolding -> Ue[:, r:r+z1]
+  //      dir < 0: [z0, n, r1] transposed right unfolding -> Ue[:, r:r+z0]
+  double *Uc = D.Ue + (long long)r * mm;
+  if (dir > 0) {
+    descs_local_rhs(r0, b0, n, z1, b1, D.BL[k], Bk, D.ZBR[k + 1], Uc, D.T1, g + 5);
+    descs_local_apply(r0, R0, r0, n, n, z1, R1, r1, D.AL[k], Ak, D.ZAR[k + 1], D.xfull, Uc, D.T1, D.T2, g + 7);
+  } else {
+    descs_local_rhs(z0, b0, n, r1, b1, D.ZBL[k], Bk, D.BR[k + 1], Uc, D.T1, g + 5);
+    descs_local_apply(z0, R0, r0, n, n, r1, R1, r1, D.ZAL[k], Ak, D.AR[k + 1], D.xfull, Uc, D.T1, D.T2, g + 7);
+    // output element (a, c) of the final GEMMs -> Ue[c + mm a] (transposed)
+    g[6].s_r0 = mm; g[6].s_c0 = 1;
+    g[9].s_r0 = mm; g[9].s_c0 = 1;
+  }
+  g[9].alpha = -1.0; g[9].beta = 1.0;
+  const int ze = dir > 0 ? z1 : z0;  // extra columns
+  enrich_tail(D, k, dir, n, r, mm, nn, ze, z0, z1, g);
   (void)d;
 }
 
@@ -592,6 +598,296 @@ tt_status amen_solve_meta(const MatMeta &A, const VecMeta &b, const VecMeta &x, 
     cudaStreamSynchronize(s);
   }
   return check_launch("amen_solve");
+}
+
+// =====================================================================
+// amen_mv (NEXT-1): y ~ A b by ALS on ||A b - y||^2.  Reuses the
+// AMEn machinery with D.x = y and the interface families
+//   AL/AR = (y | A | b) [ry, R, rb],  ZAL/ZAR = (z | A | b) [rz, R, rb],
+//   ZBL/ZBR = (z | y) [rz, ry];
+// the local "solve" is the projection y_k = Phi^{yAb} A_k Psi^{yAb} b_k.
+// =====================================================================
+namespace {
+
+__global__ void init_ifaces_mv(Dev D) {
+  const int d = D.x.d;
+  D.AL[0][0] = 1.0; D.ZAL[0][0] = 1.0; D.ZBL[0][0] = 1.0;
+  D.AR[d][0] = 1.0; D.ZAR[d][0] = 1.0; D.ZBR[d][0] = 1.0;
+}
+
+__global__ void plan_iface_mv(Dev D, int k, int dir) {
+  const int n = D.x.n[k], nb = D.b.n[k];
+  const int y0 = D.x.r[k], y1 = D.x.r[k + 1], z0 = D.z.r[k], z1 = D.z.r[k + 1];
+  const int R0 = D.A.R[k], R1 = D.A.R[k + 1], b0 = D.b.r[k], b1 = D.b.r[k + 1];
+  const double *Y = D.x.data + D.x.off[k], *Z = D.z.data + D.z.off[k], *Bk = D.b.data + D.b.off[k];
+  const double *Ak = D.A.data + D.A.off[k];
+  if (dir < 0) {
+    descs_iface_right(y0, R0, b0, n, nb, y1, R1, b1, D.AR[k + 1], Y, Ak, Bk, D.AR[k], D.T1, D.T2, D.gd + 0);
+    descs_iface_right(z0, R0, b0, n, nb, z1, R1, b1, D.ZAR[k + 1], Z, Ak, Bk, D.ZAR[k], D.T1, D.T2, D.gd + 3);
+    descs_iface_right_vec(z0, y0, n, z1, y1, D.ZBR[k + 1], Z, Y, D.ZBR[k], D.T1, D.gd + 6);
+  } else {
+    descs_iface_left(y0, R0, b0, n, nb, y1, R1, b1, D.AL[k], Y, Ak, Bk, D.AL[k + 1], D.T1, D.T2, D.gd + 0);
+    descs_iface_left(z0, R0, b0, n, nb, z1, R1, b1, D.ZAL[k], Z, Ak, Bk, D.ZAL[k + 1], D.T1, D.T2, D.gd + 3);
+    descs_iface_left_vec(z0, y0, n, z1, y1, D.ZBL[k], Z, Y, D.ZBL[k + 1], D.T1, D.gd + 6);
+  }
+}
+
+// local projection into sol, copies y_k -> xold (dx) and sol -> y_k (last core)
+__global__ void plan_local_mv(Dev D, int k) {
+  const int n = D.x.n[k], nb = D.b.n[k];
+  const int y0 = D.x.r[k], y1 = D.x.r[k + 1];
+  const int R0 = D.A.R[k], R1 = D.A.R[k + 1], b0 = D.b.r[k], b1 = D.b.r[k + 1];
+  const double *Bk = D.b.data + D.b.off[k], *Ak = D.A.data + D.A.off[k];
+  const int N = y0 * n * y1;
+  D.iv[0] = N;
+  descs_local_apply(y0, R0, b0, n, nb, y1, R1, b1, D.AL[k], Ak, D.AR[k + 1], Bk, D.sol, D.T1, D.T2, D.gd + 0);
+  D.cd[1] = cpy(N, 1, D.sol, 1, N, D.x.data + D.x.off[k], 1, N);
+  D.cd[2] = cpy(N, 1, D.x.data + D.x.off[k], 1, N, D.xold, 1, N);
+}
+
+__global__ void plan_enrich_mv(Dev D, int k, int dir) {
+  const int n = D.x.n[k], nb = D.b.n[k];
+  const int y0 = D.x.r[k], y1 = D.x.r[k + 1], z0 = D.z.r[k], z1 = D.z.r[k + 1];
+  const int R0 = D.A.R[k], R1 = D.A.R[k + 1], b0 = D.b.r[k], b1 = D.b.r[k + 1];
+  const double *Bk = D.b.data + D.b.off[k], *Ak = D.A.data + D.A.off[k];
+  const int r = D.iv[1], mm = D.iv[4], nn = D.iv[5];
+  GemmDesc *g = D.gd;
+  // crz [z0, n, z1] = (z|A|b) apply - (z|y) projection of the truncated y_k
+  descs_local_apply(z0, R0, b0, n, nb, z1, R1, b1, D.ZAL[k], Ak, D.ZAR[k + 1], Bk, D.crz, D.T1, D.T2, g + 0);
+  descs_local_rhs(z0, y0, n, z1, y1, D.ZBL[k], D.xfull, D.ZBR[k + 1], D.crz, D.T1, g + 3);
+  g[4].alpha = -1.0; g[4].beta = 1.0;
+  double *Uc = D.Ue + (long long)r * mm;
+  if (dir > 0) {
+    // [y0, n, z1]: (y|A|b) left, (z|A|b) right; minus y_k x_3 (z|y)_{k+1}^T
+    descs_local_apply(y0, R0, b0, n, nb, z1, R1, b1, D.AL[k], Ak, D.ZAR[k + 1], Bk, Uc, D.T1, D.T2, g + 5);
+    g[8] = gd_make(y0 * n, z1, y1, D.xfull, (long long)y0 * n, 0, D.ZBR[k + 1], z1, 1);
+    gd_plain(g[8], Uc, mm);
+  } else {
+    // [z0, n, y1]: (z|A|b) left, (y|A|b) right; minus (z|y)_k y_k; written transposed into Ue
+    descs_local_apply(z0, R0, b0, n, nb, y1, R1, b1, D.ZAL[k], Ak, D.AR[k + 1], Bk, Uc, D.T1, D.T2, g + 5);
+    g[7].s_r0 = mm; g[7].s_c0 = 1;
+    g[8] = gd_make(z0, n * y1, y0, D.ZBL[k], z0, 0, D.xfull, y0, 0);
+    gd_plain(g[8], Uc, 1);
+    g[8].s_r0 = mm; g[8].s_c0 = 1;
+  }
+  g[8].alpha = -1.0; g[8].beta = 1.0;
+  g[9] = gd_make(0, 0, 0, nullptr, 1, 0, nullptr, 1, 0);
+  gd_plain(g[9], nullptr, 1);
+  const int ze = dir > 0 ? z1 : z0;
+  enrich_tail(D, k, dir, n, r, mm, nn, ze, z0, z1, g);
+}
+
+}  // namespace
+
+struct MvCtx {
+  Dev D;
+  char *orth_base;
+  size_t orth_cap;
+  double *split;
+  unsigned int *bar;
+  long long Ncap, Scap;
+  int pc;
+};
+
+static tt_status carve_mv(const MatMeta &A, const VecMeta &b, const VecMeta &y, const VecMeta &z, Arena &ar,
+                          MvCtx &P) {
+  const int d = A.d;
+  if (b.d != d || y.d != d || z.d != d) return fail(TT_ERR_SHAPE, "amen_mv: number of cores differ");
+  for (int k = 0; k < d; ++k)
+    if (A.n[k] != b.n[k] || A.m[k] != y.n[k] || z.n[k] != y.n[k]) return fail(TT_ERR_SHAPE, "amen_mv: shape mismatch");
+  for (int k = 1; k < d; ++k)
+    if (y.rcap[k] <= z.rcap[k]) return fail(TT_ERR_CAPACITY, "amen_mv: y rank capacity must exceed z's");
+  std::memset(&P, 0, sizeof(P));
+  Dev &D = P.D;
+  D.x = y; D.z = z; D.b = b; D.A = A;
+  D.m = 0;
+  long long Ncap = 1, Zcap = 1, Tcap = 1, Ecap = 1, Scap = 1;
+  int pc = 1, zcm = 1;
+  for (int k = 0; k <= d; ++k) { pc = y.rcap[k] > pc ? y.rcap[k] : pc; zcm = z.rcap[k] > zcm ? z.rcap[k] : zcm; }
+  for (int k = 0; k < d; ++k) {
+    const long long n = lmax(y.n[k], b.n[k]);
+    Ncap = lmax(Ncap, (long long)y.rcap[k] * n * y.rcap[k + 1]);
+    Zcap = lmax(Zcap, (long long)z.rcap[k] * n * z.rcap[k + 1]);
+    long long rm = lmax(lmax(y.rcap[k], y.rcap[k + 1]), lmax(z.rcap[k], z.rcap[k + 1]));
+    rm = lmax(rm, lmax(b.rcap[k], b.rcap[k + 1]));
+    const long long Rm = lmax(A.Rcap[k], A.Rcap[k + 1]);
+    Tcap = lmax(Tcap, n * rm * rm * Rm);
+    Ecap = lmax(Ecap, n * lmax(y.rcap[k], y.rcap[k + 1]) * (pc + zcm));
+    Scap = lmax(Scap, lmax((long long)y.rcap[k] * n * y.rcap[k + 1], (long long)z.rcap[k] * n * z.rcap[k + 1]));
+  }
+  P.Ncap = Ncap; P.Scap = Scap; P.pc = pc;
+  for (int k = 0; k <= d; ++k) {
+    D.AL[k] = ar.take<double>((size_t)y.rcap[k] * A.Rcap[k] * b.rcap[k]);
+    D.AR[k] = ar.take<double>((size_t)y.rcap[k] * A.Rcap[k] * b.rcap[k]);
+    D.ZAL[k] = ar.take<double>((size_t)z.rcap[k] * A.Rcap[k] * b.rcap[k]);
+    D.ZAR[k] = ar.take<double>((size_t)z.rcap[k] * A.Rcap[k] * b.rcap[k]);
+    D.ZBL[k] = ar.take<double>((size_t)z.rcap[k] * y.rcap[k]);
+    D.ZBR[k] = ar.take<double>((size_t)z.rcap[k] * y.rcap[k]);
+  }
+  D.sol = ar.take<double>(Ncap);
+  D.xold = ar.take<double>(Ncap);
+  D.T1 = ar.take<double>(Tcap);
+  D.T2 = ar.take<double>(Tcap);
+  D.crz = ar.take<double>(Zcap);
+  D.xfull = ar.take<double>(Ncap);
+  D.tmp = ar.take<double>(Scap);
+  D.tmpz = ar.take<double>(Zcap);
+  D.K = ar.take<double>(Ecap);
+  D.qA = ar.take<double>(lmax(Ncap, Ecap));
+  D.qQ = ar.take<double>(Ncap);
+  D.qR = ar.take<double>((size_t)pc * pc);
+  D.tau = ar.take<double>(pc + zcm);
+  D.qT = ar.take<double>(32 * 32 * ((pc + zcm) / 32 + 2));
+  D.qA2 = ar.take<double>(Zcap);
+  D.tau2 = ar.take<double>(zcm + 1);
+  D.qT2 = ar.take<double>(32 * 32 * (zcm / 32 + 2));
+  D.qRe = ar.take<double>((size_t)(pc + zcm) * (pc + zcm));
+  D.U = ar.take<double>((size_t)pc * pc);
+  D.Vs = ar.take<double>((size_t)pc * pc);
+  D.S = ar.take<double>(pc);
+  D.J = ar.take<double>((size_t)2 * pc * pc);
+  D.Ue = ar.take<double>(Ecap);
+  D.Ct = ar.take<double>(Ncap);
+  D.gd = ar.take<GemmDesc>(NG);
+  D.qd = ar.take<QRDesc>(2);
+  D.sd = ar.take<SVDDesc>(1);
+  D.cd = ar.take<CopyDesc>(8);
+  D.iv = ar.take<int>(16);
+  D.dv = ar.take<double>(8);
+  D.limit = ar.take<int>(TT_MAX_D + 1);
+  Arena c1, c2;
+  orth_meta(y, -1, nullptr, c1, nullptr);
+  orth_meta(z, -1, nullptr, c2, nullptr);
+  P.orth_cap = c1.used > c2.used ? c1.used : c2.used;
+  P.orth_base = ar.take<char>(P.orth_cap);
+  P.split = ar.take<double>(GEMM_SPLIT_SCRATCH / 8);
+  P.bar = ar.take<unsigned int>(4);
+  return TT_OK;
+}
+
+size_t amen_mv_ws_bytes(const MatMeta &A, const VecMeta &b, const VecMeta &y, const VecMeta &z) {
+  Arena ar;
+  MvCtx P;
+  if (carve_mv(A, b, y, z, ar, P) != TT_OK) return 0;
+  return ar.used;
+}
+
+tt_status amen_mv_meta(const MatMeta &A, const VecMeta &b, const VecMeta &y, const VecMeta &z, double eps,
+                       int max_sweeps, int rmax, int *sweeps_dev, Arena &ar, cudaStream_t s) {
+  MvCtx P;
+  TT_TRY(carve_mv(A, b, y, z, ar, P));
+  if (!ar.base) return TT_OK;
+  if (!ar.ok()) return fail(TT_ERR_CAPACITY, "amen_mv: workspace too small");
+  if (!(eps > 0.0) || max_sweeps < 1 || rmax < 1) return fail(TT_ERR_ARG, "amen_mv: eps > 0, max_sweeps, rmax >= 1");
+  Dev &D = P.D;
+  const int d = A.d;
+  {
+    static thread_local std::vector<int> lim;
+    lim.assign(TT_MAX_D + 1, 1);
+    for (int k = 0; k <= d; ++k) {
+      int l = y.rcap[k] - z.rcap[k];
+      if (l > rmax) l = rmax;
+      lim[k] = l < 1 ? 1 : l;
+    }
+    cudaMemcpyAsync(D.limit, lim.data(), sizeof(int) * (d + 1), cudaMemcpyHostToDevice, s);
+    cudaStreamSynchronize(s);
+  }
+  set_dv_kernel<<<1, 1, 0, s>>>(D.dv, 1, eps);
+  set_gemm_scratch(P.split, GEMM_SPLIT_SCRATCH);
+  set_jacobi_sync(P.bar);
+  Arena oa;
+  oa.base = P.orth_base;
+  oa.cap = P.orth_cap;
+  TT_TRY(orth_meta(y, -1, nullptr, oa, s));
+  oa.used = 0;
+  TT_TRY(orth_meta(z, -1, nullptr, oa, s));
+  init_ifaces_mv<<<1, 1, 0, s>>>(D);
+  const int *yc = y.rcap, *zc = z.rcap, *bc = b.rcap, *Rc = A.Rcap;
+  struct Caps12 { GemmDesc g[12]; };
+  auto launch_caps = [&](const GemmDesc *dev, const Caps12 &hc, int from, int cnt) -> tt_status {
+    for (int i = 0; i < cnt; ++i)
+      TT_TRY(launch_gemm_k(dev + i, 1, hc.g[from + i].M, hc.g[from + i].N, hc.g[from + i].K, s));
+    return TT_OK;
+  };
+  auto iface = [&](int k, int dir) -> tt_status {
+    plan_iface_mv<<<1, 1, 0, s>>>(D, k, dir);
+    Caps12 c;
+    const int n = y.n[k], nb = b.n[k];
+    if (dir < 0) {
+      descs_iface_right(yc[k], Rc[k], bc[k], n, nb, yc[k + 1], Rc[k + 1], bc[k + 1], 0, 0, 0, 0, 0, 0, 0, c.g + 0);
+      descs_iface_right(zc[k], Rc[k], bc[k], n, nb, zc[k + 1], Rc[k + 1], bc[k + 1], 0, 0, 0, 0, 0, 0, 0, c.g + 3);
+      descs_iface_right_vec(zc[k], yc[k], n, zc[k + 1], yc[k + 1], 0, 0, 0, 0, 0, c.g + 6);
+    } else {
+      descs_iface_left(yc[k], Rc[k], bc[k], n, nb, yc[k + 1], Rc[k + 1], bc[k + 1], 0, 0, 0, 0, 0, 0, 0, c.g + 0);
+      descs_iface_left(zc[k], Rc[k], bc[k], n, nb, zc[k + 1], Rc[k + 1], bc[k + 1], 0, 0, 0, 0, 0, 0, 0, c.g + 3);
+      descs_iface_left_vec(zc[k], yc[k], n, zc[k + 1], yc[k + 1], 0, 0, 0, 0, 0, c.g + 6);
+    }
+    return launch_caps(D.gd, c, 0, 8);
+  };
+  for (int k = d - 1; k >= 1; --k) TT_TRY(iface(k, -1));
+  int dir = +1, sweep = 0;
+  for (sweep = 0; sweep < max_sweeps; ++sweep) {
+    set_dv_kernel<<<1, 1, 0, s>>>(D.dv, 2, 0.0);
+    for (int t = 0; t < d; ++t) {
+      const int k = dir > 0 ? t : d - 1 - t;
+      const int last = (t == d - 1);
+      const int n = y.n[k], nb = b.n[k];
+      Caps12 lc;
+      descs_local_apply(yc[k], Rc[k], bc[k], n, nb, yc[k + 1], Rc[k + 1], bc[k + 1], 0, 0, 0, 0, 0, 0, 0, lc.g + 0);
+      plan_local_mv<<<1, 1, 0, s>>>(D, k);
+      TT_TRY(launch_copy(D.cd + 2, 1, P.Ncap, s));
+      TT_TRY(launch_caps(D.gd, lc, 0, 3));
+      track_dx_kernel<<<1, 256, 0, s>>>(D.iv, D.sol, D.xold, D.dv);
+      if (last) {
+        TT_TRY(launch_copy(D.cd + 1, 1, P.Ncap, s));
+        continue;
+      }
+      plan_svd<<<1, 1, 0, s>>>(D, k, dir);
+      TT_TRY(launch_qr(D.qd, 1, s));
+      const int pcap = dir > 0 ? (yc[k] * n < yc[k + 1] ? yc[k] * n : yc[k + 1])
+                               : (n * yc[k + 1] < yc[k] ? n * yc[k + 1] : yc[k]);
+      TT_TRY(launch_jacobi(D.sd, 1, pcap, pcap, s));
+      trunc_kernel<<<1, 256, 0, s>>>(D, k, dir);
+      TT_TRY(launch_copy(D.cd, 1, P.Ncap, s));
+      const int big = n * (yc[k] > yc[k + 1] ? yc[k] : yc[k + 1]);
+      TT_TRY(launch_gemm(D.gd, 1, big, P.pc, s));
+      TT_TRY(launch_gemm(D.gd + 1, 1, big, big, s));
+      plan_enrich_mv<<<1, 1, 0, s>>>(D, k, dir);
+      {
+        Caps12 ec;
+        descs_local_apply(zc[k], Rc[k], bc[k], n, nb, zc[k + 1], Rc[k + 1], bc[k + 1], 0, 0, 0, 0, 0, 0, 0, ec.g + 0);
+        descs_local_rhs(zc[k], yc[k], n, zc[k + 1], yc[k + 1], 0, 0, 0, 0, 0, ec.g + 3);
+        if (dir > 0) {
+          descs_local_apply(yc[k], Rc[k], bc[k], n, nb, zc[k + 1], Rc[k + 1], bc[k + 1], 0, 0, 0, 0, 0, 0, 0, ec.g + 5);
+          ec.g[8] = gd_make(yc[k] * n, zc[k + 1], yc[k + 1], nullptr, 1, 0, nullptr, 1, 1);
+        } else {
+          descs_local_apply(zc[k], Rc[k], bc[k], n, nb, yc[k + 1], Rc[k + 1], bc[k + 1], 0, 0, 0, 0, 0, 0, 0, ec.g + 5);
+          ec.g[8] = gd_make(zc[k], n * yc[k + 1], yc[k], nullptr, 1, 0, nullptr, 1, 0);
+        }
+        TT_TRY(launch_caps(D.gd, ec, 0, 9));
+      }
+      TT_TRY(launch_qr(D.qd, 2, s));
+      TT_TRY(launch_gemm(D.gd + 10, 1, P.pc, big, s));
+      {
+        const int nb_ = dir > 0 ? y.n[k + 1] * yc[k + 2 <= d ? k + 2 : d] : P.pc;
+        const int mb_ = dir > 0 ? P.pc : y.n[k - 1] * yc[k - 1];
+        TT_TRY(launch_gemm(D.gd + 11, 1, mb_, nb_, s));
+      }
+      TT_TRY(launch_copy(D.cd, 3, P.Scap, s));
+      TT_TRY(iface(k, dir));
+    }
+    double hv[3] = {0.0, 0.0, 0.0};
+    cudaMemcpyAsync(hv, D.dv, 3 * sizeof(double), cudaMemcpyDeviceToHost, s);
+    cudaStreamSynchronize(s);
+    TT_TRY(check_launch("amen_mv sweep"));
+    if (hv[2] <= eps) { ++sweep; break; }
+    dir = -dir;
+  }
+  if (sweeps_dev) {
+    cudaMemcpyAsync(sweeps_dev, &sweep, sizeof(int), cudaMemcpyHostToDevice, s);
+    cudaStreamSynchronize(s);
+  }
+  return check_launch("amen_mv");
 }
 
 }  // namespace tt

@@ -10,4 +10,7 @@ struct AmenOpts {
 size_t amen_ws_bytes(const MatMeta &A, const VecMeta &b, const VecMeta &x, const VecMeta &z, int restart);
 tt_status amen_solve_meta(const MatMeta &A, const VecMeta &b, const VecMeta &x, const VecMeta &z, const AmenOpts &o,
                           int *sweeps_dev, double *res_dev, int *status_dev, Arena &ar, cudaStream_t s);
+size_t amen_mv_ws_bytes(const MatMeta &A, const VecMeta &b, const VecMeta &y, const VecMeta &z);
+tt_status amen_mv_meta(const MatMeta &A, const VecMeta &b, const VecMeta &y, const VecMeta &z, double eps,
+                       int max_sweeps, int rmax, int *sweeps_dev, Arena &ar, cudaStream_t s);
 }  // namespace tt

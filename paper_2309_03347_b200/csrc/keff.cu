@@ -274,6 +274,28 @@ extern "C" tt_status amen_solve(const tt_mat *A, const tt_vec *b, tt_vec *x, tt_
   return amen_solve_meta(Am, bm, xm, zm, ao, sweeps_dev, res_dev, nullptr, ar, (cudaStream_t)s);
 }
 
+extern "C" size_t amen_mv_workspace(const tt_mat *A, const tt_vec *b, const tt_vec *y, const tt_vec *z) {
+  MatMeta Am;
+  VecMeta bm, ym, zm;
+  if (make_mat_meta(A, Am) || make_vec_meta(b, bm) || make_vec_meta(y, ym) || make_vec_meta(z, zm)) return 0;
+  return amen_mv_ws_bytes(Am, bm, ym, zm);
+}
+
+extern "C" tt_status amen_mv(const tt_mat *A, const tt_vec *b, tt_vec *y, tt_vec *z, double eps, int32_t max_sweeps,
+                             int32_t rmax, int32_t *sweeps_dev, void *ws, size_t wsb, tt_stream s) {
+  MatMeta Am;
+  VecMeta bm, ym, zm;
+  TT_TRY(make_mat_meta(A, Am));
+  TT_TRY(make_vec_meta(b, bm));
+  TT_TRY(make_vec_meta(y, ym));
+  TT_TRY(make_vec_meta(z, zm));
+  if (!ws) return fail(TT_ERR_ARG, "amen_mv: NULL workspace");
+  Arena ar;
+  ar.base = (char *)ws;
+  ar.cap = wsb;
+  return amen_mv_meta(Am, bm, ym, zm, eps, max_sweeps, rmax, sweeps_dev, ar, (cudaStream_t)s);
+}
+
 extern "C" size_t keff_workspace(const tt_mat *H, const tt_mat *S, const tt_mat *F, const tt_vec *psi,
                                  const tt_vec *z, const keff_opts *o) {
   MatMeta Hm, Sm, Fm;

@@ -279,6 +279,20 @@ def amen_solve(A: TTMat, b: TTVec, x: TTVec, z: TTVec, eps: float, rmax: int = 1
     return x, sweeps, res
 
 
+def amen_mv(A: TTMat, b: TTVec, y: TTVec, z: TTVec, eps: float, rmax: int = 1 << 20, max_sweeps: int = 20,
+            stream=None):
+    """y <- A b by the fit-based sweeps (NEXT-1; y: initial guess in, product out; z: residual TT)."""
+    nb = lib().amen_mv_workspace(A.c, b.c, y.c, z.c)
+    if nb == 0:
+        check(lib().amen_mv(A.c, b.c, y.c, z.c, float(eps), int(max_sweeps), int(min(rmax, 2**30)), None, None, 0,
+                            C.c_void_p(_stream(stream))))
+    ws = workspace(nb, y.device)
+    sweeps = torch.zeros(1, dtype=torch.int32, device=y.device)
+    check(lib().amen_mv(A.c, b.c, y.c, z.c, float(eps), int(max_sweeps), int(min(rmax, 2**30)), _ptr(sweeps),
+                        _ptr(ws), ws.numel(), C.c_void_p(_stream(stream))))
+    return y, sweeps
+
+
 # ------------------------------------------------------------------ a9 ---
 
 class KeffResult:

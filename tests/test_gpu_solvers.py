@@ -142,3 +142,59 @@ def test_keff_c1_reflective():
     assert abs(res.k.item() - 1.2) <= 1e-8
     for tau, kt in enumerate(hist[:10], start=1):
         assert abs(kt - (1.2 - 0.2 * 0.5 ** tau)) <= 1e-8
+
+
+def _mv_gpu(A, b, y0, z0, rcap, eps, max_sweeps=40):
+    d = len(b)
+    y = tb.TTVec.from_cores(y0, rcap=[1] + [rcap] * (d - 1) + [1])
+    z = tb.TTVec.from_cores(z0)
+    _, sweeps = tb.amen_mv(tb.TTMat.from_cores(A), tb.TTVec.from_cores(b), y, z, eps=eps, max_sweeps=max_sweeps)
+    torch.cuda.synchronize()
+    return ott.tt_full(y.cores()), sweeps.item()
+
+
+def test_amen_mv_gpu():
+    """NEXT-1: device amen_mv vs the exact product (oracle exact
+    matvec + full contraction) and vs the oracle amen_mv, on the oracle's pins."""
+    g = inputs.rng(81)
+    modes = [2, 3, 4, 2]
+    b = inputs.random_tt(g, modes, [1, 2, 3, 2, 1])
+    y0 = inputs.random_tt(g, modes, [1, 1, 1, 1, 1])
+    z0 = inputs.random_tt(g, modes, [1, 2, 2, 2, 1])
+    I = ott.rank1_ttm([np.eye(n) for n in modes])
+    got, _ = _mv_gpu(I, b, y0, z0, 16, 1e-12)
+    ref = ott.tt_full(b)
+    assert np.linalg.norm(got - ref) <= 1e-12 * np.linalg.norm(ref)
+    Fs = [g.standard_normal((n, n)) for n in modes]
+    vs = [g.standard_normal(n).reshape(1, n, 1) for n in modes]
+    got, _ = _mv_gpu(ott.rank1_ttm(Fs), vs, y0, z0, 16, 1e-12)
+    ref = ott.tt_full(ott.tt_matvec(ott.rank1_ttm(Fs), vs))
+    assert np.linalg.norm(got - ref) <= 1e-12 * np.linalg.norm(ref)
+    # rectangular operator: modes (3, 2, 4) <- (2, 5, 3)
+    Ar = inputs.random_ttm(g, [3, 2, 4], [2, 5, 3], [1, 2, 3, 1])
+    br = inputs.random_tt(g, [2, 5, 3], [1, 2, 2, 1])
+    got, _ = _mv_gpu(Ar, br, inputs.random_tt(g, [3, 2, 4], [1, 1, 1, 1]),
+                     inputs.random_tt(g, [3, 2, 4], [1, 2, 2, 1]), 12, 1e-12)
+    ref = ott.tt_full(ott.tt_matvec(Ar, br))
+    assert np.linalg.norm(got - ref) <= 1e-12 * np.linalg.norm(ref)
+    # C2 slice d = 10 vs the dense product
+    inst = inputs.c2_slice(110)
+    d = 10
+    y0 = inputs.random_tt(g, [2] * d, [1] + [2] * (d - 1) + [1])
+    z0 = inputs.random_tt(g, [2] * d, [1] + [4] * (d - 1) + [1])
+    got, sw = _mv_gpu(inst["A"], inst["X"], y0, z0, 40, 1e-10)
+    ref = ott.ttm_full(inst["A"]) @ ott.tt_full(inst["X"])
+    assert np.linalg.norm(got - ref) <= 1e-12 * np.linalg.norm(ref), sw
+    # truncated QTT slab transport apply vs exact (and vs the oracle amen_mv)
+    p = inputs.problem_slab(4, nv=256)
+    H = T.tt_operators(p, eps=1e-12)["H"]
+    modes = T.qtt_modes(p)
+    d = len(modes)
+    x = inputs.random_tt(g, modes, [1] + [2] * (d - 1) + [1])
+    y0 = inputs.random_tt(g, modes, [1] + [2] * (d - 1) + [1])
+    z0 = inputs.random_tt(g, modes, [1] + [3] * (d - 1) + [1])
+    got, sw = _mv_gpu(H, x, y0, z0, 40, 1e-8)
+    ref = ott.tt_full(ott.tt_matvec_fast(H, x))
+    assert np.linalg.norm(got - ref) <= 1e-7 * np.linalg.norm(ref), sw
+    yo, _ = so.amen_mv(H, x, y0, z0, eps=1e-8, max_sweeps=40)
+    assert np.linalg.norm(got - ott.tt_full(yo)) <= 2e-7 * np.linalg.norm(ref)
