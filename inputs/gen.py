@@ -132,6 +132,14 @@ def quadrature_ls_style(N: int):
 # background material: cell (cx, cy, cz) takes the material of the LAST box
 # [lo, hi)^3 (cell indices) that contains it, else material 0 (Z13, Z34).
 # --------------------------------------------------------------------------
+def inv_velocity(G: int):
+    """1/v per group for the alpha problem (eq. Discretized_alphaNTE, P:341-349;
+    reading Z39: the paper's velocities come with its unavailable library).
+    One group: v = 1 (alpha in units of v cm^-1).  Multigroup: 1/v rising
+    geometrically from 1 (fastest group) to 100 (slowest); no random draws."""
+    return np.ones(1) if G == 1 else np.geomspace(1.0, 100.0, G)
+
+
 def problem_c1(boundary: str = "vacuum"):
     """BASELINE.json configs[0]: unit cube, 8 vertices/axis (7 cells, Z12),
     G=1, S2, Sigma_t=1, Sigma_s=0.5, nu Sigma_f=0.6, chi=1."""
@@ -140,7 +148,7 @@ def problem_c1(boundary: str = "vacuum"):
         "quad": quadrature_s2(), "boundary": boundary, "qtt": False,
         "materials": [{"sigma_t": np.array([1.0]), "sigma_s": np.array([[0.5]]),
                        "nu_sigma_f": np.array([0.6])}],
-        "chi": np.array([1.0]), "boxes": [],
+        "chi": np.array([1.0]), "boxes": [], "inv_v": inv_velocity(1),
     }
 
 
@@ -174,7 +182,7 @@ def problem_c3(seed: int = 3):
     return {
         "name": "C3", "nv": 64, "extent": 10.0, "G": G, "quad": quadrature_ls_style(8),
         "boundary": "vacuum", "qtt": True, "materials": [refl, fuel], "chi": chi,
-        "boxes": [((16, 16, 16), (48, 48, 48), 1)], "seed": seed,
+        "boxes": [((16, 16, 16), (48, 48, 48), 1)], "seed": seed, "inv_v": inv_velocity(G),
     }
 
 
@@ -191,7 +199,7 @@ def problem_c4(seed: int = 4):
         "name": "C4", "nv": 256, "extent": 10.0, "G": G, "quad": quadrature_ls_style(16),
         "boundary": "vacuum", "qtt": True, "materials": [refl, blanket, core], "chi": chi,
         "boxes": [((32, 32, 32), (224, 224, 224), 1), ((64, 64, 64), (192, 192, 192), 2)],
-        "seed": seed,
+        "seed": seed, "inv_v": inv_velocity(G),
     }
 
 
@@ -215,7 +223,7 @@ def problem_slab(L: int = 8, nv: int = 1024, qtt: bool = True):
         "quad": quadrature_gl_1d(L), "boundary": "vacuum", "qtt": qtt,
         "materials": [{"sigma_t": np.array([0.3264]), "sigma_s": np.array([[0.225216]]),
                        "nu_sigma_f": np.array([3.24 * 0.0816])}],
-        "chi": np.array([1.0]), "boxes": [],
+        "chi": np.array([1.0]), "boxes": [], "inv_v": inv_velocity(1),
     }
 
 
@@ -230,5 +238,5 @@ def problem_small_hetero(seed: int = 7, nv: int = 8, G: int = 2, N: int = 2, qtt
     return {
         "name": f"hetero-{nv}", "nv": nv, "extent": 1.0, "G": G, "quad": quadrature_ls_style(N),
         "boundary": "vacuum", "qtt": qtt, "materials": [m0, m1], "chi": chi,
-        "boxes": [((lo, lo, lo), (hi - 1, hi, hi), 1)], "seed": seed,
+        "boxes": [((lo, lo, lo), (hi - 1, hi, hi), 1)], "seed": seed, "inv_v": inv_velocity(G),
     }

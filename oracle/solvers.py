@@ -5,6 +5,8 @@
   gmres              plain restarted GMRES (Saad), modified Gram-Schmidt + Givens
   amen_solve         ALS/AMEn for H x = b in TT (reading Z20)
   keff_tt            eq. TT_k_eff_fixed_points with readings Z16-Z19
+  alpha_secant       eq. alpha_eig_fixed_points / TT_alpha_eig_fixed_points
+                      with the secant reading Z32, around any k-eff solver
 """
 from __future__ import annotations
 
@@ -394,3 +396,54 @@ def keff_tt(H, S, F, psi0, z0, k0=1.0, tol_k=1e-10, max_outer=200, eps_round=1e-
             break
         k = knew
     return k, psi, hist
+
+
+# ------------------------------------------------------------ alpha ---
+
+
+def alpha_secant(keff_of_alpha, alpha0=0.0, alpha1=0.01, tol=1e-10, max_it=50):
+    """Alpha-eigenvalue outer loop.  keff_of_alpha(alpha)
+    solves the k-eff problem [alpha V^{-1} + H] Psi = [S + F/k] Psi and returns k.
+    alpha^(0) = 0, alpha^(1) = 0.01; then the secant step on
+    f(alpha) = k_eff(alpha) - 1 (reading Z32; the printed update at P:1434 and
+    P:1444 is dimensionally inconsistent):
+        alpha^(t+1) = alpha^(t) + (1 - k^(t)) (alpha^(t) - alpha^(t-1)) / (k^(t) - k^(t-1)).
+    Stops when |k^(t) - 1| <= tol.  Returns (alpha, k, history [(alpha, k)])."""
+    a_prev, a = alpha0, alpha1
+    k_prev = keff_of_alpha(a_prev)
+    hist = [(a_prev, k_prev)]
+    if abs(k_prev - 1.0) <= tol:
+        return a_prev, k_prev, hist
+    k = keff_of_alpha(a)
+    hist.append((a, k))
+    for _ in range(max_it):
+        if abs(k - 1.0) <= tol:
+            return a, k, hist
+        if abs(k - k_prev) < 1e-14:
+            raise RuntimeError("alpha secant stagnated: |k(t) - k(t-1)| < 1e-14")
+        a_next = a + (1.0 - k) * (a - a_prev) / (k - k_prev)
+        a_prev, k_prev = a, k
+        a = a_next
+        k = keff_of_alpha(a)
+        hist.append((a, k))
+    raise RuntimeError("alpha secant did not converge")
+
+
+def alpha_dense(H, V, S, F, tol=1e-10, tol_k=1e-13, minnorm=False):
+    """alpha_secant with dense k-eff solves (LU / minimum norm) of H + alpha V^{-1}."""
+    def keff(a):
+        k, _, _ = keff_dense_power(H + a * V, S, F, tol=tol_k, minnorm=minnorm)
+        return k
+    return alpha_secant(keff, tol=tol)
+
+
+def alpha_tt(H, V, S, F, psi0, z0, tol=1e-9, eps_op=1e-13, **keff_kw):
+    """alpha_secant with TT k-eff solves (keff_tt) of round(H + alpha V^{-1})
+    (TT_alpha_eig_fixed_points); each k-eff solve starts from psi0."""
+    def keff(a):
+        Ha = ott.tt_as_ttm(ott.tt_round(ott.tt_add(ott.ttm_as_tt(H), ott.tt_scale(ott.ttm_as_tt(V), a)),
+                                        eps_op)[0],
+                           [c.shape[1] for c in H], [c.shape[2] for c in H])
+        k, _, _ = keff_tt(Ha, S, F, psi0, z0, **keff_kw)
+        return k
+    return alpha_secant(keff, tol=tol)

@@ -146,7 +146,8 @@ def operator_terms(prob):
     w = quad["w"]
     I_G = np.eye(G)
     terms = box_terms(prob)
-    H, S, F = [], [], []
+    H, S, F, V = [], [], [], []
+    inv_v = prob.get("inv_v")
     for b in range(8):
         sx, sy, sz = (1 if b & 1 else -1, 1 if b & 2 else -1, 1 if b & 4 else -1)
         Cb = C_b(quad, b)
@@ -165,6 +166,9 @@ def operator_terms(prob):
         H.append([Ix, Iy, Iz, Cb, np.diag(m0["sigma_t"])])
         S.append([Nx, Ny, Nz, Intg, m0["sigma_s"]])
         F.append([Nx, Ny, Nz, Intg, np.outer(chi, m0["nu_sigma_f"])])
+        if inv_v is not None:
+            # (V^{-1})^{TT,b} = diag(1/v) o (C_b (x) I) o Ip_z o Ip_y o Ip_x
+            V.append([Ix, Iy, Iz, Cb, np.diag(inv_v)])
         for (lo, hi, m, parent) in terms:
             Ex = _axis_indicator(sx, n, lo[0], hi[0])
             Ey = _axis_indicator(sy, n, lo[1], hi[1])
@@ -177,7 +181,10 @@ def operator_terms(prob):
                 S.append([Ex @ Nx, Ey @ Ny, Ez @ Nz, Intg, dss])
             if np.any(dnf != 0):
                 F.append([Ex @ Nx, Ey @ Ny, Ez @ Nz, Intg, np.outer(chi, dnf)])
-    return {"H": H, "S": S, "F": F}
+    out = {"H": H, "S": S, "F": F}
+    if inv_v is not None:
+        out["V"] = V
+    return out
 
 
 def operator_terms_1d(prob):
@@ -192,7 +199,8 @@ def operator_terms_1d(prob):
     G = prob["G"]
     m0 = prob["materials"][0]
     chi = prob["chi"]
-    H, S, F = [], [], []
+    H, S, F, V = [], [], [], []
+    inv_v = prob.get("inv_v")
     for b, sx in ((0, -1), (1, 1)):
         Cb = np.diag(((mu > 0) == (sx > 0)).astype(float))
         H.append([D_s(sx, n, h), Cb @ np.diag(mu), np.eye(G)])
@@ -200,7 +208,12 @@ def operator_terms_1d(prob):
         Intg = Cb @ np.outer(np.ones(L), w)
         S.append([IpN_s(sx, n), Intg, m0["sigma_s"]])
         F.append([IpN_s(sx, n), Intg, np.outer(chi, m0["nu_sigma_f"])])
-    return {"H": H, "S": S, "F": F}
+        if inv_v is not None:
+            V.append([Ip_s(sx, n), Cb, np.diag(inv_v)])          # P:1233-1237 in 1-D
+    out = {"H": H, "S": S, "F": F}
+    if inv_v is not None:
+        out["V"] = V
+    return out
 
 
 def kron_term(term):
@@ -240,16 +253,20 @@ def slab_eq_apply(prob, psi):
     return Hv, Sv, Fv, mask
 
 
-def slab_keff_sweep(prob, tol=1e-12, max_it=100000):
+def slab_keff_sweep(prob, tol=1e-12, max_it=100000, alpha=0.0):
     """Matrix-free Eq. 8 for the 1-D slab: H^{-1} is a transport sweep
     (per ordinate, forward substitution from the inflow face); S and F act
-    through the scalar flux phi = sum_l w_l psi_l.  Returns (k, psi, iterations)."""
+    through the scalar flux phi = sum_l w_l psi_l.  alpha != 0 solves the k problem
+    of [alpha V^{-1} + H]: in the slab V^{-1} = Ip o C_b o diag(1/v)
+    has the collision term's structure, so it enters as
+    sigma_t + alpha / v.  Returns (k, psi, iterations)."""
     n = prob["nv"]
     h = prob["extent"] / (n - 1)
     mu, w = prob["quad"]["mu"], prob["quad"]["w"]
     L = len(w)
     m0 = prob["materials"][0]
     st, ss, nf = m0["sigma_t"][0], m0["sigma_s"][0, 0], m0["nu_sigma_f"][0]
+    st = st + alpha * prob.get("inv_v", np.ones(1))[0]
 
     def rhs(psi, k):
         phi = w @ psi
@@ -294,7 +311,7 @@ def dense_operators(prob):
     """Dense H, S, F as sums of Kronecker products."""
     T = operator_terms(prob)
     out = {}
-    for key in ("H", "S", "F"):
+    for key in T:
         out[key] = sum(kron_term(t) for t in T[key])
     if prob.get("boundary", "vacuum") == "reflective":
         out = _reflective(prob, out)
@@ -304,11 +321,12 @@ def dense_operators(prob):
 # ----------------------------------------------------- Eq.-4 index loop ---
 
 
-def eq4_apply(prob, psi, k_eff=1.0):
+def eq4_apply(prob, psi, k_eff=1.0, with_v=False):
     """Evaluate the row equations of eq. Discretized_kNTE with explicit
     index loops, generalised per octant (Z7): the cell of row (i,j,k) in an octant
     with signs s is (i - [s_x>0], j - [s_y>0], k - [s_z>0]).  Returns
-    (Hpsi, Spsi, Fpsi, interior_mask) for the interior (cell-equation) rows; the
+    (Hpsi, Spsi, Fpsi, interior_mask) for the interior (cell-equation) rows (with_v:
+    also V^{-1} psi from the alpha term of eq. Discretized_alphaNTE); the
     values at inflow-face rows are left as NaN.  psi is the dense vector
     (linearised x fastest, then y, z, angle, group)."""
     n = prob["nv"]
@@ -322,6 +340,8 @@ def eq4_apply(prob, psi, k_eff=1.0):
     P = psi.reshape(G, L, n, n, n)                 # [g, l, z, y, x]
     N = G * L * n ** 3
     Hv = np.full(N, np.nan); Sv = np.full(N, np.nan); Fv = np.full(N, np.nan)
+    Vv = np.full(N, np.nan)
+    inv_v = prob.get("inv_v", np.ones(G))
     mask = np.zeros(N, dtype=bool)
     # angular integral sum_l' w_l' psi_{g', l'} per vertex (used by both S and F)
     phi = np.einsum("l,glzyx->gzyx", quad["w"], P)
@@ -349,6 +369,7 @@ def eq4_apply(prob, psi, k_eff=1.0):
                         s8 = sum(P[g, l, kk, jj, ii] for kk in (k0, k1)
                                  for jj in (j0, j1) for ii in (i0, i1))
                         Hv[row] = mu / (4 * h) * sx + eta / (4 * h) * sy + xi / (4 * h) * sz + st / 8 * s8
+                        Vv[row] = inv_v[g] / 8 * s8        # alpha term of eq. Discretized_alphaNTE
                         scat = 0.0
                         fis = 0.0
                         for gp in range(G):
@@ -359,6 +380,8 @@ def eq4_apply(prob, psi, k_eff=1.0):
                         Sv[row] = scat
                         Fv[row] = fis
                         mask[row] = True
+    if with_v:
+        return Hv, Sv, Fv, Vv, mask
     return Hv, Sv, Fv, mask
 
 
@@ -374,6 +397,7 @@ def _reflective(prob, ops):
     G = prob["G"]
     L = len(quad["w"])
     H = ops["H"].copy(); S = ops["S"].copy(); F = ops["F"].copy()
+    V = ops["V"].copy() if "V" in ops else None
     cos = np.stack([quad["mu"], quad["eta"], quad["xi"]], axis=1)
     for g in range(G):
         for l in range(L):
@@ -394,9 +418,14 @@ def _reflective(prob, ops):
                         row = i + n * (j + n * (k + n * (l + L * g)))
                         col = i + n * (j + n * (k + n * (lr + L * g)))
                         H[row, :] = 0.0; S[row, :] = 0.0; F[row, :] = 0.0
+                        if V is not None:
+                            V[row, :] = 0.0
                         H[row, row] = 1.0
                         H[row, col] -= 1.0
-    return {"H": H, "S": S, "F": F}
+    out = {"H": H, "S": S, "F": F}
+    if V is not None:
+        out["V"] = V
+    return out
 
 
 # ------------------------------------------------------ TT / QTT forms ---
@@ -455,7 +484,7 @@ def tt_operators(prob, eps=1e-13, qtt=None):
         qtt = prob.get("qtt", False)
     T = operator_terms(prob)
     make = term_qtt if qtt else term_tt
-    return {key: ttm_sum_round([make(t) for t in T[key]], eps) for key in ("H", "S", "F")}
+    return {key: ttm_sum_round([make(t) for t in T[key]], eps) for key in T}
 
 
 def ones_tt(mode_sizes):
