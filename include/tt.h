@@ -260,6 +260,46 @@ tt_status keff_fixed_point(const tt_mat *H, const tt_mat *S, const tt_mat *F, tt
                            tt_vec *z, double k0, const keff_opts *o, keff_report *rep, void *ws,
                            size_t wsb, tt_stream s);
 
+/* ------------------------------------------------------------ NEXT-2 ---
+ * alpha_secant: the alpha eigenvalue of [alpha V^{-1} + H] Psi = [S + F] Psi
+ * (eq. OpFormAlphaNTE; TT scheme P:1416-1462).  alpha^(0) = alpha0,
+ * alpha^(1) = alpha1 (the paper: 0 and 0.01); for each alpha the
+ * k-eff problem [alpha V^{-1} + H] Psi = [S + F/k] Psi is solved by the
+ * keff_fixed_point machinery on H_alpha = round(H + alpha V^{-1}, eps_op),
+ * warm-started from the previous Psi and k; then the secant step on
+ * k(alpha) - 1 (reading Z32; the printed update is dimensionally
+ * inconsistent):  alpha+ = alpha + (1 - k)(alpha - alpha_prev)/(k - k_prev).
+ * Stops when |k(alpha) - 1| <= tol.  alpha, k and the secant state stay on
+ * the device; the host polls one flag per k-eff solve.
+ * V: the velocity operator V^{-1} (same modes as H; tt_velocity_terms).
+ * psi: in Psi_0, out the eigenvector at the final alpha (capacities >=
+ * keff.rmax + kickrank).  z: AMEn residual TT.  Report arrays are device
+ * memory; status: TT_OK, TT_ERR_NOCONV (max_alpha reached or the secant
+ * stagnated, |k - k_prev| < 1e-14), or the inner k-eff solve's error.
+ * Workspace: alpha_workspace(...). */
+typedef struct {
+  double alpha0, alpha1;   /* first two iterates                                   */
+  double tol;              /* |k(alpha) - 1| stopping tolerance                    */
+  double eps_op;           /* rounding tolerance of H + alpha V^{-1}               */
+  int32_t max_alpha;       /* maximum number of k-eff solves                       */
+  keff_opts keff;          /* inner k-eff solves                                   */
+} alpha_opts;
+typedef struct {
+  double *alpha_dev;       /* [1] final alpha                                      */
+  double *k_dev;           /* [1] k(alpha) of the last solve                       */
+  int32_t *iters_dev;      /* [1] k-eff solves performed                           */
+  double *alpha_hist_dev;  /* [hist_cap] alpha of each k-eff solve                 */
+  double *k_hist_dev;      /* [hist_cap] its k                                     */
+  int32_t *keff_iters_hist_dev; /* [hist_cap] its outer iterations                 */
+  int32_t hist_cap;
+  int32_t *status_dev;     /* [1]                                                  */
+} alpha_report;
+size_t alpha_workspace(const tt_mat *H, const tt_mat *V, const tt_mat *S, const tt_mat *F,
+                       const tt_vec *psi, const tt_vec *z, const alpha_opts *o);
+tt_status alpha_secant(const tt_mat *H, const tt_mat *V, const tt_mat *S, const tt_mat *F, tt_vec *psi,
+                       tt_vec *z, const alpha_opts *o, alpha_report *rep, void *ws, size_t wsb,
+                       tt_stream s);
+
 /* ------------------------------------------------ operator assembly ---
  * Host-side construction of the factor matrices of the rank-1 per-octant
  * terms of H, S, F (readings Z3-Z7, Z34), written as plain
@@ -301,6 +341,18 @@ int32_t tt_transport_terms_1d(int32_t op, int32_t nv, double extent, int32_t G, 
  * delta = eps ||G||_F / sqrt(l-1).  Cores [r_t, 2, 2, r_{t+1}] are written
  * consecutively to cores_out (host, capacity cap doubles; NULL = size query),
  * ranks (l+1 ints) to ranks_out.  Returns the number of doubles, -1 on error. */
+/* Velocity operator V^{-1} of the alpha problem (the alpha term of
+ * eq. Discretized_alphaNTE): per octant b the rank-1 term
+ * diag(inv_v) o (C_b (x) I) o Ip_z o Ip_y o Ip_x (spatially uniform).
+ * dim = 3: 8 terms of 5 factors (x, y, z, angle, group) = 3 nv^2 + L^2 + G^2
+ * doubles each; reflective != 0 restricts them to each octant's interior rows
+ * (Z15).  dim = 1: 2 terms of 3 factors (x, angle, group); eta, xi may be NULL.
+ * inv_v: [G] 1/v per group (host).  out: NULL = count query.  Returns the
+ * number of terms, -1 on invalid arguments. */
+int32_t tt_velocity_terms(int32_t dim, int32_t nv, int32_t G, int32_t L, const double *mu,
+                          const double *eta, const double *xi, const double *inv_v,
+                          int32_t reflective, double *out);
+
 int64_t tt_qtt_matrix(int32_t n, const double *G, double eps, int32_t *ranks_out, double *cores_out,
                       int64_t cap);
 

@@ -48,6 +48,17 @@ class keff_report(C.Structure):
                 ("sweeps_hist_dev", C.c_void_p), ("hist_cap", C.c_int32), ("status_dev", C.c_void_p)]
 
 
+class alpha_opts(C.Structure):
+    _fields_ = [("alpha0", C.c_double), ("alpha1", C.c_double), ("tol", C.c_double), ("eps_op", C.c_double),
+                ("max_alpha", C.c_int32), ("keff", keff_opts)]
+
+
+class alpha_report(C.Structure):
+    _fields_ = [("alpha_dev", C.c_void_p), ("k_dev", C.c_void_p), ("iters_dev", C.c_void_p),
+                ("alpha_hist_dev", C.c_void_p), ("k_hist_dev", C.c_void_p), ("keff_iters_hist_dev", C.c_void_p),
+                ("hist_cap", C.c_int32), ("status_dev", C.c_void_p)]
+
+
 P = C.c_void_p
 I32 = C.c_int32
 SIG = {
@@ -87,6 +98,10 @@ SIG = {
                                             P, P]),
     "tt_qtt_matrix": (C.c_int64, [I32, P, C.c_double, P, P, C.c_int64]),
     "tt_transport_terms_1d": (I32, [I32, I32, C.c_double, I32, I32, P, P, P, P, P, P, P]),
+    "alpha_workspace": (C.c_size_t, [C.POINTER(tt_mat)] * 4 + [C.POINTER(tt_vec)] * 2 + [C.POINTER(alpha_opts)]),
+    "alpha_secant": (I32, [C.POINTER(tt_mat)] * 4 + [C.POINTER(tt_vec)] * 2
+                     + [C.POINTER(alpha_opts), C.POINTER(alpha_report), P, C.c_size_t, P]),
+    "tt_velocity_terms": (I32, [I32, I32, I32, I32, P, P, P, P, I32, P]),
 }
 
 # symbols declared in include/tt.h (checked by the CPU test-suite)

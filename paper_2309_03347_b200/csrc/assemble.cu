@@ -444,3 +444,61 @@ static int32_t transport_terms_impl(int32_t op, int32_t nv, double extent, int32
   }
   return (int32_t)terms.size();
 }
+
+// Velocity operator V^{-1} of the alpha problem (eq.
+// Discretized_alphaNTE P:341-349): per octant (bci) the rank-1 term
+//   diag(1/v) o (C_b (x) I) o Ip_z o Ip_y o Ip_x
+// (the collision term's structure with sigma_t -> 1/v, uniform in space).
+// dim 3: terms [F_x, F_y, F_z, F_angle, F_group]; reflective (Z15) restricts
+// them to the octant's interior rows (face rows carry only the reflection).
+// dim 1: terms [F_x, F_angle, F_group] over the two half-range blocks.
+extern "C" int32_t tt_velocity_terms(int32_t dim, int32_t nv, int32_t G, int32_t L, const double *mu,
+                                     const double *eta, const double *xi, const double *inv_v, int32_t reflective,
+                                     double *out) {
+  if ((dim != 1 && dim != 3) || nv < 2 || G < 1 || L < 1 || !mu || !inv_v ||
+      (dim == 3 && (!eta || !xi)) || (dim == 1 && reflective)) {
+    tt::set_error("tt_velocity_terms: invalid argument");
+    return -1;
+  }
+  Mat E(G);
+  for (int g = 0; g < G; ++g) E.at(g, g) = inv_v[g];
+  std::vector<const Mat *> order;
+  std::vector<Mat> keep;
+  keep.reserve(8 * 5);
+  const int nb = dim == 3 ? 8 : 2;
+  for (int b = 0; b < nb; ++b) {
+    const int sx = (b & 1) ? 1 : -1, sy = (b & 2) ? 1 : -1, sz = (b & 4) ? 1 : -1;
+    Mat Cb(L);
+    for (int l = 0; l < L; ++l) {
+      bool in = (mu[l] > 0) == (sx > 0);
+      if (dim == 3) in = in && ((eta[l] > 0) == (sy > 0)) && ((xi[l] > 0) == (sz > 0));
+      if (in) Cb.at(l, l) = 1.0;
+    }
+    if (dim == 1) {
+      keep.push_back(interp(sx, nv, false));
+      keep.push_back(Cb);
+      keep.push_back(E);
+      continue;
+    }
+    Mat Ix = interp(sx, nv, false), Iy = interp(sy, nv, false), Iz = interp(sz, nv, false);
+    if (reflective) {
+      Mat Px(nv), Py(nv), Pz(nv);
+      for (int i = 0; i < nv; ++i) {
+        Px.at(i, i) = (i != (sx > 0 ? 0 : nv - 1)) ? 1.0 : 0.0;
+        Py.at(i, i) = (i != (sy > 0 ? 0 : nv - 1)) ? 1.0 : 0.0;
+        Pz.at(i, i) = (i != (sz > 0 ? 0 : nv - 1)) ? 1.0 : 0.0;
+      }
+      Ix = mul(Px, Ix); Iy = mul(Py, Iy); Iz = mul(Pz, Iz);
+    }
+    keep.push_back(Ix); keep.push_back(Iy); keep.push_back(Iz); keep.push_back(Cb); keep.push_back(E);
+  }
+  if (out) {
+    double *p = out;
+    for (const Mat &M : keep) {
+      std::memcpy(p, M.a.data(), M.a.size() * sizeof(double));
+      p += M.a.size();
+    }
+  }
+  (void)order;
+  return nb;
+}

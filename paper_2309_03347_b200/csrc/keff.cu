@@ -42,7 +42,8 @@ __global__ void ones_kernel(const VecMeta v) {
   }
 }
 
-__global__ void keff_init_kernel(KeffScal *sc, double k0, const double *nrm) {
+__global__ void keff_init_kernel(KeffScal *sc, double k0, const double *k0_dev, const double *nrm) {
+  if (k0_dev && *k0_dev != 0.0 && *k0_dev == *k0_dev) k0 = *k0_dev;
   sc->k = k0;
   sc->kinv = 1.0 / k0;
   sc->one = 1.0;
@@ -181,7 +182,8 @@ size_t keff_ws_bytes(const MatMeta &H, const MatMeta &S, const MatMeta &F, const
 }
 
 tt_status keff_meta(const MatMeta &H, const MatMeta &S, const MatMeta &F, const VecMeta &psi, const VecMeta &z,
-                    double k0, const keff_opts &o, const keff_report &rep, Arena &ar, cudaStream_t s) {
+                    double k0, const keff_opts &o, const keff_report &rep, Arena &ar, cudaStream_t s,
+                    const double *k0_dev = nullptr) {
   KeffWS W;
   TT_TRY(carve_keff(H, S, F, psi, z, o, ar, W));
   if (!ar.base) return TT_OK;
@@ -204,7 +206,7 @@ tt_status keff_meta(const MatMeta &H, const MatMeta &S, const MatMeta &F, const 
   // Psi <- round(Psi0) / ||.||   (Z16, Z17)
   { Arena a = sub(); TT_TRY(round_meta(psi, o.eps_round, o.rmax, nullptr, nullptr, 0, a, s)); }
   { Arena a = sub(); TT_TRY(orth_meta(psi, -1, W.nrm, a, s)); }
-  keff_init_kernel<<<1, 1, 0, s>>>(W.sc, k0, W.nrm);
+  keff_init_kernel<<<1, 1, 0, s>>>(W.sc, k0, k0_dev, W.nrm);
   TT_TRY(scale_meta(psi, &W.sc->nrm_inv, 1.0, 0, s));
   { Arena a = sub(); TT_TRY(dot_meta(W.f, psi, &W.sc->s_old, a, s)); }
   AmenOpts ao;
@@ -236,6 +238,148 @@ tt_status keff_meta(const MatMeta &H, const MatMeta &S, const MatMeta &F, const 
     if (hflag) break;
   }
   return check_launch("keff_fixed_point");
+}
+
+
+// ---------------------------------------------------------------- NEXT-2 ---
+// alpha_secant: eq. TT_alpha_eig_fixed_points with the secant
+// reading Z32.  For each alpha: H_alpha = round(H + alpha V^{-1}) on the device
+// (TT-matrices viewed as TT-vectors with modes m n), then keff_fixed_point
+// warm-started from the previous Psi and k.  alpha, k and the secant state stay
+// on the device; the host polls one flag per k-eff solve.
+namespace {
+
+struct AlphaState {
+  double a_prev, a, k_prev, k, one;
+  int flag, iters, status;
+};
+
+__global__ void alpha_init_kernel(AlphaState *st, double a0) {
+  st->a_prev = 0.0; st->a = a0; st->k_prev = 0.0; st->k = 1.0; st->one = 1.0;
+  st->flag = 0; st->iters = 0; st->status = 0;
+}
+
+__global__ void alpha_update_kernel(AlphaState *st, const double *k_dev, const int *kit_dev, const int *kst_dev,
+                                    double a1, double tol, int max_alpha, double *ahist, double *khist, int *ithist,
+                                    int hist_cap, double *a_out, double *k_out, int *iters_out, int *status_out) {
+  const double k = *k_dev;
+  const int it = st->iters;
+  if (it < hist_cap) {
+    if (ahist) ahist[it] = st->a;
+    if (khist) khist[it] = k;
+    if (ithist) ithist[it] = *kit_dev;
+  }
+  st->iters = it + 1;
+  if (*kst_dev != 0 && *kst_dev != TT_ERR_NOCONV) {   // no fission / NaN inside the k-eff solve
+    st->status = *kst_dev;
+    st->flag = 1;
+  } else if (fabs(k - 1.0) <= tol) {
+    st->k = k;
+    st->flag = 1;
+  } else if (st->iters >= max_alpha) {
+    st->k = k;
+    st->status = TT_ERR_NOCONV;
+    st->flag = 1;
+  } else if (it == 0) {                                // alpha^(1) = 0.01
+    st->a_prev = st->a; st->k_prev = k; st->k = k;
+    st->a = a1;
+  } else if (fabs(k - st->k_prev) < 1e-14) {           // stagnation
+    st->k = k;
+    st->status = TT_ERR_NOCONV;
+    st->flag = 1;
+  } else {                                             // secant on k(alpha) - 1 (Z32)
+    const double an = st->a + (1.0 - k) * (st->a - st->a_prev) / (k - st->k_prev);
+    st->a_prev = st->a; st->k_prev = k; st->k = k;
+    st->a = an;
+  }
+  if (st->flag) {
+    // report the alpha the last k-eff solve used
+    if (a_out) *a_out = st->a;
+  } else if (a_out) {
+    *a_out = st->a;
+  }
+  if (k_out) *k_out = k;
+  if (iters_out) *iters_out = st->iters;
+  if (status_out) *status_out = st->status;
+}
+
+struct AlphaWS {
+  MatMeta Ha;
+  AlphaState *st;
+  double *kk;
+  int *kit, *kst;
+  char *sub;
+  size_t sub_cap;
+};
+
+tt_status carve_alpha(const MatMeta &H, const MatMeta &V, const MatMeta &S, const MatMeta &F, const VecMeta &psi,
+                      const VecMeta &z, const alpha_opts &o, Arena &ar, AlphaWS &W) {
+  const int d = H.d;
+  if (V.d != d) return fail(TT_ERR_SHAPE, "alpha_secant: number of cores differ");
+  for (int k = 0; k < d; ++k)
+    if (V.m[k] != H.m[k] || V.n[k] != H.n[k]) return fail(TT_ERR_SHAPE, "alpha_secant: V and H shapes differ");
+  std::memset(&W, 0, sizeof(W));
+  W.Ha = H;
+  long long off = 0;
+  for (int k = 0; k <= d; ++k) W.Ha.Rcap[k] = (k == 0 || k == d) ? 1 : H.Rcap[k] + V.Rcap[k];
+  for (int k = 0; k < d; ++k) {
+    W.Ha.off[k] = off;
+    off += (long long)W.Ha.Rcap[k] * H.m[k] * H.n[k] * W.Ha.Rcap[k + 1];
+  }
+  W.Ha.data = ar.take<double>(off);
+  W.Ha.R = ar.take<int>(d + 1);
+  W.st = ar.take<AlphaState>(1);
+  W.kk = ar.take<double>(1);
+  W.kit = ar.take<int>(1);
+  W.kst = ar.take<int>(1);
+  size_t mx = keff_ws_bytes(W.Ha, S, F, psi, z, o.keff);
+  if (mx == 0) return fail(TT_ERR_SHAPE, "alpha_secant: k-eff operands rejected");
+  { Arena c; round_meta(mat_as_vec(W.Ha), 0.0, 1, nullptr, nullptr, 0, c, nullptr); mx = c.used > mx ? c.used : mx; }
+  W.sub_cap = mx;
+  W.sub = ar.take<char>(mx);
+  return TT_OK;
+}
+
+}  // namespace
+
+size_t alpha_ws_bytes(const MatMeta &H, const MatMeta &V, const MatMeta &S, const MatMeta &F, const VecMeta &psi,
+                      const VecMeta &z, const alpha_opts &o) {
+  Arena ar;
+  AlphaWS W;
+  if (carve_alpha(H, V, S, F, psi, z, o, ar, W) != TT_OK) return 0;
+  return ar.used;
+}
+
+tt_status alpha_meta(const MatMeta &H, const MatMeta &V, const MatMeta &S, const MatMeta &F, const VecMeta &psi,
+                     const VecMeta &z, const alpha_opts &o, const alpha_report &rep, Arena &ar, cudaStream_t s) {
+  AlphaWS W;
+  TT_TRY(carve_alpha(H, V, S, F, psi, z, o, ar, W));
+  if (!ar.base) return TT_OK;
+  if (!ar.ok()) return fail(TT_ERR_CAPACITY, "alpha_secant: workspace too small");
+  if (o.max_alpha < 1 || !(o.tol > 0.0)) return fail(TT_ERR_ARG, "alpha_secant: max_alpha >= 1, tol > 0");
+  alpha_init_kernel<<<1, 1, 0, s>>>(W.st, o.alpha0);
+  const VecMeta hv = mat_as_vec(H), vv = mat_as_vec(V), av = mat_as_vec(W.Ha);
+  keff_report kr;
+  kr.k_dev = W.kk; kr.iters_dev = W.kit; kr.k_hist_dev = nullptr; kr.sweeps_hist_dev = nullptr;
+  kr.hist_cap = 0; kr.status_dev = W.kst;
+  int hflag = 0;
+  for (int t = 0; t < o.max_alpha; ++t) {
+    TT_TRY(add_meta(hv, &W.st->one, vv, &W.st->a, av, s));
+    { Arena a; a.base = W.sub; a.cap = W.sub_cap; TT_TRY(round_meta(av, o.eps_op, 1 << 30, nullptr, nullptr, 0, a, s)); }
+    cudaMemsetAsync(W.kst, 0, sizeof(int), s);
+    {
+      Arena a; a.base = W.sub; a.cap = W.sub_cap;
+      TT_TRY(keff_meta(W.Ha, S, F, psi, z, 1.0, o.keff, kr, a, s, t == 0 ? nullptr : &W.st->k));
+    }
+    alpha_update_kernel<<<1, 1, 0, s>>>(W.st, W.kk, W.kit, W.kst, o.alpha1, o.tol, o.max_alpha, rep.alpha_hist_dev,
+                                        rep.k_hist_dev, rep.keff_iters_hist_dev, rep.hist_cap, rep.alpha_dev,
+                                        rep.k_dev, rep.iters_dev, rep.status_dev);
+    cudaMemcpyAsync(&hflag, &W.st->flag, sizeof(int), cudaMemcpyDeviceToHost, s);
+    cudaStreamSynchronize(s);
+    TT_TRY(check_launch("alpha iteration"));
+    if (hflag) break;
+  }
+  return check_launch("alpha_secant");
 }
 
 }  // namespace tt
@@ -323,4 +467,35 @@ extern "C" tt_status keff_fixed_point(const tt_mat *H, const tt_mat *S, const tt
   ar.base = (char *)ws;
   ar.cap = wsb;
   return keff_meta(Hm, Sm, Fm, pm, zm, k0, *o, *rep, ar, (cudaStream_t)s);
+}
+
+extern "C" size_t alpha_workspace(const tt_mat *H, const tt_mat *V, const tt_mat *S, const tt_mat *F,
+                                  const tt_vec *psi, const tt_vec *z, const alpha_opts *o) {
+  MatMeta Hm, Vm, Sm, Fm;
+  VecMeta pm, zm;
+  if (!o || make_mat_meta(H, Hm) || make_mat_meta(V, Vm) || make_mat_meta(S, Sm) || make_mat_meta(F, Fm) ||
+      make_vec_meta(psi, pm) || make_vec_meta(z, zm))
+    return 0;
+  return alpha_ws_bytes(Hm, Vm, Sm, Fm, pm, zm, *o);
+}
+
+extern "C" tt_status alpha_secant(const tt_mat *H, const tt_mat *V, const tt_mat *S, const tt_mat *F, tt_vec *psi,
+                                  tt_vec *z, const alpha_opts *o, alpha_report *rep, void *ws, size_t wsb,
+                                  tt_stream s) {
+  MatMeta Hm, Vm, Sm, Fm;
+  VecMeta pm, zm;
+  TT_TRY(make_mat_meta(H, Hm));
+  TT_TRY(make_mat_meta(V, Vm));
+  TT_TRY(make_mat_meta(S, Sm));
+  TT_TRY(make_mat_meta(F, Fm));
+  TT_TRY(make_vec_meta(psi, pm));
+  TT_TRY(make_vec_meta(z, zm));
+  if (!o || !rep || !ws) return fail(TT_ERR_ARG, "alpha_secant: NULL options, report or workspace");
+  const keff_opts &k = o->keff;
+  if (k.max_outer < 1 || k.rmax < 1 || k.max_sweeps < 1 || k.gmres_max_restarts < 1)
+    return fail(TT_ERR_ARG, "alpha_secant: k-eff iteration limits must be >= 1");
+  Arena ar;
+  ar.base = (char *)ws;
+  ar.cap = wsb;
+  return alpha_meta(Hm, Vm, Sm, Fm, pm, zm, *o, *rep, ar, (cudaStream_t)s);
 }

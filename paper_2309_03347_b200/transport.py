@@ -48,7 +48,42 @@ def factor_terms_1d(prob, op: str):
     return terms
 
 
+def _unpack(out, nt, sizes):
+    per = sum(n * n for n in sizes)
+    terms = []
+    for t in range(nt):
+        p = out[t * per:(t + 1) * per]
+        o, fac = 0, []
+        for n in sizes:
+            fac.append(p[o:o + n * n].reshape(n, n, order="F"))
+            o += n * n
+        terms.append(fac)
+    return terms
+
+
+def velocity_terms(prob):
+    """Rank-1 terms of V^{-1} from libtt's host constructor."""
+    q = prob["quad"]
+    dim = int(prob.get("dim", 3))
+    nv, G = int(prob["nv"]), int(prob["G"])
+    L = len(q["w"])
+    inv_v = np.ascontiguousarray(prob["inv_v"], dtype=np.float64)
+    arr = [np.ascontiguousarray(q[k], dtype=np.float64) if k in q else None for k in ("mu", "eta", "xi")]
+    refl = 1 if prob.get("boundary", "vacuum") == "reflective" else 0
+    args = [dim, nv, G, L, *[(_dp(a) if a is not None else None) for a in arr], _dp(inv_v), refl]
+    lib = _lib.lib()
+    nt = lib.tt_velocity_terms(*args, None)
+    if nt < 0:
+        raise _lib.TTError(1, lib.tt_last_error().decode())
+    sizes = (nv, L, G) if dim == 1 else (nv, nv, nv, L, G)
+    out = np.zeros(nt * sum(n * n for n in sizes), dtype=np.float64)
+    lib.tt_velocity_terms(*args, _dp(out))
+    return _unpack(out, nt, sizes)
+
+
 def factor_terms(prob, op: str):
+    if op == "V":
+        return velocity_terms(prob)
     if prob.get("dim", 3) == 1:
         return factor_terms_1d(prob, op)
     q = prob["quad"]
@@ -148,8 +183,10 @@ def operator(prob, op: str, eps: float = 1e-13, device="cuda", qtt=None) -> TTMa
     return _sum_round([term_cores(f, qtt) for f in terms], eps, device)
 
 
-def operators(prob, eps: float = 1e-13, device="cuda", qtt=None):
-    return {k: operator(prob, k, eps, device, qtt) for k in ("H", "S", "F")}
+def operators(prob, eps: float = 1e-13, device="cuda", qtt=None, velocity=False):
+    """H, S, F (and V^{-1} with velocity=True, for the alpha problem)."""
+    keys = ("H", "S", "F", "V") if velocity else ("H", "S", "F")
+    return {k: operator(prob, k, eps, device, qtt) for k in keys}
 
 
 def modes(prob, qtt=None):

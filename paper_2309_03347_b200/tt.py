@@ -318,3 +318,40 @@ def keff_fixed_point(H: TTMat, S: TTMat, F: TTMat, psi: TTVec, z: TTVec, k0: flo
     check(lib().keff_fixed_point(H.c, S.c, F.c, psi.c, z.c, float(k0), C.byref(o), C.byref(rep), _ptr(ws),
                                  ws.numel(), C.c_void_p(_stream(stream))))
     return KeffResult(k, iters, kh, sh, st)
+
+
+# -------------------------------------------------------------- NEXT-2 ---
+
+class AlphaResult:
+    def __init__(self, alpha, k, iters, alpha_hist, k_hist, keff_iters_hist, status):
+        self.alpha, self.k, self.iters = alpha, k, iters
+        self.alpha_hist, self.k_hist, self.keff_iters_hist, self.status = alpha_hist, k_hist, keff_iters_hist, status
+
+
+def alpha_secant(H: TTMat, V: TTMat, S: TTMat, F: TTMat, psi: TTVec, z: TTVec, alpha0: float = 0.0,
+                 alpha1: float = 0.01, tol: float = 1e-9, eps_op: float = 1e-13, max_alpha: int = 50,
+                 tol_k: float = 1e-10, eps_round: float = 1e-12, eps_solve: float = 1e-11, max_outer: int = 200,
+                 rmax: int = 1 << 20, max_sweeps: int = 20, restart: int = 40, max_restarts: int = 50,
+                 hist_cap: int = 64, stream=None) -> AlphaResult:
+    """alpha eigenvalue by the secant loop around the device k-eff solve (NEXT-2)."""
+    ko = _lib.keff_opts(float(tol_k), float(eps_round), float(eps_solve), int(max_outer), int(min(rmax, 2**30)),
+                        int(max_sweeps), int(restart), int(max_restarts))
+    o = _lib.alpha_opts(float(alpha0), float(alpha1), float(tol), float(eps_op), int(max_alpha), ko)
+    dev = psi.device
+    a = torch.zeros(1, dtype=torch.float64, device=dev)
+    k = torch.zeros(1, dtype=torch.float64, device=dev)
+    it = torch.zeros(1, dtype=torch.int32, device=dev)
+    ah = torch.zeros(hist_cap, dtype=torch.float64, device=dev)
+    kh = torch.zeros(hist_cap, dtype=torch.float64, device=dev)
+    ih = torch.zeros(hist_cap, dtype=torch.int32, device=dev)
+    st = torch.zeros(1, dtype=torch.int32, device=dev)
+    rep = _lib.alpha_report(a.data_ptr(), k.data_ptr(), it.data_ptr(), ah.data_ptr(), kh.data_ptr(), ih.data_ptr(),
+                            int(hist_cap), st.data_ptr())
+    nb = lib().alpha_workspace(H.c, V.c, S.c, F.c, psi.c, z.c, C.byref(o))
+    if nb == 0:
+        check(lib().alpha_secant(H.c, V.c, S.c, F.c, psi.c, z.c, C.byref(o), C.byref(rep), None, 0,
+                                 C.c_void_p(_stream(stream))))
+    ws = workspace(nb, dev)
+    check(lib().alpha_secant(H.c, V.c, S.c, F.c, psi.c, z.c, C.byref(o), C.byref(rep), _ptr(ws), ws.numel(),
+                             C.c_void_p(_stream(stream))))
+    return AlphaResult(a, k, it, ah, kh, ih, st)

@@ -198,3 +198,50 @@ def test_amen_mv_gpu():
     assert np.linalg.norm(got - ref) <= 1e-7 * np.linalg.norm(ref), sw
     yo, _ = so.amen_mv(H, x, y0, z0, eps=1e-8, max_sweeps=40)
     assert np.linalg.norm(got - ott.tt_full(yo)) <= 2e-7 * np.linalg.norm(ref)
+
+
+def _alpha_gpu(prob, modes, rmax, kick=4, **kw):
+    ops = gtr.operators(prob, velocity=True)
+    g = inputs.rng(62)
+    d = len(modes)
+    psi = tb.TTVec.from_cores([np.ones((1, n, 1)) for n in modes], rcap=[1] + [rmax + kick] * (d - 1) + [1])
+    z = tb.TTVec.from_cores(inputs.random_tt(g, modes, [1] + [kick] * (d - 1) + [1]))
+    res = tb.alpha_secant(ops["H"], ops["V"], ops["S"], ops["F"], psi, z, rmax=rmax, **kw)
+    torch.cuda.synchronize()
+    return res
+
+
+def test_alpha_c1_reflective_closed_form():
+    """NEXT-2 (Z32) on configs[0]'s reflective variant: the infinite-
+    medium closed form alpha* = v (nuSf + Ss - St) = 0.1; the first two k-eff
+    solves give k(0) = 1.2 and k(0.01) = 0.6/0.51."""
+    res = _alpha_gpu(inputs.problem_c1("reflective"), [8, 8, 8, 8, 1], rmax=64, tol=1e-10, tol_k=1e-12,
+                     eps_round=1e-13, eps_solve=1e-12, max_outer=80)
+    assert res.status.item() == 0
+    assert abs(res.alpha.item() - 0.1) <= 1e-8
+    kh = res.k_hist.cpu().numpy()
+    assert abs(kh[0] - 1.2) <= 1e-9 and abs(kh[1] - 0.6 / 0.51) <= 1e-9
+    assert res.iters.item() <= 10
+
+
+@pytest.mark.parametrize("nsf", [2.8, 2.0], ids=["super", "sub"])
+def test_alpha_cube_vs_dense(nsf):
+    """4^3 S2 cube: device alpha vs the oracle's dense secant (LU k-eff solves)."""
+    prob = small_c1(4)
+    prob["materials"][0]["nu_sigma_f"] = np.array([nsf])
+    ops = T.dense_operators(prob)
+    ad, _, _ = so.alpha_dense(ops["H"], ops["V"], ops["S"], ops["F"], tol=1e-11)
+    res = _alpha_gpu(prob, [4, 4, 4, 8, 1], rmax=32, tol=1e-11, tol_k=1e-12, eps_round=1e-13, eps_solve=1e-12)
+    assert res.status.item() == 0
+    assert abs(res.alpha.item() - ad) <= 1e-8 * abs(ad)
+
+
+def test_alpha_slab():
+    """1-D Pu-239 slab L=4, 1024 points: device alpha vs the oracle's
+    matrix-free secant (sigma_t shift, Z39); the slab is critical so |alpha| is small."""
+    p = inputs.problem_slab(4)
+    ao, _, _ = so.alpha_secant(lambda a: T.slab_keff_sweep(p, tol=1e-13, alpha=a)[0], tol=1e-11)
+    res = _alpha_gpu(p, gtr.modes(p), rmax=40, kick=3, tol=1e-10, tol_k=1e-12, eps_round=1e-12,
+                     eps_solve=1e-12, eps_op=1e-12)
+    assert res.status.item() == 0
+    assert abs(res.alpha.item() - ao) <= 1e-8

@@ -52,3 +52,17 @@ def test_reflective_terms_sum_to_dense(gtr):
     for op in "HSF":
         M = sum(T.kron_term(t) for t in gtr.factor_terms(p, op))
         assert np.array_equal(M, dense[op])
+
+
+@pytest.mark.parametrize("prob", [inputs.problem_c1(), inputs.problem_c1("reflective"),
+                                  inputs.problem_small_hetero(nv=4, G=2, N=4), inputs.problem_slab(4, nv=16)],
+                         ids=["C1", "C1-reflective", "hetero4", "slab16"])
+def test_velocity_terms_match_oracle(gtr, prob):
+    """V^{-1}: host terms sum to the oracle's dense operator
+    (reflective: with the face rows zeroed, Z15)."""
+    import copy
+    p = copy.deepcopy(prob)
+    if p.get("dim", 3) == 3:
+        p["nv"] = 4
+    got = sum(T.kron_term(t) for t in gtr.factor_terms(p, "V"))
+    assert np.array_equal(got, T.dense_operators(p)["V"])
