@@ -171,18 +171,20 @@ def _draw_material(g, G, fissile, upscatter_from=None):
     return {"sigma_t": st, "sigma_s": ss, "nu_sigma_f": nsf}
 
 
-def problem_c3(seed: int = 3):
+def problem_c3(seed: int = 3, nv: int = 64):
     """BASELINE.json configs[2]: [0,10]^3 cm, 64 vertices/axis, G=7 downscatter,
-    S8 LS-style (80 ordinates), vacuum, fuel cells [16,48)^3 in a reflector."""
+    S8 LS-style (80 ordinates), vacuum, fuel cells [16,48)^3 in a reflector.
+    nv < 64 gives the same problem on a coarser grid (fuel cells
+    [nv/4, 3nv/4)^3), used for parity at sizes the oracle finishes quickly."""
     g = rng(seed)
     G = 7
     refl = _draw_material(g, G, fissile=False)
     fuel = _draw_material(g, G, fissile=True)
     chi = np.zeros(G); chi[0] = 0.7; chi[1] = 0.3
     return {
-        "name": "C3", "nv": 64, "extent": 10.0, "G": G, "quad": quadrature_ls_style(8),
-        "boundary": "vacuum", "qtt": True, "materials": [refl, fuel], "chi": chi,
-        "boxes": [((16, 16, 16), (48, 48, 48), 1)], "seed": seed, "inv_v": inv_velocity(G),
+        "name": "C3" if nv == 64 else f"C3-nv{nv}", "nv": nv, "extent": 10.0, "G": G,
+        "quad": quadrature_ls_style(8), "boundary": "vacuum", "qtt": True, "materials": [refl, fuel], "chi": chi,
+        "boxes": [((nv // 4,) * 3, (3 * nv // 4,) * 3, 1)], "seed": seed, "inv_v": inv_velocity(G),
     }
 
 

@@ -307,6 +307,112 @@ def slab_keff_sweep(prob, tol=1e-12, max_it=100000, alpha=0.0):
     return k, psi.reshape(-1), max_it
 
 
+def keff_sweep_3d(prob, tol=1e-10, max_it=10000, alpha=0.0, verbose=False):
+    """Matrix-free Eq. 8 for the 3-D vertex-DD problem with vacuum
+    boundaries: H^{-1} is, per (group, ordinate), a
+    transport sweep in the octant's direction solving the cell
+    equations of eq. Discretized_kNTE (row vertex = the cell's
+    downstream corner, Z7) for the downstream corner, with psi = 0 on inflow
+    faces (Z33); S and F act through the scalar flux phi_g = sum_l w_l psi_{g,l}
+    averaged over the 8 corners of each cell with that cell's cross sections
+    (Z4, Z5, Z34).  alpha adds alpha/v_g to sigma_t (the alpha term of eq.
+    Discretized_alphaNTE).  Sweeps run over wavefront planes
+    i + j + k = const, vectorised over (group, ordinate).  Returns (k, psi, it)
+    with psi shaped (G, L, n, n, n) [g, l, z, y, x]."""
+    if prob.get("boundary", "vacuum") != "vacuum" or prob.get("dim", 3) != 3:
+        raise ValueError("keff_sweep_3d: 3-D vacuum problems only")
+    n = prob["nv"]
+    nc = n - 1
+    h = prob["extent"] / nc
+    quad = prob["quad"]
+    G = prob["G"]
+    L = len(quad["w"])
+    w = quad["w"]
+    mats = prob["materials"]
+    chi = prob["chi"]
+    inv_v = prob.get("inv_v", np.ones(G))
+    mat = material_map(prob)                                   # [cz, cy, cx]
+    st = np.zeros((G, nc, nc, nc))
+    for m, M in enumerate(mats):
+        st[:, mat == m] = (M["sigma_t"] + alpha * inv_v)[:, None]
+    octs = octant_of(quad)
+    # wavefront planes of the +++ sweep (vertices 1..n-1 on every axis)
+    ii, jj, kk = np.meshgrid(np.arange(1, n), np.arange(1, n), np.arange(1, n), indexing="ij")
+    pl = (ii + jj + kk).ravel()
+    vflat = (ii + n * (jj + n * kk)).ravel()
+    cflat = ((ii - 1) + nc * ((jj - 1) + nc * (kk - 1))).ravel()
+    planes = [(vflat[pl == p], cflat[pl == p]) for p in range(3, 3 * (n - 1) + 1)]
+    corners = [(dx, dy, dz) for dz in (0, 1) for dy in (0, 1) for dx in (0, 1)]
+
+    def cell_avg(phi):                                         # phi [g, z, y, x] -> [g, cz, cy, cx]
+        acc = np.zeros((phi.shape[0], nc, nc, nc))
+        for (dx, dy, dz) in corners:
+            acc += phi[:, dz:dz + nc, dy:dy + nc, dx:dx + nc]
+        return acc / 8.0
+
+    def source(psi, k):
+        phi8 = cell_avg(np.einsum("l,glzyx->gzyx", w, psi))
+        q = np.zeros((G, nc, nc, nc))
+        for m, M in enumerate(mats):
+            Mk = M["sigma_s"] + np.outer(chi, M["nu_sigma_f"]) / k
+            sel = mat == m
+            q[:, sel] = Mk @ phi8[:, sel]
+        return q
+
+    def fsum(psi):
+        phi8 = cell_avg(np.einsum("l,glzyx->gzyx", w, psi))
+        tot = 0.0
+        for m, M in enumerate(mats):
+            tot += np.sum(M["nu_sigma_f"][:, None] * phi8[:, mat == m])
+        return tot
+
+    def sweep(q):
+        psi = np.zeros((G, L, n, n, n))
+        for b in range(8):
+            lb = np.nonzero(octs == b)[0]
+            if lb.size == 0:
+                continue
+            flips = [ax for ax, bit in ((3, 1), (2, 2), (1, 4)) if not (b & bit)]   # axes of [g, z, y, x]
+            qb = np.flip(q, axis=flips) if flips else q
+            sb = np.flip(st, axis=flips) if flips else st
+            qb = np.ascontiguousarray(qb).reshape(G, -1)
+            sb = np.ascontiguousarray(sb).reshape(G, -1) / 8.0
+            Lb = lb.size
+            a = np.tile(np.abs(quad["mu"][lb]) / (4 * h), G)[:, None]
+            bb = np.tile(np.abs(quad["eta"][lb]) / (4 * h), G)[:, None]
+            c = np.tile(np.abs(quad["xi"][lb]) / (4 * h), G)[:, None]
+            X = np.zeros((G * Lb, n ** 3))
+            for (vi, ci) in planes:
+                s8 = np.repeat(sb[:, ci], Lb, axis=0)
+                rhs = np.repeat(qb[:, ci], Lb, axis=0)
+                for (dx, dy, dz) in corners[:-1]:
+                    coef = a * (2 * dx - 1) + bb * (2 * dy - 1) + c * (2 * dz - 1) + s8
+                    rhs = rhs - coef * X[:, vi - (1 - dx) - n * (1 - dy) - n * n * (1 - dz)]
+                X[:, vi] = rhs / (a + bb + c + s8)
+            Xb = X.reshape(G, Lb, n, n, n)
+            if flips:
+                Xb = np.flip(Xb, axis=[ax + 1 for ax in flips])
+            psi[:, lb] = Xb
+        return psi
+
+    psi = np.ones((G, L, n, n, n))
+    k = 1.0
+    f_old = fsum(psi)
+    for it in range(1, max_it + 1):
+        new = sweep(source(psi, k))
+        f_new = fsum(new)
+        knew = k * f_new / f_old
+        nn = np.linalg.norm(new)
+        psi = new / nn
+        f_old = f_new / nn
+        if verbose:
+            print(it, knew, flush=True)
+        if abs(knew - k) < tol:
+            return knew, psi, it
+        k = knew
+    return k, psi, max_it
+
+
 def dense_operators(prob):
     """Dense H, S, F as sums of Kronecker products."""
     T = operator_terms(prob)

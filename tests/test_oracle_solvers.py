@@ -123,3 +123,23 @@ def test_amen_mv_pins():
     y, info = so.amen_mv(H, x, y0, z0, eps=1e-8, max_sweeps=40)
     ref = ott.tt_full(ott.tt_matvec_fast(H, x))
     assert np.linalg.norm(ott.tt_full(y) - ref) <= 1e-7 * np.linalg.norm(ref)
+
+
+def test_keff_sweep_3d_matches_dense():
+    """The matrix-free sweep iteration (used for the C3
+    truth) reproduces the dense Kronecker power iteration on small problems, and
+    its alpha shift equals the dense H + alpha V^{-1}."""
+    probs = [copy.deepcopy(inputs.problem_c1()), inputs.problem_small_hetero(nv=4, G=2, N=4)]
+    probs[0]["nv"] = 4
+    for prob in probs:
+        ops = T.dense_operators(prob)
+        kd, psid, _ = so.keff_dense_power(ops["H"], ops["S"], ops["F"], tol=1e-13)
+        ks, psis, _ = T.keff_sweep_3d(prob, tol=1e-13)
+        assert abs(ks - kd) <= 1e-11 * kd
+        v = psis.reshape(-1)
+        assert np.linalg.norm(v * np.sign(v.sum()) - psid * np.sign(psid.sum())) <= 1e-9
+    prob = probs[1]
+    ops = T.dense_operators(prob)
+    kd, _, _ = so.keff_dense_power(ops["H"] + 0.3 * ops["V"], ops["S"], ops["F"], tol=1e-13)
+    ks, _, _ = T.keff_sweep_3d(prob, tol=1e-13, alpha=0.3)
+    assert abs(ks - kd) <= 1e-11 * kd
