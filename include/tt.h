@@ -245,6 +245,11 @@ typedef struct {
   int32_t max_sweeps;
   int32_t gmres_restart;
   int32_t gmres_max_restarts;
+  int32_t matvec;          /* 0: B = round(round(S Psi) + k^{-1} round(F Psi)) by   */
+                           /*    exact products; 1: B = amen_mv(S + k^{-1} F, Psi)   */
+                           /*    to eps_round (the paper's choice),     */
+                           /*    warm-started from the previous B                    */
+  int32_t mv_max_sweeps;   /* amen_mv sweep limit (matvec = 1)                       */
 } keff_opts;
 typedef struct {
   double *k_dev;           /* [1] final k                                          */

@@ -98,8 +98,8 @@ __global__ void keff_update_kernel(KeffScal *sc, const double *nrm, double tol, 
 }
 
 struct KeffWS {
-  MatMeta FT;
-  VecMeta ones, f, SP, FP, B, z0;
+  MatMeta FT, SF;
+  VecMeta ones, f, SP, FP, B, z0, zmv;
   KeffScal *sc;
   double *nrm, *dbuf;
   int *sweeps;
@@ -144,13 +144,30 @@ tt_status carve_keff(const MatMeta &H, const MatMeta &S, const MatMeta &F, const
   W.ones = vec_like(ar, d, F.m, one);
   for (int k = 0; k <= d; ++k) cap[k] = F.Rcap[k];
   W.f = vec_like(ar, d, F.n, cap);
-  for (int k = 0; k <= d; ++k) cap[k] = S.Rcap[k] * psi.rcap[k];
-  W.SP = vec_like(ar, d, S.m, cap);
-  int capF[TT_MAX_D + 1];
-  for (int k = 0; k <= d; ++k) capF[k] = F.Rcap[k] * psi.rcap[k];
-  W.FP = vec_like(ar, d, F.m, capF);
-  for (int k = 0; k <= d; ++k) cap[k] = (k == 0 || k == d) ? 1 : S.Rcap[k] * psi.rcap[k] + F.Rcap[k] * psi.rcap[k];
-  W.B = vec_like(ar, d, psi.n, cap);
+  const bool mv = o.matvec == 1;
+  if (o.matvec != 0 && o.matvec != 1) return fail(TT_ERR_ARG, "keff: matvec must be 0 (exact) or 1 (amen_mv)");
+  if (!mv) {
+    for (int k = 0; k <= d; ++k) cap[k] = S.Rcap[k] * psi.rcap[k];
+    W.SP = vec_like(ar, d, S.m, cap);
+    int capF[TT_MAX_D + 1];
+    for (int k = 0; k <= d; ++k) capF[k] = F.Rcap[k] * psi.rcap[k];
+    W.FP = vec_like(ar, d, F.m, capF);
+    for (int k = 0; k <= d; ++k) cap[k] = (k == 0 || k == d) ? 1 : S.Rcap[k] * psi.rcap[k] + F.Rcap[k] * psi.rcap[k];
+    W.B = vec_like(ar, d, psi.n, cap);
+  } else {
+    // S + k^{-1} F as one TT-matrix (ranks add), B fitted by amen_mv in psi's capacities
+    W.SF = S;
+    long long off = 0;
+    for (int k = 0; k <= d; ++k) W.SF.Rcap[k] = (k == 0 || k == d) ? 1 : S.Rcap[k] + F.Rcap[k];
+    for (int k = 0; k < d; ++k) {
+      W.SF.off[k] = off;
+      off += (long long)W.SF.Rcap[k] * S.m[k] * S.n[k] * W.SF.Rcap[k + 1];
+    }
+    W.SF.data = ar.take<double>(off);
+    W.SF.R = ar.take<int>(d + 1);
+    W.B = vec_like(ar, d, psi.n, psi.rcap);
+    W.zmv = vec_like(ar, d, z.n, z.rcap);
+  }
   W.z0 = vec_like(ar, d, z.n, z.rcap);
   W.sc = ar.take<KeffScal>(1);
   W.nrm = ar.take<double>(1);
@@ -159,9 +176,15 @@ tt_status carve_keff(const MatMeta &H, const MatMeta &S, const MatMeta &F, const
   // scratch: the max over the sub-operations
   size_t mx = 0;
   auto upd = [&](size_t v) { mx = v > mx ? v : mx; };
-  { Arena c; round_meta(W.SP, 0.0, 1, nullptr, nullptr, 0, c, nullptr); upd(c.used); }
-  { Arena c; round_meta(W.FP, 0.0, 1, nullptr, nullptr, 0, c, nullptr); upd(c.used); }
-  { Arena c; round_meta(W.B, 0.0, 1, nullptr, nullptr, 0, c, nullptr); upd(c.used); }
+  if (!mv) {
+    { Arena c; round_meta(W.SP, 0.0, 1, nullptr, nullptr, 0, c, nullptr); upd(c.used); }
+    { Arena c; round_meta(W.FP, 0.0, 1, nullptr, nullptr, 0, c, nullptr); upd(c.used); }
+    { Arena c; round_meta(W.B, 0.0, 1, nullptr, nullptr, 0, c, nullptr); upd(c.used); }
+  } else {
+    const size_t b = amen_mv_ws_bytes(W.SF, psi, W.B, W.zmv);
+    if (b == 0) return fail(TT_ERR_CAPACITY, "keff: amen_mv operands rejected (psi capacities must exceed z's)");
+    upd(b);
+  }
   { Arena c; round_meta(W.f, 0.0, 1, nullptr, nullptr, 0, c, nullptr); upd(c.used); }
   { Arena c; round_meta(psi, 0.0, 1, nullptr, nullptr, 0, c, nullptr); upd(c.used); }
   { Arena c; dot_meta(W.f, psi, nullptr, c, nullptr); upd(c.used); }
@@ -217,13 +240,21 @@ tt_status keff_meta(const MatMeta &H, const MatMeta &S, const MatMeta &F, const 
   ao.restart = o.gmres_restart;
   ao.max_restarts = o.gmres_max_restarts;
   int hflag = 0;
+  const bool mv = o.matvec == 1;
+  if (mv) TT_TRY(copy_meta(psi, W.B, s));   // first amen_mv guess: Psi_0
   for (int it = 0; it < o.max_outer; ++it) {
-    TT_TRY(matvec_meta(S, psi, W.SP, s));
-    { Arena a = sub(); TT_TRY(round_meta(W.SP, o.eps_round, o.rmax, nullptr, nullptr, 0, a, s)); }
-    TT_TRY(matvec_meta(F, psi, W.FP, s));
-    { Arena a = sub(); TT_TRY(round_meta(W.FP, o.eps_round, o.rmax, nullptr, nullptr, 0, a, s)); }
-    TT_TRY(add_meta(W.SP, nullptr, W.FP, &W.sc->kinv, W.B, s));
-    { Arena a = sub(); TT_TRY(round_meta(W.B, o.eps_round, o.rmax, nullptr, nullptr, 0, a, s)); }
+    if (!mv) {
+      TT_TRY(matvec_meta(S, psi, W.SP, s));
+      { Arena a = sub(); TT_TRY(round_meta(W.SP, o.eps_round, o.rmax, nullptr, nullptr, 0, a, s)); }
+      TT_TRY(matvec_meta(F, psi, W.FP, s));
+      { Arena a = sub(); TT_TRY(round_meta(W.FP, o.eps_round, o.rmax, nullptr, nullptr, 0, a, s)); }
+      TT_TRY(add_meta(W.SP, nullptr, W.FP, &W.sc->kinv, W.B, s));
+      { Arena a = sub(); TT_TRY(round_meta(W.B, o.eps_round, o.rmax, nullptr, nullptr, 0, a, s)); }
+    } else {
+      TT_TRY(add_meta(mat_as_vec(S), nullptr, mat_as_vec(F), &W.sc->kinv, mat_as_vec(W.SF), s));
+      TT_TRY(copy_meta(W.z0, W.zmv, s));
+      { Arena a = sub(); TT_TRY(amen_mv_meta(W.SF, psi, W.B, W.zmv, o.eps_round, o.mv_max_sweeps, o.rmax, nullptr, a, s)); }
+    }
     TT_TRY(copy_meta(W.z0, z, s));
     { Arena a = sub(); TT_TRY(amen_solve_meta(H, W.B, psi, z, ao, W.sweeps, nullptr, nullptr, a, s)); }
     { Arena a = sub(); TT_TRY(dot_meta(W.f, psi, &W.sc->s_new, a, s)); }
@@ -461,7 +492,8 @@ extern "C" tt_status keff_fixed_point(const tt_mat *H, const tt_mat *S, const tt
   TT_TRY(make_vec_meta(psi, pm));
   TT_TRY(make_vec_meta(z, zm));
   if (!o || !rep || !ws) return fail(TT_ERR_ARG, "keff_fixed_point: NULL options, report or workspace");
-  if (o->max_outer < 1 || o->rmax < 1 || o->max_sweeps < 1 || o->gmres_max_restarts < 1)
+  if (o->max_outer < 1 || o->rmax < 1 || o->max_sweeps < 1 || o->gmres_max_restarts < 1 ||
+      (o->matvec == 1 && o->mv_max_sweeps < 1))
     return fail(TT_ERR_ARG, "keff_fixed_point: iteration limits must be >= 1");
   Arena ar;
   ar.base = (char *)ws;
@@ -492,7 +524,8 @@ extern "C" tt_status alpha_secant(const tt_mat *H, const tt_mat *V, const tt_mat
   TT_TRY(make_vec_meta(z, zm));
   if (!o || !rep || !ws) return fail(TT_ERR_ARG, "alpha_secant: NULL options, report or workspace");
   const keff_opts &k = o->keff;
-  if (k.max_outer < 1 || k.rmax < 1 || k.max_sweeps < 1 || k.gmres_max_restarts < 1)
+  if (k.max_outer < 1 || k.rmax < 1 || k.max_sweeps < 1 || k.gmres_max_restarts < 1 ||
+      (k.matvec == 1 && k.mv_max_sweeps < 1))
     return fail(TT_ERR_ARG, "alpha_secant: k-eff iteration limits must be >= 1");
   Arena ar;
   ar.base = (char *)ws;

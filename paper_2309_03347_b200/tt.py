@@ -295,6 +295,9 @@ def amen_mv(A: TTMat, b: TTVec, y: TTVec, z: TTVec, eps: float, rmax: int = 1 <<
 
 # ------------------------------------------------------------------ a9 ---
 
+_MV = {"exact": 0, "amen_mv": 1}
+
+
 class KeffResult:
     def __init__(self, k, iters, k_hist, sweeps_hist, status):
         self.k, self.iters, self.k_hist, self.sweeps_hist, self.status = k, iters, k_hist, sweeps_hist, status
@@ -303,9 +306,10 @@ class KeffResult:
 def keff_fixed_point(H: TTMat, S: TTMat, F: TTMat, psi: TTVec, z: TTVec, k0: float = 1.0, tol_k: float = 1e-10,
                      eps_round: float = 1e-12, eps_solve: float = 1e-11, max_outer: int = 200, rmax: int = 1 << 20,
                      max_sweeps: int = 20, restart: int = 40, max_restarts: int = 50, hist_cap: int = 256,
-                     stream=None) -> KeffResult:
+                     matvec: str = "exact", mv_max_sweeps: int = 10, stream=None) -> KeffResult:
+    """matvec: "exact" (exact products + rounding) or "amen_mv" (fit-based product, NEXT-1)."""
     o = _lib.keff_opts(float(tol_k), float(eps_round), float(eps_solve), int(max_outer), int(min(rmax, 2**30)),
-                       int(max_sweeps), int(restart), int(max_restarts))
+                       int(max_sweeps), int(restart), int(max_restarts), _MV[matvec], int(mv_max_sweeps))
     dev = psi.device
     k = torch.zeros(1, dtype=torch.float64, device=dev)
     iters = torch.zeros(1, dtype=torch.int32, device=dev)
@@ -332,10 +336,10 @@ def alpha_secant(H: TTMat, V: TTMat, S: TTMat, F: TTMat, psi: TTVec, z: TTVec, a
                  alpha1: float = 0.01, tol: float = 1e-9, eps_op: float = 1e-13, max_alpha: int = 50,
                  tol_k: float = 1e-10, eps_round: float = 1e-12, eps_solve: float = 1e-11, max_outer: int = 200,
                  rmax: int = 1 << 20, max_sweeps: int = 20, restart: int = 40, max_restarts: int = 50,
-                 hist_cap: int = 64, stream=None) -> AlphaResult:
+                 hist_cap: int = 64, matvec: str = "exact", mv_max_sweeps: int = 10, stream=None) -> AlphaResult:
     """alpha eigenvalue by the secant loop around the device k-eff solve (NEXT-2)."""
     ko = _lib.keff_opts(float(tol_k), float(eps_round), float(eps_solve), int(max_outer), int(min(rmax, 2**30)),
-                        int(max_sweeps), int(restart), int(max_restarts))
+                        int(max_sweeps), int(restart), int(max_restarts), _MV[matvec], int(mv_max_sweeps))
     o = _lib.alpha_opts(float(alpha0), float(alpha1), float(tol), float(eps_op), int(max_alpha), ko)
     dev = psi.device
     a = torch.zeros(1, dtype=torch.float64, device=dev)

@@ -125,6 +125,24 @@ def test_keff_c1_vacuum():
     assert abs(hist[-1] - res.k.item()) == 0.0
 
 
+@pytest.mark.parametrize("case", ["c1", "slab"])
+def test_keff_amen_mv(case):
+    """k-eff with B formed by the fit-based product (keff_opts.matvec = amen_mv,
+    P:1501-1506) reaches the same k as the oracle: C1 vacuum (dense golden value,
+    |dk|/k <= 1e-8) and the slab L=4 (matrix-free sweep)."""
+    if case == "c1":
+        kd = float(open(os.path.join(GOLD, "c1_keff_vacuum.txt")).read().split()[-1])
+        res, _ = _keff_gpu(inputs.problem_c1(), [8, 8, 8, 8, 1], rmax=64, tol_k=1e-12, eps_round=1e-13,
+                           eps_solve=1e-12, matvec="amen_mv")
+    else:
+        p = inputs.problem_slab(4)
+        kd, _, _ = T.slab_keff_sweep(p, tol=1e-13)
+        res, _ = _keff_gpu(p, gtr.modes(p), rmax=40, kick=3, tol_k=1e-11, eps_round=1e-11, eps_solve=1e-11,
+                           matvec="amen_mv")
+    assert res.status.item() == 0
+    assert abs(res.k.item() - kd) / kd <= 1e-8
+
+
 def test_keff_c1_reflective():
     """configs[0] reflective variant (reading Z15): the device-assembled operator
     equals the dense one, k -> k_inf = nuSf / (St - Ss) = 1.2 and, from psi0 = 1,
@@ -245,3 +263,30 @@ def test_alpha_slab():
                      eps_solve=1e-12, eps_op=1e-12)
     assert res.status.item() == 0
     assert abs(res.alpha.item() - ao) <= 1e-8
+
+
+def test_keff_c3_small_grid():
+    """configs[2]'s problem (two regions, G=7 downscatter, 80 S8 ordinates, QTT
+    space) on a 4^3 grid, where rmax does not bind: the device TT k-eff (B by
+    amen_mv; exact products of rank R_S r = 4800 would not fit) equals the
+    oracle's matrix-free full-grid sweep iteration (discretisation truth) to 1e-8."""
+    matvec = "amen_mv"
+    p = inputs.problem_c3(nv=4)
+    kt, _, _ = T.keff_sweep_3d(p, tol=1e-13)
+    res, psi = _keff_gpu(p, gtr.modes(p), rmax=96, kick=4, tol_k=1e-11, eps_round=1e-12, eps_solve=1e-12,
+                         matvec=matvec, max_sweeps=20)
+    assert res.status.item() == 0
+    assert abs(res.k.item() - kt) / kt <= 1e-8
+
+
+def test_keff_c3_truncated():
+    """configs[2]'s problem on an 8^3 grid with rmax = 64 (binding: the full-grid
+    solution's QTT ranks reach 391 at eps 1e-4): the TT k-eff stays within the
+    truncation level of the matrix-free truth (C3 partially
+    pinned; P:1654 reports ~1e-5 discrepancies at tolerance 1e-6)."""
+    p = inputs.problem_c3(nv=8)
+    kt = [float(l.split()[1]) for l in open(os.path.join(GOLD, "c3_keff.txt"))
+          if l.strip() and not l.startswith("#") and l.split()[0] == "8"][0]
+    res, _ = _keff_gpu(p, gtr.modes(p), rmax=64, kick=4, tol_k=1e-7, eps_round=1e-7, eps_solve=1e-7,
+                       matvec="amen_mv", max_sweeps=4, mv_max_sweeps=4, max_outer=40)
+    assert abs(res.k.item() - kt) / kt <= 2e-4
