@@ -1,5 +1,6 @@
 // Elementwise / structural TT operations: exact matvec (a1), add / scale (a2),
 // copy, dot (a8), plus the meta plumbing and error state of the C ABI.
+#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -163,6 +164,7 @@ struct MvPair {
   const int *r;   // vector ranks (device)
   int *ry;        // output ranks (device)
   int m, n, k, last;
+  int blk0;       // work estimate at the capacity ranks (host sort key)
 };
 
 // One CTA per output column rho' = a' + R1 b' (grid-strided): the slices
@@ -171,10 +173,12 @@ struct MvPair {
 // coalesced stores — one small division per entry, no per-entry index algebra.
 constexpr int MV_SMEM = 6144;  // doubles of staging (48 KB)
 
-__device__ __forceinline__ void matvec_core_cols(const double *__restrict__ A, const double *__restrict__ X,
-                                                 double *__restrict__ Y, int R0, int R1, int r0, int r1, int m,
-                                                 int n, double *sm, int smcap) {
-  const int P = R0 * r0, P1 = R1 * r1;
+template <int MC, int NC>   // MC = NC = 2: QTT 2x2 cores (compile-time modes); 0: runtime modes
+__device__ __forceinline__ void matvec_cols_t(const double *__restrict__ A, const double *__restrict__ X,
+                                              double *__restrict__ Y, int R0, int R1, int r0, int r1, int m_,
+                                              int n_, double *sm, int smcap, int cta, int ncta) {
+  const int m = MC ? MC : m_, n = NC ? NC : n_;
+  const int P = R0 * r0;
   const int na = R0 * m * n * R1;                         // the whole operator core
   const double *As = A;
   if (na <= smcap) {
@@ -183,47 +187,65 @@ __device__ __forceinline__ void matvec_core_cols(const double *__restrict__ A, c
     As = sm;
   }
   // one thread per (rho, b'): its X[b, :, b'] values are loaded once and reused
-  // for every a' in [0, R1) and i in [0, m) (R1 m independent outputs per item)
+  // for every a' in [0, R1) and i in [0, m) (R1 m independent coalesced stores per item)
   const int items = P * r1;
   const int per_col = P * m;
-  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < items; e += gridDim.x * blockDim.x) {
+  for (int e = cta * blockDim.x + threadIdx.x; e < items; e += ncta * blockDim.x) {
     const int b1 = e / P, rho = e - b1 * P;
     const int b = rho / R0, a = rho - b * R0;
-    const double *Xr = X + b + (long long)r0 * n * b1;
-    double *Yr = Y + rho + (long long)per_col * R1 * b1;
+    const double *Xr = X + b + r0 * n * b1;
+    double *Yr = Y + rho + (size_t)per_col * R1 * b1;
     const double *Ar = As + a;
-    if (n == 2) {
-      const double x0 = Xr[0], x1 = Xr[r0];
+    if (NC == 2 && MC == 2) {
+      const double x0 = __ldg(Xr), x1 = __ldg(Xr + r0);
+#pragma unroll 2
       for (int a1 = 0; a1 < R1; ++a1) {
-        const double *Aa = Ar + R0 * m * 2 * a1;
-        double *Ya = Yr + (long long)per_col * a1;
-        for (int i = 0; i < m; ++i) Ya[P * i] = fma(Aa[R0 * i], x0, Aa[R0 * (i + m)] * x1);
+        const double *Aa = Ar + 4 * R0 * a1;
+        const double y0 = fma(Aa[0], x0, Aa[2 * R0] * x1);
+        const double y1 = fma(Aa[R0], x0, Aa[3 * R0] * x1);
+        double *Ya = Yr + 2 * P * a1;
+        __stcs(Ya, y0);
+        __stcs(Ya + P, y1);
       }
     } else {
       for (int a1 = 0; a1 < R1; ++a1) {
-        const double *Aa = Ar + (long long)R0 * m * n * a1;
-        double *Ya = Yr + (long long)per_col * a1;
+        const double *Aa = Ar + R0 * m * n * a1;
+        double *Ya = Yr + (size_t)per_col * a1;
         for (int i = 0; i < m; ++i) {
           double s = 0.0;
-          for (int j = 0; j < n; ++j) s = fma(Aa[R0 * (i + m * j)], Xr[(long long)r0 * j], s);
+          for (int j = 0; j < n; ++j) s = fma(Aa[R0 * (i + m * j)], Xr[r0 * j], s);
           Ya[P * i] = s;
         }
       }
     }
   }
-  (void)P1;
 }
 
-__global__ void __launch_bounds__(256) matvec_batched_kernel(const MvPair *__restrict__ pairs, int d, int smcap) {
+__device__ void matvec_core_cols(const double *__restrict__ A, const double *__restrict__ X,
+                                 double *__restrict__ Y, int R0, int R1, int r0, int r1, int m, int n, double *sm,
+                                 int smcap) {
+  if (m == 2 && n == 2) matvec_cols_t<2, 2>(A, X, Y, R0, R1, r0, r1, m, n, sm, smcap, blockIdx.x, gridDim.x);
+  else matvec_cols_t<0, 0>(A, X, Y, R0, R1, r0, r1, m, n, sm, smcap, blockIdx.x, gridDim.x);
+}
+
+// Grid (bx, pairs): blockIdx.x = CTA within the pair, (y, z) = pair index in
+// the instance-major descriptor table.
+template <int MC, int NC, int MINB>
+__global__ void __launch_bounds__(256, MINB) matvec_batched_kernel(const MvPair *__restrict__ pairs, int np,
+                                                                   int smcap) {
   extern __shared__ double sm[];
-  const MvPair p = pairs[blockIdx.z * d + blockIdx.y];
-  const int k = p.k;
-  const int R0 = p.R[k], R1 = p.R[k + 1], r0 = p.r[k], r1 = p.r[k + 1];
-  matvec_core_cols(p.A, p.X, p.Y, R0, R1, r0, r1, p.m, p.n, sm, smcap);
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
-    p.ry[k] = R0 * r0;
-    if (p.last) p.ry[k + 1] = R1 * r1;
-    atomicAdd(&g_matvec_flops, 2ull * (unsigned long long)R0 * r0 * p.m * R1 * r1 * p.n);
+  const int pi = blockIdx.z * gridDim.y + blockIdx.y;
+  if (pi >= np) return;
+  const MvPair *pp = pairs + pi;
+  const int cta = blockIdx.x, ncta = gridDim.x;
+  const int k = pp->k;
+  const int *R = pp->R, *r = pp->r;
+  const int R0 = R[k], R1 = R[k + 1], r0 = r[k], r1 = r[k + 1];
+  matvec_cols_t<MC, NC>(pp->A, pp->X, pp->Y, R0, R1, r0, r1, pp->m, pp->n, sm, smcap, cta, ncta);
+  if (cta == 0 && threadIdx.x == 0) {
+    pp->ry[k] = R0 * r0;
+    if (pp->last) pp->ry[k + 1] = R1 * r1;
+    atomicAdd(&g_matvec_flops, 2ull * (unsigned long long)R0 * r0 * pp->m * R1 * r1 * pp->n);
   }
 }
 
@@ -257,13 +279,33 @@ tt_status matvec_batched_meta(int B, const MatMeta *A, const VecMeta *x, const V
       p.n = A[b].n[k];
       p.k = k;
       p.last = (k == d - 1);
+      p.blk0 = (int)std::min<long long>((long long)A[b].Rcap[k] * x[b].rcap[k] * x[b].rcap[k + 1] *
+                                            A[b].Rcap[k + 1] * A[b].m[k], 1LL << 30);   // work (sort key)
     }
   }
-  cudaMemcpyAsync(ws, host.data(), need, cudaMemcpyHostToDevice, s);
-  // columns per core are distributed over bx CTAs; aim for ~16 CTAs per SM in total
-  const char *ev = getenv("TT_MV_BX");
-  int bx = ev ? atoi(ev) : (4736 / (d * B) > 4 ? 4736 / (d * B) : 4);
-  bx = bx < 1 ? 1 : (bx > 256 ? 256 : bx);
+  // (kept in instance-major order: concurrent CTAs then write neighbouring
+  //  cores of one instance, which measured faster than a largest-first order)
+  // pinned staging so the table upload is a true async copy (the previous upload
+  // from this staging buffer must have completed before it is refilled)
+  static thread_local MvPair *stage = nullptr;
+  static thread_local size_t stage_cap = 0;
+  static thread_local cudaEvent_t stage_done = nullptr;
+  if (stage_done) cudaEventSynchronize(stage_done);
+  else cudaEventCreateWithFlags(&stage_done, cudaEventDisableTiming);
+  if (stage_cap < host.size()) {
+    if (stage) cudaFreeHost(stage);
+    if (cudaHostAlloc((void **)&stage, host.size() * sizeof(MvPair), cudaHostAllocDefault) != cudaSuccess) {
+      stage = nullptr;
+      stage_cap = 0;
+      return fail(TT_ERR_CUDA, "tt_matvec_batched: pinned staging allocation failed");
+    }
+    stage_cap = host.size();
+  }
+  std::memcpy(stage, host.data(), need);
+  cudaMemcpyAsync(ws, stage, need, cudaMemcpyHostToDevice, s);
+  cudaEventRecord(stage_done, s);
+  bool qtt = true;
+  for (const MvPair &p : host) qtt = qtt && p.m == 2 && p.n == 2;
   (void)mx;
   long long acap = 1;
   for (int b = 0; b < B; ++b)
@@ -272,7 +314,19 @@ tt_status matvec_batched_meta(int B, const MatMeta *A, const VecMeta *x, const V
       acap = c > acap ? c : acap;
     }
   const int smcap = acap <= 6144 ? (int)acap : 0;
-  matvec_batched_kernel<<<dim3(bx, d, B), 256, (size_t)smcap * sizeof(double), s>>>((const MvPair *)ws, d, smcap);
+  const int np = B * d;
+  const char *ev = getenv("TT_MV_MINB");
+  const int minb = ev ? atoi(ev) : 5;
+  const char *eb = getenv("TT_MV_BX");
+  int bx = eb ? atoi(eb) : 4;
+  bx = bx < 1 ? 1 : (bx > 256 ? 256 : bx);
+  const int gy = np < 65535 ? np : 65535;
+  const dim3 grid(bx, gy, (np + gy - 1) / gy);
+  const size_t shb = (size_t)smcap * sizeof(double);
+  if (!qtt) matvec_batched_kernel<0, 0, 1><<<grid, 256, shb, s>>>((const MvPair *)ws, np, smcap);
+  else if (minb >= 6) matvec_batched_kernel<2, 2, 6><<<grid, 256, shb, s>>>((const MvPair *)ws, np, smcap);
+  else if (minb == 5) matvec_batched_kernel<2, 2, 5><<<grid, 256, shb, s>>>((const MvPair *)ws, np, smcap);
+  else matvec_batched_kernel<2, 2, 4><<<grid, 256, shb, s>>>((const MvPair *)ws, np, smcap);
   return check_launch("tt_matvec_batched");
 }
 

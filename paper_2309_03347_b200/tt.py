@@ -174,16 +174,28 @@ def tt_matvec(A: TTMat, x: TTVec, y: TTVec, stream=None):
     return y
 
 
+class MatvecBatch:
+    """Marshalled arguments of one batched product (the ctypes descriptor arrays
+    and the workspace are built once; each call is one ABI call)."""
+
+    def __init__(self, As, xs, ys):
+        self.B = len(As)
+        self.keep = (As, xs, ys)
+        self.Ac = (_lib.tt_mat * self.B)(*[a._c for a in As])
+        self.xc = (_lib.tt_vec * self.B)(*[v._c for v in xs])
+        self.yc = (_lib.tt_vec * self.B)(*[v._c for v in ys])
+        nb = lib().tt_matvec_batched_workspace(self.B, self.Ac)
+        self.ws = torch.empty(max(int(nb), 256), dtype=torch.uint8, device=xs[0].device)
+
+    def __call__(self, stream=None):
+        check(lib().tt_matvec_batched(self.B, self.Ac, self.xc, self.yc, _ptr(self.ws), self.ws.numel(),
+                                      C.c_void_p(_stream(stream))))
+        return self.keep[2]
+
+
 def tt_matvec_batched(As, xs, ys, stream=None):
     """B independent products in one launch (C ABI tt_matvec_batched)."""
-    B = len(As)
-    Ac = (_lib.tt_mat * B)(*[a._c for a in As])
-    xc = (_lib.tt_vec * B)(*[v._c for v in xs])
-    yc = (_lib.tt_vec * B)(*[v._c for v in ys])
-    nb = lib().tt_matvec_batched_workspace(B, Ac)
-    ws = workspace(nb, xs[0].device)
-    check(lib().tt_matvec_batched(B, Ac, xc, yc, _ptr(ws), ws.numel(), C.c_void_p(_stream(stream))))
-    return ys
+    return MatvecBatch(As, xs, ys)(stream)
 
 
 def matvec_out(A: TTMat, x: TTVec) -> TTVec:
