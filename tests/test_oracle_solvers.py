@@ -143,3 +143,14 @@ def test_keff_sweep_3d_matches_dense():
     kd, _, _ = so.keff_dense_power(ops["H"] + 0.3 * ops["V"], ops["S"], ops["F"], tol=1e-13)
     ks, _, _ = T.keff_sweep_3d(prob, tol=1e-13, alpha=0.3)
     assert abs(ks - kd) <= 1e-11 * kd
+
+
+def test_c3_golden_file_reproduces():
+    """tests/golden/c3_keff.txt was written by make_c3_keff.py (oracle only): its
+    nv = 8 row is recomputed here."""
+    import os
+    path = os.path.join(os.path.dirname(__file__), "golden", "c3_keff.txt")
+    rows = {int(l.split()[0]): float(l.split()[1]) for l in open(path) if l.strip() and not l.startswith("#")}
+    assert set(rows) >= {8, 16, 32, 64}
+    k, _, _ = T.keff_sweep_3d(inputs.problem_c3(nv=8), tol=1e-11)
+    assert abs(k - rows[8]) <= 1e-12
