@@ -18,7 +18,7 @@ __host__ __device__ inline GemmDesc gd_make(int M, int N, int K, const double *A
   g.C = nullptr;
   g.dr = 1 << 30; g.dc = 1 << 30;
   g.s_r0 = 1; g.s_r1 = 0; g.s_c0 = 0; g.s_c1 = 0;
-  g.alpha = 1.0; g.beta = 0.0; g.alpha_dev = nullptr;
+  g.alpha = 1.0; g.beta = 0.0; g.alpha_dev = nullptr; g.skip = nullptr;
   return g;
 }
 __host__ __device__ inline void gd_scatter(GemmDesc &g, double *C, int dr, long long sr0, long long sr1, int dc,

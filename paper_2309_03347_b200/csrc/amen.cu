@@ -47,6 +47,7 @@ struct Dev {  // device-side view passed by value to the plan kernels
   double *dv;       // [8]: [0] sweep max residual, [1] eps
   int *limit;       // [d+1] per-bond truncation limit
   int m;            // GMRES restart
+  const int *gskip; // GMRES stop word: apply GEMMs after convergence are no-ops
 };
 
 __device__ GemmDesc gdd(int M, int N, int K, const double *A, long long lda, int tA, const double *B, long long ldb,
@@ -106,8 +107,9 @@ __global__ void plan_local(Dev D, int k) {
   descs_local_rhs(r0, b0, n, r1, b1, D.BL[k], Bk, D.BR[k + 1], D.rhs, D.T1, D.gd + 0);
   for (int j = -1; j < D.m; ++j) {
     const double *in = (j < 0) ? D.sol : D.V + (long long)j * D.ldv;
-    descs_local_apply(r0, R0, r0, n, n, r1, R1, r1, D.AL[k], Ak, D.AR[k + 1], in, D.w, D.T1, D.T2,
-                      D.gapp + 3 * (j + 1));
+    GemmDesc *ga = D.gapp + 3 * (j + 1);
+    descs_local_apply(r0, R0, r0, n, n, r1, R1, r1, D.AL[k], Ak, D.AR[k + 1], in, D.w, D.T1, D.T2, ga);
+    ga[0].skip = ga[1].skip = ga[2].skip = D.gskip;
   }
   D.cd[0] = cpy(N, 1, D.x.data + D.x.off[k], 1, N, D.sol, 1, N);
   D.cd[1] = cpy(N, 1, D.sol, 1, N, D.x.data + D.x.off[k], 1, N);
@@ -414,6 +416,7 @@ static tt_status carve_amen(const MatMeta &A, const VecMeta &b, const VecMeta &x
   D.dv = ar.take<double>(8);
   D.limit = ar.take<int>(TT_MAX_D + 1);
   P.gst = ar.take<GmState>(1);
+  D.gskip = P.gst ? &P.gst->stop : nullptr;
   P.H = ar.take<double>((size_t)(m + 1) * m);
   P.h1 = ar.take<double>(m + 1);
   P.h2 = ar.take<double>(m + 1);

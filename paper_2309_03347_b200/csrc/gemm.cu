@@ -98,6 +98,7 @@ __global__ void __launch_bounds__(32 * WM_ * WN_) gemm_dmma_kernel(const GemmDes
   double *sA = smem;
   double *sB = smem + STAGES * C::A_ELEMS;
   const GemmDesc g0 = descs[splits > 1 ? 0 : blockIdx.z];
+  if (g0.skip && *g0.skip) return;
   const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN;
   if (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && threadIdx.x == 0 && g0.M > 0 && g0.N > 0) {
     atomicAdd(&g_gemm_counters[0], 2ull * (unsigned long long)g0.M * g0.N * (g0.K > 0 ? g0.K : 0));
@@ -206,6 +207,7 @@ __global__ void __launch_bounds__(32 * WM_ * WN_) gemm_dmma_kernel(const GemmDes
 __global__ void gemm_splitk_reduce(const GemmDesc *__restrict__ descs, int splits, const double *__restrict__ partial,
                                    long long pld, long long pstride) {
   const GemmDesc g = descs[0];
+  if (g.skip && *g.skip) return;
   const long long total = (long long)g.M * g.N;
   double alpha = g.alpha;
   if (g.alpha_dev) alpha *= *g.alpha_dev;

@@ -50,7 +50,7 @@ __global__ void __launch_bounds__(RT) gm_start_kernel(GmState *st, const double 
     const double rel = bn > 0.0 ? beta / bn : 0.0;
     st->res = rel;
     s_done = (rel <= st->tol) || (beta == 0.0);
-    if (s_done) st->converged = 1;
+    if (s_done) { st->converged = 1; st->stop = 1; }
   }
   __syncthreads();
   if (s_done) return;
@@ -177,14 +177,46 @@ __global__ void gm_clear_stop_kernel(GmState *st) {
 
 }  // namespace
 
+// Lagged polling of the stop word: after every GM_CHUNK Arnoldi steps the word
+// is copied to pinned host memory behind an event; the host checks the copy of
+// the PREVIOUS chunk (complete while the current one runs), so the GPU never
+// drains.  Steps enqueued after the stop are no-ops (every kernel and the
+// apply GEMMs test the word).
+constexpr int GM_CHUNK = 6;
+
+struct PollSlots {
+  int *flag = nullptr;         // pinned [2]
+  cudaEvent_t ev[2] = {nullptr, nullptr};
+};
+thread_local PollSlots g_poll;
+
 tt_status gmres_solve(const GmresCtx &c, cudaStream_t s) {
   // c.apply(in, out) enqueues out = A in for device vectors.
   gm_init_kernel<<<1, 1, 0, s>>>(c.st, c.Nptr, c.m, c.tol);
   TT_TRY(check_launch("gm_init"));
+  if (c.poll && !g_poll.flag) {
+    if (cudaHostAlloc((void **)&g_poll.flag, 2 * sizeof(int), cudaHostAllocDefault) != cudaSuccess)
+      return fail(TT_ERR_CUDA, "gmres: pinned poll word allocation failed");
+    cudaEventCreateWithFlags(&g_poll.ev[0], cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&g_poll.ev[1], cudaEventDisableTiming);
+  }
   for (int cyc = 0; cyc < c.max_restarts; ++cyc) {
     TT_TRY(c.apply(c.x, c.w, -1));
     gm_start_kernel<<<1, RT, 0, s>>>(c.st, c.b, c.w, c.V);
+    int pending = -1;  // slot of the last enqueued poll copy
     for (int j = 0; j < c.m; ++j) {
+      if (c.poll && j > 0 && j % GM_CHUNK == 0) {
+        const int slot = (j / GM_CHUNK) & 1;
+        if (pending == slot) cudaEventSynchronize(g_poll.ev[slot]);   // (never: slots alternate)
+        cudaMemcpyAsync(&g_poll.flag[slot], &c.st->stop, sizeof(int), cudaMemcpyDeviceToHost, s);
+        cudaEventRecord(g_poll.ev[slot], s);
+        const int prev = slot ^ 1;
+        if (pending == prev) {
+          cudaEventSynchronize(g_poll.ev[prev]);
+          if (g_poll.flag[prev]) break;
+        }
+        pending = slot;
+      }
       TT_TRY(c.apply(c.V + (long long)j * c.ldv, c.w, j));
       gm_dots_kernel<<<j + 1, 256, 0, s>>>(c.st, c.V, c.ldv, c.w, c.h1, j, 0);
       gm_axpy_kernel<<<c.axpy_blocks, 256, 0, s>>>(c.st, c.V, c.ldv, c.w, c.h1, j);

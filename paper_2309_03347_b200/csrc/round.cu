@@ -79,7 +79,7 @@ __device__ GemmDesc gemm_desc(int M, int N, int K, const double *A, long long ld
   g.A = A; g.lda = lda;
   g.B = B; g.ldb = ldb;
   gemm_plain_c(g, C, ldc);
-  g.alpha = 1.0; g.beta = 0.0; g.alpha_dev = nullptr;
+  g.alpha = 1.0; g.beta = 0.0; g.alpha_dev = nullptr; g.skip = nullptr;
   return g;
 }
 

@@ -76,6 +76,7 @@ struct GemmDesc {
   long long s_r0, s_r1, s_c0, s_c1;
   double alpha, beta;
   const double *alpha_dev;  // if non-null, alpha *= *alpha_dev
+  const int *skip;          // if non-null and *skip != 0 the GEMM is a no-op (GMRES steps after convergence)
 };
 
 __host__ __device__ inline void gemm_plain_c(GemmDesc &g, double *C, long long ldc) {
