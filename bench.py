@@ -6,8 +6,10 @@
 A step is one pass of the whole hot path over one
 synthetic problem: one complete k-eff fixed-point solve (eqn:TT_k_eff_fixed_
 points) from psi_0 = 1, k_0 = 1 to |dk| < tol: every iteration
-runs exact matvec + rounding of S psi and F psi, the sum, the AMEn solve of
-H psi' = B (local apply, interfaces, GMRES, enrichment) and the k update.
+forms B = (S + F/k) psi by the fit-based product amen_mv (the paper's choice,
+P:1501-1506; TT_BENCH_MATVEC=exact selects exact products + rounding), runs
+the AMEn solve of H psi' = B (local apply, interfaces, GMRES, enrichment) and
+the k update.
 `value` = k-eff fixed-point iterations per second over all ranks (replicas,
 weak scaling: every rank solves its own copy, no data-path collective —
 DESIGN.md "Multi-GPU").  The contraction GFLOP/s (% of the measured FP64 DMMA
@@ -109,7 +111,8 @@ def c1_setup(device):
     z0 = inputs.random_tt(g, modes, [1, 4, 4, 4, 4, 1])
     psi0 = [np.ones((1, n, 1)) for n in modes]
     return {"prob": prob, "ops": ops, "modes": modes, "z0": z0, "psi0": psi0, "rmax": 64, "kick": 4,
-            "opts": dict(tol_k=1e-12, eps_round=1e-13, eps_solve=1e-12, rmax=64)}
+            "opts": dict(tol_k=1e-12, eps_round=1e-13, eps_solve=1e-12, rmax=64,
+                         matvec=os.environ.get("TT_BENCH_MATVEC", "amen_mv"))}
 
 
 def c1_step(st, device, host_inputs=None):
@@ -151,7 +154,7 @@ def oracle_c1_sample(iters=3):
     psi0 = [np.ones((1, n, 1)) for n in modes]
     t = time.perf_counter()
     so.keff_tt(tops["H"], tops["S"], tops["F"], psi0, z0, tol_k=0.0, eps_round=1e-13, eps_solve=1e-12,
-               max_outer=iters, dense_max=0)
+               max_outer=iters, dense_max=0, rmax=64, matvec=os.environ.get("TT_BENCH_MATVEC", "amen_mv"))
     dt = time.perf_counter() - t
     return iters / dt, dt
 
@@ -195,9 +198,10 @@ def main():
         line = {"impl": "reference", "metric": METRIC, "value": val, "unit": "iter/s", "n_gpus": args.gpus,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 / val,
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-                "data": "synthetic", "config": {"workload": "C1 (configs[0]) TT k-eff fixed point, 8^3 S2 G=1"},
+                "data": "synthetic", "config": {"workload": "C1 (configs[0]) TT k-eff fixed point, 8^3 S2 G=1, B by amen_mv"},
                 "cpu_baseline": {"value": val, "unit": "iter/s", "cores": cpu_cores(), "kind": "oracle",
-                                 "sample": "fixed-point iterations of oracle keff_tt on C1 (GMRES local solves)"},
+                                 "sample": "fixed-point iterations of oracle keff_tt on C1 (amen_mv products, GMRES "
+                                           "local solves)"},
                 "e2e": {"value": val, "unit": "iter/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
         print(json.dumps(line))
         return
@@ -279,7 +283,7 @@ def main():
             "warmup": args.warmup, "ms_per_step": dev_ms_max / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": "C1 (configs[0]): TT k-eff fixed point to |dk|<1e-12, 8^3 vertices, S2, G=1, "
-                                   "modes (8,8,8,8,1), rmax 64",
+                                   "modes (8,8,8,8,1), rmax 64, B by " + st["opts"]["matvec"],
                        "l2": "256 MB flush between timed steps", "parallelism": f"replicas x{world}"},
             "iters_per_step": iters_total / args.steps,
             "contraction_gflops": contr_gflops,
@@ -293,7 +297,7 @@ def main():
     if rank == 0 and not args.no_cpu_baseline:
         v, dt = oracle_c1_sample(iters=3)
         line["cpu_baseline"] = {"value": v, "unit": "iter/s", "cores": cpu_cores(), "kind": "oracle",
-                                "sample": f"3 fixed-point iterations of oracle keff_tt on C1 ({dt:.1f} s)"}
+                                "sample": f"3 fixed-point iterations of oracle keff_tt on C1, amen_mv products ({dt:.1f} s)"}
     if rank == 0:
         print(json.dumps(line))
     if dist:

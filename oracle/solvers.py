@@ -361,10 +361,13 @@ def amen_mv(A, b, y0, z0, eps=1e-8, max_sweeps=20, rmax=10**9):
 
 
 def keff_tt(H, S, F, psi0, z0, k0=1.0, tol_k=1e-10, max_outer=200, eps_round=1e-12,
-            eps_solve=1e-11, rmax=10**9, max_sweeps=20, dense_max=2000, verbose=False):
+            eps_solve=1e-11, rmax=10**9, max_sweeps=20, dense_max=2000, verbose=False, matvec="exact",
+            mv_max_sweeps=10):
     """Eq. TT_k_eff_fixed_points with readings Z16-Z19:
         B = round(S Psi + (1/k) F Psi);  H Psi' = B (AMEn, warm start Psi);
         k' = k <f, Psi'> / <f, Psi>  with f = F^T 1  (Z18);  Psi <- Psi'/||Psi'||.
+    matvec="amen_mv": B = amen_mv(S + (1/k) F, Psi) to eps_round, warm-started
+    from the previous B (the paper's product).
     Returns (k, Psi, history)."""
     modes = [c.shape[2] for c in F]
     ones = [np.ones((1, n, 1)) for n in modes]
@@ -375,10 +378,17 @@ def keff_tt(H, S, F, psi0, z0, k0=1.0, tol_k=1e-10, max_outer=200, eps_round=1e-
     k = k0
     s_old = ott.tt_dot(f, psi)
     hist = []
+    B = psi
+    rows = [c.shape[1] for c in S]
+    cols = [c.shape[2] for c in S]
     for tau in range(1, max_outer + 1):
-        SP, _ = ott.tt_round(ott.tt_matvec_fast(S, psi), eps_round, rmax)
-        FP, _ = ott.tt_round(ott.tt_matvec_fast(F, psi), eps_round, rmax)
-        B, _ = ott.tt_round(ott.tt_add(SP, ott.tt_scale(FP, 1.0 / k)), eps_round, rmax)
+        if matvec == "amen_mv":
+            SF = ott.tt_as_ttm(ott.tt_add(ott.ttm_as_tt(S), ott.tt_scale(ott.ttm_as_tt(F), 1.0 / k)), rows, cols)
+            B, _ = amen_mv(SF, psi, B, z0, eps=eps_round, max_sweeps=mv_max_sweeps, rmax=rmax)
+        else:
+            SP, _ = ott.tt_round(ott.tt_matvec_fast(S, psi), eps_round, rmax)
+            FP, _ = ott.tt_round(ott.tt_matvec_fast(F, psi), eps_round, rmax)
+            B, _ = ott.tt_round(ott.tt_add(SP, ott.tt_scale(FP, 1.0 / k)), eps_round, rmax)
         new, info = amen_solve(H, B, psi, z0, eps=eps_solve, max_sweeps=max_sweeps, rmax=rmax,
                                dense_max=dense_max)
         s_new = ott.tt_dot(f, new)

@@ -14,6 +14,7 @@
 // GEMM / QR / SVD / copy descriptors; the host only enqueues launches (it polls
 // the GMRES flag once per cycle and the sweep residual once per sweep).
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -327,6 +328,8 @@ struct AmenCtx {
   int pc, zcm, nmax;
   GmState *gst;
   double *H, *h1, *h2;
+  double *gpart;
+  unsigned int *gbar;
   char *orth_base;
   size_t orth_cap;
   double *split;
@@ -420,6 +423,8 @@ static tt_status carve_amen(const MatMeta &A, const VecMeta &b, const VecMeta &x
   P.H = ar.take<double>((size_t)(m + 1) * m);
   P.h1 = ar.take<double>(m + 1);
   P.h2 = ar.take<double>(m + 1);
+  P.gpart = ar.take<double>(gmres_fused_part_doubles(256));
+  P.gbar = ar.take<unsigned int>(4);
   // orthogonalisation scratch (x or z)
   Arena c1, c2;
   orth_meta(x, -1, nullptr, c1, nullptr);
@@ -527,6 +532,13 @@ tt_status amen_solve_meta(const MatMeta &A, const VecMeta &b, const VecMeta &x, 
   int hflag = 0;
   gc.host_flag = &hflag;
   gc.apply = [&](const double *, double *, int j) -> tt_status { return launch_caps(D.gapp + 3 * (j + 1), appc, 2, 3); };
+  if (!std::getenv("TT_GMRES_UNFUSED")) {
+    gc.gapp = D.gapp;
+    gc.part = P.gpart;
+    gc.bar = P.gbar;
+    gc.split = P.split;
+    gc.split_elems = GEMM_SPLIT_SCRATCH / 8;
+  }
   int dir = +1, sweep = 0;
   double hres = 0.0;
   for (sweep = 0; sweep < o.max_sweeps; ++sweep) {

@@ -8,6 +8,7 @@
 // deterministic slice reduction.
 #include <cstdlib>
 
+#include "gmres.h"
 #include "tt_common.cuh"
 
 namespace tt {
@@ -89,26 +90,19 @@ __device__ __forceinline__ void load_tile(double *sa, double *sb, const GemmDesc
 // splits > 1: split-K; CTA z computes the K-slice z and writes its raw partial
 // product to partial + z * pstride (column-major, ld = pld); gemm_splitk_reduce
 // sums the slices and applies the epilogue (deterministic order).
+// One output tile (m0, n0) of the K-slice z (splits > 1) or of the whole K.
 template <int BM, int BN, int BK, int WM_, int WN_, int STAGES>
-__global__ void __launch_bounds__(32 * WM_ * WN_) gemm_dmma_kernel(const GemmDesc *__restrict__ descs, int splits,
-                                                                   double *__restrict__ partial, long long pld,
-                                                                   long long pstride) {
+__device__ __forceinline__ void gemm_tile(const GemmDesc &g0, int m0, int n0, int z, int splits,
+                                          double *__restrict__ partial, long long pld, long long pstride,
+                                          double *smem) {
   using C = Cfg<BM, BN, BK, WM_, WN_, STAGES>;
-  extern __shared__ __align__(16) double smem[];
   double *sA = smem;
   double *sB = smem + STAGES * C::A_ELEMS;
-  const GemmDesc g0 = descs[splits > 1 ? 0 : blockIdx.z];
-  if (g0.skip && *g0.skip) return;
-  const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN;
-  if (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && threadIdx.x == 0 && g0.M > 0 && g0.N > 0) {
-    atomicAdd(&g_gemm_counters[0], 2ull * (unsigned long long)g0.M * g0.N * (g0.K > 0 ? g0.K : 0));
-    atomicAdd(&g_gemm_counters[1], 1ull);
-  }
   if (m0 >= g0.M || n0 >= g0.N) return;
   GemmDesc g = g0;
   if (splits > 1) {
     const int kc = ((g0.K + splits - 1) / splits + BK - 1) / BK * BK;
-    const int kbeg = blockIdx.z * kc;
+    const int kbeg = z * kc;
     const int kend = min(g0.K, kbeg + kc);
     g.K = kend > kbeg ? kend - kbeg : 0;
     g.A = g0.transA ? g0.A + kbeg : g0.A + (long long)kbeg * g0.lda;
@@ -158,7 +152,7 @@ __global__ void __launch_bounds__(32 * WM_ * WN_) gemm_dmma_kernel(const GemmDes
   }
   cp_async_wait<0>();
   if (splits > 1) {
-    double *P = partial + (long long)blockIdx.z * pstride;
+    double *P = partial + (long long)z * pstride;
 #pragma unroll
     for (int i = 0; i < C::TM; ++i) {
       const int r = m0 + wm + i * 8 + (lane >> 2);
@@ -202,6 +196,21 @@ __global__ void __launch_bounds__(32 * WM_ * WN_) gemm_dmma_kernel(const GemmDes
       }
     }
   }
+}
+
+template <int BM, int BN, int BK, int WM_, int WN_, int STAGES>
+__global__ void __launch_bounds__(32 * WM_ * WN_) gemm_dmma_kernel(const GemmDesc *__restrict__ descs, int splits,
+                                                                   double *__restrict__ partial, long long pld,
+                                                                   long long pstride) {
+  extern __shared__ __align__(16) double smem[];
+  const GemmDesc g0 = descs[splits > 1 ? 0 : blockIdx.z];
+  if (g0.skip && *g0.skip) return;
+  if (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && threadIdx.x == 0 && g0.M > 0 && g0.N > 0) {
+    atomicAdd(&g_gemm_counters[0], 2ull * (unsigned long long)g0.M * g0.N * (g0.K > 0 ? g0.K : 0));
+    atomicAdd(&g_gemm_counters[1], 1ull);
+  }
+  gemm_tile<BM, BN, BK, WM_, WN_, STAGES>(g0, blockIdx.x * BM, blockIdx.y * BN, blockIdx.z, splits, partial, pld,
+                                          pstride, smem);
 }
 
 __global__ void gemm_splitk_reduce(const GemmDesc *__restrict__ descs, int splits, const double *__restrict__ partial,
@@ -286,6 +295,230 @@ tt_status launch_variant(const GemmDesc *descs_dev, int count, int Mcap, int Nca
   return check_launch("gemm_dmma");
 }
 
+// ------------------------------------------------ fused GMRES Arnoldi steps ---
+// One cooperative persistent launch runs Arnoldi steps j0..j1-1 of the device
+// GMRES (gmres.cu) for the AMEn local system: per step the three chained
+// local-apply GEMM stages (descriptors gapp[3(j+1)+s], DMMA tiles distributed
+// over the CTAs, split-K with an in-kernel reduction when a stage has few
+// tiles), then CGS2 (two dot/axpy passes), the norm, the Givens update and the
+// normalisation of the new basis vector.  Every CTA owns a slice of the local
+// vector; the cross-CTA sums are reduced redundantly (same order) by every
+// CTA, so all CTAs take identical decisions and only grid barriers separate
+// the phases (6-7 per step instead of ~8 kernel launches).
+constexpr int GF_THREADS = 128;
+using GF = Cfg<64, 64, 16, 2, 2, 2>;
+constexpr int GF_LD = GM_MAX_M + 2;
+
+__device__ __forceinline__ void gbar(unsigned int *bar, unsigned int nblocks) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    volatile unsigned int *gen = bar + 1;
+    const unsigned int g = *gen;
+    __threadfence();
+    if (atomicAdd(bar, 1u) == nblocks - 1) {
+      bar[0] = 0;
+      __threadfence();
+      atomicAdd(bar + 1, 1u);
+    } else {
+      const long long t0 = clock64();
+      while (*gen == g) {
+        if (clock64() - t0 > 8000000000LL) __trap();   // never hang the device
+      }
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+struct GmChunkArgs {
+  GmState *st;
+  const GemmDesc *gapp;
+  double *V;
+  long long ldv;
+  double *w;
+  double *part;          // [3][G][GF_LD]
+  double *split;
+  long long split_elems;
+  unsigned int *bar;
+  int j0, j1;
+};
+
+__global__ void __launch_bounds__(GF_THREADS) gm_chunk_kernel(GmChunkArgs a) {
+  extern __shared__ __align__(16) double smem[];
+  __shared__ double h1s[GF_LD], h2s[GF_LD], css[GF_LD], sns[GF_LD];
+  __shared__ double red[GF_THREADS / 32 + 4];
+  const int G = gridDim.x;
+  GmState *st = a.st;
+  if (st->converged || st->stop) return;   // uniform: written by earlier launches
+  const int N = st->N, m = st->m;
+  const double tol = st->tol, bnorm = st->bnorm;
+  const int per = (N + G - 1) / G;
+  const int lo = min(N, (int)blockIdx.x * per), hi = min(N, lo + per);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int NW = GF_THREADS / 32;
+  double *part1 = a.part, *part2 = a.part + (size_t)G * GF_LD, *part3 = a.part + 2 * (size_t)G * GF_LD;
+  double *w = a.w;
+  for (int j = a.j0; j < a.j1 && j < m; ++j) {
+    if (j > a.j0) gbar(a.bar, G);            // V[:, j] of the previous step complete
+    // ---- w = A V[:, j] (three chained GEMM stages)
+    for (int sidx = 0; sidx < 3; ++sidx) {
+      const GemmDesc g = a.gapp[3 * (j + 1) + sidx];
+      if (g.M <= 0 || g.N <= 0) continue;
+      const int tm = (g.M + 63) / 64, tn = (g.N + 63) / 64, T = tm * tn;
+      int splits = 1;
+      if (T * 2 <= G && g.K >= 256) {
+        splits = min(G / T, min(g.K / 128, 16));
+        while (splits > 1 && (long long)splits * g.M * g.N > a.split_elems) --splits;
+      }
+      if (blockIdx.x == 0 && tid == 0) {
+        atomicAdd(&g_gemm_counters[0], 2ull * (unsigned long long)g.M * g.N * (g.K > 0 ? g.K : 0));
+        atomicAdd(&g_gemm_counters[1], 1ull);
+      }
+      for (int t = blockIdx.x; t < T * splits; t += G) {
+        const int z = t / T, tt = t - z * T;
+        gemm_tile<64, 64, 16, 2, 2, 2>(g, (tt % tm) * 64, (tt / tm) * 64, z, splits, a.split, g.M,
+                                       (long long)g.M * g.N, smem);
+        __syncthreads();
+      }
+      gbar(a.bar, G);
+      if (splits > 1) {
+        const long long total = (long long)g.M * g.N, ps = total;
+        double alpha = g.alpha;
+        if (g.alpha_dev) alpha *= *g.alpha_dev;
+        for (long long e = (long long)blockIdx.x * GF_THREADS + tid; e < total; e += (long long)G * GF_THREADS) {
+          const int r = (int)(e % g.M), c = (int)(e / g.M);
+          double sum = 0.0;
+          for (int z = 0; z < splits; ++z) sum += a.split[z * ps + e];
+          const long long addr = (long long)(r % g.dr) * g.s_r0 + (long long)(r / g.dr) * g.s_r1 +
+                                 (long long)(c % g.dc) * g.s_c0 + (long long)(c / g.dc) * g.s_c1;
+          double v = alpha * sum;
+          if (g.beta != 0.0) v += g.beta * g.C[addr];
+          g.C[addr] = v;
+        }
+        gbar(a.bar, G);
+      }
+    }
+    // ---- CGS2 pass 1: slice dots
+    double *my1 = part1 + (size_t)blockIdx.x * GF_LD;
+    for (int i = warp; i <= j; i += NW) {
+      const double *vi = a.V + (long long)i * a.ldv;
+      double sacc = 0.0;
+      for (int e = lo + lane; e < hi; e += 32) sacc = fma(vi[e], w[e], sacc);
+      sacc = warp_sum(sacc);
+      if (lane == 0) my1[i] = sacc;
+    }
+    gbar(a.bar, G);
+    for (int i = warp; i <= j; i += NW) {      // cross-CTA sums: one warp per entry, fixed order
+      double sacc = 0.0;
+      for (int c = lane; c < G; c += 32) sacc += part1[(size_t)c * GF_LD + i];
+      sacc = warp_sum(sacc);
+      if (lane == 0) h1s[i] = sacc;
+    }
+    __syncthreads();
+    for (int e = lo + tid; e < hi; e += GF_THREADS) {
+      double x = w[e];
+      for (int i = 0; i <= j; ++i) x = fma(-h1s[i], a.V[(long long)i * a.ldv + e], x);
+      w[e] = x;
+    }
+    __syncthreads();
+    // ---- pass 2 on the updated slice
+    double *my2 = part2 + (size_t)blockIdx.x * GF_LD;
+    for (int i = warp; i <= j; i += NW) {
+      const double *vi = a.V + (long long)i * a.ldv;
+      double sacc = 0.0;
+      for (int e = lo + lane; e < hi; e += 32) sacc = fma(vi[e], w[e], sacc);
+      sacc = warp_sum(sacc);
+      if (lane == 0) my2[i] = sacc;
+    }
+    // rotations and g[j] of earlier steps, read before CTA 0 rewrites them in this step
+    for (int i = tid; i < j; i += GF_THREADS) { css[i] = st->cs[i]; sns[i] = st->sn[i]; }
+    const double gj = st->g[j];
+    gbar(a.bar, G);
+    for (int i = warp; i <= j; i += NW) {
+      double sacc = 0.0;
+      for (int c = lane; c < G; c += 32) sacc += part2[(size_t)c * GF_LD + i];
+      sacc = warp_sum(sacc);
+      if (lane == 0) h2s[i] = sacc;
+    }
+    __syncthreads();
+    double nrm = 0.0;
+    for (int e = lo + tid; e < hi; e += GF_THREADS) {
+      double x = w[e];
+      for (int i = 0; i <= j; ++i) x = fma(-h2s[i], a.V[(long long)i * a.ldv + e], x);
+      w[e] = x;
+      nrm = fma(x, x, nrm);
+    }
+    nrm = warp_sum(nrm);
+    if (lane == 0) red[warp] = nrm;
+    __syncthreads();
+    if (tid == 0) {
+      double t = 0.0;
+      for (int q = 0; q < NW; ++q) t += red[q];
+      part3[(size_t)blockIdx.x * GF_LD] = t;
+    }
+    gbar(a.bar, G);
+    // ---- norm, Givens (identical in every CTA), normalisation
+    if (warp == 0) {
+      double hn2 = 0.0;
+      for (int c = lane; c < G; c += 32) hn2 += part3[(size_t)c * GF_LD];
+      hn2 = warp_sum(hn2);
+      if (lane == 0) red[2] = hn2;
+    }
+    __syncthreads();
+    const double hn = sqrt(red[2]);
+    // H column j: h1 + h2, then the earlier rotations
+    if (tid == 0) {
+      double col_j = 0.0, col_j1 = hn;
+      double *H = st->H;
+      // rotate entries 0..j (sequential; j <= GM_MAX_M)
+      double prev = h1s[0] + h2s[0];
+      for (int i = 0; i < j; ++i) {
+        const double b = h1s[i + 1] + h2s[i + 1];
+        const double ra = css[i] * prev + sns[i] * b;
+        const double rb = -sns[i] * prev + css[i] * b;
+        if (blockIdx.x == 0) H[i + (m + 1) * j] = ra;
+        prev = rb;
+      }
+      col_j = prev;
+      const double den = hypot(col_j, col_j1);
+      const double c = den > 0.0 ? col_j / den : 1.0, sn = den > 0.0 ? col_j1 / den : 0.0;
+      const double gnew = -sn * gj;
+      const double rel = bnorm > 0.0 ? fabs(gnew) / bnorm : 0.0;
+      int stop = 0;
+      if (rel <= tol || hn == 0.0 || j + 1 >= m) stop = 1;
+      if (!(rel == rel)) stop = 2;
+      if (blockIdx.x == 0) {
+        H[j + (m + 1) * j] = den;
+        H[j + 1 + (m + 1) * j] = 0.0;
+        st->cs[j] = c;
+        st->sn[j] = sn;
+        st->g[j + 1] = gnew;
+        st->g[j] = c * gj;
+        st->jdone = j + 1;
+        st->res = rel;
+        if (stop == 2) st->nan = 1;
+        st->stop = stop ? 1 : 0;
+      }
+      red[0] = stop ? 1.0 : 0.0;
+      red[1] = hn;
+    }
+    __syncthreads();
+    const bool stop = red[0] != 0.0;
+    if (red[1] > 0.0) {
+      const double inv = 1.0 / red[1];
+      double *vn = a.V + (long long)(j + 1) * a.ldv;
+      for (int e = lo + tid; e < hi; e += GF_THREADS) vn[e] = w[e] * inv;
+    }
+    if (stop) break;
+  }
+}
+
 }  // namespace
 
 void set_gemm_scratch(double *ptr, size_t bytes) {
@@ -313,6 +546,42 @@ void gemm_counters(unsigned long long *out, int reset) {
     unsigned long long z[2] = {0, 0};
     cudaMemcpyToSymbol(g_gemm_counters, z, sizeof(z));
   }
+}
+
+}  // namespace tt
+
+namespace tt {
+
+size_t gmres_fused_part_doubles(int G) { return (size_t)3 * G * GF_LD; }
+
+int gmres_fused_grid() {
+  static int G = 0;
+  if (!G) {
+    int dev = 0, sms = 0, occ = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaFuncSetAttribute(gm_chunk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GF::SMEM);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, gm_chunk_kernel, GF_THREADS, GF::SMEM);
+    const char *e = std::getenv("TT_GF_GRID");
+    G = (occ >= 1) ? (e ? std::atoi(e) : sms) : -1;
+    if (G > occ * sms || G > 256) G = occ * sms < 256 ? occ * sms : 256;
+  }
+  return G;
+}
+
+tt_status launch_gmres_chunk(GmState *st, const GemmDesc *gapp, double *V, long long ldv, double *w, double *part,
+                             double *split, long long split_elems, unsigned int *bar, int j0, int j1,
+                             cudaStream_t s) {
+  const int G = gmres_fused_grid();
+  if (G <= 0) return fail(TT_ERR_CUDA, "gmres: fused step kernel cannot be co-resident");
+  GmChunkArgs a;
+  a.st = st; a.gapp = gapp; a.V = V; a.ldv = ldv; a.w = w; a.part = part; a.split = split;
+  a.split_elems = split_elems; a.bar = bar; a.j0 = j0; a.j1 = j1;
+  void *args[] = {(void *)&a};
+  cudaError_t e = cudaLaunchCooperativeKernel((const void *)gm_chunk_kernel, dim3(G), dim3(GF_THREADS), args,
+                                              GF::SMEM, s);
+  if (e != cudaSuccess) return fail(TT_ERR_CUDA, std::string("gm_chunk: ") + cudaGetErrorString(e));
+  return TT_OK;
 }
 
 }  // namespace tt

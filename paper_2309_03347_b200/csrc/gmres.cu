@@ -183,6 +183,7 @@ __global__ void gm_clear_stop_kernel(GmState *st) {
 // drains.  Steps enqueued after the stop are no-ops (every kernel and the
 // apply GEMMs test the word).
 constexpr int GM_CHUNK = 6;
+constexpr int GM_FCHUNK = 5;   // Arnoldi steps per fused launch
 
 struct PollSlots {
   int *flag = nullptr;         // pinned [2]
@@ -200,11 +201,31 @@ tt_status gmres_solve(const GmresCtx &c, cudaStream_t s) {
     cudaEventCreateWithFlags(&g_poll.ev[0], cudaEventDisableTiming);
     cudaEventCreateWithFlags(&g_poll.ev[1], cudaEventDisableTiming);
   }
+  const bool fused = c.gapp && c.part && c.bar && gmres_fused_grid() > 0;
+  if (fused) cudaMemsetAsync(c.bar, 0, 2 * sizeof(unsigned int), s);
   for (int cyc = 0; cyc < c.max_restarts; ++cyc) {
     TT_TRY(c.apply(c.x, c.w, -1));
     gm_start_kernel<<<1, RT, 0, s>>>(c.st, c.b, c.w, c.V);
     int pending = -1;  // slot of the last enqueued poll copy
-    for (int j = 0; j < c.m; ++j) {
+    if (fused) {
+      for (int j0 = 0, q = 0; j0 < c.m; j0 += GM_FCHUNK, ++q) {
+        TT_TRY(launch_gmres_chunk(c.st, c.gapp, c.V, c.ldv, c.w, c.part, c.split, c.split_elems, c.bar, j0,
+                                  j0 + GM_FCHUNK < c.m ? j0 + GM_FCHUNK : c.m, s));
+        if (c.poll) {
+          // copy this chunk's stop word, then wait for the PREVIOUS chunk's copy
+          // (that chunk finished while this one runs): the GPU never drains
+          const int slot = q & 1, prev = slot ^ 1;
+          cudaMemcpyAsync(&g_poll.flag[slot], &c.st->stop, sizeof(int), cudaMemcpyDeviceToHost, s);
+          cudaEventRecord(g_poll.ev[slot], s);
+          if (pending == prev) {
+            cudaEventSynchronize(g_poll.ev[prev]);
+            if (g_poll.flag[prev]) break;
+          }
+          pending = slot;
+        }
+      }
+    }
+    for (int j = 0; j < (fused ? 0 : c.m); ++j) {
       if (c.poll && j > 0 && j % GM_CHUNK == 0) {
         const int slot = (j / GM_CHUNK) & 1;
         if (pending == slot) cudaEventSynchronize(g_poll.ev[slot]);   // (never: slots alternate)

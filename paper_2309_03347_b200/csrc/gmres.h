@@ -33,8 +33,20 @@ struct GmresCtx {
   int *host_flag;        // pinned host int for polling
   // enqueue out = A in; j = basis index (-1 for x)
   std::function<tt_status(const double *, double *, int)> apply;
+  // fused Arnoldi steps (gemm.cu gm_chunk_kernel): the apply GEMM descriptors of
+  // basis vector j are gapp[3(j+1) .. 3(j+1)+2]; NULL = one launch per operation
+  const GemmDesc *gapp = nullptr;
+  double *part = nullptr;        // gmres_fused_part_doubles(grid) doubles
+  unsigned int *bar = nullptr;   // [2] grid barrier words (zeroed by gmres_solve)
+  double *split = nullptr;       // split-K scratch
+  long long split_elems = 0;
 };
 
 tt_status gmres_solve(const GmresCtx &c, cudaStream_t s);
+
+size_t gmres_fused_part_doubles(int G);
+int gmres_fused_grid();
+tt_status launch_gmres_chunk(GmState *st, const GemmDesc *gapp, double *V, long long ldv, double *w, double *part,
+                             double *split, long long split_elems, unsigned int *bar, int j0, int j1, cudaStream_t s);
 
 }  // namespace tt

@@ -154,3 +154,17 @@ def test_c3_golden_file_reproduces():
     assert set(rows) >= {8, 16, 32, 64}
     k, _, _ = T.keff_sweep_3d(inputs.problem_c3(nv=8), tol=1e-11)
     assert abs(k - rows[8]) <= 1e-12
+
+
+def test_keff_tt_amen_mv_matches_dense_small():
+    """keff_tt with B by the fit-based product reaches the dense k."""
+    prob = copy.deepcopy(inputs.problem_c1()); prob["nv"] = 4
+    ops = T.dense_operators(prob)
+    kd, _, _ = so.keff_dense_power(ops["H"], ops["S"], ops["F"], tol=1e-13)
+    tops = T.tt_operators(prob)
+    modes = [4, 4, 4, 8, 1]
+    g = inputs.rng(34)
+    psi0 = [np.ones((1, n, 1)) for n in modes]
+    k, psi, hist = so.keff_tt(tops["H"], tops["S"], tops["F"], psi0, _z0(g, modes, 4), tol_k=1e-12,
+                              eps_round=1e-13, eps_solve=1e-12, matvec="amen_mv")
+    assert abs(k - kd) / kd < 1e-9
