@@ -85,6 +85,16 @@ const char *tt_version(void);
  * out[4] number of GEMM calls.  reset != 0 zeroes them after reading. */
 void tt_counters(uint64_t *out /* [5] */, int32_t reset);
 
+/* Live timing of the fused GMRES Arnoldi-step kernel (the dominant kernel of
+ * the k-eff solves; used by bench.py for its roofline line).  enable != 0:
+ * every later launch of the kernel by this thread is bracketed by CUDA events
+ * on its stream.  _read synchronises those events and returns the number of
+ * launches, their summed duration (ms) and flops[3] = {local-apply GEMM flops,
+ * CGS2/norm vector flops, Arnoldi steps executed} of those launches, then
+ * resets (the flop counters count every fused launch since the last read). */
+void tt_fused_profile(int32_t enable);
+void tt_fused_profile_read(int64_t *launches, double *ms, double *flops /* [3] */);
+
 /* ---------------------------------------------------------------- a1 ---
  * tt_matvec: exact TT-matrix x TT-vector product ("explicit and
  * exact algorithm").  For every core, independently,

@@ -66,6 +66,8 @@ SIG = {
     "tt_last_error": (C.c_char_p, []),
     "tt_version": (C.c_char_p, []),
     "tt_counters": (None, [C.POINTER(C.c_uint64), I32]),
+    "tt_fused_profile": (None, [I32]),
+    "tt_fused_profile_read": (None, [C.POINTER(C.c_int64), C.POINTER(C.c_double), C.POINTER(C.c_double)]),
     "tt_matvec": (I32, [C.POINTER(tt_mat), C.POINTER(tt_vec), C.POINTER(tt_vec), P]),
     "tt_matvec_batched_workspace": (C.c_size_t, [I32, C.POINTER(tt_mat)]),
     "tt_matvec_batched": (I32, [I32, C.POINTER(tt_mat), C.POINTER(tt_vec), C.POINTER(tt_vec), P, C.c_size_t, P]),

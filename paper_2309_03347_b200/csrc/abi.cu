@@ -138,6 +138,19 @@ void matvec_counters(unsigned long long *out, int reset);
 void linalg_counters(unsigned long long *out, int reset);
 }
 
+namespace tt {
+void fused_profile(int enable);
+void fused_profile_read(long long *launches, double *ms, double *flops);
+}
+
+extern "C" void tt_fused_profile(int32_t enable) { tt::fused_profile(enable); }
+
+extern "C" void tt_fused_profile_read(int64_t *launches, double *ms, double *flops) {
+  long long l = 0;
+  tt::fused_profile_read(&l, ms, flops);
+  if (launches) *launches = l;
+}
+
 extern "C" void tt_counters(uint64_t *out, int32_t reset) {
   unsigned long long g[2] = {0, 0}, mv = 0, la[2] = {0, 0};
   cudaDeviceSynchronize();

@@ -539,6 +539,7 @@ tt_status amen_solve_meta(const MatMeta &A, const VecMeta &b, const VecMeta &x, 
     gc.split = P.split;
     gc.split_elems = GEMM_SPLIT_SCRATCH / 8;
   }
+  const bool cluster_off = std::getenv("TT_GMRES_NOCLUSTER") != nullptr;
   int dir = +1, sweep = 0;
   double hres = 0.0;
   for (sweep = 0; sweep < o.max_sweeps; ++sweep) {
@@ -550,6 +551,17 @@ tt_status amen_solve_meta(const MatMeta &A, const VecMeta &b, const VecMeta &x, 
       const int n = x.n[k];
       descs_local_rhs(xc[k], bc[k], n, xc[k + 1], bc[k + 1], 0, 0, 0, 0, 0, appc.g + 0);
       descs_local_apply(xc[k], Rc[k], xc[k], n, n, xc[k + 1], Rc[k + 1], xc[k + 1], 0, 0, 0, 0, 0, 0, 0, appc.g + 2);
+      {  // small local systems: fused Arnoldi steps inside one thread-block cluster
+        int tiles = 0;
+        for (int q = 2; q < 5; ++q) {
+          const int t = ((appc.g[q].M + 63) / 64) * ((appc.g[q].N + 63) / 64);
+          tiles = t > tiles ? t : tiles;
+        }
+        const long long nloc = (long long)xc[k] * n * xc[k + 1];
+        // at capacity sizes the cluster certainly applies: launch it alone; otherwise launch
+        // both variants and let the device-resident sizes pick one (the other exits at once)
+        gc.cluster = cluster_off ? 0 : ((tiles <= 2 * gmres_cluster_size() && nloc <= 16384) ? 1 : 2);
+      }
       plan_local<<<1, 1, 0, s>>>(D, k);
       TT_TRY(launch_copy(D.cd, 1, P.Ncap, s));
       TT_TRY(launch_copy(D.cd + 2, 1, P.Ncap, s));

@@ -7,6 +7,8 @@
 // sizes can follow device-resident ranks; optional split-K with a
 // deterministic slice reduction.
 #include <cstdlib>
+#include <string>
+#include <vector>
 
 #include "gmres.h"
 #include "tt_common.cuh"
@@ -15,6 +17,8 @@ namespace tt {
 
 // algorithmic flop counter of the contraction GEMMs (2 M N K per call) and launch count
 __device__ unsigned long long g_gemm_counters[2];
+// fused GMRES step kernel: [0] local-apply GEMM flops, [1] CGS2 / norm vector flops, [2] steps
+__device__ unsigned long long g_gm_counters[3];
 
 namespace {
 
@@ -347,8 +351,24 @@ struct GmChunkArgs {
   long long split_elems;
   unsigned int *bar;
   int j0, j1;
+  int mode;              // 0 grid only, 1 cluster only, 2 device decides (both variants launched)
+  int cs;                // cluster size (for the device-side choice)
 };
 
+// Phase barrier: whole cooperative grid (atomics in global memory) or one
+// thread-block cluster (hardware barrier.cluster with release/acquire).
+template <bool CLUSTER>
+__device__ __forceinline__ void phase_sync(unsigned int *bar, unsigned int nblocks) {
+  if (CLUSTER) {
+    // release/acquire at cluster scope orders the global-memory partials too
+    asm volatile("barrier.cluster.arrive.release.aligned;\n"
+                 "barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+  } else {
+    gbar(bar, nblocks);
+  }
+}
+
+template <bool CLUSTER>
 __global__ void __launch_bounds__(GF_THREADS) gm_chunk_kernel(GmChunkArgs a) {
   extern __shared__ __align__(16) double smem[];
   __shared__ double h1s[GF_LD], h2s[GF_LD], css[GF_LD], sns[GF_LD];
@@ -357,6 +377,16 @@ __global__ void __launch_bounds__(GF_THREADS) gm_chunk_kernel(GmChunkArgs a) {
   GmState *st = a.st;
   if (st->converged || st->stop) return;   // uniform: written by earlier launches
   const int N = st->N, m = st->m;
+  if (a.mode == 2) {  // both variants launched: the device-resident sizes choose one (uniform)
+    int tiles = 0;
+    for (int q = 0; q < 3; ++q) {
+      const GemmDesc &g = a.gapp[3 * (a.j0 + 1) + q];
+      const int t = ((g.M + 63) / 64) * ((g.N + 63) / 64);
+      tiles = t > tiles ? t : tiles;
+    }
+    const bool small = tiles <= 2 * a.cs && N <= 16384;
+    if (small != CLUSTER) return;
+  }
   const double tol = st->tol, bnorm = st->bnorm;
   const int per = (N + G - 1) / G;
   const int lo = min(N, (int)blockIdx.x * per), hi = min(N, lo + per);
@@ -365,7 +395,7 @@ __global__ void __launch_bounds__(GF_THREADS) gm_chunk_kernel(GmChunkArgs a) {
   double *part1 = a.part, *part2 = a.part + (size_t)G * GF_LD, *part3 = a.part + 2 * (size_t)G * GF_LD;
   double *w = a.w;
   for (int j = a.j0; j < a.j1 && j < m; ++j) {
-    if (j > a.j0) gbar(a.bar, G);            // V[:, j] of the previous step complete
+    if (j > a.j0) phase_sync<CLUSTER>(a.bar, G);            // V[:, j] of the previous step complete
     // ---- w = A V[:, j] (three chained GEMM stages)
     for (int sidx = 0; sidx < 3; ++sidx) {
       const GemmDesc g = a.gapp[3 * (j + 1) + sidx];
@@ -377,8 +407,10 @@ __global__ void __launch_bounds__(GF_THREADS) gm_chunk_kernel(GmChunkArgs a) {
         while (splits > 1 && (long long)splits * g.M * g.N > a.split_elems) --splits;
       }
       if (blockIdx.x == 0 && tid == 0) {
-        atomicAdd(&g_gemm_counters[0], 2ull * (unsigned long long)g.M * g.N * (g.K > 0 ? g.K : 0));
+        const unsigned long long f = 2ull * (unsigned long long)g.M * g.N * (g.K > 0 ? g.K : 0);
+        atomicAdd(&g_gemm_counters[0], f);
         atomicAdd(&g_gemm_counters[1], 1ull);
+        atomicAdd(&g_gm_counters[0], f);
       }
       for (int t = blockIdx.x; t < T * splits; t += G) {
         const int z = t / T, tt = t - z * T;
@@ -386,7 +418,7 @@ __global__ void __launch_bounds__(GF_THREADS) gm_chunk_kernel(GmChunkArgs a) {
                                        (long long)g.M * g.N, smem);
         __syncthreads();
       }
-      gbar(a.bar, G);
+      phase_sync<CLUSTER>(a.bar, G);
       if (splits > 1) {
         const long long total = (long long)g.M * g.N, ps = total;
         double alpha = g.alpha;
@@ -401,7 +433,7 @@ __global__ void __launch_bounds__(GF_THREADS) gm_chunk_kernel(GmChunkArgs a) {
           if (g.beta != 0.0) v += g.beta * g.C[addr];
           g.C[addr] = v;
         }
-        gbar(a.bar, G);
+        phase_sync<CLUSTER>(a.bar, G);
       }
     }
     // ---- CGS2 pass 1: slice dots
@@ -413,7 +445,7 @@ __global__ void __launch_bounds__(GF_THREADS) gm_chunk_kernel(GmChunkArgs a) {
       sacc = warp_sum(sacc);
       if (lane == 0) my1[i] = sacc;
     }
-    gbar(a.bar, G);
+    phase_sync<CLUSTER>(a.bar, G);
     for (int i = warp; i <= j; i += NW) {      // cross-CTA sums: one warp per entry, fixed order
       double sacc = 0.0;
       for (int c = lane; c < G; c += 32) sacc += part1[(size_t)c * GF_LD + i];
@@ -439,7 +471,7 @@ __global__ void __launch_bounds__(GF_THREADS) gm_chunk_kernel(GmChunkArgs a) {
     // rotations and g[j] of earlier steps, read before CTA 0 rewrites them in this step
     for (int i = tid; i < j; i += GF_THREADS) { css[i] = st->cs[i]; sns[i] = st->sn[i]; }
     const double gj = st->g[j];
-    gbar(a.bar, G);
+    phase_sync<CLUSTER>(a.bar, G);
     for (int i = warp; i <= j; i += NW) {
       double sacc = 0.0;
       for (int c = lane; c < G; c += 32) sacc += part2[(size_t)c * GF_LD + i];
@@ -462,7 +494,7 @@ __global__ void __launch_bounds__(GF_THREADS) gm_chunk_kernel(GmChunkArgs a) {
       for (int q = 0; q < NW; ++q) t += red[q];
       part3[(size_t)blockIdx.x * GF_LD] = t;
     }
-    gbar(a.bar, G);
+    phase_sync<CLUSTER>(a.bar, G);
     // ---- norm, Givens (identical in every CTA), normalisation
     if (warp == 0) {
       double hn2 = 0.0;
@@ -510,6 +542,10 @@ __global__ void __launch_bounds__(GF_THREADS) gm_chunk_kernel(GmChunkArgs a) {
     }
     __syncthreads();
     const bool stop = red[0] != 0.0;
+    if (blockIdx.x == 0 && tid == 0) {
+      atomicAdd(&g_gm_counters[1], (unsigned long long)N * (8ull * (j + 1) + 3ull));
+      atomicAdd(&g_gm_counters[2], 1ull);
+    }
     if (red[1] > 0.0) {
       const double inv = 1.0 / red[1];
       double *vn = a.V + (long long)(j + 1) * a.ldv;
@@ -560,8 +596,10 @@ int gmres_fused_grid() {
     int dev = 0, sms = 0, occ = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaFuncSetAttribute(gm_chunk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GF::SMEM);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, gm_chunk_kernel, GF_THREADS, GF::SMEM);
+    cudaFuncSetAttribute(gm_chunk_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GF::SMEM);
+    cudaFuncSetAttribute(gm_chunk_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GF::SMEM);
+    cudaFuncSetAttribute(gm_chunk_kernel<true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, gm_chunk_kernel<false>, GF_THREADS, GF::SMEM);
     const char *e = std::getenv("TT_GF_GRID");
     G = (occ >= 1) ? (e ? std::atoi(e) : sms) : -1;
     if (G > occ * sms || G > 256) G = occ * sms < 256 ? occ * sms : 256;
@@ -569,17 +607,90 @@ int gmres_fused_grid() {
   return G;
 }
 
+// live timing of the fused kernel (tt_fused_profile): events around every launch
+struct FusedProfile {
+  bool on = false;
+  std::vector<cudaEvent_t> ev;   // pairs
+  size_t used = 0;
+};
+thread_local FusedProfile g_fp;
+
+void fused_profile(int enable) {
+  g_fp.on = enable != 0;
+  g_fp.used = 0;
+}
+
+void fused_profile_read(long long *launches, double *ms, double *flops) {
+  double t = 0.0;
+  for (size_t i = 0; i + 1 < g_fp.used; i += 2) {
+    cudaEventSynchronize(g_fp.ev[i + 1]);
+    float e = 0.f;
+    cudaEventElapsedTime(&e, g_fp.ev[i], g_fp.ev[i + 1]);
+    t += e;
+  }
+  unsigned long long c[3] = {0, 0, 0};
+  cudaMemcpyFromSymbol(c, g_gm_counters, sizeof(c));
+  const unsigned long long z[3] = {0, 0, 0};
+  cudaMemcpyToSymbol(g_gm_counters, z, sizeof(z));
+  if (launches) *launches = (long long)(g_fp.used / 2);
+  if (ms) *ms = t;
+  if (flops) { flops[0] = (double)c[0]; flops[1] = (double)c[1]; flops[2] = (double)c[2]; }
+  g_fp.used = 0;
+}
+
+int gmres_cluster_size() {
+  static int cs = 0;
+  if (!cs) {
+    const char *e = std::getenv("TT_GF_CLUSTER");
+    cs = e ? std::atoi(e) : 8;
+    cs = cs >= 16 ? 16 : (cs >= 8 ? 8 : (cs >= 4 ? 4 : 2));
+  }
+  return cs;
+}
+
 tt_status launch_gmres_chunk(GmState *st, const GemmDesc *gapp, double *V, long long ldv, double *w, double *part,
                              double *split, long long split_elems, unsigned int *bar, int j0, int j1,
-                             cudaStream_t s) {
-  const int G = gmres_fused_grid();
+                             cudaStream_t s, int cluster, int decide) {
+  const int G = cluster ? gmres_cluster_size() : gmres_fused_grid();
   if (G <= 0) return fail(TT_ERR_CUDA, "gmres: fused step kernel cannot be co-resident");
   GmChunkArgs a;
+  a.mode = decide ? 2 : cluster;
+  a.cs = gmres_cluster_size();
   a.st = st; a.gapp = gapp; a.V = V; a.ldv = ldv; a.w = w; a.part = part; a.split = split;
   a.split_elems = split_elems; a.bar = bar; a.j0 = j0; a.j1 = j1;
   void *args[] = {(void *)&a};
-  cudaError_t e = cudaLaunchCooperativeKernel((const void *)gm_chunk_kernel, dim3(G), dim3(GF_THREADS), args,
-                                              GF::SMEM, s);
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (g_fp.on) {
+    while (g_fp.ev.size() < g_fp.used + 2) {
+      cudaEvent_t ev;
+      cudaEventCreate(&ev);
+      g_fp.ev.push_back(ev);
+    }
+    e0 = g_fp.ev[g_fp.used];
+    e1 = g_fp.ev[g_fp.used + 1];
+    g_fp.used += 2;
+    cudaEventRecord(e0, s);
+  }
+  cudaError_t e;
+  if (cluster) {   // one thread-block cluster: hardware cluster barriers between the phases
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(G);
+    cfg.blockDim = dim3(GF_THREADS);
+    cfg.dynamicSmemBytes = GF::SMEM;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = G;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    e = cudaLaunchKernelEx(&cfg, gm_chunk_kernel<true>, a);
+  } else {
+    e = cudaLaunchCooperativeKernel((const void *)gm_chunk_kernel<false>, dim3(G), dim3(GF_THREADS), args, GF::SMEM,
+                                    s);
+  }
+  if (e1) cudaEventRecord(e1, s);
   if (e != cudaSuccess) return fail(TT_ERR_CUDA, std::string("gm_chunk: ") + cudaGetErrorString(e));
   return TT_OK;
 }

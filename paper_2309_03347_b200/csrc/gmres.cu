@@ -209,8 +209,14 @@ tt_status gmres_solve(const GmresCtx &c, cudaStream_t s) {
     int pending = -1;  // slot of the last enqueued poll copy
     if (fused) {
       for (int j0 = 0, q = 0; j0 < c.m; j0 += GM_FCHUNK, ++q) {
-        TT_TRY(launch_gmres_chunk(c.st, c.gapp, c.V, c.ldv, c.w, c.part, c.split, c.split_elems, c.bar, j0,
-                                  j0 + GM_FCHUNK < c.m ? j0 + GM_FCHUNK : c.m, s));
+        const int j1 = j0 + GM_FCHUNK < c.m ? j0 + GM_FCHUNK : c.m;
+        const int decide = c.cluster == 2;
+        if (c.cluster != 0)
+          TT_TRY(launch_gmres_chunk(c.st, c.gapp, c.V, c.ldv, c.w, c.part, c.split, c.split_elems, c.bar, j0, j1,
+                                    s, 1, decide));
+        if (c.cluster != 1)
+          TT_TRY(launch_gmres_chunk(c.st, c.gapp, c.V, c.ldv, c.w, c.part, c.split, c.split_elems, c.bar, j0, j1,
+                                    s, 0, decide));
         if (c.poll) {
           // copy this chunk's stop word, then wait for the PREVIOUS chunk's copy
           // (that chunk finished while this one runs): the GPU never drains

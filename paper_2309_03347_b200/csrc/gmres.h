@@ -40,6 +40,8 @@ struct GmresCtx {
   unsigned int *bar = nullptr;   // [2] grid barrier words (zeroed by gmres_solve)
   double *split = nullptr;       // split-K scratch
   long long split_elems = 0;
+  int cluster = 0;               // 0: cooperative grid; 1: one thread-block cluster (small local
+                                 // systems); 2: both launched, the device-resident sizes decide
 };
 
 tt_status gmres_solve(const GmresCtx &c, cudaStream_t s);
@@ -47,6 +49,8 @@ tt_status gmres_solve(const GmresCtx &c, cudaStream_t s);
 size_t gmres_fused_part_doubles(int G);
 int gmres_fused_grid();
 tt_status launch_gmres_chunk(GmState *st, const GemmDesc *gapp, double *V, long long ldv, double *w, double *part,
-                             double *split, long long split_elems, unsigned int *bar, int j0, int j1, cudaStream_t s);
+                             double *split, long long split_elems, unsigned int *bar, int j0, int j1, cudaStream_t s,
+                             int cluster, int decide);
+int gmres_cluster_size();
 
 }  // namespace tt
