@@ -166,8 +166,9 @@ __global__ void plan_svd(Dev D, int k, int dir) {
   q.A = D.qA; q.lda = q.m;
   q.R = D.qR; q.ldr = p;
   q.tau = D.tau; q.T = D.qT;
+  q.rt = 1;   // Jacobi on R^T = V_R S U_R^T (fewer sweeps for decaying spectra): U, V swap
   SVDDesc &s = D.sd[0];
-  s.m = p; s.p = p; s.W = D.qR; s.ldw = p; s.U = D.U; s.ldu = p; s.V = D.Vs; s.ldv = p;
+  s.m = p; s.p = p; s.W = D.qR; s.ldw = p; s.U = D.Vs; s.ldu = p; s.V = D.U; s.ldv = p;
   s.sigma = D.S; s.work = D.J; s.sweeps_out = nullptr;
   D.iv[2] = wide; D.iv[3] = p; D.iv[4] = mm; D.iv[5] = nn;
 }
@@ -237,10 +238,10 @@ __device__ void enrich_tail(const Dev &D, int k, int dir, int n, int r, int mm, 
     qzr = min(n * z1, z0);
     qz.Q = Zk; qz.q_rs = qzr; qz.q_cs = 1;
   }
-  qz.A = D.qA2; qz.lda = qz.m; qz.R = nullptr; qz.ldr = 1; qz.tau = D.tau2; qz.T = D.qT2;
+  qz.A = D.qA2; qz.lda = qz.m; qz.R = nullptr; qz.ldr = 1; qz.tau = D.tau2; qz.T = D.qT2; qz.rt = 0;
   const int q = min(mm, r + ze);
   qx.m = mm; qx.n = r + ze; qx.src = D.Ue; qx.src_rs = 1; qx.src_cs = mm;
-  qx.A = D.qA; qx.lda = mm; qx.R = D.qRe; qx.ldr = q; qx.tau = D.tau; qx.T = D.qT;
+  qx.A = D.qA; qx.lda = mm; qx.R = D.qRe; qx.ldr = q; qx.tau = D.tau; qx.T = D.qT; qx.rt = 0;
   if (dir > 0) { qx.Q = Xk; qx.q_rs = 1; qx.q_cs = mm; }     // x_k = Q as [r0, n, q]
   else { qx.Q = Xk; qx.q_rs = q; qx.q_cs = 1; }              // x_k = Q^T as [q, n, r1]
   // ---- K = Re[:, :r] C = Re[:, :r] Ct^T  (q x nn)

@@ -241,7 +241,9 @@ __global__ void __launch_bounds__(QR_THREADS) qr_kernel(const QRDesc *__restrict
   if (g.R) {
     for (long long e = tid; e < (long long)kmin * n; e += QR_THREADS) {
       const int r = (int)(e % kmin), c = (int)(e / kmin);
-      g.R[r + c * g.ldr] = (c >= r) ? A[r + c * lda] : 0.0;
+      const double v = (c >= r) ? A[r + c * lda] : 0.0;
+      if (g.rt) g.R[c + r * g.ldr] = v;
+      else g.R[r + c * g.ldr] = v;
     }
   }
   // ---- explicit Q = H_1 ... H_k [I; 0]  (orgqr, backward over panels)

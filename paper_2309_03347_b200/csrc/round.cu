@@ -106,6 +106,7 @@ __global__ void plan_orth_rl(const VecMeta x, int k, StepWS w) {
   d.Q = core; d.q_rs = q; d.q_cs = 1;                 // new core [q, n, r1] = Q^T
   d.R = w.R; d.ldr = q;
   d.tau = w.tau; d.T = w.T;
+  d.rt = 0;
   w.gd[0] = gemm_desc(rp * np, q, p, prev, (long long)rp * np, 0, w.R, q, 1, w.tmp, (long long)rp * np);
   w.cd[0] = copy_desc(rp * np, q, w.tmp, 1, (long long)rp * np, prev, 1, (long long)rp * np);
   x.r[k] = q;
@@ -125,6 +126,7 @@ __global__ void plan_orth_lr(const VecMeta x, int k, StepWS w) {
   d.Q = core; d.q_rs = 1; d.q_cs = m;                 // new core [r0, n, q] = Q
   d.R = w.R; d.ldr = q;
   d.tau = w.tau; d.T = w.T;
+  d.rt = 0;
   w.gd[0] = gemm_desc(q, n2 * r2, p, w.R, q, 0, next, p, 0, w.tmp, q);
   w.cd[0] = copy_desc(q, n2 * r2, w.tmp, 1, q, next, 1, q);
   x.r[k + 1] = q;
@@ -169,11 +171,14 @@ __global__ void plan_trunc(const VecMeta x, int k, StepWS w) {
   d.A = w.A; d.lda = d.m;
   d.R = w.R; d.ldr = p;
   d.tau = w.tau; d.T = w.T;
+  // one-sided Jacobi on R^T (= V_R S U_R^T): converges in far fewer sweeps than on R
+  // when the spectrum decays (preconditioning by the QR); U and V swap roles
+  d.rt = 1;
   SVDDesc &s = *w.sd;
   s.m = p; s.p = p;
   s.W = w.R; s.ldw = p;
-  s.U = w.U; s.ldu = p;
-  s.V = w.V; s.ldv = p;
+  s.U = w.V; s.ldu = p;
+  s.V = w.U; s.ldv = p;
   s.sigma = w.S;
   s.work = w.J;
   s.sweeps_out = nullptr;

@@ -112,6 +112,7 @@ struct QRDesc {
   long long q_rs, q_cs;
   double *R;             // out: R, min(m,n) x n, column-major (ldr); may be nullptr
   long long ldr;
+  int rt;                // 1: write R^T instead (element (r, c) of R at R[c + r*ldr])
   double *tau;           // workspace >= min(m,n)
   double *T;             // workspace >= 32*32 * ceil(min(m,n)/32)
 };
