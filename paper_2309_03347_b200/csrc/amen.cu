@@ -486,9 +486,9 @@ tt_status amen_solve_meta(const MatMeta &A, const VecMeta &b, const VecMeta &x, 
   const int *xc = x.rcap, *zc = z.rcap, *bc = b.rcap, *Rc = A.Rcap;
   struct Caps12 { GemmDesc g[12]; int cnt; };
   auto launch_caps = [&](const GemmDesc *dev, const Caps12 &hc, int from, int cnt) -> tt_status {
-    for (int i = 0; i < cnt; ++i)
-      TT_TRY(launch_gemm_k(dev + i, 1, hc.g[from + i].M, hc.g[from + i].N, hc.g[from + i].K, s));
-    return TT_OK;
+    int Mc[12], Nc[12], Kc[12];
+    for (int i = 0; i < cnt; ++i) { Mc[i] = hc.g[from + i].M; Nc[i] = hc.g[from + i].N; Kc[i] = hc.g[from + i].K; }
+    return launch_gemm_seq(dev, cnt, Mc, Nc, Kc, s);   // one cluster launch for small chains
   };
   auto iface_caps = [&](int k, int dir) {
     Caps12 c;
@@ -833,9 +833,9 @@ tt_status amen_mv_meta(const MatMeta &A, const VecMeta &b, const VecMeta &y, con
   const int *yc = y.rcap, *zc = z.rcap, *bc = b.rcap, *Rc = A.Rcap;
   struct Caps12 { GemmDesc g[12]; };
   auto launch_caps = [&](const GemmDesc *dev, const Caps12 &hc, int from, int cnt) -> tt_status {
-    for (int i = 0; i < cnt; ++i)
-      TT_TRY(launch_gemm_k(dev + i, 1, hc.g[from + i].M, hc.g[from + i].N, hc.g[from + i].K, s));
-    return TT_OK;
+    int Mc[12], Nc[12], Kc[12];
+    for (int i = 0; i < cnt; ++i) { Mc[i] = hc.g[from + i].M; Nc[i] = hc.g[from + i].N; Kc[i] = hc.g[from + i].K; }
+    return launch_gemm_seq(dev, cnt, Mc, Nc, Kc, s);   // one cluster launch for small chains
   };
   auto iface = [&](int k, int dir) -> tt_status {
     plan_iface_mv<<<1, 1, 0, s>>>(D, k, dir);

@@ -368,6 +368,63 @@ __device__ __forceinline__ void phase_sync(unsigned int *bar, unsigned int nbloc
   }
 }
 
+// One GEMM as a phase of a persistent kernel: DMMA tiles distributed over the
+// CTAs (split-K with an in-kernel reduction when the GEMM has few tiles), then a
+// phase barrier.  Uniform control flow: every CTA reads the same descriptor.
+template <bool CLUSTER>
+__device__ void gemm_stage(const GemmDesc &g, double *split, long long split_elems, unsigned int *bar, int G,
+                           double *smem, bool gm_count) {
+  if (g.M <= 0 || g.N <= 0) return;
+  if (g.skip && *g.skip) return;
+  const int tid = threadIdx.x;
+  const int tm = (g.M + 63) / 64, tn = (g.N + 63) / 64, T = tm * tn;
+  int splits = 1;
+  if (T * 2 <= G && g.K >= 256) {
+    splits = min(G / T, min(g.K / 128, 16));
+    while (splits > 1 && (long long)splits * g.M * g.N > split_elems) --splits;
+  }
+  if (blockIdx.x == 0 && tid == 0) {
+    const unsigned long long f = 2ull * (unsigned long long)g.M * g.N * (g.K > 0 ? g.K : 0);
+    atomicAdd(&g_gemm_counters[0], f);
+    atomicAdd(&g_gemm_counters[1], 1ull);
+    if (gm_count) atomicAdd(&g_gm_counters[0], f);
+  }
+  for (int t = blockIdx.x; t < T * splits; t += G) {
+    const int z = t / T, tt = t - z * T;
+    gemm_tile<64, 64, 16, 2, 2, 2>(g, (tt % tm) * 64, (tt / tm) * 64, z, splits, split, g.M, (long long)g.M * g.N,
+                                   smem);
+    __syncthreads();
+  }
+  phase_sync<CLUSTER>(bar, G);
+  if (splits > 1) {
+    const long long total = (long long)g.M * g.N, ps = total;
+    double alpha = g.alpha;
+    if (g.alpha_dev) alpha *= *g.alpha_dev;
+    for (long long e = (long long)blockIdx.x * GF_THREADS + tid; e < total; e += (long long)G * GF_THREADS) {
+      const int r = (int)(e % g.M), c = (int)(e / g.M);
+      double sum = 0.0;
+      for (int z = 0; z < splits; ++z) sum += split[z * ps + e];
+      const long long addr = (long long)(r % g.dr) * g.s_r0 + (long long)(r / g.dr) * g.s_r1 +
+                             (long long)(c % g.dc) * g.s_c0 + (long long)(c / g.dc) * g.s_c1;
+      double v = alpha * sum;
+      if (g.beta != 0.0) v += g.beta * g.C[addr];
+      g.C[addr] = v;
+    }
+    phase_sync<CLUSTER>(bar, G);
+  }
+}
+
+// A dependent chain of GEMMs (each consumes earlier outputs) in one launch of a
+// thread-block cluster: one phase per GEMM instead of one kernel launch each.
+__global__ void __launch_bounds__(GF_THREADS) gemm_seq_kernel(const GemmDesc *__restrict__ descs, int count,
+                                                              double *split, long long split_elems) {
+  extern __shared__ __align__(16) double smem[];
+  for (int i = 0; i < count; ++i) {
+    const GemmDesc g = descs[i];
+    gemm_stage<true>(g, split, split_elems, nullptr, gridDim.x, smem, false);
+  }
+}
+
 template <bool CLUSTER>
 __global__ void __launch_bounds__(GF_THREADS) gm_chunk_kernel(GmChunkArgs a) {
   extern __shared__ __align__(16) double smem[];
@@ -397,45 +454,8 @@ __global__ void __launch_bounds__(GF_THREADS) gm_chunk_kernel(GmChunkArgs a) {
   for (int j = a.j0; j < a.j1 && j < m; ++j) {
     if (j > a.j0) phase_sync<CLUSTER>(a.bar, G);            // V[:, j] of the previous step complete
     // ---- w = A V[:, j] (three chained GEMM stages)
-    for (int sidx = 0; sidx < 3; ++sidx) {
-      const GemmDesc g = a.gapp[3 * (j + 1) + sidx];
-      if (g.M <= 0 || g.N <= 0) continue;
-      const int tm = (g.M + 63) / 64, tn = (g.N + 63) / 64, T = tm * tn;
-      int splits = 1;
-      if (T * 2 <= G && g.K >= 256) {
-        splits = min(G / T, min(g.K / 128, 16));
-        while (splits > 1 && (long long)splits * g.M * g.N > a.split_elems) --splits;
-      }
-      if (blockIdx.x == 0 && tid == 0) {
-        const unsigned long long f = 2ull * (unsigned long long)g.M * g.N * (g.K > 0 ? g.K : 0);
-        atomicAdd(&g_gemm_counters[0], f);
-        atomicAdd(&g_gemm_counters[1], 1ull);
-        atomicAdd(&g_gm_counters[0], f);
-      }
-      for (int t = blockIdx.x; t < T * splits; t += G) {
-        const int z = t / T, tt = t - z * T;
-        gemm_tile<64, 64, 16, 2, 2, 2>(g, (tt % tm) * 64, (tt / tm) * 64, z, splits, a.split, g.M,
-                                       (long long)g.M * g.N, smem);
-        __syncthreads();
-      }
-      phase_sync<CLUSTER>(a.bar, G);
-      if (splits > 1) {
-        const long long total = (long long)g.M * g.N, ps = total;
-        double alpha = g.alpha;
-        if (g.alpha_dev) alpha *= *g.alpha_dev;
-        for (long long e = (long long)blockIdx.x * GF_THREADS + tid; e < total; e += (long long)G * GF_THREADS) {
-          const int r = (int)(e % g.M), c = (int)(e / g.M);
-          double sum = 0.0;
-          for (int z = 0; z < splits; ++z) sum += a.split[z * ps + e];
-          const long long addr = (long long)(r % g.dr) * g.s_r0 + (long long)(r / g.dr) * g.s_r1 +
-                                 (long long)(c % g.dc) * g.s_c0 + (long long)(c / g.dc) * g.s_c1;
-          double v = alpha * sum;
-          if (g.beta != 0.0) v += g.beta * g.C[addr];
-          g.C[addr] = v;
-        }
-        phase_sync<CLUSTER>(a.bar, G);
-      }
-    }
+    for (int sidx = 0; sidx < 3; ++sidx)
+      gemm_stage<CLUSTER>(a.gapp[3 * (j + 1) + sidx], a.split, a.split_elems, a.bar, G, smem, true);
     // ---- CGS2 pass 1: slice dots
     double *my1 = part1 + (size_t)blockIdx.x * GF_LD;
     for (int i = warp; i <= j; i += NW) {
@@ -636,6 +656,50 @@ void fused_profile_read(long long *launches, double *ms, double *flops) {
   if (ms) *ms = t;
   if (flops) { flops[0] = (double)c[0]; flops[1] = (double)c[1]; flops[2] = (double)c[2]; }
   g_fp.used = 0;
+}
+
+// Dependent GEMM chain: one cluster launch when every GEMM is small at its
+// capacity shape (<= 2 tiles per CTA of the cluster), else one launch per GEMM.
+tt_status launch_gemm_seq(const GemmDesc *descs_dev, int count, const int *Mcap, const int *Ncap, const int *Kcap,
+                          cudaStream_t s) {
+  if (count <= 0) return TT_OK;
+  // measured slower than per-GEMM launches on the full GPU for the C1/C3 chains
+  // (profiles/r01), so opt-in only: TT_GEMM_SEQ=1
+  static int off = -1;
+  if (off < 0) off = std::getenv("TT_GEMM_SEQ") ? 0 : 1;
+  const int cs = gmres_cluster_size();
+  bool small = count >= 2 && !off && gmres_fused_grid() > 0;
+  for (int i = 0; i < count && small; ++i) {
+    const long long t = (long long)((Mcap[i] + 63) / 64) * ((Ncap[i] + 63) / 64);
+    small = t <= 2 * cs;
+  }
+  if (!small) {
+    for (int i = 0; i < count; ++i) TT_TRY(launch_gemm_k(descs_dev + i, 1, Mcap[i], Ncap[i], Kcap[i], s));
+    return TT_OK;
+  }
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(gemm_seq_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GF::SMEM);
+    cudaFuncSetAttribute(gemm_seq_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    attr = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(cs);
+  cfg.blockDim = dim3(GF_THREADS);
+  cfg.dynamicSmemBytes = GF::SMEM;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = cs;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  double *sp = g_split.ptr;
+  const long long se = (long long)(g_split.bytes / sizeof(double));
+  cudaError_t e = cudaLaunchKernelEx(&cfg, gemm_seq_kernel, descs_dev, count, sp, se);
+  if (e != cudaSuccess) return fail(TT_ERR_CUDA, std::string("gemm_seq: ") + cudaGetErrorString(e));
+  return TT_OK;
 }
 
 int gmres_cluster_size() {

@@ -96,6 +96,10 @@ tt_status launch_gemm(const GemmDesc *descs_dev, int count, int Mcap, int Ncap, 
 // output has few tiles, using the scratch registered by set_gemm_scratch (the
 // calling thread's current workspace slice); deterministic slice-sum reduction.
 tt_status launch_gemm_k(const GemmDesc *descs_dev, int count, int Mcap, int Ncap, int Kcap, cudaStream_t s);
+// A dependent chain of `count` GEMMs (descriptor i consumes earlier outputs) with
+// per-GEMM capacity shapes: one thread-block-cluster launch when all are small.
+tt_status launch_gemm_seq(const GemmDesc *descs_dev, int count, const int *Mcap, const int *Ncap, const int *Kcap,
+                          cudaStream_t s);
 void set_gemm_scratch(double *ptr, size_t bytes);
 constexpr size_t GEMM_SPLIT_SCRATCH = 32ull << 20;  // bytes reserved by callers that enable split-K
 
