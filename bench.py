@@ -174,7 +174,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--workload", default="c1", choices=["c1", "c2", "c3", "c5"])
+    ap.add_argument("--workload", default="c1", choices=["c1", "c2", "c3", "c4", "c5"])
     ap.add_argument("--outer", type=int, default=30, help="c3: fixed-point iterations per step")
     ap.add_argument("--rank", type=int, default=128, help="c5 interface rank (64, 128, 256)")
     ap.add_argument("--seed", type=int, default=0)
@@ -218,8 +218,8 @@ def main():
     from paper_2309_03347_b200 import _lib
     import ctypes as C
 
-    if args.workload in ("c2", "c3", "c5"):
-        line = c3_bench(args, tb, device, world, dist) if args.workload == "c3" else \
+    if args.workload in ("c2", "c3", "c4", "c5"):
+        line = c3_bench(args, tb, device, world, dist) if args.workload in ("c3", "c4") else \
             micro_bench(args, tb, device, world, dist)
         if rank == 0:
             print(json.dumps(line))
@@ -474,11 +474,12 @@ def c3_bench(args, tb, device, world, dist):
     from paper_2309_03347_b200 import _lib
     import ctypes as C
     pk = peaks()
-    prob = inputs.problem_c3()
+    c4 = args.workload == "c4"
+    prob = inputs.problem_c4() if c4 else inputs.problem_c3()
     ops = gtr.operators(prob, eps=1e-12, device=device)
     modes = gtr.modes(prob)
     d = len(modes)
-    rmax, kick = 64, 4
+    rmax, kick = (128 if c4 else 64), 4
     g = inputs.rng(61)
     z0 = inputs.random_tt(g, modes, [1] + [kick] * (d - 1) + [1])
     cap = [1] + [rmax + kick] * (d - 1) + [1]
@@ -525,17 +526,21 @@ def c3_bench(args, tb, device, world, dist):
     gfl = (gemm_flops + mv_flops) / (dev_ms * 1e-3) / 1e9
     truth = None
     gold = os.path.join(ROOT, "tests", "golden", "c3_keff.txt")
-    if os.path.exists(gold):
+    if os.path.exists(gold) and not c4:
         for l in open(gold):
             if l.strip() and not l.startswith("#") and l.split()[0] == "64":
                 truth = float(l.split()[1])
     roof = dominant_gemm_roofline(tb, device, pk, shape=(68, 60, 68, 2, 2, 68, 60, 68),
-                                  label="C3 local shape r=68 R=60 n=2")
+                                  label="C3 local shape r=68 R=60 n=2") if not c4 else \
+        dominant_gemm_roofline(tb, device, pk, shape=(132, 84, 132, 2, 2, 132, 84, 132),
+                               label="C4 local shape r=132 R=84 n=2")
     return {"metric": METRIC, "value": iters_all / (dev_max * 1e-3), "unit": "iter/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": dev_max / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"C3 (configs[2]): 64^3 QTT, G=7, S8 (80), two regions, rmax {rmax}, eps 1e-6, "
-                                   f"B by amen_mv; step = {args.outer} fixed-point iterations from psi_0 = 1",
+            "config": {"workload": (f"C4 (configs[3]): 256^3 QTT, G=30 (upscatter 26-30), S16 (288), three regions, "
+                                    if c4 else "C3 (configs[2]): 64^3 QTT, G=7, S8 (80), two regions, ") +
+                                   f"rmax {rmax}, eps 1e-6, B by amen_mv; step = {args.outer} fixed-point "
+                                   "iterations from psi_0 = 1",
                        "l2": "256 MB flush between timed steps", "parallelism": f"replicas x{world}"},
             "k_last": ks[-1], "k_truth_matrix_free": truth,
             "k_rel_discrepancy": (abs(ks[-1] - truth) / truth) if truth else None,

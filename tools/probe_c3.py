@@ -1,5 +1,6 @@
-"""C3 (configs[2]) on the device: QTT operator assembly and the k-eff fixed point
-with B by amen_mv (NEXT-1).  Usage: probe_c3.py NV [eps] [rmax] [max_outer]"""
+"""C3 (configs[2]) / C4 (configs[3], NV=c4) on the device: QTT operator assembly
+and the k-eff fixed point with B by amen_mv (NEXT-1).
+Usage: probe_c3.py NV|c4 [eps] [rmax] [max_outer] [max_sweeps]"""
 import os
 import sys
 import time
@@ -11,12 +12,13 @@ import inputs  # noqa: E402
 import paper_2309_03347_b200 as tb  # noqa: E402
 from paper_2309_03347_b200 import transport as gtr  # noqa: E402
 
-nv = int(sys.argv[1]) if len(sys.argv) > 1 else 16
+cfg = sys.argv[1] if len(sys.argv) > 1 else "16"
 eps = float(sys.argv[2]) if len(sys.argv) > 2 else 1e-6
 rmax = int(sys.argv[3]) if len(sys.argv) > 3 else 64
 mo = int(sys.argv[4]) if len(sys.argv) > 4 else 200
 ms = int(sys.argv[5]) if len(sys.argv) > 5 else 10
-p = inputs.problem_c3(nv=nv)
+p = inputs.problem_c4() if cfg == "c4" else inputs.problem_c3(nv=int(cfg))
+nv = p["nv"]
 t = time.time()
 ops = gtr.operators(p, eps=1e-12)
 torch.cuda.synchronize()
