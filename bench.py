@@ -503,6 +503,9 @@ def c3_bench(args, tb, device, world, dist):
     cnt = (C.c_uint64 * 5)()
     lib = _lib.lib()
     lib.tt_counters(cnt, 1)
+    fl, fms, ffl = C.c_int64(0), C.c_double(0.0), (C.c_double * 3)()
+    lib.tt_fused_profile_read(C.byref(fl), C.byref(fms), ffl)
+    lib.tt_fused_profile(1)
     ms, iters, ks = [], 0, []
     with ClockSampler(torch.cuda.current_device()) as clk:
         if dist:
@@ -520,6 +523,8 @@ def c3_bench(args, tb, device, world, dist):
         if dist:
             dist.barrier()
     lib.tt_counters(cnt, 1)
+    lib.tt_fused_profile_read(C.byref(fl), C.byref(fms), ffl)
+    lib.tt_fused_profile(0)
     dev_ms = sum(ms)
     dev_max, iters_all = aggregate_ranks(dev_ms, iters, dist, device)
     gemm_flops, mv_flops, qr_flops, svd_flops, ngemm = [int(v) for v in cnt]
@@ -530,10 +535,20 @@ def c3_bench(args, tb, device, world, dist):
         for l in open(gold):
             if l.strip() and not l.startswith("#") and l.split()[0] == "64":
                 truth = float(l.split()[1])
-    roof = dominant_gemm_roofline(tb, device, pk, shape=(68, 60, 68, 2, 2, 68, 60, 68),
-                                  label="C3 local shape r=68 R=60 n=2") if not c4 else \
+    chain = dominant_gemm_roofline(tb, device, pk, shape=(68, 60, 68, 2, 2, 68, 60, 68),
+                                   label="C3 local shape r=68 R=60 n=2") if not c4 else \
         dominant_gemm_roofline(tb, device, pk, shape=(132, 84, 132, 2, 2, 132, 84, 132),
                                label="C4 local shape r=132 R=84 n=2")
+    ff = ffl[0] + ffl[1]
+    ach = ff / (fms.value * 1e-3) / 1e12 if fms.value > 0 else None
+    roof = {"kernel": "gm_chunk_kernel (fused GMRES Arnoldi steps, cluster / cooperative-grid variants)",
+            "bound": "tensor", "achieved": ach, "peak": pk["dmma_gflops"] / 1e3, "unit": "TFLOP/s",
+            "frac": (ach / (pk["dmma_gflops"] / 1e3)) if ach else None,
+            "peak_src": "measured FP64 DMMA sustained (tools/peaks_fp64)", "traffic": None,
+            "launches": fl.value, "ms_per_launch": fms.value / max(fl.value, 1),
+            "flops_per_launch": ff / max(fl.value, 1), "arnoldi_steps": ffl[2],
+            "share_of_step_time": fms.value / dev_ms if dev_ms > 0 else None,
+            "gemm_chain_alone": chain}
     return {"metric": METRIC, "value": iters_all / (dev_max * 1e-3), "unit": "iter/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": dev_max / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
