@@ -563,16 +563,25 @@ tt_status amen_solve_meta(const MatMeta &A, const VecMeta &b, const VecMeta &x, 
         // both variants and let the device-resident sizes pick one (the other exits at once)
         gc.cluster = cluster_off ? 0 : ((tiles <= 2 * gmres_cluster_size() && nloc <= 16384) ? 1 : 2);
       }
-      plan_local<<<1, 1, 0, s>>>(D, k);
-      TT_TRY(launch_copy(D.cd, 1, P.Ncap, s));
-      TT_TRY(launch_copy(D.cd + 2, 1, P.Ncap, s));
-      TT_TRY(launch_caps(D.gd, appc, 0, 2));
+      // fixed launch sequences before and after the GMRES solve: CUDA-graph replays
+      uint64_t key = hash_bytes(&D, sizeof(D));
+      {
+        const long long extra[8] = {k, dir, last, P.Ncap, P.Scap, pc, (long long)(size_t)status_dev, 0x616d};
+        key = hash_bytes(extra, sizeof(extra), key);
+      }
+      TT_TRY(run_captured(key ^ 0x1ull, s, [&]() -> tt_status {
+        plan_local<<<1, 1, 0, s>>>(D, k);
+        TT_TRY(launch_copy(D.cd, 1, P.Ncap, s));
+        TT_TRY(launch_copy(D.cd + 2, 1, P.Ncap, s));
+        return launch_caps(D.gd, appc, 0, 2);
+      }));
       TT_TRY(gmres_solve(gc, s));
+      TT_TRY(run_captured(key ^ 0x2ull, s, [&]() -> tt_status {
       track_res_kernel<<<1, 1, 0, s>>>(P.gst, D.dv, status_dev);
       track_dx_kernel<<<1, 256, 0, s>>>(D.iv, D.sol, D.xold, D.dv);
       if (last) {
         TT_TRY(launch_copy(D.cd + 1, 1, P.Ncap, s));
-        continue;
+        return TT_OK;
       }
       plan_svd<<<1, 1, 0, s>>>(D, k, dir);
       TT_TRY(launch_qr(D.qd, 1, s));
@@ -606,7 +615,8 @@ tt_status amen_solve_meta(const MatMeta &A, const VecMeta &b, const VecMeta &x, 
         TT_TRY(launch_gemm(D.gd + 11, 1, mb_, nb_, s));
       }
       TT_TRY(launch_copy(D.cd, 3, P.Scap, s));
-      TT_TRY(iface(k, dir));
+      return iface(k, dir);
+      }));
     }
     double hv[3] = {0.0, 0.0, 0.0};
     cudaMemcpyAsync(hv, D.dv, 3 * sizeof(double), cudaMemcpyDeviceToHost, s);
@@ -854,7 +864,8 @@ tt_status amen_mv_meta(const MatMeta &A, const VecMeta &b, const VecMeta &y, con
   };
   for (int k = d - 1; k >= 1; --k) TT_TRY(iface(k, -1));
   int dir = +1, sweep = 0;
-  for (sweep = 0; sweep < max_sweeps; ++sweep) {
+  // one sweep = a fixed launch sequence (device-resident sizes): replayed as a CUDA graph
+  auto one_sweep = [&]() -> tt_status {
     set_dv_kernel<<<1, 1, 0, s>>>(D.dv, 2, 0.0);
     for (int t = 0; t < d; ++t) {
       const int k = dir > 0 ? t : d - 1 - t;
@@ -904,6 +915,13 @@ tt_status amen_mv_meta(const MatMeta &A, const VecMeta &b, const VecMeta &y, con
       TT_TRY(launch_copy(D.cd, 3, P.Scap, s));
       TT_TRY(iface(k, dir));
     }
+    return TT_OK;
+  };
+  for (sweep = 0; sweep < max_sweeps; ++sweep) {
+    uint64_t key = hash_bytes(&D, sizeof(D));
+    const long long extra[5] = {dir, P.Ncap, P.Scap, P.pc, 0x6d76};
+    key = hash_bytes(extra, sizeof(extra), key);
+    TT_TRY(run_captured(key, s, one_sweep));
     double hv[3] = {0.0, 0.0, 0.0};
     cudaMemcpyAsync(hv, D.dv, 3 * sizeof(double), cudaMemcpyDeviceToHost, s);
     cudaStreamSynchronize(s);

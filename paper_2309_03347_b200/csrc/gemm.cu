@@ -310,7 +310,10 @@ tt_status launch_variant(const GemmDesc *descs_dev, int count, int Mcap, int Nca
 // CTA, so all CTAs take identical decisions and only grid barriers separate
 // the phases (6-7 per step instead of ~8 kernel launches).
 constexpr int GF_THREADS = 128;
-using GF = Cfg<64, 64, 16, 2, 2, 2>;
+#ifndef GF_BK
+#define GF_BK 16
+#endif
+using GF = Cfg<64, 64, GF_BK, 2, 2, 2>;   // persistent-kernel tiles: deeper K slices (fewer serial waits)
 constexpr int GF_LD = GM_MAX_M + 2;
 
 __device__ __forceinline__ void gbar(unsigned int *bar, unsigned int nblocks) {
@@ -391,7 +394,7 @@ __device__ void gemm_stage(const GemmDesc &g, double *split, long long split_ele
   }
   for (int t = blockIdx.x; t < T * splits; t += G) {
     const int z = t / T, tt = t - z * T;
-    gemm_tile<64, 64, 16, 2, 2, 2>(g, (tt % tm) * 64, (tt / tm) * 64, z, splits, split, g.M, (long long)g.M * g.N,
+    gemm_tile<64, 64, GF_BK, 2, 2, 2>(g, (tt % tm) * 64, (tt / tm) * 64, z, splits, split, g.M, (long long)g.M * g.N,
                                    smem);
     __syncthreads();
   }

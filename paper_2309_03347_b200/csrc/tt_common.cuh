@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stddef.h>
+#include <functional>
 #include <string>
 
 #include "tt.h"
@@ -98,6 +99,10 @@ tt_status launch_gemm(const GemmDesc *descs_dev, int count, int Mcap, int Ncap, 
 tt_status launch_gemm_k(const GemmDesc *descs_dev, int count, int Mcap, int Ncap, int Kcap, cudaStream_t s);
 // A dependent chain of `count` GEMMs (descriptor i consumes earlier outputs) with
 // per-GEMM capacity shapes: one thread-block-cluster launch when all are small.
+// CUDA-graph replay of a fixed launch sequence (graph.cu): `enqueue` launches on
+// `s` (taken by reference: it points at a private capture stream while recording).
+uint64_t hash_bytes(const void *p, size_t n, uint64_t h = 1469598103934665603ull);
+tt_status run_captured(uint64_t key, cudaStream_t &s, const std::function<tt_status()> &enqueue);
 tt_status launch_gemm_seq(const GemmDesc *descs_dev, int count, const int *Mcap, const int *Ncap, const int *Kcap,
                           cudaStream_t s);
 void set_gemm_scratch(double *ptr, size_t bytes);
