@@ -3,6 +3,8 @@
 // on the device, convergence flag in device memory.  The vector length N
 // follows the device-resident TT ranks; kernels early-exit once converged so
 // the host can enqueue a whole cycle without reading anything back.
+#include <cstdlib>
+
 #include "gmres.h"
 
 namespace tt {
@@ -183,7 +185,15 @@ __global__ void gm_clear_stop_kernel(GmState *st) {
 // drains.  Steps enqueued after the stop are no-ops (every kernel and the
 // apply GEMMs test the word).
 constexpr int GM_CHUNK = 6;
-constexpr int GM_FCHUNK = 5;   // Arnoldi steps per fused launch
+static int gm_fchunk() {        // Arnoldi steps per fused launch (TT_GM_FCHUNK)
+  static int c = 0;
+  if (!c) {
+    const char *e = std::getenv("TT_GM_FCHUNK");
+    c = e ? std::atoi(e) : 128;   // default: one launch per GMRES cycle (measured fastest)
+    c = c < 1 ? 1 : (c > 128 ? 128 : c);
+  }
+  return c;
+}
 
 struct PollSlots {
   int *flag = nullptr;         // pinned [2]
@@ -208,8 +218,8 @@ tt_status gmres_solve(const GmresCtx &c, cudaStream_t s) {
     gm_start_kernel<<<1, RT, 0, s>>>(c.st, c.b, c.w, c.V);
     int pending = -1;  // slot of the last enqueued poll copy
     if (fused) {
-      for (int j0 = 0, q = 0; j0 < c.m; j0 += GM_FCHUNK, ++q) {
-        const int j1 = j0 + GM_FCHUNK < c.m ? j0 + GM_FCHUNK : c.m;
+      for (int j0 = 0, q = 0; j0 < c.m; j0 += gm_fchunk(), ++q) {
+        const int j1 = j0 + gm_fchunk() < c.m ? j0 + gm_fchunk() : c.m;
         const int decide = c.cluster == 2;
         if (c.cluster != 0)
           TT_TRY(launch_gmres_chunk(c.st, c.gapp, c.V, c.ldv, c.w, c.part, c.split, c.split_elems, c.bar, j0, j1,
