@@ -266,6 +266,7 @@ using V64 = Variant<64, 64, 16, 2, 2, 2>;     // round-1 baseline
 using V64K = Variant<64, 64, 32, 2, 2, 3>;    // deeper K, 3 stages
 using V128 = Variant<128, 64, 16, 4, 2, 3>;   // 8 warps
 using V128S = Variant<128, 128, 16, 4, 2, 2>; // 8 warps, 32x64 warp tiles
+using V32 = Variant<32, 32, 16, 2, 2, 2>;     // small tiles for GEMMs that fill less than a wave
 
 int variant_id() {
   static int v = -1;
@@ -276,9 +277,32 @@ int variant_id() {
   return v;
 }
 
+int small_tiles_enabled() {
+  static int v = -1;
+  if (v < 0) v = std::getenv("TT_GEMM_NOSMALL") ? 0 : 1;
+  return v;
+}
+int small_tiles_waves() {   // use 32x32 tiles below this many 64x64 tiles
+  static int v = -1;
+  if (v < 0) { const char *e = std::getenv("TT_GEMM_SMALL_T"); v = e ? std::atoi(e) : 296; }
+  return v;
+}
+int small_tiles_kmax() {
+  static int v = -1;
+  if (v < 0) { const char *e = std::getenv("TT_GEMM_SMALL_K"); v = e ? std::atoi(e) : 256; }
+  return v;
+}
+
 template <class Vt>
 tt_status launch_variant(const GemmDesc *descs_dev, int count, int Mcap, int Ncap, int Kcap, cudaStream_t s) {
   const int tm = (Mcap + Vt::bm - 1) / Vt::bm, tn = (Ncap + Vt::bn - 1) / Vt::bn;
+  // less than one wave of 64x64 tiles and a short K (no split-K): 32x32 tiles (4x the CTAs)
+  if (Vt::bm == 64 && Vt::bn == 64 && small_tiles_enabled() && (long long)tm * tn * count < small_tiles_waves() &&
+      Kcap < small_tiles_kmax()) {
+    const int sm_ = (Mcap + 31) / 32, sn_ = (Ncap + 31) / 32;
+    V32::launch(dim3(sm_, sn_, count), descs_dev, 1, nullptr, 0, 0, s);
+    return check_launch("gemm_dmma small tiles");
+  }
   int splits = 1;
   if (count == 1 && Kcap >= 256 && (long long)tm * tn < 148) {
     splits = 296 / (tm * tn);
