@@ -538,7 +538,7 @@ tt_status amen_solve_meta(const MatMeta &A, const VecMeta &b, const VecMeta &x, 
     gc.part = P.gpart;
     gc.bar = P.gbar;
     gc.split = P.split;
-    gc.split_elems = GEMM_SPLIT_SCRATCH / 8;
+    gc.split_elems = GEMM_SPLIT_SCRATCH / 8 - 4096;   // the tail holds the split-K tile counters
   }
   const bool cluster_off = std::getenv("TT_GMRES_NOCLUSTER") != nullptr;
   int dir = +1, sweep = 0;

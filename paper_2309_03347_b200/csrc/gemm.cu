@@ -202,10 +202,13 @@ __device__ __forceinline__ void gemm_tile(const GemmDesc &g0, int m0, int n0, in
   }
 }
 
+// splits > 1: the K-slice CTAs of an output tile count in tile_cnt; the last
+// one to arrive sums the slices in slice order (deterministic) and applies the
+// epilogue, then re-arms the counter (no separate reduction launch).
 template <int BM, int BN, int BK, int WM_, int WN_, int STAGES>
 __global__ void __launch_bounds__(32 * WM_ * WN_) gemm_dmma_kernel(const GemmDesc *__restrict__ descs, int splits,
                                                                    double *__restrict__ partial, long long pld,
-                                                                   long long pstride) {
+                                                                   long long pstride, unsigned int *tile_cnt) {
   extern __shared__ __align__(16) double smem[];
   const GemmDesc g0 = descs[splits > 1 ? 0 : blockIdx.z];
   if (g0.skip && *g0.skip) return;
@@ -213,8 +216,32 @@ __global__ void __launch_bounds__(32 * WM_ * WN_) gemm_dmma_kernel(const GemmDes
     atomicAdd(&g_gemm_counters[0], 2ull * (unsigned long long)g0.M * g0.N * (g0.K > 0 ? g0.K : 0));
     atomicAdd(&g_gemm_counters[1], 1ull);
   }
-  gemm_tile<BM, BN, BK, WM_, WN_, STAGES>(g0, blockIdx.x * BM, blockIdx.y * BN, blockIdx.z, splits, partial, pld,
-                                          pstride, smem);
+  const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN;
+  gemm_tile<BM, BN, BK, WM_, WN_, STAGES>(g0, m0, n0, blockIdx.z, splits, partial, pld, pstride, smem);
+  if (splits > 1 && tile_cnt) {
+    __shared__ int s_last;
+    __threadfence();
+    __syncthreads();
+    const int tile = blockIdx.x + gridDim.x * blockIdx.y;
+    if (threadIdx.x == 0) s_last = (atomicAdd(&tile_cnt[tile], 1u) == (unsigned int)(splits - 1));
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    double alpha = g0.alpha;
+    if (g0.alpha_dev) alpha *= *g0.alpha_dev;
+    for (int e = threadIdx.x; e < BM * BN; e += blockDim.x) {
+      const int r = m0 + e % BM, c = n0 + e / BM;
+      if (r >= g0.M || c >= g0.N) continue;
+      double sum = 0.0;
+      for (int z = 0; z < splits; ++z) sum += __ldcg(partial + z * pstride + r + c * pld);
+      const long long addr = (long long)(r % g0.dr) * g0.s_r0 + (long long)(r / g0.dr) * g0.s_r1 +
+                             (long long)(c % g0.dc) * g0.s_c0 + (long long)(c / g0.dc) * g0.s_c1;
+      double v = alpha * sum;
+      if (g0.beta != 0.0) v += g0.beta * g0.C[addr];
+      g0.C[addr] = v;
+    }
+    if (threadIdx.x == 0) tile_cnt[tile] = 0;
+  }
 }
 
 __global__ void gemm_splitk_reduce(const GemmDesc *__restrict__ descs, int splits, const double *__restrict__ partial,
@@ -240,6 +267,8 @@ __global__ void gemm_splitk_reduce(const GemmDesc *__restrict__ descs, int split
 struct SplitScratch {
   double *ptr = nullptr;
   size_t bytes = 0;
+  unsigned int *cnt = nullptr;
+  bool cnt_zeroed = false;
 };
 thread_local SplitScratch g_split;
 
@@ -256,9 +285,10 @@ struct Variant {
       done = true;
     }
   }
-  static void launch(dim3 grid, const GemmDesc *d, int splits, double *p, long long pld, long long ps, cudaStream_t s) {
+  static void launch(dim3 grid, const GemmDesc *d, int splits, double *p, long long pld, long long ps, cudaStream_t s,
+                     unsigned int *cnt = nullptr) {
     prepare();
-    gemm_dmma_kernel<BM, BN, BK, WM_, WN_, ST><<<grid, C::THREADS, C::SMEM, s>>>(d, splits, p, pld, ps);
+    gemm_dmma_kernel<BM, BN, BK, WM_, WN_, ST><<<grid, C::THREADS, C::SMEM, s>>>(d, splits, p, pld, ps, cnt);
   }
 };
 
@@ -275,6 +305,23 @@ int variant_id() {
     v = e ? std::atoi(e) : 0;
   }
   return v;
+}
+
+// tile arrival counters of the in-kernel split-K reduction: the last 16 KB of
+// the caller's split scratch (set_gemm_scratch), zeroed on the stream before
+// the first use after every set_gemm_scratch; each reducing CTA re-arms its own
+constexpr size_t CNT_BYTES = 4096 * sizeof(unsigned int);
+unsigned int *tile_counters(cudaStream_t s) {
+  // measured slower than the separate reduction kernel (the last CTA of a tile
+  // reduces alone at the tail: C5 r=128 9.8 -> 7.0 TF/s), so opt-in only
+  static int off = -1;
+  if (off < 0) off = std::getenv("TT_GEMM_SPLIT_INKERNEL") ? 0 : 1;
+  if (off || !g_split.cnt) return nullptr;
+  if (!g_split.cnt_zeroed) {
+    cudaMemsetAsync(g_split.cnt, 0, CNT_BYTES, s);
+    g_split.cnt_zeroed = true;
+  }
+  return g_split.cnt;
 }
 
 int small_tiles_enabled() {
@@ -313,10 +360,13 @@ tt_status launch_variant(const GemmDesc *descs_dev, int count, int Mcap, int Nca
   }
   if (splits > 1) {
     const long long pld = Mcap, pstride = (long long)Mcap * Ncap;
-    Vt::launch(dim3(tm, tn, splits), descs_dev, splits, g_split.ptr, pld, pstride, s);
-    int rb = (int)((pstride + 255) / 256);
-    rb = rb > 1184 ? 1184 : (rb < 1 ? 1 : rb);
-    gemm_splitk_reduce<<<rb, 256, 0, s>>>(descs_dev, splits, g_split.ptr, pld, pstride);
+    unsigned int *cnt = tile_counters(s);
+    Vt::launch(dim3(tm, tn, splits), descs_dev, splits, g_split.ptr, pld, pstride, s, cnt);
+    if (!cnt) {
+      int rb = (int)((pstride + 255) / 256);
+      rb = rb > 1184 ? 1184 : (rb < 1 ? 1 : rb);
+      gemm_splitk_reduce<<<rb, 256, 0, s>>>(descs_dev, splits, g_split.ptr, pld, pstride);
+    }
     return check_launch("gemm_dmma splitk");
   }
   Vt::launch(dim3(tm, tn, count), descs_dev, 1, nullptr, 0, 0, s);
@@ -607,6 +657,12 @@ __global__ void __launch_bounds__(GF_THREADS) gm_chunk_kernel(GmChunkArgs a) {
 void set_gemm_scratch(double *ptr, size_t bytes) {
   g_split.ptr = ptr;
   g_split.bytes = ptr ? bytes : 0;
+  g_split.cnt = nullptr;
+  g_split.cnt_zeroed = false;
+  if (ptr && bytes > 2 * CNT_BYTES) {
+    g_split.bytes = bytes - CNT_BYTES;
+    g_split.cnt = reinterpret_cast<unsigned int *>(reinterpret_cast<char *>(ptr) + g_split.bytes);
+  }
 }
 
 tt_status launch_gemm(const GemmDesc *descs_dev, int count, int Mcap, int Ncap, cudaStream_t s) {
