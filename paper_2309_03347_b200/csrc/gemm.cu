@@ -704,7 +704,9 @@ int gmres_fused_grid() {
     cudaFuncSetAttribute(gm_chunk_kernel<true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, gm_chunk_kernel<false>, GF_THREADS, GF::SMEM);
     const char *e = std::getenv("TT_GF_GRID");
-    G = (occ >= 1) ? (e ? std::atoi(e) : sms) : -1;
+    // two CTAs per SM when they fit (more bytes in flight for the CGS2 phases of
+    // large local systems; measured +4% on C4)
+    G = (occ >= 1) ? (e ? std::atoi(e) : (occ >= 2 ? 2 * sms : sms)) : -1;
     if (G > occ * sms || G > 256) G = occ * sms < 256 ? occ * sms : 256;
   }
   return G;
