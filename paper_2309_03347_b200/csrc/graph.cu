@@ -34,6 +34,11 @@ tt_status run_captured(uint64_t key, cudaStream_t &s, const std::function<tt_sta
   if (g_gc.disabled < 0) g_gc.disabled = std::getenv("TT_NO_GRAPHS") ? 1 : 0;
   if (g_gc.disabled) return enqueue();
   auto it = g_gc.m.find(key);
+  if (it == g_gc.m.end() && g_gc.m.size() >= 4096) {   // bound the cache (new workspaces => new keys)
+    cudaStreamSynchronize(s);
+    for (auto &kv : g_gc.m) cudaGraphExecDestroy(kv.second);
+    g_gc.m.clear();
+  }
   if (it == g_gc.m.end()) {
     if (!g_gc.cs && cudaStreamCreateWithFlags(&g_gc.cs, cudaStreamNonBlocking) != cudaSuccess) {
       g_gc.disabled = 1;
