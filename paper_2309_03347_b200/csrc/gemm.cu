@@ -350,10 +350,16 @@ tt_status launch_variant(const GemmDesc *descs_dev, int count, int Mcap, int Nca
     V32::launch(dim3(sm_, sn_, count), descs_dev, 1, nullptr, 0, 0, s);
     return check_launch("gemm_dmma small tiles");
   }
+  static int tgt = -1, kmin = -1;
+  if (tgt < 0) {
+    const char *a = std::getenv("TT_SPLIT_TARGET"), *b = std::getenv("TT_SPLIT_KMIN");
+    tgt = a ? std::atoi(a) : 296;     // aim for ~2 waves of CTAs
+    kmin = b ? std::atoi(b) : 64;     // minimum K per slice (64 measured best: C5 r=128, C1)
+  }
   int splits = 1;
-  if (count == 1 && Kcap >= 256 && (long long)tm * tn < 148) {
-    splits = 296 / (tm * tn);
-    splits = splits > Kcap / 128 ? Kcap / 128 : splits;
+  if (count == 1 && Kcap >= 2 * kmin && (long long)tm * tn < 148) {
+    splits = tgt / (tm * tn);
+    splits = splits > Kcap / kmin ? Kcap / kmin : splits;
     splits = splits > 16 ? 16 : splits;
     const size_t need = (size_t)splits * Mcap * Ncap * sizeof(double);
     if (splits < 2 || !g_split.ptr || need > g_split.bytes) splits = 1;
