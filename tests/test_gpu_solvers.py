@@ -338,3 +338,35 @@ def test_transport_operator_sampled_full_size(cfg):
         scale = max(np.abs(ref).max(), 1e-300)
         assert np.max(np.abs(got - ref)) <= 1e-10 * scale, (key, np.max(np.abs(got - ref)) / scale)
         del y
+
+
+_DET_SCRIPT = r"""
+import numpy as np, torch, inputs
+import paper_2309_03347_b200 as tb
+from paper_2309_03347_b200 import transport as gtr
+p = inputs.problem_c1(); ops = gtr.operators(p); modes = [8, 8, 8, 8, 1]
+g = inputs.rng(61)
+psi = tb.TTVec.from_cores([np.ones((1, n, 1)) for n in modes], rcap=[1, 68, 68, 68, 68, 1])
+z = tb.TTVec.from_cores(inputs.random_tt(g, modes, [1, 4, 4, 4, 4, 1]))
+r = tb.keff_fixed_point(ops["H"], ops["S"], ops["F"], psi, z, tol_k=1e-12, eps_round=1e-13, eps_solve=1e-12,
+                        rmax=64, matvec="amen_mv")
+torch.cuda.synchronize()
+print(repr(r.k.item()), r.iters.item())
+"""
+
+
+def test_keff_deterministic_graphs_on_off():
+    """The device path is deterministic (fixed reduction orders, no atomics in the
+    arithmetic): two C1 solves give bitwise-identical k, and replaying the
+    captured CUDA graphs gives the same bits as direct launches (TT_NO_GRAPHS=1)."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for env_extra in ({}, {}, {"TT_NO_GRAPHS": "1"}):
+        env = dict(os.environ, PYTHONPATH=root, **env_extra)
+        r = subprocess.run([sys.executable, "-c", _DET_SCRIPT], capture_output=True, text=True, env=env, cwd=root,
+                           timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        outs.append(r.stdout.strip().splitlines()[-1])
+    assert outs[0] == outs[1] == outs[2], outs
