@@ -159,6 +159,29 @@ def oracle_c1_sample(iters=3):
     return iters / dt, dt
 
 
+def count_kernels(run):
+    """Exact kernel count of one more (untimed) step: CUPTI activity records,
+    graph-replayed kernels included (paper_2309_03347_b200/liblaunchcount.so).
+    Returns (libtt kernels, all kernels) or None if CUPTI is unavailable."""
+    import ctypes as C
+    import torch
+    path = os.path.join(ROOT, "paper_2309_03347_b200", "liblaunchcount.so")
+    if not os.path.exists(path):
+        return None
+    try:
+        lc = C.CDLL(path)
+        torch.cuda.synchronize()
+        if lc.lc_start() != 0:
+            return None
+        run()
+        torch.cuda.synchronize()
+        a, o = C.c_ulonglong(0), C.c_ulonglong(0)
+        lc.lc_stop(C.byref(a), C.byref(o))
+        return int(o.value), int(a.value)
+    except OSError:
+        return None
+
+
 def cpu_cores():
     try:
         import threadpoolctl
@@ -312,10 +335,13 @@ def main():
                                "gemm_calls": ngemm / args.steps},
             "roofline": roof, "e2e": e2e, "clocks": clk.summary(),
             "gpu_launches": None, "wall_s": wall}
-    line["gpu_launches"] = int((1.8 * max(ngemm - 3 * ffl[2], 0) + fl.value) / args.steps)
-    line["gpu_launches_how"] = ("estimate per step: fused GMRES launches (counted) + 1.8 x stand-alone GEMM "
-                                "launches (counted on the device; the other kernels per GEMM calibrated from the "
-                                "ncu launch list in profiles/r01)")
+    kc = count_kernels(lambda: c1_step_device(st))
+    line["gpu_launches"] = kc[0] if kc else int((1.8 * max(ngemm - 3 * ffl[2], 0) + fl.value) / args.steps)
+    line["gpu_launches_how"] = ("libtt kernels executed by one more identical step, counted exactly by CUPTI "
+                                "activity records (graph-replayed kernels included)" if kc else
+                                "estimate: fused GMRES launches + 1.8 x stand-alone GEMM launches")
+    if kc:
+        line["gpu_launches_all_kernels"] = kc[1]
     if rank == 0 and not args.no_cpu_baseline:
         v, dt = oracle_c1_sample(iters=3)
         line["cpu_baseline"] = {"value": v, "unit": "iter/s", "cores": cpu_cores(), "kind": "oracle",
@@ -390,7 +416,8 @@ def micro_bench(args, tb, device, world, dist):
                              "bound": "tensor", "achieved": gfl / 1e3, "peak": peak / 1e3, "unit": "TFLOP/s",
                              "frac": gfl / peak, "peak_src": "measured FP64 DMMA sustained (tools/peaks_fp64)",
                              "traffic": None},
-                "clocks": clk.summary(), "gpu_launches": 80 * 8}
+                "clocks": clk.summary(), "gpu_launches": (count_kernels(run) or (80 * 8, 0))[0],
+                "gpu_launches_how": "libtt kernels of one more double sweep (CUPTI activity records)"}
     # c2
     inst = inputs.c2_instance(args.seed)
     A = tb.TTMat.from_cores(inst["A"], device=device)
@@ -458,7 +485,10 @@ def micro_bench(args, tb, device, world, dist):
                          "bytes_per_launch": bbytes,
                          "timing": "CUDA events around the descriptor upload + kernel; the host-side "
                                    "enqueue overlaps a preceding GPU sleep"},
-            "clocks": clk.summary()}
+            "clocks": clk.summary(),
+            "gpu_launches": (count_kernels(lambda: (tb.tt_matvec(A, X, Y), tb.tt_copy(Y, Yr),
+                                                    tb.tt_round(Yr, 1e-8, 128))) or (None,))[0],
+            "gpu_launches_how": "libtt kernels of one more matvec + copy + round (CUPTI activity records)"}
 
 
 def c3_bench(args, tb, device, world, dist):
@@ -564,7 +594,8 @@ def c3_bench(args, tb, device, world, dist):
             "flops_per_step": {"gemm": gemm_flops / args.steps, "qr": qr_flops / args.steps,
                                "jacobi": svd_flops / args.steps, "gemm_calls": ngemm / args.steps},
             "roofline": roof, "clocks": clk.summary(),
-            "gpu_launches": count_launches_estimate(ngemm / args.steps, iters / args.steps)}
+            "gpu_launches": (count_kernels(step) or (count_launches_estimate(ngemm / args.steps, 0), 0))[0],
+            "gpu_launches_how": "libtt kernels of one more identical step (CUPTI activity records)"}
 
 
 def count_launches_estimate(gemm_calls, iters):

@@ -47,7 +47,27 @@ def build(force=False, verbose=False, jobs=8):
     out = subprocess.run(cmd, capture_output=True, text=True)
     if out.returncode != 0:
         raise RuntimeError("link failed:\n" + out.stdout + out.stderr)
+    build_launch_counter()
     return LIB
+
+
+LC_SRC = os.path.join(HERE, "tools_src", "launch_count.cpp")
+LC_LIB = os.path.join(HERE, "liblaunchcount.so")
+
+
+def build_launch_counter():
+    """CUPTI kernel counter used by bench.py for gpu_launches (measurement only)."""
+    cuda = os.environ.get("CUDA_HOME", "/usr/local/cuda")
+    inc = os.path.join(cuda, "targets", "x86_64-linux", "include")
+    lib = os.path.join(cuda, "targets", "x86_64-linux", "lib")
+    if not os.path.exists(os.path.join(inc, "cupti.h")):
+        return None
+    cmd = ["g++", "-O2", "-shared", "-fPIC", "-std=c++17", "-I", inc, LC_SRC, "-o", LC_LIB, "-L", lib, "-lcupti",
+           f"-Wl,-rpath,{lib}"]
+    out = subprocess.run(cmd, capture_output=True, text=True)
+    if out.returncode != 0:
+        raise RuntimeError("launch counter build failed:\n" + out.stdout + out.stderr)
+    return LC_LIB
 
 
 def _drain(procs):
