@@ -18,6 +18,10 @@ namespace {
 
 constexpr int QR_THREADS = 256;
 constexpr int NB = 32;
+// panels of up to QR_PANEL_ROWS rows are factorised in shared memory (the
+// per-column reductions and updates then never touch L2)
+constexpr int QR_PANEL_ROWS = 640;
+constexpr size_t QR_PANEL_SMEM = (size_t)QR_PANEL_ROWS * NB * sizeof(double);
 
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
@@ -43,8 +47,13 @@ __device__ double block_sum(double v, double *red) {
 __device__ void apply_block_reflector(int m, int j0, int jb, const double *A, long long lda,
                                       const double (*sT)[NB + 1], int transT, double *X, long long rs,
                                       long long cs, int c_begin, int c_end, double (*sV)[NB + 1],
-                                      double (*sX)[NB + 1], double (*sW)[NB + 1]) {
+                                      double (*sX)[NB + 1], double (*sW)[NB + 1], const double *Vsm = nullptr,
+                                      int vld = 0) {
   const int tid = threadIdx.x;
+  // V element (r, l): from the shared-memory panel copy when given (rows from j0)
+  auto vget = [&](int r, int l) -> double {
+    return Vsm ? Vsm[(r - j0) + (long long)l * vld] : A[r + (long long)(j0 + l) * lda];
+  };
   for (int cb = c_begin; cb < c_end; cb += NB) {
     const int cw = min(NB, c_end - cb);
     // W = V^T X  (jb x cw), accumulated over 32-row chunks
@@ -57,7 +66,7 @@ __device__ void apply_block_reflector(int m, int j0, int jb, const double *A, lo
         double v = 0.0;
         if (rr < rh && l < jb) {
           const int dg = j0 + l;
-          v = (r > dg) ? A[r + (long long)(j0 + l) * lda] : (r == dg ? 1.0 : 0.0);
+          v = (r > dg) ? vget(r, l) : (r == dg ? 1.0 : 0.0);
         }
         sV[rr][l] = v;
         const int c = cb + l;
@@ -111,7 +120,7 @@ __device__ void apply_block_reflector(int m, int j0, int jb, const double *A, lo
         double v = 0.0;
         if (rr < rh && l < jb) {
           const int dg = j0 + l;
-          v = (r > dg) ? A[r + (long long)(j0 + l) * lda] : (r == dg ? 1.0 : 0.0);
+          v = (r > dg) ? vget(r, l) : (r == dg ? 1.0 : 0.0);
         }
         sV[rr][l] = v;
       }
@@ -155,12 +164,26 @@ __global__ void __launch_bounds__(QR_THREADS) qr_kernel(const QRDesc *__restrict
   }
   __syncthreads();
 
+  extern __shared__ double sP[];   // panel copy (rows j0..m-1) when it fits
   for (int j0 = 0; j0 < kmin; j0 += NB) {
     const int jb = min(NB, kmin - j0);
+    const int pr = m - j0;                           // panel rows
+    const bool in_smem = pr <= QR_PANEL_ROWS;
+    if (in_smem) {
+      for (int e = tid; e < pr * jb; e += QR_THREADS) {
+        const int r = e % pr, l = e / pr;
+        sP[r + l * pr] = A[j0 + r + (long long)(j0 + l) * lda];
+      }
+      __syncthreads();
+    }
+    // panel column j of the working matrix: element i at colp[i] (global) or sP (shifted by j0)
+    auto colp = [&](int j) -> double * {
+      return in_smem ? sP + (long long)(j - j0) * pr - j0 : A + (long long)j * lda;
+    };
     // ---- panel factorisation (unblocked, Householder per column)
     for (int jj = 0; jj < jb; ++jj) {
       const int j = j0 + jj;
-      double *col = A + (long long)j * lda;
+      double *col = colp(j);
       double part = 0.0;
       for (int i = j + 1 + tid; i < m; i += QR_THREADS) part = fma(col[i], col[i], part);
       const double sigma = block_sum(part, red);
@@ -188,7 +211,7 @@ __global__ void __launch_bounds__(QR_THREADS) qr_kernel(const QRDesc *__restrict
       if (tid == 0) col[j] = s_beta;
       if (tau != 0.0) {
         for (int c = j + 1 + warp; c < j0 + jb; c += NW) {
-          double *cc = A + (long long)c * lda;
+          double *cc = colp(c);
           double w = 0.0;
           for (int i = j + lane; i < m; i += 32) w = fma(i == j ? 1.0 : col[i], cc[i], w);
           w = warp_sum(w) * tau;
@@ -202,8 +225,8 @@ __global__ void __launch_bounds__(QR_THREADS) qr_kernel(const QRDesc *__restrict
     for (int pidx = warp; pidx < jb * jb; pidx += NW) {
       const int l = pidx % jb, i = pidx / jb;
       if (l < i) {
-        const double *vl = A + (long long)(j0 + l) * lda;
-        const double *vi = A + (long long)(j0 + i) * lda;
+        const double *vl = colp(j0 + l);
+        const double *vi = colp(j0 + i);
         double s = 0.0;
         for (int r = j0 + i + 1 + lane; r < m; r += 32) s = fma(vl[r], vi[r], s);
         s = warp_sum(s);
@@ -228,13 +251,21 @@ __global__ void __launch_bounds__(QR_THREADS) qr_kernel(const QRDesc *__restrict
       }
     }
     __syncthreads();
+    if (in_smem) {   // panel back to the working matrix (V below the diagonal, R on/above)
+      for (int e = tid; e < pr * jb; e += QR_THREADS) {
+        const int r = e % pr, l = e / pr;
+        A[j0 + r + (long long)(j0 + l) * lda] = sP[r + l * pr];
+      }
+      __syncthreads();
+    }
     // keep T for the Q formation
     double *Tg = g.T + (long long)(j0 / NB) * NB * NB;
     for (int e = tid; e < NB * NB; e += QR_THREADS) Tg[e] = sT[e % NB][e / NB];
     __syncthreads();
     // ---- trailing update: A[:, j0+jb:n] <- (I - V T V^T)^T A = A - V T^T (V^T A)
     if (j0 + jb < n)
-      apply_block_reflector(m, j0, jb, A, lda, sT, 1, A, 1, lda, j0 + jb, n, sV, sX, sW);
+      apply_block_reflector(m, j0, jb, A, lda, sT, 1, A, 1, lda, j0 + jb, n, sV, sX, sW, in_smem ? sP : nullptr,
+                            pr);
     __syncthreads();
   }
   // ---- R
@@ -258,8 +289,16 @@ __global__ void __launch_bounds__(QR_THREADS) qr_kernel(const QRDesc *__restrict
       const int j0 = pnl * NB, jb = min(NB, kmin - j0);
       const double *Tg = g.T + (long long)pnl * NB * NB;
       for (int e = tid; e < NB * NB; e += QR_THREADS) sT[e % NB][e / NB] = Tg[e];
+      const int pr = m - j0;
+      const bool in_smem = pr <= QR_PANEL_ROWS;
+      if (in_smem)
+        for (int e = tid; e < pr * jb; e += QR_THREADS) {
+          const int r = e % pr, l = e / pr;
+          sP[r + l * pr] = A[j0 + r + (long long)(j0 + l) * lda];
+        }
       __syncthreads();
-      apply_block_reflector(m, j0, jb, A, lda, sT, 0, g.Q, g.q_rs, g.q_cs, j0, kmin, sV, sX, sW);
+      apply_block_reflector(m, j0, jb, A, lda, sT, 0, g.Q, g.q_rs, g.q_cs, j0, kmin, sV, sX, sW,
+                            in_smem ? sP : nullptr, pr);
       __syncthreads();
     }
   }
@@ -577,7 +616,12 @@ void linalg_counters(unsigned long long *out, int reset) {
 
 tt_status launch_qr(const QRDesc *descs_dev, int count, cudaStream_t s) {
   if (count <= 0) return TT_OK;
-  qr_kernel<<<count, QR_THREADS, 0, s>>>(descs_dev);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(qr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)QR_PANEL_SMEM);
+    attr = true;
+  }
+  qr_kernel<<<count, QR_THREADS, QR_PANEL_SMEM, s>>>(descs_dev);
   return check_launch("qr");
 }
 
