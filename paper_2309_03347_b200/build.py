@@ -11,7 +11,7 @@ INC = os.path.join(os.path.dirname(HERE), "include")
 LIB = os.path.join(HERE, "libtt.so")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
-         "-Xptxas", "-O3"]
+         "-Xptxas", "-O3"] + os.environ.get("TT_NVCC_EXTRA", "").split()   # experiments only
 
 
 def sources():

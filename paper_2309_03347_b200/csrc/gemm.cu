@@ -94,6 +94,74 @@ __device__ __forceinline__ void load_tile(double *sa, double *sb, const GemmDesc
 // splits > 1: split-K; CTA z computes the K-slice z and writes its raw partial
 // product to partial + z * pstride (column-major, ld = pld); gemm_splitk_reduce
 // sums the slices and applies the epilogue (deterministic order).
+
+// Latency-oriented 64x64 tile for short K (persistent kernels): the DMMA
+// fragments are read straight from global memory (L2) with all loads of a
+// k-block in flight, no shared-memory staging and no block barriers.
+__device__ __forceinline__ void gemm_tile_direct(const GemmDesc &g, int m0, int n0) {
+  if (m0 >= g.M || n0 >= g.N) return;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int wm = m0 + (warp % 2) * 32, wn = n0 + (warp / 2) * 32;
+  const int ar = lane >> 2, kq = lane & 3;
+  double acc[4][4][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  const double *A = g.A, *B = g.B;
+  const long long lda = g.lda, ldb = g.ldb;
+  for (int k0 = 0; k0 < g.K; k0 += 16) {
+    double af[4][4], bf[4][4];
+#pragma unroll
+    for (int kk = 0; kk < 4; ++kk) {
+      const int k = k0 + kk * 4 + kq;
+      const bool kin = k < g.K;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int mrow = wm + i * 8 + ar;
+        const bool p = kin && mrow < g.M;
+        af[kk][i] = p ? __ldg(g.transA ? A + k + (long long)mrow * lda : A + mrow + (long long)k * lda) : 0.0;
+        const int ncol = wn + i * 8 + ar;
+        const bool q = kin && ncol < g.N;
+        bf[kk][i] = q ? __ldg(g.transB ? B + ncol + (long long)k * ldb : B + k + (long long)ncol * ldb) : 0.0;
+      }
+    }
+#pragma unroll
+    for (int kk = 0; kk < 4; ++kk)
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dmma(acc[i][j][0], acc[i][j][1], af[kk][i], bf[kk][j]);
+  }
+  double alpha = g.alpha;
+  if (g.alpha_dev) alpha *= *g.alpha_dev;
+  const double beta = g.beta;
+  long long coff[4][2];
+#pragma unroll
+  for (int j = 0; j < 4; ++j)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int c = wn + j * 8 + kq * 2 + h;
+      coff[j][h] = (c < g.N) ? (long long)(c % g.dc) * g.s_c0 + (long long)(c / g.dc) * g.s_c1 : -1;
+    }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int r = wm + i * 8 + ar;
+    if (r >= g.M) continue;
+    const long long roff = (long long)(r % g.dr) * g.s_r0 + (long long)(r / g.dr) * g.s_r1;
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        if (coff[j][h] < 0) continue;
+        const long long addr = roff + coff[j][h];
+        double v = alpha * acc[i][j][h];
+        if (beta != 0.0) v += beta * g.C[addr];
+        g.C[addr] = v;
+      }
+  }
+}
+
 // One output tile (m0, n0) of the K-slice z (splits > 1) or of the whole K.
 template <int BM, int BN, int BK, int WM_, int WN_, int STAGES>
 __device__ __forceinline__ void gemm_tile(const GemmDesc &g0, int m0, int n0, int z, int splits,
@@ -393,8 +461,11 @@ constexpr int GF_THREADS = 128;
 #ifndef GF_BK
 #define GF_BK 16
 #endif
-using GF = Cfg<64, 64, GF_BK, 2, 2, 2>;   // persistent-kernel tiles: deeper K slices (fewer serial waits)
+using GF = Cfg<64, 64, GF_BK, 2, 2, 2>;   // persistent-kernel tiles
 constexpr int GF_LD = GM_MAX_M + 2;
+// dynamic shared memory of the fused kernel: GEMM tile buffers + the apply
+// descriptors of up to GM_MAX_M steps
+constexpr size_t GM_SMEM = GF::SMEM + (size_t)3 * GM_MAX_M * sizeof(GemmDesc);
 
 __device__ __forceinline__ void gbar(unsigned int *bar, unsigned int nblocks) {
   __syncthreads();
@@ -451,14 +522,17 @@ __device__ __forceinline__ void phase_sync(unsigned int *bar, unsigned int nbloc
   }
 }
 
+__constant__ int c_gm_direct_kmax = 0;       // K bound of the direct (unstaged) tile
+__device__ __forceinline__ int gm_direct_kmax() { return c_gm_direct_kmax; }
+
 // One GEMM as a phase of a persistent kernel: DMMA tiles distributed over the
 // CTAs (split-K with an in-kernel reduction when the GEMM has few tiles), then a
 // phase barrier.  Uniform control flow: every CTA reads the same descriptor.
 template <bool CLUSTER>
 __device__ void gemm_stage(const GemmDesc &g, double *split, long long split_elems, unsigned int *bar, int G,
-                           double *smem, bool gm_count) {
+                           double *smem, bool gm_count, bool check_skip = true) {
   if (g.M <= 0 || g.N <= 0) return;
-  if (g.skip && *g.skip) return;
+  if (check_skip && g.skip && *g.skip) return;
   const int tid = threadIdx.x;
   const int tm = (g.M + 63) / 64, tn = (g.N + 63) / 64, T = tm * tn;
   int splits = 1;
@@ -472,11 +546,27 @@ __device__ void gemm_stage(const GemmDesc &g, double *split, long long split_ele
     atomicAdd(&g_gemm_counters[1], 1ull);
     if (gm_count) atomicAdd(&g_gm_counters[0], f);
   }
-  for (int t = blockIdx.x; t < T * splits; t += G) {
-    const int z = t / T, tt = t - z * T;
-    gemm_tile<64, 64, GF_BK, 2, 2, 2>(g, (tt % tm) * 64, (tt / tm) * 64, z, splits, split, g.M, (long long)g.M * g.N,
-                                   smem);
-    __syncthreads();
+  const bool direct = splits == 1 && g.K <= gm_direct_kmax();
+  // small GEMMs (fewer 64x64 tiles than CTAs, or a thin M): 32x32 tiles waste
+  // less of the DMMA work on padding and spread over more CTAs
+  const bool small = splits == 1 && !direct && (T < G || g.M <= 32);
+  if (small) {
+    const int sm_ = (g.M + 31) / 32, sn_ = (g.N + 31) / 32;
+    for (int t = blockIdx.x; t < sm_ * sn_; t += G) {
+      gemm_tile<32, 32, 16, 2, 2, 2>(g, (t % sm_) * 32, (t / sm_) * 32, 0, 1, nullptr, 0, 0, smem);
+      __syncthreads();
+    }
+  } else {
+    for (int t = blockIdx.x; t < T * splits; t += G) {
+      const int z = t / T, tt = t - z * T;
+      if (direct) {
+        gemm_tile_direct(g, (tt % tm) * 64, (tt / tm) * 64);
+      } else {
+        gemm_tile<64, 64, GF_BK, 2, 2, 2>(g, (tt % tm) * 64, (tt / tm) * 64, z, splits, split, g.M,
+                                          (long long)g.M * g.N, smem);
+        __syncthreads();
+      }
+    }
   }
   phase_sync<CLUSTER>(bar, G);
   if (splits > 1) {
@@ -534,11 +624,34 @@ __global__ void __launch_bounds__(GF_THREADS) gm_chunk_kernel(GmChunkArgs a) {
   constexpr int NW = GF_THREADS / 32;
   double *part1 = a.part, *part2 = a.part + (size_t)G * GF_LD, *part3 = a.part + 2 * (size_t)G * GF_LD;
   double *w = a.w;
-  for (int j = a.j0; j < a.j1 && j < m; ++j) {
+#ifdef GM_PHASE_TIMING
+  long long ph[6] = {0, 0, 0, 0, 0, 0};
+  long long tcl = clock64();
+#define GM_PH(i) do { const long long t_ = clock64(); ph[i] += t_ - tcl; tcl = t_; } while (0)
+#else
+#define GM_PH(i) do { } while (0)
+#endif
+  // the apply descriptors of every step of this launch, staged once in shared
+  // memory (one parallel load instead of a dependent L2 read per GEMM stage)
+  const int jend = min(a.j1, m);
+  GemmDesc *sdesc = reinterpret_cast<GemmDesc *>(smem + GF::SMEM / sizeof(double));
+  {
+    const int nd = 3 * max(jend - a.j0, 0);
+    const long long nw = (long long)nd * sizeof(GemmDesc) / sizeof(long long);
+    const long long *src = reinterpret_cast<const long long *>(a.gapp + 3 * (a.j0 + 1));
+    long long *dst = reinterpret_cast<long long *>(sdesc);
+    for (long long e = threadIdx.x; e < nw; e += GF_THREADS) dst[e] = src[e];
+    __syncthreads();
+  }
+  int nsteps = 0;
+  for (int j = a.j0; j < jend; ++j) {
     if (j > a.j0) phase_sync<CLUSTER>(a.bar, G);            // V[:, j] of the previous step complete
-    // ---- w = A V[:, j] (three chained GEMM stages)
+    GM_PH(0);
+    ++nsteps;
+    // ---- w = A V[:, j] (three chained GEMM stages; the kernel itself stops on the stop word)
     for (int sidx = 0; sidx < 3; ++sidx)
-      gemm_stage<CLUSTER>(a.gapp[3 * (j + 1) + sidx], a.split, a.split_elems, a.bar, G, smem, true);
+      gemm_stage<CLUSTER>(sdesc[3 * (j - a.j0) + sidx], a.split, a.split_elems, a.bar, G, smem, true, false);
+    GM_PH(1);
     // ---- CGS2 pass 1: slice dots
     double *my1 = part1 + (size_t)blockIdx.x * GF_LD;
     for (int i = warp; i <= j; i += NW) {
@@ -549,6 +662,7 @@ __global__ void __launch_bounds__(GF_THREADS) gm_chunk_kernel(GmChunkArgs a) {
       if (lane == 0) my1[i] = sacc;
     }
     phase_sync<CLUSTER>(a.bar, G);
+    GM_PH(2);
     for (int i = warp; i <= j; i += NW) {      // cross-CTA sums: one warp per entry, fixed order
       double sacc = 0.0;
       for (int c = lane; c < G; c += 32) sacc += part1[(size_t)c * GF_LD + i];
@@ -598,6 +712,7 @@ __global__ void __launch_bounds__(GF_THREADS) gm_chunk_kernel(GmChunkArgs a) {
       part3[(size_t)blockIdx.x * GF_LD] = t;
     }
     phase_sync<CLUSTER>(a.bar, G);
+    GM_PH(3);
     // ---- norm, Givens (identical in every CTA), normalisation
     if (warp == 0) {
       double hn2 = 0.0;
@@ -654,8 +769,13 @@ __global__ void __launch_bounds__(GF_THREADS) gm_chunk_kernel(GmChunkArgs a) {
       double *vn = a.V + (long long)(j + 1) * a.ldv;
       for (int e = lo + tid; e < hi; e += GF_THREADS) vn[e] = w[e] * inv;
     }
+    GM_PH(4);
     if (stop) break;
   }
+#ifdef GM_PHASE_TIMING
+  if (blockIdx.x == 0 && threadIdx.x == 0 && nsteps > 0)
+    printf("GMPH %d %d %lld %lld %lld %lld %lld\n", (int)CLUSTER, nsteps, ph[0], ph[1], ph[2], ph[3], ph[4]);
+#endif
 }
 
 }  // namespace
@@ -705,10 +825,14 @@ int gmres_fused_grid() {
     int dev = 0, sms = 0, occ = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaFuncSetAttribute(gm_chunk_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GF::SMEM);
-    cudaFuncSetAttribute(gm_chunk_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GF::SMEM);
+    cudaFuncSetAttribute(gm_chunk_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GM_SMEM);
+    cudaFuncSetAttribute(gm_chunk_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GM_SMEM);
     cudaFuncSetAttribute(gm_chunk_kernel<true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, gm_chunk_kernel<false>, GF_THREADS, GF::SMEM);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, gm_chunk_kernel<false>, GF_THREADS, GM_SMEM);
+    if (const char *dk = std::getenv("TT_GM_DIRECT_K")) {
+      const int v = std::atoi(dk);
+      cudaMemcpyToSymbol(c_gm_direct_kmax, &v, sizeof(int));
+    }
     const char *e = std::getenv("TT_GF_GRID");
     // two CTAs per SM when they fit (more bytes in flight for the CGS2 phases of
     // large local systems; measured +4% on C4)
@@ -831,7 +955,7 @@ tt_status launch_gmres_chunk(GmState *st, const GemmDesc *gapp, double *V, long 
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(G);
     cfg.blockDim = dim3(GF_THREADS);
-    cfg.dynamicSmemBytes = GF::SMEM;
+    cfg.dynamicSmemBytes = GM_SMEM;
     cfg.stream = s;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeClusterDimension;
@@ -842,7 +966,7 @@ tt_status launch_gmres_chunk(GmState *st, const GemmDesc *gapp, double *V, long 
     cfg.numAttrs = 1;
     e = cudaLaunchKernelEx(&cfg, gm_chunk_kernel<true>, a);
   } else {
-    e = cudaLaunchCooperativeKernel((const void *)gm_chunk_kernel<false>, dim3(G), dim3(GF_THREADS), args, GF::SMEM,
+    e = cudaLaunchCooperativeKernel((const void *)gm_chunk_kernel<false>, dim3(G), dim3(GF_THREADS), args, GM_SMEM,
                                     s);
   }
   if (e1) cudaEventRecord(e1, s);
