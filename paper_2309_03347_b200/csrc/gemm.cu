@@ -598,10 +598,65 @@ __global__ void __launch_bounds__(GF_THREADS) gemm_seq_kernel(const GemmDesc *__
   }
 }
 
+// out[i] = sum_c part[c * GF_LD + i] for i < n: all G x n partials are loaded
+// in one parallel round into shared memory, then summed in c order (the same
+// bits in every CTA).  sred >= GF_RED doubles; falls back to direct reads
+// when G * n exceeds it.
+constexpr int GF_RED = 2048;
+
+// out[i] = sum_{e in [lo, hi)} V_i[e] w[e] for i < n: each warp takes groups of
+// 8 vectors and keeps 8 accumulators per lane, so all loads of a group are in
+// flight before the (shuffle) reductions.
+__device__ __forceinline__ void slice_dots(const double *V, long long ldv, const double *w, int lo, int hi, int n,
+                                           double *out) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  constexpr int NWp = GF_THREADS / 32;
+  for (int i0 = warp * 8; i0 < n; i0 += NWp * 8) {
+    double acc[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) acc[q] = 0.0;
+    for (int e = lo + lane; e < hi; e += 32) {
+      const double we = w[e];
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        if (i0 + q < n) acc[q] = fma(V[(long long)(i0 + q) * ldv + e], we, acc[q]);
+    }
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const double s = warp_sum(acc[q]);
+      if (lane == 0 && i0 + q < n) out[i0 + q] = s;
+    }
+  }
+}
+__device__ __forceinline__ void cross_cta_sum(const double *part, int G, int n, double *out, double *sred) {
+  if (G * n <= GF_RED) {
+    for (int e = threadIdx.x; e < G * n; e += GF_THREADS) {
+      const int c = e / n, i = e - c * n;
+      sred[e] = part[(size_t)c * GF_LD + i];
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < n; i += GF_THREADS) {
+      double s = 0.0;
+      for (int c = 0; c < G; ++c) s += sred[c * n + i];
+      out[i] = s;
+    }
+  } else {   // large grids: one warp per entry, lanes over the CTAs (fixed order)
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int i = warp; i < n; i += GF_THREADS / 32) {
+      double s = 0.0;
+      for (int c = lane; c < G; c += 32) s += part[(size_t)c * GF_LD + i];
+      s = warp_sum(s);
+      if (lane == 0) out[i] = s;
+    }
+  }
+  __syncthreads();
+}
+
 template <bool CLUSTER>
 __global__ void __launch_bounds__(GF_THREADS) gm_chunk_kernel(GmChunkArgs a) {
   extern __shared__ __align__(16) double smem[];
   __shared__ double h1s[GF_LD], h2s[GF_LD], css[GF_LD], sns[GF_LD];
+  double *sred = smem;   // the GEMM tile buffers are idle during the vector phases
   __shared__ double red[GF_THREADS / 32 + 4];
   const int G = gridDim.x;
   GmState *st = a.st;
@@ -654,22 +709,10 @@ __global__ void __launch_bounds__(GF_THREADS) gm_chunk_kernel(GmChunkArgs a) {
     GM_PH(1);
     // ---- CGS2 pass 1: slice dots
     double *my1 = part1 + (size_t)blockIdx.x * GF_LD;
-    for (int i = warp; i <= j; i += NW) {
-      const double *vi = a.V + (long long)i * a.ldv;
-      double sacc = 0.0;
-      for (int e = lo + lane; e < hi; e += 32) sacc = fma(vi[e], w[e], sacc);
-      sacc = warp_sum(sacc);
-      if (lane == 0) my1[i] = sacc;
-    }
+    slice_dots(a.V, a.ldv, w, lo, hi, j + 1, my1);
     phase_sync<CLUSTER>(a.bar, G);
     GM_PH(2);
-    for (int i = warp; i <= j; i += NW) {      // cross-CTA sums: one warp per entry, fixed order
-      double sacc = 0.0;
-      for (int c = lane; c < G; c += 32) sacc += part1[(size_t)c * GF_LD + i];
-      sacc = warp_sum(sacc);
-      if (lane == 0) h1s[i] = sacc;
-    }
-    __syncthreads();
+    cross_cta_sum(part1, G, j + 1, h1s, sred);  // fixed order: identical in every CTA
     for (int e = lo + tid; e < hi; e += GF_THREADS) {
       double x = w[e];
       for (int i = 0; i <= j; ++i) x = fma(-h1s[i], a.V[(long long)i * a.ldv + e], x);
@@ -678,24 +721,12 @@ __global__ void __launch_bounds__(GF_THREADS) gm_chunk_kernel(GmChunkArgs a) {
     __syncthreads();
     // ---- pass 2 on the updated slice
     double *my2 = part2 + (size_t)blockIdx.x * GF_LD;
-    for (int i = warp; i <= j; i += NW) {
-      const double *vi = a.V + (long long)i * a.ldv;
-      double sacc = 0.0;
-      for (int e = lo + lane; e < hi; e += 32) sacc = fma(vi[e], w[e], sacc);
-      sacc = warp_sum(sacc);
-      if (lane == 0) my2[i] = sacc;
-    }
+    slice_dots(a.V, a.ldv, w, lo, hi, j + 1, my2);
     // rotations and g[j] of earlier steps, read before CTA 0 rewrites them in this step
     for (int i = tid; i < j; i += GF_THREADS) { css[i] = st->cs[i]; sns[i] = st->sn[i]; }
     const double gj = st->g[j];
     phase_sync<CLUSTER>(a.bar, G);
-    for (int i = warp; i <= j; i += NW) {
-      double sacc = 0.0;
-      for (int c = lane; c < G; c += 32) sacc += part2[(size_t)c * GF_LD + i];
-      sacc = warp_sum(sacc);
-      if (lane == 0) h2s[i] = sacc;
-    }
-    __syncthreads();
+    cross_cta_sum(part2, G, j + 1, h2s, sred);
     double nrm = 0.0;
     for (int e = lo + tid; e < hi; e += GF_THREADS) {
       double x = w[e];
@@ -714,13 +745,7 @@ __global__ void __launch_bounds__(GF_THREADS) gm_chunk_kernel(GmChunkArgs a) {
     phase_sync<CLUSTER>(a.bar, G);
     GM_PH(3);
     // ---- norm, Givens (identical in every CTA), normalisation
-    if (warp == 0) {
-      double hn2 = 0.0;
-      for (int c = lane; c < G; c += 32) hn2 += part3[(size_t)c * GF_LD];
-      hn2 = warp_sum(hn2);
-      if (lane == 0) red[2] = hn2;
-    }
-    __syncthreads();
+    cross_cta_sum(part3, G, 1, red + 2, sred);
     const double hn = sqrt(red[2]);
     // H column j: h1 + h2, then the earlier rotations
     if (tid == 0) {
