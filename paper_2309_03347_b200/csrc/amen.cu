@@ -169,7 +169,12 @@ __global__ void plan_svd(Dev D, int k, int dir) {
   q.rt = 1;   // Jacobi on R^T = V_R S U_R^T (fewer sweeps for decaying spectra): U, V swap
   SVDDesc &s = D.sd[0];
   s.m = p; s.p = p; s.W = D.qR; s.ldw = p; s.U = D.Vs; s.ldu = p; s.V = D.U; s.ldv = p;
-  s.sigma = D.S; s.work = D.J; s.sweeps_out = nullptr;
+  s.sigma = D.S; s.work = D.J;
+#ifdef TT_DEBUG_SVD
+  s.sweeps_out = D.iv + 15;
+#else
+  s.sweeps_out = nullptr;
+#endif
   D.iv[2] = wide; D.iv[3] = p; D.iv[4] = mm; D.iv[5] = nn;
 }
 
@@ -182,6 +187,9 @@ __global__ void trunc_kernel(Dev D, int k, int dir) {
   __shared__ int s_r;
   const int wide = D.iv[2], p = D.iv[3], mm = D.iv[4], nn = D.iv[5];
   const int d = D.x.d, tid = threadIdx.x;
+#ifdef TT_DEBUG_SVD
+  if (tid == 0) printf("SVDDBG %d %d %d %d\n", mm, nn, p, D.iv[15]);
+#endif
   if (tid == 0) {
     double tot = 0.0;
     for (int i = 0; i < p; ++i) tot += D.S[i] * D.S[i];
