@@ -18,7 +18,11 @@ if [ "${NCU:-1}" = "1" ]; then
       -o $O/ncu_gemm_c5_r128 python bench.py --workload c5 --rank 128 --no-graph --steps 1 --warmup 0 > $O/ncu_c5.log 2>&1
   ncu --set full --import-source on --clock-control none -k regex:matvec_batched -c 1 \
       -o $O/ncu_mv_b64 python tools/probe_mv.py 64 2 > $O/ncu_mv.log 2>&1
+  ncu --set full --import-source on --clock-control none -k regex:qr_kernel --launch-skip 200 -c 2 \
+      -o $O/ncu_qr_c1 python tools/profile_c1.py --iters 2 > $O/ncu_qr.log 2>&1
   ncu --metrics gpu__time_duration.sum --clock-control none --launch-skip 600 -c 6000 --csv \
       --log-file $O/launches_c1.csv python tools/profile_c1.py --iters 6 > $O/ncu_l1.log 2>&1
+  timeout 600 python tools/timeline.py c1 30 > $O/timeline_c1.txt 2>&1
+  timeout 900 python tools/timeline.py c3 10 > $O/timeline_c3.txt 2>&1
 fi
 echo done
