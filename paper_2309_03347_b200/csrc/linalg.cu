@@ -150,11 +150,10 @@ __global__ void __launch_bounds__(QR_THREADS) qr_kernel(const QRDesc *__restrict
   }
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   constexpr int NW = QR_THREADS / 32;
-  __shared__ double red[32];
   __shared__ double sT[NB][NB + 1];
   __shared__ double sG[NB][NB + 1];
   __shared__ double sV[NB][NB + 1], sX[NB][NB + 1], sW[NB][NB + 1];
-  __shared__ double s_tau, s_scal, s_beta;
+  __shared__ double s_tau;
   double *A = g.A;
   const long long lda = g.lda;
   // copy input into the working matrix
@@ -180,14 +179,16 @@ __global__ void __launch_bounds__(QR_THREADS) qr_kernel(const QRDesc *__restrict
     auto colp = [&](int j) -> double * {
       return in_smem ? sP + (long long)(j - j0) * pr - j0 : A + (long long)j * lda;
     };
-    // ---- panel factorisation (unblocked, Householder per column)
+    // ---- panel factorisation (unblocked, Householder per column): warp 0 forms
+    //      the reflector of column j alone (warp-synchronous), then all warps
+    //      update the remaining panel columns — two block barriers per column
     for (int jj = 0; jj < jb; ++jj) {
       const int j = j0 + jj;
       double *col = colp(j);
-      double part = 0.0;
-      for (int i = j + 1 + tid; i < m; i += QR_THREADS) part = fma(col[i], col[i], part);
-      const double sigma = block_sum(part, red);
-      if (tid == 0) {
+      if (warp == 0) {
+        double part = 0.0;
+        for (int i = j + 1 + lane; i < m; i += 32) part = fma(col[i], col[i], part);
+        const double sigma = warp_sum(part);
         const double alpha = col[j];
         double tau = 0.0, scal = 0.0, beta = alpha;
         if (sigma > 0.0) {
@@ -196,19 +197,17 @@ __global__ void __launch_bounds__(QR_THREADS) qr_kernel(const QRDesc *__restrict
           tau = (beta - alpha) / beta;
           scal = 1.0 / (alpha - beta);
         }
-        s_tau = tau;
-        s_scal = scal;
-        s_beta = beta;
-        g.tau[j] = tau;
+        if (tau != 0.0)
+          for (int i = j + 1 + lane; i < m; i += 32) col[i] *= scal;
+        __syncwarp();
+        if (lane == 0) {
+          col[j] = beta;
+          s_tau = tau;
+          g.tau[j] = tau;
+        }
       }
       __syncthreads();
       const double tau = s_tau;
-      if (tau != 0.0) {
-        const double scal = s_scal;
-        for (int i = j + 1 + tid; i < m; i += QR_THREADS) col[i] *= scal;
-      }
-      __syncthreads();
-      if (tid == 0) col[j] = s_beta;
       if (tau != 0.0) {
         for (int c = j + 1 + warp; c < j0 + jb; c += NW) {
           double *cc = colp(c);
