@@ -441,7 +441,7 @@ __global__ void __launch_bounds__(1024) jacobi_kernel(const SVDDesc *__restrict_
 // orthogonalises its 2 JB columns (plus the matching V columns) in shared
 // memory with one inner Jacobi pass; a software grid barrier separates rounds
 // (the grid is launched cooperatively, so all CTAs are co-resident).
-constexpr int JB = 8;
+constexpr int JB = 4;   // measured: 4 > 8 > 2 > 16 on C2 (instances/s 5.29, 5.16, 5.11, 4.20)
 constexpr int BJ_THREADS = 256;
 
 __device__ void grid_barrier(unsigned int *bar, unsigned int nblocks) {
