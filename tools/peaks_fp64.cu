@@ -38,6 +38,23 @@ __global__ void copy_kernel(const double2 *__restrict__ a, double2 *__restrict__
     b[i] = a[i];
 }
 
+// L2-resident read bandwidth: every CTA sweeps the whole (L2-sized) buffer
+__global__ void l2_read_kernel(const double2 *__restrict__ a, size_t n, int reps, double *out) {
+  double2 acc = make_double2(0.0, 0.0);
+  for (int r = 0; r < reps; ++r)
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+      const double2 v = __ldcg(a + i);
+      acc.x += v.x;
+      acc.y += v.y;
+    }
+  if (acc.x == 12345.0) out[0] = acc.y;
+}
+
+__global__ void fill_kernel(double2 *__restrict__ b, size_t n) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+    b[i] = make_double2(1.0, 2.0);
+}
+
 template <class F>
 float time_ms(F f, int reps) {
   cudaEvent_t e0, e1;
@@ -106,8 +123,16 @@ int main() {
   cudaMemset(a, 0, n * sizeof(double2));
   float cms = time_ms([&] { copy_kernel<<<sms * 8, 512>>>(a, b, n); }, 10);
   double gbs = 2.0 * n * sizeof(double2) / (cms * 1e-3) / 1e9;
+  float wms = time_ms([&] { fill_kernel<<<sms * 8, 512>>>(b, n); }, 10);
+  double wgbs = 1.0 * n * sizeof(double2) / (wms * 1e-3) / 1e9;
+  // L2: a 48 MB buffer read 20 times (well inside the 126 MB L2)
+  const size_t nl2 = (size_t)48 * 1024 * 1024 / sizeof(double2);
+  const int reps = 20;
+  float lms = time_ms([&] { l2_read_kernel<<<sms * 4, 512>>>(a, nl2, reps, out); }, 5);
+  double l2gbs = (double)reps * nl2 * sizeof(double2) / (lms * 1e-3) / 1e9;
   printf("{\"sms\": %d, \"l2_bytes\": %d, \"dmma_tflops_burst\": %.3f, \"dmma_tflops_sustained\": %.3f, "
-         "\"dmma_best_warps_per_block\": %d, \"dfma_tflops_burst\": %.3f, \"hbm_copy_gbs\": %.1f}\n",
-         sms, l2, best_dmma, sus, best_w, best_dfma, gbs);
+         "\"dmma_best_warps_per_block\": %d, \"dfma_tflops_burst\": %.3f, \"hbm_copy_gbs\": %.1f, "
+         "\"hbm_write_gbs\": %.1f, \"l2_read_gbs\": %.1f}\n",
+         sms, l2, best_dmma, sus, best_w, best_dfma, gbs, wgbs, l2gbs);
   return 0;
 }
