@@ -312,6 +312,7 @@ __device__ void jacobi_core(int m, int p, double *W, long long ldw, double *V, l
   const int NW = blockDim.x >> 5;
   const int P2 = p + (p & 1);  // even number of players (a phantom player is skipped)
   const double tol = 4.0 * DBL_EPSILON;
+  unsigned long long fl = 0;   // flop count, one atomic per warp at the end (not per rotation)
   int sweep = 0;
   for (; sweep < 60; ++sweep) {
     if (tid == 0) *flag = 0;
@@ -340,9 +341,9 @@ __device__ void jacobi_core(int m, int p, double *W, long long ldw, double *V, l
         be = warp_sum(be);
         ga = warp_sum(ga);
         if (ga == 0.0 || al == 0.0 || be == 0.0) continue;
-        if (lane == 0) atomicAdd(&g_linalg_flops[1], 6ull * m);
+        fl += 6ull * m;
         if (fabs(ga) <= tol * sqrt(al) * sqrt(be)) continue;
-        if (lane == 0) atomicAdd(&g_linalg_flops[1], 6ull * (m + p));
+        fl += 6ull * (m + p);
         const double zeta = (be - al) / (2.0 * ga);
         const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(fma(zeta, zeta, 1.0)));
         const double c = 1.0 / sqrt(fma(t, t, 1.0)), s = c * t;
@@ -365,6 +366,7 @@ __device__ void jacobi_core(int m, int p, double *W, long long ldw, double *V, l
     __syncthreads();
   }
   if (tid == 0 && sweeps_out) *sweeps_out = sweep + 1;
+  if (lane == 0 && fl) atomicAdd(&g_linalg_flops[1], fl);
   // singular values = column norms
   for (int c = warp; c < p; c += NW) {
     const double *w = W + (long long)c * ldw;
@@ -480,6 +482,7 @@ __global__ void __launch_bounds__(BJ_THREADS) jacobi_block_kernel(const SVDDesc 
   // revisited nb-1 times per sweep, so a tighter threshold only adds rotations
   // of noise-level pairs (and their roundoff).
   const double tol = fmax(4.0, sqrt((double)m)) * DBL_EPSILON;
+  unsigned long long fl = 0;   // flop count, one atomic per warp at the end
   // init (grid-strided)
   for (long long e = blockIdx.x * (long long)BJ_THREADS + tid; e < (long long)m * p; e += (long long)G * BJ_THREADS) {
     const int r = (int)(e % m), c = (int)(e / m);
@@ -529,7 +532,7 @@ __global__ void __launch_bounds__(BJ_THREADS) jacobi_block_kernel(const SVDDesc 
               al = fma(x, x, al); be = fma(y, y, be); ga = fma(x, y, ga);
             }
             al = warp_sum(al); be = warp_sum(be); ga = warp_sum(ga);
-            if (lane == 0) atomicAdd(&g_linalg_flops[1], 6ull * m);
+            fl += 6ull * m;
             if (ga == 0.0 || al == 0.0 || be == 0.0) continue;
             if (fabs(ga) <= tol * sqrt(al) * sqrt(be)) continue;
             const double zeta = (be - al) / (2.0 * ga);
@@ -545,7 +548,7 @@ __global__ void __launch_bounds__(BJ_THREADS) jacobi_block_kernel(const SVDDesc 
               va[r] = c * x - s * y; vb[r] = s * x + c * y;
             }
             rotated = 1;
-            if (lane == 0) atomicAdd(&g_linalg_flops[1], 6ull * (m + p));
+            fl += 6ull * (m + p);
           }
           __syncthreads();
         }
@@ -568,6 +571,7 @@ __global__ void __launch_bounds__(BJ_THREADS) jacobi_block_kernel(const SVDDesc 
     if (blockIdx.x == 0 && tid == 0) *flag = 0;
     grid_barrier(bar, G);
   }
+  if (lane == 0 && fl) atomicAdd(&g_linalg_flops[1], fl);
   if (blockIdx.x != 0) return;
   if (tid == 0 && g.sweeps_out) *g.sweeps_out = sweep + 1;
   // sigma, sort, outputs (CTA 0)

@@ -22,6 +22,8 @@ std::mutex g_mu;
 struct Span { unsigned long long s, e; };
 std::vector<Span> g_spans;
 std::map<std::string, std::pair<unsigned long long, unsigned long long>> g_by_name;  // count, ns
+std::string g_watch;                                    // substring of kernel names whose instances are kept
+std::vector<std::pair<unsigned long long, unsigned long long>> g_inst;  // (start, duration) of watched kernels
 constexpr size_t BUF = 16 << 20;
 
 void CUPTIAPI buffer_requested(uint8_t **buffer, size_t *size, size_t *max_records) {
@@ -39,6 +41,8 @@ void CUPTIAPI buffer_completed(CUcontext, uint32_t, uint8_t *buffer, size_t, siz
       g_all++;
       if (k->name && (std::strncmp(k->name, "_ZN2tt", 6) == 0 || std::strstr(k->name, "tt::"))) g_ours++;
       g_spans.push_back({k->start, k->end});
+      if (!g_watch.empty() && k->name && std::strstr(k->name, g_watch.c_str()))
+        g_inst.push_back({k->start, k->end - k->start});
       auto &v = g_by_name[k->name ? std::string(k->name).substr(0, 80) : std::string("?")];
       v.first += 1;
       v.second += k->end - k->start;
@@ -55,6 +59,9 @@ extern "C" int lc_start() {
     std::lock_guard<std::mutex> lk(g_mu);
     g_spans.clear();
     g_by_name.clear();
+    g_inst.clear();
+    const char *w = std::getenv("LC_WATCH");
+    g_watch = w ? w : "";
   }
   if (cuptiActivityRegisterCallbacks(buffer_requested, buffer_completed) != CUPTI_SUCCESS) return -1;
   if (cuptiActivityEnable(CUPTI_ACTIVITY_KIND_CONCURRENT_KERNEL) != CUPTI_SUCCESS) return -2;
@@ -89,5 +96,13 @@ extern "C" int lc_dump(const char *path) {
   std::fprintf(f, "%llu %llu\n", span, busy);
   for (const auto &kv : g_by_name) std::fprintf(f, "%llu %llu %s\n", kv.second.first, kv.second.second, kv.first.c_str());
   std::fclose(f);
+  if (!g_inst.empty()) {
+    std::string p2 = std::string(path) + ".inst";
+    FILE *g = std::fopen(p2.c_str(), "w");
+    if (g) {
+      for (const auto &v : g_inst) std::fprintf(g, "%llu %llu\n", v.first, v.second);
+      std::fclose(g);
+    }
+  }
   return 0;
 }
