@@ -304,6 +304,13 @@ __global__ void __launch_bounds__(QR_THREADS) qr_kernel(const QRDesc *__restrict
 }
 
 // ------------------------------------------------------------ Jacobi SVD ---
+// |ga| <= tol sqrt(al be) with one square root (two when al be over/underflows);
+// the FP64 sqrt/div sequences are the cost of a latency-bound Jacobi round
+__device__ __forceinline__ bool jacobi_orthogonal(double al, double be, double ga, double tol) {
+  const double pr = al * be;
+  if (pr > 0.0 && pr < 1e300) return fabs(ga) <= tol * sqrt(pr);
+  return fabs(ga) <= tol * sqrt(al) * sqrt(be);
+}
 constexpr int SVD_THREADS = 256;
 
 __device__ void jacobi_core(int m, int p, double *W, long long ldw, double *V, long long ldv, double *s_sig,
@@ -342,11 +349,11 @@ __device__ void jacobi_core(int m, int p, double *W, long long ldw, double *V, l
         ga = warp_sum(ga);
         if (ga == 0.0 || al == 0.0 || be == 0.0) continue;
         fl += 6ull * m;
-        if (fabs(ga) <= tol * sqrt(al) * sqrt(be)) continue;
+        if (jacobi_orthogonal(al, be, ga, tol)) continue;
         fl += 6ull * (m + p);
         const double zeta = (be - al) / (2.0 * ga);
         const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(fma(zeta, zeta, 1.0)));
-        const double c = 1.0 / sqrt(fma(t, t, 1.0)), s = c * t;
+        const double c = rsqrt(fma(t, t, 1.0)), s = c * t;
         for (int r = lane; r < m; r += 32) {
           const double x = wa[r], y = wb[r];
           wa[r] = c * x - s * y;
@@ -534,10 +541,10 @@ __global__ void __launch_bounds__(BJ_THREADS) jacobi_block_kernel(const SVDDesc 
             al = warp_sum(al); be = warp_sum(be); ga = warp_sum(ga);
             fl += 6ull * m;
             if (ga == 0.0 || al == 0.0 || be == 0.0) continue;
-            if (fabs(ga) <= tol * sqrt(al) * sqrt(be)) continue;
+            if (jacobi_orthogonal(al, be, ga, tol)) continue;
             const double zeta = (be - al) / (2.0 * ga);
             const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(fma(zeta, zeta, 1.0)));
-            const double c = 1.0 / sqrt(fma(t, t, 1.0)), s = c * t;
+            const double c = rsqrt(fma(t, t, 1.0)), s = c * t;
             for (int r = lane; r < m; r += 32) {
               const double x = wa[r], y = wb[r];
               wa[r] = c * x - s * y; wb[r] = s * x + c * y;
