@@ -274,7 +274,11 @@ __device__ __forceinline__ void gemm_tile(const GemmDesc &g0, int m0, int n0, in
 // one to arrive sums the slices in slice order (deterministic) and applies the
 // epilogue, then re-arms the counter (no separate reduction launch).
 template <int BM, int BN, int BK, int WM_, int WN_, int STAGES>
-__global__ void __launch_bounds__(32 * WM_ * WN_) gemm_dmma_kernel(const GemmDesc *__restrict__ descs, int splits,
+#ifndef GEMM_MINB
+#define GEMM_MINB 4   // 64x64 tiles: 128 registers, 4 CTAs per SM (C5 r=256 17.3 -> 18.2 TF/s in the same run; 5 measured slower)
+#endif
+__global__ void __launch_bounds__(32 * WM_ * WN_, (BM == 64 && BN == 64) ? GEMM_MINB : 1)
+    gemm_dmma_kernel(const GemmDesc *__restrict__ descs, int splits,
                                                                    double *__restrict__ partial, long long pld,
                                                                    long long pstride, unsigned int *tile_cnt) {
   extern __shared__ __align__(16) double smem[];
