@@ -369,6 +369,8 @@ using V64K = Variant<64, 64, 32, 2, 2, 3>;    // deeper K, 3 stages
 using V128 = Variant<128, 64, 16, 4, 2, 3>;   // 8 warps
 using V128S = Variant<128, 128, 16, 4, 2, 2>; // 8 warps, 32x64 warp tiles
 using V32 = Variant<32, 32, 16, 2, 2, 2>;     // small tiles for GEMMs that fill less than a wave
+using V64S3 = Variant<64, 64, 16, 2, 2, 3>;   // 3-stage pipeline
+using V64S4 = Variant<64, 64, 16, 2, 2, 4>;   // 4-stage pipeline
 
 int variant_id() {
   static int v = -1;
@@ -830,6 +832,8 @@ tt_status launch_gemm_k(const GemmDesc *descs_dev, int count, int Mcap, int Ncap
     case 0: return launch_variant<V64>(descs_dev, count, Mcap, Ncap, Kcap, s);
     case 2: return launch_variant<V128>(descs_dev, count, Mcap, Ncap, Kcap, s);
     case 3: return launch_variant<V128S>(descs_dev, count, Mcap, Ncap, Kcap, s);
+    case 4: return launch_variant<V64S3>(descs_dev, count, Mcap, Ncap, Kcap, s);
+    case 5: return launch_variant<V64S4>(descs_dev, count, Mcap, Ncap, Kcap, s);
     default: return launch_variant<V64K>(descs_dev, count, Mcap, Ncap, Kcap, s);
   }
 }
