@@ -471,7 +471,7 @@ using GF = Cfg<64, 64, GF_BK, 2, 2, 2>;   // persistent-kernel tiles
 constexpr int GF_LD = GM_MAX_M + 2;
 // dynamic shared memory of the fused kernel: GEMM tile buffers + the apply
 // descriptors of up to GM_MAX_M steps
-constexpr size_t GM_SMEM = GF::SMEM + (size_t)3 * GM_MAX_M * sizeof(GemmDesc);
+constexpr size_t GM_SMEM = GF::SMEM + (size_t)3 * (GM_MAX_M + 1) * sizeof(GemmDesc);
 
 __device__ __forceinline__ void gbar(unsigned int *bar, unsigned int nblocks) {
   __syncthreads();
@@ -513,6 +513,10 @@ struct GmChunkArgs {
   int j0, j1;
   int mode;              // 0 grid only, 1 cluster only, 2 device decides (both variants launched)
   int cs;                // cluster size (for the device-side choice)
+  int full;              // 1: the whole restarted solve (start, cycles, updates) in this launch
+  int max_restarts;
+  const double *b;       // full: right-hand side
+  double *x;             // full: initial guess in, solution out
 };
 
 // Phase barrier: whole cooperative grid (atomics in global memory) or one
@@ -678,7 +682,8 @@ __global__ void __launch_bounds__(GF_THREADS) gm_chunk_kernel(GmChunkArgs a) {
     const bool small = tiles <= 2 * a.cs && N <= 16384;
     if (small != CLUSTER) return;
   }
-  const double tol = st->tol, bnorm = st->bnorm;
+  const double tol = st->tol;
+  double bnorm = st->bnorm;
   const int per = (N + G - 1) / G;
   const int lo = min(N, (int)blockIdx.x * per), hi = min(N, lo + per);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -694,24 +699,75 @@ __global__ void __launch_bounds__(GF_THREADS) gm_chunk_kernel(GmChunkArgs a) {
 #endif
   // the apply descriptors of every step of this launch, staged once in shared
   // memory (one parallel load instead of a dependent L2 read per GEMM stage)
-  const int jend = min(a.j1, m);
+  // full: descriptors of x (index -1) and of every basis vector; else steps j0..j1-1
+  const int jend = a.full ? m : min(a.j1, m);
+  const int jbase = a.full ? 0 : a.j0 + 1;   // staged descriptor 3 (j + 1 - jbase) + s
   GemmDesc *sdesc = reinterpret_cast<GemmDesc *>(smem + GF::SMEM / sizeof(double));
   {
-    const int nd = 3 * max(jend - a.j0, 0);
+    const int nd = 3 * max(jend + 1 - jbase, 0);
     const long long nw = (long long)nd * sizeof(GemmDesc) / sizeof(long long);
-    const long long *src = reinterpret_cast<const long long *>(a.gapp + 3 * (a.j0 + 1));
+    const long long *src = reinterpret_cast<const long long *>(a.gapp + 3 * jbase);
     long long *dst = reinterpret_cast<long long *>(sdesc);
     for (long long e = threadIdx.x; e < nw; e += GF_THREADS) dst[e] = src[e];
     __syncthreads();
   }
+  __shared__ double ys[GF_LD];
   int nsteps = 0;
-  for (int j = a.j0; j < jend; ++j) {
-    if (j > a.j0) phase_sync<CLUSTER>(a.bar, G);            // V[:, j] of the previous step complete
+  const int ncycles = a.full ? a.max_restarts : 1;
+  for (int cyc = 0; cyc < ncycles; ++cyc) {
+  int jfirst = a.j0;
+  if (a.full) {
+    // ---- cycle start: r = b - A x, beta = ||r||, V_0 = r / beta (gm_start_kernel's work)
+    for (int sidx = 0; sidx < 3; ++sidx)
+      gemm_stage<CLUSTER>(sdesc[sidx], a.split, a.split_elems, a.bar, G, smem, true, false);
+    double pb = 0.0, pr = 0.0;
+    for (int e = lo + tid; e < hi; e += GF_THREADS) {
+      const double r = a.b[e] - w[e];
+      a.V[e] = r;
+      pb = fma(a.b[e], a.b[e], pb);
+      pr = fma(r, r, pr);
+    }
+    pb = warp_sum(pb);
+    pr = warp_sum(pr);
+    if (lane == 0) { red[warp] = pb; h1s[warp] = pr; }
+    __syncthreads();
+    if (tid == 0) {
+      double tb = 0.0, tr = 0.0;
+      for (int q = 0; q < NW; ++q) { tb += red[q]; tr += h1s[q]; }
+      part1[(size_t)blockIdx.x * GF_LD] = tb;
+      part1[(size_t)blockIdx.x * GF_LD + 1] = tr;
+    }
+    phase_sync<CLUSTER>(a.bar, G);
+    cross_cta_sum(part1, G, 2, h2s, sred);
+    const double bn = sqrt(h2s[0]), beta = sqrt(h2s[1]);
+    if (cyc == 0) bnorm = bn;
+    const double rel = bn > 0.0 ? beta / bn : 0.0;
+    const bool done = (rel <= tol) || (beta == 0.0);
+    if (blockIdx.x == 0 && tid == 0) {
+      if (cyc == 0) { st->bnorm = bn; st->res0 = rel; }
+      st->beta = beta;
+      st->j = 0;
+      st->jdone = 0;
+      st->g[0] = beta;
+      st->res = rel;
+      if (done) { st->converged = 1; st->stop = 1; }
+    }
+    if (done) break;
+    const double inv = 1.0 / beta;
+    for (int e = lo + tid; e < hi; e += GF_THREADS) a.V[e] *= inv;
+    phase_sync<CLUSTER>(a.bar, G);   // V_0 and g[0] complete
+    jfirst = 0;
+  }
+  bool nan_stop = false;
+  int jlast = jfirst - 1;
+  for (int j = jfirst; j < jend; ++j) {
+    if (j > jfirst) phase_sync<CLUSTER>(a.bar, G);            // V[:, j] of the previous step complete
     GM_PH(0);
     ++nsteps;
+    jlast = j;
     // ---- w = A V[:, j] (three chained GEMM stages; the kernel itself stops on the stop word)
     for (int sidx = 0; sidx < 3; ++sidx)
-      gemm_stage<CLUSTER>(sdesc[3 * (j - a.j0) + sidx], a.split, a.split_elems, a.bar, G, smem, true, false);
+      gemm_stage<CLUSTER>(sdesc[3 * (j + 1 - jbase) + sidx], a.split, a.split_elems, a.bar, G, smem, true, false);
     GM_PH(1);
     // ---- CGS2 pass 1: slice dots
     double *my1 = part1 + (size_t)blockIdx.x * GF_LD;
@@ -788,6 +844,7 @@ __global__ void __launch_bounds__(GF_THREADS) gm_chunk_kernel(GmChunkArgs a) {
       }
       red[0] = stop ? 1.0 : 0.0;
       red[1] = hn;
+      red[3] = (stop == 2) ? 1.0 : 0.0;
     }
     __syncthreads();
     const bool stop = red[0] != 0.0;
@@ -801,8 +858,36 @@ __global__ void __launch_bounds__(GF_THREADS) gm_chunk_kernel(GmChunkArgs a) {
       for (int e = lo + tid; e < hi; e += GF_THREADS) vn[e] = w[e] * inv;
     }
     GM_PH(4);
+    if (red[3] != 0.0) nan_stop = true;
     if (stop) break;
   }
+  if (!a.full) break;
+  // ---- cycle end: x += V y with H y = g (gm_update_kernel's work), restart test
+  phase_sync<CLUSTER>(a.bar, G);   // H, g, res written by CTA 0 are visible
+  const int jd = jlast + 1;
+  if (tid == 0) {
+    const double *H = st->H;
+    for (int i = jd - 1; i >= 0; --i) {
+      double sacc = st->g[i];
+      for (int k = i + 1; k < jd; ++k) sacc -= H[i + (m + 1) * k] * ys[k];
+      ys[i] = sacc / H[i + (m + 1) * i];
+    }
+  }
+  __syncthreads();
+  for (int e = lo + tid; e < hi; e += GF_THREADS) {
+    double sacc = a.x[e];
+    for (int i = 0; i < jd; ++i) sacc = fma(ys[i], a.V[(long long)i * a.ldv + e], sacc);
+    a.x[e] = sacc;
+  }
+  const bool conv = st->res <= tol;   // written by CTA 0 before the barrier above
+  if (blockIdx.x == 0 && tid == 0) {
+    st->cycle += 1;
+    st->converged = conv ? 1 : 0;
+    st->stop = (conv || nan_stop || cyc + 1 >= ncycles) ? 1 : 0;
+  }
+  if (conv || nan_stop) break;
+  phase_sync<CLUSTER>(a.bar, G);   // x complete before the next cycle's A x
+  }   // cycles
 #ifdef GM_PHASE_TIMING
   if (blockIdx.x == 0 && threadIdx.x == 0 && nsteps > 0)
     printf("GMPH %d %d %lld %lld %lld %lld %lld\n", (int)CLUSTER, nsteps, ph[0], ph[1], ph[2], ph[3], ph[4]);
@@ -962,12 +1047,17 @@ int gmres_cluster_size() {
 
 tt_status launch_gmres_chunk(GmState *st, const GemmDesc *gapp, double *V, long long ldv, double *w, double *part,
                              double *split, long long split_elems, unsigned int *bar, int j0, int j1,
-                             cudaStream_t s, int cluster, int decide) {
+                             cudaStream_t s, int cluster, int decide, int full, int max_restarts, const double *b,
+                             double *x) {
   const int G = cluster ? gmres_cluster_size() : gmres_fused_grid();
   if (G <= 0) return fail(TT_ERR_CUDA, "gmres: fused step kernel cannot be co-resident");
   GmChunkArgs a;
   a.mode = decide ? 2 : cluster;
   a.cs = gmres_cluster_size();
+  a.full = full;
+  a.max_restarts = max_restarts;
+  a.b = b;
+  a.x = x;
   a.st = st; a.gapp = gapp; a.V = V; a.ldv = ldv; a.w = w; a.part = part; a.split = split;
   a.split_elems = split_elems; a.bar = bar; a.j0 = j0; a.j1 = j1;
   void *args[] = {(void *)&a};

@@ -213,6 +213,18 @@ tt_status gmres_solve(const GmresCtx &c, cudaStream_t s) {
   }
   const bool fused = c.gapp && c.part && c.bar && gmres_fused_grid() > 0;
   if (fused) cudaMemsetAsync(c.bar, 0, 2 * sizeof(unsigned int), s);
+  static int whole = -1;   // the whole restarted solve in one persistent launch (no host polling)
+  if (whole < 0) whole = std::getenv("TT_GMRES_PERCYCLE") ? 0 : 1;
+  if (fused && whole) {
+    const int decide = c.cluster == 2;
+    if (c.cluster != 0)
+      TT_TRY(launch_gmres_chunk(c.st, c.gapp, c.V, c.ldv, c.w, c.part, c.split, c.split_elems, c.bar, 0, c.m, s, 1,
+                                decide, 1, c.max_restarts, c.b, c.x));
+    if (c.cluster != 1)
+      TT_TRY(launch_gmres_chunk(c.st, c.gapp, c.V, c.ldv, c.w, c.part, c.split, c.split_elems, c.bar, 0, c.m, s, 0,
+                                decide, 1, c.max_restarts, c.b, c.x));
+    return check_launch("gmres (persistent)");
+  }
   for (int cyc = 0; cyc < c.max_restarts; ++cyc) {
     TT_TRY(c.apply(c.x, c.w, -1));
     gm_start_kernel<<<1, RT, 0, s>>>(c.st, c.b, c.w, c.V);

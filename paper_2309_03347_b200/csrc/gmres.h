@@ -50,7 +50,8 @@ size_t gmres_fused_part_doubles(int G);
 int gmres_fused_grid();
 tt_status launch_gmres_chunk(GmState *st, const GemmDesc *gapp, double *V, long long ldv, double *w, double *part,
                              double *split, long long split_elems, unsigned int *bar, int j0, int j1, cudaStream_t s,
-                             int cluster, int decide);
+                             int cluster, int decide, int full = 0, int max_restarts = 1, const double *b = nullptr,
+                             double *x = nullptr);
 int gmres_cluster_size();
 
 }  // namespace tt
