@@ -77,6 +77,15 @@ __global__ void init_ifaces_kernel(Dev D) {
 
 __global__ void set_dv_kernel(double *dv, int i, double v) { dv[i] = v; }
 
+// per-bond truncation limits min(rmax, xcap - zcap) >= 1 (room for the enrichment)
+__global__ void set_limits_kernel(const VecMeta x, const VecMeta z, int rmax, int *limit) {
+  for (int k = threadIdx.x; k <= x.d; k += blockDim.x) {
+    int l = x.rcap[k] - z.rcap[k];
+    l = l > rmax ? rmax : l;
+    limit[k] = l < 1 ? 1 : l;
+  }
+}
+
 // interfaces: right ones at bond k from bond k+1 and core k; left ones at bond k+1 from bond k and core k
 __global__ void plan_iface(Dev D, int k, int dir) {
   const int n = D.x.n[k];
@@ -468,17 +477,7 @@ tt_status amen_solve_meta(const MatMeta &A, const VecMeta &b, const VecMeta &x, 
   const int d = P.d, m = P.m;
   const int pc = P.pc, zcm = P.zcm, nmax = P.nmax;
   // per-bond truncation limits: min(rmax, xcap - zcap) (room for the enrichment)
-  {
-    static thread_local std::vector<int> lim;
-    lim.assign(TT_MAX_D + 1, 1);
-    for (int k = 0; k <= d; ++k) {
-      int l = x.rcap[k] - z.rcap[k];
-      if (l > o.rmax) l = o.rmax;
-      lim[k] = l < 1 ? 1 : l;
-    }
-    cudaMemcpyAsync(D.limit, lim.data(), sizeof(int) * (d + 1), cudaMemcpyHostToDevice, s);
-    cudaStreamSynchronize(s);
-  }
+  set_limits_kernel<<<1, 64, 0, s>>>(x, z, o.rmax, D.limit);   // no host round trip
   set_gm_H<<<1, 1, 0, s>>>(P.gst, P.H);
   set_dv_kernel<<<1, 1, 0, s>>>(D.dv, 1, o.eps);
   set_gemm_scratch(P.split, GEMM_SPLIT_SCRATCH);
@@ -827,17 +826,7 @@ tt_status amen_mv_meta(const MatMeta &A, const VecMeta &b, const VecMeta &y, con
   if (!(eps > 0.0) || max_sweeps < 1 || rmax < 1) return fail(TT_ERR_ARG, "amen_mv: eps > 0, max_sweeps, rmax >= 1");
   Dev &D = P.D;
   const int d = A.d;
-  {
-    static thread_local std::vector<int> lim;
-    lim.assign(TT_MAX_D + 1, 1);
-    for (int k = 0; k <= d; ++k) {
-      int l = y.rcap[k] - z.rcap[k];
-      if (l > rmax) l = rmax;
-      lim[k] = l < 1 ? 1 : l;
-    }
-    cudaMemcpyAsync(D.limit, lim.data(), sizeof(int) * (d + 1), cudaMemcpyHostToDevice, s);
-    cudaStreamSynchronize(s);
-  }
+  set_limits_kernel<<<1, 64, 0, s>>>(y, z, rmax, D.limit);
   set_dv_kernel<<<1, 1, 0, s>>>(D.dv, 1, eps);
   set_gemm_scratch(P.split, GEMM_SPLIT_SCRATCH);
   set_jacobi_sync(P.bar);
