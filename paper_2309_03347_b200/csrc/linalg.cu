@@ -144,8 +144,17 @@ __device__ void apply_block_reflector(int m, int j0, int jb, const double *A, lo
   }
 }
 
+#ifdef QR_PHASE_TIMING
+#define QR_PH(i) do { if (threadIdx.x == 0) { const long long t_ = clock64(); qph[i] += t_ - qtc; qtc = t_; } } while (0)
+#else
+#define QR_PH(i) do { } while (0)
+#endif
 __global__ void __launch_bounds__(QR_THREADS) qr_kernel(const QRDesc *__restrict__ descs) {
   const QRDesc g = descs[blockIdx.x];
+#ifdef QR_PHASE_TIMING
+  long long qph[6] = {0, 0, 0, 0, 0, 0};
+  long long qtc = clock64();
+#endif
   const int m = g.m, n = g.n, kmin = min(m, n);
   if (threadIdx.x == 0) {
     // geqrf: 2 m n k - (m + n) k^2 + 2/3 k^3 ; orgqr (explicit Q, m x k): 4 m k^2 - 4/3 k^3 (LAPACK counts)
@@ -170,6 +179,7 @@ __global__ void __launch_bounds__(QR_THREADS) qr_kernel(const QRDesc *__restrict
   __syncthreads();
 
   extern __shared__ double sP[];   // panel copy (rows j0..m-1) when it fits
+  QR_PH(0);
   for (int j0 = 0; j0 < kmin; j0 += NB) {
     const int jb = min(NB, kmin - j0);
     const int pr = m - j0;                           // panel rows
@@ -225,6 +235,7 @@ __global__ void __launch_bounds__(QR_THREADS) qr_kernel(const QRDesc *__restrict
       }
       __syncthreads();
     }
+    QR_PH(1);
     // ---- T factor (larft, forward, columnwise): T upper triangular jb x jb
     //      G[l][i] = v_l^T v_i for l < i
     for (int pidx = warp; pidx < jb * jb; pidx += NW) {
@@ -267,12 +278,14 @@ __global__ void __launch_bounds__(QR_THREADS) qr_kernel(const QRDesc *__restrict
     double *Tg = g.T + (long long)(j0 / NB) * NB * NB;
     for (int e = tid; e < NB * NB; e += QR_THREADS) Tg[e] = sT[e % NB][e / NB];
     __syncthreads();
+    QR_PH(2);
     // ---- trailing update: A[:, j0+jb:n] <- (I - V T V^T)^T A = A - V T^T (V^T A)
     if (j0 + jb < n)
       apply_block_reflector(m, j0, jb, A, lda, sT, 1, A, 1, lda, j0 + jb, n, sV, sX, sW, in_smem ? sP : nullptr,
                             pr);
     __syncthreads();
   }
+  QR_PH(3);
   // ---- R
   if (g.R) {
     for (long long e = tid; e < (long long)kmin * n; e += QR_THREADS) {
@@ -307,6 +320,10 @@ __global__ void __launch_bounds__(QR_THREADS) qr_kernel(const QRDesc *__restrict
       __syncthreads();
     }
   }
+#ifdef QR_PHASE_TIMING
+  QR_PH(4);
+  if (threadIdx.x == 0) printf("QRPH %d %d %d %lld %lld %lld %lld %lld\n", m, n, g.Q ? 1 : 0, qph[0], qph[1], qph[2], qph[3], qph[4]);
+#endif
 }
 
 // ------------------------------------------------------------ Jacobi SVD ---
