@@ -57,11 +57,6 @@ __device__ GemmDesc gdd(int M, int N, int K, const double *A, long long lda, int
   gd_plain(g, C, ldc);
   return g;
 }
-__device__ GemmDesc gd_none() {
-  GemmDesc g = gd_make(0, 0, 0, nullptr, 1, 0, nullptr, 1, 0);
-  gd_plain(g, nullptr, 1);
-  return g;
-}
 __device__ CopyDesc cpy(int rows, int cols, const double *src, long long ssr, long long ssc, double *dst,
                         long long dsr, long long dsc) {
   CopyDesc c;
@@ -461,10 +456,6 @@ size_t amen_ws_bytes(const MatMeta &A, const VecMeta &b, const VecMeta &x, const
   return ar.used;
 }
 
-static tt_status gemms(const GemmDesc *g, int count, int Mc, int Nc, cudaStream_t s) {
-  for (int i = 0; i < count; ++i) TT_TRY(launch_gemm(g + i, 1, Mc, Nc, s));
-  return TT_OK;
-}
 
 tt_status amen_solve_meta(const MatMeta &A, const VecMeta &b, const VecMeta &x, const VecMeta &z, const AmenOpts &o,
                           int *sweeps_dev, double *res_dev, int *status_dev, Arena &ar, cudaStream_t s) {

@@ -173,9 +173,6 @@ __global__ void gm_init_kernel(GmState *st, const int *Nptr, int m, double tol) 
   st->jdone = 0;
 }
 
-__global__ void gm_clear_stop_kernel(GmState *st) {
-  st->stop = 0;
-}
 
 }  // namespace
 

@@ -33,16 +33,6 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
-__device__ double block_sum(double v, double *red) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  v = warp_sum(v);
-  __syncthreads();
-  if (lane == 0) red[warp] = v;
-  __syncthreads();
-  double t = 0.0;
-  for (int i = 0; i < nw; ++i) t += red[i];
-  return t;
-}
 
 // Block reflector application on a target matrix X (rows r0.., element (r,c)
 // at X[r*rs + c*cs]):  X[r0:m, cols] -= V * (op(T) * (V^T X[r0:m, cols]))
@@ -334,7 +324,6 @@ __device__ __forceinline__ bool jacobi_orthogonal(double al, double be, double g
   if (pr > 0.0 && pr < 1e300) return fabs(ga) <= tol * sqrt(pr);
   return fabs(ga) <= tol * sqrt(al) * sqrt(be);
 }
-constexpr int SVD_THREADS = 256;
 
 __device__ void jacobi_core(int m, int p, double *W, long long ldw, double *V, long long ldv, double *s_sig,
                             int *s_pos, int *flag, int *sweeps_out) {

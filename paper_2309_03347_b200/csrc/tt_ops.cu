@@ -171,7 +171,6 @@ struct MvPair {
 // A[:, :, :, a'] (R0 m n) and X[:, :, b'] (r0 n) are staged in shared memory and
 // the contiguous column Y[:, :, rho'] (P m entries) is streamed out with
 // coalesced stores — one small division per entry, no per-entry index algebra.
-constexpr int MV_SMEM = 6144;  // doubles of staging (48 KB)
 
 template <int MC, int NC>   // MC = NC = 2: QTT 2x2 cores (compile-time modes); 0: runtime modes
 __device__ __forceinline__ void matvec_cols_t(const double *__restrict__ A, const double *__restrict__ X,
