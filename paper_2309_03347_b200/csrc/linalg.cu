@@ -73,9 +73,15 @@ __device__ void apply_block_reflector(int m, int j0, int jb, const double *A, lo
       for (int q = 0; q < QR_NQ; ++q) {
         const int e = tid + q * QR_THREADS;  // 1024 entries (l, c)
         const int l = e % NB, c = e / NB;
-        double s = acc[q];
-        for (int rr = 0; rr < NB; ++rr) s = fma(sV[rr][l], sX[rr][c], s);
-        acc[q] = s;
+        double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+#pragma unroll
+        for (int rr = 0; rr < NB; rr += 4) {
+          s0 = fma(sV[rr][l], sX[rr][c], s0);
+          s1 = fma(sV[rr + 1][l], sX[rr + 1][c], s1);
+          s2 = fma(sV[rr + 2][l], sX[rr + 2][c], s2);
+          s3 = fma(sV[rr + 3][l], sX[rr + 3][c], s3);
+        }
+        acc[q] += (s0 + s1) + (s2 + s3);
       }
       __syncthreads();
     }
@@ -124,12 +130,104 @@ __device__ void apply_block_reflector(int m, int j0, int jb, const double *A, lo
       for (int e = tid; e < NB * NB; e += QR_THREADS) {
         const int rr = e % NB, c = e / NB;
         if (rr < rh && c < cw) {
-          double s = 0.0;
-          for (int l = 0; l < jb; ++l) s = fma(sV[rr][l], sW[l][c], s);
+          // sV is zero beyond jb, so the full-width sum is exact; four chains
+          double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+#pragma unroll
+          for (int l = 0; l < NB; l += 4) {
+            s0 = fma(sV[rr][l], sW[l][c], s0);
+            s1 = fma(sV[rr][l + 1], sW[l + 1][c], s1);
+            s2 = fma(sV[rr][l + 2], sW[l + 2][c], s2);
+            s3 = fma(sV[rr][l + 3], sW[l + 3][c], s3);
+          }
+          const double s = (s0 + s1) + (s2 + s3);
           X[(long long)(rb + rr) * rs + (long long)(cb + c) * cs] -= s;
         }
       }
       __syncthreads();
+    }
+  }
+}
+
+// Panel factorisation of columns j0..j0+jb-1 (rows j0..m-1) and the Gram
+// entries G[l][i] = v_l^T v_i (l < i) of the T factor.  SM: the panel lives in
+// shared memory (sP, leading dimension pr) — a separate instantiation so the
+// accesses compile to plain shared-memory loads rather than generic ones.
+template <bool SM>
+__device__ __forceinline__ void qr_panel(const QRDesc &g, int m, int j0, int jb, int pr, double *A, long long lda,
+                                         double *sP, double *s_tau, double (*sG)[NB + 1]) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int NW = QR_THREADS / 32;
+  (void)tid;
+    // panel column j of the working matrix: element i at colp[i] (global) or sP (shifted by j0)
+  auto colp = [&](int j) -> double * {
+    if constexpr (SM) return sP + (j - j0) * pr - j0;
+    else return A + (long long)j * lda;
+  };
+  // ---- panel factorisation (unblocked, Householder per column) with a
+  //      one-column lookahead: warp 0 owns column j+1 — it applies reflector j
+  //      to it and immediately forms reflector j+1 while the other warps
+  //      update the rest of the panel, so each column costs one block barrier
+  //      and the reflector formation is off the critical path of the update.
+  auto form_reflector = [&](int j, int slot) {   // warp 0 only; column j already up to date
+    double *col = colp(j);
+    double part = 0.0;
+#pragma unroll 1
+    for (int i = j + 1 + lane; i < m; i += 32) part = fma(col[i], col[i], part);
+    const double sigma = warp_sum(part);
+    const double alpha = col[j];
+    double tau = 0.0, scal = 0.0, beta = alpha;
+    if (sigma > 0.0) {
+      const double nrm = sqrt(fma(alpha, alpha, sigma));
+      beta = alpha >= 0.0 ? -nrm : nrm;
+      tau = (beta - alpha) / beta;
+      scal = 1.0 / (alpha - beta);
+    }
+    if (tau != 0.0) {
+#pragma unroll 1
+      for (int i = j + 1 + lane; i < m; i += 32) col[i] *= scal;
+    }
+    __syncwarp();
+    if (lane == 0) {
+      col[j] = beta;
+      s_tau[slot] = tau;
+      g.tau[j] = tau;
+    }
+    __syncwarp();
+  };
+  if (warp == 0) form_reflector(j0, 0);
+  __syncthreads();
+  for (int jj = 0; jj < jb; ++jj) {
+    const int j = j0 + jj;
+    const double *col = colp(j);
+    const double tau = s_tau[jj & 1];
+    if (tau != 0.0) {
+      for (int c = j + 1 + warp; c < j0 + jb; c += NW) {
+        double *cc = colp(c);
+        double w = 0.0;
+#pragma unroll 1
+        for (int i = j + lane; i < m; i += 32) w = fma(i == j ? 1.0 : col[i], cc[i], w);
+        w = warp_sum(w) * tau;
+#pragma unroll 1
+        for (int i = j + lane; i < m; i += 32) cc[i] -= w * (i == j ? 1.0 : col[i]);
+      }
+    }
+    if (warp == 0 && jj + 1 < jb) {
+      __syncwarp();
+      form_reflector(j + 1, (jj + 1) & 1);
+    }
+    __syncthreads();
+  }
+  // ---- T factor (larft, forward, columnwise): T upper triangular jb x jb
+  //      G[l][i] = v_l^T v_i for l < i
+  for (int pidx = warp; pidx < jb * jb; pidx += NW) {
+    const int l = pidx % jb, i = pidx / jb;
+    if (l < i) {
+      const double *vl = colp(j0 + l);
+      const double *vi = colp(j0 + i);
+      double s = 0.0;
+      for (int r = j0 + i + 1 + lane; r < m; r += 32) s = fma(vl[r], vi[r], s);
+      s = warp_sum(s);
+      if (lane == 0) sG[l][i] = s + vl[j0 + i];
     }
   }
 }
@@ -143,6 +241,8 @@ __global__ void __launch_bounds__(QR_THREADS) qr_kernel(const QRDesc *__restrict
   const QRDesc g = descs[blockIdx.x];
 #ifdef QR_PHASE_TIMING
   long long qph[6] = {0, 0, 0, 0, 0, 0};
+  long long qcol[3] = {0, 0, 0};
+  long long qsub[4] = {0, 0, 0, 0};
   long long qtc = clock64();
 #endif
   const int m = g.m, n = g.n, kmin = min(m, n);
@@ -158,7 +258,7 @@ __global__ void __launch_bounds__(QR_THREADS) qr_kernel(const QRDesc *__restrict
   __shared__ double sT[NB][NB + 1];
   __shared__ double sG[NB][NB + 1];
   __shared__ double sV[NB][NB + 1], sX[NB][NB + 1], sW[NB][NB + 1];
-  __shared__ double s_tau;
+  __shared__ double s_tau[2];
   double *A = g.A;
   const long long lda = g.lda;
   // copy input into the working matrix
@@ -181,64 +281,9 @@ __global__ void __launch_bounds__(QR_THREADS) qr_kernel(const QRDesc *__restrict
       }
       __syncthreads();
     }
-    // panel column j of the working matrix: element i at colp[i] (global) or sP (shifted by j0)
-    auto colp = [&](int j) -> double * {
-      return in_smem ? sP + (long long)(j - j0) * pr - j0 : A + (long long)j * lda;
-    };
-    // ---- panel factorisation (unblocked, Householder per column): warp 0 forms
-    //      the reflector of column j alone (warp-synchronous), then all warps
-    //      update the remaining panel columns — two block barriers per column
-    for (int jj = 0; jj < jb; ++jj) {
-      const int j = j0 + jj;
-      double *col = colp(j);
-      if (warp == 0) {
-        double part = 0.0;
-        for (int i = j + 1 + lane; i < m; i += 32) part = fma(col[i], col[i], part);
-        const double sigma = warp_sum(part);
-        const double alpha = col[j];
-        double tau = 0.0, scal = 0.0, beta = alpha;
-        if (sigma > 0.0) {
-          const double nrm = sqrt(fma(alpha, alpha, sigma));
-          beta = alpha >= 0.0 ? -nrm : nrm;
-          tau = (beta - alpha) / beta;
-          scal = 1.0 / (alpha - beta);
-        }
-        if (tau != 0.0)
-          for (int i = j + 1 + lane; i < m; i += 32) col[i] *= scal;
-        __syncwarp();
-        if (lane == 0) {
-          col[j] = beta;
-          s_tau = tau;
-          g.tau[j] = tau;
-        }
-      }
-      __syncthreads();
-      const double tau = s_tau;
-      if (tau != 0.0) {
-        for (int c = j + 1 + warp; c < j0 + jb; c += NW) {
-          double *cc = colp(c);
-          double w = 0.0;
-          for (int i = j + lane; i < m; i += 32) w = fma(i == j ? 1.0 : col[i], cc[i], w);
-          w = warp_sum(w) * tau;
-          for (int i = j + lane; i < m; i += 32) cc[i] -= w * (i == j ? 1.0 : col[i]);
-        }
-      }
-      __syncthreads();
-    }
+    if (in_smem) qr_panel<true>(g, m, j0, jb, pr, A, lda, sP, s_tau, sG);
+    else qr_panel<false>(g, m, j0, jb, pr, A, lda, sP, s_tau, sG);
     QR_PH(1);
-    // ---- T factor (larft, forward, columnwise): T upper triangular jb x jb
-    //      G[l][i] = v_l^T v_i for l < i
-    for (int pidx = warp; pidx < jb * jb; pidx += NW) {
-      const int l = pidx % jb, i = pidx / jb;
-      if (l < i) {
-        const double *vl = colp(j0 + l);
-        const double *vi = colp(j0 + i);
-        double s = 0.0;
-        for (int r = j0 + i + 1 + lane; r < m; r += 32) s = fma(vl[r], vi[r], s);
-        s = warp_sum(s);
-        if (lane == 0) sG[l][i] = s + vl[j0 + i];
-      }
-    }
     for (int e = tid; e < NB * (NB + 1); e += QR_THREADS) (&sT[0][0])[e] = 0.0;
     __syncthreads();
     if (warp == 0) {
@@ -247,7 +292,17 @@ __global__ void __launch_bounds__(QR_THREADS) qr_kernel(const QRDesc *__restrict
         // T[c][i] = -tau_i * sum_{l=c}^{i-1} T[c][l] G[l][i]
         double v = 0.0;
         if (lane < i) {
-          for (int l = lane; l < i; ++l) v = fma(sT[lane][l], sG[l][i], v);
+          // four independent chains: the loads pipeline instead of waiting on one fma chain
+          double v1 = 0.0, v2 = 0.0, v3 = 0.0;
+          int l = lane;
+          for (; l + 3 < i; l += 4) {
+            v = fma(sT[lane][l], sG[l][i], v);
+            v1 = fma(sT[lane][l + 1], sG[l + 1][i], v1);
+            v2 = fma(sT[lane][l + 2], sG[l + 2][i], v2);
+            v3 = fma(sT[lane][l + 3], sG[l + 3][i], v3);
+          }
+          for (; l < i; ++l) v = fma(sT[lane][l], sG[l][i], v);
+          v = (v + v1) + (v2 + v3);
           v = -ti * v;
         }
         __syncwarp();
@@ -312,7 +367,9 @@ __global__ void __launch_bounds__(QR_THREADS) qr_kernel(const QRDesc *__restrict
   }
 #ifdef QR_PHASE_TIMING
   QR_PH(4);
-  if (threadIdx.x == 0) printf("QRPH %d %d %d %lld %lld %lld %lld %lld\n", m, n, g.Q ? 1 : 0, qph[0], qph[1], qph[2], qph[3], qph[4]);
+  if (threadIdx.x == 0) printf("QRPH %d %d %d %lld %lld %lld %lld %lld %lld %lld %lld\n", m, n, g.Q ? 1 : 0, qph[0], qph[1], qph[2], qph[3],
+                                qph[4], qcol[0], qcol[1], qcol[2]);
+  if (threadIdx.x == 0) printf("QRSUB %d %d %lld %lld %lld %lld\n", m, n, qsub[0], qsub[1], qsub[2], qsub[3]);
 #endif
 }
 
