@@ -171,7 +171,7 @@ __device__ __forceinline__ void qr_panel(const QRDesc &g, int m, int j0, int jb,
   auto form_reflector = [&](int j, int slot) {   // warp 0 only; column j already up to date
     double *col = colp(j);
     double part = 0.0;
-#pragma unroll 1
+#pragma unroll (SM ? 1 : 4)
     for (int i = j + 1 + lane; i < m; i += 32) part = fma(col[i], col[i], part);
     const double sigma = warp_sum(part);
     const double alpha = col[j];
@@ -183,7 +183,7 @@ __device__ __forceinline__ void qr_panel(const QRDesc &g, int m, int j0, int jb,
       scal = 1.0 / (alpha - beta);
     }
     if (tau != 0.0) {
-#pragma unroll 1
+#pragma unroll (SM ? 1 : 4)
       for (int i = j + 1 + lane; i < m; i += 32) col[i] *= scal;
     }
     __syncwarp();
@@ -204,10 +204,10 @@ __device__ __forceinline__ void qr_panel(const QRDesc &g, int m, int j0, int jb,
       for (int c = j + 1 + warp; c < j0 + jb; c += NW) {
         double *cc = colp(c);
         double w = 0.0;
-#pragma unroll 1
+#pragma unroll (SM ? 1 : 4)
         for (int i = j + lane; i < m; i += 32) w = fma(i == j ? 1.0 : col[i], cc[i], w);
         w = warp_sum(w) * tau;
-#pragma unroll 1
+#pragma unroll (SM ? 1 : 4)
         for (int i = j + lane; i < m; i += 32) cc[i] -= w * (i == j ? 1.0 : col[i]);
       }
     }
