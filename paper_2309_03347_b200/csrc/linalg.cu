@@ -38,7 +38,9 @@ __device__ __forceinline__ double warp_sum(double v) {
 // at X[r*rs + c*cs]):  X[r0:m, cols] -= V * (op(T) * (V^T X[r0:m, cols]))
 // where V = unit lower trapezoidal panel stored in A[:, j0:j0+jb] (lda) with its
 // implicit unit diagonal at row j0+l, and op(T) = T^T (transT = 1) or T.
-__device__ void apply_block_reflector(int m, int j0, int jb, const double *A, long long lda,
+// not inlined: one shared copy for the trailing update and the Q formation
+// keeps the kernel's code footprint down (ncu: no_instruction stalls)
+__device__ __noinline__ void apply_block_reflector(int m, int j0, int jb, const double *A, long long lda,
                                       const double (*sT)[NB + 1], int transT, double *X, long long rs,
                                       long long cs, int c_begin, int c_end, double (*sV)[NB + 1],
                                       double (*sX)[NB + 1], double (*sW)[NB + 1], const double *Vsm = nullptr,
@@ -158,7 +160,7 @@ __device__ __forceinline__ void qr_panel(const QRDesc &g, int m, int j0, int jb,
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   constexpr int NW = QR_THREADS / 32;
   (void)tid;
-    // panel column j of the working matrix: element i at colp[i] (global) or sP (shifted by j0)
+  // panel column j of the working matrix: element i at colp[i] (global) or sP (shifted by j0)
   auto colp = [&](int j) -> double * {
     if constexpr (SM) return sP + (j - j0) * pr - j0;
     else return A + (long long)j * lda;
@@ -177,10 +179,17 @@ __device__ __forceinline__ void qr_panel(const QRDesc &g, int m, int j0, int jb,
     const double alpha = col[j];
     double tau = 0.0, scal = 0.0, beta = alpha;
     if (sigma > 0.0) {
-      const double nrm = sqrt(fma(alpha, alpha, sigma));
+      // dlarfg with beta = -sign(alpha) ||x||: tau = (beta - alpha) / beta =
+      // 1 + |alpha| / ||x||, 1 / (alpha - beta) = sign(alpha) / (|alpha| + ||x||);
+      // one rsqrt and one reciprocal instead of sqrt + two divisions on the
+      // per-column critical path
+      const double ss = fma(alpha, alpha, sigma);
+      const double rs = rsqrt(ss);
+      const double nrm = ss * rs, aa = fabs(alpha);
       beta = alpha >= 0.0 ? -nrm : nrm;
-      tau = (beta - alpha) / beta;
-      scal = 1.0 / (alpha - beta);
+      tau = fma(aa, rs, 1.0);
+      const double q = __drcp_rn(aa + nrm);
+      scal = alpha >= 0.0 ? q : -q;
     }
     if (tau != 0.0) {
 #pragma unroll (SM ? 1 : 4)
@@ -254,7 +263,6 @@ __global__ void __launch_bounds__(QR_THREADS) qr_kernel(const QRDesc *__restrict
     atomicAdd(&g_linalg_flops[0], (unsigned long long)(f > 0 ? f : 0));
   }
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  constexpr int NW = QR_THREADS / 32;
   __shared__ double sT[NB][NB + 1];
   __shared__ double sG[NB][NB + 1];
   __shared__ double sV[NB][NB + 1], sX[NB][NB + 1], sW[NB][NB + 1];
@@ -378,7 +386,7 @@ __global__ void __launch_bounds__(QR_THREADS) qr_kernel(const QRDesc *__restrict
 // the FP64 sqrt/div sequences are the cost of a latency-bound Jacobi round
 __device__ __forceinline__ bool jacobi_orthogonal(double al, double be, double ga, double tol) {
   const double pr = al * be;
-  if (pr > 0.0 && pr < 1e300) return fabs(ga) <= tol * sqrt(pr);
+  if (pr > 0.0 && pr < 1e300) return ga * ga <= (tol * tol) * pr;   // |ga| <= sqrt(pr) < 1e150: no overflow
   return fabs(ga) <= tol * sqrt(al) * sqrt(be);
 }
 
@@ -420,8 +428,9 @@ __device__ void jacobi_core(int m, int p, double *W, long long ldw, double *V, l
         fl += 6ull * m;
         if (jacobi_orthogonal(al, be, ga, tol)) continue;
         fl += 6ull * (m + p);
-        const double zeta = (be - al) / (2.0 * ga);
-        const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(fma(zeta, zeta, 1.0)));
+        const double zeta = (be - al) * __drcp_rn(2.0 * ga);
+        const double tr = __drcp_rn(fabs(zeta) + sqrt(fma(zeta, zeta, 1.0)));
+        const double t = zeta >= 0.0 ? tr : -tr;
         const double c = rsqrt(fma(t, t, 1.0)), s = c * t;
         for (int r = lane; r < m; r += 32) {
           const double x = wa[r], y = wb[r];
@@ -611,8 +620,9 @@ __global__ void __launch_bounds__(BJ_THREADS) jacobi_block_kernel(const SVDDesc 
             fl += 6ull * m;
             if (ga == 0.0 || al == 0.0 || be == 0.0) continue;
             if (jacobi_orthogonal(al, be, ga, tol)) continue;
-            const double zeta = (be - al) / (2.0 * ga);
-            const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(fma(zeta, zeta, 1.0)));
+            const double zeta = (be - al) * __drcp_rn(2.0 * ga);
+            const double tr = __drcp_rn(fabs(zeta) + sqrt(fma(zeta, zeta, 1.0)));
+            const double t = zeta >= 0.0 ? tr : -tr;
             const double c = rsqrt(fma(t, t, 1.0)), s = c * t;
             for (int r = lane; r < m; r += 32) {
               const double x = wa[r], y = wb[r];

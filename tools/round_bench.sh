@@ -12,7 +12,7 @@ done
 timeout 1500 python bench.py --workload c3 --steps 3 --warmup 3 --outer 30 > $O/bench_c3_r01.json 2> $O/bench_c3.err
 timeout 1800 python bench.py --workload c4 --steps 3 --warmup 3 --outer 10 > $O/bench_c4_r01.json 2> $O/bench_c4.err
 if [ "${NCU:-1}" = "1" ]; then
-  ncu --set full --import-source on --clock-control none -k regex:gm_chunk_kernel --launch-skip 300 -c 4 \
+  ncu --set full --import-source on --clock-control none -k regex:gm_chunk_kernel --launch-skip 10 -c 3 \
       -o $O/ncu_gm_chunk_c1 python tools/profile_c1.py --iters 2 > $O/ncu_gm.log 2>&1
   ncu --set full --import-source on --clock-control none -k regex:gemm_dmma --launch-skip 200 -c 3 \
       -o $O/ncu_gemm_c5_r128 python bench.py --workload c5 --rank 128 --no-graph --steps 1 --warmup 0 > $O/ncu_c5.log 2>&1
