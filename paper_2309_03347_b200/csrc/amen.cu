@@ -71,6 +71,9 @@ __global__ void init_ifaces_kernel(Dev D) {
 }
 
 __global__ void set_dv_kernel(double *dv, int i, double v) { dv[i] = v; }
+// device scalar store without a host round trip (a pageable host-to-device
+// copy of a stack value would synchronise the stream first)
+__global__ void set_i32_kernel(int *p, int v) { *p = v; }
 
 // per-bond truncation limits min(rmax, xcap - zcap) >= 1 (room for the enrichment)
 __global__ void set_limits_kernel(const VecMeta x, const VecMeta z, int rmax, int *limit) {
@@ -625,14 +628,9 @@ tt_status amen_solve_meta(const MatMeta &A, const VecMeta &b, const VecMeta &x, 
     dir = -dir;
   }
   (void)zcm; (void)nmax;
-  if (sweeps_dev) cudaMemcpyAsync(sweeps_dev, &sweep, sizeof(int), cudaMemcpyHostToDevice, s);
+  if (sweeps_dev) set_i32_kernel<<<1, 1, 0, s>>>(sweeps_dev, sweep);
   if (res_dev) cudaMemcpyAsync(res_dev, D.dv, sizeof(double), cudaMemcpyDeviceToDevice, s);
-  cudaStreamSynchronize(s);
-  if (status_dev && !(hres <= o.eps)) {
-    int st = TT_ERR_NOCONV;
-    cudaMemcpyAsync(status_dev, &st, sizeof(int), cudaMemcpyHostToDevice, s);
-    cudaStreamSynchronize(s);
-  }
+  if (status_dev && !(hres <= o.eps)) set_i32_kernel<<<1, 1, 0, s>>>(status_dev, (int)TT_ERR_NOCONV);
   return check_launch("amen_solve");
 }
 
@@ -917,10 +915,7 @@ tt_status amen_mv_meta(const MatMeta &A, const VecMeta &b, const VecMeta &y, con
     if (hv[2] <= eps) { ++sweep; break; }
     dir = -dir;
   }
-  if (sweeps_dev) {
-    cudaMemcpyAsync(sweeps_dev, &sweep, sizeof(int), cudaMemcpyHostToDevice, s);
-    cudaStreamSynchronize(s);
-  }
+  if (sweeps_dev) set_i32_kernel<<<1, 1, 0, s>>>(sweeps_dev, sweep);
   return check_launch("amen_mv");
 }
 
