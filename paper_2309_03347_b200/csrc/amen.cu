@@ -542,6 +542,7 @@ tt_status amen_solve_meta(const MatMeta &A, const VecMeta &b, const VecMeta &x, 
     gc.split_elems = GEMM_SPLIT_SCRATCH / 8 - 4096;   // the tail holds the split-K tile counters
   }
   const bool cluster_off = std::getenv("TT_GMRES_NOCLUSTER") != nullptr;
+  const uint64_t hD = hash_bytes(&D, sizeof(D));   // D is fixed for the whole solve: hash it once
   int dir = +1, sweep = 0;
   double hres = 0.0;
   for (sweep = 0; sweep < o.max_sweeps; ++sweep) {
@@ -565,7 +566,7 @@ tt_status amen_solve_meta(const MatMeta &A, const VecMeta &b, const VecMeta &x, 
         gc.cluster = cluster_off ? 0 : ((tiles <= 2 * gmres_cluster_size() && nloc <= 16384) ? 1 : 2);
       }
       // fixed launch sequences before and after the GMRES solve: CUDA-graph replays
-      uint64_t key = hash_bytes(&D, sizeof(D));
+      uint64_t key = hD;
       {
         const long long extra[8] = {k, dir, last, P.Ncap, P.Scap, pc, (long long)(size_t)status_dev, 0x616d};
         key = hash_bytes(extra, sizeof(extra), key);
@@ -620,8 +621,7 @@ tt_status amen_solve_meta(const MatMeta &A, const VecMeta &b, const VecMeta &x, 
       }));
     }
     double hv[3] = {0.0, 0.0, 0.0};
-    cudaMemcpyAsync(hv, D.dv, 3 * sizeof(double), cudaMemcpyDeviceToHost, s);
-    cudaStreamSynchronize(s);
+    TT_TRY(read_back(hv, D.dv, 3 * sizeof(double), s));
     TT_TRY(check_launch("amen sweep"));
     hres = hv[0];
     if (hv[0] <= o.eps || hv[2] <= o.eps) { ++sweep; hres = 0.0; break; }
@@ -903,14 +903,14 @@ tt_status amen_mv_meta(const MatMeta &A, const VecMeta &b, const VecMeta &y, con
     }
     return TT_OK;
   };
+  const uint64_t hD = hash_bytes(&D, sizeof(D));   // D is fixed for the whole product: hash it once
   for (sweep = 0; sweep < max_sweeps; ++sweep) {
-    uint64_t key = hash_bytes(&D, sizeof(D));
+    uint64_t key = hD;
     const long long extra[5] = {dir, P.Ncap, P.Scap, P.pc, 0x6d76};
     key = hash_bytes(extra, sizeof(extra), key);
     TT_TRY(run_captured(key, s, one_sweep));
     double hv[3] = {0.0, 0.0, 0.0};
-    cudaMemcpyAsync(hv, D.dv, 3 * sizeof(double), cudaMemcpyDeviceToHost, s);
-    cudaStreamSynchronize(s);
+    TT_TRY(read_back(hv, D.dv, 3 * sizeof(double), s));
     TT_TRY(check_launch("amen_mv sweep"));
     if (hv[2] <= eps) { ++sweep; break; }
     dir = -dir;

@@ -263,8 +263,7 @@ tt_status keff_meta(const MatMeta &H, const MatMeta &S, const MatMeta &F, const 
     keff_update_kernel<<<1, 1, 0, s>>>(W.sc, W.nrm, o.tol_k, rep.k_hist_dev, rep.sweeps_hist_dev, W.sweeps,
                                        rep.hist_cap, o.max_outer, rep.k_dev, rep.iters_dev, rep.status_dev);
     TT_TRY(scale_meta(psi, &W.sc->nrm_inv, 1.0, 0, s));
-    cudaMemcpyAsync(&hflag, &W.sc->flag, sizeof(int), cudaMemcpyDeviceToHost, s);
-    cudaStreamSynchronize(s);
+    TT_TRY(read_back(&hflag, &W.sc->flag, sizeof(int), s));
     TT_TRY(check_launch("keff iteration"));
     if (hflag) break;
   }
@@ -405,8 +404,7 @@ tt_status alpha_meta(const MatMeta &H, const MatMeta &V, const MatMeta &S, const
     alpha_update_kernel<<<1, 1, 0, s>>>(W.st, W.kk, W.kit, W.kst, o.alpha1, o.tol, o.max_alpha, rep.alpha_hist_dev,
                                         rep.k_hist_dev, rep.keff_iters_hist_dev, rep.hist_cap, rep.alpha_dev,
                                         rep.k_dev, rep.iters_dev, rep.status_dev);
-    cudaMemcpyAsync(&hflag, &W.st->flag, sizeof(int), cudaMemcpyDeviceToHost, s);
-    cudaStreamSynchronize(s);
+    TT_TRY(read_back(&hflag, &W.st->flag, sizeof(int), s));
     TT_TRY(check_launch("alpha iteration"));
     if (hflag) break;
   }

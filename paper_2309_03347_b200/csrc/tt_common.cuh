@@ -35,6 +35,8 @@ struct MatMeta {
 void set_error(const std::string &msg);
 tt_status fail(tt_status st, const std::string &msg);
 tt_status check_launch(const char *what);
+// device -> host copy of a few bytes, waited for by polling an event (<= 256 bytes)
+tt_status read_back(void *dst, const void *src_dev, size_t bytes, cudaStream_t s);
 
 #define TT_TRY(expr)                    \
   do {                                  \

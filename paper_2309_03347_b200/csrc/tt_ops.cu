@@ -26,6 +26,31 @@ tt_status check_launch(const char *what) {
   return TT_OK;
 }
 
+// Small device -> host read of a convergence word: a pinned per-thread staging
+// buffer and an event polled by the calling thread (the drivers' sweep and
+// outer-iteration tests; measured: a pageable copy + stream synchronise left
+// the GPU idle ~80 us per test).
+tt_status read_back(void *dst, const void *src_dev, size_t bytes, cudaStream_t s) {
+  struct Stage {
+    void *buf = nullptr;
+    cudaEvent_t ev = nullptr;
+  };
+  static thread_local Stage st;
+  if (bytes > 256) return fail(TT_ERR_ARG, "read_back: at most 256 bytes");
+  if (!st.buf) {
+    if (cudaMallocHost(&st.buf, 256) != cudaSuccess) return check_launch("read_back: cudaMallocHost");
+    if (cudaEventCreateWithFlags(&st.ev, cudaEventDisableTiming) != cudaSuccess) return check_launch("read_back: event");
+  }
+  cudaMemcpyAsync(st.buf, src_dev, bytes, cudaMemcpyDeviceToHost, s);
+  cudaEventRecord(st.ev, s);
+  cudaError_t e;
+  while ((e = cudaEventQuery(st.ev)) == cudaErrorNotReady) {
+  }
+  if (e != cudaSuccess) return fail(TT_ERR_CUDA, std::string("read_back: ") + cudaGetErrorString(e));
+  std::memcpy(dst, st.buf, bytes);
+  return TT_OK;
+}
+
 // --------------------------------------------------------------- metas ---
 tt_status make_vec_meta(const tt_vec *x, VecMeta &m) {
   if (!x || !x->n || !x->rcap || !x->off || !x->r_dev || !x->data)

@@ -19,7 +19,9 @@
 namespace {
 std::atomic<unsigned long long> g_all{0}, g_ours{0};
 std::mutex g_mu;
-struct Span { unsigned long long s, e; };
+struct Span { unsigned long long s, e; int name; };
+std::map<std::string, int> g_name_id;
+std::vector<std::string> g_names;
 std::vector<Span> g_spans;
 std::map<std::string, std::pair<unsigned long long, unsigned long long>> g_by_name;  // count, ns
 std::string g_watch;                                    // substring of kernel names whose instances are kept
@@ -40,7 +42,12 @@ void CUPTIAPI buffer_completed(CUcontext, uint32_t, uint8_t *buffer, size_t, siz
       const CUpti_ActivityKernel9 *k = reinterpret_cast<const CUpti_ActivityKernel9 *>(rec);
       g_all++;
       if (k->name && (std::strncmp(k->name, "_ZN2tt", 6) == 0 || std::strstr(k->name, "tt::"))) g_ours++;
-      g_spans.push_back({k->start, k->end});
+      const std::string nm = k->name ? std::string(k->name).substr(0, 80) : std::string("?");
+      auto it = g_name_id.find(nm);
+      int id;
+      if (it == g_name_id.end()) { id = (int)g_names.size(); g_name_id[nm] = id; g_names.push_back(nm); }
+      else id = it->second;
+      g_spans.push_back({k->start, k->end, id});
       if (!g_watch.empty() && k->name && std::strstr(k->name, g_watch.c_str()))
         g_inst.push_back({k->start, k->end - k->start});
       auto &v = g_by_name[k->name ? std::string(k->name).substr(0, 80) : std::string("?")];
@@ -59,6 +66,8 @@ extern "C" int lc_start() {
     std::lock_guard<std::mutex> lk(g_mu);
     g_spans.clear();
     g_by_name.clear();
+    g_name_id.clear();
+    g_names.clear();
     g_inst.clear();
     const char *w = std::getenv("LC_WATCH");
     g_watch = w ? w : "";
@@ -92,6 +101,22 @@ extern "C" int lc_dump(const char *path) {
     else if (s.e > cur_e) cur_e = s.e;
   }
   if (have) busy += cur_e - cur_s;
+  // idle gaps (GPU waiting for the host) longer than 5 us, by the kernel that ends them
+  {
+    std::map<int, std::pair<unsigned long long, unsigned long long>> gaps;  // name -> count, ns
+    unsigned long long end = 0;
+    bool h = false;
+    for (const Span &sp : v) {
+      if (h && sp.s > end + 5000) { auto &gg = gaps[sp.name]; gg.first += 1; gg.second += sp.s - end; }
+      if (!h || sp.e > end) end = sp.e;
+      h = true;
+    }
+    std::string p3 = std::string(path) + ".gaps";
+    if (FILE *g = std::fopen(p3.c_str(), "w")) {
+      for (const auto &kv : gaps) std::fprintf(g, "%llu %llu %s\n", kv.second.first, kv.second.second, g_names[kv.first].c_str());
+      std::fclose(g);
+    }
+  }
   const unsigned long long span = v.empty() ? 0 : (v.back().e > cur_e ? v.back().e : cur_e) - v.front().s;
   std::fprintf(f, "%llu %llu\n", span, busy);
   for (const auto &kv : g_by_name) std::fprintf(f, "%llu %llu %s\n", kv.second.first, kv.second.second, kv.first.c_str());

@@ -58,3 +58,15 @@ print(f"{cfg}: {it} iterations, kernels {o.value} (all {a.value}), span {span / 
       f"({100 * busy / span:.1f}%), {span / 1e6 / it:.2f} ms per iteration")
 for ns, c, name in rows[:25]:
     print(f"{ns / 1e6:9.2f} ms {100 * ns / busy:5.1f}% {c:7d} x {ns / c / 1e3:7.1f} us  {name}")
+
+gp = out + ".gaps"
+if os.path.exists(gp):
+    gl = []
+    for l in open(gp).read().splitlines():
+        c, ns, name = l.split(" ", 2)
+        name = subprocess.run(["c++filt"], input=name, capture_output=True, text=True).stdout.strip()[:70]
+        gl.append((int(ns), int(c), name))
+    gl.sort(reverse=True)
+    print(f"idle gaps > 5 us: {sum(c for _, c, _ in gl)} totalling {sum(n for n, _, _ in gl) / 1e6:.1f} ms, by the kernel that ends them:")
+    for ns, c, name in gl[:12]:
+        print(f"{ns / 1e6:9.2f} ms {c:7d} x {ns / c / 1e3:7.1f} us  {name}")
