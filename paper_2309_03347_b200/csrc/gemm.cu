@@ -769,30 +769,58 @@ __global__ void __launch_bounds__(GF_THREADS) gm_chunk_kernel(GmChunkArgs a) {
     for (int sidx = 0; sidx < 3; ++sidx)
       gemm_stage<CLUSTER>(sdesc[3 * (j + 1 - jbase) + sidx], a.split, a.split_elems, a.bar, G, smem, true, false);
     GM_PH(1);
-    // ---- CGS2 pass 1: slice dots
+    // ---- CGS pass 1: slice dots, plus |w|^2 for the reorthogonalisation test
     double *my1 = part1 + (size_t)blockIdx.x * GF_LD;
     slice_dots(a.V, a.ldv, w, lo, hi, j + 1, my1);
+    {
+      double w2 = 0.0;
+      for (int e = lo + tid; e < hi; e += GF_THREADS) w2 = fma(w[e], w[e], w2);
+      w2 = warp_sum(w2);
+      if (lane == 0) red[warp] = w2;
+      __syncthreads();
+      if (tid == 0) {
+        double t = 0.0;
+        for (int q = 0; q < NW; ++q) t += red[q];
+        my1[j + 1] = t;
+      }
+    }
     phase_sync<CLUSTER>(a.bar, G);
     GM_PH(2);
-    cross_cta_sum(part1, G, j + 1, h1s, sred);  // fixed order: identical in every CTA
+    cross_cta_sum(part1, G, j + 2, h1s, sred);  // fixed order: identical in every CTA
     for (int e = lo + tid; e < hi; e += GF_THREADS) {
       double x = w[e];
       for (int i = 0; i <= j; ++i) x = fma(-h1s[i], a.V[(long long)i * a.ldv + e], x);
       w[e] = x;
     }
-    __syncthreads();
-    // ---- pass 2 on the updated slice
-    double *my2 = part2 + (size_t)blockIdx.x * GF_LD;
-    slice_dots(a.V, a.ldv, w, lo, hi, j + 1, my2);
+    // DGKS test (Daniel, Gragg, Kaufman & Stewart 1976): a second Gram-Schmidt
+    // pass only when the projection removed more than half of |w|^2
+    // (|w'|^2 = |w|^2 - sum h^2 < |w|^2 / 2); the decision is made on values
+    // that are identical in every CTA, so it is uniform over the grid
+    bool reorth;
+    {
+      double hh = 0.0;
+      for (int i = 0; i <= j; ++i) hh = fma(h1s[i], h1s[i], hh);
+      reorth = !(h1s[j + 1] - hh > 0.5 * h1s[j + 1]);
+    }
     // rotations and g[j] of earlier steps, read before CTA 0 rewrites them in this step
     for (int i = tid; i < j; i += GF_THREADS) { css[i] = st->cs[i]; sns[i] = st->sn[i]; }
     const double gj = st->g[j];
-    phase_sync<CLUSTER>(a.bar, G);
-    cross_cta_sum(part2, G, j + 1, h2s, sred);
+    if (reorth) {
+      __syncthreads();
+      // ---- pass 2 on the updated slice
+      double *my2 = part2 + (size_t)blockIdx.x * GF_LD;
+      slice_dots(a.V, a.ldv, w, lo, hi, j + 1, my2);
+      phase_sync<CLUSTER>(a.bar, G);
+      cross_cta_sum(part2, G, j + 1, h2s, sred);
+    } else {
+      for (int i = tid; i <= j; i += GF_THREADS) h2s[i] = 0.0;
+      __syncthreads();
+    }
     double nrm = 0.0;
     for (int e = lo + tid; e < hi; e += GF_THREADS) {
       double x = w[e];
-      for (int i = 0; i <= j; ++i) x = fma(-h2s[i], a.V[(long long)i * a.ldv + e], x);
+      if (reorth)
+        for (int i = 0; i <= j; ++i) x = fma(-h2s[i], a.V[(long long)i * a.ldv + e], x);
       w[e] = x;
       nrm = fma(x, x, nrm);
     }
@@ -849,7 +877,7 @@ __global__ void __launch_bounds__(GF_THREADS) gm_chunk_kernel(GmChunkArgs a) {
     __syncthreads();
     const bool stop = red[0] != 0.0;
     if (blockIdx.x == 0 && tid == 0) {
-      atomicAdd(&g_gm_counters[1], (unsigned long long)N * (8ull * (j + 1) + 3ull));
+      atomicAdd(&g_gm_counters[1], (unsigned long long)N * ((reorth ? 8ull : 4ull) * (j + 1) + 5ull));
       atomicAdd(&g_gm_counters[2], 1ull);
     }
     if (red[1] > 0.0) {
