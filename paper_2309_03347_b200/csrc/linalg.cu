@@ -157,9 +157,8 @@ __device__ __noinline__ void apply_block_reflector(int m, int j0, int jb, const 
 template <bool SM>
 __device__ __forceinline__ void qr_panel(const QRDesc &g, int m, int j0, int jb, int pr, double *A, long long lda,
                                          double *sP, double *s_tau, double (*sG)[NB + 1]) {
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   constexpr int NW = QR_THREADS / 32;
-  (void)tid;
   // panel column j of the working matrix: element i at colp[i] (global) or sP (shifted by j0)
   auto colp = [&](int j) -> double * {
     if constexpr (SM) return sP + (j - j0) * pr - j0;
@@ -250,8 +249,6 @@ __global__ void __launch_bounds__(QR_THREADS) qr_kernel(const QRDesc *__restrict
   const QRDesc g = descs[blockIdx.x];
 #ifdef QR_PHASE_TIMING
   long long qph[6] = {0, 0, 0, 0, 0, 0};
-  long long qcol[3] = {0, 0, 0};
-  long long qsub[4] = {0, 0, 0, 0};
   long long qtc = clock64();
 #endif
   const int m = g.m, n = g.n, kmin = min(m, n);
@@ -375,9 +372,7 @@ __global__ void __launch_bounds__(QR_THREADS) qr_kernel(const QRDesc *__restrict
   }
 #ifdef QR_PHASE_TIMING
   QR_PH(4);
-  if (threadIdx.x == 0) printf("QRPH %d %d %d %lld %lld %lld %lld %lld %lld %lld %lld\n", m, n, g.Q ? 1 : 0, qph[0], qph[1], qph[2], qph[3],
-                                qph[4], qcol[0], qcol[1], qcol[2]);
-  if (threadIdx.x == 0) printf("QRSUB %d %d %lld %lld %lld %lld\n", m, n, qsub[0], qsub[1], qsub[2], qsub[3]);
+  if (threadIdx.x == 0) printf("QRPH %d %d %d %lld %lld %lld %lld %lld\n", m, n, g.Q ? 1 : 0, qph[0], qph[1], qph[2], qph[3], qph[4]);
 #endif
 }
 
