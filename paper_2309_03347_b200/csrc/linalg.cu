@@ -17,7 +17,8 @@ __device__ unsigned long long g_linalg_flops[2];
 namespace {
 
 #ifndef QR_THREADS_DEF
-#define QR_THREADS_DEF 1024   // measured: 1024 > 512 > 256 (C1 94.1 / 94.0 / 91.1 iter/s, C2 6.13 / 6.05 / 5.55)
+#define QR_THREADS_DEF 1024   // measured: 1024 > 512 > 256 (C1 94.1 / 94.0 / 91.1 iter/s, C2 6.13 / 6.05 / 5.55;
+                              // re-measured on the final round-1 code: 1024 vs 512 = C1 103.7 / 103.5, C2 6.32 / 6.24)
 #endif
 constexpr int QR_THREADS = QR_THREADS_DEF;
 constexpr int QR_NQ = (32 * 32 + QR_THREADS - 1) / QR_THREADS;   // (l, c) entries per thread in the reflector
