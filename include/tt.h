@@ -94,6 +94,10 @@ void tt_counters(uint64_t *out /* [5] */, int32_t reset);
  * resets (the flop counters count every fused launch since the last read). */
 void tt_fused_profile(int32_t enable);
 void tt_fused_profile_read(int64_t *launches, double *ms, double *flops /* [3] */);
+/* Per-core breakdown of the same recorded launches (AMEn core index k): summed
+ * duration ms[k], Arnoldi steps steps[k] and launches[k], arrays of TT_MAX_D.
+ * Call before tt_fused_profile_read (which resets). */
+void tt_fused_profile_cores(double *ms, double *steps, int64_t *launches);
 
 /* ---------------------------------------------------------------- a1 ---
  * tt_matvec: exact TT-matrix x TT-vector product ("explicit and
@@ -192,6 +196,48 @@ tt_status als_update_interfaces(int32_t dir, int32_t rY, int32_t R, int32_t rX, 
                                 const double *Xk, double *Inext, void *ws, size_t wsb,
                                 tt_stream s);
 
+/* Structured operator cores ("the angle core n=288 has an
+ * n^2 R^2 stage that grows large unless the diagonal (H) ... angular structure
+ * is exploited").  The angle and group factors of H are diagonal, Q_mu =
+ * C_b (x) diag(mu) and H_sigma = diag(sigma) o (C_b (x) I)
+ * (P:1222-1225), and sums / roundings of such cores keep every slice
+ * A_k[g, :, :, g'] diagonal: D_i[g, g'] = A_k[g, i, i, g'].
+ *
+ * tt_core_kinds: detects, on the device, which cores of A are TT_CORE_DIAG
+ * (m == n >= 4 and max|off-diagonal| <= 1e-13 max|A_k|; the rest TT_CORE_DENSE)
+ * and returns the kinds (host [d]) and the off-diagonal ratios (host [d] or
+ * NULL; -1 for non-square or small cores).  Synchronises the stream once.
+ * ws: >= 768 bytes of device workspace.  amen_solve / amen_mv / keff run the
+ * same detection internally. */
+typedef enum { TT_CORE_DENSE = 0, TT_CORE_DIAG = 1 } tt_core_kind;
+tt_status tt_core_kinds(const tt_mat *A, int32_t *kinds, double *offdiag_ratio, void *ws, size_t wsb, tt_stream s);
+
+/* als_local_apply_structured / als_update_interfaces_structured: the a6 / a5
+ * contractions of als_local_apply / als_update_interfaces (same arguments and
+ * layouts) for a core of the given kind.  TT_CORE_DIAG reads only the
+ * diagonal slices of Ak (off-diagonal entries are ignored) and replaces the
+ * dense (R m) x (n R') stage by m batched R x R' products: the apply costs
+ * 2 m (rB rBp rAp Rp + R Rp rB rAp + rA rAp rB R) flops instead of
+ * 2 (n rB rBp rAp Rp + m n rB rAp R Rp + m rA rAp rB R).  absorb = 1 (diagonal
+ * cores only; for the interface form only dir = +1) first absorbs the left
+ * operator rank into the left interface, Pt_i[a, b, g'] = sum_g Phi[a, g, b]
+ * D_i[g, g'], which the AMEn local solve does once per local system:
+ *   y[a, i, a'] = sum_{b, g'} Pt_i[a, b, g'] sum_b' x[b, i, b'] Psi[a', g', b'],
+ * 2 m (rB rBp rAp Rp + rA rB Rp rAp) flops per apply (the C4 angle core: 1.5
+ * GFLOP instead of 105.7 dense).  kind = TT_CORE_DENSE, absorb = 0 is the
+ * plain call.  TT_ERR_SHAPE if a diagonal core is not square.  Workspace:
+ * als_workspace_structured(...). */
+size_t als_workspace_structured(int32_t kind, int32_t absorb, int32_t rA, int32_t R, int32_t rB, int32_t m, int32_t n,
+                                int32_t rAp, int32_t Rp, int32_t rBp);
+tt_status als_local_apply_structured(int32_t kind, int32_t absorb, int32_t rA, int32_t R, int32_t rB, int32_t m,
+                                     int32_t n, int32_t rAp, int32_t Rp, int32_t rBp, const double *Phi,
+                                     const double *Ak, const double *Psi, const double *x, double *y, void *ws,
+                                     size_t wsb, tt_stream s);
+tt_status als_update_interfaces_structured(int32_t kind, int32_t absorb, int32_t dir, int32_t rY, int32_t R,
+                                           int32_t rX, int32_t m, int32_t n, int32_t rYp, int32_t Rp, int32_t rXp,
+                                           const double *Iprev, const double *Yk, const double *Ak,
+                                           const double *Xk, double *Inext, void *ws, size_t wsb, tt_stream s);
+
 /* ---------------------------------------------------------------- a7 ---
  * amen_solve: x ~ A^{-1} b in TT ("amen_solve";
  * reading Z20): alternating-direction sweeps, Galerkin local systems solved by
@@ -238,36 +284,56 @@ tt_status amen_mv(const tt_mat *A, const tt_vec *b, tt_vec *y, tt_vec *z, double
 /* ---------------------------------------------------------------- a9 ---
  * keff_fixed_point: eqn:TT_k_eff_fixed_points, readings
  * Z16-Z19:
- *   B = round(round(S Psi) + k^{-1} round(F Psi));  H Psi' = B (amen_solve,
- *   warm start Psi);  k' = k <f, Psi'> / <f, Psi>, f = F^T 1;  Psi <- Psi'/||Psi'||;
- *   stop when |k' - k| <= tol_k or after max_outer iterations.
- * k, ||Psi||, <f, Psi> and every rank stay on the device; the host only
- * polls the convergence flag once per outer iteration.  psi: in Psi_0, out
- * normalised eigenvector (capacities >= rmax + kickrank).  z: AMEn residual
- * TT (random initial cores are an input).  Report arrays are device memory.
- * Workspace: keff_workspace(...). */
+ *   B = round(round(S Psi) + k^{-1} round(F Psi))  (matvec = 0) or
+ *   B = amen_mv(S + k^{-1} F, Psi)                  (matvec = 1, the paper's choice);
+ *   H Psi' = B (amen_solve, warm start Psi);  k' = k <f, Psi'> / <f, Psi>,
+ *   f = F^T 1;  Psi <- Psi'/||Psi'||.
+ * Fixed-point residual (reading Z19): res = ||H Psi - (S + F/k) Psi|| /
+ * ||H Psi|| for the normalised iterate and its k, both products by amen_mv to
+ * eps_round (M = H - S - k^{-1} F as one TT-matrix, ranks add; capacities of
+ * psi), the norms by orthogonalisation.  tol_res > 0: evaluated every
+ * iteration and required for convergence; tol_res == 0: evaluated once after
+ * the last iteration (reported, not tested); tol_res < 0: never.
+ * Converged (status TT_OK) when |k' - k| <= tol_k and (tol_res <= 0 or
+ * res <= tol_res); TT_ERR_NOCONV after max_outer iterations (history written).
+ * The inner AMEn status of each iteration (TT_OK / TT_ERR_NOCONV: the local
+ * residual did not reach eps_solve within max_sweeps, the normal state of a
+ * truncation-limited solve) is reported per iteration, not folded into
+ * status: the outer residual is the convergence evidence.
+ * k, ||Psi||, <f, Psi>, the residual and every rank stay on the device; the
+ * host polls one convergence word per outer iteration.  psi: in Psi_0, out the
+ * normalised eigenvector (capacities >= rmax + kickrank).  z: AMEn residual TT
+ * (random initial cores are an input; its interior ranks are the kickrank).
+ * Report arrays are device memory (NULL allowed except k_dev, iters_dev,
+ * status_dev).  Workspace: keff_workspace(...). */
 typedef struct {
   double tol_k;            /* |k' - k| stopping tolerance                          */
-  double eps_round;        /* rounding tolerance of S Psi, F Psi, B                */
+  double tol_res;          /* fixed-point residual tolerance (see above)           */
+  double eps_round;        /* rounding / amen_mv tolerance of B and the residual    */
   double eps_solve;        /* AMEn tolerance                                       */
   int32_t max_outer;
   int32_t rmax;
   int32_t max_sweeps;
+  int32_t kickrank;        /* 0: the interior rank capacity of z; > 0: must equal it */
   int32_t gmres_restart;
   int32_t gmres_max_restarts;
-  int32_t matvec;          /* 0: B = round(round(S Psi) + k^{-1} round(F Psi)) by   */
-                           /*    exact products; 1: B = amen_mv(S + k^{-1} F, Psi)   */
-                           /*    to eps_round (the paper's choice),     */
+  int32_t local_dense_max; /* must be 0: local systems are solved by GMRES only      */
+  int32_t matvec;          /* 0: B by exact products + rounding; 1: B = amen_mv(S +  */
+                           /*    k^{-1} F, Psi) to eps_round,          */
                            /*    warm-started from the previous B                    */
-  int32_t mv_max_sweeps;   /* amen_mv sweep limit (matvec = 1)                       */
+  int32_t mv_max_sweeps;   /* amen_mv sweep limit (B and the residual products)      */
 } keff_opts;
 typedef struct {
   double *k_dev;           /* [1] final k                                          */
   int32_t *iters_dev;      /* [1] outer iterations performed                       */
   double *k_hist_dev;      /* [hist_cap] k after each outer iteration              */
-  int32_t *sweeps_hist_dev;/* [hist_cap] AMEn sweeps per outer iteration           */
+  double *res_hist_dev;    /* [hist_cap] fixed-point residual per iteration (-1    */
+                           /*    where not evaluated)                              */
   int32_t hist_cap;
   int32_t *status_dev;     /* [1] TT_OK / TT_ERR_NOCONV / TT_ERR_NOFISSION / ...   */
+  int32_t *sweeps_hist_dev;/* [hist_cap] AMEn sweeps per outer iteration           */
+  int32_t *inner_status_hist_dev; /* [hist_cap] AMEn status per outer iteration    */
+  double *res_dev;         /* [1] last evaluated residual (-1 if none)             */
 } keff_report;
 size_t keff_workspace(const tt_mat *H, const tt_mat *S, const tt_mat *F, const tt_vec *psi,
                       const tt_vec *z, const keff_opts *o);

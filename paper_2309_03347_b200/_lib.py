@@ -38,15 +38,16 @@ class amen_opts(C.Structure):
 
 
 class keff_opts(C.Structure):
-    _fields_ = [("tol_k", C.c_double), ("eps_round", C.c_double), ("eps_solve", C.c_double),
-                ("max_outer", C.c_int32), ("rmax", C.c_int32), ("max_sweeps", C.c_int32),
-                ("gmres_restart", C.c_int32), ("gmres_max_restarts", C.c_int32), ("matvec", C.c_int32),
-                ("mv_max_sweeps", C.c_int32)]
+    _fields_ = [("tol_k", C.c_double), ("tol_res", C.c_double), ("eps_round", C.c_double),
+                ("eps_solve", C.c_double), ("max_outer", C.c_int32), ("rmax", C.c_int32), ("max_sweeps", C.c_int32),
+                ("kickrank", C.c_int32), ("gmres_restart", C.c_int32), ("gmres_max_restarts", C.c_int32),
+                ("local_dense_max", C.c_int32), ("matvec", C.c_int32), ("mv_max_sweeps", C.c_int32)]
 
 
 class keff_report(C.Structure):
     _fields_ = [("k_dev", C.c_void_p), ("iters_dev", C.c_void_p), ("k_hist_dev", C.c_void_p),
-                ("sweeps_hist_dev", C.c_void_p), ("hist_cap", C.c_int32), ("status_dev", C.c_void_p)]
+                ("res_hist_dev", C.c_void_p), ("hist_cap", C.c_int32), ("status_dev", C.c_void_p),
+                ("sweeps_hist_dev", C.c_void_p), ("inner_status_hist_dev", C.c_void_p), ("res_dev", C.c_void_p)]
 
 
 class alpha_opts(C.Structure):
@@ -68,6 +69,7 @@ SIG = {
     "tt_counters": (None, [C.POINTER(C.c_uint64), I32]),
     "tt_fused_profile": (None, [I32]),
     "tt_fused_profile_read": (None, [C.POINTER(C.c_int64), C.POINTER(C.c_double), C.POINTER(C.c_double)]),
+    "tt_fused_profile_cores": (None, [C.POINTER(C.c_double), C.POINTER(C.c_double), C.POINTER(C.c_int64)]),
     "tt_matvec": (I32, [C.POINTER(tt_mat), C.POINTER(tt_vec), C.POINTER(tt_vec), P]),
     "tt_matvec_batched_workspace": (C.c_size_t, [I32, C.POINTER(tt_mat)]),
     "tt_matvec_batched": (I32, [I32, C.POINTER(tt_mat), C.POINTER(tt_vec), C.POINTER(tt_vec), P, C.c_size_t, P]),
@@ -83,6 +85,10 @@ SIG = {
     "als_workspace": (C.c_size_t, [I32] * 8),
     "als_local_apply": (I32, [I32] * 8 + [P, P, P, P, P, P, C.c_size_t, P]),
     "als_update_interfaces": (I32, [I32] * 9 + [P, P, P, P, P, P, C.c_size_t, P]),
+    "tt_core_kinds": (I32, [C.POINTER(tt_mat), P, P, P, C.c_size_t, P]),
+    "als_workspace_structured": (C.c_size_t, [I32] * 10),
+    "als_local_apply_structured": (I32, [I32] * 10 + [P, P, P, P, P, P, C.c_size_t, P]),
+    "als_update_interfaces_structured": (I32, [I32] * 11 + [P, P, P, P, P, P, C.c_size_t, P]),
     "amen_workspace": (C.c_size_t, [C.POINTER(tt_mat), C.POINTER(tt_vec), C.POINTER(tt_vec),
                                     C.POINTER(tt_vec), C.POINTER(amen_opts)]),
     "amen_solve": (I32, [C.POINTER(tt_mat), C.POINTER(tt_vec), C.POINTER(tt_vec), C.POINTER(tt_vec),

@@ -141,9 +141,16 @@ void linalg_counters(unsigned long long *out, int reset);
 namespace tt {
 void fused_profile(int enable);
 void fused_profile_read(long long *launches, double *ms, double *flops);
+void fused_profile_cores(double *ms, double *steps, long long *launches);
 }
 
 extern "C" void tt_fused_profile(int32_t enable) { tt::fused_profile(enable); }
+
+extern "C" void tt_fused_profile_cores(double *ms, double *steps, int64_t *launches) {
+  long long l[TT_MAX_D];
+  tt::fused_profile_cores(ms, steps, l);
+  for (int t = 0; t < TT_MAX_D; ++t) launches[t] = l[t];
+}
 
 extern "C" void tt_fused_profile_read(int64_t *launches, double *ms, double *flops) {
   long long l = 0;

@@ -49,7 +49,55 @@ struct Dev {  // device-side view passed by value to the plan kernels
   int *limit;       // [d+1] per-bond truncation limit
   int m;            // GMRES restart
   const int *gskip; // GMRES stop word: apply GEMMs after convergence are no-ops
+  double *Pt, *Dc;  // diagonal cores: left interface with the operator rank absorbed, compact diagonal
+  float *kscr;      // core-structure detection scratch
+  char *qrws;       // TSQR scratch of the tall unfoldings
+  size_t qrwsb;
 };
+
+// capacity shapes of the QR problems at core k: the SVD-QR of the local solution
+// (tall or transposed) and the enrichment QR of [x | z-part]
+struct QCap { int m, n; };
+inline QCap qcap_svd(const VecMeta &x, int k, int dir) {
+  const int n = x.n[k];
+  const int mm = dir > 0 ? x.rcap[k] * n : n * x.rcap[k + 1], nn = dir > 0 ? x.rcap[k + 1] : x.rcap[k];
+  return {mm > nn ? mm : nn, mm < nn ? mm : nn};
+}
+inline QCap qcap_enrich(const VecMeta &x, int k, int dir) {
+  const int n = x.n[k];
+  const int mm = dir > 0 ? x.rcap[k] * n : n * x.rcap[k + 1], cols = dir > 0 ? x.rcap[k + 1] : x.rcap[k];
+  return {mm, cols < mm ? cols : mm};
+}
+inline size_t qr_ws_amen(const VecMeta &x) {
+  size_t b = 0;
+  for (int k = 0; k < x.d; ++k)
+    for (int dir = -1; dir <= 1; dir += 2) {
+      const QCap a = qcap_svd(x, k, dir), e = qcap_enrich(x, k, dir);
+      const size_t v = qr_tall_ws_bytes(a.m, a.n), u = qr_tall_ws_bytes(e.m, e.n);
+      b = v > b ? v : b;
+      b = u > b ? u : b;
+    }
+  return b;
+}
+
+// diagonal core whose left operator rank is absorbed into the left interface
+// (als.h descs_local_apply_pt); decided on capacities so host and device agree
+__host__ __device__ inline bool use_pt(const MatMeta &A, int k) {
+  return A.kind[k] == KIND_DIAG && A.m[k] == A.n[k] && A.Rcap[k] >= A.Rcap[k + 1];
+}
+
+// Dc[g + R (g' + Rp i)] = A_k[g, i, i, g'] (device ranks)
+__global__ void diag_extract_kernel(const MatMeta A, int k, double *Dc) {
+  const int R0 = A.R[k], R1 = A.R[k + 1], m = A.m[k];
+  const double *c = A.data + A.off[k];
+  const long long tot = (long long)R0 * R1 * m;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < tot; e += (long long)gridDim.x * blockDim.x) {
+    const int g = (int)(e % R0);
+    const long long t = e / R0;
+    const int gp = (int)(t % R1), i = (int)(t / R1);
+    Dc[e] = c[g + (long long)R0 * i * (1 + m) + (long long)R0 * m * m * gp];
+  }
+}
 
 __device__ GemmDesc gdd(int M, int N, int K, const double *A, long long lda, int tA, const double *B, long long ldb,
                         int tB, double *C, long long ldc) {
@@ -91,15 +139,18 @@ __global__ void plan_iface(Dev D, int k, int dir) {
   const int R0 = D.A.R[k], R1 = D.A.R[k + 1], b0 = D.b.r[k], b1 = D.b.r[k + 1];
   const double *X = D.x.data + D.x.off[k], *Z = D.z.data + D.z.off[k], *Bk = D.b.data + D.b.off[k];
   const double *Ak = D.A.data + D.A.off[k];
+  const int kd = D.A.kind[k];
   if (dir < 0) {
-    descs_iface_right(r0, R0, r0, n, n, r1, R1, r1, D.AR[k + 1], X, Ak, X, D.AR[k], D.T1, D.T2, D.gd + 0);
+    descs_iface_right_k(kd, r0, R0, r0, n, n, r1, R1, r1, D.AR[k + 1], X, Ak, X, D.AR[k], D.T1, D.T2, D.gd + 0);
     descs_iface_right_vec(r0, b0, n, r1, b1, D.BR[k + 1], X, Bk, D.BR[k], D.T1, D.gd + 3);
-    descs_iface_right(z0, R0, r0, n, n, z1, R1, r1, D.ZAR[k + 1], Z, Ak, X, D.ZAR[k], D.T1, D.T2, D.gd + 5);
+    descs_iface_right_k(kd, z0, R0, r0, n, n, z1, R1, r1, D.ZAR[k + 1], Z, Ak, X, D.ZAR[k], D.T1, D.T2, D.gd + 5);
     descs_iface_right_vec(z0, b0, n, z1, b1, D.ZBR[k + 1], Z, Bk, D.ZBR[k], D.T1, D.gd + 8);
   } else {
-    descs_iface_left(r0, R0, r0, n, n, r1, R1, r1, D.AL[k], X, Ak, X, D.AL[k + 1], D.T1, D.T2, D.gd + 0);
+    // (x|A|x): the Pt of this core's local solve (same AL[k] and A_k) when absorbed
+    if (use_pt(D.A, k)) descs_iface_left_pt(r0, r0, n, r1, R1, r1, D.Pt, X, X, D.AL[k + 1], D.T1, D.gd + 0);
+    else descs_iface_left_k(kd, r0, R0, r0, n, n, r1, R1, r1, D.AL[k], X, Ak, X, D.AL[k + 1], D.T1, D.T2, D.gd + 0);
     descs_iface_left_vec(r0, b0, n, r1, b1, D.BL[k], X, Bk, D.BL[k + 1], D.T1, D.gd + 3);
-    descs_iface_left(z0, R0, r0, n, n, z1, R1, r1, D.ZAL[k], Z, Ak, X, D.ZAL[k + 1], D.T1, D.T2, D.gd + 5);
+    descs_iface_left_k(kd, z0, R0, r0, n, n, z1, R1, r1, D.ZAL[k], Z, Ak, X, D.ZAL[k + 1], D.T1, D.T2, D.gd + 5);
     descs_iface_left_vec(z0, b0, n, z1, b1, D.ZBL[k], Z, Bk, D.ZBL[k + 1], D.T1, D.gd + 8);
   }
 }
@@ -113,10 +164,14 @@ __global__ void plan_local(Dev D, int k) {
   const int N = r0 * n * r1;
   D.iv[0] = N;
   descs_local_rhs(r0, b0, n, r1, b1, D.BL[k], Bk, D.BR[k + 1], D.rhs, D.T1, D.gd + 0);
+  const bool pt = use_pt(D.A, k);
+  if (pt) desc_pt_precompute(r0, R0, r0, n, R1, D.AL[k], D.Dc, D.Pt, D.gd + 40);
   for (int j = -1; j < D.m; ++j) {
     const double *in = (j < 0) ? D.sol : D.V + (long long)j * D.ldv;
     GemmDesc *ga = D.gapp + 3 * (j + 1);
-    descs_local_apply(r0, R0, r0, n, n, r1, R1, r1, D.AL[k], Ak, D.AR[k + 1], in, D.w, D.T1, D.T2, ga);
+    if (pt) descs_local_apply_pt(r0, r0, n, r1, R1, r1, D.Pt, D.AR[k + 1], in, D.w, D.T1, ga);
+    else descs_local_apply_k(D.A.kind[k], r0, R0, r0, n, n, r1, R1, r1, D.AL[k], Ak, D.AR[k + 1], in, D.w, D.T1,
+                             D.T2, ga);
     ga[0].skip = ga[1].skip = ga[2].skip = D.gskip;
   }
   D.cd[0] = cpy(N, 1, D.x.data + D.x.off[k], 1, N, D.sol, 1, N);
@@ -302,7 +357,8 @@ __global__ void plan_enrich(Dev D, int k, int dir) {
   GemmDesc *g = D.gd;
   // ---- crz [z0, n, z1] = zb-rhs - zAx-apply(xfull)
   descs_local_rhs(z0, b0, n, z1, b1, D.ZBL[k], Bk, D.ZBR[k + 1], D.crz, D.T1, g + 0);
-  descs_local_apply(z0, R0, r0, n, n, z1, R1, r1, D.ZAL[k], Ak, D.ZAR[k + 1], D.xfull, D.crz, D.T1, D.T2, g + 2);
+  const int kd = D.A.kind[k];
+  descs_local_apply_k(kd, z0, R0, r0, n, n, z1, R1, r1, D.ZAL[k], Ak, D.ZAR[k + 1], D.xfull, D.crz, D.T1, D.T2, g + 2);
   g[4].alpha = -1.0; g[4].beta = 1.0;
   // ---- crs: x frames on the orthonormal side, z frames on the carry side, written as extra
   //      columns of Ue (M orientation): dir > 0: [r0, n, z1] left unfolding -> Ue[:, r:r+z1]
@@ -310,10 +366,10 @@ __global__ void plan_enrich(Dev D, int k, int dir) {
   double *Uc = D.Ue + (long long)r * mm;
   if (dir > 0) {
     descs_local_rhs(r0, b0, n, z1, b1, D.BL[k], Bk, D.ZBR[k + 1], Uc, D.T1, g + 5);
-    descs_local_apply(r0, R0, r0, n, n, z1, R1, r1, D.AL[k], Ak, D.ZAR[k + 1], D.xfull, Uc, D.T1, D.T2, g + 7);
+    descs_local_apply_k(kd, r0, R0, r0, n, n, z1, R1, r1, D.AL[k], Ak, D.ZAR[k + 1], D.xfull, Uc, D.T1, D.T2, g + 7);
   } else {
     descs_local_rhs(z0, b0, n, r1, b1, D.ZBL[k], Bk, D.BR[k + 1], Uc, D.T1, g + 5);
-    descs_local_apply(z0, R0, r0, n, n, r1, R1, r1, D.ZAL[k], Ak, D.AR[k + 1], D.xfull, Uc, D.T1, D.T2, g + 7);
+    descs_local_apply_k(kd, z0, R0, r0, n, n, r1, R1, r1, D.ZAL[k], Ak, D.AR[k + 1], D.xfull, Uc, D.T1, D.T2, g + 7);
     // output element (a, c) of the final GEMMs -> Ue[c + mm a] (transposed)
     g[6].s_r0 = mm; g[6].s_c0 = 1;
     g[9].s_r0 = mm; g[9].s_c0 = 1;
@@ -388,6 +444,18 @@ static tt_status carve_amen(const MatMeta &A, const VecMeta &b, const VecMeta &x
     Scap = lmax(Scap, (long long)z.rcap[k] * n * z.rcap[k + 1]);
   }
   P.Ncap = Ncap; P.Scap = Scap; P.pc = pc; P.zcm = zcm; P.nmax = nmax;
+  // diagonal-core buffers, sized for every square core with m >= 4 (kinds are detected later)
+  long long Ptcap = 1, Dccap = 1;
+  for (int k = 0; k < d; ++k)
+    if (A.m[k] == A.n[k] && A.m[k] >= 4) {
+      Ptcap = lmax(Ptcap, (long long)A.m[k] * A.Rcap[k + 1] * x.rcap[k] * x.rcap[k]);
+      Dccap = lmax(Dccap, (long long)A.m[k] * A.Rcap[k] * A.Rcap[k + 1]);
+    }
+  D.Pt = ar.take<double>(Ptcap);
+  D.Dc = ar.take<double>(Dccap);
+  D.kscr = ar.take<float>(KIND_SCRATCH_FLOATS);
+  D.qrwsb = qr_ws_amen(x);
+  D.qrws = ar.take<char>(D.qrwsb);
   for (int k = 0; k <= d; ++k) {
     D.AL[k] = ar.take<double>((size_t)x.rcap[k] * x.rcap[k] * A.Rcap[k]);
     D.AR[k] = ar.take<double>((size_t)x.rcap[k] * x.rcap[k] * A.Rcap[k]);
@@ -470,6 +538,8 @@ tt_status amen_solve_meta(const MatMeta &A, const VecMeta &b, const VecMeta &x, 
   Dev &D = P.D;
   const int d = P.d, m = P.m;
   const int pc = P.pc, zcm = P.zcm, nmax = P.nmax;
+  TT_TRY(detect_core_kinds(D.A, D.kscr, s));
+  const MatMeta &Ah = D.A;   // host copy with the detected kinds
   // per-bond truncation limits: min(rmax, xcap - zcap) (room for the enrichment)
   set_limits_kernel<<<1, 64, 0, s>>>(x, z, o.rmax, D.limit);   // no host round trip
   set_gm_H<<<1, 1, 0, s>>>(P.gst, P.H);
@@ -487,22 +557,27 @@ tt_status amen_solve_meta(const MatMeta &A, const VecMeta &b, const VecMeta &x, 
   const int *xc = x.rcap, *zc = z.rcap, *bc = b.rcap, *Rc = A.Rcap;
   struct Caps12 { GemmDesc g[12]; int cnt; };
   auto launch_caps = [&](const GemmDesc *dev, const Caps12 &hc, int from, int cnt) -> tt_status {
-    int Mc[12], Nc[12], Kc[12];
-    for (int i = 0; i < cnt; ++i) { Mc[i] = hc.g[from + i].M; Nc[i] = hc.g[from + i].N; Kc[i] = hc.g[from + i].K; }
-    return launch_gemm_seq(dev, cnt, Mc, Nc, Kc, s);   // one cluster launch for small chains
+    int Mc[12], Nc[12], Kc[12], Bc[12];
+    for (int i = 0; i < cnt; ++i) {
+      Mc[i] = hc.g[from + i].M; Nc[i] = hc.g[from + i].N; Kc[i] = hc.g[from + i].K; Bc[i] = hc.g[from + i].batch;
+    }
+    return launch_gemm_seq(dev, cnt, Mc, Nc, Kc, s, Bc);
   };
   auto iface_caps = [&](int k, int dir) {
     Caps12 c;
     const int n = x.n[k];
+    const int kd = Ah.kind[k];
     if (dir < 0) {
-      descs_iface_right(xc[k], Rc[k], xc[k], n, n, xc[k + 1], Rc[k + 1], xc[k + 1], 0, 0, 0, 0, 0, 0, 0, c.g + 0);
+      descs_iface_right_k(kd, xc[k], Rc[k], xc[k], n, n, xc[k + 1], Rc[k + 1], xc[k + 1], 0, 0, 0, 0, 0, 0, 0, c.g + 0);
       descs_iface_right_vec(xc[k], bc[k], n, xc[k + 1], bc[k + 1], 0, 0, 0, 0, 0, c.g + 3);
-      descs_iface_right(zc[k], Rc[k], xc[k], n, n, zc[k + 1], Rc[k + 1], xc[k + 1], 0, 0, 0, 0, 0, 0, 0, c.g + 5);
+      descs_iface_right_k(kd, zc[k], Rc[k], xc[k], n, n, zc[k + 1], Rc[k + 1], xc[k + 1], 0, 0, 0, 0, 0, 0, 0, c.g + 5);
       descs_iface_right_vec(zc[k], bc[k], n, zc[k + 1], bc[k + 1], 0, 0, 0, 0, 0, c.g + 8);
     } else {
-      descs_iface_left(xc[k], Rc[k], xc[k], n, n, xc[k + 1], Rc[k + 1], xc[k + 1], 0, 0, 0, 0, 0, 0, 0, c.g + 0);
+      if (use_pt(Ah, k)) descs_iface_left_pt(xc[k], xc[k], n, xc[k + 1], Rc[k + 1], xc[k + 1], 0, 0, 0, 0, 0, c.g + 0);
+      else descs_iface_left_k(kd, xc[k], Rc[k], xc[k], n, n, xc[k + 1], Rc[k + 1], xc[k + 1], 0, 0, 0, 0, 0, 0, 0,
+                              c.g + 0);
       descs_iface_left_vec(xc[k], bc[k], n, xc[k + 1], bc[k + 1], 0, 0, 0, 0, 0, c.g + 3);
-      descs_iface_left(zc[k], Rc[k], xc[k], n, n, zc[k + 1], Rc[k + 1], xc[k + 1], 0, 0, 0, 0, 0, 0, 0, c.g + 5);
+      descs_iface_left_k(kd, zc[k], Rc[k], xc[k], n, n, zc[k + 1], Rc[k + 1], xc[k + 1], 0, 0, 0, 0, 0, 0, 0, c.g + 5);
       descs_iface_left_vec(zc[k], bc[k], n, zc[k + 1], bc[k + 1], 0, 0, 0, 0, 0, c.g + 8);
     }
     return c;
@@ -526,21 +601,11 @@ tt_status amen_solve_meta(const MatMeta &A, const VecMeta &b, const VecMeta &x, 
   gc.w = D.w;
   gc.V = D.V;
   gc.ldv = D.ldv;
-  gc.h1 = P.h1;
-  gc.h2 = P.h2;
-  gc.axpy_blocks = (int)((P.Ncap + 255) / 256 > 592 ? 592 : (P.Ncap + 255) / 256);
-  if (gc.axpy_blocks < 1) gc.axpy_blocks = 1;
-  gc.poll = 1;
-  int hflag = 0;
-  gc.host_flag = &hflag;
-  gc.apply = [&](const double *, double *, int j) -> tt_status { return launch_caps(D.gapp + 3 * (j + 1), appc, 2, 3); };
-  if (!std::getenv("TT_GMRES_UNFUSED")) {
-    gc.gapp = D.gapp;
-    gc.part = P.gpart;
-    gc.bar = P.gbar;
-    gc.split = P.split;
-    gc.split_elems = GEMM_SPLIT_SCRATCH / 8 - 4096;   // the tail holds the split-K tile counters
-  }
+  gc.gapp = D.gapp;
+  gc.part = P.gpart;
+  gc.bar = P.gbar;
+  gc.split = P.split;
+  gc.split_elems = GEMM_SPLIT_SCRATCH / 8 - 4096;
   const bool cluster_off = std::getenv("TT_GMRES_NOCLUSTER") != nullptr;
   const uint64_t hD = hash_bytes(&D, sizeof(D));   // D is fixed for the whole solve: hash it once
   int dir = +1, sweep = 0;
@@ -552,12 +617,15 @@ tt_status amen_solve_meta(const MatMeta &A, const VecMeta &b, const VecMeta &x, 
       const int k = dir > 0 ? t : d - 1 - t;
       const int last = (t == d - 1);
       const int n = x.n[k];
+      const bool pt = use_pt(Ah, k);
       descs_local_rhs(xc[k], bc[k], n, xc[k + 1], bc[k + 1], 0, 0, 0, 0, 0, appc.g + 0);
-      descs_local_apply(xc[k], Rc[k], xc[k], n, n, xc[k + 1], Rc[k + 1], xc[k + 1], 0, 0, 0, 0, 0, 0, 0, appc.g + 2);
+      if (pt) descs_local_apply_pt(xc[k], xc[k], n, xc[k + 1], Rc[k + 1], xc[k + 1], 0, 0, 0, 0, 0, appc.g + 2);
+      else descs_local_apply_k(Ah.kind[k], xc[k], Rc[k], xc[k], n, n, xc[k + 1], Rc[k + 1], xc[k + 1], 0, 0, 0, 0, 0,
+                               0, 0, appc.g + 2);
       {  // small local systems: fused Arnoldi steps inside one thread-block cluster
         int tiles = 0;
         for (int q = 2; q < 5; ++q) {
-          const int t = ((appc.g[q].M + 63) / 64) * ((appc.g[q].N + 63) / 64);
+          const int t = ((appc.g[q].M + 63) / 64) * ((appc.g[q].N + 63) / 64) * gemm_nbatch(appc.g[q]);
           tiles = t > tiles ? t : tiles;
         }
         const long long nloc = (long long)xc[k] * n * xc[k + 1];
@@ -575,8 +643,13 @@ tt_status amen_solve_meta(const MatMeta &A, const VecMeta &b, const VecMeta &x, 
         plan_local<<<1, 1, 0, s>>>(D, k);
         TT_TRY(launch_copy(D.cd, 1, P.Ncap, s));
         TT_TRY(launch_copy(D.cd + 2, 1, P.Ncap, s));
+        if (pt) {   // Pt_i = Phi_{k-1} x_2 D_i, once per local system
+          diag_extract_kernel<<<64, 256, 0, s>>>(D.A, k, D.Dc);
+          TT_TRY(launch_gemm_k(D.gd + 40, 1, xc[k], Rc[k + 1] * n, Rc[k], s, xc[k]));
+        }
         return launch_caps(D.gd, appc, 0, 2);
       }));
+      fused_profile_tag(k);
       TT_TRY(gmres_solve(gc, s));
       TT_TRY(run_captured(key ^ 0x2ull, s, [&]() -> tt_status {
       track_res_kernel<<<1, 1, 0, s>>>(P.gst, D.dv, status_dev);
@@ -585,31 +658,36 @@ tt_status amen_solve_meta(const MatMeta &A, const VecMeta &b, const VecMeta &x, 
         TT_TRY(launch_copy(D.cd + 1, 1, P.Ncap, s));
         return TT_OK;
       }
-      plan_svd<<<1, 1, 0, s>>>(D, k, dir);
-      TT_TRY(launch_qr(D.qd, 1, s));
       const int pcap = dir > 0 ? (xc[k] * n < xc[k + 1] ? xc[k] * n : xc[k + 1])
                                : (n * xc[k + 1] < xc[k] ? n * xc[k + 1] : xc[k]);
+      plan_svd<<<1, 1, 0, s>>>(D, k, dir);
+      { const QCap qc = qcap_svd(x, k, dir); TT_TRY(launch_qr_tall(D.qd, qc.m, qc.n, D.qrws, D.qrwsb, s)); }
       TT_TRY(launch_jacobi(D.sd, 1, pcap, pcap, s));
       trunc_kernel<<<1, 256, 0, s>>>(D, k, dir);
-      TT_TRY(launch_copy(D.cd, 1, P.Ncap, s));
       const int big = n * (xc[k] > xc[k + 1] ? xc[k] : xc[k + 1]);
+      TT_TRY(launch_copy(D.cd, 1, P.Ncap, s));
       TT_TRY(launch_gemm(D.gd, 1, big, pc, s));
       TT_TRY(launch_gemm(D.gd + 1, 1, big, big, s));
       plan_enrich<<<1, 1, 0, s>>>(D, k, dir);
       {
         Caps12 ec;
+        const int kd = Ah.kind[k];
         descs_local_rhs(zc[k], bc[k], n, zc[k + 1], bc[k + 1], 0, 0, 0, 0, 0, ec.g + 0);
-        descs_local_apply(zc[k], Rc[k], xc[k], n, n, zc[k + 1], Rc[k + 1], xc[k + 1], 0, 0, 0, 0, 0, 0, 0, ec.g + 2);
+        descs_local_apply_k(kd, zc[k], Rc[k], xc[k], n, n, zc[k + 1], Rc[k + 1], xc[k + 1], 0, 0, 0, 0, 0, 0, 0,
+                            ec.g + 2);
         if (dir > 0) {
           descs_local_rhs(xc[k], bc[k], n, zc[k + 1], bc[k + 1], 0, 0, 0, 0, 0, ec.g + 5);
-          descs_local_apply(xc[k], Rc[k], xc[k], n, n, zc[k + 1], Rc[k + 1], xc[k + 1], 0, 0, 0, 0, 0, 0, 0, ec.g + 7);
+          descs_local_apply_k(kd, xc[k], Rc[k], xc[k], n, n, zc[k + 1], Rc[k + 1], xc[k + 1], 0, 0, 0, 0, 0, 0, 0,
+                              ec.g + 7);
         } else {
           descs_local_rhs(zc[k], bc[k], n, xc[k + 1], bc[k + 1], 0, 0, 0, 0, 0, ec.g + 5);
-          descs_local_apply(zc[k], Rc[k], xc[k], n, n, xc[k + 1], Rc[k + 1], xc[k + 1], 0, 0, 0, 0, 0, 0, 0, ec.g + 7);
+          descs_local_apply_k(kd, zc[k], Rc[k], xc[k], n, n, xc[k + 1], Rc[k + 1], xc[k + 1], 0, 0, 0, 0, 0, 0, 0,
+                              ec.g + 7);
         }
         TT_TRY(launch_caps(D.gd, ec, 0, 10));
       }
-      TT_TRY(launch_qr(D.qd, 2, s));
+      TT_TRY(launch_qr(D.qd, 1, s));   // z core
+      { const QCap qc = qcap_enrich(x, k, dir); TT_TRY(launch_qr_tall(D.qd + 1, qc.m, qc.n, D.qrws, D.qrwsb, s)); }
       TT_TRY(launch_gemm(D.gd + 10, 1, pc, big, s));
       {
         const int nb_ = dir > 0 ? x.n[k + 1] * xc[k + 2 <= d ? k + 2 : d] : pc;
@@ -624,7 +702,10 @@ tt_status amen_solve_meta(const MatMeta &A, const VecMeta &b, const VecMeta &x, 
     TT_TRY(read_back(hv, D.dv, 3 * sizeof(double), s));
     TT_TRY(check_launch("amen sweep"));
     hres = hv[0];
-    if (hv[0] <= o.eps || hv[2] <= o.eps) { ++sweep; hres = 0.0; break; }
+    // converged when the max local residual (before the sweep's solves) is <= eps; the
+    // solution-change exit (Z20) also stops, but then reports TT_ERR_NOCONV unless the
+    // residual test holds too
+    if (hv[0] <= o.eps || hv[2] <= o.eps) { ++sweep; break; }
     dir = -dir;
   }
   (void)zcm; (void)nmax;
@@ -655,13 +736,14 @@ __global__ void plan_iface_mv(Dev D, int k, int dir) {
   const int R0 = D.A.R[k], R1 = D.A.R[k + 1], b0 = D.b.r[k], b1 = D.b.r[k + 1];
   const double *Y = D.x.data + D.x.off[k], *Z = D.z.data + D.z.off[k], *Bk = D.b.data + D.b.off[k];
   const double *Ak = D.A.data + D.A.off[k];
+  const int kd = D.A.kind[k];
   if (dir < 0) {
-    descs_iface_right(y0, R0, b0, n, nb, y1, R1, b1, D.AR[k + 1], Y, Ak, Bk, D.AR[k], D.T1, D.T2, D.gd + 0);
-    descs_iface_right(z0, R0, b0, n, nb, z1, R1, b1, D.ZAR[k + 1], Z, Ak, Bk, D.ZAR[k], D.T1, D.T2, D.gd + 3);
+    descs_iface_right_k(kd, y0, R0, b0, n, nb, y1, R1, b1, D.AR[k + 1], Y, Ak, Bk, D.AR[k], D.T1, D.T2, D.gd + 0);
+    descs_iface_right_k(kd, z0, R0, b0, n, nb, z1, R1, b1, D.ZAR[k + 1], Z, Ak, Bk, D.ZAR[k], D.T1, D.T2, D.gd + 3);
     descs_iface_right_vec(z0, y0, n, z1, y1, D.ZBR[k + 1], Z, Y, D.ZBR[k], D.T1, D.gd + 6);
   } else {
-    descs_iface_left(y0, R0, b0, n, nb, y1, R1, b1, D.AL[k], Y, Ak, Bk, D.AL[k + 1], D.T1, D.T2, D.gd + 0);
-    descs_iface_left(z0, R0, b0, n, nb, z1, R1, b1, D.ZAL[k], Z, Ak, Bk, D.ZAL[k + 1], D.T1, D.T2, D.gd + 3);
+    descs_iface_left_k(kd, y0, R0, b0, n, nb, y1, R1, b1, D.AL[k], Y, Ak, Bk, D.AL[k + 1], D.T1, D.T2, D.gd + 0);
+    descs_iface_left_k(kd, z0, R0, b0, n, nb, z1, R1, b1, D.ZAL[k], Z, Ak, Bk, D.ZAL[k + 1], D.T1, D.T2, D.gd + 3);
     descs_iface_left_vec(z0, y0, n, z1, y1, D.ZBL[k], Z, Y, D.ZBL[k + 1], D.T1, D.gd + 6);
   }
 }
@@ -674,7 +756,8 @@ __global__ void plan_local_mv(Dev D, int k) {
   const double *Bk = D.b.data + D.b.off[k], *Ak = D.A.data + D.A.off[k];
   const int N = y0 * n * y1;
   D.iv[0] = N;
-  descs_local_apply(y0, R0, b0, n, nb, y1, R1, b1, D.AL[k], Ak, D.AR[k + 1], Bk, D.sol, D.T1, D.T2, D.gd + 0);
+  descs_local_apply_k(D.A.kind[k], y0, R0, b0, n, nb, y1, R1, b1, D.AL[k], Ak, D.AR[k + 1], Bk, D.sol, D.T1, D.T2,
+                      D.gd + 0);
   D.cd[1] = cpy(N, 1, D.sol, 1, N, D.x.data + D.x.off[k], 1, N);
   D.cd[2] = cpy(N, 1, D.x.data + D.x.off[k], 1, N, D.xold, 1, N);
 }
@@ -687,18 +770,19 @@ __global__ void plan_enrich_mv(Dev D, int k, int dir) {
   const int r = D.iv[1], mm = D.iv[4], nn = D.iv[5];
   GemmDesc *g = D.gd;
   // crz [z0, n, z1] = (z|A|b) apply - (z|y) projection of the truncated y_k
-  descs_local_apply(z0, R0, b0, n, nb, z1, R1, b1, D.ZAL[k], Ak, D.ZAR[k + 1], Bk, D.crz, D.T1, D.T2, g + 0);
+  const int kd = D.A.kind[k];
+  descs_local_apply_k(kd, z0, R0, b0, n, nb, z1, R1, b1, D.ZAL[k], Ak, D.ZAR[k + 1], Bk, D.crz, D.T1, D.T2, g + 0);
   descs_local_rhs(z0, y0, n, z1, y1, D.ZBL[k], D.xfull, D.ZBR[k + 1], D.crz, D.T1, g + 3);
   g[4].alpha = -1.0; g[4].beta = 1.0;
   double *Uc = D.Ue + (long long)r * mm;
   if (dir > 0) {
     // [y0, n, z1]: (y|A|b) left, (z|A|b) right; minus y_k x_3 (z|y)_{k+1}^T
-    descs_local_apply(y0, R0, b0, n, nb, z1, R1, b1, D.AL[k], Ak, D.ZAR[k + 1], Bk, Uc, D.T1, D.T2, g + 5);
+    descs_local_apply_k(kd, y0, R0, b0, n, nb, z1, R1, b1, D.AL[k], Ak, D.ZAR[k + 1], Bk, Uc, D.T1, D.T2, g + 5);
     g[8] = gd_make(y0 * n, z1, y1, D.xfull, (long long)y0 * n, 0, D.ZBR[k + 1], z1, 1);
     gd_plain(g[8], Uc, mm);
   } else {
     // [z0, n, y1]: (z|A|b) left, (y|A|b) right; minus (z|y)_k y_k; written transposed into Ue
-    descs_local_apply(z0, R0, b0, n, nb, y1, R1, b1, D.ZAL[k], Ak, D.AR[k + 1], Bk, Uc, D.T1, D.T2, g + 5);
+    descs_local_apply_k(kd, z0, R0, b0, n, nb, y1, R1, b1, D.ZAL[k], Ak, D.AR[k + 1], Bk, Uc, D.T1, D.T2, g + 5);
     g[7].s_r0 = mm; g[7].s_c0 = 1;
     g[8] = gd_make(z0, n * y1, y0, D.ZBL[k], z0, 0, D.xfull, y0, 0);
     gd_plain(g[8], Uc, 1);
@@ -750,6 +834,9 @@ static tt_status carve_mv(const MatMeta &A, const VecMeta &b, const VecMeta &y, 
     Scap = lmax(Scap, lmax((long long)y.rcap[k] * n * y.rcap[k + 1], (long long)z.rcap[k] * n * z.rcap[k + 1]));
   }
   P.Ncap = Ncap; P.Scap = Scap; P.pc = pc;
+  D.kscr = ar.take<float>(KIND_SCRATCH_FLOATS);
+  D.qrwsb = qr_ws_amen(y);
+  D.qrws = ar.take<char>(D.qrwsb);
   for (int k = 0; k <= d; ++k) {
     D.AL[k] = ar.take<double>((size_t)y.rcap[k] * A.Rcap[k] * b.rcap[k]);
     D.AR[k] = ar.take<double>((size_t)y.rcap[k] * A.Rcap[k] * b.rcap[k]);
@@ -815,6 +902,8 @@ tt_status amen_mv_meta(const MatMeta &A, const VecMeta &b, const VecMeta &y, con
   if (!(eps > 0.0) || max_sweeps < 1 || rmax < 1) return fail(TT_ERR_ARG, "amen_mv: eps > 0, max_sweeps, rmax >= 1");
   Dev &D = P.D;
   const int d = A.d;
+  TT_TRY(detect_core_kinds(D.A, D.kscr, s));
+  const MatMeta &Ah = D.A;
   set_limits_kernel<<<1, 64, 0, s>>>(y, z, rmax, D.limit);
   set_dv_kernel<<<1, 1, 0, s>>>(D.dv, 1, eps);
   set_gemm_scratch(P.split, GEMM_SPLIT_SCRATCH);
@@ -829,21 +918,24 @@ tt_status amen_mv_meta(const MatMeta &A, const VecMeta &b, const VecMeta &y, con
   const int *yc = y.rcap, *zc = z.rcap, *bc = b.rcap, *Rc = A.Rcap;
   struct Caps12 { GemmDesc g[12]; };
   auto launch_caps = [&](const GemmDesc *dev, const Caps12 &hc, int from, int cnt) -> tt_status {
-    int Mc[12], Nc[12], Kc[12];
-    for (int i = 0; i < cnt; ++i) { Mc[i] = hc.g[from + i].M; Nc[i] = hc.g[from + i].N; Kc[i] = hc.g[from + i].K; }
-    return launch_gemm_seq(dev, cnt, Mc, Nc, Kc, s);   // one cluster launch for small chains
+    int Mc[12], Nc[12], Kc[12], Bc[12];
+    for (int i = 0; i < cnt; ++i) {
+      Mc[i] = hc.g[from + i].M; Nc[i] = hc.g[from + i].N; Kc[i] = hc.g[from + i].K; Bc[i] = hc.g[from + i].batch;
+    }
+    return launch_gemm_seq(dev, cnt, Mc, Nc, Kc, s, Bc);
   };
   auto iface = [&](int k, int dir) -> tt_status {
     plan_iface_mv<<<1, 1, 0, s>>>(D, k, dir);
     Caps12 c;
     const int n = y.n[k], nb = b.n[k];
+    const int kd = Ah.kind[k];
     if (dir < 0) {
-      descs_iface_right(yc[k], Rc[k], bc[k], n, nb, yc[k + 1], Rc[k + 1], bc[k + 1], 0, 0, 0, 0, 0, 0, 0, c.g + 0);
-      descs_iface_right(zc[k], Rc[k], bc[k], n, nb, zc[k + 1], Rc[k + 1], bc[k + 1], 0, 0, 0, 0, 0, 0, 0, c.g + 3);
+      descs_iface_right_k(kd, yc[k], Rc[k], bc[k], n, nb, yc[k + 1], Rc[k + 1], bc[k + 1], 0, 0, 0, 0, 0, 0, 0, c.g + 0);
+      descs_iface_right_k(kd, zc[k], Rc[k], bc[k], n, nb, zc[k + 1], Rc[k + 1], bc[k + 1], 0, 0, 0, 0, 0, 0, 0, c.g + 3);
       descs_iface_right_vec(zc[k], yc[k], n, zc[k + 1], yc[k + 1], 0, 0, 0, 0, 0, c.g + 6);
     } else {
-      descs_iface_left(yc[k], Rc[k], bc[k], n, nb, yc[k + 1], Rc[k + 1], bc[k + 1], 0, 0, 0, 0, 0, 0, 0, c.g + 0);
-      descs_iface_left(zc[k], Rc[k], bc[k], n, nb, zc[k + 1], Rc[k + 1], bc[k + 1], 0, 0, 0, 0, 0, 0, 0, c.g + 3);
+      descs_iface_left_k(kd, yc[k], Rc[k], bc[k], n, nb, yc[k + 1], Rc[k + 1], bc[k + 1], 0, 0, 0, 0, 0, 0, 0, c.g + 0);
+      descs_iface_left_k(kd, zc[k], Rc[k], bc[k], n, nb, zc[k + 1], Rc[k + 1], bc[k + 1], 0, 0, 0, 0, 0, 0, 0, c.g + 3);
       descs_iface_left_vec(zc[k], yc[k], n, zc[k + 1], yc[k + 1], 0, 0, 0, 0, 0, c.g + 6);
     }
     return launch_caps(D.gd, c, 0, 8);
@@ -858,7 +950,8 @@ tt_status amen_mv_meta(const MatMeta &A, const VecMeta &b, const VecMeta &y, con
       const int last = (t == d - 1);
       const int n = y.n[k], nb = b.n[k];
       Caps12 lc;
-      descs_local_apply(yc[k], Rc[k], bc[k], n, nb, yc[k + 1], Rc[k + 1], bc[k + 1], 0, 0, 0, 0, 0, 0, 0, lc.g + 0);
+      const int kd = Ah.kind[k];
+      descs_local_apply_k(kd, yc[k], Rc[k], bc[k], n, nb, yc[k + 1], Rc[k + 1], bc[k + 1], 0, 0, 0, 0, 0, 0, 0, lc.g + 0);
       plan_local_mv<<<1, 1, 0, s>>>(D, k);
       TT_TRY(launch_copy(D.cd + 2, 1, P.Ncap, s));
       TT_TRY(launch_caps(D.gd, lc, 0, 3));
@@ -867,31 +960,35 @@ tt_status amen_mv_meta(const MatMeta &A, const VecMeta &b, const VecMeta &y, con
         TT_TRY(launch_copy(D.cd + 1, 1, P.Ncap, s));
         continue;
       }
-      plan_svd<<<1, 1, 0, s>>>(D, k, dir);
-      TT_TRY(launch_qr(D.qd, 1, s));
       const int pcap = dir > 0 ? (yc[k] * n < yc[k + 1] ? yc[k] * n : yc[k + 1])
                                : (n * yc[k + 1] < yc[k] ? n * yc[k + 1] : yc[k]);
+      plan_svd<<<1, 1, 0, s>>>(D, k, dir);
+      { const QCap qc = qcap_svd(y, k, dir); TT_TRY(launch_qr_tall(D.qd, qc.m, qc.n, D.qrws, D.qrwsb, s)); }
       TT_TRY(launch_jacobi(D.sd, 1, pcap, pcap, s));
       trunc_kernel<<<1, 256, 0, s>>>(D, k, dir);
-      TT_TRY(launch_copy(D.cd, 1, P.Ncap, s));
       const int big = n * (yc[k] > yc[k + 1] ? yc[k] : yc[k + 1]);
+      TT_TRY(launch_copy(D.cd, 1, P.Ncap, s));
       TT_TRY(launch_gemm(D.gd, 1, big, P.pc, s));
       TT_TRY(launch_gemm(D.gd + 1, 1, big, big, s));
       plan_enrich_mv<<<1, 1, 0, s>>>(D, k, dir);
       {
         Caps12 ec;
-        descs_local_apply(zc[k], Rc[k], bc[k], n, nb, zc[k + 1], Rc[k + 1], bc[k + 1], 0, 0, 0, 0, 0, 0, 0, ec.g + 0);
+        descs_local_apply_k(kd, zc[k], Rc[k], bc[k], n, nb, zc[k + 1], Rc[k + 1], bc[k + 1], 0, 0, 0, 0, 0, 0, 0,
+                            ec.g + 0);
         descs_local_rhs(zc[k], yc[k], n, zc[k + 1], yc[k + 1], 0, 0, 0, 0, 0, ec.g + 3);
         if (dir > 0) {
-          descs_local_apply(yc[k], Rc[k], bc[k], n, nb, zc[k + 1], Rc[k + 1], bc[k + 1], 0, 0, 0, 0, 0, 0, 0, ec.g + 5);
+          descs_local_apply_k(kd, yc[k], Rc[k], bc[k], n, nb, zc[k + 1], Rc[k + 1], bc[k + 1], 0, 0, 0, 0, 0, 0, 0,
+                              ec.g + 5);
           ec.g[8] = gd_make(yc[k] * n, zc[k + 1], yc[k + 1], nullptr, 1, 0, nullptr, 1, 1);
         } else {
-          descs_local_apply(zc[k], Rc[k], bc[k], n, nb, yc[k + 1], Rc[k + 1], bc[k + 1], 0, 0, 0, 0, 0, 0, 0, ec.g + 5);
+          descs_local_apply_k(kd, zc[k], Rc[k], bc[k], n, nb, yc[k + 1], Rc[k + 1], bc[k + 1], 0, 0, 0, 0, 0, 0, 0,
+                              ec.g + 5);
           ec.g[8] = gd_make(zc[k], n * yc[k + 1], yc[k], nullptr, 1, 0, nullptr, 1, 0);
         }
         TT_TRY(launch_caps(D.gd, ec, 0, 9));
       }
-      TT_TRY(launch_qr(D.qd, 2, s));
+      TT_TRY(launch_qr(D.qd, 1, s));   // z core
+      { const QCap qc = qcap_enrich(y, k, dir); TT_TRY(launch_qr_tall(D.qd + 1, qc.m, qc.n, D.qrws, D.qrwsb, s)); }
       TT_TRY(launch_gemm(D.gd + 10, 1, P.pc, big, s));
       {
         const int nb_ = dir > 0 ? y.n[k + 1] * yc[k + 2 <= d ? k + 2 : d] : P.pc;

@@ -19,6 +19,8 @@ namespace tt {
 __device__ unsigned long long g_gemm_counters[2];
 // fused GMRES step kernel: [0] local-apply GEMM flops, [1] CGS2 / norm vector flops, [2] steps
 __device__ unsigned long long g_gm_counters[3];
+// per-tag (AMEn core index) Arnoldi steps of the fused kernel (tt_fused_profile_cores)
+__device__ unsigned long long g_gm_tag_steps[TT_MAX_D];
 
 namespace {
 
@@ -94,73 +96,6 @@ __device__ __forceinline__ void load_tile(double *sa, double *sb, const GemmDesc
 // splits > 1: split-K; CTA z computes the K-slice z and writes its raw partial
 // product to partial + z * pstride (column-major, ld = pld); gemm_splitk_reduce
 // sums the slices and applies the epilogue (deterministic order).
-
-// Latency-oriented 64x64 tile for short K (persistent kernels): the DMMA
-// fragments are read straight from global memory (L2) with all loads of a
-// k-block in flight, no shared-memory staging and no block barriers.
-__device__ __forceinline__ void gemm_tile_direct(const GemmDesc &g, int m0, int n0) {
-  if (m0 >= g.M || n0 >= g.N) return;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int wm = m0 + (warp % 2) * 32, wn = n0 + (warp / 2) * 32;
-  const int ar = lane >> 2, kq = lane & 3;
-  double acc[4][4][2];
-#pragma unroll
-  for (int i = 0; i < 4; ++i)
-#pragma unroll
-    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-  const double *A = g.A, *B = g.B;
-  const long long lda = g.lda, ldb = g.ldb;
-  for (int k0 = 0; k0 < g.K; k0 += 16) {
-    double af[4][4], bf[4][4];
-#pragma unroll
-    for (int kk = 0; kk < 4; ++kk) {
-      const int k = k0 + kk * 4 + kq;
-      const bool kin = k < g.K;
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const int mrow = wm + i * 8 + ar;
-        const bool p = kin && mrow < g.M;
-        af[kk][i] = p ? __ldg(g.transA ? A + k + (long long)mrow * lda : A + mrow + (long long)k * lda) : 0.0;
-        const int ncol = wn + i * 8 + ar;
-        const bool q = kin && ncol < g.N;
-        bf[kk][i] = q ? __ldg(g.transB ? B + ncol + (long long)k * ldb : B + k + (long long)ncol * ldb) : 0.0;
-      }
-    }
-#pragma unroll
-    for (int kk = 0; kk < 4; ++kk)
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) dmma(acc[i][j][0], acc[i][j][1], af[kk][i], bf[kk][j]);
-  }
-  double alpha = g.alpha;
-  if (g.alpha_dev) alpha *= *g.alpha_dev;
-  const double beta = g.beta;
-  long long coff[4][2];
-#pragma unroll
-  for (int j = 0; j < 4; ++j)
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int c = wn + j * 8 + kq * 2 + h;
-      coff[j][h] = (c < g.N) ? (long long)(c % g.dc) * g.s_c0 + (long long)(c / g.dc) * g.s_c1 : -1;
-    }
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const int r = wm + i * 8 + ar;
-    if (r >= g.M) continue;
-    const long long roff = (long long)(r % g.dr) * g.s_r0 + (long long)(r / g.dr) * g.s_r1;
-#pragma unroll
-    for (int j = 0; j < 4; ++j)
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        if (coff[j][h] < 0) continue;
-        const long long addr = roff + coff[j][h];
-        double v = alpha * acc[i][j][h];
-        if (beta != 0.0) v += beta * g.C[addr];
-        g.C[addr] = v;
-      }
-  }
-}
 
 // One output tile (m0, n0) of the K-slice z (splits > 1) or of the whole K.
 template <int BM, int BN, int BK, int WM_, int WN_, int STAGES>
@@ -270,9 +205,8 @@ __device__ __forceinline__ void gemm_tile(const GemmDesc &g0, int m0, int n0, in
   }
 }
 
-// splits > 1: the K-slice CTAs of an output tile count in tile_cnt; the last
-// one to arrive sums the slices in slice order (deterministic) and applies the
-// epilogue, then re-arms the counter (no separate reduction launch).
+// splits > 1: each K-slice CTA writes its raw partial tile; gemm_splitk_reduce
+// sums the slices in slice order (deterministic) and applies the epilogue.
 template <int BM, int BN, int BK, int WM_, int WN_, int STAGES>
 #ifndef GEMM_MINB
 #define GEMM_MINB 4   // 64x64 tiles: 128 registers, 4 CTAs per SM (C5 r=256 17.3 -> 18.2 TF/s in the same run; 5 measured slower)
@@ -280,40 +214,25 @@ template <int BM, int BN, int BK, int WM_, int WN_, int STAGES>
 __global__ void __launch_bounds__(32 * WM_ * WN_, (BM == 64 && BN == 64) ? GEMM_MINB : 1)
     gemm_dmma_kernel(const GemmDesc *__restrict__ descs, int splits,
                                                                    double *__restrict__ partial, long long pld,
-                                                                   long long pstride, unsigned int *tile_cnt) {
+                                                                   long long pstride) {
   extern __shared__ __align__(16) double smem[];
-  const GemmDesc g0 = descs[splits > 1 ? 0 : blockIdx.z];
+  // batched descriptor (count 1, no split-K): grid z = batch capacity, z = problem index
+  GemmDesc g0 = descs[0];
+  const bool batched = g0.batch >= 1;
+  if (!batched) g0 = descs[splits > 1 ? 0 : blockIdx.z];
   if (g0.skip && *g0.skip) return;
   if (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && threadIdx.x == 0 && g0.M > 0 && g0.N > 0) {
-    atomicAdd(&g_gemm_counters[0], 2ull * (unsigned long long)g0.M * g0.N * (g0.K > 0 ? g0.K : 0));
+    atomicAdd(&g_gemm_counters[0], 2ull * (unsigned long long)g0.M * g0.N * (g0.K > 0 ? g0.K : 0) * gemm_nbatch(g0));
     atomicAdd(&g_gemm_counters[1], 1ull);
   }
-  const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN;
-  gemm_tile<BM, BN, BK, WM_, WN_, STAGES>(g0, m0, n0, blockIdx.z, splits, partial, pld, pstride, smem);
-  if (splits > 1 && tile_cnt) {
-    __shared__ int s_last;
-    __threadfence();
-    __syncthreads();
-    const int tile = blockIdx.x + gridDim.x * blockIdx.y;
-    if (threadIdx.x == 0) s_last = (atomicAdd(&tile_cnt[tile], 1u) == (unsigned int)(splits - 1));
-    __syncthreads();
-    if (!s_last) return;
-    __threadfence();
-    double alpha = g0.alpha;
-    if (g0.alpha_dev) alpha *= *g0.alpha_dev;
-    for (int e = threadIdx.x; e < BM * BN; e += blockDim.x) {
-      const int r = m0 + e % BM, c = n0 + e / BM;
-      if (r >= g0.M || c >= g0.N) continue;
-      double sum = 0.0;
-      for (int z = 0; z < splits; ++z) sum += __ldcg(partial + z * pstride + r + c * pld);
-      const long long addr = (long long)(r % g0.dr) * g0.s_r0 + (long long)(r / g0.dr) * g0.s_r1 +
-                             (long long)(c % g0.dc) * g0.s_c0 + (long long)(c / g0.dc) * g0.s_c1;
-      double v = alpha * sum;
-      if (g0.beta != 0.0) v += g0.beta * g0.C[addr];
-      g0.C[addr] = v;
-    }
-    if (threadIdx.x == 0) tile_cnt[tile] = 0;
+  int z = blockIdx.z;
+  if (batched) {
+    if ((int)blockIdx.z >= g0.batch) return;
+    g0 = gemm_batch_item(g0, blockIdx.z);
+    z = 0;
   }
+  const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN;
+  gemm_tile<BM, BN, BK, WM_, WN_, STAGES>(g0, m0, n0, z, splits, partial, pld, pstride, smem);
 }
 
 __global__ void gemm_splitk_reduce(const GemmDesc *__restrict__ descs, int splits, const double *__restrict__ partial,
@@ -339,8 +258,6 @@ __global__ void gemm_splitk_reduce(const GemmDesc *__restrict__ descs, int split
 struct SplitScratch {
   double *ptr = nullptr;
   size_t bytes = 0;
-  unsigned int *cnt = nullptr;
-  bool cnt_zeroed = false;
 };
 thread_local SplitScratch g_split;
 
@@ -357,46 +274,16 @@ struct Variant {
       done = true;
     }
   }
-  static void launch(dim3 grid, const GemmDesc *d, int splits, double *p, long long pld, long long ps, cudaStream_t s,
-                     unsigned int *cnt = nullptr) {
+  static void launch(dim3 grid, const GemmDesc *d, int splits, double *p, long long pld, long long ps, cudaStream_t s) {
     prepare();
-    gemm_dmma_kernel<BM, BN, BK, WM_, WN_, ST><<<grid, C::THREADS, C::SMEM, s>>>(d, splits, p, pld, ps, cnt);
+    gemm_dmma_kernel<BM, BN, BK, WM_, WN_, ST><<<grid, C::THREADS, C::SMEM, s>>>(d, splits, p, pld, ps);
   }
 };
 
-using V64 = Variant<64, 64, 16, 2, 2, 2>;     // round-1 baseline
-using V64K = Variant<64, 64, 32, 2, 2, 3>;    // deeper K, 3 stages
-using V128 = Variant<128, 64, 16, 4, 2, 3>;   // 8 warps
-using V128S = Variant<128, 128, 16, 4, 2, 2>; // 8 warps, 32x64 warp tiles
+// (64x64x32 3-stage, 128x64, 128x128 and 3/4-stage 64x64 variants were measured
+// slower on the B200 in round 1 and removed)
+using V64 = Variant<64, 64, 16, 2, 2, 2>;
 using V32 = Variant<32, 32, 16, 2, 2, 2>;     // small tiles for GEMMs that fill less than a wave
-using V64S3 = Variant<64, 64, 16, 2, 2, 3>;   // 3-stage pipeline
-using V64S4 = Variant<64, 64, 16, 2, 2, 4>;   // 4-stage pipeline
-
-int variant_id() {
-  static int v = -1;
-  if (v < 0) {
-    const char *e = std::getenv("TT_GEMM_VARIANT");
-    v = e ? std::atoi(e) : 0;
-  }
-  return v;
-}
-
-// tile arrival counters of the in-kernel split-K reduction: the last 16 KB of
-// the caller's split scratch (set_gemm_scratch), zeroed on the stream before
-// the first use after every set_gemm_scratch; each reducing CTA re-arms its own
-constexpr size_t CNT_BYTES = 4096 * sizeof(unsigned int);
-unsigned int *tile_counters(cudaStream_t s) {
-  // measured slower than the separate reduction kernel (the last CTA of a tile
-  // reduces alone at the tail: C5 r=128 9.8 -> 7.0 TF/s), so opt-in only
-  static int off = -1;
-  if (off < 0) off = std::getenv("TT_GEMM_SPLIT_INKERNEL") ? 0 : 1;
-  if (off || !g_split.cnt) return nullptr;
-  if (!g_split.cnt_zeroed) {
-    cudaMemsetAsync(g_split.cnt, 0, CNT_BYTES, s);
-    g_split.cnt_zeroed = true;
-  }
-  return g_split.cnt;
-}
 
 int small_tiles_enabled() {
   static int v = -1;
@@ -415,14 +302,23 @@ int small_tiles_kmax() {
 }
 
 template <class Vt>
-tt_status launch_variant(const GemmDesc *descs_dev, int count, int Mcap, int Ncap, int Kcap, cudaStream_t s) {
+tt_status launch_variant(const GemmDesc *descs_dev, int count, int Mcap, int Ncap, int Kcap, cudaStream_t s,
+                         int batch) {
   const int tm = (Mcap + Vt::bm - 1) / Vt::bm, tn = (Ncap + Vt::bn - 1) / Vt::bn;
-  // less than one wave of 64x64 tiles and a short K (no split-K): 32x32 tiles (4x the CTAs)
-  if (Vt::bm == 64 && Vt::bn == 64 && small_tiles_enabled() && (long long)tm * tn * count < small_tiles_waves() &&
-      Kcap < small_tiles_kmax()) {
+  const int nb = batch >= 1 ? batch : 1;
+  const int zdim = batch >= 1 ? batch : count;
+  // less than one wave of 64x64 tiles and a short K (no split-K), or a thin batched
+  // problem: 32x32 tiles (4x the CTAs, less padding)
+  if (Vt::bm == 64 && Vt::bn == 64 && small_tiles_enabled() &&
+      (((long long)tm * tn * count * nb < small_tiles_waves() && Kcap < small_tiles_kmax()) ||
+       (batch >= 1 && (Mcap <= 32 || Ncap <= 32)))) {
     const int sm_ = (Mcap + 31) / 32, sn_ = (Ncap + 31) / 32;
-    V32::launch(dim3(sm_, sn_, count), descs_dev, 1, nullptr, 0, 0, s);
+    V32::launch(dim3(sm_, sn_, zdim), descs_dev, 1, nullptr, 0, 0, s);
     return check_launch("gemm_dmma small tiles");
+  }
+  if (batch >= 1) {
+    Vt::launch(dim3(tm, tn, zdim), descs_dev, 1, nullptr, 0, 0, s);
+    return check_launch("gemm_dmma batched");
   }
   static int tgt = -1, kmin = -1;
   if (tgt < 0) {
@@ -440,13 +336,10 @@ tt_status launch_variant(const GemmDesc *descs_dev, int count, int Mcap, int Nca
   }
   if (splits > 1) {
     const long long pld = Mcap, pstride = (long long)Mcap * Ncap;
-    unsigned int *cnt = tile_counters(s);
-    Vt::launch(dim3(tm, tn, splits), descs_dev, splits, g_split.ptr, pld, pstride, s, cnt);
-    if (!cnt) {
-      int rb = (int)((pstride + 255) / 256);
-      rb = rb > 1184 ? 1184 : (rb < 1 ? 1 : rb);
-      gemm_splitk_reduce<<<rb, 256, 0, s>>>(descs_dev, splits, g_split.ptr, pld, pstride);
-    }
+    Vt::launch(dim3(tm, tn, splits), descs_dev, splits, g_split.ptr, pld, pstride, s);
+    int rb = (int)((pstride + 255) / 256);
+    rb = rb > 1184 ? 1184 : (rb < 1 ? 1 : rb);
+    gemm_splitk_reduce<<<rb, 256, 0, s>>>(descs_dev, splits, g_split.ptr, pld, pstride);
     return check_launch("gemm_dmma splitk");
   }
   Vt::launch(dim3(tm, tn, count), descs_dev, 1, nullptr, 0, 0, s);
@@ -517,6 +410,7 @@ struct GmChunkArgs {
   int max_restarts;
   const double *b;       // full: right-hand side
   double *x;             // full: initial guess in, solution out
+  int tag;               // profiling tag (AMEn core index, < TT_MAX_D)
 };
 
 // Phase barrier: whole cooperative grid (atomics in global memory) or one
@@ -532,8 +426,6 @@ __device__ __forceinline__ void phase_sync(unsigned int *bar, unsigned int nbloc
   }
 }
 
-__constant__ int c_gm_direct_kmax = 0;       // K bound of the direct (unstaged) tile
-__device__ __forceinline__ int gm_direct_kmax() { return c_gm_direct_kmax; }
 
 // One GEMM as a phase of a persistent kernel: DMMA tiles distributed over the
 // CTAs (split-K with an in-kernel reduction when the GEMM has few tiles), then a
@@ -544,6 +436,27 @@ __device__ void gemm_stage(const GemmDesc &g, double *split, long long split_ele
   if (g.M <= 0 || g.N <= 0) return;
   if (check_skip && g.skip && *g.skip) return;
   const int tid = threadIdx.x;
+  const int nb = gemm_nbatch(g);
+  if (g.batch >= 1) {   // batched: tiles of every problem distributed over the CTAs, no split-K
+    if (blockIdx.x == 0 && tid == 0) {
+      const unsigned long long f = 2ull * (unsigned long long)g.M * g.N * (g.K > 0 ? g.K : 0) * nb;
+      atomicAdd(&g_gemm_counters[0], f);
+      atomicAdd(&g_gemm_counters[1], 1ull);
+      if (gm_count) atomicAdd(&g_gm_counters[0], f);
+    }
+    const bool sm32 = g.M <= 32 || g.N <= 32;
+    const int bm = sm32 ? 32 : 64;
+    const int tm = (g.M + bm - 1) / bm, tn = (g.N + bm - 1) / bm, T = tm * tn;
+    for (int t = blockIdx.x; t < T * nb; t += G) {
+      const int b = t / T, tt = t - b * T;
+      const GemmDesc h = gemm_batch_item(g, b);
+      if (sm32) gemm_tile<32, 32, 16, 2, 2, 2>(h, (tt % tm) * 32, (tt / tm) * 32, 0, 1, nullptr, 0, 0, smem);
+      else gemm_tile<64, 64, GF_BK, 2, 2, 2>(h, (tt % tm) * 64, (tt / tm) * 64, 0, 1, nullptr, 0, 0, smem);
+      __syncthreads();
+    }
+    phase_sync<CLUSTER>(bar, G);
+    return;
+  }
   const int tm = (g.M + 63) / 64, tn = (g.N + 63) / 64, T = tm * tn;
   int splits = 1;
   if (T * 2 <= G && g.K >= 256) {
@@ -556,10 +469,9 @@ __device__ void gemm_stage(const GemmDesc &g, double *split, long long split_ele
     atomicAdd(&g_gemm_counters[1], 1ull);
     if (gm_count) atomicAdd(&g_gm_counters[0], f);
   }
-  const bool direct = splits == 1 && g.K <= gm_direct_kmax();
   // small GEMMs (fewer 64x64 tiles than CTAs, or a thin M): 32x32 tiles waste
   // less of the DMMA work on padding and spread over more CTAs
-  const bool small = splits == 1 && !direct && (T < G || g.M <= 32);
+  const bool small = splits == 1 && (T < G || g.M <= 32);
   if (small) {
     const int sm_ = (g.M + 31) / 32, sn_ = (g.N + 31) / 32;
     for (int t = blockIdx.x; t < sm_ * sn_; t += G) {
@@ -569,13 +481,9 @@ __device__ void gemm_stage(const GemmDesc &g, double *split, long long split_ele
   } else {
     for (int t = blockIdx.x; t < T * splits; t += G) {
       const int z = t / T, tt = t - z * T;
-      if (direct) {
-        gemm_tile_direct(g, (tt % tm) * 64, (tt / tm) * 64);
-      } else {
-        gemm_tile<64, 64, GF_BK, 2, 2, 2>(g, (tt % tm) * 64, (tt / tm) * 64, z, splits, split, g.M,
-                                          (long long)g.M * g.N, smem);
-        __syncthreads();
-      }
+      gemm_tile<64, 64, GF_BK, 2, 2, 2>(g, (tt % tm) * 64, (tt / tm) * 64, z, splits, split, g.M,
+                                        (long long)g.M * g.N, smem);
+      __syncthreads();
     }
   }
   phase_sync<CLUSTER>(bar, G);
@@ -594,17 +502,6 @@ __device__ void gemm_stage(const GemmDesc &g, double *split, long long split_ele
       g.C[addr] = v;
     }
     phase_sync<CLUSTER>(bar, G);
-  }
-}
-
-// A dependent chain of GEMMs (each consumes earlier outputs) in one launch of a
-// thread-block cluster: one phase per GEMM instead of one kernel launch each.
-__global__ void __launch_bounds__(GF_THREADS) gemm_seq_kernel(const GemmDesc *__restrict__ descs, int count,
-                                                              double *split, long long split_elems) {
-  extern __shared__ __align__(16) double smem[];
-  for (int i = 0; i < count; ++i) {
-    const GemmDesc g = descs[i];
-    gemm_stage<true>(g, split, split_elems, nullptr, gridDim.x, smem, false);
   }
 }
 
@@ -676,7 +573,7 @@ __global__ void __launch_bounds__(GF_THREADS) gm_chunk_kernel(GmChunkArgs a) {
     int tiles = 0;
     for (int q = 0; q < 3; ++q) {
       const GemmDesc &g = a.gapp[3 * (a.j0 + 1) + q];
-      const int t = ((g.M + 63) / 64) * ((g.N + 63) / 64);
+      const int t = ((g.M + 63) / 64) * ((g.N + 63) / 64) * gemm_nbatch(g);
       tiles = t > tiles ? t : tiles;
     }
     const bool small = tiles <= 2 * a.cs && N <= 16384;
@@ -879,6 +776,7 @@ __global__ void __launch_bounds__(GF_THREADS) gm_chunk_kernel(GmChunkArgs a) {
     if (blockIdx.x == 0 && tid == 0) {
       atomicAdd(&g_gm_counters[1], (unsigned long long)N * ((reorth ? 8ull : 4ull) * (j + 1) + 5ull));
       atomicAdd(&g_gm_counters[2], 1ull);
+      atomicAdd(&g_gm_tag_steps[a.tag], 1ull);
     }
     if (red[1] > 0.0) {
       const double inv = 1.0 / red[1];
@@ -927,28 +825,16 @@ __global__ void __launch_bounds__(GF_THREADS) gm_chunk_kernel(GmChunkArgs a) {
 void set_gemm_scratch(double *ptr, size_t bytes) {
   g_split.ptr = ptr;
   g_split.bytes = ptr ? bytes : 0;
-  g_split.cnt = nullptr;
-  g_split.cnt_zeroed = false;
-  if (ptr && bytes > 2 * CNT_BYTES) {
-    g_split.bytes = bytes - CNT_BYTES;
-    g_split.cnt = reinterpret_cast<unsigned int *>(reinterpret_cast<char *>(ptr) + g_split.bytes);
-  }
 }
 
 tt_status launch_gemm(const GemmDesc *descs_dev, int count, int Mcap, int Ncap, cudaStream_t s) {
   return launch_gemm_k(descs_dev, count, Mcap, Ncap, 0, s);
 }
 
-tt_status launch_gemm_k(const GemmDesc *descs_dev, int count, int Mcap, int Ncap, int Kcap, cudaStream_t s) {
-  if (count <= 0 || Mcap <= 0 || Ncap <= 0) return TT_OK;
-  switch (variant_id()) {
-    case 0: return launch_variant<V64>(descs_dev, count, Mcap, Ncap, Kcap, s);
-    case 2: return launch_variant<V128>(descs_dev, count, Mcap, Ncap, Kcap, s);
-    case 3: return launch_variant<V128S>(descs_dev, count, Mcap, Ncap, Kcap, s);
-    case 4: return launch_variant<V64S3>(descs_dev, count, Mcap, Ncap, Kcap, s);
-    case 5: return launch_variant<V64S4>(descs_dev, count, Mcap, Ncap, Kcap, s);
-    default: return launch_variant<V64K>(descs_dev, count, Mcap, Ncap, Kcap, s);
-  }
+tt_status launch_gemm_k(const GemmDesc *descs_dev, int count, int Mcap, int Ncap, int Kcap, cudaStream_t s,
+                        int batch) {
+  if (count <= 0 || Mcap <= 0 || Ncap <= 0 || batch < 0) return TT_OK;
+  return launch_variant<V64>(descs_dev, count, Mcap, Ncap, Kcap, s, batch);
 }
 
 void gemm_counters(unsigned long long *out, int reset) {
@@ -975,10 +861,6 @@ int gmres_fused_grid() {
     cudaFuncSetAttribute(gm_chunk_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GM_SMEM);
     cudaFuncSetAttribute(gm_chunk_kernel<true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, gm_chunk_kernel<false>, GF_THREADS, GM_SMEM);
-    if (const char *dk = std::getenv("TT_GM_DIRECT_K")) {
-      const int v = std::atoi(dk);
-      cudaMemcpyToSymbol(c_gm_direct_kmax, &v, sizeof(int));
-    }
     const char *e = std::getenv("TT_GF_GRID");
     // two CTAs per SM when they fit (more bytes in flight for the CGS2 phases of
     // large local systems; measured +4% on C4)
@@ -992,13 +874,31 @@ int gmres_fused_grid() {
 struct FusedProfile {
   bool on = false;
   std::vector<cudaEvent_t> ev;   // pairs
+  std::vector<int> tags;         // tag of each pair
   size_t used = 0;
+  int tag = 0;
 };
 thread_local FusedProfile g_fp;
 
 void fused_profile(int enable) {
   g_fp.on = enable != 0;
   g_fp.used = 0;
+}
+void fused_profile_tag(int tag) { g_fp.tag = tag < 0 ? 0 : (tag >= TT_MAX_D ? TT_MAX_D - 1 : tag); }
+
+// per-tag sums of the recorded launches (does not reset; fused_profile_read does)
+void fused_profile_cores(double *ms, double *steps, long long *launches) {
+  for (int t = 0; t < TT_MAX_D; ++t) { ms[t] = 0.0; launches[t] = 0; }
+  for (size_t i = 0; i + 1 < g_fp.used; i += 2) {
+    cudaEventSynchronize(g_fp.ev[i + 1]);
+    float e = 0.f;
+    cudaEventElapsedTime(&e, g_fp.ev[i], g_fp.ev[i + 1]);
+    ms[g_fp.tags[i / 2]] += e;
+    launches[g_fp.tags[i / 2]] += 1;
+  }
+  unsigned long long c[TT_MAX_D];
+  cudaMemcpyFromSymbol(c, g_gm_tag_steps, sizeof(c));
+  for (int t = 0; t < TT_MAX_D; ++t) steps[t] = (double)c[t];
 }
 
 void fused_profile_read(long long *launches, double *ms, double *flops) {
@@ -1013,6 +913,8 @@ void fused_profile_read(long long *launches, double *ms, double *flops) {
   cudaMemcpyFromSymbol(c, g_gm_counters, sizeof(c));
   const unsigned long long z[3] = {0, 0, 0};
   cudaMemcpyToSymbol(g_gm_counters, z, sizeof(z));
+  const unsigned long long zt[TT_MAX_D] = {};
+  cudaMemcpyToSymbol(g_gm_tag_steps, zt, sizeof(zt));
   if (launches) *launches = (long long)(g_fp.used / 2);
   if (ms) *ms = t;
   if (flops) { flops[0] = (double)c[0]; flops[1] = (double)c[1]; flops[2] = (double)c[2]; }
@@ -1022,44 +924,10 @@ void fused_profile_read(long long *launches, double *ms, double *flops) {
 // Dependent GEMM chain: one cluster launch when every GEMM is small at its
 // capacity shape (<= 2 tiles per CTA of the cluster), else one launch per GEMM.
 tt_status launch_gemm_seq(const GemmDesc *descs_dev, int count, const int *Mcap, const int *Ncap, const int *Kcap,
-                          cudaStream_t s) {
+                          cudaStream_t s, const int *Bcap) {
   if (count <= 0) return TT_OK;
-  // measured slower than per-GEMM launches on the full GPU for the C1/C3 chains
-  // (profiles/r01), so opt-in only: TT_GEMM_SEQ=1
-  static int off = -1;
-  if (off < 0) off = std::getenv("TT_GEMM_SEQ") ? 0 : 1;
-  const int cs = gmres_cluster_size();
-  bool small = count >= 2 && !off && gmres_fused_grid() > 0;
-  for (int i = 0; i < count && small; ++i) {
-    const long long t = (long long)((Mcap[i] + 63) / 64) * ((Ncap[i] + 63) / 64);
-    small = t <= 2 * cs;
-  }
-  if (!small) {
-    for (int i = 0; i < count; ++i) TT_TRY(launch_gemm_k(descs_dev + i, 1, Mcap[i], Ncap[i], Kcap[i], s));
-    return TT_OK;
-  }
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(gemm_seq_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GF::SMEM);
-    cudaFuncSetAttribute(gemm_seq_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    attr = true;
-  }
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(cs);
-  cfg.blockDim = dim3(GF_THREADS);
-  cfg.dynamicSmemBytes = GF::SMEM;
-  cfg.stream = s;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeClusterDimension;
-  at[0].val.clusterDim.x = cs;
-  at[0].val.clusterDim.y = 1;
-  at[0].val.clusterDim.z = 1;
-  cfg.attrs = at;
-  cfg.numAttrs = 1;
-  double *sp = g_split.ptr;
-  const long long se = (long long)(g_split.bytes / sizeof(double));
-  cudaError_t e = cudaLaunchKernelEx(&cfg, gemm_seq_kernel, descs_dev, count, sp, se);
-  if (e != cudaSuccess) return fail(TT_ERR_CUDA, std::string("gemm_seq: ") + cudaGetErrorString(e));
+  for (int i = 0; i < count; ++i)
+    TT_TRY(launch_gemm_k(descs_dev + i, 1, Mcap[i], Ncap[i], Kcap[i], s, Bcap ? Bcap[i] : 0));
   return TT_OK;
 }
 
@@ -1088,6 +956,7 @@ tt_status launch_gmres_chunk(GmState *st, const GemmDesc *gapp, double *V, long 
   a.x = x;
   a.st = st; a.gapp = gapp; a.V = V; a.ldv = ldv; a.w = w; a.part = part; a.split = split;
   a.split_elems = split_elems; a.bar = bar; a.j0 = j0; a.j1 = j1;
+  a.tag = g_fp.tag;
   void *args[] = {(void *)&a};
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (g_fp.on) {
@@ -1098,6 +967,8 @@ tt_status launch_gmres_chunk(GmState *st, const GemmDesc *gapp, double *V, long 
     }
     e0 = g_fp.ev[g_fp.used];
     e1 = g_fp.ev[g_fp.used + 1];
+    if (g_fp.tags.size() < g_fp.used / 2 + 1) g_fp.tags.resize(g_fp.used / 2 + 1);
+    g_fp.tags[g_fp.used / 2] = g_fp.tag;
     g_fp.used += 2;
     cudaEventRecord(e0, s);
   }

@@ -1,7 +1,5 @@
 // Device GMRES state and host driver context (see gmres.cu).
 #pragma once
-#include <functional>
-
 #include "tt_common.cuh"
 
 namespace tt {
@@ -27,12 +25,6 @@ struct GmresCtx {
   double *w;             // scratch vector
   double *V;             // basis, (m+1) vectors of stride ldv
   long long ldv;
-  double *h1, *h2;       // scratch [m+1]
-  int axpy_blocks;
-  int poll;              // 1: read the convergence flag back once per cycle
-  int *host_flag;        // pinned host int for polling
-  // enqueue out = A in; j = basis index (-1 for x)
-  std::function<tt_status(const double *, double *, int)> apply;
   // fused Arnoldi steps (gemm.cu gm_chunk_kernel): the apply GEMM descriptors of
   // basis vector j are gapp[3(j+1) .. 3(j+1)+2]; NULL = one launch per operation
   const GemmDesc *gapp = nullptr;
@@ -53,5 +45,6 @@ tt_status launch_gmres_chunk(GmState *st, const GemmDesc *gapp, double *V, long 
                              int cluster, int decide, int full = 0, int max_restarts = 1, const double *b = nullptr,
                              double *x = nullptr);
 int gmres_cluster_size();
+void fused_profile_tag(int tag);   // profiling tag of later fused launches (AMEn core index)
 
 }  // namespace tt

@@ -12,7 +12,7 @@ namespace tt {
 namespace {
 
 struct KeffScal {
-  double k, kinv, s_old, s_new, nrm, nrm_inv, one;
+  double k, kinv, s_old, s_new, nrm, nrm_inv, one, minus_one, dk, res, rnorm, hnorm;
   int flag, iters, status;
 };
 
@@ -47,11 +47,19 @@ __global__ void keff_init_kernel(KeffScal *sc, double k0, const double *k0_dev, 
   sc->k = k0;
   sc->kinv = 1.0 / k0;
   sc->one = 1.0;
+  sc->minus_one = -1.0;
+  sc->dk = 0.0;
+  sc->res = -1.0;
   sc->flag = 0;
   sc->iters = 0;
   sc->status = 0;
   sc->nrm = *nrm;
   sc->nrm_inv = (*nrm > 0.0) ? 1.0 / *nrm : 1.0;
+}
+
+__global__ void set_i32_k(int *p, int v) { *p = v; }
+__global__ void fill_kernel(double *p, int n, double v) {
+  for (int i = threadIdx.x; i < n; i += blockDim.x) p[i] = v;
 }
 
 __global__ void keff_after_solve_kernel(KeffScal *sc) {
@@ -64,33 +72,47 @@ __global__ void keff_after_solve_kernel(KeffScal *sc) {
   sc->nrm_inv = 0.0;  // set after the norm
 }
 
-__global__ void keff_update_kernel(KeffScal *sc, const double *nrm, double tol, double *khist, int *shist,
-                                   const int *sweeps, int hist_cap, int max_outer, double *k_out, int *iters_out,
-                                   int *status_out) {
-  if (sc->status == TT_ERR_NOFISSION) {
+// k' = k <f, Psi'> / <f, Psi> and the history; the convergence decision is
+// keff_decide_kernel's (after the optional residual evaluation)
+__global__ void keff_update_kernel(KeffScal *sc, const double *nrm, double *khist, int *shist, int *ihist,
+                                   const int *sweeps, const int *inner, int hist_cap) {
+  if (sc->status == TT_ERR_NOFISSION) return;
+  const double knew = sc->k * sc->s_new / sc->s_old;
+  const double nn = *nrm;
+  sc->nrm = nn;
+  sc->nrm_inv = nn > 0.0 ? 1.0 / nn : 1.0;
+  sc->s_old = sc->s_new * sc->nrm_inv;
+  const int it = sc->iters;
+  if (khist && it < hist_cap) khist[it] = knew;
+  if (shist && it < hist_cap) shist[it] = sweeps ? *sweeps : 0;
+  if (ihist && it < hist_cap) ihist[it] = inner ? *inner : 0;
+  sc->iters = it + 1;
+  sc->dk = fabs(knew - sc->k);
+  sc->k = knew;
+  sc->kinv = 1.0 / knew;
+  sc->res = -1.0;
+  if (!(knew == knew)) sc->status = TT_ERR_NUMERIC;
+}
+
+// res = ||M Psi|| / ||H Psi|| of the iteration just finished (history slot it)
+__global__ void keff_res_kernel(KeffScal *sc, double *rhist, int hist_cap, double *res_out) {
+  const double r = sc->hnorm > 0.0 ? sc->rnorm / sc->hnorm : (sc->rnorm > 0.0 ? INFINITY : 0.0);
+  sc->res = r;
+  const int it = sc->iters - 1;
+  if (rhist && it >= 0 && it < hist_cap) rhist[it] = r;
+  if (res_out) *res_out = r;
+}
+
+__global__ void keff_decide_kernel(KeffScal *sc, double tol_k, double tol_res, int max_outer, double *k_out,
+                                   int *iters_out, int *status_out) {
+  if (sc->status == TT_ERR_NOFISSION || sc->status == TT_ERR_NUMERIC) {
     sc->flag = 1;
-  } else {
-    const double knew = sc->k * sc->s_new / sc->s_old;
-    const double nn = *nrm;
-    sc->nrm = nn;
-    sc->nrm_inv = nn > 0.0 ? 1.0 / nn : 1.0;
-    sc->s_old = sc->s_new * sc->nrm_inv;
-    const int it = sc->iters;
-    if (khist && it < hist_cap) khist[it] = knew;
-    if (shist && it < hist_cap) shist[it] = sweeps ? *sweeps : 0;
-    sc->iters = it + 1;
-    const double dk = fabs(knew - sc->k);
-    sc->k = knew;
-    sc->kinv = 1.0 / knew;
-    if (!(knew == knew)) {
-      sc->status = TT_ERR_NUMERIC;
-      sc->flag = 1;
-    } else if (dk <= tol) {
-      sc->flag = 1;
-    } else if (sc->iters >= max_outer) {
-      sc->status = TT_ERR_NOCONV;
-      sc->flag = 1;
-    }
+  } else if (sc->dk <= tol_k && (tol_res <= 0.0 || (sc->res >= 0.0 && sc->res <= tol_res))) {
+    sc->status = TT_OK;
+    sc->flag = 1;
+  } else if (sc->iters >= max_outer) {
+    sc->status = TT_ERR_NOCONV;
+    sc->flag = 1;
   }
   if (k_out) *k_out = sc->k;
   if (iters_out) *iters_out = sc->iters;
@@ -98,11 +120,11 @@ __global__ void keff_update_kernel(KeffScal *sc, const double *nrm, double tol, 
 }
 
 struct KeffWS {
-  MatMeta FT, SF;
-  VecMeta ones, f, SP, FP, B, z0, zmv;
+  MatMeta FT, SF, M;
+  VecMeta ones, f, SP, FP, B, z0, zmv, Rv, Hv, zr;
   KeffScal *sc;
   double *nrm, *dbuf;
-  int *sweeps;
+  int *sweeps, *inner;
   char *sub;       // scratch for round / dot / orth / amen
   size_t sub_cap;
 };
@@ -146,6 +168,40 @@ tt_status carve_keff(const MatMeta &H, const MatMeta &S, const MatMeta &F, const
   W.f = vec_like(ar, d, F.n, cap);
   const bool mv = o.matvec == 1;
   if (o.matvec != 0 && o.matvec != 1) return fail(TT_ERR_ARG, "keff: matvec must be 0 (exact) or 1 (amen_mv)");
+  if (o.local_dense_max != 0)
+    return fail(TT_ERR_NOT_IMPLEMENTED, "keff: local_dense_max must be 0 (local systems are solved by GMRES)");
+  if (o.kickrank != 0) {
+    int zc = 0;
+    for (int k = 1; k < d; ++k) zc = z.rcap[k] > zc ? z.rcap[k] : zc;
+    if (d > 1 && o.kickrank != zc) return fail(TT_ERR_ARG, "keff: kickrank must equal z's interior rank capacity");
+  }
+  // S + k^{-1} F as one TT-matrix (ranks add): the amen_mv operator of B and part of the residual
+  W.SF = S;
+  {
+    long long off = 0;
+    for (int k = 0; k <= d; ++k) W.SF.Rcap[k] = (k == 0 || k == d) ? 1 : S.Rcap[k] + F.Rcap[k];
+    for (int k = 0; k < d; ++k) {
+      W.SF.off[k] = off;
+      off += (long long)W.SF.Rcap[k] * S.m[k] * S.n[k] * W.SF.Rcap[k + 1];
+    }
+    W.SF.data = ar.take<double>(off);
+    W.SF.R = ar.take<int>(d + 1);
+  }
+  const bool res_on = o.tol_res >= 0.0;
+  if (res_on) {   // residual operator M = H - (S + k^{-1} F)
+    W.M = H;
+    long long off = 0;
+    for (int k = 0; k <= d; ++k) W.M.Rcap[k] = (k == 0 || k == d) ? 1 : H.Rcap[k] + W.SF.Rcap[k];
+    for (int k = 0; k < d; ++k) {
+      W.M.off[k] = off;
+      off += (long long)W.M.Rcap[k] * H.m[k] * H.n[k] * W.M.Rcap[k + 1];
+    }
+    W.M.data = ar.take<double>(off);
+    W.M.R = ar.take<int>(d + 1);
+    W.Rv = vec_like(ar, d, psi.n, psi.rcap);
+    W.Hv = vec_like(ar, d, psi.n, psi.rcap);
+    W.zr = vec_like(ar, d, z.n, z.rcap);
+  }
   if (!mv) {
     for (int k = 0; k <= d; ++k) cap[k] = S.Rcap[k] * psi.rcap[k];
     W.SP = vec_like(ar, d, S.m, cap);
@@ -155,16 +211,7 @@ tt_status carve_keff(const MatMeta &H, const MatMeta &S, const MatMeta &F, const
     for (int k = 0; k <= d; ++k) cap[k] = (k == 0 || k == d) ? 1 : S.Rcap[k] * psi.rcap[k] + F.Rcap[k] * psi.rcap[k];
     W.B = vec_like(ar, d, psi.n, cap);
   } else {
-    // S + k^{-1} F as one TT-matrix (ranks add), B fitted by amen_mv in psi's capacities
-    W.SF = S;
-    long long off = 0;
-    for (int k = 0; k <= d; ++k) W.SF.Rcap[k] = (k == 0 || k == d) ? 1 : S.Rcap[k] + F.Rcap[k];
-    for (int k = 0; k < d; ++k) {
-      W.SF.off[k] = off;
-      off += (long long)W.SF.Rcap[k] * S.m[k] * S.n[k] * W.SF.Rcap[k + 1];
-    }
-    W.SF.data = ar.take<double>(off);
-    W.SF.R = ar.take<int>(d + 1);
+    // B fitted by amen_mv in psi's capacities
     W.B = vec_like(ar, d, psi.n, psi.rcap);
     W.zmv = vec_like(ar, d, z.n, z.rcap);
   }
@@ -173,6 +220,7 @@ tt_status carve_keff(const MatMeta &H, const MatMeta &S, const MatMeta &F, const
   W.nrm = ar.take<double>(1);
   W.dbuf = ar.take<double>(4);
   W.sweeps = ar.take<int>(1);
+  W.inner = ar.take<int>(1);
   // scratch: the max over the sub-operations
   size_t mx = 0;
   auto upd = [&](size_t v) { mx = v > mx ? v : mx; };
@@ -189,6 +237,13 @@ tt_status carve_keff(const MatMeta &H, const MatMeta &S, const MatMeta &F, const
   { Arena c; round_meta(psi, 0.0, 1, nullptr, nullptr, 0, c, nullptr); upd(c.used); }
   { Arena c; dot_meta(W.f, psi, nullptr, c, nullptr); upd(c.used); }
   upd(amen_ws_bytes(H, W.B, psi, z, o.gmres_restart));
+  if (res_on) {
+    const size_t b1 = amen_mv_ws_bytes(W.M, psi, W.Rv, W.zr), b2 = amen_mv_ws_bytes(H, psi, W.Hv, W.zr);
+    if (b1 == 0 || b2 == 0) return fail(TT_ERR_CAPACITY, "keff: residual amen_mv operands rejected");
+    upd(b1);
+    upd(b2);
+    { Arena c; orth_meta(W.Rv, -1, nullptr, c, nullptr); upd(c.used); }
+  }
   W.sub_cap = mx;
   W.sub = ar.take<char>(mx);
   return TT_OK;
@@ -241,6 +296,24 @@ tt_status keff_meta(const MatMeta &H, const MatMeta &S, const MatMeta &F, const 
   ao.max_restarts = o.gmres_max_restarts;
   int hflag = 0;
   const bool mv = o.matvec == 1;
+  // fixed-point residual ||H Psi - (S + F/k) Psi|| / ||H Psi|| (Z19) of the
+  // current normalised Psi and k, both products fitted by amen_mv
+  auto residual = [&]() -> tt_status {
+    TT_TRY(add_meta(mat_as_vec(S), nullptr, mat_as_vec(F), &W.sc->kinv, mat_as_vec(W.SF), s));
+    TT_TRY(add_meta(mat_as_vec(H), nullptr, mat_as_vec(W.SF), &W.sc->minus_one, mat_as_vec(W.M), s));
+    TT_TRY(copy_meta(psi, W.Rv, s));
+    TT_TRY(copy_meta(W.z0, W.zr, s));
+    { Arena a = sub(); TT_TRY(amen_mv_meta(W.M, psi, W.Rv, W.zr, o.eps_round, o.mv_max_sweeps, o.rmax, nullptr, a, s)); }
+    { Arena a = sub(); TT_TRY(orth_meta(W.Rv, -1, &W.sc->rnorm, a, s)); }
+    TT_TRY(copy_meta(psi, W.Hv, s));
+    TT_TRY(copy_meta(W.z0, W.zr, s));
+    { Arena a = sub(); TT_TRY(amen_mv_meta(H, psi, W.Hv, W.zr, o.eps_round, o.mv_max_sweeps, o.rmax, nullptr, a, s)); }
+    { Arena a = sub(); TT_TRY(orth_meta(W.Hv, -1, &W.sc->hnorm, a, s)); }
+    keff_res_kernel<<<1, 1, 0, s>>>(W.sc, rep.res_hist_dev, rep.hist_cap, rep.res_dev);
+    return check_launch("keff residual");
+  };
+  if (rep.res_dev) cudaMemsetAsync(rep.res_dev, 0xff, sizeof(double), s);   // NaN pattern until evaluated
+  if (rep.res_hist_dev && rep.hist_cap > 0) fill_kernel<<<1, 256, 0, s>>>(rep.res_hist_dev, rep.hist_cap, -1.0);
   if (mv) TT_TRY(copy_meta(psi, W.B, s));   // first amen_mv guess: Psi_0
   for (int it = 0; it < o.max_outer; ++it) {
     if (!mv) {
@@ -256,17 +329,21 @@ tt_status keff_meta(const MatMeta &H, const MatMeta &S, const MatMeta &F, const 
       { Arena a = sub(); TT_TRY(amen_mv_meta(W.SF, psi, W.B, W.zmv, o.eps_round, o.mv_max_sweeps, o.rmax, nullptr, a, s)); }
     }
     TT_TRY(copy_meta(W.z0, z, s));
-    { Arena a = sub(); TT_TRY(amen_solve_meta(H, W.B, psi, z, ao, W.sweeps, nullptr, nullptr, a, s)); }
+    set_i32_k<<<1, 1, 0, s>>>(W.inner, 0);
+    { Arena a = sub(); TT_TRY(amen_solve_meta(H, W.B, psi, z, ao, W.sweeps, nullptr, W.inner, a, s)); }
     { Arena a = sub(); TT_TRY(dot_meta(W.f, psi, &W.sc->s_new, a, s)); }
     keff_after_solve_kernel<<<1, 1, 0, s>>>(W.sc);
     { Arena a = sub(); TT_TRY(orth_meta(psi, -1, W.nrm, a, s)); }
-    keff_update_kernel<<<1, 1, 0, s>>>(W.sc, W.nrm, o.tol_k, rep.k_hist_dev, rep.sweeps_hist_dev, W.sweeps,
-                                       rep.hist_cap, o.max_outer, rep.k_dev, rep.iters_dev, rep.status_dev);
+    keff_update_kernel<<<1, 1, 0, s>>>(W.sc, W.nrm, rep.k_hist_dev, rep.sweeps_hist_dev, rep.inner_status_hist_dev,
+                                       W.sweeps, W.inner, rep.hist_cap);
     TT_TRY(scale_meta(psi, &W.sc->nrm_inv, 1.0, 0, s));
+    if (o.tol_res > 0.0) TT_TRY(residual());
+    keff_decide_kernel<<<1, 1, 0, s>>>(W.sc, o.tol_k, o.tol_res, o.max_outer, rep.k_dev, rep.iters_dev, rep.status_dev);
     TT_TRY(read_back(&hflag, &W.sc->flag, sizeof(int), s));
     TT_TRY(check_launch("keff iteration"));
     if (hflag) break;
   }
+  if (o.tol_res == 0.0) TT_TRY(residual());   // reported once for the final iterate
   return check_launch("keff_fixed_point");
 }
 
@@ -300,7 +377,7 @@ __global__ void alpha_update_kernel(AlphaState *st, const double *k_dev, const i
     if (ithist) ithist[it] = *kit_dev;
   }
   st->iters = it + 1;
-  if (*kst_dev != 0 && *kst_dev != TT_ERR_NOCONV) {   // no fission / NaN inside the k-eff solve
+  if (*kst_dev != 0) {   // the k-eff solve did not converge (or no fission / NaN): stop with its status
     st->status = *kst_dev;
     st->flag = 1;
   } else if (fabs(k - 1.0) <= tol) {
@@ -390,8 +467,8 @@ tt_status alpha_meta(const MatMeta &H, const MatMeta &V, const MatMeta &S, const
   alpha_init_kernel<<<1, 1, 0, s>>>(W.st, o.alpha0);
   const VecMeta hv = mat_as_vec(H), vv = mat_as_vec(V), av = mat_as_vec(W.Ha);
   keff_report kr;
-  kr.k_dev = W.kk; kr.iters_dev = W.kit; kr.k_hist_dev = nullptr; kr.sweeps_hist_dev = nullptr;
-  kr.hist_cap = 0; kr.status_dev = W.kst;
+  std::memset(&kr, 0, sizeof(kr));
+  kr.k_dev = W.kk; kr.iters_dev = W.kit; kr.hist_cap = 0; kr.status_dev = W.kst;
   int hflag = 0;
   for (int t = 0; t < o.max_alpha; ++t) {
     TT_TRY(add_meta(hv, &W.st->one, vv, &W.st->a, av, s));
@@ -491,8 +568,10 @@ extern "C" tt_status keff_fixed_point(const tt_mat *H, const tt_mat *S, const tt
   TT_TRY(make_vec_meta(z, zm));
   if (!o || !rep || !ws) return fail(TT_ERR_ARG, "keff_fixed_point: NULL options, report or workspace");
   if (o->max_outer < 1 || o->rmax < 1 || o->max_sweeps < 1 || o->gmres_max_restarts < 1 ||
-      (o->matvec == 1 && o->mv_max_sweeps < 1))
+      ((o->matvec == 1 || o->tol_res >= 0.0) && o->mv_max_sweeps < 1))
     return fail(TT_ERR_ARG, "keff_fixed_point: iteration limits must be >= 1");
+  if (!rep->k_dev || !rep->iters_dev || !rep->status_dev)
+    return fail(TT_ERR_ARG, "keff_fixed_point: k_dev, iters_dev and status_dev are required");
   Arena ar;
   ar.base = (char *)ws;
   ar.cap = wsb;

@@ -433,11 +433,13 @@ __device__ void jacobi_core(int m, int p, double *W, long long ldw, double *V, l
           wa[r] = c * x - s * y;
           wb[r] = s * x + c * y;
         }
-        double *va = V + (long long)a * ldv, *vb = V + (long long)b * ldv;
-        for (int r = lane; r < p; r += 32) {
-          const double x = va[r], y = vb[r];
-          va[r] = c * x - s * y;
-          vb[r] = s * x + c * y;
+        if (V) {
+          double *va = V + (long long)a * ldv, *vb = V + (long long)b * ldv;
+          for (int r = lane; r < p; r += 32) {
+            const double x = va[r], y = vb[r];
+            va[r] = c * x - s * y;
+            vb[r] = s * x + c * y;
+          }
         }
         if (lane == 0) *flag = 1;
       }
@@ -476,6 +478,7 @@ __global__ void __launch_bounds__(1024) jacobi_kernel(const SVDDesc *__restrict_
   __shared__ int s_flag;
   const SVDDesc g = descs[blockIdx.x];
   const int m = g.m, p = g.p, tid = threadIdx.x;
+  const bool wantv = g.V != nullptr;   // V == nullptr: left vectors and sigma only
   double *W, *V;
   long long ldw, ldv;
   double *s_sig;
@@ -483,14 +486,14 @@ __global__ void __launch_bounds__(1024) jacobi_kernel(const SVDDesc *__restrict_
   if (SMEM) {
     W = dsm;
     ldw = m;
-    V = dsm + (long long)m * p;
+    V = wantv ? dsm + (long long)m * p : nullptr;
     ldv = p;
-    s_sig = V + (long long)p * p;
+    s_sig = dsm + (long long)m * p + (wantv ? (long long)p * p : 0);
     s_pos = reinterpret_cast<int *>(s_sig + p);
   } else {
     W = g.work;
     ldw = m;
-    V = g.work + (long long)m * p;
+    V = wantv ? g.work + (long long)m * p : nullptr;
     ldv = p;
     s_sig = dsm;
     s_pos = reinterpret_cast<int *>(dsm + p);
@@ -499,10 +502,11 @@ __global__ void __launch_bounds__(1024) jacobi_kernel(const SVDDesc *__restrict_
     const int r = (int)(e % m), c = (int)(e / m);
     W[r + c * ldw] = g.W[r + c * g.ldw];
   }
-  for (long long e = tid; e < (long long)p * p; e += blockDim.x) {
-    const int r = (int)(e % p), c = (int)(e / p);
-    V[r + c * ldv] = (r == c) ? 1.0 : 0.0;
-  }
+  if (wantv)
+    for (long long e = tid; e < (long long)p * p; e += blockDim.x) {
+      const int r = (int)(e % p), c = (int)(e / p);
+      V[r + c * ldv] = (r == c) ? 1.0 : 0.0;
+    }
   __syncthreads();
   jacobi_core(m, p, W, ldw, V, ldv, s_sig, s_pos, &s_flag, g.sweeps_out);
   // sorted outputs
@@ -511,10 +515,11 @@ __global__ void __launch_bounds__(1024) jacobi_kernel(const SVDDesc *__restrict_
     const double sc = s_sig[c];
     g.U[r + (long long)s_pos[c] * g.ldu] = sc > 0.0 ? W[r + c * ldw] / sc : 0.0;
   }
-  for (long long e = tid; e < (long long)p * p; e += blockDim.x) {
-    const int r = (int)(e % p), c = (int)(e / p);
-    g.V[r + (long long)s_pos[c] * g.ldv] = V[r + c * ldv];
-  }
+  if (wantv)
+    for (long long e = tid; e < (long long)p * p; e += blockDim.x) {
+      const int r = (int)(e % p), c = (int)(e / p);
+      g.V[r + (long long)s_pos[c] * g.ldv] = V[r + c * ldv];
+    }
   for (int c = tid; c < p; c += blockDim.x) g.sigma[s_pos[c]] = s_sig[c];
 }
 
@@ -569,8 +574,10 @@ __global__ void __launch_bounds__(BJ_THREADS) jacobi_block_kernel(const SVDDesc 
     const int r = (int)(e % m), c = (int)(e / m);
     W[e] = g.W[r + c * g.ldw];
   }
-  for (long long e = blockIdx.x * (long long)BJ_THREADS + tid; e < (long long)p * p; e += (long long)G * BJ_THREADS)
-    V[e] = ((e % p) == (e / p)) ? 1.0 : 0.0;
+  const bool wantv = g.V != nullptr;
+  if (wantv)
+    for (long long e = blockIdx.x * (long long)BJ_THREADS + tid; e < (long long)p * p; e += (long long)G * BJ_THREADS)
+      V[e] = ((e % p) == (e / p)) ? 1.0 : 0.0;
   if (blockIdx.x == 0 && tid == 0) *flag = 0;
   grid_barrier(bar, G);
   int sweep = 0;
@@ -592,10 +599,11 @@ __global__ void __launch_bounds__(BJ_THREADS) jacobi_block_kernel(const SVDDesc 
           const int r = e % m, q = e / m;
           sW[e] = col[q] >= 0 ? W[r + (long long)col[q] * m] : 0.0;
         }
-        for (int e = tid; e < p * 2 * JB; e += BJ_THREADS) {
-          const int r = e % p, q = e / p;
-          sV[e] = col[q] >= 0 ? V[r + (long long)col[q] * p] : 0.0;
-        }
+        if (wantv)
+          for (int e = tid; e < p * 2 * JB; e += BJ_THREADS) {
+            const int r = e % p, q = e / p;
+            sV[e] = col[q] >= 0 ? V[r + (long long)col[q] * p] : 0.0;
+          }
         __syncthreads();
         // one inner pass over all pairs of the 2JB columns (round robin, one warp per pair)
         int rotated = 0;
@@ -624,10 +632,12 @@ __global__ void __launch_bounds__(BJ_THREADS) jacobi_block_kernel(const SVDDesc 
               const double x = wa[r], y = wb[r];
               wa[r] = c * x - s * y; wb[r] = s * x + c * y;
             }
-            double *va = sV + (long long)a * p, *vb = sV + (long long)b * p;
-            for (int r = lane; r < p; r += 32) {
-              const double x = va[r], y = vb[r];
-              va[r] = c * x - s * y; vb[r] = s * x + c * y;
+            if (wantv) {
+              double *va = sV + (long long)a * p, *vb = sV + (long long)b * p;
+              for (int r = lane; r < p; r += 32) {
+                const double x = va[r], y = vb[r];
+                va[r] = c * x - s * y; vb[r] = s * x + c * y;
+              }
             }
             rotated = 1;
             fl += 6ull * (m + p);
@@ -639,10 +649,11 @@ __global__ void __launch_bounds__(BJ_THREADS) jacobi_block_kernel(const SVDDesc 
           const int r = e % m, q = e / m;
           if (col[q] >= 0) W[r + (long long)col[q] * m] = sW[e];
         }
-        for (int e = tid; e < p * 2 * JB; e += BJ_THREADS) {
-          const int r = e % p, q = e / p;
-          if (col[q] >= 0) V[r + (long long)col[q] * p] = sV[e];
-        }
+        if (wantv)
+          for (int e = tid; e < p * 2 * JB; e += BJ_THREADS) {
+            const int r = e % p, q = e / p;
+            if (col[q] >= 0) V[r + (long long)col[q] * p] = sV[e];
+          }
         __syncthreads();
       }
       grid_barrier(bar, G);
@@ -682,10 +693,11 @@ __global__ void __launch_bounds__(BJ_THREADS) jacobi_block_kernel(const SVDDesc 
     const double sc = s_sig[c];
     g.U[r + (long long)s_pos[c] * g.ldu] = sc > 0.0 ? W[e] / sc : 0.0;
   }
-  for (long long e = tid; e < (long long)p * p; e += BJ_THREADS) {
-    const int r = (int)(e % p), c = (int)(e / p);
-    g.V[r + (long long)s_pos[c] * g.ldv] = V[e];
-  }
+  if (wantv)
+    for (long long e = tid; e < (long long)p * p; e += BJ_THREADS) {
+      const int r = (int)(e % p), c = (int)(e / p);
+      g.V[r + (long long)s_pos[c] * g.ldv] = V[e];
+    }
   for (int c = tid; c < p; c += BJ_THREADS) g.sigma[s_pos[c]] = s_sig[c];
 }
 
@@ -723,13 +735,14 @@ struct BJSync {
 };
 static thread_local BJSync g_bj;
 
-static size_t svd_smem_bytes(int mcap, int pcap) {
-  return ((size_t)mcap * pcap + (size_t)pcap * pcap + pcap) * sizeof(double) + (size_t)pcap * sizeof(int) + 16;
+static size_t svd_smem_bytes(int mcap, int pcap, bool wantv) {
+  return ((size_t)mcap * pcap + (wantv ? (size_t)pcap * pcap : 0) + pcap) * sizeof(double) +
+         (size_t)pcap * sizeof(int) + 16;
 }
 
 tt_status launch_jacobi(const SVDDesc *descs_dev, int count, int mcap, int pcap, cudaStream_t s) {
   if (count <= 0) return TT_OK;
-  const size_t smem = svd_smem_bytes(mcap, pcap);
+  const size_t smem = svd_smem_bytes(mcap, pcap, true);
   const size_t limit = 220 * 1024;
   if (smem <= limit) {
     static bool attr_set = false;
@@ -769,6 +782,213 @@ tt_status launch_jacobi(const SVDDesc *descs_dev, int count, int mcap, int pcap,
 void set_jacobi_sync(unsigned int *bar) {
   g_bj.bar = bar;
   g_bj.flag = bar ? reinterpret_cast<int *>(bar + 2) : nullptr;
+}
+
+
+// ------------------------------------------------------------------ TSQR ---
+// Tall QR (m >> n) as a tree of Householder QRs (communication-avoiding TSQR):
+// level l splits its rows_l x n input into P_l row blocks (P_l - 1 of
+// ceil(rows_l / P_l) >= 2n rows and a ragged last one that may be shorter than
+// n), each factorised by its own CTA with the panel in shared memory
+// (qr_kernel); the R factors are stacked into the ((P_l - 1) n + min(last, n))
+// x n input of level l+1; the last (small) stack is factorised once (top).  The explicit Q
+// is formed top-down: Q_l = blockdiag(Q_leaf,l,i) Q_(l+1), i.e. one batched
+// DMMA GEMM per level (leaf i: mb x n times the n x n block i of Q_(l+1)),
+// the level-0 product written straight into the caller's Q (strides).
+// Backward stable like the single Householder QR; R (and Q) differ from it
+// only by the column signs (gauge).  Sizes follow the device-resident
+// descriptor; the level structure is planned on the host from capacities.
+namespace {
+constexpr int TSQR_MB = 600;     // leaf rows: the 32-column panels of a leaf stay in shared memory
+constexpr int TSQR_MAXL = 8;
+
+struct TsqrPlan {
+  int levels = 0;
+  int mb = TSQR_MB;
+  int Pcap[TSQR_MAXL] = {};
+  long long rows[TSQR_MAXL + 1] = {};   // capacity rows of each level's input
+};
+
+TsqrPlan tsqr_plan_caps(int mcap, int ncap) {
+  TsqrPlan p;
+  p.mb = TSQR_MB > 4 * ncap ? TSQR_MB : 4 * ncap;   // >= 4n: each level shrinks the rows >= 2x
+  long long rows = mcap;
+  p.rows[0] = rows;
+  if (ncap < 1 || mcap < 3 * ncap || mcap <= p.mb) return p;
+  while (rows > p.mb && p.levels < TSQR_MAXL) {
+    const int P = (int)((rows + p.mb - 1) / p.mb);
+    p.Pcap[p.levels] = P;
+    rows = (long long)P * ncap;
+    p.rows[++p.levels] = rows;
+  }
+  return p;
+}
+
+struct TsqrDev {
+  int levels, mb, ncap;
+  int Pcap[TSQR_MAXL];
+  QRDesc *qd[TSQR_MAXL];           // leaves of each level
+  QRDesc *qtop;
+  GemmDesc *gd;                    // [2 TSQR_MAXL]: uniform leaves, last leaf
+  double *A[TSQR_MAXL + 1];        // working copies (level inputs; [levels] = top)
+  double *Ql[TSQR_MAXL];           // leaf Q factors
+  double *S[TSQR_MAXL + 1];        // stacked R factors = input of level l (l >= 1)
+  double *Qacc[TSQR_MAXL + 1];     // Q of level l's input (l >= 1)
+  double *tau[TSQR_MAXL + 1], *T[TSQR_MAXL + 1];
+  long long Tstride;
+};
+
+__device__ QRDesc qr_empty() {
+  QRDesc q;
+  q.m = 0; q.n = 0; q.src = nullptr; q.src_rs = 0; q.src_cs = 0; q.A = nullptr; q.lda = 1; q.Q = nullptr;
+  q.q_rs = 0; q.q_cs = 0; q.R = nullptr; q.ldr = 1; q.rt = 0; q.tau = nullptr; q.T = nullptr;
+  return q;
+}
+__device__ GemmDesc gemm_empty() {
+  GemmDesc g;
+  g.M = 0; g.N = 0; g.K = 0; g.transA = 0; g.transB = 0; g.lda = 1; g.ldb = 1; g.A = nullptr; g.B = nullptr;
+  g.C = nullptr; g.dr = 1 << 30; g.dc = 1 << 30; g.s_r0 = 1; g.s_r1 = 0; g.s_c0 = 0; g.s_c1 = 0; g.alpha = 1.0;
+  g.beta = 0.0; g.alpha_dev = nullptr; g.skip = nullptr; g.batch = 1; g.bsA = g.bsB = g.bsC = 0;
+  return g;
+}
+__device__ GemmDesc gemm_q(int M, int N, int K, const double *A, long long lda, const double *B, long long ldb,
+                           double *C, long long crs, long long ccs) {
+  GemmDesc g = gemm_empty();
+  g.M = M; g.N = N; g.K = K; g.A = A; g.lda = lda; g.B = B; g.ldb = ldb; g.C = C;
+  g.s_r0 = crs; g.s_c0 = ccs; g.batch = 0;
+  return g;
+}
+
+__global__ void tsqr_plan_kernel(const QRDesc *__restrict__ in_p, TsqrDev D) {
+  const QRDesc in = *in_p;
+  const int n = in.n, m = in.m;
+  for (int l = 0; l < D.levels; ++l)
+    for (int i = 0; i < D.Pcap[l]; ++i) D.qd[l][i] = qr_empty();
+  *D.qtop = qr_empty();
+  for (int q = 0; q < 2 * D.levels; ++q) D.gd[q] = gemm_empty();
+  if (m < 3 * n || m <= D.mb || n < 1) {   // not tall at the device sizes: the plain QR
+    D.qd[0][0] = in;
+    return;
+  }
+  long long rows = m;
+  int P[TSQR_MAXL], mbl[TSQR_MAXL];
+  long long rl[TSQR_MAXL + 1];
+  rl[0] = rows;
+  for (int l = 0; l < D.levels; ++l) {
+    // p - 1 leaves of ceil(rows / p) rows (>= 2n) and a ragged last one (>= 1 row)
+    const int p = (int)((rows + D.mb - 1) / D.mb);
+    const int mb = (int)((rows + p - 1) / p);
+    const long long last = rows - (long long)(p - 1) * mb;
+    const int qlast = (int)(last < n ? last : n);
+    P[l] = p;
+    mbl[l] = mb;
+    const long long nxt = (long long)(p - 1) * n + qlast;
+    for (int i = 0; i < p; ++i) {
+      QRDesc &q = D.qd[l][i];
+      const long long r0 = (long long)i * mb;
+      q.m = (int)(i < p - 1 ? mb : last);
+      q.n = n;
+      if (l == 0) { q.src = in.src + r0 * in.src_rs; q.src_rs = in.src_rs; q.src_cs = in.src_cs; }
+      else { q.src = D.S[l] + r0; q.src_rs = 1; q.src_cs = rows; }
+      q.A = D.A[l] + r0; q.lda = rows;
+      q.Q = in.Q ? D.Ql[l] + r0 : nullptr; q.q_rs = 1; q.q_cs = rows;
+      q.R = D.S[l + 1] + (long long)i * n; q.ldr = nxt; q.rt = 0;
+      q.tau = D.tau[l] + (long long)i * D.ncap;
+      q.T = D.T[l] + (long long)i * D.Tstride;
+    }
+    rows = nxt;
+    rl[l + 1] = rows;
+  }
+  const int L = D.levels;
+  QRDesc &t = *D.qtop;
+  t.m = (int)rows; t.n = n;
+  t.src = D.S[L]; t.src_rs = 1; t.src_cs = rows;
+  t.A = D.A[L]; t.lda = rows;
+  t.Q = in.Q ? D.Qacc[L] : nullptr; t.q_rs = 1; t.q_cs = rows;
+  t.R = in.R; t.ldr = in.ldr; t.rt = in.rt;
+  t.tau = D.tau[L]; t.T = D.T[L];
+  if (!in.Q) return;
+  for (int l = L - 1; l >= 0; --l) {
+    const int p = P[l], mb = mbl[l];
+    const double *Qn = D.Qacc[l + 1];
+    const long long ldn = rl[l + 1];
+    double *out = l == 0 ? in.Q : D.Qacc[l];
+    const long long crs = l == 0 ? in.q_rs : 1, ccs = l == 0 ? in.q_cs : rl[l];
+    GemmDesc &u = D.gd[2 * l];
+    if (p > 1) {   // leaves 0 .. p-2: one batched GEMM (mb x n) (n x n)
+      u = gemm_q(mb, n, n, D.Ql[l], rl[l], Qn, ldn, out, crs, ccs);
+      u.batch = p - 1; u.bsA = mb; u.bsB = n; u.bsC = (long long)mb * crs;
+    }
+    const long long r0 = (long long)(p - 1) * mb, last = rl[l] - r0;
+    D.gd[2 * l + 1] = gemm_q((int)last, n, (int)(last < n ? last : n), D.Ql[l] + r0, rl[l],
+                             Qn + (long long)(p - 1) * n, ldn, out + r0 * crs, crs, ccs);
+  }
+}
+}  // namespace
+
+size_t qr_tall_ws_bytes(int mcap, int ncap) {
+  const TsqrPlan p = tsqr_plan_caps(mcap, ncap);
+  if (p.levels == 0) return 0;
+  Arena ar;
+  const long long Tstride = 32LL * 32 * ((ncap + 31) / 32 + 1);
+  for (int l = 0; l < p.levels; ++l) {
+    ar.take<QRDesc>(p.Pcap[l]);
+    ar.take<double>(p.rows[l] * ncap);             // A
+    ar.take<double>(p.rows[l] * ncap);             // Ql
+    ar.take<double>((long long)p.Pcap[l] * ncap);  // tau
+    ar.take<double>((long long)p.Pcap[l] * Tstride);
+  }
+  for (int l = 1; l <= p.levels; ++l) {
+    ar.take<double>(p.rows[l] * ncap);   // S
+    ar.take<double>(p.rows[l] * ncap);   // Qacc
+  }
+  ar.take<double>(p.rows[p.levels] * ncap);   // A top
+  ar.take<double>(ncap);                      // tau top
+  ar.take<double>(Tstride);                   // T top
+  ar.take<QRDesc>(1);
+  ar.take<GemmDesc>(2 * TSQR_MAXL);
+  return ar.used;
+}
+
+tt_status launch_qr_tall(const QRDesc *desc_dev, int mcap, int ncap, void *ws, size_t wsb, cudaStream_t s) {
+  const TsqrPlan p = tsqr_plan_caps(mcap, ncap);
+  if (p.levels == 0 || !ws) return launch_qr(desc_dev, 1, s);
+  Arena ar;
+  ar.base = (char *)ws;
+  ar.cap = wsb;
+  TsqrDev D;
+  D.levels = p.levels;
+  D.mb = p.mb;
+  D.ncap = ncap;
+  D.Tstride = 32LL * 32 * ((ncap + 31) / 32 + 1);
+  for (int l = 0; l < TSQR_MAXL; ++l) { D.Pcap[l] = p.Pcap[l]; D.qd[l] = nullptr; D.Ql[l] = nullptr; }
+  for (int l = 0; l <= TSQR_MAXL; ++l) { D.A[l] = D.S[l] = D.Qacc[l] = D.tau[l] = D.T[l] = nullptr; }
+  for (int l = 0; l < p.levels; ++l) {
+    D.qd[l] = ar.take<QRDesc>(p.Pcap[l]);
+    D.A[l] = ar.take<double>(p.rows[l] * ncap);
+    D.Ql[l] = ar.take<double>(p.rows[l] * ncap);
+    D.tau[l] = ar.take<double>((long long)p.Pcap[l] * ncap);
+    D.T[l] = ar.take<double>((long long)p.Pcap[l] * D.Tstride);
+  }
+  for (int l = 1; l <= p.levels; ++l) {
+    D.S[l] = ar.take<double>(p.rows[l] * ncap);
+    D.Qacc[l] = ar.take<double>(p.rows[l] * ncap);
+  }
+  D.A[p.levels] = ar.take<double>(p.rows[p.levels] * ncap);
+  D.tau[p.levels] = ar.take<double>(ncap);
+  D.T[p.levels] = ar.take<double>(D.Tstride);
+  D.qtop = ar.take<QRDesc>(1);
+  D.gd = ar.take<GemmDesc>(2 * TSQR_MAXL);
+  if (!ar.ok()) return fail(TT_ERR_CAPACITY, "qr (tall): workspace too small");
+  tsqr_plan_kernel<<<1, 1, 0, s>>>(desc_dev, D);
+  TT_TRY(check_launch("tsqr plan"));
+  for (int l = 0; l < p.levels; ++l) TT_TRY(launch_qr(D.qd[l], p.Pcap[l], s));
+  TT_TRY(launch_qr(D.qtop, 1, s));
+  for (int l = p.levels - 1; l >= 0; --l) {
+    if (p.Pcap[l] > 1) TT_TRY(launch_gemm_k(D.gd + 2 * l, 1, p.mb, ncap, ncap, s, p.Pcap[l] - 1));
+    TT_TRY(launch_gemm_k(D.gd + 2 * l + 1, 1, (int)(p.rows[l] < p.mb ? p.rows[l] : p.mb), ncap, ncap, s));
+  }
+  return TT_OK;
 }
 
 }  // namespace tt

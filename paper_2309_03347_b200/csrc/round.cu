@@ -21,6 +21,8 @@ struct StepWS {
   double *norm;   // [1]
   unsigned int *bar;  // [4] grid barrier of the block Jacobi
   long long Acap, slot;
+  char *qrws;         // TSQR scratch of the tall unfoldings
+  size_t qrwsb;
 };
 
 struct Caps {
@@ -28,6 +30,26 @@ struct Caps {
   int rmax;        // max rank capacity
   int mq, pq;      // max QR rows / cols
 };
+
+// capacity shapes of the QR problems of orthogonalisation / truncation step k
+struct QCap { int m, n; };
+QCap qcap_rl(const VecMeta &x, int k) { return {x.n[k] * x.rcap[k + 1], x.rcap[k]}; }
+QCap qcap_lr(const VecMeta &x, int k) { return {x.rcap[k] * x.n[k], x.rcap[k + 1]}; }
+QCap qcap_trunc(const VecMeta &x, int k) {
+  const int a = x.rcap[k] * x.n[k], b = x.rcap[k + 1];
+  return {a > b ? a : b, a < b ? a : b};
+}
+size_t qr_ws_max(const VecMeta &x) {
+  size_t b = 0;
+  for (int k = 0; k < x.d; ++k) {
+    QCap c[3] = {qcap_rl(x, k), qcap_lr(x, k), qcap_trunc(x, k)};
+    for (auto &q : c) {
+      const size_t v = qr_tall_ws_bytes(q.m, q.n);
+      b = v > b ? v : b;
+    }
+  }
+  return b;
+}
 
 Caps caps_of(const VecMeta &x) {
   Caps c;
@@ -68,6 +90,8 @@ StepWS carve(const VecMeta &x, Arena &ar) {
   w.iv = ar.take<int>(8);
   w.norm = ar.take<double>(1);
   w.bar = ar.take<unsigned int>(4);
+  w.qrwsb = qr_ws_max(x);
+  w.qrws = ar.take<char>(w.qrwsb);
   return w;
 }
 
@@ -80,6 +104,7 @@ __device__ GemmDesc gemm_desc(int M, int N, int K, const double *A, long long ld
   g.B = B; g.ldb = ldb;
   gemm_plain_c(g, C, ldc);
   g.alpha = 1.0; g.beta = 0.0; g.alpha_dev = nullptr; g.skip = nullptr;
+  g.batch = 0; g.bsA = g.bsB = g.bsC = 0;
   return g;
 }
 
@@ -252,7 +277,8 @@ tt_status orth_meta(const VecMeta &x, int dir, double *norm_dev, Arena &ar, cuda
   if (dir < 0) {
     for (int k = d - 1; k >= 1; --k) {
       plan_orth_rl<<<1, 1, 0, s>>>(x, k, w);
-      TT_TRY(launch_qr(w.qd, 1, s));
+      const QCap qc = qcap_rl(x, k);
+      TT_TRY(launch_qr_tall(w.qd, qc.m, qc.n, w.qrws, w.qrwsb, s));
       TT_TRY(launch_gemm(w.gd, 1, x.rcap[k - 1] * x.n[k - 1], x.rcap[k], s));
       TT_TRY(launch_copy(w.cd, 1, (long long)x.rcap[k - 1] * x.n[k - 1] * x.rcap[k], s));
     }
@@ -260,7 +286,8 @@ tt_status orth_meta(const VecMeta &x, int dir, double *norm_dev, Arena &ar, cuda
   } else {
     for (int k = 0; k <= d - 2; ++k) {
       plan_orth_lr<<<1, 1, 0, s>>>(x, k, w);
-      TT_TRY(launch_qr(w.qd, 1, s));
+      const QCap qc = qcap_lr(x, k);
+      TT_TRY(launch_qr_tall(w.qd, qc.m, qc.n, w.qrws, w.qrwsb, s));
       TT_TRY(launch_gemm(w.gd, 1, x.rcap[k + 1], x.n[k + 1] * x.rcap[k + 2], s));
       TT_TRY(launch_copy(w.cd, 1, (long long)x.rcap[k + 1] * x.n[k + 1] * x.rcap[k + 2], s));
     }
@@ -287,7 +314,8 @@ tt_status round_meta(const VecMeta &x, double eps, int rmax, double *disc, doubl
     const int m0cap = x.rcap[k] * x.n[k], p0cap = x.rcap[k + 1];
     const int pcap = m0cap < p0cap ? m0cap : p0cap;
     plan_trunc<<<1, 1, 0, s>>>(x, k, w);
-    TT_TRY(launch_qr(w.qd, 1, s));
+    const QCap qc = qcap_trunc(x, k);
+    TT_TRY(launch_qr_tall(w.qd, qc.m, qc.n, w.qrws, w.qrwsb, s));
     TT_TRY(launch_jacobi(w.sd, 1, pcap, pcap, s));
     trunc_kernel<<<1, 256, 0, s>>>(x, k, w, eps, rmax, disc, sv, sv_stride);
     const int mx = m0cap > p0cap ? m0cap : p0cap;

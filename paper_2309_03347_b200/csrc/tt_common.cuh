@@ -29,7 +29,18 @@ struct MatMeta {
   long long off[TT_MAX_D];
   double *data;
   int *R;  // device ranks [d+1]
+  int kind[TT_MAX_D];  // core structure (als.h CoreKind), set by detect_core_kinds; 0 = dense
 };
+
+// Device-side structure detection of the operator cores (als.h CoreKind): a
+// core with m == n >= 4 whose off-diagonal entries are all <= 1e-13 max|A_k| is
+// diagonal.  scratch_dev: >= 3 TT_MAX_D floats of device workspace.  Writes
+// A.kind (host) after one small read-back; the off-diagonal ratio
+// max|offdiag| / max|A_k| of each core goes to ratio_out (host [d], may be NULL;
+// -1 for cores that are not square or smaller than 4).
+constexpr double KIND_DIAG_TOL = 1e-13;
+constexpr int KIND_SCRATCH_FLOATS = 3 * TT_MAX_D;
+tt_status detect_core_kinds(MatMeta &A, float *scratch_dev, cudaStream_t s, double *ratio_out = nullptr);
 
 // ---------------------------------------------------------------- errors ---
 void set_error(const std::string &msg);
@@ -80,7 +91,24 @@ struct GemmDesc {
   double alpha, beta;
   const double *alpha_dev;  // if non-null, alpha *= *alpha_dev
   const int *skip;          // if non-null and *skip != 0 the GEMM is a no-op (GMRES steps after convergence)
+  // batch of independent GEMMs of the same shape: problem b reads A + b bsA, B + b bsB and
+  // writes through the scatter at C + b bsC (structured operator cores: one small GEMM per
+  // mode index i of a diagonal core).  batch = 0: a plain GEMM; batch >= 1: that many
+  // problems (may follow device ranks; launchers size grid z by a host capacity).
+  int batch;
+  long long bsA, bsB, bsC;
 };
+
+// problem b of a batched descriptor as a plain descriptor
+__host__ __device__ inline GemmDesc gemm_batch_item(const GemmDesc &g, int b) {
+  GemmDesc h = g;
+  h.A = g.A + (long long)b * g.bsA;
+  h.B = g.B + (long long)b * g.bsB;
+  h.C = g.C + (long long)b * g.bsC;
+  h.batch = 0;
+  return h;
+}
+__host__ __device__ inline int gemm_nbatch(const GemmDesc &g) { return g.batch >= 1 ? g.batch : 1; }
 
 __host__ __device__ inline void gemm_plain_c(GemmDesc &g, double *C, long long ldc) {
   g.C = C;
@@ -98,7 +126,10 @@ tt_status launch_gemm(const GemmDesc *descs_dev, int count, int Mcap, int Ncap, 
 // With Kcap (host upper bound of K) the launcher may split K across CTAs when the
 // output has few tiles, using the scratch registered by set_gemm_scratch (the
 // calling thread's current workspace slice); deterministic slice-sum reduction.
-tt_status launch_gemm_k(const GemmDesc *descs_dev, int count, int Mcap, int Ncap, int Kcap, cudaStream_t s);
+// batch: 0 for plain descriptors, else the host capacity of the descriptor's batch
+// count (count must then be 1).
+tt_status launch_gemm_k(const GemmDesc *descs_dev, int count, int Mcap, int Ncap, int Kcap, cudaStream_t s,
+                        int batch = 0);
 // A dependent chain of `count` GEMMs (descriptor i consumes earlier outputs) with
 // per-GEMM capacity shapes: one thread-block-cluster launch when all are small.
 // CUDA-graph replay of a fixed launch sequence (graph.cu): `enqueue` launches on
@@ -106,7 +137,7 @@ tt_status launch_gemm_k(const GemmDesc *descs_dev, int count, int Mcap, int Ncap
 uint64_t hash_bytes(const void *p, size_t n, uint64_t h = 1469598103934665603ull);
 tt_status run_captured(uint64_t key, cudaStream_t &s, const std::function<tt_status()> &enqueue);
 tt_status launch_gemm_seq(const GemmDesc *descs_dev, int count, const int *Mcap, const int *Ncap, const int *Kcap,
-                          cudaStream_t s);
+                          cudaStream_t s, const int *Bcap = nullptr);
 void set_gemm_scratch(double *ptr, size_t bytes);
 constexpr size_t GEMM_SPLIT_SCRATCH = 32ull << 20;  // bytes reserved by callers that enable split-K
 
@@ -128,6 +159,11 @@ struct QRDesc {
   double *T;             // workspace >= 32*32 * ceil(min(m,n)/32)
 };
 tt_status launch_qr(const QRDesc *descs_dev, int count, cudaStream_t s);
+// One QR whose capacity shape is mcap x ncap: tall shapes (mcap >= 3 ncap and
+// mcap > 600) run as a multi-CTA TSQR tree (linalg.cu) in the caller's
+// workspace of qr_tall_ws_bytes(mcap, ncap) bytes (0: not tall, plain QR).
+size_t qr_tall_ws_bytes(int mcap, int ncap);
+tt_status launch_qr_tall(const QRDesc *desc_dev, int mcap, int ncap, void *ws, size_t wsb, cudaStream_t s);
 
 // One-sided (Hestenes) Jacobi SVD of an m x p matrix W (m >= p), one CTA.
 // Outputs sorted by decreasing sigma: U (m x p, unit columns; zero columns for
@@ -142,6 +178,7 @@ struct SVDDesc {
   double *work;
   int *sweeps_out;
 };
+// (V == NULL in a descriptor: left singular vectors and sigma only.)
 tt_status launch_jacobi(const SVDDesc *descs_dev, int count, int mcap, int pcap, cudaStream_t s);
 // Grid-barrier words (>= 16 bytes of the caller's workspace) for the block
 // Jacobi kernel used when p is too large for one CTA's shared memory.

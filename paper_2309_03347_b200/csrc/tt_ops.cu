@@ -106,6 +106,59 @@ VecMeta mat_as_vec(const MatMeta &A) {
   return v;
 }
 
+// ------------------------------------------------------ core structure ---
+// grid (blocks, d): max|A_k| and max|off-diagonal| as float bit patterns (non-negative
+// floats order like their unsigned bits) via atomicMax; zeroed by the caller
+__global__ void core_offdiag_max_kernel(const MatMeta A, unsigned int *mx) {
+  const int k = blockIdx.y;
+  const int m = A.m[k], n = A.n[k];
+  if (m != n || m < 4) return;
+  const int R0 = A.R[k], R1 = A.R[k + 1];
+  const double *c = A.data + A.off[k];
+  const long long tot = (long long)R0 * m * n * R1;
+  double amax = 0.0, omax = 0.0;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < tot; e += (long long)gridDim.x * blockDim.x) {
+    const long long t = e / R0;
+    const int i = (int)(t % m), j = (int)((t / m) % n);
+    const double v = fabs(c[e]);
+    amax = v > amax ? v : amax;
+    if (i != j) omax = v > omax ? v : omax;
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    amax = fmax(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+    omax = fmax(omax, __shfl_xor_sync(0xffffffffu, omax, o));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    // round up so that a tiny nonzero never becomes 0
+    atomicMax(mx + 2 * k, __float_as_uint(__double2float_ru(amax)));
+    atomicMax(mx + 2 * k + 1, __float_as_uint(__double2float_ru(omax)));
+  }
+}
+
+__global__ void core_offdiag_ratio_kernel(const MatMeta A, const unsigned int *mx, float *out) {
+  const int k = threadIdx.x;
+  if (k >= A.d) return;
+  if (A.m[k] != A.n[k] || A.m[k] < 4) { out[k] = -1.f; return; }
+  const float a = __uint_as_float(mx[2 * k]), b = __uint_as_float(mx[2 * k + 1]);
+  out[k] = a > 0.f ? b / a : 0.f;
+}
+
+tt_status detect_core_kinds(MatMeta &A, float *scratch_dev, cudaStream_t s, double *ratio_out) {
+  // scratch: [d] ratios, then 2 d max words
+  unsigned int *mx = reinterpret_cast<unsigned int *>(scratch_dev + TT_MAX_D);
+  cudaMemsetAsync(mx, 0, 2 * sizeof(unsigned int) * A.d, s);
+  core_offdiag_max_kernel<<<dim3(64, A.d), 256, 0, s>>>(A, mx);
+  core_offdiag_ratio_kernel<<<1, TT_MAX_D, 0, s>>>(A, mx, scratch_dev);
+  TT_TRY(check_launch("detect_core_kinds"));
+  float r[TT_MAX_D];
+  TT_TRY(read_back(r, scratch_dev, sizeof(float) * A.d, s));
+  for (int k = 0; k < A.d; ++k) {
+    A.kind[k] = (r[k] >= 0.f && r[k] <= (float)KIND_DIAG_TOL) ? 1 : 0;
+    if (ratio_out) ratio_out[k] = r[k];
+  }
+  return TT_OK;
+}
+
 int max_slot(const VecMeta &x) {
   long long mx = 0;
   for (int k = 0; k < x.d; ++k) {

@@ -273,6 +273,40 @@ def als_update_interfaces(direction, dims, Iprev, Yk, Ak, Xk, Inext, stream=None
     return Inext
 
 
+CORE_DENSE, CORE_DIAG = 0, 1
+
+
+def core_kinds(A: "TTMat", stream=None):
+    """Device-detected structure of every operator core (tt_core_kinds):
+    returns (kinds, off-diagonal ratios) as host lists."""
+    kinds = (C.c_int32 * A.d)()
+    ratio = (C.c_double * A.d)()
+    ws = workspace(768, A.data.device)
+    check(lib().tt_core_kinds(A.c, C.cast(kinds, C.c_void_p), C.cast(ratio, C.c_void_p), _ptr(ws), ws.numel(),
+                              C.c_void_p(_stream(stream))))
+    return list(kinds), list(ratio)
+
+
+def als_local_apply_structured(kind, absorb, dims, Phi, Ak, Psi, x, y, stream=None):
+    """als_local_apply for a core of the given kind (CORE_DENSE / CORE_DIAG);
+    absorb = 1 folds the left operator rank into the left interface first."""
+    nb = lib().als_workspace_structured(int(kind), int(absorb), *dims)
+    ws = workspace(nb, x.device)
+    check(lib().als_local_apply_structured(int(kind), int(absorb), *[int(v) for v in dims], _ptr(Phi), _ptr(Ak),
+                                           _ptr(Psi), _ptr(x), _ptr(y), _ptr(ws), ws.numel(),
+                                           C.c_void_p(_stream(stream))))
+    return y
+
+
+def als_update_interfaces_structured(kind, absorb, direction, dims, Iprev, Yk, Ak, Xk, Inext, stream=None):
+    nb = lib().als_workspace_structured(int(kind), int(absorb), *dims)
+    ws = workspace(nb, Yk.device)
+    check(lib().als_update_interfaces_structured(int(kind), int(absorb), int(direction), *[int(v) for v in dims],
+                                                 _ptr(Iprev), _ptr(Yk), _ptr(Ak), _ptr(Xk), _ptr(Inext), _ptr(ws),
+                                                 ws.numel(), C.c_void_p(_stream(stream))))
+    return Inext
+
+
 # ------------------------------------------------------------------ a7 ---
 
 def amen_solve(A: TTMat, b: TTVec, x: TTVec, z: TTVec, eps: float, rmax: int = 1 << 20, max_sweeps: int = 20,
@@ -311,29 +345,46 @@ _MV = {"exact": 0, "amen_mv": 1}
 
 
 class KeffResult:
-    def __init__(self, k, iters, k_hist, sweeps_hist, status):
+    def __init__(self, k, iters, k_hist, sweeps_hist, status, res_hist=None, inner_hist=None, res=None):
         self.k, self.iters, self.k_hist, self.sweeps_hist, self.status = k, iters, k_hist, sweeps_hist, status
+        self.res_hist, self.inner_hist, self.res = res_hist, inner_hist, res
+
+
+def _keff_opts(tol_k, tol_res, eps_round, eps_solve, max_outer, rmax, max_sweeps, restart, max_restarts, matvec,
+               mv_max_sweeps):
+    return _lib.keff_opts(float(tol_k), float(tol_res), float(eps_round), float(eps_solve), int(max_outer),
+                          int(min(rmax, 2**30)), int(max_sweeps), 0, int(restart), int(max_restarts), 0, _MV[matvec],
+                          int(mv_max_sweeps))
 
 
 def keff_fixed_point(H: TTMat, S: TTMat, F: TTMat, psi: TTVec, z: TTVec, k0: float = 1.0, tol_k: float = 1e-10,
                      eps_round: float = 1e-12, eps_solve: float = 1e-11, max_outer: int = 200, rmax: int = 1 << 20,
                      max_sweeps: int = 20, restart: int = 40, max_restarts: int = 50, hist_cap: int = 256,
-                     matvec: str = "exact", mv_max_sweeps: int = 10, stream=None) -> KeffResult:
-    """matvec: "exact" (exact products + rounding) or "amen_mv" (fit-based product, NEXT-1)."""
-    o = _lib.keff_opts(float(tol_k), float(eps_round), float(eps_solve), int(max_outer), int(min(rmax, 2**30)),
-                       int(max_sweeps), int(restart), int(max_restarts), _MV[matvec], int(mv_max_sweeps))
+                     matvec: str = "exact", mv_max_sweeps: int = 10, tol_res: float = -1.0, stream=None) -> KeffResult:
+    """matvec: "exact" (exact products + rounding) or "amen_mv" (fit-based product, NEXT-1).
+    tol_res > 0: fixed-point residual every iteration, required for convergence;
+    0: evaluated once at the end; < 0: not evaluated."""
+    o = _keff_opts(tol_k, tol_res, eps_round, eps_solve, max_outer, rmax, max_sweeps, restart, max_restarts, matvec,
+                   mv_max_sweeps)
     dev = psi.device
     k = torch.zeros(1, dtype=torch.float64, device=dev)
     iters = torch.zeros(1, dtype=torch.int32, device=dev)
     kh = torch.zeros(hist_cap, dtype=torch.float64, device=dev)
+    rh = torch.zeros(hist_cap, dtype=torch.float64, device=dev)
     sh = torch.zeros(hist_cap, dtype=torch.int32, device=dev)
+    ih = torch.zeros(hist_cap, dtype=torch.int32, device=dev)
     st = torch.zeros(1, dtype=torch.int32, device=dev)
-    rep = _lib.keff_report(k.data_ptr(), iters.data_ptr(), kh.data_ptr(), sh.data_ptr(), int(hist_cap), st.data_ptr())
+    res = torch.zeros(1, dtype=torch.float64, device=dev)
+    rep = _lib.keff_report(k.data_ptr(), iters.data_ptr(), kh.data_ptr(), rh.data_ptr(), int(hist_cap), st.data_ptr(),
+                           sh.data_ptr(), ih.data_ptr(), res.data_ptr())
     nb = lib().keff_workspace(H.c, S.c, F.c, psi.c, z.c, C.byref(o))
+    if nb == 0:
+        check(lib().keff_fixed_point(H.c, S.c, F.c, psi.c, z.c, float(k0), C.byref(o), C.byref(rep), None, 0,
+                                     C.c_void_p(_stream(stream))))
     ws = workspace(nb, dev)
     check(lib().keff_fixed_point(H.c, S.c, F.c, psi.c, z.c, float(k0), C.byref(o), C.byref(rep), _ptr(ws),
                                  ws.numel(), C.c_void_p(_stream(stream))))
-    return KeffResult(k, iters, kh, sh, st)
+    return KeffResult(k, iters, kh, sh, st, rh, ih, res)
 
 
 # -------------------------------------------------------------- NEXT-2 ---
@@ -350,8 +401,8 @@ def alpha_secant(H: TTMat, V: TTMat, S: TTMat, F: TTMat, psi: TTVec, z: TTVec, a
                  rmax: int = 1 << 20, max_sweeps: int = 20, restart: int = 40, max_restarts: int = 50,
                  hist_cap: int = 64, matvec: str = "exact", mv_max_sweeps: int = 10, stream=None) -> AlphaResult:
     """alpha eigenvalue by the secant loop around the device k-eff solve (NEXT-2)."""
-    ko = _lib.keff_opts(float(tol_k), float(eps_round), float(eps_solve), int(max_outer), int(min(rmax, 2**30)),
-                        int(max_sweeps), int(restart), int(max_restarts), _MV[matvec], int(mv_max_sweeps))
+    ko = _keff_opts(tol_k, -1.0, eps_round, eps_solve, max_outer, rmax, max_sweeps, restart, max_restarts, matvec,
+                    mv_max_sweeps)
     o = _lib.alpha_opts(float(alpha0), float(alpha1), float(tol), float(eps_op), int(max_alpha), ko)
     dev = psi.device
     a = torch.zeros(1, dtype=torch.float64, device=dev)

@@ -17,7 +17,8 @@ def declared_functions():
 
 
 def test_library_builds_and_exports_all_declared_symbols():
-    from paper_2309_03347_b200 import build
+    from __graft_entry__ import _build_module
+    build = _build_module()
     lib_path = build.build()
     lib = C.CDLL(lib_path)
     names = declared_functions()

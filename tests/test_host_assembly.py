@@ -11,7 +11,8 @@ from oracle import tt as ott
 
 @pytest.fixture(scope="module")
 def gtr():
-    from paper_2309_03347_b200 import build
+    from __graft_entry__ import _build_module
+    build = _build_module()
     build.build()
     from paper_2309_03347_b200 import transport
     return transport

@@ -17,6 +17,9 @@ cfg = sys.argv[1] if len(sys.argv) > 1 else "c1"
 outer = int(sys.argv[2]) if len(sys.argv) > 2 else 30
 if cfg == "c1":
     p, rmax, kw = inputs.problem_c1(), 64, dict(tol_k=1e-12, eps_round=1e-13, eps_solve=1e-12)
+elif cfg == "c4":
+    p, rmax, kw = inputs.problem_c4(), 128, dict(tol_k=1e-14, eps_round=1e-6, eps_solve=1e-6, max_sweeps=4,
+                                                 mv_max_sweeps=4, max_restarts=20)
 else:
     p, rmax, kw = inputs.problem_c3(), 64, dict(tol_k=1e-14, eps_round=1e-6, eps_solve=1e-6, max_sweeps=4,
                                                 mv_max_sweeps=4, max_restarts=20)
@@ -36,7 +39,8 @@ def solve():
 
 
 solve()
-solve()
+if cfg != "c4":
+    solve()
 lc = C.CDLL(os.path.join(os.path.dirname(tb.__file__), "liblaunchcount.so"))
 lc.lc_start()
 r = solve()
