@@ -1,22 +1,24 @@
 """Benchmark of the B200 hot path of arXiv 2309.03347 (TT/QTT k-eigenvalue).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c1|c2|c3|c5]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c4|c1|c2|c3|c5]
                     [--impl ours|reference]
 
-A step is one pass of the whole hot path over one
-synthetic problem: one complete k-eff fixed-point solve (eqn:TT_k_eff_fixed_
-points) from psi_0 = 1, k_0 = 1 to |dk| < tol: every iteration
-forms B = (S + F/k) psi by the fit-based product amen_mv (the paper's choice,
-P:1501-1506; TT_BENCH_MATVEC=exact selects exact products + rounding), runs
-the AMEn solve of H psi' = B (local apply, interfaces, GMRES, enrichment) and
-the k update.
-`value` = k-eff fixed-point iterations per second over all ranks (replicas,
-weak scaling: every rank solves its own copy, no data-path collective —
-DESIGN.md "Multi-GPU").  The contraction GFLOP/s (% of the measured FP64 DMMA
-peak) is reported beside it, and `roofline` gives the dominant kernel.
-The c2 / c5 workloads are the matvec+round and ALS sweep microbenchmarks; c3
-is configs[2] (64^3 QTT, G=7, 80 ordinates, rmax 64, eps 1e-6) with B formed
-by amen_mv, a step being --outer fixed-point iterations from psi_0 = 1.
+Default workload: BASELINE.json configs[3] (C4: 256^3 QTT, G=30 with upscatter,
+S16 288 ordinates, three regions, eps 1e-6, rmax 128) -- the largest
+single-GPU config, on which the metric's "k-eff fixed-point iterations/sec" is
+quoted.  A step is ONE fixed-point iteration of eqn:TT_k_eff_fixed_points
+(reading Z36): B = amen_mv((S + F/k), Psi) (the paper's product,
+P:1501-1506), the AMEn solve of H Psi' = B (local applies, interface updates,
+GMRES, truncation, enrichment: every §8(a) row), <f, Psi'>, ||Psi'|| and the k
+update, continuing the solve from the state the previous step left on the
+device (keff_opts.warm).  Untimed settle iterations bring the ranks to rmax
+first, so the timed steps are the steady-state (most expensive) iterations.
+`value` = iterations/s over all ranks (replicas, weak scaling: every rank
+solves its own copy, no data-path collective -- DESIGN.md "Multi-GPU").
+The metric's first half is reported in the same line on its own configs:
+`c5_r256` (configs[4] ALS double sweep, GFLOP/s and % of the FP64 DMMA peak)
+and `c2_b64` (configs[1] 64-instance batched tt_matvec, GB/s and % of HBM).
+--workload c1 / c2 / c3 / c5 time the other configs on their own.
 
 --impl reference times the fp64 CPU oracle (oracle/, the only other place
 bench.py executes it) on a bounded sample of the same workload.
@@ -197,8 +199,9 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--workload", default="c1", choices=["c1", "c2", "c3", "c4", "c5"])
-    ap.add_argument("--outer", type=int, default=30, help="c3: fixed-point iterations per step")
+    ap.add_argument("--workload", default="c4", choices=["c1", "c2", "c3", "c4", "c5"])
+    ap.add_argument("--settle", type=int, default=None, help="c3/c4: untimed iterations before the warm-up")
+    ap.add_argument("--no-extras", action="store_true", help="c4: skip the c5_r256 / c2_b64 keys")
     ap.add_argument("--rank", type=int, default=128, help="c5 interface rank (64, 128, 256)")
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-graph", action="store_true", help="c5: launch the sweep without a CUDA graph")
@@ -206,12 +209,34 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
 
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # not under torchrun: launch N ranks (one process per GPU) ourselves
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", "--master-port", os.environ.get("MASTER_PORT", "29531"),
+               os.path.abspath(__file__)] + sys.argv[1:]
+        sys.exit(subprocess.call(cmd))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
 
     if args.impl == "reference":
         if rank != 0:
+            return
+        if args.workload == "c4":
+            vals, cb = [], None
+            for _ in range(max(1, min(args.steps, 3))):
+                cb = cpu_baseline("c4")
+                vals.append(cb["value"])
+            val = statistics.median(vals)
+            cb["value"] = val
+            line = {"impl": "reference", "metric": METRIC, "value": val, "unit": "iter/s", "n_gpus": args.gpus,
+                    "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 / val, "higher_is_better": True,
+                    "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                    "config": {"workload": KEFF_CFG["c4"]["label"] + ", rmax 128, eps 1e-6, B by amen_mv; step = one "
+                                           "k-eff fixed-point iteration (oracle estimate, see cpu_baseline.sample)"},
+                    "cpu_baseline": cb,
+                    "e2e": {"value": val, "unit": "iter/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+            print(json.dumps(line))
             return
         v, dt = oracle_c1_sample(iters=max(1, min(args.steps, 5)))
         vals = [v]
@@ -242,8 +267,15 @@ def main():
     import ctypes as C
 
     if args.workload in ("c2", "c3", "c4", "c5"):
-        line = c3_bench(args, tb, device, world, dist) if args.workload in ("c3", "c4") else \
-            micro_bench(args, tb, device, world, dist)
+        if args.workload in ("c3", "c4"):
+            line = keff_bench(args, tb, device, world, dist, rank)
+            if args.workload == "c4" and not args.no_extras:
+                line.update(extras(args, tb, device, world))
+            if rank == 0 and not args.no_cpu_baseline:
+                line["cpu_baseline"] = cpu_baseline(args.workload, line.get("arnoldi_steps_per_core_per_step"),
+                                                    line.get("psi_ranks"))
+        else:
+            line = micro_bench(args, tb, device, world, dist)
         if rank == 0:
             print(json.dumps(line))
         if dist:
@@ -491,111 +523,328 @@ def micro_bench(args, tb, device, world, dist):
             "gpu_launches_how": "libtt kernels of one more matvec + copy + round (CUPTI activity records)"}
 
 
-def c3_bench(args, tb, device, world, dist):
-    """configs[2]: k-eff fixed point on the 64^3 two-region problem (QTT space,
-    G=7, S8 80 ordinates), rmax 64, eps 1e-6, B = amen_mv((S + F/k), Psi).
-    A step = args.outer iterations from psi_0 = 1, k_0 = 1 (the iteration does
-    not reach |dk| <= 1e-6 once rmax binds: the full-grid solution is not low
-    rank, so the count is fixed).  value = iterations/s; k is compared with the
-    oracle's matrix-free truth (tests/golden/c3_keff.txt) when present."""
+KEFF_CFG = {
+    "c3": dict(rmax=64, label="C3 (configs[2]): 64^3 QTT (6 bits/axis), G=7 downscatter, S8 LS-style (80), two regions"),
+    "c4": dict(rmax=128, label="C4 (configs[3]): 256^3 QTT (8 bits/axis), G=30 (upscatter 26-30), S16 LS-style (288), "
+                               "core/blanket/reflector"),
+}
+KEFF_OPTS = dict(tol_k=0.0, eps_round=1e-6, eps_solve=1e-6, matvec="amen_mv", max_sweeps=4, mv_max_sweeps=4,
+                 restart=40, max_restarts=20)
+
+
+def keff_bench(args, tb, device, world, dist, rank):
+    """configs[3] (C4, the default) / configs[2] (C3): the k-eff fixed point
+     with B = amen_mv((S + F/k), Psi) and AMEn solves of
+    H Psi' = B, eps 1e-6, rmax 128 / 64.  A step is ONE fixed-point iteration
+    (reading Z36: the B product, the AMEn solve run to its sweep limit, the
+    <f, Psi'> / norm / k update), continuing the solve: `--settle` untimed
+    iterations from psi_0 = 1, k_0 = 1 bring the ranks to rmax first (the
+    steady state, the most expensive iterations), then W warm-up steps, then
+    K timed steps; each step is one keff_fixed_point call with max_outer = 1
+    and keff_opts.warm = 1 (psi, k, the amen_mv guess and the AMEn z0 carried
+    over on the device, include/tt.h)."""
     import torch
     import inputs
     from paper_2309_03347_b200 import transport as gtr
     from paper_2309_03347_b200 import _lib
     import ctypes as C
     pk = peaks()
-    c4 = args.workload == "c4"
-    prob = inputs.problem_c4() if c4 else inputs.problem_c3()
+    cfg = KEFF_CFG[args.workload]
+    t_setup = time.perf_counter()
+    prob = inputs.problem_c4() if args.workload == "c4" else inputs.problem_c3()
     ops = gtr.operators(prob, eps=1e-12, device=device)
     modes = gtr.modes(prob)
     d = len(modes)
-    rmax, kick = (128 if c4 else 64), 4
+    rmax, kick = cfg["rmax"], 4
     g = inputs.rng(61)
     z0 = inputs.random_tt(g, modes, [1] + [kick] * (d - 1) + [1])
     cap = [1] + [rmax + kick] * (d - 1) + [1]
-    psi_init = tb.TTVec.from_cores([np.ones((1, n, 1)) for n in modes], rcap=cap, device=device)
     psi = tb.TTVec.from_cores([np.ones((1, n, 1)) for n in modes], rcap=cap, device=device)
-    z_init = tb.TTVec.from_cores(z0, device=device)
     z = tb.TTVec.from_cores(z0, device=device)
-    opts = dict(tol_k=1e-14, eps_round=1e-6, eps_solve=1e-6, rmax=rmax, max_outer=args.outer, matvec="amen_mv",
-                max_sweeps=4, mv_max_sweeps=4, restart=40, max_restarts=20)
-    flush = torch.empty(256 * 1024 * 1024 // 8, dtype=torch.float64, device=device)
-    s = torch.cuda.current_stream()
-
-    def step():
-        tb.tt_copy(psi_init, psi)
-        tb.tt_copy(z_init, z)
-        return tb.keff_fixed_point(ops["H"], ops["S"], ops["F"], psi, z, **opts)
-
-    for _ in range(args.warmup):
-        step()
+    opts = dict(KEFF_OPTS, rmax=rmax)
     torch.cuda.synchronize()
+    t_asm = time.perf_counter() - t_setup
+    nb = tb.keff_workspace_bytes(ops["H"], ops["S"], ops["F"], psi, z, rmax=rmax, matvec=opts["matvec"],
+                                 restart=opts["restart"])
+    ws = torch.empty(nb, dtype=torch.uint8, device=device)
+    state = {"k": 1.0, "warm": False}
+
+    def step(n=1):
+        r = tb.keff_fixed_point(ops["H"], ops["S"], ops["F"], psi, z, k0=state["k"], max_outer=n,
+                                warm=state["warm"], ws=ws, **opts)
+        state["warm"] = True
+        return r
+
+    settle = args.settle if args.settle is not None else 8
+    r = step(settle)
+    state["k"] = r.k.item()
+    settle_hist = r.k_hist[:settle].cpu().tolist()
+    for _ in range(args.warmup):
+        r = step()
+        state["k"] = r.k.item()
+    torch.cuda.synchronize()
+    ranks_before = psi.ranks()
+    flush = torch.empty(256 * 1024 * 1024 // 8, dtype=torch.float64, device=device)   # > 126 MB L2
     cnt = (C.c_uint64 * 5)()
     lib = _lib.lib()
     lib.tt_counters(cnt, 1)
     fl, fms, ffl = C.c_int64(0), C.c_double(0.0), (C.c_double * 3)()
     lib.tt_fused_profile_read(C.byref(fl), C.byref(fms), ffl)
     lib.tt_fused_profile(1)
-    ms, iters, ks = [], 0, []
-    with ClockSampler(torch.cuda.current_device()) as clk:
+    s = torch.cuda.current_stream()
+    ms, ks, sweeps = [], [], []
+    with ClockSampler(local_index(device)) as clk:
         if dist:
             dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
         for _ in range(args.steps):
-            flush.fill_(1.0)
+            flush.fill_(1.0)                          # evict L2 between timed steps (untimed)
             e0, e1 = _events()
             e0.record(s)
-            res = step()
+            r = step()
             e1.record(s)
             e1.synchronize()
             ms.append(e0.elapsed_time(e1))
-            iters += int(res.iters.item())
-            ks.append(res.k.item())
+            state["k"] = r.k.item()
+            ks.append(state["k"])
+            sweeps.append(int(r.sweeps_hist[0].item()))
+        torch.cuda.synchronize()
         if dist:
             dist.barrier()
+        wall = time.perf_counter() - t0
     lib.tt_counters(cnt, 1)
+    cms, cst, cl = (C.c_double * 64)(), (C.c_double * 64)(), (C.c_int64 * 64)()
+    lib.tt_fused_profile_cores(cms, cst, cl)
     lib.tt_fused_profile_read(C.byref(fl), C.byref(fms), ffl)
     lib.tt_fused_profile(0)
+    steps_per_core = [cst[t] / args.steps for t in range(d)]
     dev_ms = sum(ms)
-    dev_max, iters_all = aggregate_ranks(dev_ms, iters, dist, device)
+    dev_max, iters_all = aggregate_ranks(dev_ms, args.steps, dist, device)
     gemm_flops, mv_flops, qr_flops, svd_flops, ngemm = [int(v) for v in cnt]
     gfl = (gemm_flops + mv_flops) / (dev_ms * 1e-3) / 1e9
-    truth = None
-    gold = os.path.join(ROOT, "tests", "golden", "c3_keff.txt")
-    if os.path.exists(gold) and not c4:
-        for l in open(gold):
-            if l.strip() and not l.startswith("#") and l.split()[0] == "64":
-                truth = float(l.split()[1])
-    chain = dominant_gemm_roofline(tb, device, pk, shape=(68, 60, 68, 2, 2, 68, 60, 68),
-                                   label="C3 local shape r=68 R=60 n=2") if not c4 else \
-        dominant_gemm_roofline(tb, device, pk, shape=(132, 84, 132, 2, 2, 132, 84, 132),
-                               label="C4 local shape r=132 R=84 n=2")
     ff = ffl[0] + ffl[1]
     ach = ff / (fms.value * 1e-3) / 1e12 if fms.value > 0 else None
-    roof = {"kernel": "gm_chunk_kernel (fused GMRES Arnoldi steps, cluster / cooperative-grid variants)",
-            "bound": "tensor", "achieved": ach, "peak": pk["dmma_gflops"] / 1e3, "unit": "TFLOP/s",
-            "frac": (ach / (pk["dmma_gflops"] / 1e3)) if ach else None,
-            "peak_src": "measured FP64 DMMA sustained (tools/peaks_fp64)", "traffic": None,
+    dm = pk["dmma_gflops"] / 1e3
+    roof = {"kernel": "gm_chunk_kernel (fused GMRES of the AMEn local systems: local-apply DMMA GEMM stages + "
+                      "Gram-Schmidt + Givens, one persistent launch per local solve)",
+            "bound": "tensor", "achieved": ach, "peak": dm, "unit": "TFLOP/s",
+            "frac": (ach / dm) if ach else None, "peak_src": pk["dmma_src"],
+            "traffic": ncu_traffic("gm_chunk_kernel", args.workload),
             "launches": fl.value, "ms_per_launch": fms.value / max(fl.value, 1),
-            "flops_per_launch": ff / max(fl.value, 1), "arnoldi_steps": ffl[2],
+            "flops_per_launch": ff / max(fl.value, 1), "arnoldi_steps_per_step": ffl[2] / args.steps,
             "share_of_step_time": fms.value / dev_ms if dev_ms > 0 else None,
-            "gemm_chain_alone": chain}
-    return {"metric": METRIC, "value": iters_all / (dev_max * 1e-3), "unit": "iter/s", "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": dev_max / args.steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": (f"C4 (configs[3]): 256^3 QTT, G=30 (upscatter 26-30), S16 (288), three regions, "
-                                    if c4 else "C3 (configs[2]): 64^3 QTT, G=7, S8 (80), two regions, ") +
-                                   f"rmax {rmax}, eps 1e-6, B by amen_mv; step = {args.outer} fixed-point "
-                                   "iterations from psi_0 = 1",
-                       "l2": "256 MB flush between timed steps", "parallelism": f"replicas x{world}"},
-            "k_last": ks[-1], "k_truth_matrix_free": truth,
-            "k_rel_discrepancy": (abs(ks[-1] - truth) / truth) if truth else None,
-            "psi_ranks": psi.ranks(), "operator_ranks": {k: v.ranks() for k, v in ops.items()},
-            "contraction_gflops": gfl, "contraction_pct_dmma_peak": 100.0 * gfl / pk["dmma_gflops"],
-            "flops_per_step": {"gemm": gemm_flops / args.steps, "qr": qr_flops / args.steps,
-                               "jacobi": svd_flops / args.steps, "gemm_calls": ngemm / args.steps},
-            "roofline": roof, "clocks": clk.summary(),
-            "gpu_launches": (count_kernels(step) or (count_launches_estimate(ngemm / args.steps, 0), 0))[0],
-            "gpu_launches_how": "libtt kernels of one more identical step (CUPTI activity records)"}
+            "how": "flops = the local-apply GEMM flops (diagonal operator cores counted at their structured cost) "
+                   "+ Gram-Schmidt/normalisation vector flops, counted on the device; time = CUDA events around "
+                   "every launch inside the timed region (tt_fused_profile)"}
+    res = {"metric": METRIC, "value": iters_all / (dev_max * 1e-3), "unit": "iter/s", "n_gpus": world,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": dev_max / args.steps,
+           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "config": {"workload": cfg["label"] + f", rmax {rmax}, eps 1e-6, B by amen_mv, AMEn <= 4 sweeps, "
+                                  f"GMRES(40); step = one k-eff fixed-point iteration continuing the solve after "
+                                  f"{settle} settle + {args.warmup} warm-up iterations from psi_0 = 1, k_0 = 1",
+                      "l2": "256 MB flush between timed steps", "parallelism": f"replicas x{world}"},
+           "k_after_settle": settle_hist[-1] if settle_hist else None, "k_last": ks[-1], "k_steps": ks,
+           "sweeps_per_step": sweeps, "psi_ranks": psi.ranks(), "psi_ranks_before_timing": ranks_before,
+           "operator_ranks": {k: v.ranks() for k, v in ops.items()},
+           "contraction_gflops": gfl, "contraction_pct_dmma_peak": 100.0 * gfl / pk["dmma_gflops"],
+           "flops_per_step": {"gemm": gemm_flops / args.steps, "qr": qr_flops / args.steps,
+                              "jacobi": svd_flops / args.steps, "gemm_calls": ngemm / args.steps},
+           "arnoldi_steps_per_core_per_step": steps_per_core,
+           "roofline": roof, "clocks": clk.summary(), "wall_s": wall, "setup_s": t_asm}
+    kc = count_kernels(step)
+    res["gpu_launches"] = kc[0] if kc else None
+    res["gpu_launches_how"] = "libtt kernels of one more identical step (CUPTI activity records)"
+    if kc:
+        res["gpu_launches_all_kernels"] = kc[1]
+    res["e2e"] = e2e_keff(tb, ops, psi, z, state, opts, ws, args.steps)
+    if args.workload == "c3":
+        gold = os.path.join(ROOT, "tests", "golden", "c3_keff.txt")
+        for line in open(gold):
+            if line.strip() and not line.startswith("#") and line.split()[0] == "64":
+                res["k_truth_matrix_free"] = float(line.split()[1])
+                res["k_rel_discrepancy"] = abs(ks[-1] - res["k_truth_matrix_free"]) / res["k_truth_matrix_free"]
+    return res
+
+
+def e2e_keff(tb, ops, psi, z, state, opts, ws, steps):
+    """The same metric through the public API with HOST buffers: every step copies
+    the operator cores (H, S, F) and the current psi from pinned host memory,
+    runs one fixed-point iteration (keff_fixed_point, max_outer = 1, a fresh
+    call: psi re-rounded, the amen_mv guess restarted from psi) and reads psi
+    and k back into pinned host memory."""
+    import torch
+    host = {k: v.data.cpu().pin_memory() for k, v in ops.items()}
+    hpsi = psi.data.cpu().pin_memory()
+    hr = psi.r_dev.cpu().pin_memory()
+    hz, hzr = z.data.cpu().pin_memory(), z.r_dev.cpu().pin_memory()
+    out_psi = torch.empty_like(hpsi).pin_memory()
+    out_k = torch.empty(1, dtype=torch.float64).pin_memory()
+    s = torch.cuda.current_stream()
+    e0, e1 = _events()
+    torch.cuda.synchronize()
+    e0.record(s)
+    k = state["k"]
+    for _ in range(steps):
+        for key, v in ops.items():
+            v.data.copy_(host[key], non_blocking=True)
+        psi.data.copy_(hpsi, non_blocking=True)
+        psi.r_dev.copy_(hr, non_blocking=True)
+        z.data.copy_(hz, non_blocking=True)
+        z.r_dev.copy_(hzr, non_blocking=True)
+        r = tb.keff_fixed_point(ops["H"], ops["S"], ops["F"], psi, z, k0=k, max_outer=1, warm=False, ws=ws, **opts)
+        out_psi.copy_(psi.data, non_blocking=True)
+        out_k.copy_(r.k, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        k = float(out_k[0])
+    e1.record(s)
+    e1.synchronize()
+    ms = e0.elapsed_time(e1)
+    h2d = sum(int(v.numel()) * 8 for v in host.values()) + int(hpsi.numel() + hz.numel()) * 8 + \
+        int(hr.numel() + hzr.numel()) * 4
+    return {"value": steps / (ms * 1e-3), "unit": "iter/s", "h2d_bytes_per_step": h2d,
+            "d2h_bytes_per_step": int(out_psi.numel()) * 8 + 8,
+            "how": "per step: H, S, F cores + psi + z host->device (pinned), one keff_fixed_point iteration (fresh "
+                   "call), psi + k device->host"}
+
+
+def extras(args, tb, device, world):
+    """The metric's first half on its own configs, in the same run: C5 (configs[4])
+    ALS double sweep at r = 256 (GFLOP/s, % of the FP64 DMMA peak) and the C2
+    (configs[1]) 64-instance batched tt_matvec (GB/s, % of the measured HBM
+    copy bandwidth)."""
+    import copy
+    out = {}
+    a = copy.copy(args)
+    a.workload, a.rank, a.no_graph = "c5", 256, False
+    a.steps, a.warmup = max(5, min(args.steps, 10)), 3
+    l5 = micro_bench(a, tb, device, world, None)
+    out["c5_r256"] = {"value": l5["value"], "unit": l5["unit"], "pct_dmma_peak": l5["pct_dmma_peak"],
+                      "ms_per_sweep": l5["ms_per_step"], "flops_per_sweep": l5["flops_per_step"],
+                      "config": l5["config"]["workload"], "gpu_launches": l5["gpu_launches"]}
+    a.workload, a.steps = "c2", max(5, min(args.steps, 10))
+    l2 = micro_bench(a, tb, device, world, None)
+    rf = l2["roofline"]
+    out["c2_b64"] = {"value": rf["achieved"], "unit": "GB/s", "pct_hbm_measured": 100.0 * rf["frac"],
+                     "pct_8tbs_nominal": 100.0 * rf["achieved"] / 8000.0, "ms_per_launch": l2["matvec_b64_ms"],
+                     "bytes_per_launch": rf["bytes_per_launch"], "peak_src": rf["peak_src"],
+                     "config": "C2 (configs[1]) 64 independent d=30 instances (seeds 0-63), one tt_matvec_batched "
+                               "launch", "b1_matvec_plus_round_instances_per_s": l2["value"],
+                     "b1_round_ms": l2["round_ms"]}
+    return out
+
+
+def host_info():
+    info = {"nproc": os.cpu_count()}
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                info["cpu_model"] = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    try:
+        import threadpoolctl
+        info["blas"] = [{"api": i.get("internal_api"), "lib": os.path.basename(i.get("filepath", "")),
+                         "threads": i.get("num_threads")} for i in threadpoolctl.threadpool_info()]
+    except Exception:
+        pass
+    return info
+
+
+def c4_shapes(ranks=None):
+    """The C4 steady-state local-system shapes: psi ranks at rmax 128 (+ kickrank 4)
+    bounded by the mode products from each end, operator ranks of H (PROBE,
+    bench runs: H [1,4,6,...,84,36,4,1])."""
+    import inputs
+    modes = [2] * 24 + [288, 30]
+    d = len(modes)
+    if ranks is None:
+        ranks = [1] + [int(min(132.0, np.prod(modes[:k], dtype=float), np.prod(modes[k:], dtype=float)))
+                       for k in range(1, d)] + [1]
+    RH = [1, 4, 6, 6, 6, 6, 8, 11, 7, 25, 34, 34, 34, 34, 36, 38, 16, 56, 76, 76, 76, 76, 80, 84, 36, 4, 1]
+    return modes, ranks, RH
+
+
+# Arnoldi steps per core per C4 fixed-point iteration in the steady state (GPU
+# run, tools/probe_c4.py 8 3, round 2); used when no live GPU counts exist (the
+# reference arm)
+C4_STEPS_PER_CORE = [6.7, 15.0, 25.0, 40.7, 81.0, 156.0, 350.0, 553.0, 1338.0, 345.3, 303.3, 307.3, 313.3, 324.7,
+                     362.3, 308.0, 309.7, 328.3, 314.7, 316.0, 317.7, 309.0, 280.3, 204.0, 105.0, 0.0]
+
+
+def oracle_apply_sample(steps_per_core=None, ranks=None, budget_s=10.0):
+    """Bounded sample of the C4 workload on the CPU oracle: one oracle a6 local
+    apply (oracle.tt.local_apply, the operation behind every Arnoldi step of
+    the AMEn local solves, ~98% of an iteration's flops) at each of the 26
+    C4 core shapes of the steady state (psi ranks <= 132, H's ranks), seeded
+    Gaussian operands.  The oracle's time per fixed-point iteration is
+    estimated as sum_k (Arnoldi steps at core k per iteration) x t_apply(k),
+    with the per-core step counts of the GPU's timed iterations (or 300 per
+    core if not given): QR, SVD, Gram-Schmidt and amen_mv are left out, so
+    this OVERSTATES the oracle's iterations/s."""
+    import inputs
+    from oracle import tt as ott
+    modes, r, RH = c4_shapes(ranks)
+    d = len(modes)
+    g = inputs.rng(77)
+    ops = []
+    for k in range(d):
+        n = modes[k]
+        ops.append((g.standard_normal((r[k], RH[k], r[k])), g.standard_normal((RH[k], n, n, RH[k + 1])),
+                    g.standard_normal((r[k + 1], RH[k + 1], r[k + 1])), g.standard_normal((r[k], n, r[k + 1]))))
+    times = [[] for _ in range(d)]
+    t0 = time.perf_counter()
+    while True:    # whole passes over the 26 shapes until the CPU budget is spent (median per shape)
+        for k in range(d):
+            t = time.perf_counter()
+            ott.local_apply(*ops[k])
+            times[k].append(time.perf_counter() - t)
+        if time.perf_counter() - t0 >= budget_s:
+            break
+    sample_s = time.perf_counter() - t0
+    t_core = [statistics.median(v) for v in times]
+    spc = steps_per_core if steps_per_core else C4_STEPS_PER_CORE
+    t_iter = sum(a * b for a, b in zip(spc, t_core))
+    return 1.0 / t_iter, t_iter, sample_s, t_core
+
+
+def cpu_baseline(workload, steps_per_core=None, ranks=None):
+    if workload != "c4":
+        return None
+    hi = host_info()
+    v, t_iter, sample_s, t_core = oracle_apply_sample(steps_per_core, ranks)
+    out = {"value": v, "unit": "iter/s", "cores": cpu_cores(), "kind": "oracle",
+           "sample": (f"oracle a6 local applies (oracle.tt.local_apply) at each of the 26 C4 steady-state core "
+                      f"shapes, repeated passes for {sample_s:.1f} s of CPU work (median per shape), scaled to one fixed-point iteration by the Arnoldi "
+                      f"steps per core of the GPU's timed iterations ({t_iter:.1f} s per iteration); QR, SVD, "
+                      f"Gram-Schmidt and amen_mv left out, so this overstates the oracle's rate"),
+           "host": hi, "t_apply_per_core_s": t_core}
+    try:   # the same sample on one thread
+        import threadpoolctl
+        with threadpoolctl.threadpool_limits(1):
+            v1, t1, s1, _ = oracle_apply_sample(steps_per_core, ranks, budget_s=5.0)
+        out["value_1thread"] = v1
+        out["sample_1thread_s"] = s1
+    except Exception as e:
+        out["value_1thread"] = None
+        out["note_1thread"] = repr(e)[:200]
+    return out
+
+
+def local_index(device):
+    return device.index if getattr(device, "index", None) is not None else 0
+
+
+def ncu_traffic(kernel, workload):
+    """dram__bytes_read.sum + dram__bytes_write.sum of one launch of `kernel` from
+    the committed ncu --set full capture (profiles/r02/ncu_traffic.json), with
+    that launch's algorithmic flops for comparison; None if not captured."""
+    path = os.path.join(ROOT, "profiles", "r02", "ncu_traffic.json")
+    try:
+        return json.load(open(path))[workload][kernel]
+    except Exception:
+        return None
 
 
 def count_launches_estimate(gemm_calls, iters):

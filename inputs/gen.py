@@ -188,19 +188,24 @@ def problem_c3(seed: int = 3, nv: int = 64):
     }
 
 
-def problem_c4(seed: int = 4):
+def problem_c4(seed: int = 4, nv: int = 256):
     """BASELINE.json configs[3]: 256 vertices/axis, G=30 with upscatter in groups
-    26-30 (1-based), S16 LS-style (288), core/blanket/reflector (Z13)."""
+    26-30 (1-based), S16 LS-style (288), core/blanket/reflector (Z13).
+    nv < 256 gives the same materials on a coarser grid (blanket cells
+    [nv/8, 7nv/8)^3, core [nv/4, 3nv/4)^3), used for parity at sizes the
+    oracle's matrix-free sweep finishes quickly."""
     g = rng(seed)
     G = 30
     refl = _draw_material(g, G, fissile=False, upscatter_from=26)
     blanket = _draw_material(g, G, fissile=True, upscatter_from=26)
     core = _draw_material(g, G, fissile=True, upscatter_from=26)
     chi = np.zeros(G); chi[0] = 0.7; chi[1] = 0.3
+    b0, b1, c0, c1 = nv // 8, 7 * nv // 8, nv // 4, 3 * nv // 4
     return {
-        "name": "C4", "nv": 256, "extent": 10.0, "G": G, "quad": quadrature_ls_style(16),
+        "name": "C4" if nv == 256 else f"C4-nv{nv}", "nv": nv, "extent": 10.0, "G": G,
+        "quad": quadrature_ls_style(16),
         "boundary": "vacuum", "qtt": True, "materials": [refl, blanket, core], "chi": chi,
-        "boxes": [((32, 32, 32), (224, 224, 224), 1), ((64, 64, 64), (192, 192, 192), 2)],
+        "boxes": [((b0,) * 3, (b1,) * 3, 1), ((c0,) * 3, (c1,) * 3, 2)],
         "seed": seed, "inv_v": inv_velocity(G),
     }
 

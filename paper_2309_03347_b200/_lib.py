@@ -41,7 +41,8 @@ class keff_opts(C.Structure):
     _fields_ = [("tol_k", C.c_double), ("tol_res", C.c_double), ("eps_round", C.c_double),
                 ("eps_solve", C.c_double), ("max_outer", C.c_int32), ("rmax", C.c_int32), ("max_sweeps", C.c_int32),
                 ("kickrank", C.c_int32), ("gmres_restart", C.c_int32), ("gmres_max_restarts", C.c_int32),
-                ("local_dense_max", C.c_int32), ("matvec", C.c_int32), ("mv_max_sweeps", C.c_int32)]
+                ("local_dense_max", C.c_int32), ("matvec", C.c_int32), ("mv_max_sweeps", C.c_int32),
+                ("warm", C.c_int32)]
 
 
 class keff_report(C.Structure):

@@ -279,10 +279,12 @@ tt_status keff_meta(const MatMeta &H, const MatMeta &S, const MatMeta &F, const 
   ones_kernel<<<d, 256, 0, s>>>(W.ones);
   TT_TRY(matvec_meta(W.FT, W.ones, W.f, s));
   { Arena a = sub(); TT_TRY(round_meta(W.f, 1e-14, 1 << 30, nullptr, nullptr, 0, a, s)); }
-  // keep the AMEn residual TT's initial cores (the oracle restarts every solve from z0)
-  TT_TRY(copy_meta(z, W.z0, s));
+  // keep the AMEn residual TT's initial cores (the oracle restarts every solve from z0);
+  // a warm call continues the previous one: z0 and the amen_mv guess of B are
+  // still in the workspace and psi is already a rounded, normalised iterate
+  if (!o.warm) TT_TRY(copy_meta(z, W.z0, s));
   // Psi <- round(Psi0) / ||.||   (Z16, Z17)
-  { Arena a = sub(); TT_TRY(round_meta(psi, o.eps_round, o.rmax, nullptr, nullptr, 0, a, s)); }
+  if (!o.warm) { Arena a = sub(); TT_TRY(round_meta(psi, o.eps_round, o.rmax, nullptr, nullptr, 0, a, s)); }
   { Arena a = sub(); TT_TRY(orth_meta(psi, -1, W.nrm, a, s)); }
   keff_init_kernel<<<1, 1, 0, s>>>(W.sc, k0, k0_dev, W.nrm);
   TT_TRY(scale_meta(psi, &W.sc->nrm_inv, 1.0, 0, s));
@@ -314,7 +316,7 @@ tt_status keff_meta(const MatMeta &H, const MatMeta &S, const MatMeta &F, const 
   };
   if (rep.res_dev) cudaMemsetAsync(rep.res_dev, 0xff, sizeof(double), s);   // NaN pattern until evaluated
   if (rep.res_hist_dev && rep.hist_cap > 0) fill_kernel<<<1, 256, 0, s>>>(rep.res_hist_dev, rep.hist_cap, -1.0);
-  if (mv) TT_TRY(copy_meta(psi, W.B, s));   // first amen_mv guess: Psi_0
+  if (mv && !o.warm) TT_TRY(copy_meta(psi, W.B, s));   // first amen_mv guess: Psi_0
   for (int it = 0; it < o.max_outer; ++it) {
     if (!mv) {
       TT_TRY(matvec_meta(S, psi, W.SP, s));

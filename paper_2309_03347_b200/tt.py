@@ -351,21 +351,25 @@ class KeffResult:
 
 
 def _keff_opts(tol_k, tol_res, eps_round, eps_solve, max_outer, rmax, max_sweeps, restart, max_restarts, matvec,
-               mv_max_sweeps):
+               mv_max_sweeps, warm=False):
     return _lib.keff_opts(float(tol_k), float(tol_res), float(eps_round), float(eps_solve), int(max_outer),
                           int(min(rmax, 2**30)), int(max_sweeps), 0, int(restart), int(max_restarts), 0, _MV[matvec],
-                          int(mv_max_sweeps))
+                          int(mv_max_sweeps), int(bool(warm)))
 
 
 def keff_fixed_point(H: TTMat, S: TTMat, F: TTMat, psi: TTVec, z: TTVec, k0: float = 1.0, tol_k: float = 1e-10,
                      eps_round: float = 1e-12, eps_solve: float = 1e-11, max_outer: int = 200, rmax: int = 1 << 20,
                      max_sweeps: int = 20, restart: int = 40, max_restarts: int = 50, hist_cap: int = 256,
-                     matvec: str = "exact", mv_max_sweeps: int = 10, tol_res: float = -1.0, stream=None) -> KeffResult:
+                     matvec: str = "exact", mv_max_sweeps: int = 10, tol_res: float = -1.0, warm: bool = False,
+                     ws: Optional[torch.Tensor] = None, stream=None) -> KeffResult:
     """matvec: "exact" (exact products + rounding) or "amen_mv" (fit-based product, NEXT-1).
     tol_res > 0: fixed-point residual every iteration, required for convergence;
-    0: evaluated once at the end; < 0: not evaluated."""
+    0: evaluated once at the end; < 0: not evaluated.  warm: continue the previous
+    call with the same operators and options (keff_opts.warm, include/tt.h); a warm
+    call needs the workspace of that call: pass a dedicated uint8 tensor `ws`
+    (keff_workspace_bytes) to both."""
     o = _keff_opts(tol_k, tol_res, eps_round, eps_solve, max_outer, rmax, max_sweeps, restart, max_restarts, matvec,
-                   mv_max_sweeps)
+                   mv_max_sweeps, warm)
     dev = psi.device
     k = torch.zeros(1, dtype=torch.float64, device=dev)
     iters = torch.zeros(1, dtype=torch.int32, device=dev)
@@ -381,10 +385,19 @@ def keff_fixed_point(H: TTMat, S: TTMat, F: TTMat, psi: TTVec, z: TTVec, k0: flo
     if nb == 0:
         check(lib().keff_fixed_point(H.c, S.c, F.c, psi.c, z.c, float(k0), C.byref(o), C.byref(rep), None, 0,
                                      C.c_void_p(_stream(stream))))
-    ws = workspace(nb, dev)
+    if ws is None:
+        ws = workspace(nb, dev)
+    elif ws.numel() < nb:
+        raise ValueError(f"keff_fixed_point: workspace of {ws.numel()} bytes, {nb} needed")
     check(lib().keff_fixed_point(H.c, S.c, F.c, psi.c, z.c, float(k0), C.byref(o), C.byref(rep), _ptr(ws),
                                  ws.numel(), C.c_void_p(_stream(stream))))
     return KeffResult(k, iters, kh, sh, st, rh, ih, res)
+
+
+def keff_workspace_bytes(H: TTMat, S: TTMat, F: TTMat, psi: TTVec, z: TTVec, tol_res: float = -1.0,
+                         rmax: int = 1 << 20, matvec: str = "exact", restart: int = 40) -> int:
+    o = _keff_opts(1e-10, tol_res, 1e-12, 1e-11, 1, rmax, 1, restart, 1, matvec, 1)
+    return int(lib().keff_workspace(H.c, S.c, F.c, psi.c, z.c, C.byref(o)))
 
 
 # -------------------------------------------------------------- NEXT-2 ---

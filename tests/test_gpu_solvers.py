@@ -292,6 +292,27 @@ def test_keff_c3_truncated():
     assert abs(res.k.item() - kt) / kt <= 2e-4
 
 
+def _golden(name, nv):
+    return [float(l.split()[1]) for l in open(os.path.join(GOLD, name))
+            if l.strip() and not l.startswith("#") and l.split()[0] == str(nv)][0]
+
+
+def test_keff_c4_small_grid():
+    """configs[3]'s physics (G=30 with upscatter into groups 26-30, S16 LS-style 288
+    ordinates, core/blanket/reflector) on a 4^3 grid, where rmax does not bind
+    (the QTT bonds are <= 64, the angle|group bond <= 30): the device TT k-eff
+    (B by amen_mv) equals the oracle's matrix-free full-grid sweep iteration
+    (tests/golden/c4_keff.txt, make_c4_keff.py) to 1e-8, with the fixed-point
+    residual ||H Psi - (S + F/k) Psi|| / ||H Psi|| (Z19) required <= 1e-9."""
+    p = inputs.problem_c4(nv=4)
+    kt = _golden("c4_keff.txt", 4)
+    res, _ = _keff_gpu(p, gtr.modes(p), rmax=96, kick=4, tol_k=1e-11, tol_res=1e-9, eps_round=1e-12,
+                       eps_solve=1e-12, matvec="amen_mv", max_sweeps=20)
+    assert res.status.item() == 0
+    assert 0.0 <= res.res.item() <= 1e-9
+    assert abs(res.k.item() - kt) / kt <= 1e-8
+
+
 def _qtt_vec(v, eps=1e-14):
     """QTT cores (bits LSB first, Z28) of a 2^l vector, by the oracle's TT-SVD."""
     l = int(round(np.log2(v.size)))
@@ -370,3 +391,28 @@ def test_keff_deterministic_graphs_on_off():
         assert r.returncode == 0, r.stderr[-2000:]
         outs.append(r.stdout.strip().splitlines()[-1])
     assert outs[0] == outs[1] == outs[2], outs
+
+
+def test_keff_warm_continuation():
+    """keff_opts.warm (the bench's one-iteration step): 1 cold + 5 warm calls of one
+    outer iteration follow the single 6-iteration call's k history (the warm call
+    only re-orthogonalises the already normalised Psi)."""
+    p = small_c1(4)
+    modes = [4, 4, 4, 8, 1]
+    kw = dict(tol_k=0.0, eps_round=1e-10, eps_solve=1e-10, matvec="amen_mv", max_sweeps=6, mv_max_sweeps=6)
+    ref, _ = _keff_gpu(p, modes, rmax=32, max_outer=6, **kw)
+    kref = ref.k_hist[:6].cpu().numpy()
+    ops = gtr.operators(p)
+    g = inputs.rng(61)
+    d = len(modes)
+    psi = tb.TTVec.from_cores([np.ones((1, n, 1)) for n in modes], rcap=[1] + [36] * (d - 1) + [1])
+    z = tb.TTVec.from_cores(inputs.random_tt(g, modes, [1] + [4] * (d - 1) + [1]))
+    nb = tb.keff_workspace_bytes(ops["H"], ops["S"], ops["F"], psi, z, rmax=32, matvec="amen_mv")
+    ws = torch.empty(nb, dtype=torch.uint8, device="cuda")
+    k, ks = 1.0, []
+    for it in range(6):
+        r = tb.keff_fixed_point(ops["H"], ops["S"], ops["F"], psi, z, k0=k, max_outer=1, rmax=32, warm=it > 0,
+                                ws=ws, **kw)
+        k = r.k.item()
+        ks.append(k)
+    assert np.max(np.abs(np.array(ks) - kref) / kref) <= 1e-9, (ks, kref)

@@ -200,13 +200,11 @@ def test_round_c2_d30_rmax128(seed):
     ref, info = ott.tt_round(Yc, 1e-8, 128)
     assert Y.ranks() == ott.ranks(ref)
     s1 = max(s[0] for s in info["sv"])
-    # Z22: rmax binds on most bonds here, so each bond's singular values inherit the
-    # roundoff of every earlier truncated subspace (~20 chained cuts): 2e-12 sigma_1
-    binds = 0
+    # <= 1e-12 sigma_1 at every bond, before and after the bonds
+    # where rmax binds (measured on the B200: <= 6e-15 sigma_1, tools/probe_round_dev.py;
+    # two LAPACK SVD drivers in the oracle differ by <= 5e-15, tools/round_oracle_ab.py)
     for k, s in enumerate(info["sv"]):
-        tol = (1e-12 if binds == 0 else 2e-12) * s1
-        assert np.max(np.abs(sv[k, :len(s)].cpu().numpy() - s)) <= tol
-        binds += int(ott.ranks(ref)[k + 1] < len(s))
+        assert np.max(np.abs(sv[k, :len(s)].cpu().numpy() - s)) <= 1e-12 * s1, k
     nrm = info["norm"]
     # near-ties at the cut make the truncated subspace ill-determined: skip those bonds
     ties = any(r < len(s) and abs(s[r - 1] - s[r]) <= 1e-10 * s1

@@ -168,3 +168,35 @@ def test_keff_tt_amen_mv_matches_dense_small():
     k, psi, hist = so.keff_tt(tops["H"], tops["S"], tops["F"], psi0, _z0(g, modes, 4), tol_k=1e-12,
                               eps_round=1e-13, eps_solve=1e-12, matvec="amen_mv")
     assert abs(k - kd) / kd < 1e-9
+
+
+def test_c4_golden_file_reproduces():
+    """tests/golden/c4_keff.txt was written by make_c4_keff.py (oracle only): its
+    nv = 4 row (configs[3] physics on a 4^3 grid) is recomputed here."""
+    import os
+    path = os.path.join(os.path.dirname(__file__), "golden", "c4_keff.txt")
+    rows = {int(l.split()[0]): float(l.split()[1]) for l in open(path) if l.strip() and not l.startswith("#")}
+    assert set(rows) >= {4, 8}
+    k, _, _ = T.keff_sweep_3d(inputs.problem_c4(nv=4), tol=1e-12)
+    assert abs(k - rows[4]) <= 1e-12
+
+
+def test_keff_sweep_3d_upscatter_three_regions_matches_dense():
+    """The C4 physics the matrix-free sweep iteration carries (three nested regions,
+    upscatter into groups 26-30, Z14) reproduces the dense Kronecker power
+    iteration: configs[3]'s materials restricted to groups 24-30 (so the
+    upscatter block is inside) on a 4^3 grid with S2."""
+    p = inputs.problem_c4(nv=4)
+    sel = np.arange(23, 30)
+    for M in p["materials"]:
+        M["sigma_t"], M["nu_sigma_f"] = M["sigma_t"][sel], M["nu_sigma_f"][sel]
+        M["sigma_s"] = M["sigma_s"][np.ix_(sel, sel)]
+    assert np.count_nonzero(np.triu(p["materials"][2]["sigma_s"], 1)) > 0        # upscatter present
+    p["chi"] = np.full(sel.size, 1.0 / sel.size)
+    p["G"], p["quad"], p["inv_v"] = sel.size, inputs.quadrature_s2(), p["inv_v"][sel]
+    ops = T.dense_operators(p)
+    kd, psid, _ = so.keff_dense_power(ops["H"], ops["S"], ops["F"], tol=1e-13)
+    ks, psis, _ = T.keff_sweep_3d(p, tol=1e-13)
+    assert abs(ks - kd) <= 1e-11 * kd
+    v = psis.reshape(-1)
+    assert np.linalg.norm(v * np.sign(v.sum()) - psid * np.sign(psid.sum())) <= 1e-9
