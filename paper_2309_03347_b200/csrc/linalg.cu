@@ -21,7 +21,6 @@ namespace {
                               // re-measured on the final round-1 code: 1024 vs 512 = C1 103.7 / 103.5, C2 6.32 / 6.24)
 #endif
 constexpr int QR_THREADS = QR_THREADS_DEF;
-constexpr int QR_NQ = (32 * 32 + QR_THREADS - 1) / QR_THREADS;   // (l, c) entries per thread in the reflector
 constexpr int NB = 32;
 // panels of up to QR_PANEL_ROWS rows are factorised in shared memory (the
 // per-column reductions and updates then never touch L2)
@@ -35,118 +34,170 @@ __device__ __forceinline__ double warp_sum(double v) {
 }
 
 
-// Block reflector application on a target matrix X (rows r0.., element (r,c)
-// at X[r*rs + c*cs]):  X[r0:m, cols] -= V * (op(T) * (V^T X[r0:m, cols]))
-// where V = unit lower trapezoidal panel stored in A[:, j0:j0+jb] (lda) with its
-// implicit unit diagonal at row j0+l, and op(T) = T^T (transT = 1) or T.
-// not inlined: one shared copy for the trailing update and the Q formation
-// keeps the kernel's code footprint down (ncu: no_instruction stalls)
-__device__ __noinline__ void apply_block_reflector(int m, int j0, int jb, const double *A, long long lda,
-                                      const double (*sT)[NB + 1], int transT, double *X, long long rs,
-                                      long long cs, int c_begin, int c_end, double (*sV)[NB + 1],
-                                      double (*sX)[NB + 1], double (*sW)[NB + 1], const double *Vsm = nullptr,
-                                      int vld = 0) {
-  const int tid = threadIdx.x;
-  // V element (r, l): from the shared-memory panel copy when given (rows from j0)
-  auto vget = [&](int r, int l) -> double {
-    return Vsm ? Vsm[(r - j0) + (long long)l * vld] : A[r + (long long)(j0 + l) * lda];
+// Block reflector application on a target matrix X (element (r, c) at
+// X[r*rs + c*cs]):  X[j0:m, c] -= V * (op(T) * (V^T X[j0:m, c])) for the
+// columns c in [c_begin, c_end), op(T) = T^T (transT = 1, the trailing update
+// of geqrf) or T (transT = 0, orgqr).  V is the unit lower trapezoidal panel:
+// element (row j0 + rr, reflector l) at V[rr + l * ldv], the shared-memory
+// panel copy (SM) or the working matrix in global memory (V = A + j0 + j0 lda).
+// On the FP64 tensor pipe (mma.sync.m8n8k4.f64 = DMMA), one warp per chunk of 8
+// target columns, no block barrier:
+//   W  (32 x 8)  = V^T X_chunk       4 accumulator tiles over mr/4 k-steps
+//   W' (32 x 8)  = op(T) W            8 k-steps, W moved from the accumulator
+//                                     layout to B fragments by shuffles
+//   X_chunk     -= V W'              row tiles of 8, X loaded as the accumulator
+// (the scalar version read one shared-memory double per FMA and was bound by
+// shared-memory bandwidth: 373 us for the Q of a 264 x 132 QR).
+__device__ __forceinline__ void dmma_f64(double &c0, double &c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+// 32 x 8 block in accumulator layout (tile i: lane t holds rows 8i + t/4, columns
+// 2(t%4) + {0, 1}) -> B fragments of the 8 k-steps (lane t: row 4kk + t%4, column t/4)
+__device__ __forceinline__ void acc_to_bfrag(const double (&d)[4][2], double (&b)[8], int lane) {
+  const int n = lane >> 2;
+#pragma unroll
+  for (int kk = 0; kk < 8; ++kk) {
+    const int mrow = 4 * kk + (lane & 3);
+    const int src = (mrow & 7) * 4 + (n >> 1);
+    const double v0 = __shfl_sync(0xffffffffu, d[kk >> 1][0], src);
+    const double v1 = __shfl_sync(0xffffffffu, d[kk >> 1][1], src);
+    b[kk] = (n & 1) ? v1 : v0;
+  }
+}
+
+template <bool SM>
+__device__ __forceinline__ void apply_block_reflector(int m, int j0, int jb, const double *__restrict__ V, int ldv,
+                                                      const double (*sT)[NB + 1], int transT, double *X,
+                                                      long long rs, long long cs, int c_begin, int c_end) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, NW = blockDim.x >> 5;
+  const int mr = m - j0;                  // rows j0..m-1
+  const int q4 = lane & 3, g8 = lane >> 2;
+  // masked V element (row rr, reflector l): unit lower trapezoid, zero outside
+  auto vm = [&](int rr, int l) -> double {
+    if (l >= jb || rr >= mr || rr < l) return 0.0;
+    return rr == l ? 1.0 : V[rr + l * ldv];
   };
-  for (int cb = c_begin; cb < c_end; cb += NB) {
-    const int cw = min(NB, c_end - cb);
-    // W = V^T X  (jb x cw), accumulated over 32-row chunks
-    double acc[QR_NQ];
+  const int nchunk = (c_end - c_begin + 7) >> 3;
+  for (int ch = warp; ch < nchunk; ch += NW) {
+    const int c0 = c_begin + 8 * ch;
+    double *X0 = X + (long long)j0 * rs + (long long)c0 * cs;
+    // ---- W = V^T X_chunk: A[m = l][k = rr] = V(rr, l), B[k = rr][n] = X(rr, c0 + n)
+    double w[4][2];
 #pragma unroll
-    for (int q = 0; q < QR_NQ; ++q) acc[q] = 0.0;
-    for (int rb = j0; rb < m; rb += NB) {
-      const int rh = min(NB, m - rb);
-      for (int e = tid; e < NB * NB; e += QR_THREADS) {
-        const int rr = e % NB, l = e / NB;
-        const int r = rb + rr;
-        double v = 0.0;
-        if (rr < rh && l < jb) {
-          const int dg = j0 + l;
-          v = (r > dg) ? vget(r, l) : (r == dg ? 1.0 : 0.0);
-        }
-        sV[rr][l] = v;
-        const int c = cb + l;
-        sX[rr][l] = (rr < rh && l < cw) ? X[(long long)r * rs + (long long)c * cs] : 0.0;
-      }
-      __syncthreads();
+    for (int i = 0; i < 4; ++i) w[i][0] = w[i][1] = 0.0;
+    const bool colok = c0 + g8 < c_end;
+    const double *xb = X0 + (long long)g8 * cs;
+    int r0 = 0;
+    for (; r0 < 32 && r0 < mr; r0 += 4) {                 // triangle rows: masked
+      const int rr = r0 + q4;
+      const double b = (colok && rr < mr) ? xb[(long long)rr * rs] : 0.0;
 #pragma unroll
-      for (int q = 0; q < QR_NQ; ++q) {
-        const int e = tid + q * QR_THREADS;  // 1024 entries (l, c)
-        const int l = e % NB, c = e / NB;
-        double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-#pragma unroll
-        for (int rr = 0; rr < NB; rr += 4) {
-          s0 = fma(sV[rr][l], sX[rr][c], s0);
-          s1 = fma(sV[rr + 1][l], sX[rr + 1][c], s1);
-          s2 = fma(sV[rr + 2][l], sX[rr + 2][c], s2);
-          s3 = fma(sV[rr + 3][l], sX[rr + 3][c], s3);
-        }
-        acc[q] += (s0 + s1) + (s2 + s3);
-      }
-      __syncthreads();
+      for (int i = 0; i < 4; ++i) dmma_f64(w[i][0], w[i][1], vm(rr, 8 * i + g8), b);
     }
+    if (jb == NB) {
+      // full rows, all 32 reflectors stored: 8 k-steps per batch, their X loads
+      // issued together (X lives in L2 / global memory)
+      for (; r0 + 32 <= mr; r0 += 32) {
+        double b[8];
 #pragma unroll
-    for (int q = 0; q < QR_NQ; ++q) {
-      const int e = tid + q * QR_THREADS;
-      sW[e % NB][e / NB] = acc[q];
-    }
-    __syncthreads();
-    // W' = op(T) W
+        for (int u = 0; u < 8; ++u) b[u] = colok ? xb[(long long)(r0 + 4 * u + q4) * rs] : 0.0;
 #pragma unroll
-    for (int q = 0; q < QR_NQ; ++q) {
-      const int e = tid + q * QR_THREADS;
-      const int l = e % NB, c = e / NB;
-      double s = 0.0;
-      if (l < jb) {
-        if (transT) {
-          for (int p = 0; p <= l; ++p) s = fma(sT[p][l], sW[p][c], s);
-        } else {
-          for (int p = l; p < jb; ++p) s = fma(sT[l][p], sW[p][c], s);
+        for (int u = 0; u < 8; ++u) {
+          const double *vp = V + r0 + 4 * u + q4 + g8 * ldv;
+#pragma unroll
+          for (int i = 0; i < 4; ++i) dmma_f64(w[i][0], w[i][1], vp[8 * i * ldv], b[u]);
         }
       }
-      acc[q] = s;
-    }
-    __syncthreads();
+      for (; r0 + 4 <= mr; r0 += 4) {
+        const int rr = r0 + q4;
+        const double b = colok ? xb[(long long)rr * rs] : 0.0;
+        const double *vp = V + rr + g8 * ldv;
 #pragma unroll
-    for (int q = 0; q < QR_NQ; ++q) {
-      const int e = tid + q * QR_THREADS;
-      sW[e % NB][e / NB] = acc[q];
+        for (int i = 0; i < 4; ++i) dmma_f64(w[i][0], w[i][1], vp[8 * i * ldv], b);
+      }
     }
-    __syncthreads();
-    // X -= V W'
-    for (int rb = j0; rb < m; rb += NB) {
-      const int rh = min(NB, m - rb);
-      for (int e = tid; e < NB * NB; e += QR_THREADS) {
-        const int rr = e % NB, l = e / NB;
-        const int r = rb + rr;
-        double v = 0.0;
-        if (rr < rh && l < jb) {
-          const int dg = j0 + l;
-          v = (r > dg) ? vget(r, l) : (r == dg ? 1.0 : 0.0);
-        }
-        sV[rr][l] = v;
-      }
-      __syncthreads();
-      for (int e = tid; e < NB * NB; e += QR_THREADS) {
-        const int rr = e % NB, c = e / NB;
-        if (rr < rh && c < cw) {
-          // sV is zero beyond jb, so the full-width sum is exact; four chains
-          double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+    for (; r0 < mr; r0 += 4) {                            // ragged tail / short panel
+      const int rr = r0 + q4;
+      const double b = (colok && rr < mr) ? xb[(long long)rr * rs] : 0.0;
 #pragma unroll
-          for (int l = 0; l < NB; l += 4) {
-            s0 = fma(sV[rr][l], sW[l][c], s0);
-            s1 = fma(sV[rr][l + 1], sW[l + 1][c], s1);
-            s2 = fma(sV[rr][l + 2], sW[l + 2][c], s2);
-            s3 = fma(sV[rr][l + 3], sW[l + 3][c], s3);
-          }
-          const double s = (s0 + s1) + (s2 + s3);
-          X[(long long)(rb + rr) * rs + (long long)(cb + c) * cs] -= s;
+      for (int i = 0; i < 4; ++i) dmma_f64(w[i][0], w[i][1], vm(rr, 8 * i + g8), b);
+    }
+    // ---- W' = op(T) W: A[m][k] = op(T)(m, k) from shared memory, B = W fragments
+    double bw[8];
+    acc_to_bfrag(w, bw, lane);
+    double wp[4][2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) wp[i][0] = wp[i][1] = 0.0;
+#pragma unroll
+    for (int kk = 0; kk < 8; ++kk) {
+      const int k = 4 * kk + q4;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int mm = 8 * i + g8;
+        const double a = transT ? sT[k][mm] : sT[mm][k];
+        dmma_f64(wp[i][0], wp[i][1], a, bw[kk]);
+      }
+    }
+    double bn[8];
+    acc_to_bfrag(wp, bn, lane);
+#pragma unroll
+    for (int kk = 0; kk < 8; ++kk) bn[kk] = -bn[kk];
+    // ---- X_chunk -= V W': row tiles of 8; C = X (lane: row t/4, columns 2(t%4) + {0,1})
+    const int ca = c0 + 2 * q4, cb = ca + 1;
+    const bool oka = ca < c_end, okb = cb < c_end;
+    double *xa = X0 + (long long)(2 * q4) * cs, *xbb = xa + cs;
+    int t0 = 0;
+    if (jb == NB) {
+      for (; t0 < 32 && t0 < mr; t0 += 8) {                // triangle rows: masked
+        const int rr = t0 + g8;
+        const bool rok = rr < mr;
+        double d0 = (rok && oka) ? xa[(long long)rr * rs] : 0.0;
+        double d1 = (rok && okb) ? xbb[(long long)rr * rs] : 0.0;
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) dmma_f64(d0, d1, vm(rr, 4 * kk + q4), bn[kk]);
+        if (rok && oka) xa[(long long)rr * rs] = d0;
+        if (rok && okb) xbb[(long long)rr * rs] = d1;
+      }
+      for (; t0 + 32 <= mr; t0 += 32) {                   // 4 full row tiles per batch
+        double d[4][2];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const long long rr = t0 + 8 * u + g8;
+          d[u][0] = oka ? xa[rr * rs] : 0.0;
+          d[u][1] = okb ? xbb[rr * rs] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const double *vp = V + t0 + 8 * u + g8 + q4 * ldv;
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk) dmma_f64(d[u][0], d[u][1], vp[4 * kk * ldv], bn[kk]);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const long long rr = t0 + 8 * u + g8;
+          if (oka) xa[rr * rs] = d[u][0];
+          if (okb) xbb[rr * rs] = d[u][1];
         }
       }
-      __syncthreads();
+    }
+    for (; t0 < mr; t0 += 8) {
+      const int rr = t0 + g8;
+      const bool rok = rr < mr;
+      double d0 = (rok && oka) ? xa[(long long)rr * rs] : 0.0;
+      double d1 = (rok && okb) ? xbb[(long long)rr * rs] : 0.0;
+      if (t0 >= 32 && t0 + 8 <= mr && jb == NB) {
+        const double *vp = V + rr + q4 * ldv;
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) dmma_f64(d0, d1, vp[4 * kk * ldv], bn[kk]);
+      } else {
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) dmma_f64(d0, d1, vm(rr, 4 * kk + q4), bn[kk]);
+      }
+      if (rok && oka) xa[(long long)rr * rs] = d0;
+      if (rok && okb) xbb[(long long)rr * rs] = d1;
     }
   }
 }
@@ -170,12 +221,34 @@ __device__ __forceinline__ void qr_panel(const QRDesc &g, int m, int j0, int jb,
   //      to it and immediately forms reflector j+1 while the other warps
   //      update the rest of the panel, so each column costs one block barrier
   //      and the reflector formation is off the critical path of the update.
+  // per-lane strided loops over rows lo..m-1 with four independent chains, so the
+  // shared-memory loads of one lane overlap (the column step is a latency chain)
+  auto dot_rows = [&](const double *a, const double *b, int lo) -> double {
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+    int i = lo + lane;
+    for (; i + 96 < m; i += 128) {
+      s0 = fma(a[i], b[i], s0);
+      s1 = fma(a[i + 32], b[i + 32], s1);
+      s2 = fma(a[i + 64], b[i + 64], s2);
+      s3 = fma(a[i + 96], b[i + 96], s3);
+    }
+    for (; i < m; i += 32) s0 = fma(a[i], b[i], s0);
+    return (s0 + s1) + (s2 + s3);
+  };
+  auto axpy_rows = [&](double *y, const double *x, double a, int lo) {
+    int i = lo + lane;
+    for (; i + 96 < m; i += 128) {
+      const double x0 = x[i], x1 = x[i + 32], x2 = x[i + 64], x3 = x[i + 96];
+      y[i] = fma(-a, x0, y[i]);
+      y[i + 32] = fma(-a, x1, y[i + 32]);
+      y[i + 64] = fma(-a, x2, y[i + 64]);
+      y[i + 96] = fma(-a, x3, y[i + 96]);
+    }
+    for (; i < m; i += 32) y[i] = fma(-a, x[i], y[i]);
+  };
   auto form_reflector = [&](int j, int slot) {   // warp 0 only; column j already up to date
     double *col = colp(j);
-    double part = 0.0;
-#pragma unroll (SM ? 1 : 4)
-    for (int i = j + 1 + lane; i < m; i += 32) part = fma(col[i], col[i], part);
-    const double sigma = warp_sum(part);
+    const double sigma = warp_sum(dot_rows(col, col, j + 1));
     const double alpha = col[j];
     double tau = 0.0, scal = 0.0, beta = alpha;
     if (sigma > 0.0) {
@@ -192,8 +265,14 @@ __device__ __forceinline__ void qr_panel(const QRDesc &g, int m, int j0, int jb,
       scal = alpha >= 0.0 ? q : -q;
     }
     if (tau != 0.0) {
-#pragma unroll (SM ? 1 : 4)
-      for (int i = j + 1 + lane; i < m; i += 32) col[i] *= scal;
+      int i = j + 1 + lane;
+      for (; i + 96 < m; i += 128) {
+        col[i] *= scal;
+        col[i + 32] *= scal;
+        col[i + 64] *= scal;
+        col[i + 96] *= scal;
+      }
+      for (; i < m; i += 32) col[i] *= scal;
     }
     __syncwarp();
     if (lane == 0) {
@@ -212,12 +291,10 @@ __device__ __forceinline__ void qr_panel(const QRDesc &g, int m, int j0, int jb,
     if (tau != 0.0) {
       for (int c = j + 1 + warp; c < j0 + jb; c += NW) {
         double *cc = colp(c);
-        double w = 0.0;
-#pragma unroll (SM ? 1 : 4)
-        for (int i = j + lane; i < m; i += 32) w = fma(i == j ? 1.0 : col[i], cc[i], w);
-        w = warp_sum(w) * tau;
-#pragma unroll (SM ? 1 : 4)
-        for (int i = j + lane; i < m; i += 32) cc[i] -= w * (i == j ? 1.0 : col[i]);
+        // w = tau v^T cc with v = (1, col[j+1..m-1])
+        const double w = warp_sum(dot_rows(col, cc, j + 1) + (lane == 0 ? cc[j] : 0.0)) * tau;
+        if (lane == 0) cc[j] -= w;
+        axpy_rows(cc, col, w, j + 1);
       }
     }
     if (warp == 0 && jj + 1 < jb) {
@@ -227,16 +304,31 @@ __device__ __forceinline__ void qr_panel(const QRDesc &g, int m, int j0, int jb,
     __syncthreads();
   }
   // ---- T factor (larft, forward, columnwise): T upper triangular jb x jb
-  //      G[l][i] = v_l^T v_i for l < i
-  for (int pidx = warp; pidx < jb * jb; pidx += NW) {
-    const int l = pidx % jb, i = pidx / jb;
-    if (l < i) {
-      const double *vl = colp(j0 + l);
-      const double *vi = colp(j0 + i);
-      double s = 0.0;
-      for (int r = j0 + i + 1 + lane; r < m; r += 32) s = fma(vl[r], vi[r], s);
-      s = warp_sum(s);
-      if (lane == 0) sG[l][i] = s + vl[j0 + i];
+  //      G[l][i] = v_l^T v_i for l < i: the upper 8x8 tiles of V^T V on the
+  //      FP64 tensor pipe (one warp per tile, rows over the k-steps)
+  {
+    const double *V = SM ? sP : A + j0 + (long long)j0 * lda;
+    const int ldv = SM ? pr : (int)lda, mr = m - j0, q4 = lane & 3, g8 = lane >> 2;
+    auto vm = [&](int rr, int l) -> double {
+      if (l >= jb || rr >= mr || rr < l) return 0.0;
+      return rr == l ? 1.0 : V[rr + l * ldv];
+    };
+    const int nt = (jb + 7) >> 3;
+    for (int t = warp; t < nt * nt; t += NW) {
+      const int ti = t % nt, tj = t / nt;
+      if (ti > tj) continue;
+      double d0 = 0.0, d1 = 0.0;
+      int r0 = 0;
+      for (; r0 < 32 && r0 < mr; r0 += 4) dmma_f64(d0, d1, vm(r0 + q4, 8 * ti + g8), vm(r0 + q4, 8 * tj + g8));
+      if (jb == NB)
+        for (; r0 + 4 <= mr; r0 += 4) {
+          const double *vp = V + r0 + q4;
+          dmma_f64(d0, d1, vp[(8 * ti + g8) * ldv], vp[(8 * tj + g8) * ldv]);
+        }
+      for (; r0 < mr; r0 += 4) dmma_f64(d0, d1, vm(r0 + q4, 8 * ti + g8), vm(r0 + q4, 8 * tj + g8));
+      const int l = 8 * ti + g8, i0 = 8 * tj + 2 * q4;
+      if (l < i0 && i0 < jb) sG[l][i0] = d0;
+      if (l < i0 + 1 && i0 + 1 < jb) sG[l][i0 + 1] = d1;
     }
   }
 }
@@ -263,7 +355,6 @@ __global__ void __launch_bounds__(QR_THREADS) qr_kernel(const QRDesc *__restrict
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   __shared__ double sT[NB][NB + 1];
   __shared__ double sG[NB][NB + 1];
-  __shared__ double sV[NB][NB + 1], sX[NB][NB + 1], sW[NB][NB + 1];
   __shared__ double s_tau[2];
   double *A = g.A;
   const long long lda = g.lda;
@@ -332,8 +423,9 @@ __global__ void __launch_bounds__(QR_THREADS) qr_kernel(const QRDesc *__restrict
     QR_PH(2);
     // ---- trailing update: A[:, j0+jb:n] <- (I - V T V^T)^T A = A - V T^T (V^T A)
     if (j0 + jb < n)
-      apply_block_reflector(m, j0, jb, A, lda, sT, 1, A, 1, lda, j0 + jb, n, sV, sX, sW, in_smem ? sP : nullptr,
-                            pr);
+      if (in_smem) apply_block_reflector<true>(m, j0, jb, sP, pr, sT, 1, A, 1, lda, j0 + jb, n);
+      else apply_block_reflector<false>(m, j0, jb, A + j0 + (long long)j0 * lda, (int)lda, sT, 1, A, 1, lda, j0 + jb,
+                                        n);
     __syncthreads();
   }
   QR_PH(3);
@@ -366,8 +458,9 @@ __global__ void __launch_bounds__(QR_THREADS) qr_kernel(const QRDesc *__restrict
           sP[r + l * pr] = A[j0 + r + (long long)(j0 + l) * lda];
         }
       __syncthreads();
-      apply_block_reflector(m, j0, jb, A, lda, sT, 0, g.Q, g.q_rs, g.q_cs, j0, kmin, sV, sX, sW,
-                            in_smem ? sP : nullptr, pr);
+      if (in_smem) apply_block_reflector<true>(m, j0, jb, sP, pr, sT, 0, g.Q, g.q_rs, g.q_cs, j0, kmin);
+      else apply_block_reflector<false>(m, j0, jb, A + j0 + (long long)j0 * lda, (int)lda, sT, 0, g.Q, g.q_rs,
+                                        g.q_cs, j0, kmin);
       __syncthreads();
     }
   }
