@@ -421,12 +421,21 @@ int32_t tt_transport_terms_1d(int32_t op, int32_t nv, double extent, int32_t G, 
                               const double *sigma_s, const double *nu_sigma_f, const double *chi,
                               double *out);
 
-/* Algorithm 1 for one factor, host side: a 2^l x 2^l column-major
- * matrix G is reshaped to 2 x..x 2, its row/column bits paired (i_t, j_t) LSB
- * first (Z28), and TT-SVD'd with modes 4 (row bit fastest) and the tail rule
- * delta = eps ||G||_F / sqrt(l-1).  Cores [r_t, 2, 2, r_{t+1}] are written
- * consecutively to cores_out (host, capacity cap doubles; NULL = size query),
- * ranks (l+1 ints) to ranks_out.  Returns the number of doubles, -1 on error. */
+/* Algorithm 1 (alg:TTtoQTT) for one factor, on the device: the
+ * 2^l x 2^l column-major matrix M (device pointer) is reshaped to 2 x..x 2, its
+ * row/column bits paired (i_t, j_t) LSB first (Z28) into modes of 4 (row bit
+ * fastest), written as the exact index-forwarding TT of that tensor (ranks
+ * 4^min(t, l-t)) into q and rounded on the device to eps (tt_round: the
+ * TT-SVD with the tail rule delta = eps ||M||_F / sqrt(l-1), reading Z21).
+ * q: d = l cores, modes 4, rank capacities >= 4^min(t, l-t) (caller-owned;
+ * on return its device ranks are the QTT ranks and core t, viewed as
+ * [r_t, 2, 2, r_{t+1}], is the QTT-matrix core).  Errors: TT_ERR_ARG (n not a
+ * power of two >= 2, NULL pointers), TT_ERR_SHAPE, TT_ERR_CAPACITY.
+ * Workspace: tt_qtt_matrix_dev_workspace(q). */
+size_t tt_qtt_matrix_dev_workspace(const tt_vec *q);
+tt_status tt_qtt_matrix_dev(int32_t n, const double *M, double eps, tt_vec *q, void *ws, size_t wsb,
+                            tt_stream s);
+
 /* Velocity operator V^{-1} of the alpha problem (the alpha term of
  * eq. Discretized_alphaNTE): per octant b the rank-1 term
  * diag(inv_v) o (C_b (x) I) o Ip_z o Ip_y o Ip_x (spatially uniform).
@@ -439,8 +448,7 @@ int32_t tt_velocity_terms(int32_t dim, int32_t nv, int32_t G, int32_t L, const d
                           const double *eta, const double *xi, const double *inv_v,
                           int32_t reflective, double *out);
 
-int64_t tt_qtt_matrix(int32_t n, const double *G, double eps, int32_t *ranks_out, double *cores_out,
-                      int64_t cap);
+
 
 #ifdef __cplusplus
 }

@@ -79,149 +79,94 @@ struct Term {
 }  // namespace
 
 // ------------------------------------------------ Alg. 1 ---
-// Host one-sided Jacobi SVD of an m x n column-major matrix (m >= n):
-// W <- U diag(s), V accumulated; returns s sorted descending with U, V permuted.
-static void host_svd(int m, int n, std::vector<double> &W, std::vector<double> &s, std::vector<double> &V) {
-  V.assign((size_t)n * n, 0.0);
-  for (int i = 0; i < n; ++i) V[(size_t)i * n + i] = 1.0;
-  for (int sweep = 0; sweep < 80; ++sweep) {
-    bool rot = false;
-    for (int a = 0; a < n - 1; ++a)
-      for (int b = a + 1; b < n; ++b) {
-        double al = 0, be = 0, ga = 0;
-        for (int r = 0; r < m; ++r) {
-          const double x = W[(size_t)a * m + r], y = W[(size_t)b * m + r];
-          al += x * x; be += y * y; ga += x * y;
-        }
-        if (ga == 0.0 || al == 0.0 || be == 0.0 || std::fabs(ga) <= 1e-15 * std::sqrt(al) * std::sqrt(be)) continue;
-        const double zeta = (be - al) / (2.0 * ga);
-        const double t = (zeta >= 0 ? 1.0 : -1.0) / (std::fabs(zeta) + std::sqrt(1.0 + zeta * zeta));
-        const double c = 1.0 / std::sqrt(1.0 + t * t), sn = c * t;
-        for (int r = 0; r < m; ++r) {
-          const double x = W[(size_t)a * m + r], y = W[(size_t)b * m + r];
-          W[(size_t)a * m + r] = c * x - sn * y;
-          W[(size_t)b * m + r] = sn * x + c * y;
-        }
-        for (int r = 0; r < n; ++r) {
-          const double x = V[(size_t)a * n + r], y = V[(size_t)b * n + r];
-          V[(size_t)a * n + r] = c * x - sn * y;
-          V[(size_t)b * n + r] = sn * x + c * y;
-        }
-        rot = true;
+// Device QTT-matrix of a 2^l x 2^l factor: the tensor T(i_0, .., i_{l-1}) with
+// mode index i_t = (row bit t) + 2 (column bit t) (bits LSB first, Z28) is
+// written as an EXACT TT with index-forwarding cores — cores t < h carry the
+// digits i_0..i_t in their right rank index, cores t > h carry i_t..i_{l-1} in
+// their left rank index, core h = floor(l/2) holds the n^2 entries of the
+// factor — ranks 4^min(t, l-t) (<= n); tt_round of that TT to eps is the TT-SVD
+// of T (rounding an exact TT = TT-SVD with the same per-bond rule, Oseledets
+// 2011 / reading Z21), i.e. Alg. 1's "compute G_k's QTT-matrix format".
+namespace tt {
+namespace {
+__global__ void qtt_forward_kernel(const VecMeta q, int l, int n, const double *__restrict__ M) {
+  const int t = blockIdx.y, h = l / 2;
+  auto rk = [&](int b) { int e = b < l - b ? b : l - b; return 1 << (2 * e); };
+  const int r0 = rk(t), r1 = rk(t + 1);
+  double *core = q.data + q.off[t];
+  const long long total = (long long)r0 * 4 * r1;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int a = (int)(e % r0);
+    const long long rest = e / r0;
+    const int i = (int)(rest % 4), b = (int)(rest / 4);
+    double v;
+    if (t < h) {          // left forwarding: b = a + r0 i
+      v = (b == a + r0 * i) ? 1.0 : 0.0;
+    } else if (t > h) {   // right forwarding: a = i + 4 b
+      v = (a == i + 4 * b) ? 1.0 : 0.0;
+    } else {              // data core: a = digits 0..h-1, b = digits h+1..l-1
+      int row = 0, col = 0, s = 0;
+      for (int k = 0; k < h; ++k, ++s) {
+        const int dg = (a >> (2 * k)) & 3;
+        row |= (dg & 1) << s;
+        col |= (dg >> 1) << s;
       }
-    if (!rot) break;
+      row |= (i & 1) << s;
+      col |= (i >> 1) << s;
+      ++s;
+      for (int k = 0; k < l - h - 1; ++k, ++s) {
+        const int dg = (b >> (2 * k)) & 3;
+        row |= (dg & 1) << s;
+        col |= (dg >> 1) << s;
+      }
+      v = M[row + (long long)n * col];
+    }
+    core[e] = v;
   }
-  s.assign(n, 0.0);
-  for (int c = 0; c < n; ++c) {
-    double t = 0;
-    for (int r = 0; r < m; ++r) t += W[(size_t)c * m + r] * W[(size_t)c * m + r];
-    s[c] = std::sqrt(t);
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    q.r[t] = r0;
+    if (t == l - 1) q.r[t + 1] = 1;
   }
-  std::vector<int> idx(n);
-  for (int i = 0; i < n; ++i) idx[i] = i;
-  std::sort(idx.begin(), idx.end(), [&](int x, int y) { return s[x] > s[y]; });
-  std::vector<double> W2((size_t)m * n), V2((size_t)n * n), s2(n);
-  for (int i = 0; i < n; ++i) {
-    const int c = idx[i];
-    s2[i] = s[c];
-    for (int r = 0; r < m; ++r) W2[(size_t)i * m + r] = s[c] > 0 ? W[(size_t)c * m + r] / s[c] : 0.0;
-    for (int r = 0; r < n; ++r) V2[(size_t)i * n + r] = V[(size_t)c * n + r];
-  }
-  W.swap(W2); V.swap(V2); s.swap(s2);
 }
 
-// QTT-matrix of a 2^l x 2^l matrix G (column-major): reshape to 2 x..x 2, pair
-// the row/column bits (i_t, j_t) LSB first (Z28), TT-SVD with modes 4 (row bit
-// fastest) and tail rule delta = eps ||G|| / sqrt(l-1).  Writes the cores
-// [r_t, 2, 2, r_{t+1}] consecutively into cores_out (capacity cap doubles) and
-// the ranks (l+1) into ranks_out.  Returns the number of doubles written, or -1.
-extern "C" int64_t tt_qtt_matrix(int32_t n, const double *G, double eps, int32_t *ranks_out, double *cores_out,
-                                 int64_t cap) {
-  int l = 0;
+tt_status qtt_check(int32_t n, const VecMeta &qm, int &l) {
+  l = 0;
   while ((1 << l) < n) ++l;
-  if (n < 2 || (1 << l) != n || !G || !ranks_out) {
-    tt::set_error("tt_qtt_matrix: n must be a power of two >= 2");
-    return -1;
+  if (n < 2 || (1 << l) != n) return fail(TT_ERR_ARG, "tt_qtt_matrix_dev: n must be a power of two >= 2");
+  if (qm.d != l) return fail(TT_ERR_SHAPE, "tt_qtt_matrix_dev: q must have log2(n) cores");
+  for (int t = 0; t < l; ++t) {
+    const int e = t < l - t ? t : l - t;
+    if (qm.n[t] != 4) return fail(TT_ERR_SHAPE, "tt_qtt_matrix_dev: q modes must be 4");
+    if (qm.rcap[t] < (1 << (2 * e))) return fail(TT_ERR_CAPACITY, "tt_qtt_matrix_dev: rank capacity below 4^min(t, l-t)");
   }
-  const size_t N = (size_t)n * n;
-  std::vector<double> T(N);
-  double nrm2 = 0;
-  for (int j = 0; j < n; ++j)
-    for (int i = 0; i < n; ++i) {
-      size_t lin = 0, mul = 1;
-      for (int t = 0; t < l; ++t) {
-        lin += mul * (((i >> t) & 1) + 2 * ((j >> t) & 1));
-        mul *= 4;
-      }
-      T[lin] = G[(size_t)i + (size_t)n * j];
-      nrm2 += T[lin] * T[lin];
-    }
-  const double delta = l > 1 ? eps * std::sqrt(nrm2) / std::sqrt((double)(l - 1)) : 0.0;
-  std::vector<double> C = T;  // current remainder, r x rest (column-major)
-  int r = 1;
-  size_t rest = N;
-  int64_t used = 0;
-  ranks_out[0] = 1;
-  std::vector<std::vector<double>> cores;
-  for (int t = 0; t < l - 1; ++t) {
-    const int rows = r * 4;
-    rest /= 4;
-    const int cols = (int)rest;
-    // SVD of the (rows x cols) unfolding; Jacobi on the orientation with fewer columns
-    std::vector<double> U, S, Vt;
-    int rk;
-    if (rows >= cols) {
-      std::vector<double> W = C, V;
-      host_svd(rows, cols, W, S, V);
-      rk = cols;
-      U = W;                       // rows x cols
-      Vt.assign((size_t)cols * cols, 0.0);
-      for (int i = 0; i < cols; ++i)
-        for (int c = 0; c < cols; ++c) Vt[(size_t)i + (size_t)cols * c] = V[(size_t)i * cols + c];  // (V^T)[i][c]
-    } else {
-      std::vector<double> W((size_t)cols * rows);  // transpose
-      for (int i = 0; i < rows; ++i)
-        for (int c = 0; c < cols; ++c) W[(size_t)i * cols + c] = C[(size_t)i + (size_t)rows * c];
-      std::vector<double> V;
-      host_svd(cols, rows, W, S, V);  // C^T = W S V^T -> C = V S W^T
-      rk = rows;
-      U.assign((size_t)rows * rows, 0.0);
-      for (int i = 0; i < rows; ++i)
-        for (int c = 0; c < rows; ++c) U[(size_t)c * rows + i] = V[(size_t)c * rows + i];
-      Vt.assign((size_t)rows * cols, 0.0);
-      for (int i = 0; i < rows; ++i)
-        for (int c = 0; c < cols; ++c) Vt[(size_t)i + (size_t)rows * c] = W[(size_t)i * cols + c];
-    }
-    // tail rule
-    double tail = 0;
-    int rn = rk;
-    for (int i = rk - 1; i >= 1; --i) {
-      if (tail + S[i] * S[i] <= delta * delta) { tail += S[i] * S[i]; rn = i; } else break;
-    }
-    std::vector<double> core((size_t)rows * rn);
-    for (int c = 0; c < rn; ++c)
-      for (int i = 0; i < rows; ++i) core[(size_t)i + (size_t)rows * c] = U[(size_t)c * rows + i];
-    cores.push_back(core);
-    ranks_out[t + 1] = rn;
-    std::vector<double> Cn((size_t)rn * cols);
-    for (int c = 0; c < cols; ++c)
-      for (int i = 0; i < rn; ++i) Cn[(size_t)i + (size_t)rn * c] = S[i] * Vt[(size_t)i + (size_t)rk * c];
-    C.swap(Cn);
-    r = rn;
-  }
-  cores.push_back(C);  // r x 4 (last core [r, 2, 2, 1])
-  ranks_out[l] = 1;
-  for (auto &c : cores) {
-    if (cores_out) {
-      if (used + (int64_t)c.size() > cap) {
-        tt::set_error("tt_qtt_matrix: output capacity too small");
-        return -1;
-      }
-      std::memcpy(cores_out + used, c.data(), c.size() * sizeof(double));
-    }
-    used += (int64_t)c.size();
-  }
-  return used;
+  return TT_OK;
+}
+}  // namespace
+}  // namespace tt
+
+extern "C" size_t tt_qtt_matrix_dev_workspace(const tt_vec *q) {
+  tt::VecMeta qm;
+  if (tt::make_vec_meta(q, qm) != TT_OK) return 0;
+  tt::Arena ar;
+  tt::round_meta(qm, 0.0, 1, nullptr, nullptr, 0, ar, nullptr);
+  return ar.used;
+}
+
+extern "C" tt_status tt_qtt_matrix_dev(int32_t n, const double *M, double eps, tt_vec *q, void *ws, size_t wsb,
+                                       tt_stream s) {
+  tt::VecMeta qm;
+  TT_TRY(tt::make_vec_meta(q, qm));
+  int l = 0;
+  TT_TRY(tt::qtt_check(n, qm, l));
+  if (!M || !ws) return tt::fail(TT_ERR_ARG, "tt_qtt_matrix_dev: NULL matrix or workspace");
+  const cudaStream_t st = (cudaStream_t)s;
+  tt::qtt_forward_kernel<<<dim3(64, l), 256, 0, st>>>(qm, l, n, M);
+  TT_TRY(tt::check_launch("qtt_forward"));
+  tt::Arena ar;
+  ar.base = (char *)ws;
+  ar.cap = wsb;
+  return tt::round_meta(qm, eps, 1 << 30, nullptr, nullptr, 0, ar, st);
 }
 
 // 1-D slab: the 3-D construction restricted to the x factor, the

@@ -2,10 +2,11 @@
 
 The per-octant rank-1 factor matrices come from libtt's host-side C++
 constructor (tt_transport_terms); power-of-two spatial factors are converted to
-QTT by libtt's host implementation of Algorithm 1 (tt_qtt_matrix)
-when the problem asks for QTT; the sum over octants / parts (ranks add,
-P:1290-1293) and the rank reduction run on the GPU with
-tt_add and tt_round.  One-off setup, not a hot-path step."""
+QTT on the GPU by Algorithm 1 (tt_qtt_matrix_dev: TT-SVD by
+rounding the exact index-forwarding TT) when the problem asks for QTT; the sum
+over octants / parts (ranks add) and the rank
+reduction run on the GPU with tt_add and tt_round.  One-off setup, not
+a hot-path step."""
 from __future__ import annotations
 
 import ctypes as C
@@ -121,33 +122,54 @@ def factor_terms(prob, op: str):
     return terms
 
 
-def qtt_matrix(M: np.ndarray, eps: float = 1e-14):
-    """QTT cores [r, 2, 2, r'] of a 2^l x 2^l matrix via libtt's Alg. 1."""
-    n = M.shape[0]
-    l = int(round(np.log2(n)))
-    Mf = np.ascontiguousarray(M.reshape(-1, order="F"), dtype=np.float64)
-    ranks = np.zeros(l + 1, dtype=np.int32)
-    lib = _lib.lib()
-    size = lib.tt_qtt_matrix(n, _dp(Mf), float(eps), _dp(ranks), None, 0)
-    if size < 0:
-        raise _lib.TTError(1, lib.tt_last_error().decode())
-    out = np.zeros(size, dtype=np.float64)
-    lib.tt_qtt_matrix(n, _dp(Mf), float(eps), _dp(ranks), _dp(out), size)
-    cores, o = [], 0
-    for t in range(l):
-        c = ranks[t] * 4 * ranks[t + 1]
-        cores.append(out[o:o + c].reshape(ranks[t], 2, 2, ranks[t + 1], order="F"))
-        o += c
-    return cores
+class _QttCache:
+    """Device QTT conversion of the factors: one TT-vector slot and workspace per
+    matrix size, identical factors (the same D / Ip matrix in several octant
+    terms) converted once."""
+
+    def __init__(self):
+        self.slots, self.done = {}, {}
+
+    def get(self, M: np.ndarray, eps: float, device):
+        key = (M.shape[0], eps, M.tobytes())
+        hit = self.done.get(key)
+        if hit is not None:
+            return hit
+        import torch
+        from .tt import workspace
+        n = M.shape[0]
+        l = int(round(np.log2(n)))
+        if (1 << l) != n or l < 1:
+            raise _lib.TTError(1, "qtt_matrix: n must be a power of two >= 2")
+        if n not in self.slots:
+            rc = [1 << (2 * min(t, l - t)) for t in range(l + 1)]
+            self.slots[n] = TTVec([4] * l, rc, device)
+        q = self.slots[n]
+        Md = torch.from_numpy(np.ascontiguousarray(M.reshape(-1, order="F"), dtype=np.float64)).to(q.device)
+        lib = _lib.lib()
+        ws = workspace(lib.tt_qtt_matrix_dev_workspace(q.c), q.device)
+        _lib.check(lib.tt_qtt_matrix_dev(n, C.c_void_p(Md.data_ptr()), float(eps), q.c, C.c_void_p(ws.data_ptr()),
+                                         ws.numel(), C.c_void_p(torch.cuda.current_stream(q.device).cuda_stream)))
+        cores = [c.reshape(c.shape[0], 2, 2, c.shape[2], order="F") for c in q.cores()]
+        self.done[key] = cores
+        return cores
 
 
-def term_cores(fac, qtt: bool):
+_QTT = _QttCache()
+
+
+def qtt_matrix(M: np.ndarray, eps: float = 1e-14, device="cuda"):
+    """QTT cores [r, 2, 2, r'] of a 2^l x 2^l matrix by libtt's device Alg. 1."""
+    return _QTT.get(np.asarray(M, dtype=np.float64), eps, device)
+
+
+def term_cores(fac, qtt: bool, device="cuda"):
     """Cores of one rank-1 term in core order (x, y, z, angle, group)."""
     if not qtt:
         return [f.reshape(1, f.shape[0], f.shape[1], 1, order="F") for f in fac]
     cores = []
     for f in fac[:-2]:
-        cores += qtt_matrix(f)
+        cores += qtt_matrix(f, device=device)
     for f in fac[-2:]:
         cores.append(f.reshape(1, f.shape[0], f.shape[1], 1, order="F"))
     return cores
@@ -180,7 +202,7 @@ def operator(prob, op: str, eps: float = 1e-13, device="cuda", qtt=None) -> TTMa
     if qtt is None:
         qtt = bool(prob.get("qtt", False))
     terms = factor_terms(prob, op)
-    return _sum_round([term_cores(f, qtt) for f in terms], eps, device)
+    return _sum_round([term_cores(f, qtt, device) for f in terms], eps, device)
 
 
 def operators(prob, eps: float = 1e-13, device="cuda", qtt=None, velocity=False):

@@ -214,10 +214,11 @@ def test_round_c2_d30_rmax128(seed):
     assert max(Y.ranks()) <= 128
 
 
-@pytest.mark.parametrize("p", [100, 200, 256])
+@pytest.mark.parametrize("p", [100, 136, 200, 256])
 def test_round_large_bond_svd(p):
     """d=2 TT with a p x p bond: the truncation SVD runs the shared-memory Jacobi
-    (p <= 112) or the grid block Jacobi (p > 112); singular values vs LAPACK."""
+    (p <= 112) or the grid block Jacobi (p > 112; p = 136 is the C4 bond
+    rmax + kickrank); singular values vs LAPACK."""
     g = inputs.rng(45 + p)
     M = g.standard_normal((p, p)) @ np.diag(np.logspace(0, -10, p)) @ g.standard_normal((p, p))
     X = [M.reshape(1, p, p), np.eye(p).reshape(p, p, 1)]

@@ -30,19 +30,6 @@ def test_factor_terms_match_oracle(gtr, prob):
                 assert np.array_equal(a, b)
 
 
-def test_qtt_alg1_host(gtr):
-    """Host Alg. 1 reproduces the displayed factors exactly in QTT."""
-    for M in (T.D_plus(8, 0.25), T.D_minus(64, 0.1), T.Ip_plus_noBC(16), T.Ip_minus(32), np.eye(4)):
-        cores = gtr.qtt_matrix(M)
-        assert np.max(np.abs(ott.ttm_full(cores) - M)) <= 1e-13 * np.abs(M).max()
-        assert max(ott.ranks(cores)) <= 3
-    g = inputs.rng(71)
-    R = g.standard_normal((8, 8))                 # generic matrix: full QTT ranks
-    cores = gtr.qtt_matrix(R)
-    assert np.max(np.abs(ott.ttm_full(cores) - R)) <= 1e-13 * np.abs(R).max()
-    assert ott.ranks(cores) == [1, 4, 4, 1]
-
-
 def test_reflective_terms_sum_to_dense(gtr):
     """Reading Z15: the rank-1 reflective terms of the host builder sum to the
     oracle's dense reflective operators (row-replacement construction)."""
