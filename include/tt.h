@@ -165,6 +165,16 @@ size_t tt_round_workspace(const tt_vec *x);
 tt_status tt_round(tt_vec *x, double eps, int32_t rmax, double *discarded_sq_dev,
                    double *sv_dev, int32_t sv_stride, void *ws, size_t wsb, tt_stream s);
 
+/* tt_round_batched: tt_round (same rule, Z21) of B independent TT-vectors x[0..B-1]
+ * (same number of cores; shapes, ranks and capacities may differ) in place,
+ * one launch per step for all instances (BASELINE.json configs[1]: B = 64 C2
+ * products).  discarded_sq_dev: [B][d-1] tail energies or NULL.  Errors as
+ * tt_round; TT_ERR_SHAPE if the core counts differ.  Workspace:
+ * tt_round_batched_workspace(B, x). */
+size_t tt_round_batched_workspace(int32_t B, const tt_vec *x);
+tt_status tt_round_batched(int32_t B, tt_vec *x, double eps, int32_t rmax, double *discarded_sq_dev,
+                           void *ws, size_t wsb, tt_stream s);
+
 /* ------------------------------------------------------------ a5, a6 ---
  * Interfaces and local operator of ALS/AMEn ("fix all but one TT
  * core").  Orientation: Phi[alpha, gamma, beta] with

@@ -132,6 +132,28 @@ extern "C" tt_status tt_round(tt_vec *x, double eps, int32_t rmax, double *disca
   return round_meta(xm, eps, rmax, discarded_sq_dev, sv_dev, sv_stride, ar, (cudaStream_t)s);
 }
 
+extern "C" size_t tt_round_batched_workspace(int32_t B, const tt_vec *x) {
+  if (B < 1 || !x) return 0;
+  std::vector<VecMeta> xm(B);
+  for (int b = 0; b < B; ++b)
+    if (make_vec_meta(x + b, xm[b]) != TT_OK) return 0;
+  Arena ar;
+  if (round_batched_meta(B, xm.data(), 0.0, 1, nullptr, 0, ar, nullptr) != TT_OK) return 0;
+  return ar.used;
+}
+
+extern "C" tt_status tt_round_batched(int32_t B, tt_vec *x, double eps, int32_t rmax, double *discarded_sq_dev,
+                                      void *ws, size_t wsb, tt_stream s) {
+  if (B < 1 || !x) return fail(TT_ERR_ARG, "tt_round_batched: B >= 1 instances required");
+  if (!ws) return fail(TT_ERR_ARG, "tt_round_batched: NULL workspace");
+  std::vector<VecMeta> xm(B);
+  for (int b = 0; b < B; ++b) TT_TRY(make_vec_meta(x + b, xm[b]));
+  Arena ar;
+  ar.base = (char *)ws;
+  ar.cap = wsb;
+  return round_batched_meta(B, xm.data(), eps, rmax, discarded_sq_dev, xm[0].d - 1, ar, (cudaStream_t)s);
+}
+
 namespace tt {
 void gemm_counters(unsigned long long *out, int reset);
 void matvec_counters(unsigned long long *out, int reset);

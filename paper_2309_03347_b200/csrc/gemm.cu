@@ -357,11 +357,15 @@ tt_status launch_variant(const GemmDesc *descs_dev, int count, int Mcap, int Nca
 // CTA, so all CTAs take identical decisions and only grid barriers separate
 // the phases (6-7 per step instead of ~8 kernel launches).
 constexpr int GF_THREADS = 128;
+#ifndef GF_ST
+#define GF_ST 2
+#endif
 #ifndef GF_BK
 #define GF_BK 16
 #endif
-using GF = Cfg<64, 64, GF_BK, 2, 2, 2>;   // persistent-kernel tiles
+using GF = Cfg<64, 64, GF_BK, 2, 2, GF_ST>;   // persistent-kernel tiles
 constexpr int GF_LD = GM_MAX_M + 2;
+constexpr int GF_MAX_GRID = 512;   // partial-sum buffer capacity (gmres_fused_part_doubles)
 // dynamic shared memory of the fused kernel: GEMM tile buffers + the apply
 // descriptors of up to GM_MAX_M steps
 constexpr size_t GM_SMEM = GF::SMEM + (size_t)3 * (GM_MAX_M + 1) * sizeof(GemmDesc);
@@ -451,7 +455,7 @@ __device__ void gemm_stage(const GemmDesc &g, double *split, long long split_ele
       const int b = t / T, tt = t - b * T;
       const GemmDesc h = gemm_batch_item(g, b);
       if (sm32) gemm_tile<32, 32, 16, 2, 2, 2>(h, (tt % tm) * 32, (tt / tm) * 32, 0, 1, nullptr, 0, 0, smem);
-      else gemm_tile<64, 64, GF_BK, 2, 2, 2>(h, (tt % tm) * 64, (tt / tm) * 64, 0, 1, nullptr, 0, 0, smem);
+      else gemm_tile<64, 64, GF_BK, 2, 2, GF_ST>(h, (tt % tm) * 64, (tt / tm) * 64, 0, 1, nullptr, 0, 0, smem);
       __syncthreads();
     }
     phase_sync<CLUSTER>(bar, G);
@@ -481,7 +485,7 @@ __device__ void gemm_stage(const GemmDesc &g, double *split, long long split_ele
   } else {
     for (int t = blockIdx.x; t < T * splits; t += G) {
       const int z = t / T, tt = t - z * T;
-      gemm_tile<64, 64, GF_BK, 2, 2, 2>(g, (tt % tm) * 64, (tt / tm) * 64, z, splits, split, g.M,
+      gemm_tile<64, 64, GF_BK, 2, 2, GF_ST>(g, (tt % tm) * 64, (tt / tm) * 64, z, splits, split, g.M,
                                         (long long)g.M * g.N, smem);
       __syncthreads();
     }
@@ -547,13 +551,26 @@ __device__ __forceinline__ void cross_cta_sum(const double *part, int G, int n, 
       for (int c = 0; c < G; ++c) s += sred[c * n + i];
       out[i] = s;
     }
-  } else {   // large grids: one warp per entry, lanes over the CTAs (fixed order)
+  } else {   // large grids: lanes over the CTAs (fixed order), each warp a group of 8
+             // entries with all their loads in flight (one entry at a time paid one
+             // L2 round trip per entry: ~13 us per reduction at 256 CTAs, 40 entries)
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    for (int i = warp; i < n; i += GF_THREADS / 32) {
-      double s = 0.0;
-      for (int c = lane; c < G; c += 32) s += part[(size_t)c * GF_LD + i];
-      s = warp_sum(s);
-      if (lane == 0) out[i] = s;
+    for (int i0 = warp * 8; i0 < n; i0 += (GF_THREADS / 32) * 8) {
+      double acc[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) acc[q] = 0.0;
+#pragma unroll 2
+      for (int c = lane; c < G; c += 32) {
+        const double *pc = part + (size_t)c * GF_LD + i0;
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          if (i0 + q < n) acc[q] += pc[q];
+      }
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const double s = warp_sum(acc[q]);
+        if (lane == 0 && i0 + q < n) out[i0 + q] = s;
+      }
     }
   }
   __syncthreads();
@@ -864,8 +881,10 @@ int gmres_fused_grid() {
     const char *e = std::getenv("TT_GF_GRID");
     // two CTAs per SM when they fit (more bytes in flight for the CGS2 phases of
     // large local systems; measured +4% on C4)
+    // all SMs equally loaded: 2 CTAs on each of the 148 SMs (296), not 256 (which
+    // left 40 SMs with one CTA and made the tile rounds uneven)
     G = (occ >= 1) ? (e ? std::atoi(e) : (occ >= 2 ? 2 * sms : sms)) : -1;
-    if (G > occ * sms || G > 256) G = occ * sms < 256 ? occ * sms : 256;
+    if (G > occ * sms || G > GF_MAX_GRID) G = occ * sms < GF_MAX_GRID ? occ * sms : GF_MAX_GRID;
   }
   return G;
 }

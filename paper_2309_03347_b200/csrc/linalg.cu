@@ -643,7 +643,9 @@ __device__ void grid_barrier(unsigned int *bar, unsigned int nblocks) {
       __threadfence();
       atomicAdd(bar + 1, 1u);
     } else {
+      const long long t0 = clock64();
       while (*gen == g) {
+        if (clock64() - t0 > 8000000000LL) __trap();   // never hang the device (~4 s)
       }
     }
     __threadfence();

@@ -3,7 +3,9 @@
 // "plan" kernel that reads the current ranks and writes the descriptors of
 // the step's QR / SVD / GEMM / copy kernels into the workspace; nothing is
 // read back to the host, so the whole sweep is graph-capturable.
+#include <algorithm>
 #include <cmath>
+#include <vector>
 
 #include "tt_common.cuh"
 
@@ -15,8 +17,9 @@ struct StepWS {
   double *A, *Q, *R, *tau, *T, *U, *V, *S, *J, *QU, *tmp;
   QRDesc *qd;
   SVDDesc *sd;
-  GemmDesc *gd;   // [2]
-  CopyDesc *cd;   // [2]
+  GemmDesc *gd;   // [2]: slot s at gd[s * bs]
+  CopyDesc *cd;   // [2]: slot s at cd[s * bs]
+  int bs;         // batch stride of the descriptor slots (1 unbatched, B in tt_round_batched)
   int *iv;        // [8] step integers (wide flag, sizes)
   double *norm;   // [1]
   unsigned int *bar;  // [4] grid barrier of the block Jacobi
@@ -87,6 +90,7 @@ StepWS carve(const VecMeta &x, Arena &ar) {
   w.sd = ar.take<SVDDesc>(1);
   w.gd = ar.take<GemmDesc>(2);
   w.cd = ar.take<CopyDesc>(2);
+  w.bs = 1;
   w.iv = ar.take<int>(8);
   w.norm = ar.take<double>(1);
   w.bar = ar.take<unsigned int>(4);
@@ -118,7 +122,7 @@ __device__ CopyDesc copy_desc(int rows, int cols, const double *src, long long s
 }
 
 // ---- right-to-left orthogonalisation step at core k (k >= 1)
-__global__ void plan_orth_rl(const VecMeta x, int k, StepWS w) {
+__device__ __forceinline__ void plan_orth_rl_d(const VecMeta &x, int k, const StepWS &w) {
   const int r0 = x.r[k], n = x.n[k], r1 = x.r[k + 1];
   const int rp = x.r[k - 1], np = x.n[k - 1];
   const int m = n * r1, p = r0, q = min(m, p);
@@ -138,7 +142,7 @@ __global__ void plan_orth_rl(const VecMeta x, int k, StepWS w) {
 }
 
 // ---- left-to-right orthogonalisation step at core k (k <= d-2)
-__global__ void plan_orth_lr(const VecMeta x, int k, StepWS w) {
+__device__ __forceinline__ void plan_orth_lr_d(const VecMeta &x, int k, const StepWS &w) {
   const int r0 = x.r[k], n = x.n[k], r1 = x.r[k + 1];
   const int n2 = x.n[k + 1], r2 = x.r[k + 2];
   const int m = r0 * n, p = r1, q = min(m, p);
@@ -157,7 +161,7 @@ __global__ void plan_orth_lr(const VecMeta x, int k, StepWS w) {
   x.r[k + 1] = q;
 }
 
-__global__ void core_norm_kernel(const VecMeta x, int k, double *out, double *out2) {
+__device__ __forceinline__ void core_norm_d(const VecMeta &x, int k, double *out, double *out2) {
   __shared__ double red[32];
   const int total = x.r[k] * x.n[k] * x.r[k + 1];
   const double *c = x.data + x.off[k];
@@ -177,7 +181,7 @@ __global__ void core_norm_kernel(const VecMeta x, int k, double *out, double *ou
 }
 
 // ---- truncation step at core k (k <= d-2): SVD of the left unfolding
-__global__ void plan_trunc(const VecMeta x, int k, StepWS w) {
+__device__ __forceinline__ void plan_trunc_d(const VecMeta &x, int k, const StepWS &w) {
   const int r0 = x.r[k], n = x.n[k], r1 = x.r[k + 1];
   const int m0 = r0 * n, p0 = r1;
   const int wide = m0 < p0;
@@ -210,8 +214,8 @@ __global__ void plan_trunc(const VecMeta x, int k, StepWS w) {
   w.iv[0] = wide; w.iv[1] = p; w.iv[2] = m0; w.iv[3] = p0;
 }
 
-__global__ void trunc_kernel(const VecMeta x, int k, StepWS w, double eps, int rmax, double *disc,
-                             double *sv, int sv_stride) {
+__device__ __forceinline__ void trunc_d(const VecMeta &x, int k, const StepWS &w, double eps, int rmax,
+                                        double *disc, double *sv, int sv_stride) {
   __shared__ int s_r;
   const int wide = w.iv[0], p = w.iv[1], m0 = w.iv[2], p0 = w.iv[3];
   const int tid = threadIdx.x;
@@ -254,15 +258,38 @@ __global__ void trunc_kernel(const VecMeta x, int k, StepWS w, double eps, int r
     double *next = x.data + x.off[k + 1];
     if (!wide) {
       w.gd[0] = gemm_desc(m0, r, p, w.Q, m0, 0, w.U, p, 0, core, m0);
-      w.gd[1] = gemm_desc(r, n2 * r2, p0, w.V, p, 1, next, p0, 0, w.tmp, r);
+      w.gd[w.bs] = gemm_desc(r, n2 * r2, p0, w.V, p, 1, next, p0, 0, w.tmp, r);
       w.cd[0] = copy_desc(0, 0, nullptr, 0, 0, nullptr, 0, 0);
     } else {
       w.gd[0] = gemm_desc(p0, r, m0, w.Q, p0, 0, w.U, m0, 0, w.QU, p0);
       w.cd[0] = copy_desc(m0, r, w.V, 1, p, core, 1, m0);
-      w.gd[1] = gemm_desc(r, n2 * r2, p0, w.QU, p0, 1, next, p0, 0, w.tmp, r);
+      w.gd[w.bs] = gemm_desc(r, n2 * r2, p0, w.QU, p0, 1, next, p0, 0, w.tmp, r);
     }
-    w.cd[1] = copy_desc(r, n2 * r2, w.tmp, 1, r, next, 1, r);
+    w.cd[w.bs] = copy_desc(r, n2 * r2, w.tmp, 1, r, next, 1, r);
   }
+}
+
+// single-instance kernels and their batched forms (instance = blockIdx.x)
+__global__ void plan_orth_rl(const VecMeta x, int k, StepWS w) { plan_orth_rl_d(x, k, w); }
+__global__ void plan_orth_lr(const VecMeta x, int k, StepWS w) { plan_orth_lr_d(x, k, w); }
+__global__ void plan_trunc(const VecMeta x, int k, StepWS w) { plan_trunc_d(x, k, w); }
+__global__ void core_norm_kernel(const VecMeta x, int k, double *out, double *out2) { core_norm_d(x, k, out, out2); }
+__global__ void trunc_kernel(const VecMeta x, int k, StepWS w, double eps, int rmax, double *disc, double *sv,
+                             int sv_stride) {
+  trunc_d(x, k, w, eps, rmax, disc, sv, sv_stride);
+}
+__global__ void plan_orth_rl_b(const VecMeta *xs, int k, const StepWS *ws) {
+  if (k < xs[blockIdx.x].d) plan_orth_rl_d(xs[blockIdx.x], k, ws[blockIdx.x]);
+}
+__global__ void plan_trunc_b(const VecMeta *xs, int k, const StepWS *ws) {
+  plan_trunc_d(xs[blockIdx.x], k, ws[blockIdx.x]);
+}
+__global__ void core_norm_b(const VecMeta *xs, const StepWS *ws) {
+  core_norm_d(xs[blockIdx.x], 0, nullptr, ws[blockIdx.x].norm);
+}
+__global__ void trunc_b(const VecMeta *xs, int k, const StepWS *ws, double eps, int rmax, double *disc, int dstride) {
+  trunc_d(xs[blockIdx.x], k, ws[blockIdx.x], eps, rmax, disc ? disc + (long long)blockIdx.x * dstride : nullptr,
+          nullptr, 0);
 }
 
 }  // namespace
@@ -326,6 +353,78 @@ tt_status round_meta(const VecMeta &x, double eps, int rmax, double *disc, doubl
   }
   (void)c;
   return check_launch("tt_round");
+}
+
+// ----------------------------------------------------- batched rounding ---
+// B independent TT-vectors of the same number of cores rounded together: every
+// orthogonalisation / truncation step is one plan launch over the B instances
+// (grid B), one QR launch with B descriptors (one CTA per instance), one
+// Jacobi launch with B descriptors, and batched GEMM / copy launches (grid z =
+// instance) — 4 + 8 launches per core instead of B times that, and the B
+// latency-bound QR / SVD chains run side by side on the SMs.
+tt_status round_batched_meta(int B, const VecMeta *xs, double eps, int rmax, double *disc, int dstride, Arena &ar,
+                             cudaStream_t s) {
+  if (B < 1) return fail(TT_ERR_ARG, "tt_round_batched: B must be >= 1");
+  if (eps < 0.0 || !(eps == eps)) return fail(TT_ERR_ARG, "tt_round_batched: eps must be >= 0");
+  if (rmax < 1) return fail(TT_ERR_ARG, "tt_round_batched: rmax must be >= 1");
+  const int d = xs[0].d;
+  for (int b = 1; b < B; ++b)
+    if (xs[b].d != d) return fail(TT_ERR_SHAPE, "tt_round_batched: instances must have the same number of cores");
+  std::vector<StepWS> w(B);
+  for (int b = 0; b < B; ++b) w[b] = carve(xs[b], ar);
+  QRDesc *qd = ar.take<QRDesc>(B);
+  SVDDesc *sd = ar.take<SVDDesc>(B);
+  GemmDesc *gd = ar.take<GemmDesc>(2 * B);
+  CopyDesc *cd = ar.take<CopyDesc>(2 * B);
+  VecMeta *xd = ar.take<VecMeta>(B);
+  StepWS *wd = ar.take<StepWS>(B);
+  if (!ar.base) return TT_OK;
+  if (!ar.ok()) return fail(TT_ERR_CAPACITY, "tt_round_batched: workspace too small");
+  for (int b = 0; b < B; ++b) {
+    w[b].qd = qd + b;
+    w[b].sd = sd + b;
+    w[b].gd = gd + b;
+    w[b].cd = cd + b;
+    w[b].bs = B;
+  }
+  // pageable source: cudaMemcpyAsync returns once the host arrays have been consumed
+  if (cudaMemcpyAsync(xd, xs, sizeof(VecMeta) * B, cudaMemcpyHostToDevice, s) != cudaSuccess ||
+      cudaMemcpyAsync(wd, w.data(), sizeof(StepWS) * B, cudaMemcpyHostToDevice, s) != cudaSuccess)
+    return fail(TT_ERR_CUDA, "tt_round_batched: descriptor upload");
+  auto cap_max = [&](auto f) {
+    long long v = 0;
+    for (int b = 0; b < B; ++b) v = std::max<long long>(v, f(xs[b]));
+    return v;
+  };
+  // right-to-left orthogonalisation
+  for (int k = d - 1; k >= 1; --k) {
+    plan_orth_rl_b<<<B, 1, 0, s>>>(xd, k, wd);
+    TT_TRY(launch_qr(qd, B, s));
+    const int Mc = (int)cap_max([&](const VecMeta &x) { return (long long)x.rcap[k - 1] * x.n[k - 1]; });
+    const int Nc = (int)cap_max([&](const VecMeta &x) { return (long long)x.rcap[k]; });
+    TT_TRY(launch_gemm(gd, B, Mc, Nc, s));
+    TT_TRY(launch_copy(cd, B, cap_max([&](const VecMeta &x) {
+      return (long long)x.rcap[k - 1] * x.n[k - 1] * x.rcap[k]; }), s));
+  }
+  core_norm_b<<<B, 256, 0, s>>>(xd, wd);
+  // left-to-right truncation
+  for (int k = 0; k <= d - 2; ++k) {
+    const int m0c = (int)cap_max([&](const VecMeta &x) { return (long long)x.rcap[k] * x.n[k]; });
+    const int p0c = (int)cap_max([&](const VecMeta &x) { return (long long)x.rcap[k + 1]; });
+    const int pcap = (int)cap_max([&](const VecMeta &x) {
+      const long long a = (long long)x.rcap[k] * x.n[k], c = x.rcap[k + 1];
+      return a < c ? a : c; });
+    plan_trunc_b<<<B, 1, 0, s>>>(xd, k, wd);
+    TT_TRY(launch_qr(qd, B, s));
+    TT_TRY(launch_jacobi(sd, B, pcap, pcap, s));
+    trunc_b<<<B, 256, 0, s>>>(xd, k, wd, eps, rmax, disc, dstride);
+    TT_TRY(launch_gemm(gd, B, m0c > p0c ? m0c : p0c, p0c, s));
+    TT_TRY(launch_copy(cd, B, (long long)m0c * p0c, s));
+    const int n2r2 = (int)cap_max([&](const VecMeta &x) { return (long long)x.n[k + 1] * x.rcap[k + 2]; });
+    TT_TRY(launch_gemm(gd + B, B, p0c, n2r2, s));
+    TT_TRY(launch_copy(cd + B, B, (long long)p0c * n2r2, s));
+  }
+  return check_launch("tt_round_batched");
 }
 
 }  // namespace tt

@@ -208,6 +208,8 @@ tt_status dot_meta(const VecMeta &x, const VecMeta &y, double *out, Arena &ar, c
 tt_status orth_meta(const VecMeta &x, int dir, double *norm_dev, Arena &ar, cudaStream_t s);
 tt_status round_meta(const VecMeta &x, double eps, int rmax, double *disc, double *sv, int sv_stride,
                      Arena &ar, cudaStream_t s);
+tt_status round_batched_meta(int B, const VecMeta *xs, double eps, int rmax, double *disc, int dstride, Arena &ar,
+                             cudaStream_t s);
 
 int max_slot(const VecMeta &x);      // max_k rcap[k] n_k rcap[k+1]
 int max_rank(const VecMeta &x);

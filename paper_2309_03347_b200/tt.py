@@ -255,6 +255,31 @@ def tt_round(x: TTVec, eps: float, rmax: int = 1 << 30, want_info: bool = False,
     return x
 
 
+class RoundBatch:
+    """Marshalled arguments of one batched rounding (tt_round_batched): the ctypes
+    descriptor array and the workspace are built once; each call is one ABI call."""
+
+    def __init__(self, xs):
+        self.B = len(xs)
+        self.keep = xs
+        self.xc = (_lib.tt_vec * self.B)(*[v._c for v in xs])
+        nb = lib().tt_round_batched_workspace(self.B, self.xc)
+        if nb == 0:
+            raise TTError(1, "tt_round_batched: workspace query rejected the instances")
+        self.ws = torch.empty(int(nb), dtype=torch.uint8, device=xs[0].device)
+        self.disc = torch.zeros(self.B * max(xs[0].d - 1, 1), dtype=F64, device=xs[0].device)
+
+    def __call__(self, eps: float, rmax: int = 1 << 30, stream=None):
+        check(lib().tt_round_batched(self.B, self.xc, float(eps), int(min(rmax, 2**31 - 1)), _ptr(self.disc),
+                                     _ptr(self.ws), self.ws.numel(), C.c_void_p(_stream(stream))))
+        return self.disc.view(self.B, -1)
+
+
+def tt_round_batched(xs, eps: float, rmax: int = 1 << 30, stream=None):
+    """tt_round of B independent TT-vectors in place, one launch per step for all."""
+    return RoundBatch(xs)(eps, rmax, stream)
+
+
 def als_local_apply(dims, Phi, Ak, Psi, x, y, stream=None):
     """dims = (rA, R, rB, m, n, rAp, Rp, rBp); arrays are flat device tensors."""
     nb = lib().als_workspace(*dims)

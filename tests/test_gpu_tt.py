@@ -214,6 +214,40 @@ def test_round_c2_d30_rmax128(seed):
     assert max(Y.ranks()) <= 128
 
 
+def test_round_batched_c2():
+    """tt_round_batched (configs[1]: independent C2 products rounded together, one
+    launch per step for all): every instance matches the oracle's tt_round —
+    same ranks, tail energies (error identity) to 1e-10 relative, and the rounded
+    tensor to 1e-12 ||X|| (absent near-ties at the cut) — plus a d=10 batch with
+    ragged shapes where rmax does not bind (eps bound)."""
+    seeds = list(range(6))
+    insts = [inputs.c2_instance(sd) for sd in seeds]
+    Ys = [tb.matvec_out(tb.TTMat.from_cores(i["A"]), tb.TTVec.from_cores(i["X"])) for i in insts]
+    disc = tb.tt_round_batched(Ys, 1e-8, 128)
+    torch.cuda.synchronize()
+    for b, inst in enumerate(insts):
+        ref, info = ott.tt_round(ott.tt_matvec_fast(inst["A"], inst["X"]), 1e-8, 128)
+        assert Ys[b].ranks() == ott.ranks(ref), b
+        nrm = info["norm"]
+        got_disc = disc[b].cpu().numpy()
+        assert np.max(np.abs(got_disc - np.array(info["discarded_sq"]))) <= 1e-10 * nrm ** 2, b
+        ties = any(r < len(sv) and abs(sv[r - 1] - sv[r]) <= 1e-10 * info["sv"][0][0]
+                   for r, sv in zip(ott.ranks(ref)[1:-1], info["sv"]))
+        if not ties:
+            assert tt_diff_norm(Ys[b].cores(), ref) <= 1e-12 * nrm + math.sqrt(sum(info["discarded_sq"])) * 1e-6, b
+    # d = 10 slices (different ranks per instance), rmax not binding: eps bound
+    sl = [inputs.c2_slice(200 + q) for q in range(3)]
+    Xs = [ott.tt_matvec_fast(i["A"], i["X"]) for i in sl]
+    Gs = [tb.TTVec.from_cores(X) for X in Xs]
+    tb.tt_round_batched(Gs, 1e-3)
+    torch.cuda.synchronize()
+    for G, X in zip(Gs, Xs):
+        full = ott.tt_full(X)
+        ref, _ = ott.tt_round(X, 1e-3)
+        assert G.ranks() == ott.ranks(ref)
+        assert np.linalg.norm(ott.tt_full(G.cores()) - full) <= 1e-3 * np.linalg.norm(full) * (1 + 1e-12)
+
+
 @pytest.mark.parametrize("p", [100, 136, 200, 256])
 def test_round_large_bond_svd(p):
     """d=2 TT with a p x p bond: the truncation SVD runs the shared-memory Jacobi
