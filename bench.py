@@ -205,6 +205,7 @@ def main():
     ap.add_argument("--rank", type=int, default=128, help="c5 interface rank (64, 128, 256)")
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-graph", action="store_true", help="c5: launch the sweep without a CUDA graph")
+    ap.add_argument("--one-stream", action="store_true", help="c5: applies and updates on one stream")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
@@ -418,7 +419,7 @@ def micro_bench(args, tb, device, world, dist):
         sp.build_right()
         run = sp.double_sweep
         if not args.no_graph:
-            run = sp.capture().replay
+            run = sp.capture(two_streams=not args.one_stream).replay
         for _ in range(args.warmup):
             run()
         ms = []
@@ -440,7 +441,9 @@ def micro_bench(args, tb, device, world, dist):
                 "vs_baseline": None, "dtype": "f64", "data": "synthetic",
                 "config": {"workload": f"C5 (configs[4]) ALS double sweep, d=40, r={args.rank}, R 5-8, "
                                        f"n in {{2,4,8,16}}, seed {args.seed}",
-                           "launch": "CUDA graph of the 80 core visits" if not args.no_graph else "stream",
+                           "launch": ("CUDA graph of the 80 core visits" + (", applies on a side stream beside the "
+                                      "interface-update chain" if not args.one_stream else ", one stream"))
+                                     if not args.no_graph else "stream",
                            "l2": "256 MB flush between timed steps"},
                 "pct_dmma_peak": 100.0 * gfl / peak, "flops_per_step": flops, "ms_p10_p90": [
                     float(np.percentile(ms, 10)), float(np.percentile(ms, 90))],
@@ -736,7 +739,7 @@ def extras(args, tb, device, world):
     import copy
     out = {}
     a = copy.copy(args)
-    a.workload, a.rank, a.no_graph = "c5", 256, False
+    a.workload, a.rank, a.no_graph, a.one_stream = "c5", 256, False, False
     a.steps, a.warmup = max(5, min(args.steps, 10)), 3
     l5 = micro_bench(a, tb, device, world, None)
     out["c5_r256"] = {"value": l5["value"], "unit": l5["unit"], "pct_dmma_peak": l5["pct_dmma_peak"],

@@ -148,6 +148,11 @@ tt_status tt_dot(const tt_vec *x, const tt_vec *y, double *out_dev, void *ws, si
  * norm_dev (may be NULL) receives ||x||_F = ||orthogonality centre||_F.
  * Workspace: tt_orthogonalize_workspace(x). */
 size_t tt_orthogonalize_workspace(const tt_vec *x);
+/* tt_normalize: x <- x / ||x||_F (right-to-left orthogonalisation, then the first
+ * core scaled by the reciprocal of the norm, read on the device); ||x||_F is
+ * written to norm_dev (device, [1]).  Workspace: tt_orthogonalize_workspace(x).
+ * Used for the per-interface normalisation of reading Z25. */
+tt_status tt_normalize(tt_vec *x, double *norm_dev, void *ws, size_t wsb, tt_stream s);
 tt_status tt_orthogonalize(tt_vec *x, int32_t dir, double *norm_dev, void *ws, size_t wsb,
                            tt_stream s);
 

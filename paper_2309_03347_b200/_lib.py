@@ -106,6 +106,7 @@ SIG = {
     "tt_transport_terms": (I32, [I32, I32, C.c_double, I32, I32, P, P, P, P, I32, P, P, P, P, I32, P, P, P, P]),
     "tt_transport_terms_reflective": (I32, [I32, I32, C.c_double, I32, I32, P, P, P, P, I32, P, P, P, P, I32, P, P,
                                             P, P]),
+    "tt_normalize": (I32, [C.POINTER(tt_vec), P, P, C.c_size_t, P]),
     "tt_round_batched_workspace": (C.c_size_t, [I32, C.POINTER(tt_vec)]),
     "tt_round_batched": (I32, [I32, C.POINTER(tt_vec), C.c_double, I32, P, P, C.c_size_t, P]),
     "tt_qtt_matrix_dev_workspace": (C.c_size_t, [C.POINTER(tt_vec)]),

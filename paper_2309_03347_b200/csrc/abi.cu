@@ -112,6 +112,17 @@ extern "C" tt_status tt_orthogonalize(tt_vec *x, int32_t dir, double *norm_dev, 
   return orth_meta(xm, dir, norm_dev, ar, (cudaStream_t)s);
 }
 
+extern "C" tt_status tt_normalize(tt_vec *x, double *norm_dev, void *ws, size_t wsb, tt_stream s) {
+  VecMeta xm;
+  TT_TRY(make_vec_meta(x, xm));
+  if (!ws || !norm_dev) return fail(TT_ERR_ARG, "tt_normalize: NULL workspace or norm");
+  Arena ar;
+  ar.base = (char *)ws;
+  ar.cap = wsb;
+  TT_TRY(orth_meta(xm, -1, norm_dev, ar, (cudaStream_t)s));
+  return scale_meta(xm, norm_dev, 1.0, 1, (cudaStream_t)s);
+}
+
 extern "C" size_t tt_round_workspace(const tt_vec *x) {
   VecMeta xm;
   if (make_vec_meta(x, xm) != TT_OK) return 0;

@@ -8,7 +8,7 @@ from __future__ import annotations
 import numpy as np
 import torch
 
-from .tt import als_local_apply, als_update_interfaces
+from .tt import TTVec, als_local_apply, als_update_interfaces, tt_normalize
 
 
 class SweepProblem:
@@ -40,10 +40,15 @@ class SweepProblem:
         for k in range(self.d - 1, 0, -1):
             als_update_interfaces(-1, self.dims_apply(k), self.Psi[k + 1], self.X[k], self.A[k], self.X[k],
                                   self.Psi[k])
-            if normalize:
-                self.Psi[k].div_(self.Psi[k].norm())
+            if normalize:   # Z25, by libtt (the interface viewed as a one-core TT-vector)
+                v = TTVec([self.Psi[k].numel()], [1, 1], self.X[0].device)
+                v.data = self.Psi[k]
+                v._c.data = self.Psi[k].data_ptr()
+                tt_normalize(v)
 
-    def double_sweep(self):
+    def double_sweep(self, two_streams=False):
+        if two_streams:
+            return self._double_sweep_2s()
         for k in range(self.d - 1):
             als_local_apply(self.dims_apply(k), self.Phi[k], self.A[k], self.Psi[k + 1], self.X[k], self.y)
             als_update_interfaces(+1, self.dims_apply(k), self.Phi[k], self.X[k], self.A[k], self.X[k],
@@ -53,7 +58,40 @@ class SweepProblem:
             als_update_interfaces(-1, self.dims_apply(k), self.Psi[k + 1], self.X[k], self.A[k], self.X[k],
                                   self.Psi[k])
 
-    def capture(self):
+    def _double_sweep_2s(self):
+        """The same double sweep with the local applies off the critical path: the
+        interface updates (the dependent chain Phi_k -> Phi_{k+1}) stay on the
+        current stream, each apply runs on a side stream as soon as the interface
+        it reads is complete (an event per core), with its own workspace; the
+        side stream joins at the end (graph-capturable fork/join)."""
+        from . import _lib
+        main = torch.cuda.current_stream()
+        if getattr(self, "side", None) is None:
+            need = max(_lib.lib().als_workspace(*self.dims_apply(k)) for k in range(self.d))
+            self.side = torch.cuda.Stream(device=self.X[0].device)
+            self.ws_side = torch.empty(need, dtype=torch.uint8, device=self.X[0].device)
+            self.ws_main = torch.empty(need, dtype=torch.uint8, device=self.X[0].device)
+        side = self.side
+
+        def apply_async(k):
+            ev = torch.cuda.Event()
+            ev.record(main)
+            side.wait_event(ev)
+            with torch.cuda.stream(side):
+                als_local_apply(self.dims_apply(k), self.Phi[k], self.A[k], self.Psi[k + 1], self.X[k], self.y,
+                                stream=side, ws=self.ws_side)
+
+        for k in range(self.d - 1):
+            apply_async(k)
+            als_update_interfaces(+1, self.dims_apply(k), self.Phi[k], self.X[k], self.A[k], self.X[k],
+                                  self.Phi[k + 1], stream=main, ws=self.ws_main)
+        for k in range(self.d - 1, 0, -1):
+            apply_async(k)
+            als_update_interfaces(-1, self.dims_apply(k), self.Psi[k + 1], self.X[k], self.A[k], self.X[k],
+                                  self.Psi[k], stream=main, ws=self.ws_main)
+        main.wait_stream(side)
+
+    def capture(self, two_streams=True):
         """Record one double sweep into a CUDA graph (the sequence of libtt launches
         is fixed for fixed shapes); replay with self.graph.replay()."""
         from .tt import workspace
@@ -63,12 +101,12 @@ class SweepProblem:
         s = torch.cuda.Stream()
         s.wait_stream(torch.cuda.current_stream())
         with torch.cuda.stream(s):
-            self.double_sweep()                    # warm (cudaFuncSetAttribute etc.)
+            self.double_sweep(two_streams)         # warm (cudaFuncSetAttribute etc.)
         torch.cuda.current_stream().wait_stream(s)
         torch.cuda.synchronize()
         self.graph = torch.cuda.CUDAGraph()
         with torch.cuda.graph(self.graph):
-            self.double_sweep()
+            self.double_sweep(two_streams)
         return self.graph
 
     def flops(self):

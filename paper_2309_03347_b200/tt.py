@@ -255,6 +255,16 @@ def tt_round(x: TTVec, eps: float, rmax: int = 1 << 30, want_info: bool = False,
     return x
 
 
+def tt_normalize(x: TTVec, norm: Optional[torch.Tensor] = None, stream=None):
+    """x <- x / ||x||_F on the device; returns the norm (device tensor)."""
+    if norm is None:
+        norm = torch.zeros(1, dtype=F64, device=x.device)
+    nb = lib().tt_orthogonalize_workspace(x.c)
+    ws = workspace(nb, x.device)
+    check(lib().tt_normalize(x.c, _ptr(norm), _ptr(ws), ws.numel(), C.c_void_p(_stream(stream))))
+    return norm
+
+
 class RoundBatch:
     """Marshalled arguments of one batched rounding (tt_round_batched): the ctypes
     descriptor array and the workspace are built once; each call is one ABI call."""
@@ -280,19 +290,22 @@ def tt_round_batched(xs, eps: float, rmax: int = 1 << 30, stream=None):
     return RoundBatch(xs)(eps, rmax, stream)
 
 
-def als_local_apply(dims, Phi, Ak, Psi, x, y, stream=None):
-    """dims = (rA, R, rB, m, n, rAp, Rp, rBp); arrays are flat device tensors."""
+def als_local_apply(dims, Phi, Ak, Psi, x, y, stream=None, ws=None):
+    """dims = (rA, R, rB, m, n, rAp, Rp, rBp); arrays are flat device tensors.
+    ws: dedicated uint8 workspace (>= als_workspace bytes) for concurrent calls."""
     nb = lib().als_workspace(*dims)
-    ws = workspace(nb, x.device)
+    if ws is None:
+        ws = workspace(nb, x.device)
     check(lib().als_local_apply(*[int(v) for v in dims], _ptr(Phi), _ptr(Ak), _ptr(Psi), _ptr(x), _ptr(y),
                                 _ptr(ws), ws.numel(), C.c_void_p(_stream(stream))))
     return y
 
 
-def als_update_interfaces(direction, dims, Iprev, Yk, Ak, Xk, Inext, stream=None):
+def als_update_interfaces(direction, dims, Iprev, Yk, Ak, Xk, Inext, stream=None, ws=None):
     """dims = (rY, R, rX, m, n, rYp, Rp, rXp); Ak = None for the vector interface."""
     nb = lib().als_workspace(*dims)
-    ws = workspace(nb, Yk.device)
+    if ws is None:
+        ws = workspace(nb, Yk.device)
     check(lib().als_update_interfaces(int(direction), *[int(v) for v in dims], _ptr(Iprev), _ptr(Yk), _ptr(Ak),
                                       _ptr(Xk), _ptr(Inext), _ptr(ws), ws.numel(), C.c_void_p(_stream(stream))))
     return Inext
