@@ -507,7 +507,7 @@ static tt_status carve_amen(const MatMeta &A, const VecMeta &b, const VecMeta &x
   P.H = ar.take<double>((size_t)(m + 1) * m);
   P.h1 = ar.take<double>(m + 1);
   P.h2 = ar.take<double>(m + 1);
-  P.gpart = ar.take<double>(gmres_fused_part_doubles(512));
+  P.gpart = ar.take<double>(gmres_fused_part_doubles(1024));
   P.gbar = ar.take<unsigned int>(4);
   // orthogonalisation scratch (x or z)
   Arena c1, c2;

@@ -365,7 +365,7 @@ constexpr int GF_THREADS = 128;
 #endif
 using GF = Cfg<64, 64, GF_BK, 2, 2, GF_ST>;   // persistent-kernel tiles
 constexpr int GF_LD = GM_MAX_M + 2;
-constexpr int GF_MAX_GRID = 512;   // partial-sum buffer capacity (gmres_fused_part_doubles)
+constexpr int GF_MAX_GRID = 1024;   // partial-sum buffer capacity (gmres_fused_part_doubles)
 // dynamic shared memory of the fused kernel: GEMM tile buffers + the apply
 // descriptors of up to GM_MAX_M steps
 constexpr size_t GM_SMEM = GF::SMEM + (size_t)3 * (GM_MAX_M + 1) * sizeof(GemmDesc);
@@ -577,7 +577,10 @@ __device__ __forceinline__ void cross_cta_sum(const double *part, int G, int n, 
 }
 
 template <bool CLUSTER>
-__global__ void __launch_bounds__(GF_THREADS) gm_chunk_kernel(GmChunkArgs a) {
+#ifndef GF_MINB
+#define GF_MINB 1
+#endif
+__global__ void __launch_bounds__(GF_THREADS, GF_MINB) gm_chunk_kernel(GmChunkArgs a) {
   extern __shared__ __align__(16) double smem[];
   __shared__ double h1s[GF_LD], h2s[GF_LD], css[GF_LD], sns[GF_LD];
   double *sred = smem;   // the GEMM tile buffers are idle during the vector phases

@@ -7,6 +7,8 @@
 // descriptors in device memory (they follow device-resident TT ranks).
 #include <cfloat>
 
+#include <cooperative_groups.h>
+
 #include "tt_common.cuh"
 
 namespace tt {
@@ -623,6 +625,157 @@ __global__ void __launch_bounds__(1024) jacobi_kernel(const SVDDesc *__restrict_
   for (int c = tid; c < p; c += blockDim.x) g.sigma[s_pos[c]] = s_sig[c];
 }
 
+// ------------------------------------ cluster Jacobi (distributed shared memory) ---
+// The one-sided round-robin Jacobi of jacobi_core spread over a thread-block
+// cluster: column c of W (and of V) lives in the shared memory of CTA c % C at
+// slot c / C; every warp of the cluster takes pairs of a round (warp-global
+// index over the cluster) and reads / rotates its two columns through
+// distributed shared memory (generic pointers from map_shared_rank), and a
+// hardware cluster barrier separates the rounds (the grid version paid a
+// software grid barrier and a global-memory round trip of every block per
+// round).  One cluster per problem (grid = count x C).  Same rotation, test and
+// ordering as jacobi_core, so the same sweep count on the same input.
+constexpr int JC_MAXC = 16;
+constexpr int JC_R = 10;   // rows per lane held in registers: m, p <= 320
+__global__ void __launch_bounds__(512) jacobi_cluster_kernel(const SVDDesc *__restrict__ descs, int C) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cl = cg::this_cluster();
+  extern __shared__ __align__(16) double jsm[];
+  __shared__ int s_flag;
+  __shared__ double s_sig[2];   // unused placeholder (sigma lives in jsm)
+  const int rank = (int)cl.block_rank();
+  const SVDDesc g = descs[blockIdx.x / C];
+  const int m = g.m, p = g.p, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int NW = blockDim.x >> 5, NWC = NW * C;
+  const int ncl = (p + C - 1) / C;             // local column slots
+  const bool wantv = g.V != nullptr;
+  double *sW = jsm;                            // ncl x m
+  double *sV = sW + (size_t)ncl * m;           // ncl x p
+  double *sig = sV + (wantv ? (size_t)ncl * p : 0);   // p (all sigmas, gathered)
+  int *pos = reinterpret_cast<int *>(sig + p); // p
+  auto colW = [&](int c) -> double * { return cl.map_shared_rank(sW + (size_t)(c / C) * m, c % C); };
+  auto colV = [&](int c) -> double * { return cl.map_shared_rank(sV + (size_t)(c / C) * p, c % C); };
+  // load the local columns of W, V = I
+  for (int e = tid; e < ncl * m; e += blockDim.x) {
+    const int q = e / m, r = e - q * m, c = q * C + rank;
+    sW[e] = c < p ? g.W[r + (long long)c * g.ldw] : 0.0;
+  }
+  if (wantv)
+    for (int e = tid; e < ncl * p; e += blockDim.x) {
+      const int q = e / p, r = e - q * p, c = q * C + rank;
+      sV[e] = (c < p && r == c) ? 1.0 : 0.0;
+    }
+  if (tid == 0) s_flag = 0;
+  cl.sync();
+  const int P2 = p + (p & 1);
+  const double tol = 4.0 * DBL_EPSILON;
+  unsigned long long fl = 0;
+  int sweep = 0;
+  for (; sweep < 60; ++sweep) {
+    for (int rnd = 0; rnd < P2 - 1; ++rnd) {
+      for (int pr = rank * NW + warp; pr < P2 / 2; pr += NWC) {
+        int a, b;
+        if (pr == 0) { a = P2 - 1; b = rnd; }
+        else { a = (rnd + pr) % (P2 - 1); b = (rnd - pr + (P2 - 1)) % (P2 - 1); }
+        if (a >= p || b >= p) continue;
+        if (a > b) { int t = a; a = b; b = t; }
+        double *wa = colW(a), *wb = colW(b);
+        double *va = wantv ? colV(a) : nullptr, *vb = wantv ? colV(b) : nullptr;
+        // all four (mostly remote) columns loaded into registers up front: one
+        // distributed-shared-memory latency per pair instead of one per pass
+        double xa[JC_R], xb[JC_R], ya[JC_R], yb[JC_R];
+#pragma unroll
+        for (int q = 0; q < JC_R; ++q) {
+          const int r = lane + 32 * q;
+          xa[q] = r < m ? wa[r] : 0.0;
+          xb[q] = r < m ? wb[r] : 0.0;
+          ya[q] = (wantv && r < p) ? va[r] : 0.0;
+          yb[q] = (wantv && r < p) ? vb[r] : 0.0;
+        }
+        double al = 0.0, be = 0.0, ga = 0.0;
+#pragma unroll
+        for (int q = 0; q < JC_R; ++q) {
+          al = fma(xa[q], xa[q], al);
+          be = fma(xb[q], xb[q], be);
+          ga = fma(xa[q], xb[q], ga);
+        }
+        al = warp_sum(al);
+        be = warp_sum(be);
+        ga = warp_sum(ga);
+        if (ga == 0.0 || al == 0.0 || be == 0.0) continue;
+        fl += 6ull * m;
+        if (jacobi_orthogonal(al, be, ga, tol)) continue;
+        fl += 6ull * (m + p);
+        const double zeta = (be - al) * __drcp_rn(2.0 * ga);
+        const double tr = __drcp_rn(fabs(zeta) + sqrt(fma(zeta, zeta, 1.0)));
+        const double t = zeta >= 0.0 ? tr : -tr;
+        const double c = rsqrt(fma(t, t, 1.0)), sn = c * t;
+#pragma unroll
+        for (int q = 0; q < JC_R; ++q) {
+          const int r = lane + 32 * q;
+          if (r < m) {
+            wa[r] = c * xa[q] - sn * xb[q];
+            wb[r] = sn * xa[q] + c * xb[q];
+          }
+          if (wantv && r < p) {
+            va[r] = c * ya[q] - sn * yb[q];
+            vb[r] = sn * ya[q] + c * yb[q];
+          }
+        }
+        if (lane == 0) s_flag = 1;
+      }
+      cl.sync();
+    }
+    // any rotation in the cluster this sweep?
+    int any = 0;
+    for (int q = 0; q < C; ++q) any |= *cl.map_shared_rank(&s_flag, q);
+    cl.sync();
+    if (tid == 0) s_flag = 0;
+    if (!any) break;
+    cl.sync();
+  }
+  if (lane == 0 && fl) atomicAdd(&g_linalg_flops[1], fl);
+  if (rank == 0 && tid == 0 && g.sweeps_out) *g.sweeps_out = sweep + 1;
+  // sigma of the local columns, gathered into every CTA, then the rank sort
+  for (int q = warp; q < ncl; q += NW) {
+    const int c = q * C + rank;
+    if (c >= p) continue;
+    const double *w = sW + (size_t)q * m;
+    double sacc = 0.0;
+    for (int r = lane; r < m; r += 32) sacc = fma(w[r], w[r], sacc);
+    sacc = warp_sum(sacc);
+    if (lane == 0) sig[c] = sqrt(sacc);
+  }
+  cl.sync();
+  for (int c = tid; c < p; c += blockDim.x)
+    if (c % C != rank) sig[c] = *cl.map_shared_rank(sig + c, c % C);
+  cl.sync();   // remote reads done before any CTA exits
+  for (int i = tid; i < p; i += blockDim.x) {
+    const double si = sig[i];
+    int ps = 0;
+    for (int j = 0; j < p; ++j) {
+      const double sj = sig[j];
+      ps += (sj > si) || (sj == si && j < i);
+    }
+    pos[i] = ps;
+  }
+  __syncthreads();
+  for (int e = tid; e < ncl * m; e += blockDim.x) {
+    const int q = e / m, r = e - q * m, c = q * C + rank;
+    if (c >= p) continue;
+    const double sc = sig[c];
+    g.U[r + (long long)pos[c] * g.ldu] = sc > 0.0 ? sW[e] / sc : 0.0;
+  }
+  if (wantv)
+    for (int e = tid; e < ncl * p; e += blockDim.x) {
+      const int q = e / p, r = e - q * p, c = q * C + rank;
+      if (c < p) g.V[r + (long long)pos[c] * g.ldv] = sV[e];
+    }
+  if (rank == 0)
+    for (int c = tid; c < p; c += blockDim.x) g.sigma[pos[c]] = sig[c];
+  (void)s_sig;
+}
+
 // ------------------------------------------- block Jacobi across a grid ---
 // One-sided block Jacobi for larger p: the p columns form nb blocks of JB
 // columns; each round pairs blocks by a round-robin tournament and every CTA
@@ -842,6 +995,41 @@ static size_t svd_smem_bytes(int mcap, int pcap, bool wantv) {
          (size_t)pcap * sizeof(int) + 16;
 }
 
+// cluster Jacobi: the smallest cluster (2..16 CTAs) whose per-CTA share of W and
+// V fits in shared memory; false if none does (or the launch is refused)
+static bool cluster_jacobi(const SVDDesc *descs_dev, int count, int mcap, int pcap, size_t limit, cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(jacobi_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)limit);
+    cudaFuncSetAttribute(jacobi_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    attr = true;
+  }
+  if (mcap > 32 * JC_R || pcap > 32 * JC_R) return false;
+  const int pairs = (pcap + 1) / 2;
+  for (int C = 2; C <= JC_MAXC; C *= 2) {
+    const long long ncl = (pcap + C - 1) / C;
+    const size_t smem = (size_t)ncl * (mcap + pcap) * sizeof(double) + (size_t)pcap * (sizeof(double) + sizeof(int));
+    const int warps = (pairs + C - 1) / C;
+    if (smem > limit || warps > 16) continue;   // <= 512 threads: 72 registers fit
+    const int threads = 32 * (warps < 2 ? 2 : warps);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(count * C);
+    cfg.blockDim = dim3(threads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = C;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    if (cudaLaunchKernelEx(&cfg, jacobi_cluster_kernel, descs_dev, C) == cudaSuccess) return true;
+    cudaGetLastError();
+  }
+  return false;
+}
+
 tt_status launch_jacobi(const SVDDesc *descs_dev, int count, int mcap, int pcap, cudaStream_t s) {
   if (count <= 0) return TT_OK;
   const size_t smem = svd_smem_bytes(mcap, pcap, true);
@@ -853,6 +1041,8 @@ tt_status launch_jacobi(const SVDDesc *descs_dev, int count, int mcap, int pcap,
       attr_set = true;
     }
     jacobi_kernel<true><<<count, svd_threads(pcap), smem, s>>>(descs_dev);
+  } else if (cluster_jacobi(descs_dev, count, mcap, pcap, limit, s)) {
+    // one thread-block cluster per problem, columns in distributed shared memory
   } else if (count == 1 && g_bj.bar &&
              ((size_t)mcap + pcap) * 2 * JB * sizeof(double) <= limit) {
     // block Jacobi over a cooperative grid: one CTA per block pair
