@@ -32,7 +32,7 @@ g = inputs.rng(61)
 z = tb.TTVec.from_cores(inputs.random_tt(g, modes, [1] + [4] * (d - 1) + [1]))
 psi = tb.TTVec.from_cores([np.ones((1, n, 1)) for n in modes], rcap=[1] + [rmax + 4] * (d - 1) + [1])
 kw = dict(tol_k=1e-14, eps_round=1e-6, eps_solve=1e-6, rmax=rmax, matvec="amen_mv", max_sweeps=4, mv_max_sweeps=4,
-          restart=40, max_restarts=20)
+          restart=int(os.environ.get("TT_RESTART", "40")), max_restarts=20)
 t0 = time.time()
 r = tb.keff_fixed_point(ops["H"], ops["S"], ops["F"], psi, z, max_outer=W, **kw)
 torch.cuda.synchronize()
