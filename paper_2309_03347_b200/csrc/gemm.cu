@@ -613,7 +613,7 @@ __global__ void __launch_bounds__(GF_THREADS, GF_MINB) gm_chunk_kernel(GmChunkAr
   double *part1 = a.part, *part2 = a.part + (size_t)G * GF_LD, *part3 = a.part + 2 * (size_t)G * GF_LD;
   double *w = a.w;
 #ifdef GM_PHASE_TIMING
-  long long ph[6] = {0, 0, 0, 0, 0, 0};
+  long long ph[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   long long tcl = clock64();
 #define GM_PH(i) do { const long long t_ = clock64(); ph[i] += t_ - tcl; tcl = t_; } while (0)
 #else
@@ -688,8 +688,12 @@ __global__ void __launch_bounds__(GF_THREADS, GF_MINB) gm_chunk_kernel(GmChunkAr
     ++nsteps;
     jlast = j;
     // ---- w = A V[:, j] (three chained GEMM stages; the kernel itself stops on the stop word)
-    for (int sidx = 0; sidx < 3; ++sidx)
+    for (int sidx = 0; sidx < 3; ++sidx) {
       gemm_stage<CLUSTER>(sdesc[3 * (j + 1 - jbase) + sidx], a.split, a.split_elems, a.bar, G, smem, true, false);
+#ifdef GM_PHASE_TIMING
+      if (sidx < 2) GM_PH(5 + sidx);
+#endif
+    }
     GM_PH(1);
     // ---- CGS pass 1: slice dots, plus |w|^2 for the reorthogonalisation test
     double *my1 = part1 + (size_t)blockIdx.x * GF_LD;
@@ -841,7 +845,8 @@ __global__ void __launch_bounds__(GF_THREADS, GF_MINB) gm_chunk_kernel(GmChunkAr
   }   // cycles
 #ifdef GM_PHASE_TIMING
   if (blockIdx.x == 0 && threadIdx.x == 0 && nsteps > 0)
-    printf("GMPH %d %d %lld %lld %lld %lld %lld\n", (int)CLUSTER, nsteps, ph[0], ph[1], ph[2], ph[3], ph[4]);
+    printf("GMPH %d %d %lld %lld %lld %lld %lld %lld %lld\n", (int)CLUSTER, nsteps, ph[0], ph[1], ph[2], ph[3], ph[4],
+           ph[5], ph[6]);
 #endif
 }
 
