@@ -274,6 +274,10 @@ typedef struct {
   int32_t rmax;
   int32_t gmres_restart;   /* Krylov basis size m                                  */
   int32_t gmres_max_restarts;
+  int32_t local_dense_max; /* local systems of size <= this are solved densely      */
+                           /*    (Gauss-Jordan with partial pivoting; an exactly    */
+                           /*    singular system is regularised with mu = 1e-12     */
+                           /*    ||B||_F, reading Z35); 0 = GMRES only (default)    */
 } amen_opts;
 size_t amen_workspace(const tt_mat *A, const tt_vec *b, const tt_vec *x, const tt_vec *z,
                       const amen_opts *o);
@@ -332,7 +336,8 @@ typedef struct {
   int32_t kickrank;        /* 0: the interior rank capacity of z; > 0: must equal it */
   int32_t gmres_restart;
   int32_t gmres_max_restarts;
-  int32_t local_dense_max; /* must be 0: local systems are solved by GMRES only      */
+  int32_t local_dense_max; /* local systems of size <= this are solved densely (*/
+                           /*    Z20/Z35; see amen_opts); 0 = GMRES only             */
   int32_t matvec;          /* 0: B by exact products + rounding; 1: B = amen_mv(S +  */
                            /*    k^{-1} F, Psi) to eps_round,          */
                            /*    warm-started from the previous B                    */

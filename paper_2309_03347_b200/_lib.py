@@ -34,7 +34,8 @@ class tt_mat(C.Structure):
 
 class amen_opts(C.Structure):
     _fields_ = [("eps", C.c_double), ("local_tol", C.c_double), ("max_sweeps", C.c_int32),
-                ("rmax", C.c_int32), ("gmres_restart", C.c_int32), ("gmres_max_restarts", C.c_int32)]
+                ("rmax", C.c_int32), ("gmres_restart", C.c_int32), ("gmres_max_restarts", C.c_int32),
+                ("local_dense_max", C.c_int32)]
 
 
 class keff_opts(C.Structure):

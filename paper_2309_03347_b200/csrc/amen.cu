@@ -406,10 +406,14 @@ struct AmenCtx {
   size_t orth_cap;
   double *split;
   unsigned int *bar;
+  int dcap;                      // dense local solver capacity (0: off)
+  double *dM, *dl, *dpart;
+  unsigned int *dbar;
+  int *dmu;
 };
 
 static tt_status carve_amen(const MatMeta &A, const VecMeta &b, const VecMeta &x, const VecMeta &z, int m, Arena &ar,
-                            AmenCtx &P) {
+                            AmenCtx &P, int dense_max = 0) {
   const int d = A.d;
   if (b.d != d || x.d != d || z.d != d) return fail(TT_ERR_SHAPE, "amen_solve: number of cores differ");
   for (int k = 0; k < d; ++k) {
@@ -517,13 +521,23 @@ static tt_status carve_amen(const MatMeta &A, const VecMeta &b, const VecMeta &x
   P.orth_base = ar.take<char>(P.orth_cap);
   P.split = ar.take<double>(GEMM_SPLIT_SCRATCH / 8);
   P.bar = ar.take<unsigned int>(4);
+  if (dense_max < 0) return fail(TT_ERR_ARG, "amen_solve: local_dense_max must be >= 0");
+  P.dcap = (int)(dense_max < Ncap ? dense_max : Ncap);
+  if (P.dcap > 0) {
+    P.dM = ar.take<double>((size_t)P.dcap * (P.dcap + 1));
+    P.dl = ar.take<double>((size_t)2 * (P.dcap + 2));
+    P.dpart = ar.take<double>((size_t)4 * 1024);
+    P.dbar = ar.take<unsigned int>(4);
+    P.dmu = ar.take<int>(4);
+  }
   return TT_OK;
 }
 
-size_t amen_ws_bytes(const MatMeta &A, const VecMeta &b, const VecMeta &x, const VecMeta &z, int restart) {
+size_t amen_ws_bytes(const MatMeta &A, const VecMeta &b, const VecMeta &x, const VecMeta &z, int restart,
+                     int dense_max) {
   Arena ar;
   AmenCtx P;
-  if (carve_amen(A, b, x, z, restart, ar, P) != TT_OK) return 0;
+  if (carve_amen(A, b, x, z, restart, ar, P, dense_max) != TT_OK) return 0;
   return ar.used;
 }
 
@@ -531,7 +545,7 @@ size_t amen_ws_bytes(const MatMeta &A, const VecMeta &b, const VecMeta &x, const
 tt_status amen_solve_meta(const MatMeta &A, const VecMeta &b, const VecMeta &x, const VecMeta &z, const AmenOpts &o,
                           int *sweeps_dev, double *res_dev, int *status_dev, Arena &ar, cudaStream_t s) {
   AmenCtx P;
-  TT_TRY(carve_amen(A, b, x, z, o.restart, ar, P));
+  TT_TRY(carve_amen(A, b, x, z, o.restart, ar, P, o.dense_max));
   if (!ar.base) return TT_OK;
   if (!ar.ok()) return fail(TT_ERR_CAPACITY, "amen_solve: workspace too small");
   if (!(o.eps > 0.0)) return fail(TT_ERR_ARG, "amen_solve: eps must be > 0");
@@ -544,6 +558,7 @@ tt_status amen_solve_meta(const MatMeta &A, const VecMeta &b, const VecMeta &x, 
   set_limits_kernel<<<1, 64, 0, s>>>(x, z, o.rmax, D.limit);   // no host round trip
   set_gm_H<<<1, 1, 0, s>>>(P.gst, P.H);
   set_dv_kernel<<<1, 1, 0, s>>>(D.dv, 1, o.eps);
+  if (P.dcap > 0) cudaMemsetAsync(P.dmu, 0, sizeof(int), s);
   set_gemm_scratch(P.split, GEMM_SPLIT_SCRATCH);
   set_jacobi_sync(P.bar);
   Arena oa;
@@ -606,6 +621,7 @@ tt_status amen_solve_meta(const MatMeta &A, const VecMeta &b, const VecMeta &x, 
   gc.bar = P.gbar;
   gc.split = P.split;
   gc.split_elems = GEMM_SPLIT_SCRATCH / 8 - 4096;
+  gc.dense_max = P.dcap;
   const bool cluster_off = std::getenv("TT_GMRES_NOCLUSTER") != nullptr;
   const uint64_t hD = hash_bytes(&D, sizeof(D));   // D is fixed for the whole solve: hash it once
   int dir = +1, sweep = 0;
@@ -651,6 +667,15 @@ tt_status amen_solve_meta(const MatMeta &A, const VecMeta &b, const VecMeta &x, 
       }));
       fused_profile_tag(k);
       TT_TRY(gmres_solve(gc, s));
+      if (P.dcap > 0) {   // N <= local_dense_max: dense solve (the GMRES launches above returned at once)
+        DenseArgs da;
+        da.Nptr = D.iv; da.dense_max = P.dcap; da.k = k; da.n = n;
+        da.r = D.x.r; da.R = D.A.R;
+        da.Phi = D.AL[k]; da.A = D.A.data + D.A.off[k]; da.Psi = D.AR[k + 1];
+        da.rhs = D.rhs; da.x = D.sol;
+        da.M = P.dM; da.lbuf = P.dl; da.part = P.dpart; da.bar = P.dbar; da.mu_count = P.dmu; da.st = P.gst;
+        TT_TRY(launch_dense_local(da, P.dcap, s));
+      }
       TT_TRY(run_captured(key ^ 0x2ull, s, [&]() -> tt_status {
       track_res_kernel<<<1, 1, 0, s>>>(P.gst, D.dv, status_dev);
       track_dx_kernel<<<1, 256, 0, s>>>(D.iv, D.sol, D.xold, D.dv);

@@ -6,8 +6,10 @@ namespace tt {
 struct AmenOpts {
   double eps, local_tol;
   int max_sweeps, rmax, restart, max_restarts;
+  int dense_max = 0;   // local systems with N <= dense_max: dense solve (a7)
 };
-size_t amen_ws_bytes(const MatMeta &A, const VecMeta &b, const VecMeta &x, const VecMeta &z, int restart);
+size_t amen_ws_bytes(const MatMeta &A, const VecMeta &b, const VecMeta &x, const VecMeta &z, int restart,
+                     int dense_max = 0);
 tt_status amen_solve_meta(const MatMeta &A, const VecMeta &b, const VecMeta &x, const VecMeta &z, const AmenOpts &o,
                           int *sweeps_dev, double *res_dev, int *status_dev, Arena &ar, cudaStream_t s);
 size_t amen_mv_ws_bytes(const MatMeta &A, const VecMeta &b, const VecMeta &y, const VecMeta &z);

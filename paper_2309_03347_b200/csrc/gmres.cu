@@ -14,12 +14,15 @@ namespace tt {
 
 namespace {
 
-__global__ void gm_init_kernel(GmState *st, const int *Nptr, int m, double tol) {
+__global__ void gm_init_kernel(GmState *st, const int *Nptr, int m, double tol, int dense_max) {
   st->N = *Nptr;
   st->m = m;
   st->tol = tol;
-  st->converged = 0;
-  st->stop = 0;
+  // N <= dense_max: the dense local solver takes this system, the fused GMRES
+  // launches return at once
+  const int skip = st->N <= dense_max ? 1 : 0;
+  st->converged = skip;
+  st->stop = skip;
   st->cycle = 0;
   st->nan = 0;
   st->jdone = 0;
@@ -28,7 +31,7 @@ __global__ void gm_init_kernel(GmState *st, const int *Nptr, int m, double tol) 
 }  // namespace
 
 tt_status gmres_solve(const GmresCtx &c, cudaStream_t s) {
-  gm_init_kernel<<<1, 1, 0, s>>>(c.st, c.Nptr, c.m, c.tol);
+  gm_init_kernel<<<1, 1, 0, s>>>(c.st, c.Nptr, c.m, c.tol, c.dense_max);
   TT_TRY(check_launch("gm_init"));
   if (!(c.gapp && c.part && c.bar && gmres_fused_grid() > 0))
     return fail(TT_ERR_CUDA, "gmres: the fused solve kernel is unavailable (not co-resident)");

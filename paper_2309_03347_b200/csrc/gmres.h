@@ -32,11 +32,27 @@ struct GmresCtx {
   unsigned int *bar = nullptr;   // [2] grid barrier words (zeroed by gmres_solve)
   double *split = nullptr;       // split-K scratch
   long long split_elems = 0;
+  int dense_max = 0;             // local systems with N <= dense_max go to the dense solver
   int cluster = 0;               // 0: cooperative grid; 1: one thread-block cluster (small local
                                  // systems); 2: both launched, the device-resident sizes decide
 };
 
 tt_status gmres_solve(const GmresCtx &c, cudaStream_t s);
+
+// dense local solver (dense.cu): local systems with N <= dense_max
+struct DenseArgs {
+  const int *Nptr;        // device: local size N
+  int dense_max, k, n;    // size threshold, core index, mode size
+  const int *r, *R;       // device ranks of x and of the operator
+  const double *Phi, *A, *Psi;   // left interface [r0, R0, r0], core [R0, n, n, R1], right [r1, R1, r1]
+  const double *rhs;
+  double *x;              // in: initial guess, out: solution
+  double *M, *lbuf, *part;   // [dm x (dm+1)], [2 (dm+2)], [1024 x 4]
+  unsigned int *bar;
+  int *mu_count;          // device counter of mu-regularised solves (Z35)
+  GmState *st;            // res0 / res / converged for the sweep bookkeeping
+};
+tt_status launch_dense_local(const DenseArgs &a, int dense_cap, cudaStream_t s);
 
 size_t gmres_fused_part_doubles(int G);
 int gmres_fused_grid();

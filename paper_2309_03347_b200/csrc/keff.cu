@@ -168,8 +168,7 @@ tt_status carve_keff(const MatMeta &H, const MatMeta &S, const MatMeta &F, const
   W.f = vec_like(ar, d, F.n, cap);
   const bool mv = o.matvec == 1;
   if (o.matvec != 0 && o.matvec != 1) return fail(TT_ERR_ARG, "keff: matvec must be 0 (exact) or 1 (amen_mv)");
-  if (o.local_dense_max != 0)
-    return fail(TT_ERR_NOT_IMPLEMENTED, "keff: local_dense_max must be 0 (local systems are solved by GMRES)");
+  if (o.local_dense_max < 0) return fail(TT_ERR_ARG, "keff: local_dense_max must be >= 0");
   if (o.kickrank != 0) {
     int zc = 0;
     for (int k = 1; k < d; ++k) zc = z.rcap[k] > zc ? z.rcap[k] : zc;
@@ -236,7 +235,7 @@ tt_status carve_keff(const MatMeta &H, const MatMeta &S, const MatMeta &F, const
   { Arena c; round_meta(W.f, 0.0, 1, nullptr, nullptr, 0, c, nullptr); upd(c.used); }
   { Arena c; round_meta(psi, 0.0, 1, nullptr, nullptr, 0, c, nullptr); upd(c.used); }
   { Arena c; dot_meta(W.f, psi, nullptr, c, nullptr); upd(c.used); }
-  upd(amen_ws_bytes(H, W.B, psi, z, o.gmres_restart));
+  upd(amen_ws_bytes(H, W.B, psi, z, o.gmres_restart, o.local_dense_max));
   if (res_on) {
     const size_t b1 = amen_mv_ws_bytes(W.M, psi, W.Rv, W.zr), b2 = amen_mv_ws_bytes(H, psi, W.Hv, W.zr);
     if (b1 == 0 || b2 == 0) return fail(TT_ERR_CAPACITY, "keff: residual amen_mv operands rejected");
@@ -296,6 +295,7 @@ tt_status keff_meta(const MatMeta &H, const MatMeta &S, const MatMeta &F, const 
   ao.rmax = o.rmax;
   ao.restart = o.gmres_restart;
   ao.max_restarts = o.gmres_max_restarts;
+  ao.dense_max = o.local_dense_max;
   int hflag = 0;
   const bool mv = o.matvec == 1;
   // fixed-point residual ||H Psi - (S + F/k) Psi|| / ||H Psi|| (Z19) of the
@@ -499,7 +499,7 @@ extern "C" size_t amen_workspace(const tt_mat *A, const tt_vec *b, const tt_vec 
   MatMeta Am;
   VecMeta bm, xm, zm;
   if (!o || make_mat_meta(A, Am) || make_vec_meta(b, bm) || make_vec_meta(x, xm) || make_vec_meta(z, zm)) return 0;
-  return amen_ws_bytes(Am, bm, xm, zm, o->gmres_restart);
+  return amen_ws_bytes(Am, bm, xm, zm, o->gmres_restart, o->local_dense_max);
 }
 
 extern "C" tt_status amen_solve(const tt_mat *A, const tt_vec *b, tt_vec *x, tt_vec *z, const amen_opts *o,
@@ -520,6 +520,7 @@ extern "C" tt_status amen_solve(const tt_mat *A, const tt_vec *b, tt_vec *x, tt_
   ao.rmax = o->rmax;
   ao.restart = o->gmres_restart;
   ao.max_restarts = o->gmres_max_restarts;
+  ao.dense_max = o->local_dense_max;
   Arena ar;
   ar.base = (char *)ws;
   ar.cap = wsb;

@@ -348,10 +348,12 @@ def als_update_interfaces_structured(kind, absorb, direction, dims, Iprev, Yk, A
 # ------------------------------------------------------------------ a7 ---
 
 def amen_solve(A: TTMat, b: TTVec, x: TTVec, z: TTVec, eps: float, rmax: int = 1 << 20, max_sweeps: int = 20,
-               restart: int = 40, max_restarts: int = 50, local_tol: float = 0.0, stream=None):
-    """x <- AMEn solution of A x = b (x: initial guess in, solution out; z: residual TT)."""
+               restart: int = 40, max_restarts: int = 50, local_tol: float = 0.0, local_dense_max: int = 0,
+               stream=None):
+    """x <- AMEn solution of A x = b (x: initial guess in, solution out; z: residual TT).
+    local_dense_max > 0: local systems of that size or smaller are solved densely."""
     o = _lib.amen_opts(float(eps), float(local_tol), int(max_sweeps), int(min(rmax, 2**30)), int(restart),
-                       int(max_restarts))
+                       int(max_restarts), int(local_dense_max))
     nb = lib().amen_workspace(A.c, b.c, x.c, z.c, C.byref(o))
     if nb == 0:
         check(lib().amen_solve(A.c, b.c, x.c, z.c, C.byref(o), None, None, None, 0, C.c_void_p(_stream(stream))))
@@ -389,17 +391,17 @@ class KeffResult:
 
 
 def _keff_opts(tol_k, tol_res, eps_round, eps_solve, max_outer, rmax, max_sweeps, restart, max_restarts, matvec,
-               mv_max_sweeps, warm=False):
+               mv_max_sweeps, warm=False, local_dense_max=0):
     return _lib.keff_opts(float(tol_k), float(tol_res), float(eps_round), float(eps_solve), int(max_outer),
-                          int(min(rmax, 2**30)), int(max_sweeps), 0, int(restart), int(max_restarts), 0, _MV[matvec],
-                          int(mv_max_sweeps), int(bool(warm)))
+                          int(min(rmax, 2**30)), int(max_sweeps), 0, int(restart), int(max_restarts),
+                          int(local_dense_max), _MV[matvec], int(mv_max_sweeps), int(bool(warm)))
 
 
 def keff_fixed_point(H: TTMat, S: TTMat, F: TTMat, psi: TTVec, z: TTVec, k0: float = 1.0, tol_k: float = 1e-10,
                      eps_round: float = 1e-12, eps_solve: float = 1e-11, max_outer: int = 200, rmax: int = 1 << 20,
                      max_sweeps: int = 20, restart: int = 40, max_restarts: int = 50, hist_cap: int = 256,
                      matvec: str = "exact", mv_max_sweeps: int = 10, tol_res: float = -1.0, warm: bool = False,
-                     ws: Optional[torch.Tensor] = None, stream=None) -> KeffResult:
+                     ws: Optional[torch.Tensor] = None, local_dense_max: int = 0, stream=None) -> KeffResult:
     """matvec: "exact" (exact products + rounding) or "amen_mv" (fit-based product, NEXT-1).
     tol_res > 0: fixed-point residual every iteration, required for convergence;
     0: evaluated once at the end; < 0: not evaluated.  warm: continue the previous
@@ -407,7 +409,7 @@ def keff_fixed_point(H: TTMat, S: TTMat, F: TTMat, psi: TTVec, z: TTVec, k0: flo
     call needs the workspace of that call: pass a dedicated uint8 tensor `ws`
     (keff_workspace_bytes) to both."""
     o = _keff_opts(tol_k, tol_res, eps_round, eps_solve, max_outer, rmax, max_sweeps, restart, max_restarts, matvec,
-                   mv_max_sweeps, warm)
+                   mv_max_sweeps, warm, local_dense_max)
     dev = psi.device
     k = torch.zeros(1, dtype=torch.float64, device=dev)
     iters = torch.zeros(1, dtype=torch.int32, device=dev)
@@ -433,8 +435,8 @@ def keff_fixed_point(H: TTMat, S: TTMat, F: TTMat, psi: TTVec, z: TTVec, k0: flo
 
 
 def keff_workspace_bytes(H: TTMat, S: TTMat, F: TTMat, psi: TTVec, z: TTVec, tol_res: float = -1.0,
-                         rmax: int = 1 << 20, matvec: str = "exact", restart: int = 40) -> int:
-    o = _keff_opts(1e-10, tol_res, 1e-12, 1e-11, 1, rmax, 1, restart, 1, matvec, 1)
+                         rmax: int = 1 << 20, matvec: str = "exact", restart: int = 40, local_dense_max: int = 0) -> int:
+    o = _keff_opts(1e-10, tol_res, 1e-12, 1e-11, 1, rmax, 1, restart, 1, matvec, 1, False, local_dense_max)
     return int(lib().keff_workspace(H.c, S.c, F.c, psi.c, z.c, C.byref(o)))
 
 

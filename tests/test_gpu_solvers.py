@@ -496,3 +496,52 @@ def test_keff_warm_continuation():
         k = r.k.item()
         ks.append(k)
     assert np.max(np.abs(np.array(ks) - kref) / kref) <= 1e-9, (ks, kref)
+
+
+def test_amen_dense_local_solver():
+    """a7's dense branch (Z20): local systems of size <= local_dense_max are
+    solved by Gauss-Jordan with partial pivoting on the device.  (1) transport H
+    on a 4^3 S2 cube vs a dense LU solve (<= 1e-8, as the GMRES branch);
+    (2) a singular operator (zero diagonal entries; the rhs vanishes on them):
+    the exactly singular local systems are regularised with mu = 1e-12 ||B||_F
+    (Z35) and the result equals the oracle's amen_solve with its dense branch
+    (np.linalg.solve -> LinAlgError -> B + mu I)."""
+    g = inputs.rng(64)
+    prob = small_c1(4)
+    ops = gtr.operators(prob)
+    Hd = T.dense_operators(prob)["H"]
+    modes = [4, 4, 4, 8, 1]
+    b = inputs.random_tt(g, modes, [1, 2, 3, 2, 1, 1])
+    x = tb.TTVec.from_cores([np.ones((1, n, 1)) for n in modes], rcap=[1, 20, 20, 20, 20, 1])
+    z = tb.TTVec.from_cores(inputs.random_tt(g, modes, [1, 4, 4, 4, 4, 1]))
+    tb.amen_solve(ops["H"], tb.TTVec.from_cores(b), x, z, eps=1e-11, local_dense_max=2000)
+    torch.cuda.synchronize()
+    ref = np.linalg.solve(Hd, ott.tt_full(b))
+    assert np.linalg.norm(ott.tt_full(x.cores()) - ref) <= 1e-8 * np.linalg.norm(ref)
+    # singular: A = diag(d1) (x) diag(d2) (x) diag(d3) with zeros, b zero on the null rows
+    dims = [3, 4, 2]
+    ds = [np.array([1.0, 2.0, 0.0]), np.array([1.5, 0.0, 3.0, 0.5]), np.array([2.0, 1.0])]
+    A = ott.rank1_ttm([np.diag(v) for v in ds])
+    bv = [np.where(v != 0.0, 1.0 + g.random(v.size), 0.0).reshape(1, -1, 1) for v in ds]
+    x0 = [np.ones((1, n, 1)) for n in dims]
+    z0 = inputs.random_tt(g, dims, [1, 2, 2, 1])
+    xo, _ = so.amen_solve(A, bv, x0, z0, eps=1e-12, max_sweeps=4, dense_max=2000)
+    xg = tb.TTVec.from_cores(x0, rcap=[1, 6, 6, 1])
+    tb.amen_solve(tb.TTMat.from_cores(A), tb.TTVec.from_cores(bv), xg, tb.TTVec.from_cores(z0), eps=1e-12,
+                  max_sweeps=4, local_dense_max=2000)
+    torch.cuda.synchronize()
+    fo, fg = ott.tt_full(xo), ott.tt_full(xg.cores())
+    assert np.linalg.norm(fg - fo) <= 1e-9 * np.linalg.norm(fo), (np.linalg.norm(fg - fo), np.linalg.norm(fo))
+
+
+def test_keff_dense_local_solver_c1():
+    """k-eff (C1 4^3 cube) with the dense local solver (local_dense_max = 2000, the
+    SPEC's threshold; the oracle's keff_tt default) reaches the dense power
+    iteration's k to 1e-8."""
+    prob = small_c1(4)
+    ops = T.dense_operators(prob)
+    kd, _, _ = so.keff_dense_power(ops["H"], ops["S"], ops["F"], tol=1e-13)
+    res, _ = _keff_gpu(prob, [4, 4, 4, 8, 1], rmax=32, tol_k=1e-12, eps_round=1e-13, eps_solve=1e-12,
+                       local_dense_max=2000)
+    assert res.status.item() == 0
+    assert abs(res.k.item() - kd) / kd <= 1e-8
