@@ -88,7 +88,8 @@ void tt_counters(uint64_t *out /* [5] */, int32_t reset);
 /* Live timing of the fused GMRES Arnoldi-step kernel (the dominant kernel of
  * the k-eff solves; used by bench.py for its roofline line).  enable != 0:
  * every later launch of the kernel by this thread is bracketed by CUDA events
- * on its stream.  _read synchronises those events and returns the number of
+ * on its stream (host-stepped graph modes 0/1; in mode 2 the in-kernel
+ * %globaltimer of CTA 0 times each launch that does work).  _read synchronises those events and returns the number of
  * launches, their summed duration (ms) and flops[3] = {local-apply GEMM flops,
  * CGS2/norm vector flops, Arnoldi steps executed} of those launches, then
  * resets (the flop counters count every fused launch since the last read). */
@@ -98,6 +99,30 @@ void tt_fused_profile_read(int64_t *launches, double *ms, double *flops /* [3] *
  * duration ms[k], Arnoldi steps steps[k] and launches[k], arrays of TT_MAX_D.
  * Call before tt_fused_profile_read (which resets). */
 void tt_fused_profile_cores(double *ms, double *steps, int64_t *launches);
+/* The in-kernel timer alone: summed %globaltimer duration (ms) and number of the
+ * fused launches that did work since the last read (either this call or a
+ * tt_fused_profile_read that found no events); resets it.  Used to cross-check
+ * the timer against CUDA events on the host-stepped path. */
+void tt_fused_timer_read(double *ms, int64_t *launches);
+
+/* CUDA-graph execution mode of the drivers (calling thread):
+ *   2 (default) device-resident loops: amen_solve, amen_mv, keff_fixed_point and
+ *     alpha_secant each run as ONE graph launch whose convergence loops are
+ *     conditional WHILE/IF nodes decided on the device (no host round trip
+ *     inside the call; one small read-back at entry detects the operator core
+ *     structure).  The fused GMRES kernel is then timed by its in-kernel
+ *     %globaltimer (tt_fused_profile_read), events cannot bracket it;
+ *   1 fixed launch sequences replayed as graphs, loops polled by the host
+ *     (one read-back per sweep / outer iteration);
+ *   0 no graphs.
+ * The environment sets the default (TT_NO_GRAPHS=1 -> 0, TT_NO_DEVLOOP=1 -> 1);
+ * mode < 0 restores it.  A capture or instantiation failure is returned as
+ * TT_ERR_CUDA, never a silent change of mode.  Graphs are cached under the exact
+ * bytes of everything they depend on (operands, workspace, options, report
+ * pointers); _stats returns captures, replays and cached graphs so far. */
+void tt_set_graph_mode(int32_t mode);
+int32_t tt_graph_mode(void);
+void tt_graph_stats(int64_t *captures, int64_t *replays, int64_t *cached);
 
 /* ---------------------------------------------------------------- a1 ---
  * tt_matvec: exact TT-matrix x TT-vector product ("explicit and

@@ -12,9 +12,9 @@ from .tt import (AlphaResult, KeffResult, alpha_secant, TTMat, TTVec, als_local_
                  keff_fixed_point, keff_workspace_bytes, matvec_out, tt_add, tt_copy, tt_dot, tt_matvec, tt_matvec_batched, tt_orthogonalize, tt_round,
                  tt_round_batched, RoundBatch,
                  tt_scale, CORE_DENSE, CORE_DIAG, core_kinds, als_local_apply_structured,
-                 als_update_interfaces_structured)
+                 als_update_interfaces_structured, set_graph_mode, graph_mode, graph_stats)
 
 __all__ = ["TTError", "TTMat", "TTVec", "tt_matvec", "matvec_out", "tt_add", "tt_scale", "tt_copy", "tt_dot",
            "tt_orthogonalize", "tt_round", "tt_round_batched", "RoundBatch", "als_local_apply", "als_update_interfaces", "amen_mv", "amen_solve",
            "keff_fixed_point", "keff_workspace_bytes", "KeffResult", "alpha_secant", "AlphaResult", "CORE_DENSE", "CORE_DIAG", "core_kinds",
-           "als_local_apply_structured", "als_update_interfaces_structured"]
+           "als_local_apply_structured", "als_update_interfaces_structured", "set_graph_mode", "graph_mode", "graph_stats"]

@@ -72,6 +72,10 @@ SIG = {
     "tt_fused_profile": (None, [I32]),
     "tt_fused_profile_read": (None, [C.POINTER(C.c_int64), C.POINTER(C.c_double), C.POINTER(C.c_double)]),
     "tt_fused_profile_cores": (None, [C.POINTER(C.c_double), C.POINTER(C.c_double), C.POINTER(C.c_int64)]),
+    "tt_set_graph_mode": (None, [I32]),
+    "tt_fused_timer_read": (None, [C.POINTER(C.c_double), C.POINTER(C.c_int64)]),
+    "tt_graph_mode": (I32, []),
+    "tt_graph_stats": (None, [C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
     "tt_matvec": (I32, [C.POINTER(tt_mat), C.POINTER(tt_vec), C.POINTER(tt_vec), P]),
     "tt_matvec_batched_workspace": (C.c_size_t, [I32, C.POINTER(tt_mat)]),
     "tt_matvec_batched": (I32, [I32, C.POINTER(tt_mat), C.POINTER(tt_vec), C.POINTER(tt_vec), P, C.c_size_t, P]),

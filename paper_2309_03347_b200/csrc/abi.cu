@@ -175,9 +175,26 @@ namespace tt {
 void fused_profile(int enable);
 void fused_profile_read(long long *launches, double *ms, double *flops);
 void fused_profile_cores(double *ms, double *steps, long long *launches);
+void fused_timer_read(double *ms, long long *launches);
+}
+
+extern "C" void tt_fused_timer_read(double *ms, int64_t *launches) {
+  long long l = 0;
+  tt::fused_timer_read(ms, &l);
+  if (launches) *launches = l;
 }
 
 extern "C" void tt_fused_profile(int32_t enable) { tt::fused_profile(enable); }
+
+extern "C" void tt_set_graph_mode(int32_t mode) { tt::set_graph_mode(mode); }
+extern "C" int32_t tt_graph_mode(void) { return tt::graph_mode(); }
+extern "C" void tt_graph_stats(int64_t *captures, int64_t *replays, int64_t *cached) {
+  long long c = 0, r = 0, n = 0;
+  tt::graph_stats(&c, &r, &n);
+  if (captures) *captures = c;
+  if (replays) *replays = r;
+  if (cached) *cached = n;
+}
 
 extern "C" void tt_fused_profile_cores(double *ms, double *steps, int64_t *launches) {
   long long l[TT_MAX_D];

@@ -107,6 +107,7 @@ extern "C" tt_status als_local_apply(int32_t rA, int32_t R, int32_t rB, int32_t 
   double *T2 = ar.take<double>(mx);
   GemmDesc *dev = ar.take<GemmDesc>(3);
   set_gemm_scratch(ar.take<double>(GEMM_SPLIT_SCRATCH / 8), GEMM_SPLIT_SCRATCH);
+  ScratchScope scratch_scope;
   Desc3 d;
   descs_local_apply(rA, R, rB, m, n, rAp, Rp, rBp, Phi, Ak, Psi, x, y, T1, T2, d.g);
   int Mc[3] = {rB * n, R * m, rA}, Nc[3] = {rAp * Rp, rB * rAp, m * rAp};
@@ -134,6 +135,7 @@ extern "C" tt_status als_update_interfaces(int32_t dir, int32_t rY, int32_t R, i
   double *T2 = ar.take<double>(mx);
   GemmDesc *dev = ar.take<GemmDesc>(3);
   set_gemm_scratch(ar.take<double>(GEMM_SPLIT_SCRATCH / 8), GEMM_SPLIT_SCRATCH);
+  ScratchScope scratch_scope;
   Desc3 d;
   if (Ak) {
     if (dir > 0) {
@@ -200,6 +202,7 @@ extern "C" tt_status als_local_apply_structured(int32_t kind, int32_t absorb, in
   double *T2 = ar.take<double>(mx);
   GemmDesc *dev = ar.take<GemmDesc>(4);
   set_gemm_scratch(ar.take<double>(GEMM_SPLIT_SCRATCH / 8), GEMM_SPLIT_SCRATCH);
+  ScratchScope scratch_scope;
   GemmDesc g[4];
   if (!absorb) {
     descs_local_apply_k(kind, rA, R, rB, m, n, rAp, Rp, rBp, Phi, Ak, Psi, x, y, T1, T2, g);
@@ -237,6 +240,7 @@ extern "C" tt_status als_update_interfaces_structured(int32_t kind, int32_t abso
   double *T2 = ar.take<double>(mx);
   GemmDesc *dev = ar.take<GemmDesc>(4);
   set_gemm_scratch(ar.take<double>(GEMM_SPLIT_SCRATCH / 8), GEMM_SPLIT_SCRATCH);
+  ScratchScope scratch_scope;
   GemmDesc g[4];
   if (!absorb) {
     if (dir > 0) descs_iface_left_k(kind, rY, R, rX, m, n, rYp, Rp, rXp, Iprev, Yk, Ak, Xk, Inext, T1, T2, g);

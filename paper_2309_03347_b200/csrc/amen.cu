@@ -387,6 +387,51 @@ static long long lmax(long long a, long long b) { return a > b ? a : b; }
 namespace {
 __global__ void set_gm_H(GmState *st, double *H) { st->H = H; }
 
+// ---- device-resident sweep loops ---------------------------------
+// after a sweep: count it and decide on the device whether another one runs.
+// AMEn (mv = 0): stop when the max local residual dv[0] <= eps or the max
+// relative solution change dv[2] <= eps (Z20); amen_mv (mv = 1): dv[2] <= eps.
+__global__ void sweep_check_kernel(const double *dv, double eps, int max_sweeps, int *cnt, int mv,
+                                   cudaGraphConditionalHandle hw, cudaGraphConditionalHandle hi) {
+  const bool conv = mv ? (dv[2] <= eps) : (dv[0] <= eps || dv[2] <= eps);
+  const int c = *cnt + 1;
+  *cnt = c;
+  const unsigned int more = (!conv && c < max_sweeps) ? 1u : 0u;
+  cudaGraphSetConditional(hw, more);
+  cudaGraphSetConditional(hi, more);
+}
+// workspace-internal report of a captured solve -> the caller's pointers
+__global__ void report_out_kernel(const int *sw, const double *res, const int *st, int *sweeps_dev, double *res_dev,
+                                  int *status_dev) {
+  if (sweeps_dev) *sweeps_dev = *sw;
+  if (res_dev) *res_dev = *res;
+  if (status_dev && *st != 0) *status_dev = *st;
+}
+// the host loop's epilogue: sweeps performed, last residual, NOCONV unless dv[0] <= eps
+__global__ void sweep_post_kernel(const double *dv, double eps, const int *cnt, int *sweeps_dev, double *res_dev,
+                                  int *status_dev) {
+  if (sweeps_dev) *sweeps_dev = *cnt;
+  if (res_dev) *res_dev = dv[0];
+  if (status_dev && !(dv[0] <= eps)) *status_dev = (int)TT_ERR_NOCONV;
+}
+// while (more) { sweep(+1); check; if (more) { sweep(-1); check } } as a WHILE
+// node with a nested IF: the directions alternate exactly as in the host loop
+tt_status sweep_loop(cudaStream_t &s, const double *dv, double eps, int max_sweeps, int *cnt, int mv,
+                     const std::function<tt_status(int)> &one_sweep) {
+  return dev_while(s, [&](cudaGraphConditionalHandle hw) -> tt_status {
+    TT_TRY(one_sweep(+1));
+    cudaGraphConditionalHandle hi;
+    TT_TRY(cond_handle(s, &hi));
+    sweep_check_kernel<<<1, 1, 0, s>>>(dv, eps, max_sweeps, cnt, mv, hw, hi);
+    TT_TRY(check_launch("sweep_check"));
+    return cond_node(s, hi, 0, [&]() -> tt_status {
+      TT_TRY(one_sweep(-1));
+      sweep_check_kernel<<<1, 1, 0, s>>>(dv, eps, max_sweeps, cnt, mv, hw, hw);
+      return check_launch("sweep_check");
+    });
+  });
+}
+
 // host evaluation of a descriptor chain with capacity ranks -> per-GEMM grid caps
 struct CapChain {
   int M[12], N[12];
@@ -545,6 +590,7 @@ size_t amen_ws_bytes(const MatMeta &A, const VecMeta &b, const VecMeta &x, const
 tt_status amen_solve_meta(const MatMeta &A, const VecMeta &b, const VecMeta &x, const VecMeta &z, const AmenOpts &o,
                           int *sweeps_dev, double *res_dev, int *status_dev, Arena &ar, cudaStream_t s) {
   AmenCtx P;
+  const Arena ar0 = ar;
   TT_TRY(carve_amen(A, b, x, z, o.restart, ar, P, o.dense_max));
   if (!ar.base) return TT_OK;
   if (!ar.ok()) return fail(TT_ERR_CAPACITY, "amen_solve: workspace too small");
@@ -552,7 +598,29 @@ tt_status amen_solve_meta(const MatMeta &A, const VecMeta &b, const VecMeta &x, 
   Dev &D = P.D;
   const int d = P.d, m = P.m;
   const int pc = P.pc, zcm = P.zcm, nmax = P.nmax;
-  TT_TRY(detect_core_kinds(D.A, D.kscr, s));
+  if (!D.A.kinds_set) TT_TRY(detect_core_kinds(D.A, D.kscr, s));   // one read-back, before any capture
+  if (graph_mode() >= 2 && !stream_capturing(s)) {
+    // the whole solve as one graph: sweep loop on the device (K11); replayed while
+    // the operands, workspace and options are the same
+    gmres_fused_grid();   // one-time attribute / occupancy queries outside the capture
+    GraphKey key;
+    key.add(D);
+    const double dd[2] = {o.eps, o.local_tol};
+    const int ii[5] = {o.max_sweeps, o.rmax, o.restart, o.max_restarts, o.dense_max};
+    key.add(dd);
+    key.add(ii);
+    const MatMeta Ak = D.A;
+    // the graph reports into the workspace (iv[13] sweeps, dv[6] residual, iv[12]
+    // status) so it does not depend on the caller's pointers; copied out below
+    TT_TRY(run_captured(key, s, [&]() -> tt_status {
+      set_i32_kernel<<<1, 1, 0, s>>>(D.iv + 12, 0);
+      Arena a = ar0;
+      return amen_solve_meta(Ak, b, x, z, o, D.iv + 13, D.dv + 6, D.iv + 12, a, s);
+    }));
+    report_out_kernel<<<1, 1, 0, s>>>(D.iv + 13, D.dv + 6, D.iv + 12, sweeps_dev, res_dev, status_dev);
+    return check_launch("amen_solve report");
+  }
+  ScratchScope scratch_scope;
   const MatMeta &Ah = D.A;   // host copy with the detected kinds
   // per-bond truncation limits: min(rmax, xcap - zcap) (room for the enrichment)
   set_limits_kernel<<<1, 64, 0, s>>>(x, z, o.rmax, D.limit);   // no host round trip
@@ -623,10 +691,14 @@ tt_status amen_solve_meta(const MatMeta &A, const VecMeta &b, const VecMeta &x, 
   gc.split_elems = GEMM_SPLIT_SCRATCH / 8 - 4096;
   gc.dense_max = P.dcap;
   const bool cluster_off = std::getenv("TT_GMRES_NOCLUSTER") != nullptr;
-  const uint64_t hD = hash_bytes(&D, sizeof(D));   // D is fixed for the whole solve: hash it once
-  int dir = +1, sweep = 0;
-  double hres = 0.0;
-  for (sweep = 0; sweep < o.max_sweeps; ++sweep) {
+  GraphKey base;   // D is fixed for the whole solve
+  base.add(D);
+  {
+    const long long extra[6] = {P.Ncap, P.Scap, pc, (long long)(size_t)status_dev, P.dcap, 0x616d};
+    base.add(extra);
+  }
+  // one sweep in direction dir: a fixed launch sequence whose sizes follow the device ranks
+  auto one_sweep = [&](int dir) -> tt_status {
     set_dv_kernel<<<1, 1, 0, s>>>(D.dv, 0, 0.0);
     set_dv_kernel<<<1, 1, 0, s>>>(D.dv, 2, 0.0);
     for (int t = 0; t < d; ++t) {
@@ -650,12 +722,16 @@ tt_status amen_solve_meta(const MatMeta &A, const VecMeta &b, const VecMeta &x, 
         gc.cluster = cluster_off ? 0 : ((tiles <= 2 * gmres_cluster_size() && nloc <= 16384) ? 1 : 2);
       }
       // fixed launch sequences before and after the GMRES solve: CUDA-graph replays
-      uint64_t key = hD;
+      // (recorded inline when the whole solve is being captured)
+      GraphKey key1 = base, key2;
       {
-        const long long extra[8] = {k, dir, last, P.Ncap, P.Scap, pc, (long long)(size_t)status_dev, 0x616d};
-        key = hash_bytes(extra, sizeof(extra), key);
+        const int extra[3] = {k, dir, last};
+        key1.add(extra);
+        key2 = key1;
+        key1.add(1);
+        key2.add(2);
       }
-      TT_TRY(run_captured(key ^ 0x1ull, s, [&]() -> tt_status {
+      TT_TRY(run_captured(key1, s, [&]() -> tt_status {
         plan_local<<<1, 1, 0, s>>>(D, k);
         TT_TRY(launch_copy(D.cd, 1, P.Ncap, s));
         TT_TRY(launch_copy(D.cd + 2, 1, P.Ncap, s));
@@ -676,7 +752,7 @@ tt_status amen_solve_meta(const MatMeta &A, const VecMeta &b, const VecMeta &x, 
         da.M = P.dM; da.lbuf = P.dl; da.part = P.dpart; da.bar = P.dbar; da.mu_count = P.dmu; da.st = P.gst;
         TT_TRY(launch_dense_local(da, P.dcap, s));
       }
-      TT_TRY(run_captured(key ^ 0x2ull, s, [&]() -> tt_status {
+      TT_TRY(run_captured(key2, s, [&]() -> tt_status {
       track_res_kernel<<<1, 1, 0, s>>>(P.gst, D.dv, status_dev);
       track_dx_kernel<<<1, 256, 0, s>>>(D.iv, D.sol, D.xold, D.dv);
       if (last) {
@@ -723,17 +799,29 @@ tt_status amen_solve_meta(const MatMeta &A, const VecMeta &b, const VecMeta &x, 
       return iface(k, dir);
       }));
     }
+    return check_launch("amen sweep");
+  };
+  (void)zcm; (void)nmax;
+  // converged when the max local residual (before the sweep's solves) is <= eps; the
+  // solution-change exit (Z20) also stops, but then reports TT_ERR_NOCONV unless the
+  // residual test holds too
+  if (device_loops(s)) {   // K11: the sweep loop as conditional graph nodes, decided on the device
+    set_i32_kernel<<<1, 1, 0, s>>>(D.iv + 14, 0);
+    TT_TRY(sweep_loop(s, D.dv, o.eps, o.max_sweeps, D.iv + 14, 0, one_sweep));
+    sweep_post_kernel<<<1, 1, 0, s>>>(D.dv, o.eps, D.iv + 14, sweeps_dev, res_dev, status_dev);
+    return check_launch("amen_solve");
+  }
+  int dir = +1, sweep = 0;
+  double hres = 0.0;
+  for (sweep = 0; sweep < o.max_sweeps; ++sweep) {
+    TT_TRY(one_sweep(dir));
     double hv[3] = {0.0, 0.0, 0.0};
     TT_TRY(read_back(hv, D.dv, 3 * sizeof(double), s));
     TT_TRY(check_launch("amen sweep"));
     hres = hv[0];
-    // converged when the max local residual (before the sweep's solves) is <= eps; the
-    // solution-change exit (Z20) also stops, but then reports TT_ERR_NOCONV unless the
-    // residual test holds too
     if (hv[0] <= o.eps || hv[2] <= o.eps) { ++sweep; break; }
     dir = -dir;
   }
-  (void)zcm; (void)nmax;
   if (sweeps_dev) set_i32_kernel<<<1, 1, 0, s>>>(sweeps_dev, sweep);
   if (res_dev) cudaMemcpyAsync(res_dev, D.dv, sizeof(double), cudaMemcpyDeviceToDevice, s);
   if (status_dev && !(hres <= o.eps)) set_i32_kernel<<<1, 1, 0, s>>>(status_dev, (int)TT_ERR_NOCONV);
@@ -921,13 +1009,29 @@ size_t amen_mv_ws_bytes(const MatMeta &A, const VecMeta &b, const VecMeta &y, co
 tt_status amen_mv_meta(const MatMeta &A, const VecMeta &b, const VecMeta &y, const VecMeta &z, double eps,
                        int max_sweeps, int rmax, int *sweeps_dev, Arena &ar, cudaStream_t s) {
   MvCtx P;
+  const Arena ar0 = ar;
   TT_TRY(carve_mv(A, b, y, z, ar, P));
   if (!ar.base) return TT_OK;
   if (!ar.ok()) return fail(TT_ERR_CAPACITY, "amen_mv: workspace too small");
   if (!(eps > 0.0) || max_sweeps < 1 || rmax < 1) return fail(TT_ERR_ARG, "amen_mv: eps > 0, max_sweeps, rmax >= 1");
   Dev &D = P.D;
   const int d = A.d;
-  TT_TRY(detect_core_kinds(D.A, D.kscr, s));
+  if (!D.A.kinds_set) TT_TRY(detect_core_kinds(D.A, D.kscr, s));   // one read-back, before any capture
+  if (graph_mode() >= 2 && !stream_capturing(s)) {   // the whole product as one graph (K11)
+    GraphKey key;
+    key.add(D);
+    const int ii[2] = {max_sweeps, rmax};
+    key.add(eps);
+    key.add(ii);
+    const MatMeta Ak = D.A;
+    TT_TRY(run_captured(key, s, [&]() -> tt_status {
+      Arena a = ar0;
+      return amen_mv_meta(Ak, b, y, z, eps, max_sweeps, rmax, D.iv + 13, a, s);
+    }));
+    report_out_kernel<<<1, 1, 0, s>>>(D.iv + 13, nullptr, nullptr, sweeps_dev, nullptr, nullptr);
+    return check_launch("amen_mv report");
+  }
+  ScratchScope scratch_scope;
   const MatMeta &Ah = D.A;
   set_limits_kernel<<<1, 64, 0, s>>>(y, z, rmax, D.limit);
   set_dv_kernel<<<1, 1, 0, s>>>(D.dv, 1, eps);
@@ -966,9 +1070,8 @@ tt_status amen_mv_meta(const MatMeta &A, const VecMeta &b, const VecMeta &y, con
     return launch_caps(D.gd, c, 0, 8);
   };
   for (int k = d - 1; k >= 1; --k) TT_TRY(iface(k, -1));
-  int dir = +1, sweep = 0;
   // one sweep = a fixed launch sequence (device-resident sizes): replayed as a CUDA graph
-  auto one_sweep = [&]() -> tt_status {
+  auto one_sweep = [&](int dir) -> tt_status {
     set_dv_kernel<<<1, 1, 0, s>>>(D.dv, 2, 0.0);
     for (int t = 0; t < d; ++t) {
       const int k = dir > 0 ? t : d - 1 - t;
@@ -1025,12 +1128,23 @@ tt_status amen_mv_meta(const MatMeta &A, const VecMeta &b, const VecMeta &y, con
     }
     return TT_OK;
   };
-  const uint64_t hD = hash_bytes(&D, sizeof(D));   // D is fixed for the whole product: hash it once
+  if (device_loops(s)) {   // K11: sweep loop decided on the device
+    set_i32_kernel<<<1, 1, 0, s>>>(D.iv + 14, 0);
+    TT_TRY(sweep_loop(s, D.dv, eps, max_sweeps, D.iv + 14, 1, one_sweep));
+    sweep_post_kernel<<<1, 1, 0, s>>>(D.dv, eps, D.iv + 14, sweeps_dev, nullptr, nullptr);
+    return check_launch("amen_mv");
+  }
+  GraphKey base;   // D is fixed for the whole product
+  base.add(D);
+  {
+    const long long extra[4] = {P.Ncap, P.Scap, P.pc, 0x6d76};
+    base.add(extra);
+  }
+  int dir = +1, sweep = 0;
   for (sweep = 0; sweep < max_sweeps; ++sweep) {
-    uint64_t key = hD;
-    const long long extra[5] = {dir, P.Ncap, P.Scap, P.pc, 0x6d76};
-    key = hash_bytes(extra, sizeof(extra), key);
-    TT_TRY(run_captured(key, s, one_sweep));
+    GraphKey key = base;
+    key.add(dir);
+    TT_TRY(run_captured(key, s, [&]() { return one_sweep(dir); }));
     double hv[3] = {0.0, 0.0, 0.0};
     TT_TRY(read_back(hv, D.dv, 3 * sizeof(double), s));
     TT_TRY(check_launch("amen_mv sweep"));

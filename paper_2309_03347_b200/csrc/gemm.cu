@@ -23,6 +23,17 @@ __device__ unsigned long long g_gemm_counters[2];
 __device__ unsigned long long g_gm_counters[3];
 // per-tag (AMEn core index) Arnoldi steps of the fused kernel (tt_fused_profile_cores)
 __device__ unsigned long long g_gm_tag_steps[TT_MAX_D];
+// per-tag in-kernel duration (%globaltimer ns, CTA 0 from entry to exit) and launches that
+// did work: the fused kernel's timing when it runs inside device-resident graph loops,
+// where no host-recorded event can bracket an individual launch
+__device__ unsigned long long g_gm_tag_ns[TT_MAX_D];
+__device__ unsigned long long g_gm_tag_launches[TT_MAX_D];
+
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
 
 namespace {
 
@@ -368,6 +379,9 @@ constexpr int GF_THREADS = 128;
 #ifndef GF_BK
 #define GF_BK 16
 #endif
+#ifndef GF_EFF32
+#define GF_EFF32 0.8   // DMMA efficiency of a 32x32 tile relative to 64x64 in the stage-time model
+#endif
 using GF = Cfg<64, 64, GF_BK, 2, 2, GF_ST>;   // persistent-kernel tiles
 constexpr int GF_LD = GM_MAX_M + 2;
 constexpr int GF_MAX_GRID = 1024;   // partial-sum buffer capacity (gmres_fused_part_doubles)
@@ -469,25 +483,42 @@ __device__ void gemm_stage(const GemmDesc &g, double *split, long long split_ele
     phase_sync<CLUSTER>(bar, G);
     return;
   }
-  const int tm = (g.M + 63) / 64, tn = (g.N + 63) / 64, T = tm * tn;
-  int splits = 1;
-  if (T * 2 <= G && g.K >= 256) {
-    splits = min(G / T, min(g.K / 128, GF_MAXSPLIT));
-    while (splits > 1 && (long long)splits * g.M * g.N > split_elems) --splits;
-  }
   if (blockIdx.x == 0 && tid == 0) {
     const unsigned long long f = 2ull * (unsigned long long)g.M * g.N * (g.K > 0 ? g.K : 0);
     atomicAdd(&g_gemm_counters[0], f);
     atomicAdd(&g_gemm_counters[1], 1ull);
     if (gm_count) atomicAdd(&g_gm_counters[0], f);
   }
-  // small GEMMs (fewer 64x64 tiles than CTAs, or a thin M): 32x32 tiles waste
-  // less of the DMMA work on padding and spread over more CTAs
-  const bool small = splits == 1 && (T < G || g.M <= 32);
-  if (small) {
-    const int sm_ = (g.M + 31) / 32, sn_ = (g.N + 31) / 32;
-    for (int t = blockIdx.x; t < sm_ * sn_; t += G) {
-      gemm_tile<32, 32, 16, 2, 2, 2>(g, (t % sm_) * 32, (t / sm_) * 32, 0, 1, nullptr, 0, 0, smem);
+  // Tile shape per stage: 64x64 or 32x32 tiles, each with split-K when the output
+  // has few tiles, whichever minimises the modelled stage time = rounds of tiles
+  // over the G CTAs x padded tile work (the ranks of the C4 local systems, e.g.
+  // 264 = 4 x 64 + 8 and 68 = 64 + 4 rows, waste up to half of a 64-wide tile on
+  // padding; 32x32 tiles pay GF_EFF32 for their lower operand reuse).  Uniform:
+  // every CTA evaluates the same model on the same descriptor.
+  int bm = 64, tm = (g.M + 63) / 64, tn = (g.N + 63) / 64, splits = 1;
+  {
+    double best = 0.0;
+    for (int v = 0; v < 2; ++v) {
+      const int b = v == 0 ? 64 : 32;
+      const int m_ = (g.M + b - 1) / b, n_ = (g.N + b - 1) / b, T_ = m_ * n_;
+      int sp = 1;
+      if (T_ * 2 <= G && g.K >= 256) {
+        sp = min(G / T_, min(g.K / 128, GF_MAXSPLIT));
+        while (sp > 1 && (long long)sp * g.M * g.N > split_elems) --sp;
+      }
+      const int kt = ((g.K + sp - 1) / sp + 15) / 16;
+      const double rounds = (double)((T_ * sp + G - 1) / G);
+      double cost = rounds * (double)b * b * kt * (v == 0 ? 1.0 : 1.0 / GF_EFF32);
+      if (sp > 1) cost += (double)g.M * g.N * sp / (G * GF_THREADS) * 8.0;   // slice reduction (+ a barrier)
+      if (v == 0 || cost < best) { best = cost; bm = b; tm = m_; tn = n_; splits = sp; }
+    }
+  }
+  const int T = tm * tn;
+  if (bm == 32) {
+    for (int t = blockIdx.x; t < T * splits; t += G) {
+      const int z = t / T, tt = t - z * T;
+      gemm_tile<32, 32, 16, 2, 2, 2>(g, (tt % tm) * 32, (tt / tm) * 32, z, splits, split, g.M,
+                                     (long long)g.M * g.N, smem);
       __syncthreads();
     }
   } else {
@@ -607,6 +638,7 @@ __global__ void __launch_bounds__(GF_THREADS, GF_MINB) gm_chunk_kernel(GmChunkAr
     const bool small = tiles <= 2 * a.cs && N <= 16384;
     if (small != CLUSTER) return;
   }
+  const unsigned long long t_entry = (blockIdx.x == 0 && threadIdx.x == 0) ? globaltimer_ns() : 0ull;
   const double tol = st->tol;
   double bnorm = st->bnorm;
   const int per = (N + G - 1) / G;
@@ -846,6 +878,10 @@ __global__ void __launch_bounds__(GF_THREADS, GF_MINB) gm_chunk_kernel(GmChunkAr
   if (conv || nan_stop) break;
   phase_sync<CLUSTER>(a.bar, G);   // x complete before the next cycle's A x
   }   // cycles
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    atomicAdd(&g_gm_tag_ns[a.tag], globaltimer_ns() - t_entry);
+    atomicAdd(&g_gm_tag_launches[a.tag], 1ull);
+  }
 #ifdef GM_PHASE_TIMING
   if (blockIdx.x == 0 && threadIdx.x == 0 && nsteps > 0)
     printf("GMPH %d %d %lld %lld %lld %lld %lld %lld %lld\n", (int)CLUSTER, nsteps, ph[0], ph[1], ph[2], ph[3], ph[4],
@@ -934,6 +970,27 @@ void fused_profile_cores(double *ms, double *steps, long long *launches) {
   unsigned long long c[TT_MAX_D];
   cudaMemcpyFromSymbol(c, g_gm_tag_steps, sizeof(c));
   for (int t = 0; t < TT_MAX_D; ++t) steps[t] = (double)c[t];
+  if (g_fp.used == 0) {   // no events (device-resident loops): the in-kernel timer
+    unsigned long long ns[TT_MAX_D], nl[TT_MAX_D];
+    cudaMemcpyFromSymbol(ns, g_gm_tag_ns, sizeof(ns));
+    cudaMemcpyFromSymbol(nl, g_gm_tag_launches, sizeof(nl));
+    for (int t = 0; t < TT_MAX_D; ++t) { ms[t] = 1e-6 * (double)ns[t]; launches[t] = (long long)nl[t]; }
+  }
+}
+
+// in-kernel timer totals since the last read (ms, launches that did work); resets them
+void fused_timer_read(double *ms, long long *launches) {
+  unsigned long long ns[TT_MAX_D], nl[TT_MAX_D];
+  cudaMemcpyFromSymbol(ns, g_gm_tag_ns, sizeof(ns));
+  cudaMemcpyFromSymbol(nl, g_gm_tag_launches, sizeof(nl));
+  double t = 0.0;
+  long long l = 0;
+  for (int i = 0; i < TT_MAX_D; ++i) { t += 1e-6 * (double)ns[i]; l += (long long)nl[i]; }
+  const unsigned long long z[TT_MAX_D] = {};
+  cudaMemcpyToSymbol(g_gm_tag_ns, z, sizeof(z));
+  cudaMemcpyToSymbol(g_gm_tag_launches, z, sizeof(z));
+  if (ms) *ms = t;
+  if (launches) *launches = l;
 }
 
 void fused_profile_read(long long *launches, double *ms, double *flops) {
@@ -944,14 +1001,19 @@ void fused_profile_read(long long *launches, double *ms, double *flops) {
     cudaEventElapsedTime(&e, g_fp.ev[i], g_fp.ev[i + 1]);
     t += e;
   }
+  const bool events = g_fp.used > 0;
+  double tk = 0.0;
+  long long lk = 0;
+  if (!events) fused_timer_read(&tk, &lk);   // (with events the timer totals stay for tt_fused_timer_read)
   unsigned long long c[3] = {0, 0, 0};
   cudaMemcpyFromSymbol(c, g_gm_counters, sizeof(c));
   const unsigned long long z[3] = {0, 0, 0};
   cudaMemcpyToSymbol(g_gm_counters, z, sizeof(z));
   const unsigned long long zt[TT_MAX_D] = {};
   cudaMemcpyToSymbol(g_gm_tag_steps, zt, sizeof(zt));
-  if (launches) *launches = (long long)(g_fp.used / 2);
-  if (ms) *ms = t;
+  // events when they were recorded (host-stepped loops), else the in-kernel timer
+  if (launches) *launches = events ? (long long)(g_fp.used / 2) : lk;
+  if (ms) *ms = events ? t : tk;
   if (flops) { flops[0] = (double)c[0]; flops[1] = (double)c[1]; flops[2] = (double)c[2]; }
   g_fp.used = 0;
 }
@@ -994,7 +1056,7 @@ tt_status launch_gmres_chunk(GmState *st, const GemmDesc *gapp, double *V, long 
   a.tag = g_fp.tag;
   void *args[] = {(void *)&a};
   cudaEvent_t e0 = nullptr, e1 = nullptr;
-  if (g_fp.on) {
+  if (g_fp.on && !stream_capturing(s)) {   // (inside a captured graph: the in-kernel timer only)
     while (g_fp.ev.size() < g_fp.used + 2) {
       cudaEvent_t ev;
       cudaEventCreate(&ev);

@@ -5,6 +5,7 @@
 #include <cstring>
 
 #include "amen.h"
+#include "gmres.h"
 #include "tt_common.cuh"
 
 namespace tt {
@@ -119,11 +120,19 @@ __global__ void keff_decide_kernel(KeffScal *sc, double tol_k, double tol_res, i
   if (status_out) *status_out = sc->status;
 }
 
+constexpr int KEFF_HIST = 1024;   // iterations recorded in the histories (include/tt.h)
+
 struct KeffWS {
   MatMeta FT, SF, M;
   VecMeta ones, f, SP, FP, B, z0, zmv, Rv, Hv, zr;
   KeffScal *sc;
-  double *nrm, *dbuf;
+  double *nrm, *dbuf, *k0buf;
+  float *kscr;     // operator-kind detection scratch
+  // report buffers inside the workspace: the captured graph writes these (so it
+  // does not depend on the caller's report pointers) and a copy-out kernel after
+  // the launch fills the caller's keff_report
+  double *ok, *ores, *okh, *orh;
+  int *oit, *ost, *osh, *oih;
   int *sweeps, *inner;
   char *sub;       // scratch for round / dot / orth / amen
   size_t sub_cap;
@@ -218,6 +227,16 @@ tt_status carve_keff(const MatMeta &H, const MatMeta &S, const MatMeta &F, const
   W.sc = ar.take<KeffScal>(1);
   W.nrm = ar.take<double>(1);
   W.dbuf = ar.take<double>(4);
+  W.k0buf = ar.take<double>(1);
+  W.kscr = ar.take<float>(KIND_SCRATCH_FLOATS);
+  W.ok = ar.take<double>(1);
+  W.ores = ar.take<double>(1);
+  W.okh = ar.take<double>(KEFF_HIST);
+  W.orh = ar.take<double>(KEFF_HIST);
+  W.oit = ar.take<int>(1);
+  W.ost = ar.take<int>(1);
+  W.osh = ar.take<int>(KEFF_HIST);
+  W.oih = ar.take<int>(KEFF_HIST);
   W.sweeps = ar.take<int>(1);
   W.inner = ar.take<int>(1);
   // scratch: the max over the sub-operations
@@ -258,14 +277,36 @@ size_t keff_ws_bytes(const MatMeta &H, const MatMeta &S, const MatMeta &F, const
   return ar.used;
 }
 
-tt_status keff_meta(const MatMeta &H, const MatMeta &S, const MatMeta &F, const VecMeta &psi, const VecMeta &z,
-                    double k0, const keff_opts &o, const keff_report &rep, Arena &ar, cudaStream_t s,
-                    const double *k0_dev = nullptr) {
+// kinds of the operator cores (als.h CoreKind) detected once per call, before any
+// capture; the derived operators inherit them: S + F/k and H - (S + F/k) are
+// block sums whose core k is diagonal iff every summand's core k is
+tt_status detect_ops_kinds(MatMeta &H, MatMeta &S, MatMeta &F, float *scratch, cudaStream_t s) {
+  if (!H.kinds_set) TT_TRY(detect_core_kinds(H, scratch, s));
+  if (!S.kinds_set) TT_TRY(detect_core_kinds(S, scratch, s));
+  if (!F.kinds_set) TT_TRY(detect_core_kinds(F, scratch, s));
+  return TT_OK;
+}
+void derive_kinds(KeffWS &W, const MatMeta &H, const MatMeta &S, const MatMeta &F) {
+  for (int k = 0; k < H.d; ++k) {
+    W.SF.kind[k] = S.kind[k] && F.kind[k];
+    W.M.kind[k] = H.kind[k] && W.SF.kind[k];
+  }
+  W.SF.kinds_set = 1;
+  W.M.kinds_set = 1;
+}
+
+// The enqueue of one keff_fixed_point call; k0 is read on the device (k0_dev).
+// Kinds of H, S, F must be set.  Under a capture with device loops the outer
+// iteration is a conditional WHILE node (K11).
+tt_status keff_body(const MatMeta &H, const MatMeta &S, const MatMeta &F, const VecMeta &psi, const VecMeta &z,
+                    const double *k0_dev, const keff_opts &o, const keff_report &rep, Arena &ar, cudaStream_t s) {
   KeffWS W;
   TT_TRY(carve_keff(H, S, F, psi, z, o, ar, W));
   if (!ar.base) return TT_OK;
   if (!ar.ok()) return fail(TT_ERR_CAPACITY, "keff_fixed_point: workspace too small");
-  if (!(k0 != 0.0)) return fail(TT_ERR_ARG, "keff_fixed_point: k0 must be nonzero");
+  if (!H.kinds_set || !S.kinds_set || !F.kinds_set) return fail(TT_ERR_ARG, "keff: operator kinds not detected");
+  derive_kinds(W, H, S, F);
+  const double k0 = 1.0;   // placeholder: keff_init_kernel takes *k0_dev
   const int d = H.d;
   auto sub = [&]() {
     Arena a;
@@ -296,7 +337,6 @@ tt_status keff_meta(const MatMeta &H, const MatMeta &S, const MatMeta &F, const 
   ao.restart = o.gmres_restart;
   ao.max_restarts = o.gmres_max_restarts;
   ao.dense_max = o.local_dense_max;
-  int hflag = 0;
   const bool mv = o.matvec == 1;
   // fixed-point residual ||H Psi - (S + F/k) Psi|| / ||H Psi|| (Z19) of the
   // current normalised Psi and k, both products fitted by amen_mv
@@ -317,7 +357,8 @@ tt_status keff_meta(const MatMeta &H, const MatMeta &S, const MatMeta &F, const 
   if (rep.res_dev) cudaMemsetAsync(rep.res_dev, 0xff, sizeof(double), s);   // NaN pattern until evaluated
   if (rep.res_hist_dev && rep.hist_cap > 0) fill_kernel<<<1, 256, 0, s>>>(rep.res_hist_dev, rep.hist_cap, -1.0);
   if (mv && !o.warm) TT_TRY(copy_meta(psi, W.B, s));   // first amen_mv guess: Psi_0
-  for (int it = 0; it < o.max_outer; ++it) {
+  // one fixed-point iteration (Eq. 8), ending with the device decision in sc->flag
+  auto iteration = [&]() -> tt_status {
     if (!mv) {
       TT_TRY(matvec_meta(S, psi, W.SP, s));
       { Arena a = sub(); TT_TRY(round_meta(W.SP, o.eps_round, o.rmax, nullptr, nullptr, 0, a, s)); }
@@ -341,12 +382,89 @@ tt_status keff_meta(const MatMeta &H, const MatMeta &S, const MatMeta &F, const 
     TT_TRY(scale_meta(psi, &W.sc->nrm_inv, 1.0, 0, s));
     if (o.tol_res > 0.0) TT_TRY(residual());
     keff_decide_kernel<<<1, 1, 0, s>>>(W.sc, o.tol_k, o.tol_res, o.max_outer, rep.k_dev, rep.iters_dev, rep.status_dev);
-    TT_TRY(read_back(&hflag, &W.sc->flag, sizeof(int), s));
-    TT_TRY(check_launch("keff iteration"));
-    if (hflag) break;
+    return check_launch("keff iteration");
+  };
+  if (device_loops(s)) {   // K11: do { iteration } while (!flag) as a conditional WHILE node
+    TT_TRY(dev_while(s, [&](cudaGraphConditionalHandle h) -> tt_status {
+      TT_TRY(iteration());
+      return cond_from_flag(h, &W.sc->flag, s);
+    }));
+  } else {
+    for (int it = 0; it < o.max_outer; ++it) {
+      TT_TRY(iteration());
+      int hflag = 0;
+      TT_TRY(read_back(&hflag, &W.sc->flag, sizeof(int), s));
+      TT_TRY(check_launch("keff iteration"));
+      if (hflag) break;
+    }
   }
   if (o.tol_res == 0.0) TT_TRY(residual());   // reported once for the final iterate
   return check_launch("keff_fixed_point");
+}
+
+__global__ void set_f64_kernel(double *p, double v) { *p = v; }
+
+// internal report -> the caller's keff_report (n history entries; res_hist beyond
+// them keeps the "not evaluated" mark -1)
+__global__ void keff_copy_out_kernel(const keff_report in, const keff_report out, int n) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    if (out.k_dev) *out.k_dev = *in.k_dev;
+    if (out.iters_dev) *out.iters_dev = *in.iters_dev;
+    if (out.status_dev) *out.status_dev = *in.status_dev;
+    if (out.res_dev) *out.res_dev = *in.res_dev;
+  }
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < out.hist_cap; i += gridDim.x * blockDim.x) {
+    const bool h = i < n;
+    if (out.k_hist_dev && h) out.k_hist_dev[i] = in.k_hist_dev[i];
+    if (out.res_hist_dev) out.res_hist_dev[i] = h ? in.res_hist_dev[i] : -1.0;
+    if (out.sweeps_hist_dev && h) out.sweeps_hist_dev[i] = in.sweeps_hist_dev[i];
+    if (out.inner_status_hist_dev && h) out.inner_status_hist_dev[i] = in.inner_status_hist_dev[i];
+  }
+}
+
+// keff_fixed_point entry: detect the operator kinds (one read-back), store k0 on
+// the device, then enqueue the call — as ONE graph launch in graph mode 2 (the
+// outer loop and every sweep loop decided on the device), replayed while the
+// operands, workspace and options are the same.
+tt_status keff_meta(const MatMeta &H0, const MatMeta &S0, const MatMeta &F0, const VecMeta &psi, const VecMeta &z,
+                    double k0, const keff_opts &o, const keff_report &rep, Arena &ar, cudaStream_t s) {
+  KeffWS W;
+  const Arena ar0 = ar;
+  TT_TRY(carve_keff(H0, S0, F0, psi, z, o, ar, W));
+  if (!ar.base) return TT_OK;
+  if (!ar.ok()) return fail(TT_ERR_CAPACITY, "keff_fixed_point: workspace too small");
+  if (!(k0 != 0.0)) return fail(TT_ERR_ARG, "keff_fixed_point: k0 must be nonzero");
+  MatMeta H = H0, S = S0, F = F0;
+  TT_TRY(detect_ops_kinds(H, S, F, W.kscr, s));
+  set_f64_kernel<<<1, 1, 0, s>>>(W.k0buf, k0);
+  TT_TRY(check_launch("keff k0"));
+  keff_report ir;
+  ir.k_dev = W.ok; ir.iters_dev = W.oit; ir.k_hist_dev = W.okh; ir.res_hist_dev = W.orh; ir.hist_cap = KEFF_HIST;
+  ir.status_dev = W.ost; ir.sweeps_hist_dev = W.osh; ir.inner_status_hist_dev = W.oih; ir.res_dev = W.ores;
+  auto body = [&]() -> tt_status {
+    Arena a = ar0;
+    return keff_body(H, S, F, psi, z, W.k0buf, o, ir, a, s);
+  };
+  auto copy_out = [&]() -> tt_status {
+    const int n = rep.hist_cap < KEFF_HIST ? rep.hist_cap : KEFF_HIST;
+    keff_copy_out_kernel<<<1, 256, 0, s>>>(ir, rep, n < 0 ? 0 : n);
+    return check_launch("keff report");
+  };
+  if (graph_mode() < 2 || stream_capturing(s)) {
+    TT_TRY(body());
+    return copy_out();
+  }
+  gmres_fused_grid();   // one-time attribute / occupancy queries outside the capture
+  GraphKey key;
+  key.add(H); key.add(S); key.add(F); key.add(psi); key.add(z);
+  key.add(o.tol_k); key.add(o.tol_res); key.add(o.eps_round); key.add(o.eps_solve);
+  const int ii[10] = {o.max_outer, o.rmax, o.max_sweeps, o.kickrank, o.gmres_restart, o.gmres_max_restarts,
+                      o.local_dense_max, o.matvec, o.mv_max_sweeps, o.warm};
+  key.add(ii);
+  key.add(ar0.base);
+  key.add(ar0.cap);
+  TT_TRY(run_captured(key, s, body));
+  return copy_out();
 }
 
 
@@ -412,11 +530,31 @@ __global__ void alpha_update_kernel(AlphaState *st, const double *k_dev, const i
   if (status_out) *status_out = st->status;
 }
 
+constexpr int ALPHA_HIST = 256;   // alpha iterations recorded in the histories
+
+__global__ void alpha_copy_out_kernel(const alpha_report in, const alpha_report out, int n) {
+  if (threadIdx.x == 0) {
+    if (out.alpha_dev) *out.alpha_dev = *in.alpha_dev;
+    if (out.k_dev) *out.k_dev = *in.k_dev;
+    if (out.iters_dev) *out.iters_dev = *in.iters_dev;
+    if (out.status_dev) *out.status_dev = *in.status_dev;
+  }
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    if (out.alpha_hist_dev) out.alpha_hist_dev[i] = in.alpha_hist_dev[i];
+    if (out.k_hist_dev) out.k_hist_dev[i] = in.k_hist_dev[i];
+    if (out.keff_iters_hist_dev) out.keff_iters_hist_dev[i] = in.keff_iters_hist_dev[i];
+  }
+}
+
 struct AlphaWS {
   MatMeta Ha;
   AlphaState *st;
   double *kk;
   int *kit, *kst;
+  float *kscr;
+  // internal report (see KeffWS): alpha, k, iterations, status, histories
+  double *oa, *ok, *oah, *okh;
+  int *oit, *ost, *oith;
   char *sub;
   size_t sub_cap;
 };
@@ -441,6 +579,14 @@ tt_status carve_alpha(const MatMeta &H, const MatMeta &V, const MatMeta &S, cons
   W.kk = ar.take<double>(1);
   W.kit = ar.take<int>(1);
   W.kst = ar.take<int>(1);
+  W.kscr = ar.take<float>(KIND_SCRATCH_FLOATS);
+  W.oa = ar.take<double>(1);
+  W.ok = ar.take<double>(1);
+  W.oah = ar.take<double>(ALPHA_HIST);
+  W.okh = ar.take<double>(ALPHA_HIST);
+  W.oit = ar.take<int>(1);
+  W.ost = ar.take<int>(1);
+  W.oith = ar.take<int>(ALPHA_HIST);
   size_t mx = keff_ws_bytes(W.Ha, S, F, psi, z, o.keff);
   if (mx == 0) return fail(TT_ERR_SHAPE, "alpha_secant: k-eff operands rejected");
   { Arena c; round_meta(mat_as_vec(W.Ha), 0.0, 1, nullptr, nullptr, 0, c, nullptr); mx = c.used > mx ? c.used : mx; }
@@ -459,35 +605,75 @@ size_t alpha_ws_bytes(const MatMeta &H, const MatMeta &V, const MatMeta &S, cons
   return ar.used;
 }
 
-tt_status alpha_meta(const MatMeta &H, const MatMeta &V, const MatMeta &S, const MatMeta &F, const VecMeta &psi,
+tt_status alpha_meta(const MatMeta &H0, const MatMeta &V0, const MatMeta &S0, const MatMeta &F0, const VecMeta &psi,
                      const VecMeta &z, const alpha_opts &o, const alpha_report &rep, Arena &ar, cudaStream_t s) {
   AlphaWS W;
-  TT_TRY(carve_alpha(H, V, S, F, psi, z, o, ar, W));
+  const Arena ar0 = ar;
+  TT_TRY(carve_alpha(H0, V0, S0, F0, psi, z, o, ar, W));
   if (!ar.base) return TT_OK;
   if (!ar.ok()) return fail(TT_ERR_CAPACITY, "alpha_secant: workspace too small");
   if (o.max_alpha < 1 || !(o.tol > 0.0)) return fail(TT_ERR_ARG, "alpha_secant: max_alpha >= 1, tol > 0");
-  alpha_init_kernel<<<1, 1, 0, s>>>(W.st, o.alpha0);
+  MatMeta H = H0, V = V0, S = S0, F = F0;
+  if (!V.kinds_set) TT_TRY(detect_core_kinds(V, W.kscr, s));
+  TT_TRY(detect_ops_kinds(H, S, F, W.kscr, s));
+  for (int k = 0; k < H.d; ++k) W.Ha.kind[k] = H.kind[k] && V.kind[k];   // H + alpha V^{-1}: block sum
+  W.Ha.kinds_set = 1;
   const VecMeta hv = mat_as_vec(H), vv = mat_as_vec(V), av = mat_as_vec(W.Ha);
   keff_report kr;
   std::memset(&kr, 0, sizeof(kr));
   kr.k_dev = W.kk; kr.iters_dev = W.kit; kr.hist_cap = 0; kr.status_dev = W.kst;
-  int hflag = 0;
-  for (int t = 0; t < o.max_alpha; ++t) {
+  alpha_report ir;
+  ir.alpha_dev = W.oa; ir.k_dev = W.ok; ir.iters_dev = W.oit; ir.alpha_hist_dev = W.oah; ir.k_hist_dev = W.okh;
+  ir.keff_iters_hist_dev = W.oith; ir.hist_cap = ALPHA_HIST; ir.status_dev = W.ost;
+  auto copy_out = [&]() -> tt_status {
+    int n = rep.hist_cap < ALPHA_HIST ? rep.hist_cap : ALPHA_HIST;
+    n = n < o.max_alpha ? n : o.max_alpha;
+    alpha_copy_out_kernel<<<1, 256, 0, s>>>(ir, rep, n < 0 ? 0 : n);
+    return check_launch("alpha report");
+  };
+  // one secant step: H_alpha, the k-eff solve warm-started from the previous Psi
+  // and k (the first from k0 = st->k = 1), the device update of alpha
+  auto step = [&]() -> tt_status {
     TT_TRY(add_meta(hv, &W.st->one, vv, &W.st->a, av, s));
     { Arena a; a.base = W.sub; a.cap = W.sub_cap; TT_TRY(round_meta(av, o.eps_op, 1 << 30, nullptr, nullptr, 0, a, s)); }
     cudaMemsetAsync(W.kst, 0, sizeof(int), s);
-    {
-      Arena a; a.base = W.sub; a.cap = W.sub_cap;
-      TT_TRY(keff_meta(W.Ha, S, F, psi, z, 1.0, o.keff, kr, a, s, t == 0 ? nullptr : &W.st->k));
+    { Arena a; a.base = W.sub; a.cap = W.sub_cap; TT_TRY(keff_body(W.Ha, S, F, psi, z, &W.st->k, o.keff, kr, a, s)); }
+    alpha_update_kernel<<<1, 1, 0, s>>>(W.st, W.kk, W.kit, W.kst, o.alpha1, o.tol, o.max_alpha, ir.alpha_hist_dev,
+                                        ir.k_hist_dev, ir.keff_iters_hist_dev, ir.hist_cap, ir.alpha_dev,
+                                        ir.k_dev, ir.iters_dev, ir.status_dev);
+    return check_launch("alpha iteration");
+  };
+  auto all = [&]() -> tt_status {
+    alpha_init_kernel<<<1, 1, 0, s>>>(W.st, o.alpha0);
+    if (device_loops(s))   // K11: the secant loop as a conditional WHILE node
+      return dev_while(s, [&](cudaGraphConditionalHandle h) -> tt_status {
+        TT_TRY(step());
+        return cond_from_flag(h, &W.st->flag, s);
+      });
+    for (int t = 0; t < o.max_alpha; ++t) {
+      TT_TRY(step());
+      int hflag = 0;
+      TT_TRY(read_back(&hflag, &W.st->flag, sizeof(int), s));
+      TT_TRY(check_launch("alpha iteration"));
+      if (hflag) break;
     }
-    alpha_update_kernel<<<1, 1, 0, s>>>(W.st, W.kk, W.kit, W.kst, o.alpha1, o.tol, o.max_alpha, rep.alpha_hist_dev,
-                                        rep.k_hist_dev, rep.keff_iters_hist_dev, rep.hist_cap, rep.alpha_dev,
-                                        rep.k_dev, rep.iters_dev, rep.status_dev);
-    TT_TRY(read_back(&hflag, &W.st->flag, sizeof(int), s));
-    TT_TRY(check_launch("alpha iteration"));
-    if (hflag) break;
+    return check_launch("alpha_secant");
+  };
+  if (graph_mode() < 2 || stream_capturing(s)) {
+    TT_TRY(all());
+    return copy_out();
   }
-  return check_launch("alpha_secant");
+  gmres_fused_grid();
+  GraphKey key;
+  key.add(H); key.add(V); key.add(S); key.add(F); key.add(psi); key.add(z);
+  const double dd[6] = {o.alpha0, o.alpha1, o.tol, o.eps_op, o.keff.tol_k, o.keff.tol_res};
+  const double de[2] = {o.keff.eps_round, o.keff.eps_solve};
+  const int ii[11] = {o.max_alpha, o.keff.max_outer, o.keff.rmax, o.keff.max_sweeps, o.keff.kickrank,
+                      o.keff.gmres_restart, o.keff.gmres_max_restarts, o.keff.local_dense_max, o.keff.matvec,
+                      o.keff.mv_max_sweeps, o.keff.warm};
+  key.add(dd); key.add(de); key.add(ii); key.add(ar0.base); key.add(ar0.cap);
+  TT_TRY(run_captured(key, s, all));
+  return copy_out();
 }
 
 }  // namespace tt

@@ -30,6 +30,8 @@ struct MatMeta {
   double *data;
   int *R;  // device ranks [d+1]
   int kind[TT_MAX_D];  // core structure (als.h CoreKind), set by detect_core_kinds; 0 = dense
+  int kinds_set;       // 1: kind[] is valid (the drivers detect once per call, before any capture)
+  int pad_;            // explicit: no padding bytes (metas are part of the CUDA-graph cache keys)
 };
 
 // Device-side structure detection of the operator cores (als.h CoreKind): a
@@ -130,15 +132,42 @@ tt_status launch_gemm(const GemmDesc *descs_dev, int count, int Mcap, int Ncap, 
 // count (count must then be 1).
 tt_status launch_gemm_k(const GemmDesc *descs_dev, int count, int Mcap, int Ncap, int Kcap, cudaStream_t s,
                         int batch = 0);
-// A dependent chain of `count` GEMMs (descriptor i consumes earlier outputs) with
-// per-GEMM capacity shapes: one thread-block-cluster launch when all are small.
 // CUDA-graph replay of a fixed launch sequence (graph.cu): `enqueue` launches on
 // `s` (taken by reference: it points at a private capture stream while recording).
+// The key is the exact bytes the sequence depends on (compared in full on a hit).
 uint64_t hash_bytes(const void *p, size_t n, uint64_t h = 1469598103934665603ull);
-tt_status run_captured(uint64_t key, cudaStream_t &s, const std::function<tt_status()> &enqueue);
+struct GraphKey {
+  uint64_t h = 1469598103934665603ull;
+  std::string bytes;
+  void add(const void *p, size_t n);
+  template <class T> void add(const T &v) { add(&v, sizeof(T)); }
+};
+tt_status run_captured(const GraphKey &key, cudaStream_t &s, const std::function<tt_status()> &enqueue);
+// 0 no graphs, 1 replayed sequences + host-polled loops, 2 device-resident loops
+int graph_mode();
+void set_graph_mode(int mode);   // -1: back to the environment default
+void graph_stats(long long *captures, long long *replays, long long *cached);
+bool stream_capturing(cudaStream_t s);
+// true when the drivers' convergence loops are to be emitted as conditional
+// graph nodes (graph mode 2 and s is being captured)
+bool device_loops(cudaStream_t s);
+tt_status cond_handle(cudaStream_t s, cudaGraphConditionalHandle *h);
+tt_status cond_node(cudaStream_t &s, cudaGraphConditionalHandle h, int is_while,
+                    const std::function<tt_status()> &body);
+tt_status cond_set(cudaGraphConditionalHandle h, unsigned int v, cudaStream_t s);
+tt_status cond_from_flag(cudaGraphConditionalHandle h, const int *flag_dev, cudaStream_t s);   // h = (*flag == 0)
+// do { body(h) } while (h): the body must end by setting h on the device
+tt_status dev_while(cudaStream_t &s, const std::function<tt_status(cudaGraphConditionalHandle)> &body);
+// A dependent chain of `count` GEMMs (descriptor i consumes earlier outputs) with
+// per-GEMM capacity shapes, one launch each.
 tt_status launch_gemm_seq(const GemmDesc *descs_dev, int count, const int *Mcap, const int *Ncap, const int *Kcap,
                           cudaStream_t s, const int *Bcap = nullptr);
 void set_gemm_scratch(double *ptr, size_t bytes);
+// the split-K scratch registered by a driver is a slice of ITS workspace: cleared
+// when the driver returns, so no later launch writes into a released workspace
+struct ScratchScope {
+  ~ScratchScope() { set_gemm_scratch(nullptr, 0); }
+};
 constexpr size_t GEMM_SPLIT_SCRATCH = 32ull << 20;  // bytes reserved by callers that enable split-K
 
 // ------------------------------------------------------------- linalg ---

@@ -156,6 +156,7 @@ tt_status detect_core_kinds(MatMeta &A, float *scratch_dev, cudaStream_t s, doub
     A.kind[k] = (r[k] >= 0.f && r[k] <= (float)KIND_DIAG_TOL) ? 1 : 0;
     if (ratio_out) ratio_out[k] = r[k];
   }
+  A.kinds_set = 1;
   return TT_OK;
 }
 

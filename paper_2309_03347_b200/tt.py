@@ -475,3 +475,23 @@ def alpha_secant(H: TTMat, V: TTMat, S: TTMat, F: TTMat, psi: TTVec, z: TTVec, a
     check(lib().alpha_secant(H.c, V.c, S.c, F.c, psi.c, z.c, C.byref(o), C.byref(rep), _ptr(ws), ws.numel(),
                              C.c_void_p(_stream(stream))))
     return AlphaResult(a, k, it, ah, kh, ih, st)
+
+
+# ------------------------------------------------------------ K11 graphs ---
+
+def set_graph_mode(mode: int):
+    """Driver execution mode of the calling thread (include/tt.h tt_set_graph_mode):
+    2 device-resident loops (default), 1 replayed sequences + host-polled loops,
+    0 no graphs, -1 the environment default."""
+    lib().tt_set_graph_mode(int(mode))
+
+
+def graph_mode() -> int:
+    return int(lib().tt_graph_mode())
+
+
+def graph_stats():
+    """(captures, replays, cached graphs) of the calling thread so far."""
+    c, r, n = C.c_int64(0), C.c_int64(0), C.c_int64(0)
+    lib().tt_graph_stats(C.byref(c), C.byref(r), C.byref(n))
+    return c.value, r.value, n.value

@@ -458,19 +458,20 @@ print(repr(r.k.item()), r.iters.item())
 
 def test_keff_deterministic_graphs_on_off():
     """The device path is deterministic (fixed reduction orders, no atomics in the
-    arithmetic): two C1 solves give bitwise-identical k, and replaying the
-    captured CUDA graphs gives the same bits as direct launches (TT_NO_GRAPHS=1)."""
+    arithmetic): two C1 solves give bitwise-identical k, and the device-resident
+    graph (default), the host-polled loops of replayed sequences (TT_NO_DEVLOOP=1)
+    and direct launches (TT_NO_GRAPHS=1) give the same bits."""
     import subprocess
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     outs = []
-    for env_extra in ({}, {}, {"TT_NO_GRAPHS": "1"}):
+    for env_extra in ({}, {}, {"TT_NO_GRAPHS": "1"}, {"TT_NO_DEVLOOP": "1"}):
         env = dict(os.environ, PYTHONPATH=root, **env_extra)
         r = subprocess.run([sys.executable, "-c", _DET_SCRIPT], capture_output=True, text=True, env=env, cwd=root,
                            timeout=600)
         assert r.returncode == 0, r.stderr[-2000:]
         outs.append(r.stdout.strip().splitlines()[-1])
-    assert outs[0] == outs[1] == outs[2], outs
+    assert outs[0] == outs[1] == outs[2] == outs[3], outs
 
 
 def test_keff_warm_continuation():
@@ -545,3 +546,87 @@ def test_keff_dense_local_solver_c1():
                        local_dense_max=2000)
     assert res.status.item() == 0
     assert abs(res.k.item() - kd) / kd <= 1e-8
+
+
+# ------------------------------------------------------------------ K11 ---
+
+def _in_modes(fn):
+    out = {}
+    try:
+        for mode in (2, 1, 0):
+            tb.set_graph_mode(mode)
+            out[mode] = fn()
+            torch.cuda.synchronize()
+    finally:
+        tb.set_graph_mode(-1)
+    return out
+
+
+def test_device_loops_keff_bitwise():
+    """keff_fixed_point as ONE graph launch (outer WHILE node, nested
+    amen_mv / AMEn sweep WHILE + IF nodes, residual every iteration) gives the
+    same k, histories, status and Psi bits as the host-polled loops (mode 1) and
+    direct launches (mode 0); a repeated call replays the cached graph."""
+    p = small_c1(4)
+    modes = [4, 4, 4, 8, 1]
+
+    def run():
+        r, psi = _keff_gpu(p, modes, rmax=32, max_outer=12, tol_k=1e-12, tol_res=1e-6, eps_round=1e-10,
+                           eps_solve=1e-10, matvec="amen_mv", max_sweeps=6, mv_max_sweeps=6)
+        return (r.k.item(), r.iters.item(), r.status.item(), r.k_hist[:12].cpu().numpy().tolist(),
+                r.sweeps_hist[:12].cpu().numpy().tolist(), r.res_hist[:12].cpu().numpy().tolist(),
+                [c.tobytes() for c in psi.cores()])
+    out = _in_modes(run)
+    assert out[2][:6] == out[1][:6] == out[0][:6], (out[2][:6], out[1][:6])
+    assert out[2][6] == out[1][6] == out[0][6]
+    assert out[2][1] >= 3
+    # exact-product B variant, one more time in mode 2: the second identical call replays
+    ops = gtr.operators(p)
+    g = inputs.rng(61)
+    psi = tb.TTVec.from_cores([np.ones((1, n, 1)) for n in modes], rcap=[1, 36, 36, 36, 36, 1])
+    z = tb.TTVec.from_cores(inputs.random_tt(g, modes, [1, 4, 4, 4, 4, 1]))
+    nb = tb.keff_workspace_bytes(ops["H"], ops["S"], ops["F"], psi, z, rmax=32)
+    ws = torch.empty(nb, dtype=torch.uint8, device="cuda")
+    psi0, zc0 = [c.copy() for c in psi.cores()], [c.copy() for c in z.cores()]
+    ks = []
+    for rep in range(2):
+        psi.set_cores(psi0)
+        z.set_cores(zc0)
+        if rep == 1:
+            c0, r0, _ = tb.graph_stats()
+        r = tb.keff_fixed_point(ops["H"], ops["S"], ops["F"], psi, z, rmax=32, max_outer=3, tol_k=0.0,
+                                eps_round=1e-10, eps_solve=1e-10, ws=ws)
+        ks.append(r.k.item())
+    c1, r1, _ = tb.graph_stats()
+    assert c1 == c0 and r1 == r0 + 1, (c0, c1, r0, r1)
+    assert ks[0] == ks[1], ks
+
+
+def test_device_loops_amen_and_alpha_bitwise():
+    """amen_solve (sweep WHILE + IF) and alpha_secant (secant WHILE around the
+    k-eff WHILE) in one graph each: the same bits as modes 1 and 0."""
+    g = inputs.rng(60)
+    prob = small_c1(4)
+    ops = gtr.operators(prob)
+    modes = [4, 4, 4, 8, 1]
+    b = inputs.random_tt(g, modes, [1, 2, 3, 2, 1, 1])
+    zc = inputs.random_tt(g, modes, [1, 4, 4, 4, 4, 1])
+
+    def run_amen():
+        x = tb.TTVec.from_cores([np.ones((1, n, 1)) for n in modes], rcap=[1, 20, 20, 20, 20, 1])
+        z = tb.TTVec.from_cores(zc)
+        _, sweeps, res = tb.amen_solve(ops["H"], tb.TTVec.from_cores(b), x, z, eps=1e-11)
+        return sweeps.item(), res.item(), [c.tobytes() for c in x.cores()]
+    out = _in_modes(run_amen)
+    assert out[2] == out[1] == out[0], (out[2][:2], out[1][:2], out[0][:2])
+
+    sup = small_c1(4)
+    sup["materials"][0]["nu_sigma_f"] = np.array([2.8])   # supercritical cube (test_alpha_cube_vs_dense)
+
+    def run_alpha():
+        r = _alpha_gpu(sup, modes, rmax=32, tol=1e-11, tol_k=1e-12, eps_round=1e-13, eps_solve=1e-12)
+        return (r.alpha.item(), r.k.item(), r.iters.item(), r.status.item(),
+                r.alpha_hist[:r.iters.item()].cpu().numpy().tolist())
+    out = _in_modes(run_alpha)
+    assert out[2] == out[1] == out[0], (out[2], out[1], out[0])
+    assert out[2][3] == 0
