@@ -65,46 +65,80 @@ struct Cfg {
   static constexpr size_t SMEM = (size_t)STAGES * (A_ELEMS + B_ELEMS) * sizeof(double);
 };
 
-template <class C, int BM, int BN, int BK>
-__device__ __forceinline__ void load_tile(double *sa, double *sb, const GemmDesc &g, int m0, int n0, int k0,
-                                          int tid) {
-  constexpr int T = C::THREADS;
-  const double *A = g.A, *B = g.B;
-  if (!g.transA) {  // A(m,k) = A[m + k lda]: consecutive threads along m
+// Operand tile loader with strength-reduced addressing.  An operand tile is
+// MN x BK (MN = BM rows of A or BN columns of B) staged as smem[k][MN + PAD].
+// Each thread owns NI = MN BK / T elements whose (mn, k) positions inside the
+// tile never change, so the global address of element i at k-tile kt is
+// p + i istride + kt kstep: one pointer, advanced once per k-tile, instead of a
+// 64-bit multiply, two divisions and two bound tests per element and k-tile
+// (ncu source page of the round-2 fused GMRES kernel: ~50 SASS instructions per
+// cp.async, as many issue slots in the load code as in the DMMA block).
+//   mn-contiguous operand (A not transposed, B transposed): thread -> mn = tid % MN,
+//     k = tid / MN + i (T / MN); the mn bound is one bit, the k bound per element.
+//   k-contiguous operand (A transposed, B not transposed): thread -> k = tid % BK,
+//     mn = tid / BK + i (T / BK); the k bound is one test, the mn bounds a bit mask.
+template <int MN, int BK, int T>
+struct OpLoader {
+  static constexpr int NI = MN * BK / T;
+  static_assert(T % MN == 0 && T % BK == 0 && NI >= 1 && NI <= 32, "tile / thread-count mismatch");
+  const double *p;      // element 0 of this thread at the next k-tile to load
+  const double *safe;   // any valid address (predicated-off copies read nothing)
+  long long istride, kstep;
+  unsigned mask;        // bit i: element i inside the mn range
+  int soff;             // smem offset of element 0
+  int kfirst;           // k index of element 0 inside a k-tile
+  int K;
+  bool kc;              // k-contiguous operand
+  __device__ __forceinline__ void init(const double *base, long long ld, bool kcontig, int mn0, int MNtot, int K_,
+                                       int tid) {
+    kc = kcontig;
+    K = K_;
+    safe = base;
+    if (!kc) {
+      const int mn = tid % MN, kk = tid / MN;
+      p = base + (mn0 + mn) + (long long)kk * ld;
+      istride = (long long)(T / MN) * ld;
+      kstep = (long long)BK * ld;
+      soff = kk * (MN + PAD) + mn;
+      kfirst = kk;
+      mask = (mn0 + mn < MNtot) ? 0xffffffffu : 0u;
+    } else {
+      const int kk = tid % BK, mn = tid / BK;
+      p = base + kk + (long long)(mn0 + mn) * ld;
+      istride = (long long)(T / BK) * ld;
+      kstep = BK;
+      soff = kk * (MN + PAD) + mn;
+      kfirst = kk;
+      unsigned mk = 0;
 #pragma unroll
-    for (int e = tid; e < BM * BK; e += T) {
-      const int m = e % BM, k = e / BM;
-      const int gm = m0 + m, gk = k0 + k;
-      const bool p = gm < g.M && gk < g.K;
-      cp_async8(sa + k * (BM + PAD) + m, p ? A + gm + (long long)gk * g.lda : A, p);
-    }
-  } else {  // A(m,k) = A[k + m lda]: consecutive threads along k
-#pragma unroll
-    for (int e = tid; e < BM * BK; e += T) {
-      const int k = e % BK, m = e / BK;
-      const int gm = m0 + m, gk = k0 + k;
-      const bool p = gm < g.M && gk < g.K;
-      cp_async8(sa + k * (BM + PAD) + m, p ? A + gk + (long long)gm * g.lda : A, p);
+      for (int i = 0; i < NI; ++i)
+        if (mn0 + mn + i * (T / BK) < MNtot) mk |= 1u << i;
+      mask = mk;
     }
   }
-  if (!g.transB) {  // B(k,n) = B[k + n ldb]
+  // load the k-tile starting at k0 (k-tiles must be requested in increasing order)
+  __device__ __forceinline__ void load(double *sbuf, int k0) {
+    const double *q = p;
+    if (!kc) {
+      const bool mok = mask != 0;
 #pragma unroll
-    for (int e = tid; e < BN * BK; e += T) {
-      const int k = e % BK, n = e / BK;
-      const int gn = n0 + n, gk = k0 + k;
-      const bool p = gn < g.N && gk < g.K;
-      cp_async8(sb + k * (BN + PAD) + n, p ? B + gk + (long long)gn * g.ldb : B, p);
-    }
-  } else {  // B(k,n) = B[n + k ldb]
+      for (int i = 0; i < NI; ++i) {
+        const bool pr = mok && (k0 + kfirst + i * (T / MN) < K);
+        cp_async8(sbuf + soff + i * ((T / MN) * (MN + PAD)), pr ? q : safe, pr);
+        q += istride;
+      }
+    } else {
+      const bool kok = k0 + kfirst < K;
 #pragma unroll
-    for (int e = tid; e < BN * BK; e += T) {
-      const int n = e % BN, k = e / BN;
-      const int gn = n0 + n, gk = k0 + k;
-      const bool p = gn < g.N && gk < g.K;
-      cp_async8(sb + k * (BN + PAD) + n, p ? B + gn + (long long)gk * g.ldb : B, p);
+      for (int i = 0; i < NI; ++i) {
+        const bool pr = kok && ((mask >> i) & 1u);
+        cp_async8(sbuf + soff + i * (T / BK), pr ? q : safe, pr);
+        q += istride;
+      }
     }
+    p += kstep;
   }
-}
+};
 
 // splits > 1: split-K; CTA z computes the K-slice z and writes its raw partial
 // product to partial + z * pstride (column-major, ld = pld); gemm_splitk_reduce
@@ -137,10 +171,17 @@ __device__ __forceinline__ void gemm_tile(const GemmDesc &g0, int m0, int n0, in
     for (int j = 0; j < C::TN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
   const int nk = (g.K + BK - 1) / BK;
+  OpLoader<BM, BK, C::THREADS> la;
+  OpLoader<BN, BK, C::THREADS> lb;
+  la.init(g.A, g.lda, g.transA != 0, m0, g.M, g.K, tid);
+  lb.init(g.B, g.ldb, g.transB == 0, n0, g.N, g.K, tid);
   // prologue: STAGES-1 tiles in flight
 #pragma unroll
   for (int st = 0; st < STAGES - 1; ++st) {
-    if (st < nk) load_tile<C, BM, BN, BK>(sA + st * C::A_ELEMS, sB + st * C::B_ELEMS, g, m0, n0, st * BK, tid);
+    if (st < nk) {
+      la.load(sA + st * C::A_ELEMS, st * BK);
+      lb.load(sB + st * C::B_ELEMS, st * BK);
+    }
     cp_async_commit();
   }
   for (int kt = 0; kt < nk; ++kt) {
@@ -150,7 +191,8 @@ __device__ __forceinline__ void gemm_tile(const GemmDesc &g0, int m0, int n0, in
       const int nt = kt + STAGES - 1;
       if (nt < nk) {
         const int sl = nt % STAGES;
-        load_tile<C, BM, BN, BK>(sA + sl * C::A_ELEMS, sB + sl * C::B_ELEMS, g, m0, n0, nt * BK, tid);
+        la.load(sA + sl * C::A_ELEMS, nt * BK);
+        lb.load(sB + sl * C::B_ELEMS, nt * BK);
       }
       cp_async_commit();
     }
