@@ -498,9 +498,13 @@ __device__ __forceinline__ void phase_sync(unsigned int *bar, unsigned int nbloc
 // One GEMM as a phase of a persistent kernel: DMMA tiles distributed over the
 // CTAs (split-K with an in-kernel reduction when the GEMM has few tiles), then a
 // phase barrier.  Uniform control flow: every CTA reads the same descriptor.
+// own_lo/own_hi >= 0: the output is the plain contiguous vector C[0 .. M N) and the
+// caller goes on to work on its own slice [own_lo, own_hi) only: after a split-K
+// pass each CTA reduces the slices of exactly that range and the closing grid
+// barrier is dropped (the next phase reads what this CTA wrote itself).
 template <bool CLUSTER>
 __device__ void gemm_stage(const GemmDesc &g, double *split, long long split_elems, unsigned int *bar, int G,
-                           double *smem, bool gm_count, bool check_skip = true) {
+                           double *smem, bool gm_count, bool check_skip = true, int own_lo = -1, int own_hi = -1) {
   if (g.M <= 0 || g.N <= 0) return;
   if (check_skip && g.skip && *g.skip) return;
   const int tid = threadIdx.x;
@@ -576,6 +580,17 @@ __device__ void gemm_stage(const GemmDesc &g, double *split, long long split_ele
     const long long total = (long long)g.M * g.N, ps = total;
     double alpha = g.alpha;
     if (g.alpha_dev) alpha *= *g.alpha_dev;
+    if (own_lo >= 0 && g.s_r0 == 1 && g.s_c0 == g.M && g.dr >= g.M && g.dc >= g.N) {
+      for (int e = own_lo + tid; e < own_hi; e += GF_THREADS) {
+        double sum = 0.0;
+        for (int z = 0; z < splits; ++z) sum += split[z * ps + e];
+        double v = alpha * sum;
+        if (g.beta != 0.0) v += g.beta * g.C[e];
+        g.C[e] = v;
+      }
+      __syncthreads();
+      return;
+    }
     for (long long e = (long long)blockIdx.x * GF_THREADS + tid; e < total; e += (long long)G * GF_THREADS) {
       const int r = (int)(e % g.M), c = (int)(e / g.M);
       double sum = 0.0;
@@ -590,15 +605,10 @@ __device__ void gemm_stage(const GemmDesc &g, double *split, long long split_ele
   }
 }
 
-// out[i] = sum_c part[c * GF_LD + i] for i < n: all G x n partials are loaded
-// in one parallel round into shared memory, then summed in c order (the same
-// bits in every CTA).  sred >= GF_RED doubles; falls back to direct reads
-// when G * n exceeds it.
-constexpr int GF_RED = 2048;
-
 // out[i] = sum_{e in [lo, hi)} V_i[e] w[e] for i < n: each warp takes groups of
-// 8 vectors and keeps 8 accumulators per lane, so all loads of a group are in
-// flight before the (shuffle) reductions.
+// 8 vectors and keeps 8 accumulators per lane; two elements per lane and trip,
+// so 16 basis loads are in flight before the first FMA (a CTA's slice of a QTT
+// core's local vector is ~120 elements: the phase is pure L2 latency).
 __device__ __forceinline__ void slice_dots(const double *V, long long ldv, const double *w, int lo, int hi, int n,
                                            double *out) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -607,11 +617,20 @@ __device__ __forceinline__ void slice_dots(const double *V, long long ldv, const
     double acc[8];
 #pragma unroll
     for (int q = 0; q < 8; ++q) acc[q] = 0.0;
-    for (int e = lo + lane; e < hi; e += 32) {
-      const double we = w[e];
+    const double *Vg = V + (long long)i0 * ldv;
+    for (int e = lo + lane; e < hi; e += 64) {
+      const int e2 = e + 32;
+      const bool p2 = e2 < hi;
+      const double w0 = w[e], w1 = p2 ? w[e2] : 0.0;
+      double v0[8], v1[8];
 #pragma unroll
-      for (int q = 0; q < 8; ++q)
-        if (i0 + q < n) acc[q] = fma(V[(long long)(i0 + q) * ldv + e], we, acc[q]);
+      for (int q = 0; q < 8; ++q) {
+        const bool pq = i0 + q < n;
+        v0[q] = pq ? Vg[(long long)q * ldv + e] : 0.0;
+        v1[q] = (pq && p2) ? Vg[(long long)q * ldv + e2] : 0.0;
+      }
+#pragma unroll
+      for (int q = 0; q < 8; ++q) acc[q] = fma(v1[q], w1, fma(v0[q], w0, acc[q]));
     }
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
@@ -620,38 +639,50 @@ __device__ __forceinline__ void slice_dots(const double *V, long long ldv, const
     }
   }
 }
-__device__ __forceinline__ void cross_cta_sum(const double *part, int G, int n, double *out, double *sred) {
-  if (G * n <= GF_RED) {
-    for (int e = threadIdx.x; e < G * n; e += GF_THREADS) {
-      const int c = e / n, i = e - c * n;
-      sred[e] = part[(size_t)c * GF_LD + i];
-    }
-    __syncthreads();
-    for (int i = threadIdx.x; i < n; i += GF_THREADS) {
-      double s = 0.0;
-      for (int c = 0; c < G; ++c) s += sred[c * n + i];
-      out[i] = s;
-    }
-  } else {   // large grids: lanes over the CTAs (fixed order), each warp a group of 8
-             // entries with all their loads in flight (one entry at a time paid one
-             // L2 round trip per entry: ~13 us per reduction at 256 CTAs, 40 entries)
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    for (int i0 = warp * 8; i0 < n; i0 += (GF_THREADS / 32) * 8) {
-      double acc[8];
+// x - sum_{i < nv} h[i] V_i[e]: the Gram-Schmidt update of one element, basis
+// loads in batches of 8 (independent loads; a plain loop paid one L2 round trip
+// per basis vector: ~19 us per Arnoldi step at j ~ 40).
+__device__ __forceinline__ double gs_update(const double *V, long long ldv, const double *h, int nv, int e,
+                                            double x) {
+  for (int i0 = 0; i0 < nv; i0 += 8) {
+    double v[8];
 #pragma unroll
-      for (int q = 0; q < 8; ++q) acc[q] = 0.0;
-#pragma unroll 2
-      for (int c = lane; c < G; c += 32) {
+    for (int q = 0; q < 8; ++q) v[q] = (i0 + q < nv) ? V[(long long)(i0 + q) * ldv + e] : 0.0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+      if (i0 + q < nv) x = fma(-h[i0 + q], v[q], x);
+  }
+  return x;
+}
+__device__ __forceinline__ void cross_cta_sum(const double *part, int G, int n, double *out) {
+  // out[i] = sum_c part[c * GF_LD + i] for i < n
+  // lanes over the CTAs (fixed order: the same bits in every CTA), each warp a group
+  // of 8 entries, four CTAs per lane and trip so 32 loads are in flight (one entry
+  // at a time paid one L2 round trip per entry; a single thread summing G values
+  // from shared memory cost 4 us for the norm alone)
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int i0 = warp * 8; i0 < n; i0 += (GF_THREADS / 32) * 8) {
+    double acc[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) acc[q] = 0.0;
+    for (int c0 = lane; c0 < G; c0 += 128) {
+      double v[4][8];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int c = c0 + 32 * u;
         const double *pc = part + (size_t)c * GF_LD + i0;
 #pragma unroll
-        for (int q = 0; q < 8; ++q)
-          if (i0 + q < n) acc[q] += pc[q];
+        for (int q = 0; q < 8; ++q) v[u][q] = (c < G && i0 + q < n) ? pc[q] : 0.0;
       }
 #pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        const double s = warp_sum(acc[q]);
-        if (lane == 0 && i0 + q < n) out[i0 + q] = s;
-      }
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int q = 0; q < 8; ++q) acc[q] += v[u][q];
+    }
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const double s = warp_sum(acc[q]);
+      if (lane == 0 && i0 + q < n) out[i0 + q] = s;
     }
   }
   __syncthreads();
@@ -664,7 +695,6 @@ template <bool CLUSTER>
 __global__ void __launch_bounds__(GF_THREADS, GF_MINB) gm_chunk_kernel(GmChunkArgs a) {
   extern __shared__ __align__(16) double smem[];
   __shared__ double h1s[GF_LD], h2s[GF_LD], css[GF_LD], sns[GF_LD];
-  double *sred = smem;   // the GEMM tile buffers are idle during the vector phases
   __shared__ double red[GF_THREADS / 32 + 4];
   const int G = gridDim.x;
   GmState *st = a.st;
@@ -690,7 +720,8 @@ __global__ void __launch_bounds__(GF_THREADS, GF_MINB) gm_chunk_kernel(GmChunkAr
   double *part1 = a.part, *part2 = a.part + (size_t)G * GF_LD, *part3 = a.part + 2 * (size_t)G * GF_LD;
   double *w = a.w;
 #ifdef GM_PHASE_TIMING
-  long long ph[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  long long ph[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+  long long nre = 0;
   long long tcl = clock64();
 #define GM_PH(i) do { const long long t_ = clock64(); ph[i] += t_ - tcl; tcl = t_; } while (0)
 #else
@@ -718,7 +749,7 @@ __global__ void __launch_bounds__(GF_THREADS, GF_MINB) gm_chunk_kernel(GmChunkAr
   if (a.full) {
     // ---- cycle start: r = b - A x, beta = ||r||, V_0 = r / beta (gm_start_kernel's work)
     for (int sidx = 0; sidx < 3; ++sidx)
-      gemm_stage<CLUSTER>(sdesc[sidx], a.split, a.split_elems, a.bar, G, smem, true, false);
+      gemm_stage<CLUSTER>(sdesc[sidx], a.split, a.split_elems, a.bar, G, smem, true, false, sidx == 2 ? lo : -1, hi);
     double pb = 0.0, pr = 0.0;
     for (int e = lo + tid; e < hi; e += GF_THREADS) {
       const double r = a.b[e] - w[e];
@@ -737,7 +768,7 @@ __global__ void __launch_bounds__(GF_THREADS, GF_MINB) gm_chunk_kernel(GmChunkAr
       part1[(size_t)blockIdx.x * GF_LD + 1] = tr;
     }
     phase_sync<CLUSTER>(a.bar, G);
-    cross_cta_sum(part1, G, 2, h2s, sred);
+    cross_cta_sum(part1, G, 2, h2s);
     const double bn = sqrt(h2s[0]), beta = sqrt(h2s[1]);
     if (cyc == 0) bnorm = bn;
     const double rel = bn > 0.0 ? beta / bn : 0.0;
@@ -766,7 +797,8 @@ __global__ void __launch_bounds__(GF_THREADS, GF_MINB) gm_chunk_kernel(GmChunkAr
     jlast = j;
     // ---- w = A V[:, j] (three chained GEMM stages; the kernel itself stops on the stop word)
     for (int sidx = 0; sidx < 3; ++sidx) {
-      gemm_stage<CLUSTER>(sdesc[3 * (j + 1 - jbase) + sidx], a.split, a.split_elems, a.bar, G, smem, true, false);
+      gemm_stage<CLUSTER>(sdesc[3 * (j + 1 - jbase) + sidx], a.split, a.split_elems, a.bar, G, smem, true, false,
+                          sidx == 2 ? lo : -1, hi);
 #ifdef GM_PHASE_TIMING
       if (sidx < 2) GM_PH(5 + sidx);
 #endif
@@ -789,12 +821,10 @@ __global__ void __launch_bounds__(GF_THREADS, GF_MINB) gm_chunk_kernel(GmChunkAr
     }
     phase_sync<CLUSTER>(a.bar, G);
     GM_PH(2);
-    cross_cta_sum(part1, G, j + 2, h1s, sred);  // fixed order: identical in every CTA
-    for (int e = lo + tid; e < hi; e += GF_THREADS) {
-      double x = w[e];
-      for (int i = 0; i <= j; ++i) x = fma(-h1s[i], a.V[(long long)i * a.ldv + e], x);
-      w[e] = x;
-    }
+    cross_cta_sum(part1, G, j + 2, h1s);  // fixed order: identical in every CTA
+    GM_PH(7);
+    for (int e = lo + tid; e < hi; e += GF_THREADS) w[e] = gs_update(a.V, a.ldv, h1s, j + 1, e, w[e]);
+    GM_PH(8);
     // DGKS test (Daniel, Gragg, Kaufman & Stewart 1976): a second Gram-Schmidt
     // pass only when the projection removed more than half of |w|^2
     // (|w'|^2 = |w|^2 - sum h^2 < |w|^2 / 2); the decision is made on values
@@ -814,7 +844,11 @@ __global__ void __launch_bounds__(GF_THREADS, GF_MINB) gm_chunk_kernel(GmChunkAr
       double *my2 = part2 + (size_t)blockIdx.x * GF_LD;
       slice_dots(a.V, a.ldv, w, lo, hi, j + 1, my2);
       phase_sync<CLUSTER>(a.bar, G);
-      cross_cta_sum(part2, G, j + 1, h2s, sred);
+      cross_cta_sum(part2, G, j + 1, h2s);
+#ifdef GM_PHASE_TIMING
+      ++nre;
+#endif
+      GM_PH(9);
     } else {
       for (int i = tid; i <= j; i += GF_THREADS) h2s[i] = 0.0;
       __syncthreads();
@@ -822,9 +856,10 @@ __global__ void __launch_bounds__(GF_THREADS, GF_MINB) gm_chunk_kernel(GmChunkAr
     double nrm = 0.0;
     for (int e = lo + tid; e < hi; e += GF_THREADS) {
       double x = w[e];
-      if (reorth)
-        for (int i = 0; i <= j; ++i) x = fma(-h2s[i], a.V[(long long)i * a.ldv + e], x);
-      w[e] = x;
+      if (reorth) {
+        x = gs_update(a.V, a.ldv, h2s, j + 1, e, x);
+        w[e] = x;
+      }
       nrm = fma(x, x, nrm);
     }
     nrm = warp_sum(nrm);
@@ -835,10 +870,11 @@ __global__ void __launch_bounds__(GF_THREADS, GF_MINB) gm_chunk_kernel(GmChunkAr
       for (int q = 0; q < NW; ++q) t += red[q];
       part3[(size_t)blockIdx.x * GF_LD] = t;
     }
+    GM_PH(10);
     phase_sync<CLUSTER>(a.bar, G);
     GM_PH(3);
     // ---- norm, Givens (identical in every CTA), normalisation
-    cross_cta_sum(part3, G, 1, red + 2, sred);
+    cross_cta_sum(part3, G, 1, red + 2);
     const double hn = sqrt(red[2]);
     // H column j: h1 + h2, then the earlier rotations
     if (tid == 0) {
@@ -926,8 +962,8 @@ __global__ void __launch_bounds__(GF_THREADS, GF_MINB) gm_chunk_kernel(GmChunkAr
   }
 #ifdef GM_PHASE_TIMING
   if (blockIdx.x == 0 && threadIdx.x == 0 && nsteps > 0)
-    printf("GMPH %d %d %lld %lld %lld %lld %lld %lld %lld\n", (int)CLUSTER, nsteps, ph[0], ph[1], ph[2], ph[3], ph[4],
-           ph[5], ph[6]);
+    printf("GMPH %d %d %lld %lld %lld %lld %lld %lld %lld %lld %lld %lld %lld %lld\n", (int)CLUSTER, nsteps, ph[0], ph[1],
+           ph[2], ph[3], ph[4], ph[5], ph[6], ph[7], ph[8], ph[9], ph[10], nre);
 #endif
 }
 
