@@ -424,12 +424,33 @@ constexpr int GF_THREADS = 128;
 #ifndef GF_EFF32
 #define GF_EFF32 0.8   // DMMA efficiency of a 32x32 tile relative to 64x64 in the stage-time model
 #endif
+#ifndef GF_FLEX
+#define GF_FLEX 1      // flexible streamed tiles for the plain stage GEMMs of the persistent kernel
+#endif
+#ifndef GF_FLEX_FIXED
+#define GF_FLEX_FIXED 1.0   // fixed cost of a tile (epilogue, bookkeeping) in k-tiles
+#endif
+#ifndef GF_FLEX_LDS
+#define GF_FLEX_LDS 0.5     // cost of a fragment load relative to a DMMA
+#endif
+#ifndef GF_FLEX_FLOOR
+#define GF_FLEX_FLOOR 6.0   // shortest useful k-tile (load latency / pipeline depth) in DMMA units
+#endif
+#ifndef GF_FLEX_RED
+#define GF_FLEX_RED 0.25    // cost of one split-K slice element in the reduction pass
+#endif
 using GF = Cfg<64, 64, GF_BK, 2, 2, GF_ST>;   // persistent-kernel tiles
 constexpr int GF_LD = GM_MAX_M + 2;
 constexpr int GF_MAX_GRID = 1024;   // partial-sum buffer capacity (gmres_fused_part_doubles)
 // dynamic shared memory of the fused kernel: GEMM tile buffers + the apply
 // descriptors of up to GM_MAX_M steps
-constexpr size_t GM_SMEM = GF::SMEM + (size_t)3 * (GM_MAX_M + 1) * sizeof(GemmDesc);
+#ifndef GF_FS
+#define GF_FS 2        // pipeline slots of the flexible streamed tiles (3 slots measured 17% slower on C4:
+                       // 2 x 87 KB of shared memory per SM leave 60 KB of L1 for the operands shared by a stage's tiles)
+#endif
+constexpr size_t GF_FLEX_SMEM = (size_t)GF_FS * (GF::A_ELEMS + GF::B_ELEMS) * sizeof(double);
+constexpr size_t GF_TILE_SMEM = GF::SMEM > GF_FLEX_SMEM ? GF::SMEM : GF_FLEX_SMEM;
+constexpr size_t GM_SMEM = GF_TILE_SMEM + (size_t)3 * sizeof(GemmDesc);
 
 // Software grid barrier with one atomic per CTA: the arrival word counts up and
 // the last arriver's increment flips its top bit (CTA 0 adds 0x80000000 -
@@ -481,6 +502,224 @@ struct GmChunkArgs {
   int tag;               // profiling tag (AMEn core index, < TT_MAX_D)
 };
 
+// ---- flexible streamed tiles for the persistent kernel --------------------
+// The stage GEMMs of the C4 local applies have awkward sizes (ranks 132 = 128 +
+// kickrank, 264, R m = 68 / 152 rows) and a short K (132 - 152): fixed 64x64
+// tiles lost 20-45% of their DMMAs to padding, up to 40% of a stage to the last
+// partial round of tiles over the grid, and paid the pipeline prologue and the
+// scattered epilogue once per tile.  Here every warp computes a x b units of
+// 8 x 8 (a, b <= 4, the same for all warps of a stage: 12 compiled shapes), the
+// 4 warps are laid out 2 x 2 or 1 x 4, so a CTA tile is (WM a) x (WN b) units;
+// the shape is chosen per stage by a small cost model (rounds of tiles over the
+// grid x k-tiles x DMMAs and fragment loads of a warp), and a CTA streams
+// through all its (tile, k-tile) pairs in ONE software pipeline: the first
+// k-tile of the next output tile is in flight while the current tile's last
+// k-tile is multiplied and its epilogue is stored.
+struct FlexPlan {
+  int a, b, wm;           // warp tile in units, warps along M (1 or 2; along N: 4 / wm)
+  int tm, tn, splits, kc; // tiles per dimension, K slices, K per slice (multiple of BK)
+};
+struct FlexTile {
+  int m0, n0, z, kbeg, klen, nk;
+};
+__device__ __forceinline__ FlexTile flex_tile(const GemmDesc &g, const FlexPlan &pl, int w) {
+  FlexTile t;
+  const int T = pl.tm * pl.tn;
+  t.z = w / T;
+  const int tt = w - t.z * T;
+  t.m0 = (tt % pl.tm) * (8 * pl.wm * pl.a);
+  t.n0 = (tt / pl.tm) * (8 * (4 / pl.wm) * pl.b);
+  t.kbeg = t.z * pl.kc;
+  const int kend = min(g.K, t.kbeg + pl.kc);
+  t.klen = kend > t.kbeg ? kend - t.kbeg : 0;
+  t.nk = max(1, (t.klen + GF_BK - 1) / GF_BK);   // an empty slice still writes its zeros
+  return t;
+}
+__device__ inline FlexPlan flex_plan(const GemmDesc &g, int G, long long split_elems) {
+  FlexPlan best;
+  best.a = best.b = 4; best.wm = 2;
+  best.tm = best.tn = best.splits = 1;
+  best.kc = GF_BK;
+  if (g.M <= 0 || g.N <= 0) return best;
+  const int Um = (g.M + 7) >> 3, Un = (g.N + 7) >> 3;
+  double bc = -1.0;
+  for (int wm = 2; wm >= 1; --wm)
+    for (int a = 2; a <= 4; ++a)
+      for (int b = (wm == 1 ? 1 : 2); b <= (wm == 1 ? 2 : 4); ++b) {
+        const int wn = 4 / wm;
+        const int tm = (Um + wm * a - 1) / (wm * a), tn = (Un + wn * b - 1) / (wn * b);
+        const long long T = (long long)tm * tn;
+        int sp = 1;
+        if (T * 2 <= G && g.K >= 256) {
+          sp = (int)min((long long)G / T, (long long)min(g.K / 128, GF_MAXSPLIT));
+          while (sp > 1 && (long long)sp * g.M * g.N > split_elems) --sp;
+          if (sp < 1) sp = 1;
+        }
+        const int kt = ((g.K + sp - 1) / sp + GF_BK - 1) / GF_BK;
+        const double rounds = (double)((T * sp + G - 1) / G);
+        const double ktile = a * b + GF_FLEX_LDS * (a + b);
+        double cost = rounds * (kt + GF_FLEX_FIXED) * (ktile > GF_FLEX_FLOOR ? ktile : GF_FLEX_FLOOR);
+        if (sp > 1) cost += (double)g.M * g.N * sp / (G * GF_THREADS) * GF_FLEX_RED;
+        if (bc < 0.0 || cost < bc) {
+          bc = cost;
+          best.a = a; best.b = b; best.wm = wm; best.tm = tm; best.tn = tn; best.splits = sp;
+        }
+      }
+  best.kc = ((g.K + best.splits - 1) / best.splits + GF_BK - 1) / GF_BK * GF_BK;
+  return best;
+}
+
+template <int A, int B>
+__device__ __forceinline__ void flex_mma(double (&acc)[4][4][2], const double *__restrict__ a,
+                                         const double *__restrict__ b, int lane) {
+  constexpr int LD = 64 + PAD;
+#pragma unroll
+  for (int kk = 0; kk < GF_BK; kk += 4) {
+    const int kr = kk + (lane & 3);
+    double af[A], bf[B];
+#pragma unroll
+    for (int i = 0; i < A; ++i) af[i] = a[kr * LD + i * 8];
+#pragma unroll
+    for (int j = 0; j < B; ++j) bf[j] = b[kr * LD + j * 8];
+#pragma unroll
+    for (int i = 0; i < A; ++i)
+#pragma unroll
+      for (int j = 0; j < B; ++j) dmma(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+  }
+}
+
+// All tiles of one GEMM owned by this CTA (work items blockIdx.x, + G, ...).
+__device__ __forceinline__ void flex_gemm(const GemmDesc &g, const FlexPlan &pl, double *__restrict__ split, int G,
+                                          double *smem) {
+  using C = Cfg<64, 64, GF_BK, 2, 2, 2>;
+  double *sA = smem;
+  double *sB = smem + GF_FS * C::A_ELEMS;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int W = pl.tm * pl.tn * pl.splits;
+  int wl = blockIdx.x;                 // item being loaded
+  if (wl >= W) return;
+  const int tileM = 8 * pl.wm * pl.a, tileN = 8 * (4 / pl.wm) * pl.b;
+  const int wm = (warp % pl.wm) * 8 * pl.a, wn = (warp / pl.wm) * 8 * pl.b;
+  const int code = pl.a * 4 + pl.b;
+  OpLoader<64, GF_BK, C::THREADS> la, lb;
+  FlexTile tl = flex_tile(g, pl, wl);
+  int ktl = 0;
+  auto init_loaders = [&](const FlexTile &t) {
+    const double *A = g.transA ? g.A + t.kbeg : g.A + (long long)t.kbeg * g.lda;
+    const double *B = g.transB ? g.B + (long long)t.kbeg * g.ldb : g.B + t.kbeg;
+    la.init(A, g.lda, g.transA != 0, t.m0, min(g.M, t.m0 + tileM), t.klen, tid);
+    lb.init(B, g.ldb, g.transB == 0, t.n0, min(g.N, t.n0 + tileN), t.klen, tid);
+  };
+  init_loaders(tl);
+  int lslot = 0;                       // ring slot of the next load
+  auto issue_next = [&]() {            // next k-tile of the item being loaded, or the first one of the next item
+    if (wl < W && ktl >= tl.nk) {
+      wl += G;
+      if (wl < W) {
+        tl = flex_tile(g, pl, wl);
+        init_loaders(tl);
+        ktl = 0;
+      }
+    }
+    if (wl < W) {
+      la.load(sA + lslot * C::A_ELEMS, ktl * GF_BK);
+      lb.load(sB + lslot * C::B_ELEMS, ktl * GF_BK);
+      ++ktl;
+      lslot = lslot + 1 == GF_FS ? 0 : lslot + 1;
+    }
+    cp_async_commit();
+  };
+#pragma unroll
+  for (int d = 0; d < GF_FS - 1; ++d) issue_next();
+  int wc = blockIdx.x;                 // item being multiplied
+  FlexTile tc = flex_tile(g, pl, wc);
+  int ktc = 0, slot = 0;
+  double alpha = g.alpha;
+  if (g.alpha_dev) alpha *= *g.alpha_dev;
+  const double beta = g.beta;
+  double acc[4][4][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  while (wc < W) {
+    cp_async_wait<GF_FS - 2>();
+    __syncthreads();
+    issue_next();
+    {
+      const double *a = sA + slot * C::A_ELEMS + wm + (lane >> 2);
+      const double *b = sB + slot * C::B_ELEMS + wn + (lane >> 2);
+      switch (code) {   // uniform over the CTA
+        case 4 * 2 + 1: flex_mma<2, 1>(acc, a, b, lane); break;
+        case 4 * 3 + 1: flex_mma<3, 1>(acc, a, b, lane); break;
+        case 4 * 4 + 1: flex_mma<4, 1>(acc, a, b, lane); break;
+        case 4 * 2 + 2: flex_mma<2, 2>(acc, a, b, lane); break;
+        case 4 * 2 + 3: flex_mma<2, 3>(acc, a, b, lane); break;
+        case 4 * 2 + 4: flex_mma<2, 4>(acc, a, b, lane); break;
+        case 4 * 3 + 2: flex_mma<3, 2>(acc, a, b, lane); break;
+        case 4 * 3 + 3: flex_mma<3, 3>(acc, a, b, lane); break;
+        case 4 * 3 + 4: flex_mma<3, 4>(acc, a, b, lane); break;
+        case 4 * 4 + 2: flex_mma<4, 2>(acc, a, b, lane); break;
+        case 4 * 4 + 3: flex_mma<4, 3>(acc, a, b, lane); break;
+        default: flex_mma<4, 4>(acc, a, b, lane); break;
+      }
+    }
+    ++ktc;
+    slot = slot + 1 == GF_FS ? 0 : slot + 1;
+    if (ktc == tc.nk) {   // epilogue of this output tile (the next tile's first k-tile is in flight)
+      if (pl.splits > 1) {
+        double *P = split + (long long)tc.z * ((long long)g.M * g.N);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int r = tc.m0 + wm + i * 8 + (lane >> 2);
+          if (i >= pl.a || r >= g.M) continue;
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const int c = tc.n0 + wn + j * 8 + (lane & 3) * 2 + h;
+              if (j < pl.b && c < g.N) P[r + (long long)c * g.M] = acc[i][j][h];
+            }
+        }
+      } else {
+        long long coff[4][2];
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int c = tc.n0 + wn + j * 8 + (lane & 3) * 2 + h;
+            coff[j][h] = (j < pl.b && c < g.N) ? (long long)(c % g.dc) * g.s_c0 + (long long)(c / g.dc) * g.s_c1 : -1;
+          }
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int r = tc.m0 + wm + i * 8 + (lane >> 2);
+          if (i >= pl.a || r >= g.M) continue;
+          const long long roff = (long long)(r % g.dr) * g.s_r0 + (long long)(r / g.dr) * g.s_r1;
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              if (coff[j][h] < 0) continue;
+              const long long addr = roff + coff[j][h];
+              double v = alpha * acc[i][j][h];
+              if (beta != 0.0) v += beta * g.C[addr];
+              g.C[addr] = v;
+            }
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+      wc += G;
+      ktc = 0;
+      if (wc < W) tc = flex_tile(g, pl, wc);
+    }
+  }
+  cp_async_wait<0>();
+  __syncthreads();
+}
+
 // Phase barrier: whole cooperative grid (atomics in global memory) or one
 // thread-block cluster (hardware barrier.cluster with release/acquire).
 template <bool CLUSTER>
@@ -504,7 +743,8 @@ __device__ __forceinline__ void phase_sync(unsigned int *bar, unsigned int nbloc
 // barrier is dropped (the next phase reads what this CTA wrote itself).
 template <bool CLUSTER>
 __device__ void gemm_stage(const GemmDesc &g, double *split, long long split_elems, unsigned int *bar, int G,
-                           double *smem, bool gm_count, bool check_skip = true, int own_lo = -1, int own_hi = -1) {
+                           double *smem, bool gm_count, bool check_skip = true, int own_lo = -1, int own_hi = -1,
+                           const FlexPlan *plan = nullptr) {
   if (g.M <= 0 || g.N <= 0) return;
   if (check_skip && g.skip && *g.skip) return;
   const int tid = threadIdx.x;
@@ -535,6 +775,12 @@ __device__ void gemm_stage(const GemmDesc &g, double *split, long long split_ele
     atomicAdd(&g_gemm_counters[1], 1ull);
     if (gm_count) atomicAdd(&g_gm_counters[0], f);
   }
+#if GF_FLEX
+  // uniform: the same model on the same descriptor in every CTA (the persistent kernel plans each stage once)
+  const FlexPlan pl = plan ? *plan : flex_plan(g, G, split_elems);
+  const int splits = pl.splits;
+  flex_gemm(g, pl, split, G, smem);
+#else
   // Tile shape per stage: 64x64 or 32x32 tiles, each with split-K when the output
   // has few tiles, whichever minimises the modelled stage time = rounds of tiles
   // over the G CTAs x padded tile work (the ranks of the C4 local systems, e.g.
@@ -575,6 +821,7 @@ __device__ void gemm_stage(const GemmDesc &g, double *split, long long split_ele
       __syncthreads();
     }
   }
+#endif
   phase_sync<CLUSTER>(bar, G);
   if (splits > 1) {
     const long long total = (long long)g.M * g.N, ps = total;
@@ -727,20 +974,30 @@ __global__ void __launch_bounds__(GF_THREADS, GF_MINB) gm_chunk_kernel(GmChunkAr
 #else
 #define GM_PH(i) do { } while (0)
 #endif
-  // the apply descriptors of every step of this launch, staged once in shared
-  // memory (one parallel load instead of a dependent L2 read per GEMM stage)
-  // full: descriptors of x (index -1) and of every basis vector; else steps j0..j1-1
+  // The three apply descriptors of the CURRENT step live in shared memory; the
+  // next step's are fetched into registers before the barrier that opens the
+  // step and stored after it (the barrier wait hides the L2 latency).  Staging
+  // the descriptors of all <= 41 steps took 18 KB of shared memory per CTA; the
+  // kernel's operands shared by all tiles of a stage (x, A_k) live in L1, and
+  // the shared-memory carve-out of 2 CTAs per SM decides its size.
+  // full: descriptor set 0 = apply to x, set j + 1 = apply to basis vector j.
   const int jend = a.full ? m : min(a.j1, m);
-  const int jbase = a.full ? 0 : a.j0 + 1;   // staged descriptor 3 (j + 1 - jbase) + s
-  GemmDesc *sdesc = reinterpret_cast<GemmDesc *>(smem + GF::SMEM / sizeof(double));
-  {
-    const int nd = 3 * max(jend + 1 - jbase, 0);
-    const long long nw = (long long)nd * sizeof(GemmDesc) / sizeof(long long);
-    const long long *src = reinterpret_cast<const long long *>(a.gapp + 3 * jbase);
-    long long *dst = reinterpret_cast<long long *>(sdesc);
-    for (long long e = threadIdx.x; e < nw; e += GF_THREADS) dst[e] = src[e];
+  GemmDesc *sdesc = reinterpret_cast<GemmDesc *>(smem + GF_TILE_SMEM / sizeof(double));
+  constexpr int DW = 3 * (int)sizeof(GemmDesc) / (int)sizeof(long long);
+  static_assert(DW <= GF_THREADS && sizeof(GemmDesc) % sizeof(long long) == 0, "descriptor staging");
+  auto desc_fetch = [&](int set) -> long long {
+    return threadIdx.x < DW ? reinterpret_cast<const long long *>(a.gapp + 3 * set)[threadIdx.x] : 0ll;
+  };
+  auto desc_store = [&](long long v) {
     __syncthreads();
-  }
+    if (threadIdx.x < DW) reinterpret_cast<long long *>(sdesc)[threadIdx.x] = v;
+    __syncthreads();
+  };
+  desc_store(desc_fetch(a.full ? 0 : a.j0 + 1));
+  // tile plans of the three apply stages (the same shapes at every step of this launch)
+  __shared__ FlexPlan plans[3];
+  if (threadIdx.x < 3) plans[threadIdx.x] = flex_plan(sdesc[threadIdx.x], G, a.split_elems);
+  __syncthreads();
   __shared__ double ys[GF_LD];
   int nsteps = 0;
   const int ncycles = a.full ? a.max_restarts : 1;
@@ -748,8 +1005,10 @@ __global__ void __launch_bounds__(GF_THREADS, GF_MINB) gm_chunk_kernel(GmChunkAr
   int jfirst = a.j0;
   if (a.full) {
     // ---- cycle start: r = b - A x, beta = ||r||, V_0 = r / beta (gm_start_kernel's work)
+    if (cyc > 0) desc_store(desc_fetch(0));
     for (int sidx = 0; sidx < 3; ++sidx)
-      gemm_stage<CLUSTER>(sdesc[sidx], a.split, a.split_elems, a.bar, G, smem, true, false, sidx == 2 ? lo : -1, hi);
+      gemm_stage<CLUSTER>(sdesc[sidx], a.split, a.split_elems, a.bar, G, smem, true, false, sidx == 2 ? lo : -1, hi,
+                          &plans[sidx]);
     double pb = 0.0, pr = 0.0;
     for (int e = lo + tid; e < hi; e += GF_THREADS) {
       const double r = a.b[e] - w[e];
@@ -791,14 +1050,18 @@ __global__ void __launch_bounds__(GF_THREADS, GF_MINB) gm_chunk_kernel(GmChunkAr
   bool nan_stop = false;
   int jlast = jfirst - 1;
   for (int j = jfirst; j < jend; ++j) {
-    if (j > jfirst) phase_sync<CLUSTER>(a.bar, G);            // V[:, j] of the previous step complete
+    {
+      const long long dn = desc_fetch(j + 1);
+      if (j > jfirst) phase_sync<CLUSTER>(a.bar, G);          // V[:, j] of the previous step complete
+      desc_store(dn);
+    }
     GM_PH(0);
     ++nsteps;
     jlast = j;
     // ---- w = A V[:, j] (three chained GEMM stages; the kernel itself stops on the stop word)
     for (int sidx = 0; sidx < 3; ++sidx) {
-      gemm_stage<CLUSTER>(sdesc[3 * (j + 1 - jbase) + sidx], a.split, a.split_elems, a.bar, G, smem, true, false,
-                          sidx == 2 ? lo : -1, hi);
+      gemm_stage<CLUSTER>(sdesc[sidx], a.split, a.split_elems, a.bar, G, smem, true, false,
+                          sidx == 2 ? lo : -1, hi, &plans[sidx]);
 #ifdef GM_PHASE_TIMING
       if (sidx < 2) GM_PH(5 + sidx);
 #endif
