@@ -65,6 +65,23 @@ struct Cfg {
   static constexpr size_t SMEM = (size_t)STAGES * (A_ELEMS + B_ELEMS) * sizeof(double);
 };
 
+// Two-level scatter index idx -> (idx % d) s0 + (idx / d) s1 walked incrementally:
+// one division per thread and tile, then carries (the epilogue's per-row and
+// per-column divisions were 11% of the fused GMRES kernel's stall samples).
+struct ScatIdx {
+  int q, rem, d;
+  __device__ __forceinline__ void init(int idx, int d_) {
+    d = d_ > 0 ? d_ : (1 << 30);
+    q = idx / d;
+    rem = idx - q * d;
+  }
+  __device__ __forceinline__ void advance(int step) {
+    rem += step;
+    while (rem >= d) { rem -= d; ++q; }
+  }
+  __device__ __forceinline__ long long off(long long s0, long long s1) const { return (long long)rem * s0 + (long long)q * s1; }
+};
+
 // Operand tile loader with strength-reduced addressing.  An operand tile is
 // MN x BK (MN = BM rows of A or BN columns of B) staged as smem[k][MN + PAD].
 // Each thread owns NI = MN BK / T elements whose (mn, k) positions inside the
@@ -234,18 +251,23 @@ __device__ __forceinline__ void gemm_tile(const GemmDesc &g0, int m0, int n0, in
   const double beta = g.beta;
   // scatter offsets: one div/mod per owned row and column (not per element)
   long long coff[C::TN][2];
+  ScatIdx ci, ri;
+  ci.init(n0 + wn + (lane & 3) * 2, g.dc);
 #pragma unroll
   for (int j = 0; j < C::TN; ++j)
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const int c = n0 + wn + j * 8 + (lane & 3) * 2 + h;
-      coff[j][h] = (c < g.N) ? (long long)(c % g.dc) * g.s_c0 + (long long)(c / g.dc) * g.s_c1 : -1;
+      coff[j][h] = (c < g.N) ? ci.off(g.s_c0, g.s_c1) : -1;
+      ci.advance(h == 0 ? 1 : 7);
     }
+  ri.init(m0 + wm + (lane >> 2), g.dr);
 #pragma unroll
   for (int i = 0; i < C::TM; ++i) {
     const int r = m0 + wm + i * 8 + (lane >> 2);
+    const long long roff = ri.off(g.s_r0, g.s_r1);
+    ri.advance(8);
     if (r >= g.M) continue;
-    const long long roff = (long long)(r % g.dr) * g.s_r0 + (long long)(r / g.dr) * g.s_r1;
 #pragma unroll
     for (int j = 0; j < C::TN; ++j) {
 #pragma unroll
@@ -683,18 +705,23 @@ __device__ __forceinline__ void flex_gemm(const GemmDesc &g, const FlexPlan &pl,
         }
       } else {
         long long coff[4][2];
+        ScatIdx ci, ri;
+        ci.init(tc.n0 + wn + (lane & 3) * 2, g.dc);
 #pragma unroll
         for (int j = 0; j < 4; ++j)
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
             const int c = tc.n0 + wn + j * 8 + (lane & 3) * 2 + h;
-            coff[j][h] = (j < pl.b && c < g.N) ? (long long)(c % g.dc) * g.s_c0 + (long long)(c / g.dc) * g.s_c1 : -1;
+            coff[j][h] = (j < pl.b && c < g.N) ? ci.off(g.s_c0, g.s_c1) : -1;
+            ci.advance(h == 0 ? 1 : 7);
           }
+        ri.init(tc.m0 + wm + (lane >> 2), g.dr);
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
           const int r = tc.m0 + wm + i * 8 + (lane >> 2);
+          const long long roff = ri.off(g.s_r0, g.s_r1);
+          ri.advance(8);
           if (i >= pl.a || r >= g.M) continue;
-          const long long roff = (long long)(r % g.dr) * g.s_r0 + (long long)(r / g.dr) * g.s_r1;
 #pragma unroll
           for (int j = 0; j < 4; ++j)
 #pragma unroll
@@ -1086,7 +1113,15 @@ __global__ void __launch_bounds__(GF_THREADS, GF_MINB) gm_chunk_kernel(GmChunkAr
     GM_PH(2);
     cross_cta_sum(part1, G, j + 2, h1s);  // fixed order: identical in every CTA
     GM_PH(7);
-    for (int e = lo + tid; e < hi; e += GF_THREADS) w[e] = gs_update(a.V, a.ldv, h1s, j + 1, e, w[e]);
+    // w' = w - V h1 on the own slice, with |w'|^2 accumulated on the way
+    double n1 = 0.0;
+    for (int e = lo + tid; e < hi; e += GF_THREADS) {
+      const double x = gs_update(a.V, a.ldv, h1s, j + 1, e, w[e]);
+      w[e] = x;
+      n1 = fma(x, x, n1);
+    }
+    n1 = warp_sum(n1);
+    if (lane == 0) red[warp] = n1;
     GM_PH(8);
     // DGKS test (Daniel, Gragg, Kaufman & Stewart 1976): a second Gram-Schmidt
     // pass only when the projection removed more than half of |w|^2
@@ -1101,13 +1136,29 @@ __global__ void __launch_bounds__(GF_THREADS, GF_MINB) gm_chunk_kernel(GmChunkAr
     // rotations and g[j] of earlier steps, read before CTA 0 rewrites them in this step
     for (int i = tid; i < j; i += GF_THREADS) { css[i] = st->cs[i]; sns[i] = st->sn[i]; }
     const double gj = st->g[j];
+    __syncthreads();
+    double n1cta = 0.0;
+    for (int q = 0; q < NW; ++q) n1cta += red[q];   // this CTA's share of |w'|^2 (same value in every thread)
+    // With the second pass, |w''|^2 = |w' - V h2|^2 = |w'|^2 - |h2|^2 (V orthonormal), and
+    // h2 is a rounding-level correction (|h2| << |w'|), so the subtraction loses nothing:
+    // |w'|^2 rides along with the pass-2 dots in ONE reduction and the separate norm
+    // reduction + barrier are dropped; the update w'' and the normalisation are then one
+    // pass over the slice.  Guard: if |h2|^2 > |w'|^2 / 100 (never seen; near-breakdown)
+    // the norm is reduced explicitly as in the single-pass case.
+    bool fused_norm = false;
+    double hn2 = 0.0;
     if (reorth) {
-      __syncthreads();
       // ---- pass 2 on the updated slice
       double *my2 = part2 + (size_t)blockIdx.x * GF_LD;
       slice_dots(a.V, a.ldv, w, lo, hi, j + 1, my2);
+      if (tid == 0) my2[j + 1] = n1cta;
       phase_sync<CLUSTER>(a.bar, G);
-      cross_cta_sum(part2, G, j + 1, h2s);
+      cross_cta_sum(part2, G, j + 2, h2s);
+      double hh2 = 0.0;
+      for (int i = 0; i <= j; ++i) hh2 = fma(h2s[i], h2s[i], hh2);
+      const double n1tot = h2s[j + 1];
+      fused_norm = hh2 <= 0.01 * n1tot;
+      hn2 = n1tot - hh2;
 #ifdef GM_PHASE_TIMING
       ++nre;
 #endif
@@ -1116,29 +1167,33 @@ __global__ void __launch_bounds__(GF_THREADS, GF_MINB) gm_chunk_kernel(GmChunkAr
       for (int i = tid; i <= j; i += GF_THREADS) h2s[i] = 0.0;
       __syncthreads();
     }
-    double nrm = 0.0;
-    for (int e = lo + tid; e < hi; e += GF_THREADS) {
-      double x = w[e];
-      if (reorth) {
-        x = gs_update(a.V, a.ldv, h2s, j + 1, e, x);
-        w[e] = x;
+    if (!fused_norm) {
+      double nrm = n1cta;
+      if (reorth) {   // rare: explicit second update and norm
+        nrm = 0.0;
+        for (int e = lo + tid; e < hi; e += GF_THREADS) {
+          const double x = gs_update(a.V, a.ldv, h2s, j + 1, e, w[e]);
+          w[e] = x;
+          nrm = fma(x, x, nrm);
+        }
+        nrm = warp_sum(nrm);
+        __syncthreads();
+        if (lane == 0) red[warp] = nrm;
+        __syncthreads();
+        nrm = 0.0;
+        for (int q = 0; q < NW; ++q) nrm += red[q];
       }
-      nrm = fma(x, x, nrm);
+      if (tid == 0) part3[(size_t)blockIdx.x * GF_LD] = nrm;
+      GM_PH(10);
+      phase_sync<CLUSTER>(a.bar, G);
+      GM_PH(3);
+      __syncthreads();
+      cross_cta_sum(part3, G, 1, red + 2);
+      hn2 = red[2];
     }
-    nrm = warp_sum(nrm);
-    if (lane == 0) red[warp] = nrm;
-    __syncthreads();
-    if (tid == 0) {
-      double t = 0.0;
-      for (int q = 0; q < NW; ++q) t += red[q];
-      part3[(size_t)blockIdx.x * GF_LD] = t;
-    }
-    GM_PH(10);
-    phase_sync<CLUSTER>(a.bar, G);
-    GM_PH(3);
     // ---- norm, Givens (identical in every CTA), normalisation
-    cross_cta_sum(part3, G, 1, red + 2);
-    const double hn = sqrt(red[2]);
+    const double hn = hn2 < 0.0 ? 0.0 : sqrt(hn2);   // (a NaN stays a NaN: the Givens step reports it)
+    __syncthreads();   // red[] is rewritten below
     // H column j: h1 + h2, then the earlier rotations
     if (tid == 0) {
       double col_j = 0.0, col_j1 = hn;
@@ -1186,7 +1241,11 @@ __global__ void __launch_bounds__(GF_THREADS, GF_MINB) gm_chunk_kernel(GmChunkAr
     if (red[1] > 0.0) {
       const double inv = 1.0 / red[1];
       double *vn = a.V + (long long)(j + 1) * a.ldv;
-      for (int e = lo + tid; e < hi; e += GF_THREADS) vn[e] = w[e] * inv;
+      if (fused_norm) {   // w'' = w' - V h2 and its normalisation in one pass
+        for (int e = lo + tid; e < hi; e += GF_THREADS) vn[e] = gs_update(a.V, a.ldv, h2s, j + 1, e, w[e]) * inv;
+      } else {
+        for (int e = lo + tid; e < hi; e += GF_THREADS) vn[e] = w[e] * inv;
+      }
     }
     GM_PH(4);
     if (red[3] != 0.0) nan_stop = true;
