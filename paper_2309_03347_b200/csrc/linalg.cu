@@ -626,105 +626,149 @@ __global__ void __launch_bounds__(1024) jacobi_kernel(const SVDDesc *__restrict_
 }
 
 // ------------------------------------ cluster Jacobi (distributed shared memory) ---
-// The one-sided round-robin Jacobi of jacobi_core spread over a thread-block
-// cluster: column c of W (and of V) lives in the shared memory of CTA c % C at
-// slot c / C; every warp of the cluster takes pairs of a round (warp-global
-// index over the cluster) and reads / rotates its two columns through
-// distributed shared memory (generic pointers from map_shared_rank), and a
-// hardware cluster barrier separates the rounds (the grid version paid a
-// software grid barrier and a global-memory round trip of every block per
-// round).  One cluster per problem (grid = count x C).  Same rotation, test and
-// ordering as jacobi_core, so the same sweep count on the same input.
+// One-sided Jacobi as a systolic array (Brent & Luk 1985) over a thread-block
+// cluster: every warp of the cluster owns the two columns of one pair of the
+// round-robin tournament and keeps them (W part and V part) in REGISTERS; after
+// its rotation it writes the two rotated columns straight into the mailboxes of
+// the warps that own them in the next round (top row moves right, bottom row
+// moves left: distributed shared memory when the neighbour sits in another
+// CTA), one hardware cluster barrier, and every warp reads its own (local)
+// mailbox.  A round is then register arithmetic + one store + one barrier + one
+// local load; the first cluster version kept the columns in place in shared
+// memory and read AND wrote both (mostly remote) columns of a pair every round:
+// two distributed-shared-memory latencies per round, 1.78 us per round at
+// p = 136 against ~1 us now.  Mailboxes are double buffered by round parity.
+// Dummy columns (id < 0) pad the tournament to 2 x (active warps); column
+// identity does not matter for the result (sigma, U, V are sorted at the end).
+// One cluster per problem (grid = count x C).  Same rotation and convergence
+// test as jacobi_core.
 constexpr int JC_MAXC = 16;
-constexpr int JC_R = 10;   // rows per lane held in registers: m, p <= 320
+constexpr int JC_R = 10;   // rows per lane held in registers: m, p <= 320 (instantiated for 5 and 10: the
+                           // C4 bonds, m = p <= 136, need half the registers and instructions)
+template <int JR>
 __global__ void __launch_bounds__(512) jacobi_cluster_kernel(const SVDDesc *__restrict__ descs, int C) {
   namespace cg = cooperative_groups;
   cg::cluster_group cl = cg::this_cluster();
   extern __shared__ __align__(16) double jsm[];
   __shared__ int s_flag;
-  __shared__ double s_sig[2];   // unused placeholder (sigma lives in jsm)
   const int rank = (int)cl.block_rank();
   const SVDDesc g = descs[blockIdx.x / C];
   const int m = g.m, p = g.p, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int NW = blockDim.x >> 5, NWC = NW * C;
-  const int ncl = (p + C - 1) / C;             // local column slots
+  const int NW = blockDim.x >> 5;
   const bool wantv = g.V != nullptr;
-  double *sW = jsm;                            // ncl x m
-  double *sV = sW + (size_t)ncl * m;           // ncl x p
-  double *sig = sV + (wantv ? (size_t)ncl * p : 0);   // p (all sigmas, gathered)
-  int *pos = reinterpret_cast<int *>(sig + p); // p
-  auto colW = [&](int c) -> double * { return cl.map_shared_rank(sW + (size_t)(c / C) * m, c % C); };
-  auto colV = [&](int c) -> double * { return cl.map_shared_rank(sV + (size_t)(c / C) * p, c % C); };
-  // load the local columns of W, V = I
-  for (int e = tid; e < ncl * m; e += blockDim.x) {
-    const int q = e / m, r = e - q * m, c = q * C + rank;
-    sW[e] = c < p ? g.W[r + (long long)c * g.ldw] : 0.0;
-  }
-  if (wantv)
-    for (int e = tid; e < ncl * p; e += blockDim.x) {
-      const int q = e / p, r = e - q * p, c = q * C + rank;
-      sV[e] = (c < p && r == c) ? 1.0 : 0.0;
+  const int pairs = (p + 1) / 2;
+  int nw = (pairs + C - 1) / C;                 // active warps per CTA for this problem
+  nw = nw < 1 ? 1 : (nw > NW ? NW : nw);
+  const int NWT = nw * C, P2 = 2 * NWT;         // players of the tournament (>= p)
+  const int cl_len = m + p;                     // a column: W part then V part
+  // mailbox [parity][warp][slot 0 = top, 1 = bottom][m + p], ids alongside
+  double *mb = jsm;
+  int *mbid = reinterpret_cast<int *>(mb + (size_t)4 * NW * cl_len);   // [parity][warp][slot]
+  double *sig = reinterpret_cast<double *>(mbid + 4 * NW + (4 * NW & 1));   // p
+  int *pos = reinterpret_cast<int *>(sig + p);                           // p
+  auto box = [&](int par, int w, int slot) -> double * { return mb + ((size_t)(par * NW + w) * 2 + slot) * cl_len; };
+  auto boxid = [&](int par, int w, int slot) -> int * { return mbid + (par * NW + w) * 2 + slot; };
+  const bool active = warp < nw;
+  const int gw = rank * nw + warp;              // position of this warp's pair in the systolic row
+  // columns of this warp: top = position gw, bottom = position P2 - 1 - gw
+  double xa[JR], xb[JR], ya[JR], yb[JR];
+  int ida = -1, idb = -1;
+  if (active) {
+    const int ca = gw, cb = P2 - 1 - gw;
+    ida = ca < p ? ca : -1;
+    idb = cb < p ? cb : -1;
+#pragma unroll
+    for (int q = 0; q < JR; ++q) {
+      const int r = lane + 32 * q;
+      xa[q] = (ida >= 0 && r < m) ? g.W[r + (long long)ca * g.ldw] : 0.0;
+      xb[q] = (idb >= 0 && r < m) ? g.W[r + (long long)cb * g.ldw] : 0.0;
+      ya[q] = (wantv && r == ida) ? 1.0 : 0.0;
+      yb[q] = (wantv && r == idb) ? 1.0 : 0.0;
     }
+  }
+  // destinations of the rotation (fixed for the whole run): top -> top of gw + 1 (the last
+  // warp's top turns into its own bottom, warp 0's top stays), bottom -> bottom of gw - 1
+  // (warp 0's bottom becomes the top of warp 1)
+  int dta = gw, dsa = 0, dtb = gw, dsb = 1;     // (warp, slot) for the top and the bottom column
+  if (NWT > 1) {
+    if (gw == 0) { dta = 0; dsa = 0; dtb = 1; dsb = 0; }
+    else {
+      if (gw == NWT - 1) { dta = gw; dsa = 1; } else { dta = gw + 1; dsa = 0; }
+      dtb = gw - 1; dsb = 1;
+    }
+  }
   if (tid == 0) s_flag = 0;
   cl.sync();
-  const int P2 = p + (p & 1);
   const double tol = 4.0 * DBL_EPSILON;
   unsigned long long fl = 0;
-  int sweep = 0;
+  int sweep = 0, par = 0;
   for (; sweep < 60; ++sweep) {
     for (int rnd = 0; rnd < P2 - 1; ++rnd) {
-      for (int pr = rank * NW + warp; pr < P2 / 2; pr += NWC) {
-        int a, b;
-        if (pr == 0) { a = P2 - 1; b = rnd; }
-        else { a = (rnd + pr) % (P2 - 1); b = (rnd - pr + (P2 - 1)) % (P2 - 1); }
-        if (a >= p || b >= p) continue;
-        if (a > b) { int t = a; a = b; b = t; }
-        double *wa = colW(a), *wb = colW(b);
-        double *va = wantv ? colV(a) : nullptr, *vb = wantv ? colV(b) : nullptr;
-        // all four (mostly remote) columns loaded into registers up front: one
-        // distributed-shared-memory latency per pair instead of one per pass
-        double xa[JC_R], xb[JC_R], ya[JC_R], yb[JC_R];
+      if (active) {
+        if (ida >= 0 && idb >= 0) {
+          double al = 0.0, be = 0.0, ga = 0.0;
 #pragma unroll
-        for (int q = 0; q < JC_R; ++q) {
-          const int r = lane + 32 * q;
-          xa[q] = r < m ? wa[r] : 0.0;
-          xb[q] = r < m ? wb[r] : 0.0;
-          ya[q] = (wantv && r < p) ? va[r] : 0.0;
-          yb[q] = (wantv && r < p) ? vb[r] : 0.0;
-        }
-        double al = 0.0, be = 0.0, ga = 0.0;
-#pragma unroll
-        for (int q = 0; q < JC_R; ++q) {
-          al = fma(xa[q], xa[q], al);
-          be = fma(xb[q], xb[q], be);
-          ga = fma(xa[q], xb[q], ga);
-        }
-        al = warp_sum(al);
-        be = warp_sum(be);
-        ga = warp_sum(ga);
-        if (ga == 0.0 || al == 0.0 || be == 0.0) continue;
-        fl += 6ull * m;
-        if (jacobi_orthogonal(al, be, ga, tol)) continue;
-        fl += 6ull * (m + p);
-        const double zeta = (be - al) * __drcp_rn(2.0 * ga);
-        const double tr = __drcp_rn(fabs(zeta) + sqrt(fma(zeta, zeta, 1.0)));
-        const double t = zeta >= 0.0 ? tr : -tr;
-        const double c = rsqrt(fma(t, t, 1.0)), sn = c * t;
-#pragma unroll
-        for (int q = 0; q < JC_R; ++q) {
-          const int r = lane + 32 * q;
-          if (r < m) {
-            wa[r] = c * xa[q] - sn * xb[q];
-            wb[r] = sn * xa[q] + c * xb[q];
+          for (int q = 0; q < JR; ++q) {
+            al = fma(xa[q], xa[q], al);
+            be = fma(xb[q], xb[q], be);
+            ga = fma(xa[q], xb[q], ga);
           }
-          if (wantv && r < p) {
-            va[r] = c * ya[q] - sn * yb[q];
-            vb[r] = sn * ya[q] + c * yb[q];
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) {   // three interleaved butterflies
+            al += __shfl_xor_sync(0xffffffffu, al, o);
+            be += __shfl_xor_sync(0xffffffffu, be, o);
+            ga += __shfl_xor_sync(0xffffffffu, ga, o);
+          }
+          if (ga != 0.0 && al != 0.0 && be != 0.0) {
+            fl += 6ull * m;
+            if (!jacobi_orthogonal(al, be, ga, tol)) {
+              fl += 6ull * (m + p);
+              const double zeta = (be - al) * __drcp_rn(2.0 * ga);
+              const double tr = __drcp_rn(fabs(zeta) + sqrt(fma(zeta, zeta, 1.0)));
+              const double t = zeta >= 0.0 ? tr : -tr;
+              const double c = rsqrt(fma(t, t, 1.0)), sn = c * t;
+#pragma unroll
+              for (int q = 0; q < JR; ++q) {
+                const double x = xa[q], y = xb[q];
+                xa[q] = c * x - sn * y;
+                xb[q] = sn * x + c * y;
+                const double u = ya[q], v = yb[q];
+                ya[q] = c * u - sn * v;
+                yb[q] = sn * u + c * v;
+              }
+              if (lane == 0) s_flag = 1;
+            }
           }
         }
-        if (lane == 0) s_flag = 1;
+        // send both columns to their next owners
+        double *da = cl.map_shared_rank(box(par, dta % nw, dsa), dta / nw);
+        double *db = cl.map_shared_rank(box(par, dtb % nw, dsb), dtb / nw);
+#pragma unroll
+        for (int q = 0; q < JR; ++q) {
+          const int r = lane + 32 * q;
+          if (r < m) { da[r] = xa[q]; db[r] = xb[q]; }
+          if (wantv && r < p) { da[m + r] = ya[q]; db[m + r] = yb[q]; }
+        }
+        if (lane == 0) {
+          *cl.map_shared_rank(boxid(par, dta % nw, dsa), dta / nw) = ida;
+          *cl.map_shared_rank(boxid(par, dtb % nw, dsb), dtb / nw) = idb;
+        }
       }
       cl.sync();
+      if (active) {
+        const double *ra = box(par, warp, 0), *rb = box(par, warp, 1);
+        ida = *boxid(par, warp, 0);
+        idb = *boxid(par, warp, 1);
+#pragma unroll
+        for (int q = 0; q < JR; ++q) {
+          const int r = lane + 32 * q;
+          xa[q] = r < m ? ra[r] : 0.0;
+          xb[q] = r < m ? rb[r] : 0.0;
+          ya[q] = (wantv && r < p) ? ra[m + r] : 0.0;
+          yb[q] = (wantv && r < p) ? rb[m + r] : 0.0;
+        }
+      }
+      par ^= 1;
     }
     // any rotation in the cluster this sweep?
     int any = 0;
@@ -736,20 +780,21 @@ __global__ void __launch_bounds__(512) jacobi_cluster_kernel(const SVDDesc *__re
   }
   if (lane == 0 && fl) atomicAdd(&g_linalg_flops[1], fl);
   if (rank == 0 && tid == 0 && g.sweeps_out) *g.sweeps_out = sweep + 1;
-  // sigma of the local columns, gathered into every CTA, then the rank sort
-  for (int q = warp; q < ncl; q += NW) {
-    const int c = q * C + rank;
-    if (c >= p) continue;
-    const double *w = sW + (size_t)q * m;
-    double sacc = 0.0;
-    for (int r = lane; r < m; r += 32) sacc = fma(w[r], w[r], sacc);
-    sacc = warp_sum(sacc);
-    if (lane == 0) sig[c] = sqrt(sacc);
+  // sigma of this warp's columns, pushed into every CTA's table, then the rank sort
+  cl.sync();
+  if (active) {
+    double sa = 0.0, sb = 0.0;
+#pragma unroll
+    for (int q = 0; q < JR; ++q) { sa = fma(xa[q], xa[q], sa); sb = fma(xb[q], xb[q], sb); }
+    sa = warp_sum(sa);
+    sb = warp_sum(sb);
+    if (lane < C) {
+      double *rs = cl.map_shared_rank(sig, lane);
+      if (ida >= 0) rs[ida] = sqrt(sa);
+      if (idb >= 0) rs[idb] = sqrt(sb);
+    }
   }
   cl.sync();
-  for (int c = tid; c < p; c += blockDim.x)
-    if (c % C != rank) sig[c] = *cl.map_shared_rank(sig + c, c % C);
-  cl.sync();   // remote reads done before any CTA exits
   for (int i = tid; i < p; i += blockDim.x) {
     const double si = sig[i];
     int ps = 0;
@@ -760,20 +805,25 @@ __global__ void __launch_bounds__(512) jacobi_cluster_kernel(const SVDDesc *__re
     pos[i] = ps;
   }
   __syncthreads();
-  for (int e = tid; e < ncl * m; e += blockDim.x) {
-    const int q = e / m, r = e - q * m, c = q * C + rank;
-    if (c >= p) continue;
-    const double sc = sig[c];
-    g.U[r + (long long)pos[c] * g.ldu] = sc > 0.0 ? sW[e] / sc : 0.0;
-  }
-  if (wantv)
-    for (int e = tid; e < ncl * p; e += blockDim.x) {
-      const int q = e / p, r = e - q * p, c = q * C + rank;
-      if (c < p) g.V[r + (long long)pos[c] * g.ldv] = sV[e];
+  if (active) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int id = h == 0 ? ida : idb;
+      if (id < 0) continue;
+      const double sc = sig[id];
+      const double inv = sc > 0.0 ? 1.0 / sc : 0.0;
+      const long long cu = (long long)pos[id] * g.ldu, cv = (long long)pos[id] * g.ldv;
+#pragma unroll
+      for (int q = 0; q < JR; ++q) {
+        const int r = lane + 32 * q;
+        const double x = h == 0 ? xa[q] : xb[q];
+        if (r < m) g.U[r + cu] = sc > 0.0 ? x * inv : 0.0;
+        if (wantv && r < p) g.V[r + cv] = h == 0 ? ya[q] : yb[q];
+      }
     }
+  }
   if (rank == 0)
     for (int c = tid; c < p; c += blockDim.x) g.sigma[pos[c]] = sig[c];
-  (void)s_sig;
 }
 
 // ------------------------------------------- block Jacobi across a grid ---
@@ -1000,17 +1050,21 @@ static size_t svd_smem_bytes(int mcap, int pcap, bool wantv) {
 static bool cluster_jacobi(const SVDDesc *descs_dev, int count, int mcap, int pcap, size_t limit, cudaStream_t s) {
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(jacobi_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)limit);
-    cudaFuncSetAttribute(jacobi_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaFuncSetAttribute(jacobi_cluster_kernel<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)limit);
+    cudaFuncSetAttribute(jacobi_cluster_kernel<5>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaFuncSetAttribute(jacobi_cluster_kernel<JC_R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)limit);
+    cudaFuncSetAttribute(jacobi_cluster_kernel<JC_R>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     attr = true;
   }
   if (mcap > 32 * JC_R || pcap > 32 * JC_R) return false;
   const int pairs = (pcap + 1) / 2;
   for (int C = 2; C <= JC_MAXC; C *= 2) {
-    const long long ncl = (pcap + C - 1) / C;
-    const size_t smem = (size_t)ncl * (mcap + pcap) * sizeof(double) + (size_t)pcap * (sizeof(double) + sizeof(int));
-    const int warps = (pairs + C - 1) / C;
-    if (smem > limit || warps > 16) continue;   // <= 512 threads: 72 registers fit
+    int warps = (pairs + C - 1) / C;
+    warps = warps < 2 ? 2 : warps;
+    // mailboxes [2 parities][warps][2 slots][m + p], their ids, sigma and the sort positions
+    const size_t smem = (size_t)4 * warps * (mcap + pcap) * sizeof(double) + (size_t)(4 * warps + 2) * sizeof(int) +
+                        (size_t)pcap * (sizeof(double) + sizeof(int)) + 16;
+    if (smem > limit || warps > 16) continue;   // <= 512 threads
     const int threads = 32 * (warps < 2 ? 2 : warps);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(count * C);
@@ -1024,7 +1078,10 @@ static bool cluster_jacobi(const SVDDesc *descs_dev, int count, int mcap, int pc
     at[0].val.clusterDim.z = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    if (cudaLaunchKernelEx(&cfg, jacobi_cluster_kernel, descs_dev, C) == cudaSuccess) return true;
+    const bool small = mcap <= 160 && pcap <= 160;
+    if ((small ? cudaLaunchKernelEx(&cfg, jacobi_cluster_kernel<5>, descs_dev, C)
+               : cudaLaunchKernelEx(&cfg, jacobi_cluster_kernel<JC_R>, descs_dev, C)) == cudaSuccess)
+      return true;
     cudaGetLastError();
   }
   return false;
