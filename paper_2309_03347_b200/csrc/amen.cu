@@ -184,10 +184,11 @@ __global__ void track_dx_kernel(const int *Nptr, const double *sol, const double
   __shared__ double r1[32], r2[32];
   const int N = *Nptr;
   double a = 0.0, b = 0.0;
+#pragma unroll 4
   for (int i = threadIdx.x; i < N; i += blockDim.x) {
-    const double d = sol[i] - xold[i];
+    const double sv = sol[i], d = sv - xold[i];
     a = fma(d, d, a);
-    b = fma(sol[i], sol[i], b);
+    b = fma(sv, sv, b);
   }
   for (int o = 16; o > 0; o >>= 1) {
     a += __shfl_xor_sync(0xffffffffu, a, o);
@@ -754,7 +755,7 @@ tt_status amen_solve_meta(const MatMeta &A, const VecMeta &b, const VecMeta &x, 
       }
       TT_TRY(run_captured(key2, s, [&]() -> tt_status {
       track_res_kernel<<<1, 1, 0, s>>>(P.gst, D.dv, status_dev);
-      track_dx_kernel<<<1, 256, 0, s>>>(D.iv, D.sol, D.xold, D.dv);
+      track_dx_kernel<<<1, 1024, 0, s>>>(D.iv, D.sol, D.xold, D.dv);
       if (last) {
         TT_TRY(launch_copy(D.cd + 1, 1, P.Ncap, s));
         return TT_OK;
@@ -1083,7 +1084,7 @@ tt_status amen_mv_meta(const MatMeta &A, const VecMeta &b, const VecMeta &y, con
       plan_local_mv<<<1, 1, 0, s>>>(D, k);
       TT_TRY(launch_copy(D.cd + 2, 1, P.Ncap, s));
       TT_TRY(launch_caps(D.gd, lc, 0, 3));
-      track_dx_kernel<<<1, 256, 0, s>>>(D.iv, D.sol, D.xold, D.dv);
+      track_dx_kernel<<<1, 1024, 0, s>>>(D.iv, D.sol, D.xold, D.dv);
       if (last) {
         TT_TRY(launch_copy(D.cd + 1, 1, P.Ncap, s));
         continue;

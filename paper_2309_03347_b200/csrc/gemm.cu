@@ -455,8 +455,8 @@ constexpr int GF_THREADS = 128;
 #ifndef GF_FLEX_LDS
 #define GF_FLEX_LDS 0.5     // cost of a fragment load relative to a DMMA
 #endif
-#ifndef GF_FLEX_FLOOR
-#define GF_FLEX_FLOOR 6.0   // shortest useful k-tile (load latency / pipeline depth) in DMMA units
+#ifndef GF_FLEX_KT0
+#define GF_FLEX_KT0 4.0     // per-k-tile overhead of a warp (barrier, cp.async issue) in DMMA units
 #endif
 #ifndef GF_FLEX_RED
 #define GF_FLEX_RED 0.25    // cost of one split-K slice element in the reduction pass
@@ -579,8 +579,8 @@ __device__ inline FlexPlan flex_plan(const GemmDesc &g, int G, long long split_e
         }
         const int kt = ((g.K + sp - 1) / sp + GF_BK - 1) / GF_BK;
         const double rounds = (double)((T * sp + G - 1) / G);
-        const double ktile = a * b + GF_FLEX_LDS * (a + b);
-        double cost = rounds * (kt + GF_FLEX_FIXED) * (ktile > GF_FLEX_FLOOR ? ktile : GF_FLEX_FLOOR);
+        const double ktile = a * b + GF_FLEX_LDS * (a + b) + GF_FLEX_KT0;
+        double cost = rounds * (kt + GF_FLEX_FIXED) * ktile;
         if (sp > 1) cost += (double)g.M * g.N * sp / (G * GF_THREADS) * GF_FLEX_RED;
         if (bc < 0.0 || cost < bc) {
           bc = cost;
