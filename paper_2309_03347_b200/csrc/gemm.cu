@@ -617,9 +617,19 @@ __device__ __forceinline__ void flex_gemm(const GemmDesc &g, const FlexPlan &pl,
   double *sA = smem;
   double *sB = smem + GF_FS * C::A_ELEMS;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int W = pl.tm * pl.tn * pl.splits;
-  int wl = blockIdx.x;                 // item being loaded
+  // This CTA's items: a contiguous range of the (m-tile fastest) item order, so its
+  // successive tiles share their B columns (and split-K slice): the second operand of
+  // a tile is then an L1 hit instead of another L2 read (cp.async.ca; the operand
+  // traffic of a stage was ~2.6 TB/s out of L2 with items dealt out round-robin).
+  const int Wtot = pl.tm * pl.tn * pl.splits;
+  int wl, W;                           // item being loaded, end of the range
+  {
+    const int q = Wtot / G, rem = Wtot - q * G, c = blockIdx.x;
+    wl = c * q + min(c, rem);
+    W = wl + q + (c < rem ? 1 : 0);
+  }
   if (wl >= W) return;
+  const int wfirst = wl;
   const int tileM = 8 * pl.wm * pl.a, tileN = 8 * (4 / pl.wm) * pl.b;
   const int wm = (warp % pl.wm) * 8 * pl.a, wn = (warp / pl.wm) * 8 * pl.b;
   const int code = pl.a * 4 + pl.b;
@@ -636,7 +646,7 @@ __device__ __forceinline__ void flex_gemm(const GemmDesc &g, const FlexPlan &pl,
   int lslot = 0;                       // ring slot of the next load
   auto issue_next = [&]() {            // next k-tile of the item being loaded, or the first one of the next item
     if (wl < W && ktl >= tl.nk) {
-      wl += G;
+      wl += 1;
       if (wl < W) {
         tl = flex_tile(g, pl, wl);
         init_loaders(tl);
@@ -653,7 +663,7 @@ __device__ __forceinline__ void flex_gemm(const GemmDesc &g, const FlexPlan &pl,
   };
 #pragma unroll
   for (int d = 0; d < GF_FS - 1; ++d) issue_next();
-  int wc = blockIdx.x;                 // item being multiplied
+  int wc = wfirst;                     // item being multiplied
   FlexTile tc = flex_tile(g, pl, wc);
   int ktc = 0, slot = 0;
   double alpha = g.alpha;
@@ -738,7 +748,7 @@ __device__ __forceinline__ void flex_gemm(const GemmDesc &g, const FlexPlan &pl,
       for (int i = 0; i < 4; ++i)
 #pragma unroll
         for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-      wc += G;
+      wc += 1;
       ktc = 0;
       if (wc < W) tc = flex_tile(g, pl, wc);
     }
