@@ -558,7 +558,7 @@ static tt_status carve_amen(const MatMeta &A, const VecMeta &b, const VecMeta &x
   P.h1 = ar.take<double>(m + 1);
   P.h2 = ar.take<double>(m + 1);
   P.gpart = ar.take<double>(gmres_fused_part_doubles(1024));
-  P.gbar = ar.take<unsigned int>(4);
+  P.gbar = ar.take<unsigned int>(GM_BAR_WORDS + 2);
   // orthogonalisation scratch (x or z)
   Arena c1, c2;
   orth_meta(x, -1, nullptr, c1, nullptr);

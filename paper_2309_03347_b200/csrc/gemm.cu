@@ -938,6 +938,41 @@ __device__ __forceinline__ double gs_update(const double *V, long long ldv, cons
   }
   return x;
 }
+// Two-level cross-CTA sum, first level: the CTAs form groups of GF_GRP; each CTA
+// publishes its partial row and takes a ticket of its group's counter; the last
+// arriver sums the group's rows in CTA order (the same bits whoever is last) into
+// the group's row of gpart.  After the grid barrier every CTA sums the ~19 group
+// rows instead of all 296 CTA rows: each CTA reading every other CTA's row was
+// 29 MB of L2 reads per reduction (4.3 us, twice per Arnoldi step).  The counters
+// only ever grow by the group size per reduction, and a grid barrier separates
+// successive reductions, so "ticket + 1 divisible by the group size" marks the last.
+constexpr int GF_GRP = 16;
+__device__ __forceinline__ void group_reduce(const double *part, double *gpart, unsigned int *cnt, int G, int n,
+                                             int *s_last) {
+  const int grp = blockIdx.x / GF_GRP, c0 = grp * GF_GRP;
+  const int gsize = min(GF_GRP, G - c0);
+  __syncthreads();   // this CTA's row is complete
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const unsigned int t = atomicAdd(cnt + grp, 1u);
+    const int last = ((t + 1u) % (unsigned int)gsize) == 0u;
+    if (last) __threadfence();
+    *s_last = last;
+  }
+  __syncthreads();
+  if (*s_last) {
+    for (int i = threadIdx.x; i < n; i += GF_THREADS) {
+      double v[GF_GRP];
+#pragma unroll
+      for (int c = 0; c < GF_GRP; ++c) v[c] = c < gsize ? __ldcg(part + (size_t)(c0 + c) * GF_LD + i) : 0.0;
+      double sacc = 0.0;
+#pragma unroll
+      for (int c = 0; c < GF_GRP; ++c) sacc += v[c];
+      gpart[(size_t)grp * GF_LD + i] = sacc;
+    }
+  }
+}
+
 __device__ __forceinline__ void cross_cta_sum(const double *part, int G, int n, double *out) {
   // out[i] = sum_c part[c * GF_LD + i] for i < n
   // lanes over the CTAs (fixed order: the same bits in every CTA), each warp a group
@@ -1002,6 +1037,12 @@ __global__ void __launch_bounds__(GF_THREADS, GF_MINB) gm_chunk_kernel(GmChunkAr
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   constexpr int NW = GF_THREADS / 32;
   double *part1 = a.part, *part2 = a.part + (size_t)G * GF_LD, *part3 = a.part + 2 * (size_t)G * GF_LD;
+  // two-level sums on the big grid: group rows behind the three CTA-row tables
+  double *gpart1 = a.part + 3 * (size_t)G * GF_LD, *gpart2 = gpart1 + (size_t)GM_GROUPS_MAX * GF_LD;
+  unsigned int *gcnt = a.bar + 2;
+  const bool two_level = !CLUSTER && G >= 4 * GF_GRP;
+  const int NG = (G + GF_GRP - 1) / GF_GRP;
+  __shared__ int s_last;
   double *w = a.w;
 #ifdef GM_PHASE_TIMING
   long long ph[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
@@ -1119,9 +1160,12 @@ __global__ void __launch_bounds__(GF_THREADS, GF_MINB) gm_chunk_kernel(GmChunkAr
         my1[j + 1] = t;
       }
     }
+    if (two_level) group_reduce(part1, gpart1, gcnt, G, j + 2, &s_last);
     phase_sync<CLUSTER>(a.bar, G);
     GM_PH(2);
-    cross_cta_sum(part1, G, j + 2, h1s);  // fixed order: identical in every CTA
+    // fixed order: identical in every CTA
+    if (two_level) cross_cta_sum(gpart1, NG, j + 2, h1s);
+    else cross_cta_sum(part1, G, j + 2, h1s);
     GM_PH(7);
     // w' = w - V h1 on the own slice, with |w'|^2 accumulated on the way
     double n1 = 0.0;
@@ -1162,8 +1206,10 @@ __global__ void __launch_bounds__(GF_THREADS, GF_MINB) gm_chunk_kernel(GmChunkAr
       double *my2 = part2 + (size_t)blockIdx.x * GF_LD;
       slice_dots(a.V, a.ldv, w, lo, hi, j + 1, my2);
       if (tid == 0) my2[j + 1] = n1cta;
+      if (two_level) group_reduce(part2, gpart2, gcnt, G, j + 2, &s_last);
       phase_sync<CLUSTER>(a.bar, G);
-      cross_cta_sum(part2, G, j + 2, h2s);
+      if (two_level) cross_cta_sum(gpart2, NG, j + 2, h2s);
+      else cross_cta_sum(part2, G, j + 2, h2s);
       double hh2 = 0.0;
       for (int i = 0; i <= j; ++i) hh2 = fma(h2s[i], h2s[i], hh2);
       const double n1tot = h2s[j + 1];
@@ -1328,7 +1374,7 @@ void gemm_counters(unsigned long long *out, int reset) {
 
 namespace tt {
 
-size_t gmres_fused_part_doubles(int G) { return (size_t)3 * G * GF_LD; }
+size_t gmres_fused_part_doubles(int G) { return (size_t)(3 * G + 2 * GM_GROUPS_MAX) * GF_LD; }
 
 int gmres_fused_grid() {
   static int G = 0;

@@ -35,7 +35,7 @@ tt_status gmres_solve(const GmresCtx &c, cudaStream_t s) {
   TT_TRY(check_launch("gm_init"));
   if (!(c.gapp && c.part && c.bar && gmres_fused_grid() > 0))
     return fail(TT_ERR_CUDA, "gmres: the fused solve kernel is unavailable (not co-resident)");
-  cudaMemsetAsync(c.bar, 0, 2 * sizeof(unsigned int), s);
+  cudaMemsetAsync(c.bar, 0, GM_BAR_WORDS * sizeof(unsigned int), s);
   const int decide = c.cluster == 2;
   if (c.cluster != 0)
     TT_TRY(launch_gmres_chunk(c.st, c.gapp, c.V, c.ldv, c.w, c.part, c.split, c.split_elems, c.bar, 0, c.m, s, 1,

@@ -5,6 +5,10 @@
 namespace tt {
 
 constexpr int GM_MAX_M = 128;
+// grid-barrier word (+1 spare) followed by the arrival counters of the CTA groups of the
+// fused kernel's two-level cross-CTA sums; zeroed by gmres_solve
+constexpr int GM_GROUPS_MAX = 64;
+constexpr int GM_BAR_WORDS = 2 + GM_GROUPS_MAX;
 
 struct GmState {
   int N, m, converged, stop, cycle, nan, j, jdone;
@@ -29,7 +33,7 @@ struct GmresCtx {
   // basis vector j are gapp[3(j+1) .. 3(j+1)+2]; NULL = one launch per operation
   const GemmDesc *gapp = nullptr;
   double *part = nullptr;        // gmres_fused_part_doubles(grid) doubles
-  unsigned int *bar = nullptr;   // [2] grid barrier words (zeroed by gmres_solve)
+  unsigned int *bar = nullptr;   // [GM_BAR_WORDS] grid barrier word + group counters (zeroed by gmres_solve)
   double *split = nullptr;       // split-K scratch
   long long split_elems = 0;
   int dense_max = 0;             // local systems with N <= dense_max go to the dense solver
