@@ -789,18 +789,20 @@ def e2e_keff(tb, ops, psi, z, state, opts, ws, steps):
 
 def extras(args, tb, device, world):
     """The metric's first half on its own configs, in the same run: C5 (configs[4])
-    ALS double sweep at r = 256 (GFLOP/s, % of the FP64 DMMA peak) and the C2
+    ALS double sweep at r = 256, 128, 64 (GFLOP/s, % of the FP64 DMMA peak) and the C2
     (configs[1]) 64-instance batched tt_matvec (GB/s, % of the measured HBM
     copy bandwidth)."""
     import copy
     out = {}
     a = copy.copy(args)
-    a.workload, a.rank, a.no_graph, a.one_stream = "c5", 256, False, False
+    a.workload, a.no_graph, a.one_stream = "c5", False, False
     a.steps, a.warmup = max(5, min(args.steps, 10)), 3
-    l5 = micro_bench(a, tb, device, world, None)
-    out["c5_r256"] = {"value": l5["value"], "unit": l5["unit"], "pct_dmma_peak": l5["pct_dmma_peak"],
-                      "ms_per_sweep": l5["ms_per_step"], "flops_per_sweep": l5["flops_per_step"],
-                      "config": l5["config"]["workload"], "gpu_launches": l5["gpu_launches"]}
+    for r in (256, 128, 64):   # configs[4] names all three interface ranks
+        a.rank = r
+        l5 = micro_bench(a, tb, device, world, None)
+        out[f"c5_r{r}"] = {"value": l5["value"], "unit": l5["unit"], "pct_dmma_peak": l5["pct_dmma_peak"],
+                           "ms_per_sweep": l5["ms_per_step"], "flops_per_sweep": l5["flops_per_step"],
+                           "config": l5["config"]["workload"], "gpu_launches": l5["gpu_launches"]}
     a.workload, a.steps = "c2", max(5, min(args.steps, 10))
     l2 = micro_bench(a, tb, device, world, None)
     rf = l2["roofline"]

@@ -1009,7 +1009,10 @@ __device__ __forceinline__ void cross_cta_sum(const double *part, int G, int n, 
 
 template <bool CLUSTER>
 #ifndef GF_MINB
-#define GF_MINB 1
+#define GF_MINB 3   // 168 registers, 3 CTAs per SM (444 CTAs): C4 fused time -4% against 2 per SM after the
+                    // round-2 loader and tile work (the GEMM stages hide more latency; the barrier-bound
+                    // core 8 loses 8%); 4 per SM (128 registers) is 20% slower; round 2 began at 1 -> 254
+                    // registers, 2 per SM
 #endif
 __global__ void __launch_bounds__(GF_THREADS, GF_MINB) gm_chunk_kernel(GmChunkArgs a) {
   extern __shared__ __align__(16) double smem[];
@@ -1389,9 +1392,8 @@ int gmres_fused_grid() {
     const char *e = std::getenv("TT_GF_GRID");
     // two CTAs per SM when they fit (more bytes in flight for the CGS2 phases of
     // large local systems; measured +4% on C4)
-    // all SMs equally loaded: 2 CTAs on each of the 148 SMs (296), not 256 (which
-    // left 40 SMs with one CTA and made the tile rounds uneven)
-    G = (occ >= 1) ? (e ? std::atoi(e) : (occ >= 2 ? 2 * sms : sms)) : -1;
+    // all SMs equally loaded: the same number of CTAs (up to 3) on each of the 148 SMs
+    G = (occ >= 1) ? (e ? std::atoi(e) : (occ >= 3 ? 3 : occ) * sms) : -1;
     if (G > occ * sms || G > GF_MAX_GRID) G = occ * sms < GF_MAX_GRID ? occ * sms : GF_MAX_GRID;
   }
   return G;
