@@ -498,6 +498,32 @@ __device__ __forceinline__ void gbar(unsigned int *bar, unsigned int nblocks) {
   __syncthreads();
 }
 
+// The same barrier split into arrival and wait, so work that nobody else waits
+// for (the Givens update of an Arnoldi step) overlaps the barrier's latency.
+// The token is meaningful in thread 0 only.
+__device__ __forceinline__ unsigned int gbar_arrive(unsigned int *bar, unsigned int nblocks) {
+  __syncthreads();
+  unsigned int old = 0;
+  if (threadIdx.x == 0) {
+    const unsigned int inc = blockIdx.x == 0 ? 0x80000000u - (nblocks - 1) : 1u;
+    __threadfence();
+    old = atomicAdd(bar, inc);
+  }
+  return old;
+}
+__device__ __forceinline__ void gbar_wait(unsigned int *bar, unsigned int old) {
+  if (threadIdx.x == 0) {
+    volatile unsigned int *w = bar;
+    unsigned int spins = 0;
+    const long long t0 = clock64();
+    while (((old ^ *w) & 0x80000000u) == 0) {
+      if ((++spins & 1023u) == 0 && clock64() - t0 > 8000000000LL) __trap();   // never hang the device
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -759,6 +785,22 @@ __device__ __forceinline__ void flex_gemm(const GemmDesc &g, const FlexPlan &pl,
 
 // Phase barrier: whole cooperative grid (atomics in global memory) or one
 // thread-block cluster (hardware barrier.cluster with release/acquire).
+template <bool CLUSTER>
+__device__ __forceinline__ unsigned int phase_arrive(unsigned int *bar, unsigned int nblocks) {
+  if (CLUSTER) {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
+    return 0;
+  }
+  return gbar_arrive(bar, nblocks);
+}
+template <bool CLUSTER>
+__device__ __forceinline__ void phase_wait(unsigned int *bar, unsigned int token) {
+  if (CLUSTER) {
+    asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+  } else {
+    gbar_wait(bar, token);
+  }
+}
 template <bool CLUSTER>
 __device__ __forceinline__ void phase_sync(unsigned int *bar, unsigned int nblocks) {
   if (CLUSTER) {
@@ -1131,11 +1173,9 @@ __global__ void __launch_bounds__(GF_THREADS, GF_MINB) gm_chunk_kernel(GmChunkAr
   bool nan_stop = false;
   int jlast = jfirst - 1;
   for (int j = jfirst; j < jend; ++j) {
-    {
-      const long long dn = desc_fetch(j + 1);
-      if (j > jfirst) phase_sync<CLUSTER>(a.bar, G);          // V[:, j] of the previous step complete
-      desc_store(dn);
-    }
+    // (V[:, j] is complete: the previous step ended with a barrier; its descriptors were
+    // stored there too)
+    if (j == jfirst) desc_store(desc_fetch(j + 1));
     GM_PH(0);
     ++nsteps;
     jlast = j;
@@ -1250,9 +1290,21 @@ __global__ void __launch_bounds__(GF_THREADS, GF_MINB) gm_chunk_kernel(GmChunkAr
       cross_cta_sum(part3, G, 1, red + 2);
       hn2 = red[2];
     }
-    // ---- norm, Givens (identical in every CTA), normalisation
+    // ---- norm, normalisation, then the barrier that publishes V[:, j+1] with the
+    //      Givens update (identical in every CTA, nobody waits for it) between the
+    //      barrier's arrival and its wait
     const double hn = hn2 < 0.0 ? 0.0 : sqrt(hn2);   // (a NaN stays a NaN: the Givens step reports it)
-    __syncthreads();   // red[] is rewritten below
+    if (hn > 0.0) {
+      const double inv = 1.0 / hn;
+      double *vn = a.V + (long long)(j + 1) * a.ldv;
+      if (fused_norm) {   // w'' = w' - V h2 and its normalisation in one pass
+        for (int e = lo + tid; e < hi; e += GF_THREADS) vn[e] = gs_update(a.V, a.ldv, h2s, j + 1, e, w[e]) * inv;
+      } else {
+        for (int e = lo + tid; e < hi; e += GF_THREADS) vn[e] = w[e] * inv;
+      }
+    }
+    const long long dnext = j + 1 < jend ? desc_fetch(j + 2) : 0ll;
+    const unsigned int token = phase_arrive<CLUSTER>(a.bar, G);
     // H column j: h1 + h2, then the earlier rotations
     if (tid == 0) {
       double col_j = 0.0, col_j1 = hn;
@@ -1285,30 +1337,20 @@ __global__ void __launch_bounds__(GF_THREADS, GF_MINB) gm_chunk_kernel(GmChunkAr
         st->res = rel;
         if (stop == 2) st->nan = 1;
         st->stop = stop ? 1 : 0;
+        atomicAdd(&g_gm_counters[1], (unsigned long long)N * ((reorth ? 8ull : 4ull) * (j + 1) + 5ull));
+        atomicAdd(&g_gm_counters[2], 1ull);
+        atomicAdd(&g_gm_tag_steps[a.tag], 1ull);
       }
       red[0] = stop ? 1.0 : 0.0;
-      red[1] = hn;
       red[3] = (stop == 2) ? 1.0 : 0.0;
     }
-    __syncthreads();
+    __syncthreads();   // red[] of the Givens step (the cluster barrier's wait does not order it)
+    phase_wait<CLUSTER>(a.bar, token);
     const bool stop = red[0] != 0.0;
-    if (blockIdx.x == 0 && tid == 0) {
-      atomicAdd(&g_gm_counters[1], (unsigned long long)N * ((reorth ? 8ull : 4ull) * (j + 1) + 5ull));
-      atomicAdd(&g_gm_counters[2], 1ull);
-      atomicAdd(&g_gm_tag_steps[a.tag], 1ull);
-    }
-    if (red[1] > 0.0) {
-      const double inv = 1.0 / red[1];
-      double *vn = a.V + (long long)(j + 1) * a.ldv;
-      if (fused_norm) {   // w'' = w' - V h2 and its normalisation in one pass
-        for (int e = lo + tid; e < hi; e += GF_THREADS) vn[e] = gs_update(a.V, a.ldv, h2s, j + 1, e, w[e]) * inv;
-      } else {
-        for (int e = lo + tid; e < hi; e += GF_THREADS) vn[e] = w[e] * inv;
-      }
-    }
     GM_PH(4);
     if (red[3] != 0.0) nan_stop = true;
     if (stop) break;
+    if (j + 1 < jend) desc_store(dnext);
   }
   if (!a.full) break;
   // ---- cycle end: x += V y with H y = g (gm_update_kernel's work), restart test
