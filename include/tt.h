@@ -369,9 +369,9 @@ typedef struct {
   int32_t mv_max_sweeps;   /* amen_mv sweep limit (B and the residual products)      */
   int32_t warm;            /* 1: continue a previous call (same operators, options   */
                            /*    and workspace): psi is that call's normalised       */
-                           /*    iterate (not re-rounded), the amen_mv guess of B    */
-                           /*    and the AMEn residual start cores z0 are kept in    */
-                           /*    the workspace, k0 is its k; 0: fresh start           */
+                           /*    iterate (not re-rounded), the amen_mv guess of B,   */
+                           /*    the AMEn residual start cores z0 and f = F^T 1 are  */
+                           /*    kept in the workspace, k0 is its k; 0: fresh start   */
 } keff_opts;
 typedef struct {
   double *k_dev;           /* [1] final k                                          */

@@ -314,11 +314,14 @@ tt_status keff_body(const MatMeta &H, const MatMeta &S, const MatMeta &F, const 
     a.cap = W.sub_cap;
     return a;
   };
-  // f = round(F^T 1)   (reading Z18)
-  transpose_ttm_kernel<<<dim3(64, d), 256, 0, s>>>(F, W.FT);
-  ones_kernel<<<d, 256, 0, s>>>(W.ones);
-  TT_TRY(matvec_meta(W.FT, W.ones, W.f, s));
-  { Arena a = sub(); TT_TRY(round_meta(W.f, 1e-14, 1 << 30, nullptr, nullptr, 0, a, s)); }
+  // f = round(F^T 1)   (reading Z18: built once per solve; a warm call continues a solve
+  // with the same operators, so f is still in the workspace like z0 and the amen_mv guess)
+  if (!o.warm) {
+    transpose_ttm_kernel<<<dim3(64, d), 256, 0, s>>>(F, W.FT);
+    ones_kernel<<<d, 256, 0, s>>>(W.ones);
+    TT_TRY(matvec_meta(W.FT, W.ones, W.f, s));
+    { Arena a = sub(); TT_TRY(round_meta(W.f, 1e-14, 1 << 30, nullptr, nullptr, 0, a, s)); }
+  }
   // keep the AMEn residual TT's initial cores (the oracle restarts every solve from z0);
   // a warm call continues the previous one: z0 and the amen_mv guess of B are
   // still in the workspace and psi is already a rounded, normalised iterate
