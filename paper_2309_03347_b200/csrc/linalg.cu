@@ -204,6 +204,83 @@ __device__ __forceinline__ void apply_block_reflector(int m, int j0, int jb, con
   }
 }
 
+// Register-resident panel for short panels (pr <= 32 MR rows, panel in shared
+// memory): warp w owns panel column w and keeps it in registers (MR doubles per
+// lane) for the whole panel factorisation.  Step jj: warp jj forms reflector jj
+// from its registers and writes the finished column (R above the diagonal, beta,
+// v below) to the panel; one block barrier; every later warp reads v_jj once
+// from shared memory and updates its own registers.  The column-in-shared-memory
+// version moved three columns' worth of shared-memory traffic per updated column
+// and step (read v, read and write the column) and the lookahead warp's dependent
+// loads queued behind it; here a step reads v once per warp and the next owner
+// goes straight from its update to its reflector.
+template <int MR>
+__device__ __forceinline__ void qr_panel_reg(const QRDesc &g, int j0, int jb, int pr, double *sP, double *s_tau) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const bool own = warp < jb;
+  double *mycol = sP + (size_t)warp * pr;
+  double x[MR];
+#pragma unroll
+  for (int q = 0; q < MR; ++q) {
+    const int r = lane + 32 * q;
+    x[q] = (own && r < pr) ? mycol[r] : 0.0;
+  }
+  for (int jj = 0; jj < jb; ++jj) {
+    if (warp == jj) {   // local diagonal row jj < 32: lane jj, q = 0
+      double sigma = 0.0;
+#pragma unroll
+      for (int q = 0; q < MR; ++q)
+        if (lane + 32 * q > jj) sigma = fma(x[q], x[q], sigma);
+      sigma = warp_sum(sigma);
+      const double alpha = __shfl_sync(0xffffffffu, x[0], jj);
+      double tau = 0.0, scal = 0.0, beta = alpha;
+      if (sigma > 0.0 && fma(alpha, alpha, sigma) > 1e-200) {   // tiny-column guard: reading Z41
+        const double ss = fma(alpha, alpha, sigma);
+        const double rs = rsqrt(ss);
+        const double nrm = ss * rs, aa = fabs(alpha);
+        beta = alpha >= 0.0 ? -nrm : nrm;
+        tau = fma(aa, rs, 1.0);
+        const double qv = __drcp_rn(aa + nrm);
+        scal = alpha >= 0.0 ? qv : -qv;
+      }
+      if (tau != 0.0) {
+#pragma unroll
+        for (int q = 0; q < MR; ++q)
+          if (lane + 32 * q > jj) x[q] *= scal;
+      }
+      if (lane == jj) x[0] = beta;
+#pragma unroll
+      for (int q = 0; q < MR; ++q) {
+        const int r = lane + 32 * q;
+        if (r < pr) mycol[r] = x[q];
+      }
+      if (lane == 0) {
+        s_tau[jj & 1] = tau;
+        g.tau[j0 + jj] = tau;
+      }
+    }
+    __syncthreads();
+    const double tau = s_tau[jj & 1];
+    if (own && warp > jj && tau != 0.0) {
+      const double *v = sP + (size_t)jj * pr;
+      double vv[MR];
+#pragma unroll
+      for (int q = 0; q < MR; ++q) {
+        const int r = lane + 32 * q;
+        vv[q] = (r > jj && r < pr) ? v[r] : 0.0;
+      }
+      double d = (lane == jj) ? x[0] : 0.0;   // v_jj[jj] = 1
+#pragma unroll
+      for (int q = 0; q < MR; ++q) d = fma(vv[q], x[q], d);
+      d = warp_sum(d) * tau;
+#pragma unroll
+      for (int q = 0; q < MR; ++q) x[q] = fma(-d, vv[q], x[q]);
+      if (lane == jj) x[0] -= d;
+    }
+  }
+  __syncthreads();
+}
+
 // Panel factorisation of columns j0..j0+jb-1 (rows j0..m-1) and the Gram
 // entries G[l][i] = v_l^T v_i (l < i) of the T factor.  SM: the panel lives in
 // shared memory (sP, leading dimension pr) — a separate instantiation so the
@@ -291,9 +368,12 @@ __device__ __forceinline__ void qr_panel(const QRDesc &g, int m, int j0, int jb,
     }
     __syncwarp();
   };
-  if (warp == 0) form_reflector(j0, 0);
+  constexpr int PANEL_MR = 9;
+  const bool regpanel = SM && pr <= 32 * PANEL_MR;
+  if (regpanel) qr_panel_reg<PANEL_MR>(g, j0, jb, pr, sP, s_tau);
+  if (!regpanel && warp == 0) form_reflector(j0, 0);
   __syncthreads();
-  for (int jj = 0; jj < jb; ++jj) {
+  for (int jj = 0; jj < (regpanel ? 0 : jb); ++jj) {
     const int j = j0 + jj;
     const double *col = colp(j);
     const double tau = s_tau[jj & 1];
