@@ -1138,7 +1138,32 @@ static bool cluster_jacobi(const SVDDesc *descs_dev, int count, int mcap, int pc
   }
   if (mcap > 32 * JC_R || pcap > 32 * JC_R) return false;
   const int pairs = (pcap + 1) / 2;
-  for (int C = 2; C <= JC_MAXC; C *= 2) {
+  // Cluster sizes in order of preference.  One problem (latency): the shortest modelled
+  // SVD = rounds per sweep (2 C ceil(pairs / C) - 1 players: dummy columns pad the
+  // tournament) x time per round, which grows with the warps per CTA (measured at
+  // p = 132: 1.01 / 1.11 / 1.22 us per round at 6 / 9 / 11 warps => ~0.75 + 0.042 warps):
+  // p = 132 runs on 11 CTAs x 6 warps (131 rounds, 1.05 ms) instead of 8 x 9 (143 rounds,
+  // 1.27 ms).  Batched problems (throughput): the smallest power of two that fits, so as
+  // many problems as possible are co-resident.
+  int order[JC_MAXC + 1], no = 0;
+  static int forced = -1;
+  if (forced < 0) { const char *e = std::getenv("TT_JC_CLUSTER"); forced = e ? std::atoi(e) : 0; }
+  if (count > 1) {
+    for (int C = 2; C <= JC_MAXC; C *= 2) order[no++] = C;
+  } else {
+    for (int C = 2; C <= JC_MAXC; ++C) order[no++] = C;
+    auto key = [&](int C) {
+      const int nw = (pairs + C - 1) / C;
+      return (long long)(2 * C * nw) * (18 + (nw < 2 ? 2 : nw));
+    };
+    for (int i = 1; i < no; ++i)
+      for (int j = i; j > 0 && key(order[j]) < key(order[j - 1]); --j) {
+        const int t = order[j]; order[j] = order[j - 1]; order[j - 1] = t;
+      }
+  }
+  if (forced >= 2 && forced <= JC_MAXC) { order[0] = forced; no = 1; }
+  for (int oi = 0; oi < no; ++oi) {
+    const int C = order[oi];
     int warps = (pairs + C - 1) / C;
     warps = warps < 2 ? 2 : warps;
     // mailboxes [2 parities][warps][2 slots][m + p], their ids, sigma and the sort positions
